@@ -1,0 +1,153 @@
+"""ctypes wrapper of the C++ oracle (oracle/nacs_oracle.cpp) — TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / reference arm
+may import this module.  It never imports the product package and the product
+never imports it.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+SRC = os.path.join(HERE, "nacs_oracle.cpp")
+LIB = os.path.join(HERE, "liboracle.so")
+
+METHOD = {"ahp": 0, "topsis": 1}
+# Table 4: (CPU, RAM, Fragmentation, Bandwidth)
+SCHEMAS = {"flat": (0.25, 0.25, 0.25, 0.25),
+           "clustering": (0.17, 0.17, 0.5, 0.16),
+           "network": (0.17, 0.17, 0.16, 0.5)}
+
+
+def build(force: bool = False) -> str:
+    if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < os.path.getmtime(SRC):
+        subprocess.check_call(["g++", "-O2", "-std=c++17", "-fopenmp", "-shared", "-fPIC",
+                               "-o", LIB, SRC])
+    return LIB
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        _lib = C.CDLL(build())
+        P = C.c_void_p
+        _lib.orc_rank.restype = C.c_int
+        _lib.orc_rank.argtypes = [C.c_int] * 4 + [P] * 4 + [C.c_int, P, C.c_int, C.c_int, C.c_int,
+                                                          C.c_int, C.c_int, C.c_int, P, P, C.c_int, P,
+                                                          P, P, P, P]
+        _lib.orc_ahp_priority.argtypes = [C.c_int, P, C.c_int, P]
+        _lib.orc_ahp_l1.argtypes = [P, C.c_int, C.c_int, P]
+        _lib.orc_widest_path.restype = C.c_int
+        _lib.orc_widest_path.argtypes = [C.c_int, P, C.c_int, C.c_int, P, P, P]
+        _lib.orc_schedule.restype = C.c_int
+        _lib.orc_schedule.argtypes = [C.c_int] * 4 + [P] * 4 + [C.c_int, P, C.c_int, C.c_int, C.c_int,
+                                                          C.c_int, C.c_int] + [P] * 19 + [C.c_int]
+    return _lib
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def _i32(a):
+    return np.ascontiguousarray(a, dtype=np.int32)
+
+
+def _weights(w):
+    if isinstance(w, str):
+        w = SCHEMAS[w]
+    return np.ascontiguousarray(w, dtype=np.float64)
+
+
+def rank(snap: dict, method: str, weights, dem_cpu: int, dem_ram: int, flows=(), excluded=(),
+         ahp_rule: int = 0, l1_mode: int = 0, path_filter: int = 1):
+    """One pod step's ranking.  flows: iterable of (server v, demand D_v)."""
+    k = snap["k"]
+    n = k ** 3 // 4
+    cpu, ram = _i32(snap["cpu_res"]), _i32(snap["ram_res"])
+    act = np.ascontiguousarray(snap["active"], dtype=np.uint8)
+    link = _i32(snap["link_res"])
+    fv = _i32([f[0] for f in flows]) if len(flows) else np.zeros(1, np.int32)
+    fd = _i32([f[1] for f in flows]) if len(flows) else np.zeros(1, np.int32)
+    ex = _i32(list(excluded)) if len(excluded) else np.zeros(1, np.int32)
+    w = _weights(weights)
+    mask = np.zeros(n, np.uint8)
+    score = np.zeros(n, np.float64)
+    tie = np.zeros(n, np.uint8)
+    best = np.zeros(1, np.int32)
+    nf = lib().orc_rank(k, snap["cpu_cap"], snap["ram_cap"], snap["link_cap"], _p(cpu), _p(ram), _p(act),
+                        _p(link), METHOD[method], _p(w), ahp_rule, l1_mode, path_filter, int(dem_cpu),
+                        int(dem_ram), len(flows), _p(fv), _p(fd), len(excluded), _p(ex), _p(mask),
+                        _p(score), _p(best), _p(tie))
+    return dict(mask=mask, score=score, best=int(best[0]), tie=tie, n_feasible=nf)
+
+
+def ahp_priority(x, rule: int = 0) -> np.ndarray:
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    out = np.zeros(x.size, np.float64)
+    lib().orc_ahp_priority(x.size, _p(x), rule, _p(out))
+    return out
+
+
+def ahp_l1(weights, ahp_rule: int = 0, l1_mode: int = 0) -> np.ndarray:
+    w = _weights(weights)
+    out = np.zeros(4, np.float64)
+    lib().orc_ahp_l1(_p(w), ahp_rule, l1_mode, _p(out))
+    return out
+
+
+def widest_path(k: int, link_res, u: int, v: int):
+    link = _i32(link_res)
+    fab = np.zeros(1, np.float64)
+    links = np.zeros(4, np.int32)
+    nl = np.zeros(1, np.int32)
+    pid = lib().orc_widest_path(k, _p(link), u, v, _p(fab), _p(links), _p(nl))
+    return pid, float(fab[0]), links[: nl[0]].tolist()
+
+
+def schedule(snap: dict, reqs: dict, method: str, weights, sequential: bool, hint=None,
+             ahp_rule: int = 0, l1_mode: int = 0, path_filter: int = 1, nthreads: int | None = None):
+    """Schedule a CSR batch.  Returns (placements, counters, final_state).
+
+    final_state is the state after the batch (sequential) or the unchanged snapshot (batch).
+    counters: pod_steps, retries, excused_ties, hint_mismatch, servers_ranked.
+    """
+    k = snap["k"]
+    cpu, ram = _i32(snap["cpu_res"]).copy(), _i32(snap["ram_res"]).copy()
+    act = np.ascontiguousarray(snap["active"], dtype=np.uint8).copy()
+    link = _i32(snap["link_res"]).copy()
+    R = int(reqs["n_requests"])
+    Cn = int(reqs["container_off"][-1])
+    Vn = int(reqs["vlink_off"][-1])
+    arr = {key: _i32(reqs[key]) for key in ("container_off", "cpu_min", "cpu_max", "ram_min", "ram_max",
+                                            "pod_of", "vlink_off", "vl_src", "vl_dst", "bw_min", "bw_max")}
+    out = dict(status=np.zeros(R, np.int32), server_of_container=np.zeros(max(Cn, 1), np.int32),
+               cpu_alloc=np.zeros(max(Cn, 1), np.int32), ram_alloc=np.zeros(max(Cn, 1), np.int32),
+               bw_alloc=np.zeros(max(Vn, 1), np.int32), path_of_vlink=np.zeros(max(Vn, 1), np.int32))
+    cnt = np.zeros(5, np.int64)
+    hint_a = None if hint is None else _i32(hint)
+    if nthreads is None:
+        nthreads = len(os.sched_getaffinity(0))
+    w = _weights(weights)
+    lib().orc_schedule(k, snap["cpu_cap"], snap["ram_cap"], snap["link_cap"], _p(cpu), _p(ram), _p(act),
+                       _p(link), METHOD[method], _p(w), ahp_rule, l1_mode, path_filter, int(sequential), R,
+                       _p(arr["container_off"]), _p(arr["cpu_min"]), _p(arr["cpu_max"]), _p(arr["ram_min"]),
+                       _p(arr["ram_max"]), _p(arr["pod_of"]), _p(arr["vlink_off"]), _p(arr["vl_src"]),
+                       _p(arr["vl_dst"]), _p(arr["bw_min"]), _p(arr["bw_max"]), _p(hint_a), _p(out["status"]),
+                       _p(out["server_of_container"]), _p(out["cpu_alloc"]), _p(out["ram_alloc"]),
+                       _p(out["bw_alloc"]), _p(out["path_of_vlink"]), _p(cnt), int(nthreads))
+    for key in ("server_of_container", "cpu_alloc", "ram_alloc"):
+        out[key] = out[key][:Cn]
+    for key in ("bw_alloc", "path_of_vlink"):
+        out[key] = out[key][:Vn]
+    counters = dict(zip(("pod_steps", "retries", "excused_ties", "hint_mismatch", "servers_ranked"),
+                        cnt.tolist()))
+    state = dict(snap, cpu_res=cpu, ram_res=ram, active=act, link_res=link)
+    return out, counters, state
