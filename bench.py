@@ -1,0 +1,326 @@
+#!/usr/bin/env python
+"""Benchmark of the hot path: pods placed/s and servers ranked/s (BASELINE.json metric).
+
+One step = one pass of the whole hot path (snapshot, request
+decode, flows, filter, statistics, scoring, argmax, commit, top-up) over one batch:
+nacs_schedule_batch on config C4 — fat-tree k=32 (8192 servers), 100k requests per GPU
+(weak scaling: every rank schedules its own 100k-request shard), TOPSIS with the Flat
+schema.  A second line of numbers ("ahp") runs AHP Flat on C3 (k=16, 10k requests), the
+largest config whose O(n_f^2) AHP pass fits a bench step.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+Multi-GPU: launched by torchrun; one process per GPU, no data-path collective (requests
+are independent, R21); the timed region is bracketed by barriers and the max over ranks
+is taken.  --impl reference times the CPU oracle (the deliberately slow double-precision
+program written from the paper) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+from inputs import gen  # noqa: E402
+
+# Algorithmic operation counts.
+TOPSIS_OPS_ALL = 3       # per server ranked: the CPU/RAM/access-bandwidth compares of the filter
+TOPSIS_OPS_FEAS = 45     # per feasible server: stats (14) + closeness (30) + argmax (1)
+AHP_RCP_PER_PAIR = 1     # per unordered pair per non-constant criterion per pass: one reciprocal
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-ahp", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    FIELDS = "clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown," \
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, device: int):
+        self.device = device
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def workload(rank: int, method: str):
+    """Snapshot and this rank's request shard (weak scaling: 100k C4 requests per rank)."""
+    if method == "topsis":
+        snap = gen.snapshot(32, gen.CONFIG_SEEDS["C4"])
+        reqs = gen.requests(gen.CONFIG_REQUESTS["C4"], gen.CONFIG_SEEDS["C4"] + 1000 + 7919 * rank)
+        name = "C4: fat-tree k=32 (8192 servers), 100k requests/GPU of 4-20 containers, TOPSIS Flat, batch"
+    else:
+        snap = gen.snapshot(16, gen.CONFIG_SEEDS["C3"])
+        reqs = gen.requests(gen.CONFIG_REQUESTS["C3"], gen.CONFIG_SEEDS["C3"] + 1000 + 7919 * rank)
+        name = "C3: fat-tree k=16 (1024 servers), 10k requests/GPU, AHP Flat, batch"
+    return snap, reqs, name
+
+
+def run_ours(args, rank, world, local):
+    import torch
+    from paper_1909_07673_b200 import nacs
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    stream = torch.cuda.current_stream(dev)
+    ctx = nacs.Context(local, stream)
+    pk, pk_kind = peaks()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        import torch.distributed as dist
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        import torch.distributed as dist
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+    def measure(method):
+        snap, reqs, name = workload(rank, method)
+        ctx.load_topology(snap)
+        d = {k: (torch.from_numpy(v).to(dev) if isinstance(v, np.ndarray) else v) for k, v in reqs.items()}
+        out = ctx._alloc_out(reqs, True)[0]
+        for _ in range(args.warmup):
+            ctx.schedule_batch(d, method, "flat", out=out, flags=nacs.NACS_ASYNC)
+        torch.cuda.synchronize(dev)
+        st0 = ctx.last_stats()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        sampler = ClockSampler(local)
+        barrier()
+        with sampler:
+            t0 = torch.cuda.Event(enable_timing=True)
+            t1 = torch.cuda.Event(enable_timing=True)
+            t0.record(stream)
+            for i in range(args.steps):
+                flush.zero_()
+                ev[i][0].record(stream)
+                ctx.schedule_batch(d, method, "flat", out=out, flags=nacs.NACS_ASYNC)
+                ev[i][1].record(stream)
+            t1.record(stream)
+            torch.cuda.synchronize(dev)
+        barrier()
+        total_ms = max_over_ranks(t0.elapsed_time(t1))
+        kern_ms = [a.elapsed_time(b) for a, b in ev]
+        kern_avg = max_over_ranks(sum(kern_ms) / len(kern_ms))
+        st = ctx.last_stats()  # stats of the last step (deterministic: identical every step)
+        pod_steps = sum_over_ranks(st["pod_steps"])
+        value = pod_steps * args.steps / (total_ms / 1e3)
+        n = snap["k"] ** 3 // 4
+        res = dict(name=name, value=value, ms_per_step=total_ms / args.steps, kernel_ms=kern_avg,
+                   pod_steps_per_step=pod_steps, servers_ranked_per_s=value * n, n=n, stats=st,
+                   clocks=sampler.summary(), snap=snap, reqs=reqs, out=out, d=d)
+        return res
+
+    topsis = measure("topsis")
+    ahp = None if args.no_ahp else measure("ahp")
+
+    # roofline of the dominant kernel (k_batch<TOPSIS>): issue-bound ALU
+    clocks = topsis["clocks"]
+    mhz = float(pk.get("sm_max_mhz", 1965.0))
+    alu_peak = 148 * 128 * mhz * 1e6 / 1e12  # Top/s: 4 schedulers x 32 lanes per SM per clock
+    st = topsis["stats"]
+    ops = TOPSIS_OPS_ALL * st["servers_ranked"] + TOPSIS_OPS_FEAS * st["feasible"]
+    achieved = ops / (topsis["kernel_ms"] / 1e3) / 1e12
+    roofline = {"bound": "alu", "achieved": achieved, "peak": alu_peak, "unit": "Top/s",
+                "frac": achieved / alu_peak, "traffic": None, "kernel": "k_batch<TOPSIS>",
+                "peak_source": f"148 SMs x 128 lanes x {mhz:.0f} MHz (sm_max_mhz, {pk_kind})"}
+
+    ahp_obj = None
+    if ahp is not None:
+        sa = ahp["stats"]
+        rcp = 2 * sa["ahp_pairs"]  # two passes; pairs = sum over non-constant criteria of nf(nf-1)/2
+        mufu_peak = 16 * 148 * mhz * 1e6 / 1e12
+        ach = rcp / (ahp["kernel_ms"] / 1e3) / 1e12
+        ahp_obj = {"workload": ahp["name"], "value": ahp["value"], "unit": "pods/s",
+                   "servers_ranked_per_s": ahp["servers_ranked_per_s"], "ms_per_step": ahp["ms_per_step"],
+                   "pod_steps_per_step": ahp["pod_steps_per_step"], "fp64_decisions": sa["fp64_decisions"],
+                   "roofline": {"bound": "mufu", "achieved": ach, "peak": mufu_peak, "unit": "T rcp/s",
+                                "frac": ach / mufu_peak, "kernel": "k_batch<AHP>",
+                                "peak_source": f"16 MUFU/clk/SM x 148 x {mhz:.0f} MHz"}}
+
+    # e2e: the public API with host buffers (staging copies inside the timed region)
+    e2e = None
+    if not args.no_e2e:
+        snap, reqs = topsis["snap"], topsis["reqs"]
+        ctx.load_topology(snap)
+        ctx.schedule_batch(reqs, "topsis", "flat")
+        barrier()
+        t = time.perf_counter()
+        for _ in range(args.steps):
+            ctx.schedule_batch(reqs, "topsis", "flat")
+        torch.cuda.synchronize(dev)
+        el = max_over_ranks(time.perf_counter() - t)
+        R = reqs["n_requests"]
+        Cn, Vn = int(reqs["container_off"][-1]), int(reqs["vlink_off"][-1])
+        e2e = {"value": topsis["pod_steps_per_step"] * args.steps / el, "unit": "pods/s",
+               "h2d_bytes_per_step": 4 * (2 * (R + 1) + 5 * Cn + 4 * Vn),
+               "d2h_bytes_per_step": 4 * (R + 3 * Cn + 2 * Vn)}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(topsis["snap"], topsis["reqs"], budget_s=15.0)
+
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank == 0:
+        line = {"metric": "pods placed/sec (and servers ranked/sec)", "value": topsis["value"], "unit": "pods/s",
+                "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": topsis["ms_per_step"], "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": {"workload": topsis["name"], "k": 32, "servers": topsis["n"],
+                           "requests_per_gpu": gen.CONFIG_REQUESTS["C4"], "method": "topsis", "schema": "flat",
+                           "parallelism": f"request-sharded x{world}", "l2": "flushed between steps (256 MB write)"},
+                "servers_ranked_per_s": topsis["servers_ranked_per_s"],
+                "pod_steps_per_step": topsis["pod_steps_per_step"],
+                "kernel_ms": topsis["kernel_ms"], "fp64_decisions": topsis["stats"]["fp64_decisions"],
+                "retries": topsis["stats"]["retries"],
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": args.steps,
+                "clocks": clocks, "ahp": ahp_obj,
+                "paper_context": "T5 (P:416-426): TOPSIS 3.48-3.84 s, AHP 6.90-9.45 s per 6000-request k=20 campaign "
+                                 "on an unnamed CUDA 10.1 GPU (~10-14 M / 4-7 M servers ranked/s derived)"}
+        print(json.dumps(line))
+
+
+def cpu_baseline(snap, reqs, budget_s=15.0, method="topsis"):
+    """The oracle as it stands, on the host cores, on a bounded sample of the workload."""
+    from oracle import oracle as O
+    cores = len(os.sched_getaffinity(0))
+    n_req = 64
+    while True:
+        sub = gen.subset(reqs, np.arange(n_req))
+        t = time.perf_counter()
+        _, cnt, _ = O.schedule(snap, sub, method, "flat", sequential=False, nthreads=cores)
+        el = time.perf_counter() - t
+        if el > budget_s / 4 or n_req >= reqs["n_requests"]:
+            break
+        n_req = min(reqs["n_requests"], int(n_req * max(2.0, budget_s / max(el, 1e-3) / 2)))
+    return {"value": cnt["pod_steps"] / el, "unit": "pods/s", "cores": cores, "kind": "oracle",
+            "sample": f"first {n_req} requests of the workload ({cnt['pod_steps']} pod steps), "
+                      f"{method} flat, C++ double oracle, OpenMP over requests, {el:.1f} s"}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    snap, reqs, name = workload(0, "topsis")
+    from oracle import oracle as O
+    O.build()
+    cores = len(os.sched_getaffinity(0))
+    sample = gen.subset(reqs, np.arange(256))
+    for _ in range(args.warmup):
+        O.schedule(snap, gen.subset(reqs, np.arange(16)), "topsis", "flat", sequential=False, nthreads=cores)
+    t = time.perf_counter()
+    pods = 0
+    for _ in range(args.steps):
+        _, cnt, _ = O.schedule(snap, sample, "topsis", "flat", sequential=False, nthreads=cores)
+        pods += cnt["pod_steps"]
+    el = time.perf_counter() - t
+    value = pods / el
+    desc = f"first 256 requests of the workload per step ({pods // max(args.steps, 1)} pod steps), C++ double oracle"
+    print(json.dumps({"impl": "reference", "metric": "pods placed/sec (and servers ranked/sec)", "value": value,
+                      "unit": "pods/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                      "ms_per_step": el / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+                      "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                      "config": {"workload": name, "k": 32, "method": "topsis", "schema": "flat"},
+                      "cpu_baseline": {"value": value, "unit": "pods/s", "cores": cores, "kind": "oracle",
+                                       "sample": desc},
+                      "e2e": {"value": value, "unit": "pods/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    run_ours(args, rank, world, local)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,182 @@
+/* nacs.h — C ABI of libnacs: the per-pod server ranking and placement hot path of
+ * arXiv 1909.07673, "Network-Aware Container Scheduling in Multi-Tenant Data Center"
+ * (§V), running as hand-written sm_100a CUDA kernels.
+ *
+ * Citations: "P:n" = /root/reference/PAPER.md line n (paper section / equation named
+ * beside it); readings R1-R24 are listed in DESIGN.md §3.
+ *
+ * Units (reading R5): every quantity is an int32 in fixed units — CPU in millicores,
+ * RAM in MiB, bandwidth in Mbps.  Every capacity must be <= NACS_MAX_CAP so that all
+ * residuals and differences are exact in FP32 on the device.
+ *
+ * Ownership: the caller owns every input and output array.  The library copies inputs
+ * during the call and never retains caller pointers.  The context owns its device
+ * buffers and releases them in nacs_destroy().
+ *
+ * Pointers: host pointers unless nacs_options.flags has NACS_DEVICE_PTRS, in which case
+ * every array passed to that call is a device pointer on the context's device (for
+ * example a torch tensor's data_ptr()).  With NACS_ASYNC the call is stream-ordered on
+ * the context stream and returns without synchronising; the caller synchronises the
+ * stream before reading outputs.  Without NACS_ASYNC every call is synchronous.
+ *
+ * Errors: calls return nacs_status.  Invalid parameters are errors (NACS_EINVAL);
+ * nacs_last_error() lists every violation found.  On any error the context state is
+ * unchanged.  A request that cannot be placed is not an error: its status is 0 and all
+ * its mappings are -1.  A context is single-writer and not thread-safe.
+ */
+#ifndef NACS_H
+#define NACS_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct nacs_ctx nacs_ctx;
+
+typedef enum {
+  NACS_OK = 0,
+  NACS_EINVAL = 1,   /* invalid argument (see nacs_last_error) */
+  NACS_ENOMEM = 2,   /* device or pinned host allocation failed */
+  NACS_ECUDA = 3,    /* a CUDA runtime call failed */
+  NACS_ENCCL = 4,    /* reserved for the server-sharded mode */
+  NACS_ENOTOPO = 5,  /* no topology loaded */
+  NACS_ETOOBIG = 6   /* a size limit below is exceeded */
+} nacs_status;
+
+typedef enum { NACS_AHP = 0, NACS_TOPSIS = 1 } nacs_method;
+
+/* nacs_options.flags */
+#define NACS_DEVICE_PTRS 1u  /* arrays are device pointers */
+#define NACS_ASYNC 2u        /* stream-ordered, no synchronisation (implies no host-side validation) */
+#define NACS_EXACT_FP64 4u   /* decide every argmax in FP64 (the FP32 pass still runs) */
+
+/* Limits. */
+#define NACS_MAX_CAP 8388607     /* 2^23 - 1: every value exact in FP32 */
+#define NACS_MAX_K 64            /* fat-tree arity: h = k/2 <= 32 aggregation switches per pod */
+#define NACS_MAX_CONTAINERS 128  /* containers (hence pods) per request */
+#define NACS_MAX_VLINKS 512      /* virtual links per request */
+
+/* G^s(N^s, E^s) as a k-ary fat-tree (§II-A; §IV-B1; Table 1).
+ * n = k^3/4 servers, h = k/2, E = k^2/2 edge switches, L = 3k^3/4 physical links.
+ * Server u hangs off edge switch u / h; edge switch e lies in pod e / h.
+ * Canonical link order: access[n] (server u <-> its edge switch) |
+ *   edge-agg[E][h] (edge e <-> aggregation switch a of its pod) |
+ *   agg-core[k][h][h] (aggregation switch a of pod p <-> core switch (a, b)).
+ * Links are undirected with one shared residual (§V-D).
+ * All arrays are host pointers. */
+typedef struct {
+  int32_t k;                             /* even, 2 <= k <= NACS_MAX_K */
+  int32_t cpu_cap, ram_cap, link_cap;    /* homogeneous capacities, 1..NACS_MAX_CAP */
+  const int32_t *cpu_res, *ram_res;      /* [n] residual c^s_u[r] in [0, cap]; NULL = fresh */
+  const uint8_t *active;                 /* [n] f_u in {0,1}; NULL = derived: res < cap (R22) */
+  const int32_t *link_res;               /* [L] residual bw in [0, link_cap]; NULL = fresh */
+} nacs_topology;
+
+/* One pod step for nacs_rank_*: the pod's summed c^min and its flows to
+ * already-placed peer pods (R17): flow f goes to server flow_server[f] with aggregate
+ * bw^min demand flow_bw[f] > 0 (servers distinct).  excluded[] servers are never
+ * feasible (R18 retries). */
+typedef struct {
+  int32_t cpu_demand, ram_demand;        /* > 0 */
+  int32_t n_flows;                       /* 0..NACS_MAX_CONTAINERS */
+  const int32_t *flow_server, *flow_bw;  /* [n_flows] */
+  int32_t n_excluded;                    /* 0..n */
+  const int32_t *excluded;               /* [n_excluded] */
+} nacs_pod_query;
+
+/* A batch of requests Req(N^c, E^c) in CSR form (§II-A; Table 1).
+ * Request r owns containers container_off[r] .. container_off[r+1]-1 and virtual links
+ * vlink_off[r] .. vlink_off[r+1]-1; vl_src / vl_dst are request-local container ids.
+ * pod_of[i] is the request-local pod id of container i; the ids must be exactly
+ * 0..P-1 and pods are placed in ascending id (R15). */
+typedef struct {
+  int32_t n_requests;
+  const int32_t *container_off;                          /* [n_requests+1], starts at 0 */
+  const int32_t *cpu_min, *cpu_max, *ram_min, *ram_max;  /* per container: 0 < min <= max */
+  const int32_t *pod_of;                                 /* per container */
+  const int32_t *vlink_off;                              /* [n_requests+1], starts at 0 */
+  const int32_t *vl_src, *vl_dst, *bw_min, *bw_max;      /* per vlink: src != dst, 0 < min <= max */
+} nacs_requests;
+
+/* Outputs M_c, M_ec, c^a, bw^a (Table 2), caller-allocated, sized like
+ * the request arrays.  status: 1 accepted, 0 rejected (no feasible server for a pod,
+ * R20), -1 invalid request (only reported this way with NACS_DEVICE_PTRS; host-pointer
+ * calls return NACS_EINVAL instead).  A non-accepted request has all mappings -1 and all
+ * allocations 0.  path_of_vlink: -1 intra-server; 0 same edge switch; 1+a via
+ * aggregation switch a of the shared pod; 1+h+a*h+b via core switch (a,b). */
+typedef struct {
+  int32_t *status;               /* [n_requests] */
+  int32_t *server_of_container;  /* [sum containers] */
+  int32_t *cpu_alloc, *ram_alloc;/* [sum containers] c^a within [c^min, c^max] (R19) */
+  int32_t *bw_alloc;             /* [sum vlinks] bw^a within [bw^min, bw^max] (R19) */
+  int32_t *path_of_vlink;        /* [sum vlinks] */
+} nacs_placements;
+
+/* Method options.  weights: W over (CPU, RAM, Fragmentation, Bandwidth) (Table 4
+ * P:319-330, R1), finite, >= 0, |sum - 1| <= 1e-6 (R24). */
+typedef struct {
+  nacs_method method;
+  double weights[4];
+  int32_t ahp_rule;     /* 0 literal cell d / 1/(-d) / 1 (R8, default); 1 shifted 1+d / 1/(1-d) / 1 */
+  int32_t l1_mode;      /* 0 L1 = AHP pairwise priority of W (R10, default); 1 L1 = W */
+  int32_t path_filter;  /* 1 filter on path bandwidth (R6, default); 0 CPU/RAM-only filter */
+  uint32_t flags;       /* NACS_DEVICE_PTRS | NACS_ASYNC | NACS_EXACT_FP64 */
+} nacs_options;
+
+/* Counters of the last rank/schedule call (reading them synchronises the context stream). */
+typedef struct {
+  int64_t pod_steps;       /* rankings run (every pod step and every R18 retry) */
+  int64_t servers_ranked;  /* pod_steps x n */
+  int64_t retries;         /* R18 commit failures */
+  int64_t fp64_decisions;  /* argmaxes decided by the FP64 near-tie rescore */
+  int64_t invalid;         /* requests rejected as invalid on the device */
+  int64_t feasible;        /* sum over pod steps of |F| (feasible servers) */
+  int64_t ahp_pairs;       /* AHP: sum over pod steps and non-constant criteria of |F|(|F|-1)/2 */
+} nacs_stats;
+
+/* Create a context on CUDA device `device`.  cuda_stream: a cudaStream_t to order all
+ * work on (NULL = the library creates its own non-blocking stream). */
+nacs_status nacs_create(nacs_ctx **out, int device, void *cuda_stream);
+void nacs_destroy(nacs_ctx *ctx);
+
+/* Load (or replace) the DC state.  Validates k, capacities and residual ranges. */
+nacs_status nacs_load_topology(nacs_ctx *ctx, const nacs_topology *topo);
+
+/* Copy the current state back to host arrays (any may be NULL): cpu_res[n], ram_res[n],
+ * active[n], link_res[L]. */
+nacs_status nacs_read_topology(nacs_ctx *ctx, int32_t *cpu_res, int32_t *ram_res, uint8_t *active,
+                               int32_t *link_res);
+
+/* Rank every server for one pod step on the current state (no state change):
+ * feasibility filter (Eq. 4-7, R6) then AHP (Eq. 9-10, R7-R11) or
+ * TOPSIS (R12-R13) scores over the feasible set, then the argmax with the
+ * lowest server index on ties (R14).  mask[n] (uint8, may be NULL): 1 = feasible.
+ * scores[n] (float, may be NULL): the FP32 score of feasible servers, 0 elsewhere.
+ * best: the chosen server, -1 if none is feasible. */
+nacs_status nacs_rank_ahp(nacs_ctx *ctx, const nacs_options *opt, const nacs_pod_query *q, uint8_t *mask,
+                          float *scores, int32_t *best);
+nacs_status nacs_rank_topsis(nacs_ctx *ctx, const nacs_options *opt, const nacs_pod_query *q,
+                             uint8_t *mask, float *scores, int32_t *best);
+
+/* Schedule requests one after another against the live state (the paper's online
+ * semantics): for each pod in ascending id, rank, select, and commit
+ * (Eq. 4-5, R16-R18); at request end top up allocations (R19).  An accepted request
+ * stays committed; a rejected one leaves the state unchanged (R20). */
+nacs_status nacs_schedule_request(nacs_ctx *ctx, const nacs_options *opt, const nacs_requests *reqs,
+                                  nacs_placements *out);
+
+/* Schedule every request of the batch against the same current state, each with its own
+ * private overlay (R21): requests do not see each other and the state is not modified. */
+nacs_status nacs_schedule_batch(nacs_ctx *ctx, const nacs_options *opt, const nacs_requests *batch,
+                                nacs_placements *out);
+
+nacs_status nacs_last_stats(nacs_ctx *ctx, nacs_stats *out);
+const char *nacs_last_error(const nacs_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* NACS_H */

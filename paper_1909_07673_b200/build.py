@@ -1,0 +1,39 @@
+"""Build libnacs.so in-tree with nvcc for sm_100a (no JIT, no torch extension cache)."""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+CSRC = os.path.join(HERE, "csrc")
+LIB = os.path.join(HERE, "libnacs.so")
+SOURCES = [os.path.join(CSRC, f) for f in ("nacs_kernels.cu", "nacs_api.cu")]
+DEPS = SOURCES + [os.path.join(CSRC, "nacs_internal.h"), os.path.join(ROOT, "include", "nacs.h")]
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
+         "-Xcompiler", "-fPIC", "-shared", "-cudart", "static", "-Xptxas", "-v"]
+
+
+def stale() -> bool:
+    if not os.path.exists(LIB):
+        return True
+    t = os.path.getmtime(LIB)
+    return any(os.path.getmtime(d) > t for d in DEPS)
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    if force or stale():
+        cmd = [NVCC, *FLAGS, "-I", os.path.join(ROOT, "include"), "-o", LIB, *SOURCES]
+        p = subprocess.run(cmd, capture_output=True, text=True)
+        if p.returncode != 0:
+            sys.stderr.write(p.stdout + p.stderr)
+            raise RuntimeError("nvcc failed building libnacs.so")
+        if verbose:
+            sys.stderr.write(p.stderr)
+    return LIB
+
+
+if __name__ == "__main__":
+    build(force=True, verbose=True)

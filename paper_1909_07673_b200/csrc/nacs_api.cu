@@ -1,0 +1,634 @@
+// nacs_api.cu — the C ABI of libnacs (include/nacs.h): context, validation, staging of
+// inputs and outputs, kernel launches.  Every step of the method runs in the kernels of
+// nacs_kernels.cu; this file only checks arguments and moves bytes.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/nacs.h"
+#include "nacs_internal.h"
+
+using nacs::Geo;
+using nacs::Opt;
+
+namespace {
+
+template <class T>
+struct DevArr {
+  T* p = nullptr;
+  size_t cap = 0;
+  cudaError_t reserve(size_t n) {
+    if (n <= cap) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    size_t m = n + n / 4 + 64;
+    cudaError_t e = cudaMalloc(&p, m * sizeof(T));
+    if (e == cudaSuccess) cap = m;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+struct PinArr {
+  unsigned char* p = nullptr;
+  size_t cap = 0;
+  cudaError_t reserve(size_t n) {
+    if (n <= cap) return cudaSuccess;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    cap = 0;
+    size_t m = n + n / 4 + 4096;
+    cudaError_t e = cudaMallocHost(&p, m);
+    if (e == cudaSuccess) cap = m;
+    return e;
+  }
+  void release() {
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+}  // namespace
+
+struct nacs_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  bool has_topo = false;
+  Geo g{};
+  int num_sms = 0;
+  DevArr<int> state;
+  DevArr<int> req_in;        // packed CSR inputs
+  DevArr<int> req_out;       // packed outputs
+  DevArr<int2> ulog;
+  DevArr<double> w64;
+  DevArr<float> ahp_ws;
+  DevArr<int> misc;          // next-request counter, query arrays, best
+  DevArr<unsigned char> mask;
+  DevArr<float> scores;
+  DevArr<unsigned long long> stats;
+  PinArr pin_in, pin_out;
+  std::string err;
+  nacs_stats last{};
+  bool stats_pending = false;
+};
+
+namespace {
+
+nacs_status fail(nacs_ctx* c, nacs_status s, const std::string& msg) {
+  if (c) c->err = msg;
+  return s;
+}
+
+nacs_status cuda_fail(nacs_ctx* c, cudaError_t e, const char* where) {
+  std::string m = std::string(where) + ": " + cudaGetErrorString(e);
+  cudaGetLastError();
+  return fail(c, e == cudaErrorMemoryAllocation ? NACS_ENOMEM : NACS_ECUDA, m);
+}
+
+#define CK(call)                                              \
+  do {                                                        \
+    cudaError_t e_ = (call);                                  \
+    if (e_ != cudaSuccess) return cuda_fail(ctx, e_, #call);  \
+  } while (0)
+
+nacs_status check_options(nacs_ctx* ctx, const nacs_options* o, Opt* out) {
+  if (!o) return fail(ctx, NACS_EINVAL, "options: NULL");
+  std::string m;
+  if (o->method != NACS_AHP && o->method != NACS_TOPSIS) m += "options.method not AHP/TOPSIS; ";
+  double sum = 0;
+  for (int k = 0; k < 4; ++k) {
+    if (!std::isfinite(o->weights[k]) || o->weights[k] < 0) m += "options.weights[" + std::to_string(k) + "] not finite and >= 0; ";
+    sum += o->weights[k];
+  }
+  if (!(std::fabs(sum - 1.0) <= 1e-6)) m += "options.weights do not sum to 1 (|sum-1| > 1e-6); ";
+  if (o->ahp_rule != 0 && o->ahp_rule != 1) m += "options.ahp_rule not 0/1; ";
+  if (o->l1_mode != 0 && o->l1_mode != 1) m += "options.l1_mode not 0/1; ";
+  if (o->path_filter != 0 && o->path_filter != 1) m += "options.path_filter not 0/1; ";
+  if (o->flags & ~(NACS_DEVICE_PTRS | NACS_ASYNC | NACS_EXACT_FP64)) m += "options.flags has unknown bits; ";
+  if (!m.empty()) return fail(ctx, NACS_EINVAL, m);
+  out->method = (int)o->method;
+  for (int k = 0; k < 4; ++k) out->wd[k] = o->weights[k];
+  out->ahp_rule = o->ahp_rule;
+  out->l1_mode = o->l1_mode;
+  out->path_filter = o->path_filter;
+  out->exact64 = (o->flags & NACS_EXACT_FP64) ? 1 : 0;
+  return NACS_OK;
+}
+
+// Host-side validation of a host-pointer CSR batch (R24).  Lists every violation.
+nacs_status check_requests_host(nacs_ctx* ctx, const nacs_requests* q, int* C_out, int* V_out) {
+  if (!q) return fail(ctx, NACS_EINVAL, "requests: NULL");
+  if (q->n_requests < 0) return fail(ctx, NACS_EINVAL, "requests.n_requests < 0");
+  int R = q->n_requests;
+  if (R == 0) { *C_out = *V_out = 0; return NACS_OK; }
+  if (!q->container_off || !q->vlink_off || !q->cpu_min || !q->cpu_max || !q->ram_min || !q->ram_max ||
+      !q->pod_of)
+    return fail(ctx, NACS_EINVAL, "requests: NULL array");
+  if (q->container_off[0] != 0 || q->vlink_off[0] != 0)
+    return fail(ctx, NACS_EINVAL, "requests: offsets must start at 0");
+  std::string m;
+  int nbad = 0;
+  bool big = false;
+  for (int r = 0; r < R; ++r) {
+    int c0 = q->container_off[r], c1 = q->container_off[r + 1];
+    int v0 = q->vlink_off[r], v1 = q->vlink_off[r + 1];
+    if (c1 < c0 || v1 < v0) {
+      m += "request " + std::to_string(r) + ": decreasing offsets; ";
+      ++nbad;
+      break;
+    }
+    if (v1 > v0 && (!q->vl_src || !q->vl_dst || !q->bw_min || !q->bw_max))
+      return fail(ctx, NACS_EINVAL, "requests: NULL vlink array");
+    int bad = nacs::validate_request(c1 - c0, v1 - v0, q->cpu_min + c0, q->cpu_max + c0, q->ram_min + c0,
+                                     q->ram_max + c0, q->pod_of + c0, q->vl_src + v0, q->vl_dst + v0,
+                                     q->bw_min + v0, q->bw_max + v0);
+    if (bad) {
+      ++nbad;
+      if (bad == 1) big = true;
+      if (nbad <= 32) {
+        m += "request " + std::to_string(r) + ":";
+        if (bad & 1) m += " size (containers 1.." + std::to_string(nacs::MAXC) + ", vlinks <= " +
+                          std::to_string(nacs::MAXV) + ")";
+        if (bad & 2) m += " non-positive c^min";
+        if (bad & 4) m += " c^min > c^max";
+        if (bad & 8) m += " pod ids not 0..P-1";
+        if (bad & 16) m += " vlink endpoint out of range or self-loop";
+        if (bad & 32) m += " bw^min <= 0 or bw^min > bw^max";
+        m += "; ";
+      }
+    }
+  }
+  if (nbad) {
+    if (nbad > 32) m += "... " + std::to_string(nbad) + " invalid requests in total";
+    return fail(ctx, big ? NACS_ETOOBIG : NACS_EINVAL, m);
+  }
+  *C_out = q->container_off[R];
+  *V_out = q->vlink_off[R];
+  return NACS_OK;
+}
+
+nacs_status check_placements(nacs_ctx* ctx, const nacs_placements* o) {
+  if (!o || !o->status || !o->server_of_container || !o->cpu_alloc || !o->ram_alloc || !o->bw_alloc ||
+      !o->path_of_vlink)
+    return fail(ctx, NACS_EINVAL, "placements: NULL array");
+  return NACS_OK;
+}
+
+// Stage a host CSR batch into device memory with one copy; returns device views.
+nacs_status stage_requests(nacs_ctx* ctx, const nacs_requests* q, int C, int V, nacs::ReqsDev* R) {
+  int Rn = q->n_requests;
+  size_t words = 2 * (size_t)(Rn + 1) + 5 * (size_t)C + 4 * (size_t)V;
+  CK(ctx->pin_in.reserve(words * 4));
+  CK(ctx->req_in.reserve(words));
+  int* h = reinterpret_cast<int*>(ctx->pin_in.p);
+  size_t o = 0;
+  auto put = [&](const int32_t* src, size_t n) {
+    size_t at = o;
+    if (n) std::memcpy(h + o, src, n * 4);
+    o += n;
+    return at;
+  };
+  size_t a_coff = put(q->container_off, Rn + 1), a_voff = put(q->vlink_off, Rn + 1);
+  size_t a_cmin = put(q->cpu_min, C), a_cmax = put(q->cpu_max, C), a_rmin = put(q->ram_min, C);
+  size_t a_rmax = put(q->ram_max, C), a_pod = put(q->pod_of, C);
+  size_t a_src = put(q->vl_src, V), a_dst = put(q->vl_dst, V), a_bmin = put(q->bw_min, V), a_bmax = put(q->bw_max, V);
+  CK(cudaMemcpyAsync(ctx->req_in.p, h, words * 4, cudaMemcpyHostToDevice, ctx->stream));
+  int* d = ctx->req_in.p;
+  R->n = Rn;
+  R->coff = d + a_coff;
+  R->voff = d + a_voff;
+  R->cpu_min = d + a_cmin;
+  R->cpu_max = d + a_cmax;
+  R->ram_min = d + a_rmin;
+  R->ram_max = d + a_rmax;
+  R->pod_of = d + a_pod;
+  R->src = d + a_src;
+  R->dst = d + a_dst;
+  R->bw_min = d + a_bmin;
+  R->bw_max = d + a_bmax;
+  return NACS_OK;
+}
+
+nacs::ReqsDev device_requests(const nacs_requests* q) {
+  nacs::ReqsDev R;
+  R.n = q->n_requests;
+  R.coff = q->container_off;
+  R.voff = q->vlink_off;
+  R.cpu_min = q->cpu_min;
+  R.cpu_max = q->cpu_max;
+  R.ram_min = q->ram_min;
+  R.ram_max = q->ram_max;
+  R.pod_of = q->pod_of;
+  R.src = q->vl_src;
+  R.dst = q->vl_dst;
+  R.bw_min = q->bw_min;
+  R.bw_max = q->bw_max;
+  return R;
+}
+
+nacs_status device_outputs(nacs_ctx* ctx, int R, int C, int V, nacs::OutDev* O) {
+  size_t words = (size_t)R + 3 * (size_t)C + 2 * (size_t)V;
+  CK(ctx->req_out.reserve(words + 1));
+  int* d = ctx->req_out.p;
+  O->status = d;
+  O->server = d + R;
+  O->cpu_a = d + R + C;
+  O->ram_a = d + R + 2 * (size_t)C;
+  O->bw_a = d + R + 3 * (size_t)C;
+  O->path = d + R + 3 * (size_t)C + V;
+  return NACS_OK;
+}
+
+nacs_status unstage_outputs(nacs_ctx* ctx, int R, int C, int V, nacs_placements* out) {
+  size_t words = (size_t)R + 3 * (size_t)C + 2 * (size_t)V;
+  CK(ctx->pin_out.reserve(words * 4 + 4));
+  CK(cudaMemcpyAsync(ctx->pin_out.p, ctx->req_out.p, words * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  const int* h = reinterpret_cast<const int*>(ctx->pin_out.p);
+  std::memcpy(out->status, h, (size_t)R * 4);
+  std::memcpy(out->server_of_container, h + R, (size_t)C * 4);
+  std::memcpy(out->cpu_alloc, h + R + C, (size_t)C * 4);
+  std::memcpy(out->ram_alloc, h + R + 2 * (size_t)C, (size_t)C * 4);
+  std::memcpy(out->bw_alloc, h + R + 3 * (size_t)C, (size_t)V * 4);
+  std::memcpy(out->path_of_vlink, h + R + 3 * (size_t)C + V, (size_t)V * 4);
+  return NACS_OK;
+}
+
+nacs_status begin_call(nacs_ctx* ctx) {
+  if (!ctx) return NACS_EINVAL;
+  ctx->err.clear();
+  CK(cudaSetDevice(ctx->device));
+  if (!ctx->has_topo) return fail(ctx, NACS_ENOTOPO, "no topology loaded");
+  CK(ctx->stats.reserve(nacs::ST_N));
+  CK(cudaMemsetAsync(ctx->stats.p, 0, sizeof(unsigned long long) * nacs::ST_N, ctx->stream));
+  ctx->stats_pending = true;
+  return NACS_OK;
+}
+
+nacs_status finish_stats(nacs_ctx* ctx) {
+  if (!ctx->stats_pending) return NACS_OK;
+  unsigned long long h[nacs::ST_N];
+  CK(cudaMemcpyAsync(h, ctx->stats.p, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  ctx->last.pod_steps = (int64_t)h[nacs::ST_POD_STEPS];
+  ctx->last.servers_ranked = (int64_t)h[nacs::ST_POD_STEPS] * ctx->g.n;
+  ctx->last.retries = (int64_t)h[nacs::ST_RETRIES];
+  ctx->last.fp64_decisions = (int64_t)h[nacs::ST_FP64];
+  ctx->last.invalid = (int64_t)h[nacs::ST_INVALID];
+  ctx->last.feasible = (int64_t)h[nacs::ST_FEAS];
+  ctx->last.ahp_pairs = (int64_t)h[nacs::ST_PAIRS];
+  ctx->stats_pending = false;
+  return NACS_OK;
+}
+
+nacs_status rank_impl(nacs_ctx* ctx, const nacs_options* opt, const nacs_pod_query* q, uint8_t* mask,
+                      float* scores, int32_t* best, int method) {
+  nacs_status st = begin_call(ctx);
+  if (st) return st;
+  Opt o;
+  if ((st = check_options(ctx, opt, &o))) return st;
+  if (o.method != method) return fail(ctx, NACS_EINVAL, "options.method does not match the rank call");
+  if (!q || !best) return fail(ctx, NACS_EINVAL, "query/best: NULL");
+  const bool dev = opt->flags & NACS_DEVICE_PTRS;
+  const Geo& g = ctx->g;
+  std::string m;
+  if (q->cpu_demand <= 0 || q->ram_demand <= 0) m += "query demands must be > 0; ";
+  if (q->n_flows < 0 || q->n_flows > nacs::MAXF) m += "query.n_flows out of 0..128; ";
+  if (q->n_excluded < 0 || q->n_excluded > g.n) m += "query.n_excluded out of range; ";
+  if (q->n_flows > 0 && (!q->flow_server || !q->flow_bw)) m += "query flow arrays NULL; ";
+  if (q->n_excluded > 0 && !q->excluded) m += "query.excluded NULL; ";
+  if (!m.empty()) return fail(ctx, NACS_EINVAL, m);
+  int nf = q->n_flows, nx = q->n_excluded;
+  CK(ctx->misc.reserve(2 * (size_t)nf + nx + 8));
+  const int *dfv, *dfD, *dex;
+  if (!dev) {
+    std::vector<int> fv(q->flow_server, q->flow_server + nf), fD(q->flow_bw, q->flow_bw + nf);
+    for (int f = 0; f < nf; ++f) {
+      if (fv[f] < 0 || fv[f] >= g.n) m += "flow " + std::to_string(f) + ": server out of range; ";
+      if (fD[f] <= 0) m += "flow " + std::to_string(f) + ": demand <= 0; ";
+    }
+    // flows sorted by server (commit order), servers distinct
+    std::vector<int> idx(nf);
+    for (int f = 0; f < nf; ++f) idx[f] = f;
+    std::sort(idx.begin(), idx.end(), [&](int a, int b) { return fv[a] < fv[b]; });
+    std::vector<int> h(2 * (size_t)nf + nx + 1);
+    for (int f = 0; f < nf; ++f) {
+      h[f] = fv[idx[f]];
+      h[nf + f] = fD[idx[f]];
+      if (f && h[f] == h[f - 1]) m += "flow servers not distinct; ";
+    }
+    for (int i = 0; i < nx; ++i) {
+      h[2 * nf + i] = q->excluded[i];
+      if (q->excluded[i] < 0 || q->excluded[i] >= g.n) m += "excluded server out of range; ";
+    }
+    if (!m.empty()) return fail(ctx, NACS_EINVAL, m);
+    CK(cudaMemcpyAsync(ctx->misc.p + 4, h.data(), h.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
+    dfv = ctx->misc.p + 4;
+    dfD = ctx->misc.p + 4 + nf;
+    dex = ctx->misc.p + 4 + 2 * nf;
+  } else {
+    dfv = q->flow_server;
+    dfD = q->flow_bw;
+    dex = q->excluded;
+  }
+  CK(ctx->mask.reserve(g.n));
+  CK(ctx->scores.reserve(g.n));
+  nacs::QueryDev qd;
+  qd.dc = q->cpu_demand;
+  qd.dr = q->ram_demand;
+  qd.nflow = nf;
+  qd.nex = nx;
+  qd.fv = dfv;
+  qd.fD = dfD;
+  qd.ex = dex;
+  qd.mask = (dev && mask) ? mask : ctx->mask.p;
+  qd.scores = (dev && scores) ? scores : ctx->scores.p;
+  qd.best = dev ? best : ctx->misc.p;
+  if (method == 0) {
+    CK(ctx->ahp_ws.reserve(10 * (size_t)g.n));
+    CK(ctx->w64.reserve(4 * (size_t)g.n));
+  }
+  CK(nacs::launch_rank(g, o, ctx->state.p, qd, ctx->ahp_ws.p, ctx->w64.p, ctx->stats.p, ctx->stream));
+  if (!dev) {
+    if (mask) CK(cudaMemcpyAsync(mask, qd.mask, g.n, cudaMemcpyDeviceToHost, ctx->stream));
+    if (scores) CK(cudaMemcpyAsync(scores, qd.scores, 4 * (size_t)g.n, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(best, qd.best, 4, cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  if (!(opt->flags & NACS_ASYNC)) {
+    CK(cudaStreamSynchronize(ctx->stream));
+    if ((st = finish_stats(ctx))) return st;
+  }
+  return NACS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+nacs_status nacs_create(nacs_ctx** out, int device, void* cuda_stream) {
+  if (!out) return NACS_EINVAL;
+  *out = nullptr;
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+    cudaGetLastError();
+    return NACS_ECUDA;
+  }
+  if (device < 0 || device >= count) return NACS_EINVAL;
+  nacs_ctx* ctx = new nacs_ctx();
+  ctx->device = device;
+  cudaError_t e = cudaSetDevice(device);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
+  if (e == cudaSuccess) {
+    if (cuda_stream) {
+      ctx->stream = static_cast<cudaStream_t>(cuda_stream);
+    } else {
+      e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+      ctx->own_stream = true;
+    }
+  }
+  if (e != cudaSuccess) {
+    delete ctx;
+    cudaGetLastError();
+    return NACS_ECUDA;
+  }
+  *out = ctx;
+  return NACS_OK;
+}
+
+void nacs_destroy(nacs_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  ctx->state.release();
+  ctx->req_in.release();
+  ctx->req_out.release();
+  ctx->ulog.release();
+  ctx->w64.release();
+  ctx->ahp_ws.release();
+  ctx->misc.release();
+  ctx->mask.release();
+  ctx->scores.release();
+  ctx->stats.release();
+  ctx->pin_in.release();
+  ctx->pin_out.release();
+  if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+nacs_status nacs_load_topology(nacs_ctx* ctx, const nacs_topology* t) {
+  if (!ctx) return NACS_EINVAL;
+  ctx->err.clear();
+  if (!t) return fail(ctx, NACS_EINVAL, "topology: NULL");
+  std::string m;
+  if (t->k < 2 || t->k % 2) m += "k must be even and >= 2; ";
+  if (t->cpu_cap <= 0 || t->ram_cap <= 0 || t->link_cap <= 0) m += "capacities must be > 0; ";
+  if (!m.empty()) return fail(ctx, NACS_EINVAL, m);
+  if (t->k > NACS_MAX_K) return fail(ctx, NACS_ETOOBIG, "k > NACS_MAX_K (64)");
+  if (t->cpu_cap > NACS_MAX_CAP || t->ram_cap > NACS_MAX_CAP || t->link_cap > NACS_MAX_CAP)
+    return fail(ctx, NACS_ETOOBIG, "a capacity exceeds NACS_MAX_CAP (2^23-1)");
+  Geo g;
+  g.k = t->k;
+  g.h = t->k / 2;
+  g.n = t->k * t->k * t->k / 4;
+  g.E = t->k * t->k / 2;
+  g.L = 3 * g.n;
+  g.cpu_cap = t->cpu_cap;
+  g.ram_cap = t->ram_cap;
+  g.link_cap = t->link_cap;
+  g.magic_h = (unsigned)((((unsigned long long)1 << 32) + g.h - 1) / g.h);
+  std::vector<int> h((size_t)g.words());
+  int n = g.n;
+  int bad_cpu = 0, bad_ram = 0, bad_act = 0, bad_link = 0;
+  for (int u = 0; u < n; ++u) {
+    int c = t->cpu_res ? t->cpu_res[u] : g.cpu_cap;
+    int r = t->ram_res ? t->ram_res[u] : g.ram_cap;
+    if (c < 0 || c > g.cpu_cap) ++bad_cpu;
+    if (r < 0 || r > g.ram_cap) ++bad_ram;
+    int a;
+    if (t->active) {
+      a = t->active[u];
+      if (a > 1) ++bad_act;
+    } else {
+      a = (c < g.cpu_cap || r < g.ram_cap) ? 1 : 0;
+    }
+    h[u] = c;
+    h[n + u] = r;
+    h[2 * n + u] = a;
+  }
+  for (int l = 0; l < g.L; ++l) {
+    int b = t->link_res ? t->link_res[l] : g.link_cap;
+    if (b < 0 || b > g.link_cap) ++bad_link;
+    h[3 * n + l] = b;
+  }
+  if (bad_cpu) m += std::to_string(bad_cpu) + " cpu_res outside [0, cpu_cap]; ";
+  if (bad_ram) m += std::to_string(bad_ram) + " ram_res outside [0, ram_cap]; ";
+  if (bad_act) m += std::to_string(bad_act) + " active not 0/1; ";
+  if (bad_link) m += std::to_string(bad_link) + " link_res outside [0, link_cap]; ";
+  if (!m.empty()) return fail(ctx, NACS_EINVAL, m);
+  CK(cudaSetDevice(ctx->device));
+  CK(ctx->state.reserve(h.size()));
+  CK(cudaMemcpyAsync(ctx->state.p, h.data(), h.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  ctx->g = g;
+  ctx->has_topo = true;
+  return NACS_OK;
+}
+
+nacs_status nacs_read_topology(nacs_ctx* ctx, int32_t* cpu_res, int32_t* ram_res, uint8_t* active,
+                               int32_t* link_res) {
+  if (!ctx) return NACS_EINVAL;
+  ctx->err.clear();
+  if (!ctx->has_topo) return fail(ctx, NACS_ENOTOPO, "no topology loaded");
+  CK(cudaSetDevice(ctx->device));
+  const Geo& g = ctx->g;
+  std::vector<int> h((size_t)g.words());
+  CK(cudaMemcpyAsync(h.data(), ctx->state.p, h.size() * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  int n = g.n;
+  for (int u = 0; u < n; ++u) {
+    if (cpu_res) cpu_res[u] = h[u];
+    if (ram_res) ram_res[u] = h[n + u];
+    if (active) active[u] = (uint8_t)h[2 * n + u];
+  }
+  if (link_res) std::memcpy(link_res, h.data() + 3 * n, (size_t)g.L * 4);
+  return NACS_OK;
+}
+
+nacs_status nacs_rank_ahp(nacs_ctx* ctx, const nacs_options* opt, const nacs_pod_query* q, uint8_t* mask,
+                          float* scores, int32_t* best) {
+  return rank_impl(ctx, opt, q, mask, scores, best, 0);
+}
+
+nacs_status nacs_rank_topsis(nacs_ctx* ctx, const nacs_options* opt, const nacs_pod_query* q, uint8_t* mask,
+                             float* scores, int32_t* best) {
+  return rank_impl(ctx, opt, q, mask, scores, best, 1);
+}
+
+nacs_status nacs_schedule_batch(nacs_ctx* ctx, const nacs_options* opt, const nacs_requests* batch,
+                                nacs_placements* out) {
+  nacs_status st = begin_call(ctx);
+  if (st) return st;
+  Opt o;
+  if ((st = check_options(ctx, opt, &o))) return st;
+  if ((st = check_placements(ctx, out))) return st;
+  if (!batch || batch->n_requests < 0) return fail(ctx, NACS_EINVAL, "requests: NULL or n_requests < 0");
+  const bool dev = opt->flags & NACS_DEVICE_PTRS;
+  const Geo& g = ctx->g;
+  if (!nacs::batch_smem_bytes(g, o.method))
+    return fail(ctx, NACS_ETOOBIG, "snapshot does not fit in shared memory for nacs_schedule_batch");
+  int R = batch->n_requests;
+  if (R == 0) return finish_stats(ctx);
+  nacs::ReqsDev Rd;
+  nacs::OutDev Od;
+  int C = 0, V = 0;
+  if (!dev) {
+    if ((st = check_requests_host(ctx, batch, &C, &V))) return st;
+    if ((st = stage_requests(ctx, batch, C, V, &Rd))) return st;
+    if ((st = device_outputs(ctx, R, C, V, &Od))) return st;
+  } else {
+    Rd = device_requests(batch);
+    Od.status = out->status;
+    Od.server = out->server_of_container;
+    Od.cpu_a = out->cpu_alloc;
+    Od.ram_a = out->ram_alloc;
+    Od.bw_a = out->bw_alloc;
+    Od.path = out->path_of_vlink;
+  }
+  int per_sm = 0;
+  CK(nacs::batch_occupancy(g, o.method, &per_sm));
+  if (per_sm <= 0) return fail(ctx, NACS_ETOOBIG, "batch kernel cannot be resident");
+  int grid = ctx->num_sms * per_sm;
+  if (grid > R) grid = R;
+  CK(ctx->ulog.reserve((size_t)grid * nacs::ULOG_CAP));
+  if (o.method == 0) CK(ctx->w64.reserve((size_t)grid * 4 * g.n));
+  CK(ctx->misc.reserve(8));
+  CK(cudaMemsetAsync(ctx->misc.p, 0, sizeof(int), ctx->stream));
+  CK(nacs::launch_batch(g, o, ctx->state.p, Rd, Od, ctx->ulog.p, ctx->w64.p, ctx->misc.p, ctx->stats.p, grid,
+                        ctx->stream));
+  if (!dev) {
+    if ((st = unstage_outputs(ctx, R, C, V, out))) return st;
+  }
+  if (!(opt->flags & NACS_ASYNC)) {
+    CK(cudaStreamSynchronize(ctx->stream));
+    if ((st = finish_stats(ctx))) return st;
+    if (ctx->last.invalid > 0)
+      return fail(ctx, NACS_EINVAL, std::to_string(ctx->last.invalid) + " invalid requests (status -1)");
+  }
+  return NACS_OK;
+}
+
+nacs_status nacs_schedule_request(nacs_ctx* ctx, const nacs_options* opt, const nacs_requests* reqs,
+                                  nacs_placements* out) {
+  nacs_status st = begin_call(ctx);
+  if (st) return st;
+  Opt o;
+  if ((st = check_options(ctx, opt, &o))) return st;
+  if ((st = check_placements(ctx, out))) return st;
+  if (!reqs || reqs->n_requests < 0) return fail(ctx, NACS_EINVAL, "requests: NULL or n_requests < 0");
+  const bool dev = opt->flags & NACS_DEVICE_PTRS;
+  const bool async = opt->flags & NACS_ASYNC;
+  const Geo& g = ctx->g;
+  int R = reqs->n_requests;
+  if (R == 0) return finish_stats(ctx);
+  nacs::ReqsDev Rd;
+  nacs::OutDev Od;
+  int C = 0, V = 0;
+  if (!dev) {
+    if ((st = check_requests_host(ctx, reqs, &C, &V))) return st;
+    if ((st = stage_requests(ctx, reqs, C, V, &Rd))) return st;
+    if ((st = device_outputs(ctx, R, C, V, &Od))) return st;
+  } else {
+    Rd = device_requests(reqs);
+    Od.status = out->status;
+    Od.server = out->server_of_container;
+    Od.cpu_a = out->cpu_alloc;
+    Od.ram_a = out->ram_alloc;
+    Od.bw_a = out->bw_alloc;
+    Od.path = out->path_of_vlink;
+    if (!async) {  // validate before touching the state: an error leaves it unchanged
+      CK(nacs::launch_validate(Rd, Od.status, ctx->stats.p, ctx->stream));
+      unsigned long long h[nacs::ST_N];
+      CK(cudaMemcpyAsync(h, ctx->stats.p, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+      CK(cudaStreamSynchronize(ctx->stream));
+      if (h[nacs::ST_INVALID])
+        return fail(ctx, NACS_EINVAL, std::to_string(h[nacs::ST_INVALID]) + " invalid requests");
+    }
+  }
+  CK(ctx->ulog.reserve(nacs::ULOG_CAP));
+  if (o.method == 0) {
+    CK(ctx->ahp_ws.reserve(10 * (size_t)g.n));
+    CK(ctx->w64.reserve(4 * (size_t)g.n));
+  }
+  CK(nacs::launch_sequential(g, o, ctx->state.p, Rd, Od, ctx->ulog.p, ctx->ahp_ws.p, ctx->w64.p, ctx->stats.p,
+                             ctx->stream));
+  if (!dev) {
+    if ((st = unstage_outputs(ctx, R, C, V, out))) return st;
+  }
+  if (!async) {
+    CK(cudaStreamSynchronize(ctx->stream));
+    if ((st = finish_stats(ctx))) return st;
+  }
+  return NACS_OK;
+}
+
+nacs_status nacs_last_stats(nacs_ctx* ctx, nacs_stats* out) {
+  if (!ctx || !out) return NACS_EINVAL;
+  nacs_status st = finish_stats(ctx);
+  if (st) return st;
+  *out = ctx->last;
+  return NACS_OK;
+}
+
+const char* nacs_last_error(const nacs_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+}  // extern "C"

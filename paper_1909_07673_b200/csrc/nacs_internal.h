@@ -1,0 +1,107 @@
+// nacs_internal.h — types shared by the host API (nacs_api.cu) and the kernels
+// (nacs_kernels.cu) of libnacs.  Not part of the public ABI (include/nacs.h).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace nacs {
+
+constexpr int MAXC = 128;   // NACS_MAX_CONTAINERS: containers (and pods) per request
+constexpr int MAXV = 512;   // NACS_MAX_VLINKS: virtual links per request
+constexpr int MAXF = 128;   // flows per pod step (one per distinct peer server, <= pods)
+constexpr int MAXK = 64;    // NACS_MAX_K
+constexpr int MAXW = 32;    // warps per CTA
+// undo-log entries one request can need: 3 per pod + 6 per flow + 2 per container
+// (top-up) + 6 per vlink (top-up); every vlink belongs to at most one flow.
+constexpr int ULOG_CAP = 3 * MAXC + 6 * MAXV + 2 * MAXC + 6 * MAXV + 64;
+
+// Fat-tree geometry (include/nacs.h).  Device state layout, int32 words:
+//   cpu[n] | ram[n] | act[n] | links[L] = access[n] | edge-agg[E*h] | agg-core[k*h*h]
+// so the criteria table (cpu, ram, act, acc) is the first 4n words, structure-of-arrays.
+struct Geo {
+  int k, h, n, E, L;
+  int cpu_cap, ram_cap, link_cap;
+  unsigned magic_h;  // ceil(2^32 / h): x / h == __umulhi(x, magic_h) for x < 2^24
+  __host__ __device__ int words() const { return 3 * n + L; }
+};
+
+struct Opt {
+  int method;        // 0 AHP, 1 TOPSIS
+  double wd[4];      // weights W
+  int ahp_rule;      // 0 literal, 1 shifted
+  int l1_mode;       // 0 pairwise on W, 1 L1 = W
+  int path_filter;   // 1 filter on path bandwidth, 0 CPU/RAM only
+  int exact64;       // decide every argmax in FP64
+};
+
+struct ReqsDev {
+  int n;
+  const int *coff, *cpu_min, *cpu_max, *ram_min, *ram_max, *pod_of;
+  const int *voff, *src, *dst, *bw_min, *bw_max;
+};
+
+struct OutDev {
+  int *status, *server, *cpu_a, *ram_a, *bw_a, *path;
+};
+
+struct QueryDev {
+  int dc, dr, nflow, nex;
+  const int *fv, *fD, *ex;  // device arrays
+  uint8_t *mask;            // [n] or null
+  float *scores;            // [n] or null
+  int *best;                // [1]
+};
+
+enum { ST_POD_STEPS = 0, ST_RETRIES = 1, ST_FP64 = 2, ST_INVALID = 3, ST_FEAS = 4, ST_PAIRS = 5, ST_N = 6 };
+
+// Request validation shared by the host path and the kernels (reading R24).
+// Returns 0 if valid, else a bitmask: 1 size limit, 2 demands, 4 min>max, 8 pod ids,
+// 16 vlink endpoints, 32 vlink bandwidth.
+__host__ __device__ inline int validate_request(int nC, int nV, const int* cpu_min, const int* cpu_max,
+                                                const int* ram_min, const int* ram_max, const int* pod_of,
+                                                const int* src, const int* dst, const int* bw_min,
+                                                const int* bw_max) {
+  if (nC <= 0 || nC > MAXC || nV < 0 || nV > MAXV) return 1;
+  int bad = 0;
+  unsigned used[MAXC / 32] = {0, 0, 0, 0};
+  int maxp = -1;
+  for (int i = 0; i < nC; ++i) {
+    if (cpu_min[i] <= 0 || ram_min[i] <= 0) bad |= 2;
+    if (cpu_min[i] > cpu_max[i] || ram_min[i] > ram_max[i]) bad |= 4;
+    int p = pod_of[i];
+    if (p < 0 || p >= nC) { bad |= 8; continue; }
+    used[p >> 5] |= 1u << (p & 31);
+    if (p > maxp) maxp = p;
+  }
+  for (int p = 0; p <= maxp; ++p)
+    if (!((used[p >> 5] >> (p & 31)) & 1u)) bad |= 8;
+  for (int e = 0; e < nV; ++e) {
+    if (src[e] < 0 || src[e] >= nC || dst[e] < 0 || dst[e] >= nC || src[e] == dst[e]) bad |= 16;
+    if (bw_min[e] <= 0 || bw_min[e] > bw_max[e]) bad |= 32;
+  }
+  return bad;
+}
+
+// Launchers (nacs_kernels.cu).  Each returns the cudaError_t of the launch.
+struct LaunchInfo {
+  int grid, block;
+  size_t dyn_smem;
+};
+
+// dynamic shared memory of the batch kernel, 0 if it does not fit
+size_t batch_smem_bytes(const Geo& g, int method);
+int batch_block_size(const Geo& g);
+cudaError_t batch_occupancy(const Geo& g, int method, int* blocks_per_sm);
+
+cudaError_t launch_batch(const Geo& g, const Opt& o, const int* d_state, const ReqsDev& R, const OutDev& O,
+                         int2* ulog, double* w64, int* next, unsigned long long* stats, int grid,
+                         cudaStream_t s);
+// sequential: one CTA, requests in order, in place on d_state
+cudaError_t launch_sequential(const Geo& g, const Opt& o, int* d_state, const ReqsDev& R, const OutDev& O,
+                              int2* ulog, float* ahp_ws, double* w64, unsigned long long* stats,
+                              cudaStream_t s);
+cudaError_t launch_rank(const Geo& g, const Opt& o, int* d_state, const QueryDev& q, float* ahp_ws,
+                        double* w64, unsigned long long* stats, cudaStream_t s);
+cudaError_t launch_validate(const ReqsDev& R, int* status, unsigned long long* stats, cudaStream_t s);
+
+}  // namespace nacs

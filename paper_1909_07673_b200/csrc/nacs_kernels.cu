@@ -1,0 +1,1236 @@
+// nacs_kernels.cu — sm_100a kernels of libnacs: one pod step = feasibility filter,
+// per-criterion statistics, AHP or TOPSIS scoring, argmax, commit (§V,
+// P:298-386; readings R1-R24 in DESIGN.md).
+//
+// Execution model.  A CTA runs whole requests: for every pod (ascending id, R15) it
+// builds the pod's flows to placed peers (a1-a2), marks fabric-infeasible edge switches
+// (a2), filters servers and reduces the criteria statistics (a3-a4), scores the feasible
+// servers and reduces a top-2 argmax key (a5-a7), then one warp commits (a8).  The
+// request end tops allocations up (a9).
+//   * k_batch: persistent CTAs; each holds a private copy of the whole snapshot in
+//     shared memory (loaded once per CTA with a TMA bulk copy) and mutates it in place;
+//     an undo log restores it after every request (R21 snapshot isolation).
+//   * k_sequential: one CTA, requests in order, in place on the global state (the
+//     paper's online semantics); a rejected request is rolled back (R20).
+//   * k_rank: one CTA, one pod query, no commit.
+//
+// Numerics.  All state is integer.  Criteria are read as int32 and every difference
+// (x - min, max - x) is taken in integers, then converted exactly to FP32 with the
+// 2^23 magic-number trick (no I2F on the hot loop).  TOPSIS norms are exact integer sums
+// of squares (64-bit).  Scores are FP32; an argmax whose top-2 FP32 gap is inside the
+// derived FP32 error bound is re-decided in FP64 over the near-max candidates (R14).
+#include <cfloat>
+#include <climits>
+#include <cstdint>
+
+#include "nacs_internal.h"
+
+namespace nacs {
+
+#define FULL 0xffffffffu
+
+// ---------------------------------------------------------------- helpers ----
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float rsqrt_approx(float x) {
+  float r;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+// s * d rounded once, for an integer 0 <= d < 2^23: (2^23 + d) is exact in FP32 and
+// fma(s, 2^23 + d, -s*2^23) = round(s * d).  s2p23 = s * 2^23 (exact).
+__device__ __forceinline__ float scaled_diff(float s, float s2p23, int d) {
+  return fmaf(s, __int_as_float(0x4B000000 | d), -s2p23);
+}
+__device__ __forceinline__ float exact_f(int d) {  // 0 <= d < 2^23, exact
+  return __int_as_float(0x4B000000 | d) - 8388608.0f;
+}
+__device__ __forceinline__ unsigned div_h(unsigned x, unsigned magic) { return __umulhi(x, magic); }
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+// FP32 error-bound constants.  u = 2^-24.
+// TOPSIS: |r32 - r| <= 20u; ambiguous top-2 gap <= 2^-17 (> 4 x 40u).
+constexpr float kTopsisDelta = 7.62939453125e-06f;  // 2^-17
+// AHP: relative error of PG in FP32 <= (96 + 2*ceil(nf/32)) u; ambiguous if the
+// relative top-2 gap is <= 2 x that.
+__device__ __forceinline__ float ahp_delta_rel(int nf) {
+  return 2.0f * (96.0f + 2.0f * (float)((nf + 31) / 32)) * 5.9604644775390625e-08f;
+}
+
+// ------------------------------------------------------------ scratch -------
+struct Scratch {
+  // request
+  int nC, nV, P, req_ok;
+  int cpod[MAXC];
+  int pod_cpu[MAXC], pod_ram[MAXC], pod_srv[MAXC];
+  int vpath[MAXV];
+  // pod step
+  int p, dc, dr, nflow, sumD, G, vm;
+  int fv[MAXF], fD[MAXF], fok[MAXF], fpath[MAXF], fexcl[MAXF];
+  unsigned pm[MAXK];
+  int fail, log_n, log_mark;
+  // statistics over the feasible set F
+  int nf, nact, mn[4], mx[4];
+  unsigned long long sq[4];
+  float sf[4], s2p23[4];
+  double sd[4];
+  // AHP per-criterion configuration
+  int ahp_const[4];
+  float ahp_scale[4];
+  double ahp_scaled[4];
+  float L1[4];
+  double L1d[4];
+  // selection
+  unsigned long long key1, key2;
+  int best, amb;
+  // block reductions
+  int red_i[MAXW][8];
+  unsigned long long red_u[MAXW][3];
+  unsigned long long red_k[MAXW][2];
+  double red_d[MAXW];
+  int red_j[MAXW];
+  int scan[MAXW];
+  // request fetch (batch)
+  int next_req;
+  // counters (thread 0)
+  unsigned long long c_steps, c_retries, c_fp64, c_invalid, c_feas, c_pairs;
+};
+
+struct Ctx {
+  Geo g;
+  Opt o;
+  int* st;             // state words (shared memory in k_batch, global otherwise)
+  const int* snap;     // global snapshot (k_batch) for reference
+  Scratch* s;
+  unsigned* maskw;     // [nW] feasibility bitmap of the current pod step
+  unsigned* special;   // [nW] flow servers and excluded servers of the pod step
+  unsigned* edgebad;   // [nEW] edge switches some flow cannot reach with its demand
+  float* xs;           // AHP: [4][nfcap] feasible criteria values (compacted, server order)
+  int* xid;            // AHP: [nfcap] server of each compacted slot
+  float* wcol;         // AHP: [4][nfcap] 1 / column sums
+  float* pg;           // AHP: [nfcap] FP32 global priorities
+  double* w64;         // AHP FP64 rescore: [4][nfcap]
+  int nfcap;
+  int2* ulog;          // undo log (global)
+  int tid, B, NW, lane, warp;
+  int nW, nEW;
+};
+
+// ------------------------------------------------------- undo log (1 thread) --
+__device__ __forceinline__ void st_set(Ctx& c, int off, int val) {
+  Scratch* s = c.s;
+  c.ulog[s->log_n] = make_int2(off, c.st[off]);
+  s->log_n += 1;
+  c.st[off] = val;
+}
+__device__ __forceinline__ void undo_to(Ctx& c, int mark) {
+  Scratch* s = c.s;
+  for (int i = s->log_n - 1; i >= mark; --i) {
+    int2 e = c.ulog[i];
+    c.st[e.x] = e.y;
+  }
+  s->log_n = mark;
+}
+
+// ------------------------------------------------------------ reductions -----
+__device__ __forceinline__ void top2_insert(unsigned long long& k1, unsigned long long& k2,
+                                            unsigned long long k) {
+  if (k > k1) { k2 = k1; k1 = k; }
+  else if (k > k2) { k2 = k; }
+}
+__device__ __forceinline__ void top2_merge(unsigned long long& a1, unsigned long long& a2,
+                                           unsigned long long b1, unsigned long long b2) {
+  unsigned long long hi = a1 > b1 ? a1 : b1;
+  unsigned long long lo = a1 > b1 ? b1 : a1;
+  unsigned long long s2 = a2 > b2 ? a2 : b2;
+  a1 = hi;
+  a2 = lo > s2 ? lo : s2;
+}
+
+// Block-wide top-2 of 64-bit keys; result in s->key1, s->key2.  All threads call.
+__device__ void block_top2(Ctx& c, unsigned long long k1, unsigned long long k2) {
+  Scratch* s = c.s;
+  for (int o = 16; o > 0; o >>= 1) {
+    unsigned long long b1 = __shfl_xor_sync(FULL, k1, o);
+    unsigned long long b2 = __shfl_xor_sync(FULL, k2, o);
+    top2_merge(k1, k2, b1, b2);
+  }
+  if (c.lane == 0) { s->red_k[c.warp][0] = k1; s->red_k[c.warp][1] = k2; }
+  __syncthreads();
+  if (c.warp == 0) {
+    k1 = c.lane < c.NW ? s->red_k[c.lane][0] : 0ull;
+    k2 = c.lane < c.NW ? s->red_k[c.lane][1] : 0ull;
+    for (int o = 16; o > 0; o >>= 1) {
+      unsigned long long b1 = __shfl_xor_sync(FULL, k1, o);
+      unsigned long long b2 = __shfl_xor_sync(FULL, k2, o);
+      top2_merge(k1, k2, b1, b2);
+    }
+    if (c.lane == 0) { s->key1 = k1; s->key2 = k2; }
+  }
+  __syncthreads();
+}
+
+// Block-wide argmax of (double value, index): larger value, then lower index.
+__device__ void block_argmax64(Ctx& c, double v, int j) {
+  Scratch* s = c.s;
+  for (int o = 16; o > 0; o >>= 1) {
+    double bv = __shfl_xor_sync(FULL, v, o);
+    int bj = __shfl_xor_sync(FULL, j, o);
+    if (bv > v || (bv == v && (unsigned)bj < (unsigned)j)) { v = bv; j = bj; }
+  }
+  if (c.lane == 0) { s->red_d[c.warp] = v; s->red_j[c.warp] = j; }
+  __syncthreads();
+  if (c.warp == 0) {
+    v = c.lane < c.NW ? s->red_d[c.lane] : -DBL_MAX;
+    j = c.lane < c.NW ? s->red_j[c.lane] : -1;
+    for (int o = 16; o > 0; o >>= 1) {
+      double bv = __shfl_xor_sync(FULL, v, o);
+      int bj = __shfl_xor_sync(FULL, j, o);
+      if (bv > v || (bv == v && (unsigned)bj < (unsigned)j)) { v = bv; j = bj; }
+    }
+    if (c.lane == 0) s->best = j;
+  }
+  __syncthreads();
+}
+
+// Exclusive block scan of one int per thread.
+__device__ int block_exscan(Ctx& c, int x) {
+  Scratch* s = c.s;
+  int inc = x;
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(FULL, inc, o);
+    if (c.lane >= o) inc += y;
+  }
+  if (c.lane == 31) s->scan[c.warp] = inc;
+  __syncthreads();
+  if (c.warp == 0) {
+    int t = c.lane < c.NW ? s->scan[c.lane] : 0;
+    int ti = t;
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(FULL, ti, o);
+      if (c.lane >= o) ti += y;
+    }
+    if (c.lane < c.NW) s->scan[c.lane] = ti - t;
+  }
+  __syncthreads();
+  int r = s->scan[c.warp] + inc - x;
+  __syncthreads();
+  return r;
+}
+
+// ------------------------------------------------------ AHP L1 (Eq. 9, R10) --
+__device__ double ahp_cell64(double d, int rule) {
+  if (rule == 0) return d > 0 ? d : (d < 0 ? 1.0 / (-d) : 1.0);
+  return d > 0 ? 1.0 + d : (d < 0 ? 1.0 / (1.0 - d) : 1.0);
+}
+// criteria-level priority of the weights (one thread)
+__device__ void ahp_l1_dev(const Opt& o, double L1[4]) {
+  if (o.l1_mode == 1) {
+    for (int c = 0; c < 4; ++c) L1[c] = o.wd[c];
+    return;
+  }
+  double lo = o.wd[0], hi = o.wd[0];
+  for (int c = 1; c < 4; ++c) { lo = fmin(lo, o.wd[c]); hi = fmax(hi, o.wd[c]); }
+  if (hi == lo) {
+    for (int c = 0; c < 4; ++c) L1[c] = 0.25;
+    return;
+  }
+  double col[4];
+  for (int j = 0; j < 4; ++j) {
+    col[j] = 0;
+    for (int i = 0; i < 4; ++i) col[j] += ahp_cell64(9.0 * (o.wd[i] - o.wd[j]) / (hi - lo), o.ahp_rule);
+  }
+  for (int i = 0; i < 4; ++i) {
+    double a = 0;
+    for (int j = 0; j < 4; ++j) a += ahp_cell64(9.0 * (o.wd[i] - o.wd[j]) / (hi - lo), o.ahp_rule) / col[j];
+    L1[i] = a / 4.0;
+  }
+}
+
+// ------------------------------------------------------------- fabric ------
+// Widest ECMP path from server u to server v on the current residuals (R16),
+// computed by warp 0; returns (path id, fabric bottleneck) in all lanes.
+__device__ int2 widest_path_warp(Ctx& c, int u, int v) {
+  const Geo& g = c.g;
+  int h = g.h;
+  int eu = (int)div_h(u, g.magic_h), ev = (int)div_h(v, g.magic_h);
+  if (eu == ev) return make_int2(0, INT_MAX);
+  int pu = (int)div_h(eu, g.magic_h), pv = (int)div_h(ev, g.magic_h);
+  const int* EA = c.st + 4 * g.n;
+  const int* AC = EA + g.E * h;
+  int best = -1, bt = INT_MAX;
+  if (pu == pv) {
+    for (int a = c.lane; a < h; a += 32) {
+      int b = min(EA[eu * h + a], EA[ev * h + a]);
+      if (b > best) { best = b; bt = a; }
+    }
+  } else {
+    for (int t = c.lane; t < h * h; t += 32) {
+      int a = (int)div_h(t, g.magic_h), b = t - a * h;
+      int x = min(min(EA[eu * h + a], EA[ev * h + a]), min(AC[(pu * h + a) * h + b], AC[(pv * h + a) * h + b]));
+      if (x > best) { best = x; bt = t; }
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    int ob = __shfl_xor_sync(FULL, best, o);
+    int ot = __shfl_xor_sync(FULL, bt, o);
+    if (ob > best || (ob == best && ot < bt)) { best = ob; bt = ot; }
+  }
+  return make_int2(pu == pv ? 1 + bt : 1 + h + bt, best);
+}
+
+// Offsets of the fabric links of path `pid` between servers u and v; returns count.
+__device__ int path_links(const Geo& g, int u, int v, int pid, int off[4]) {
+  if (pid <= 0) return 0;
+  int h = g.h;
+  int eu = (int)div_h(u, g.magic_h), ev = (int)div_h(v, g.magic_h);
+  int ea0 = 4 * g.n, ac0 = ea0 + g.E * h;
+  if (pid <= h) {
+    int a = pid - 1;
+    off[0] = ea0 + eu * h + a;
+    off[1] = ea0 + ev * h + a;
+    return 2;
+  }
+  int t = pid - 1 - h;
+  int a = (int)div_h(t, g.magic_h), b = t - a * h;
+  int pu = (int)div_h(eu, g.magic_h), pv = (int)div_h(ev, g.magic_h);
+  off[0] = ea0 + eu * h + a;
+  off[1] = ac0 + (pu * h + a) * h + b;
+  off[2] = ac0 + (pv * h + a) * h + b;
+  off[3] = ea0 + ev * h + a;
+  return 4;
+}
+
+// a2: mark edge switches from which some flow's widest fabric bottleneck is below its
+// demand (SURVEY §8(a) a2 as threshold bitmasks).  All threads.
+__device__ void fabric_tables(Ctx& c) {
+  Scratch* s = c.s;
+  const Geo& g = c.g;
+  int h = g.h;
+  const int* EA = c.st + 4 * g.n;
+  const int* AC = EA + g.E * h;
+  for (int f = 0; f < s->nflow; ++f) {
+    int v = s->fv[f], D = s->fD[f];
+    int ev = (int)div_h(v, g.magic_h), pv = (int)div_h(ev, g.magic_h);
+    for (int p = c.tid; p < g.k; p += c.B) s->pm[p] = 0u;
+    if (c.tid == 0) s->vm = 0;
+    __syncthreads();
+    // pm[p] bit a: some core (a, b) links pod p and pod pv with both links >= D
+    for (int t = c.tid; t < g.k * h; t += c.B) {
+      int p = (int)div_h(t, g.magic_h), a = t - p * h;
+      bool ok = false;
+      const int* r1 = AC + (p * h + a) * h;
+      const int* r2 = AC + (pv * h + a) * h;
+      for (int b = 0; b < h && !ok; ++b) ok = r1[b] >= D && r2[b] >= D;
+      if (ok) atomicOr(&s->pm[p], 1u << a);
+    }
+    for (int a = c.tid; a < h; a += c.B)
+      if (EA[ev * h + a] >= D) atomicOr((unsigned*)&s->vm, 1u << a);
+    __syncthreads();
+    unsigned vm = (unsigned)s->vm;
+    for (int e = c.tid; e < g.E; e += c.B) {
+      if (e == ev) continue;  // same edge switch: access links only
+      unsigned em = 0;
+      for (int a = 0; a < h; ++a) em |= (EA[e * h + a] >= D ? 1u : 0u) << a;
+      int pe = (int)div_h(e, g.magic_h);
+      unsigned ok = (pe == pv) ? (em & vm) : (em & vm & s->pm[pe]);
+      if (!ok) atomicOr(&c.edgebad[e >> 5], 1u << (e & 31));
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------- pass A -------
+// a3 + a4: feasibility mask and statistics over F.  Writes maskw, s->nf, mn, mx, sq.
+template <bool WRITE_MASK>
+__device__ void pass_filter(Ctx& c, uint8_t* mask_out, float* scores_out) {
+  Scratch* s = c.s;
+  const Geo& g = c.g;
+  const int n = g.n;
+  const int* cpu = c.st;
+  const int* ram = c.st + n;
+  const int* act = c.st + 2 * n;
+  const int* acc = c.st + 3 * n;
+  const int dc = s->dc, dr = s->dr, sumD = s->sumD;
+  const bool net = c.o.path_filter && s->nflow > 0;
+  const bool G = s->G != 0;
+  int nf = 0, nact = 0;
+  unsigned mn0 = UINT_MAX, mn1 = UINT_MAX, mn3 = UINT_MAX, mx0 = 0, mx1 = 0, mx3 = 0;
+  unsigned long long q0 = 0, q1 = 0, q3 = 0;
+  for (int base = c.warp * 32; base < n; base += c.B) {
+    int u = base + c.lane;
+    bool in = u < n;
+    int x0 = 0, x1 = 0, x2 = 0, x3 = 0;
+    if (in) { x0 = cpu[u]; x1 = ram[u]; x2 = act[u]; x3 = acc[u]; }
+    bool ok = in && x0 >= dc && x1 >= dr;
+    if (net) {
+      unsigned e = div_h((unsigned)u, g.magic_h);
+      ok = ok && G && x3 >= sumD && !((c.edgebad[e >> 5] >> (e & 31)) & 1u);
+    }
+    unsigned sp = c.special[base >> 5];
+    if ((sp >> c.lane) & 1u) {
+      // a flow server (its own flow needs no network) or an excluded server (R18)
+      int f = -1;
+      for (int i = 0; i < s->nflow; ++i) if (s->fv[i] == u) f = i;
+      if (f < 0 || s->fexcl[f]) ok = false;
+      else ok = x0 >= dc && x1 >= dr && (!c.o.path_filter || s->fok[f]);
+    }
+    unsigned bal = __ballot_sync(FULL, ok);
+    if (c.lane == 0) c.maskw[base >> 5] = bal;
+    if (WRITE_MASK && in) { mask_out[u] = ok ? 1 : 0; scores_out[u] = 0.0f; }
+    if (ok) {
+      nf += 1;
+      nact += x2;
+      mn0 = min(mn0, (unsigned)x0); mx0 = max(mx0, (unsigned)x0);
+      mn1 = min(mn1, (unsigned)x1); mx1 = max(mx1, (unsigned)x1);
+      mn3 = min(mn3, (unsigned)x3); mx3 = max(mx3, (unsigned)x3);
+      q0 += (unsigned long long)((unsigned)x0) * (unsigned)x0;
+      q1 += (unsigned long long)((unsigned)x1) * (unsigned)x1;
+      q3 += (unsigned long long)((unsigned)x3) * (unsigned)x3;
+    }
+  }
+  // warp reductions (redux.sync for 32-bit, shuffles for 64-bit sums)
+  nf = (int)__reduce_add_sync(FULL, (unsigned)nf);
+  nact = (int)__reduce_add_sync(FULL, (unsigned)nact);
+  mn0 = __reduce_min_sync(FULL, mn0); mx0 = __reduce_max_sync(FULL, mx0);
+  mn1 = __reduce_min_sync(FULL, mn1); mx1 = __reduce_max_sync(FULL, mx1);
+  mn3 = __reduce_min_sync(FULL, mn3); mx3 = __reduce_max_sync(FULL, mx3);
+  for (int o = 16; o > 0; o >>= 1) {
+    q0 += __shfl_xor_sync(FULL, q0, o);
+    q1 += __shfl_xor_sync(FULL, q1, o);
+    q3 += __shfl_xor_sync(FULL, q3, o);
+  }
+  if (c.lane == 0) {
+    int* r = s->red_i[c.warp];
+    r[0] = nf; r[1] = nact; r[2] = (int)mn0; r[3] = (int)mx0; r[4] = (int)mn1; r[5] = (int)mx1;
+    r[6] = (int)mn3; r[7] = (int)mx3;
+    s->red_u[c.warp][0] = q0; s->red_u[c.warp][1] = q1; s->red_u[c.warp][2] = q3;
+  }
+  __syncthreads();
+  if (c.warp == 0) {
+    bool in = c.lane < c.NW;
+    const int* r = s->red_i[in ? c.lane : 0];
+    nf = in ? r[0] : 0; nact = in ? r[1] : 0;
+    mn0 = in ? (unsigned)r[2] : UINT_MAX; mx0 = in ? (unsigned)r[3] : 0;
+    mn1 = in ? (unsigned)r[4] : UINT_MAX; mx1 = in ? (unsigned)r[5] : 0;
+    mn3 = in ? (unsigned)r[6] : UINT_MAX; mx3 = in ? (unsigned)r[7] : 0;
+    q0 = in ? s->red_u[c.lane][0] : 0; q1 = in ? s->red_u[c.lane][1] : 0; q3 = in ? s->red_u[c.lane][2] : 0;
+    nf = (int)__reduce_add_sync(FULL, (unsigned)nf);
+    nact = (int)__reduce_add_sync(FULL, (unsigned)nact);
+    mn0 = __reduce_min_sync(FULL, mn0); mx0 = __reduce_max_sync(FULL, mx0);
+    mn1 = __reduce_min_sync(FULL, mn1); mx1 = __reduce_max_sync(FULL, mx1);
+    mn3 = __reduce_min_sync(FULL, mn3); mx3 = __reduce_max_sync(FULL, mx3);
+    for (int o = 16; o > 0; o >>= 1) {
+      q0 += __shfl_xor_sync(FULL, q0, o);
+      q1 += __shfl_xor_sync(FULL, q1, o);
+      q3 += __shfl_xor_sync(FULL, q3, o);
+    }
+    if (c.lane == 0) {
+      s->nf = nf;
+      s->nact = nact;
+      s->mn[0] = (int)mn0; s->mx[0] = (int)mx0;
+      s->mn[1] = (int)mn1; s->mx[1] = (int)mx1;
+      s->mn[2] = nact == nf ? 1 : 0; s->mx[2] = nact > 0 ? 1 : 0;  // f_u in {0,1}
+      s->mn[3] = (int)mn3; s->mx[3] = (int)mx3;
+      s->sq[0] = q0; s->sq[1] = q1; s->sq[2] = (unsigned long long)nact; s->sq[3] = q3;
+      s->c_feas += (unsigned long long)nf;
+    }
+  }
+  __syncthreads();
+}
+
+// ------------------------------------------------------------ TOPSIS --------
+// a5T: closeness of server u in FP32 (R12-R13): v_uc = w_c x_uc / ||x_c||;
+// Ed+ = ||v_u - A+||, Ed- = ||v_u - A-||, with A+ = max, A- = min over F (benefit
+// criteria, R3); differences taken in exact integers then scaled once.
+__device__ __forceinline__ float topsis32(const Scratch* s, int x0, int x1, int x2, int x3) {
+  float p0 = scaled_diff(s->sf[0], s->s2p23[0], s->mx[0] - x0);
+  float m0 = scaled_diff(s->sf[0], s->s2p23[0], x0 - s->mn[0]);
+  float p1 = scaled_diff(s->sf[1], s->s2p23[1], s->mx[1] - x1);
+  float m1 = scaled_diff(s->sf[1], s->s2p23[1], x1 - s->mn[1]);
+  float p2 = scaled_diff(s->sf[2], s->s2p23[2], s->mx[2] - x2);
+  float m2 = scaled_diff(s->sf[2], s->s2p23[2], x2 - s->mn[2]);
+  float p3 = scaled_diff(s->sf[3], s->s2p23[3], s->mx[3] - x3);
+  float m3 = scaled_diff(s->sf[3], s->s2p23[3], x3 - s->mn[3]);
+  float ep2 = fmaf(p3, p3, fmaf(p2, p2, fmaf(p1, p1, p0 * p0)));
+  float em2 = fmaf(m3, m3, fmaf(m2, m2, fmaf(m1, m1, m0 * m0)));
+  float ep = ep2 > 0.f ? ep2 * rsqrt_approx(ep2) : 0.f;
+  float em = em2 > 0.f ? em2 * rsqrt_approx(em2) : 0.f;
+  float den = ep + em;
+  return den > 0.f ? em * rcp_approx(den) : 0.f;
+}
+__device__ double topsis64(const Scratch* s, int x0, int x1, int x2, int x3) {
+  int x[4] = {x0, x1, x2, x3};
+  double ep = 0, em = 0;
+  for (int c = 0; c < 4; ++c) {
+    double p = s->sd[c] * (double)(s->mx[c] - x[c]);
+    double m = s->sd[c] * (double)(x[c] - s->mn[c]);
+    ep += p * p;
+    em += m * m;
+  }
+  ep = sqrt(ep);
+  em = sqrt(em);
+  return (ep + em) > 0 ? em / (ep + em) : 0.0;
+}
+
+template <bool WRITE_SCORES>
+__device__ void select_topsis(Ctx& c, float* scores_out) {
+  Scratch* s = c.s;
+  const int n = c.g.n;
+  const int* st = c.st;
+  if (c.tid == 0) {
+    for (int k = 0; k < 4; ++k) {
+      double N = sqrt((double)s->sq[k]);
+      double sd = N > 0 ? c.o.wd[k] / N : 0.0;
+      s->sd[k] = sd;
+      s->sf[k] = (float)sd;
+      s->s2p23[k] = (float)sd * 8388608.0f;
+    }
+  }
+  __syncthreads();
+  unsigned long long k1 = 0, k2 = 0;
+  for (int base = c.warp * 32; base < n; base += c.B) {
+    unsigned bits = c.maskw[base >> 5];
+    if (!((bits >> c.lane) & 1u)) continue;
+    int u = base + c.lane;
+    float r = topsis32(s, st[u], st[n + u], st[2 * n + u], st[3 * n + u]);
+    if (WRITE_SCORES) scores_out[u] = r;
+    unsigned long long key = ((unsigned long long)__float_as_uint(r) << 32) | (0xFFFFFFFFu - (unsigned)u);
+    top2_insert(k1, k2, key);
+  }
+  block_top2(c, k1, k2);
+  if (c.tid == 0) {
+    float s1 = __uint_as_float((unsigned)(s->key1 >> 32));
+    float s2 = __uint_as_float((unsigned)(s->key2 >> 32));
+    s->best = (int)(0xFFFFFFFFu - (unsigned)(s->key1 & 0xFFFFFFFFull));
+    s->amb = c.o.exact64 || (s->key2 != 0ull && s1 - s2 <= kTopsisDelta);
+  }
+  __syncthreads();
+  if (s->amb) {  // FP64 re-decision over the near-max candidates (R14)
+    float s1 = __uint_as_float((unsigned)(s->key1 >> 32));
+    float thr = c.o.exact64 ? -1.0f : s1 - 2.0f * kTopsisDelta;
+    double bv = -DBL_MAX;
+    int bj = -1;
+    for (int base = c.warp * 32; base < n; base += c.B) {
+      unsigned bits = c.maskw[base >> 5];
+      if (!((bits >> c.lane) & 1u)) continue;
+      int u = base + c.lane;
+      int x0 = st[u], x1 = st[n + u], x2 = st[2 * n + u], x3 = st[3 * n + u];
+      if (topsis32(s, x0, x1, x2, x3) < thr) continue;
+      double r = topsis64(s, x0, x1, x2, x3);
+      if (r > bv || (r == bv && u < bj)) { bv = r; bj = u; }
+    }
+    block_argmax64(c, bv, bj);
+    if (c.tid == 0) s->c_fp64 += 1;
+  }
+}
+
+// --------------------------------------------------------------- AHP --------
+// a5A + a6A (Eq. 9-10, readings R7-R11): per criterion c with lo < hi over
+// F, d_ij = 9 (x_i - x_j) / (hi - lo), a_ij = cell(d_ij); colsum_j = sum_i a_ij;
+// L2_c[i] = (1/nf) sum_j a_ij / colsum_j; PG[i] = sum_c L1[c] L2_c[i].  The pairwise
+// matrix is never stored: each thread streams rows of the compacted criteria.
+__device__ __forceinline__ float ahp_cell32(float d, int rule) {
+  float pos = rule ? 1.0f + d : d;
+  float neg = rcp_approx(rule ? 1.0f - d : -d);
+  return d > 0.f ? pos : (d < 0.f ? neg : 1.0f);
+}
+
+template <bool WRITE_SCORES>
+__device__ void select_ahp(Ctx& c, float* scores_out) {
+  Scratch* s = c.s;
+  const Geo& g = c.g;
+  const int n = g.n;
+  const int nf = s->nf;
+  const int cap = c.nfcap;
+  // compaction of F in server order
+  int wpt = (c.nW + c.B - 1) / c.B;
+  int w0 = c.tid * wpt, w1 = min(w0 + wpt, c.nW);
+  int cnt = 0;
+  for (int w = w0; w < w1; ++w) cnt += __popc(c.maskw[w]);
+  int pos = block_exscan(c, cnt);
+  for (int w = w0; w < w1; ++w) {
+    unsigned bits = c.maskw[w];
+    while (bits) {
+      int b = __ffs(bits) - 1;
+      bits &= bits - 1;
+      int u = w * 32 + b;
+      c.xs[0 * cap + pos] = (float)c.st[u];
+      c.xs[1 * cap + pos] = (float)c.st[n + u];
+      c.xs[2 * cap + pos] = (float)c.st[2 * n + u];
+      c.xs[3 * cap + pos] = (float)c.st[3 * n + u];
+      c.xid[pos] = u;
+      ++pos;
+    }
+  }
+  if (c.tid == 0) {
+    for (int k = 0; k < 4; ++k) {
+      int lo = s->mn[k], hi = s->mx[k];
+      s->ahp_const[k] = hi == lo;
+      double sc = hi > lo ? 9.0 / (double)(hi - lo) : 0.0;
+      s->ahp_scaled[k] = sc;
+      s->ahp_scale[k] = (float)sc;
+      if (hi > lo) s->c_pairs += (unsigned long long)nf * (unsigned long long)(nf - 1) / 2;
+    }
+  }
+  __syncthreads();
+  const int rule = c.o.ahp_rule;
+  // pass 1: 1 / column sums
+  for (int k = 0; k < 4; ++k) {
+    if (s->ahp_const[k]) continue;
+    const float* x = c.xs + k * cap;
+    const float sc = s->ahp_scale[k];
+    for (int j = c.tid; j < nf; j += c.B) {
+      float xj = x[j];
+      float outer = 0.f;
+      int i = 0;
+      for (; i + 32 <= nf; i += 32) {
+        float inner = 0.f;
+#pragma unroll 8
+        for (int t = 0; t < 32; ++t) inner += ahp_cell32((x[i + t] - xj) * sc, rule);
+        outer += inner;
+      }
+      float inner = 0.f;
+      for (; i < nf; ++i) inner += ahp_cell32((x[i] - xj) * sc, rule);
+      outer += inner;
+      c.wcol[k * cap + j] = rcp_approx(outer);
+    }
+  }
+  __syncthreads();
+  // pass 2: global priority
+  float a[4];
+  for (int k = 0; k < 4; ++k) a[k] = s->L1[k] * rcp_approx((float)nf);
+  unsigned long long k1 = 0, k2 = 0;
+  for (int i = c.tid; i < nf; i += c.B) {
+    float pgv = 0.f;
+    for (int k = 0; k < 4; ++k) {
+      if (s->ahp_const[k]) { pgv += a[k]; continue; }
+      const float* x = c.xs + k * cap;
+      const float* w = c.wcol + k * cap;
+      const float sc = s->ahp_scale[k];
+      float xi = x[i];
+      float outer = 0.f;
+      int j = 0;
+      for (; j + 32 <= nf; j += 32) {
+        float inner = 0.f;
+#pragma unroll 8
+        for (int t = 0; t < 32; ++t) inner = fmaf(ahp_cell32((xi - x[j + t]) * sc, rule), w[j + t], inner);
+        outer += inner;
+      }
+      float inner = 0.f;
+      for (; j < nf; ++j) inner = fmaf(ahp_cell32((xi - x[j]) * sc, rule), w[j], inner);
+      outer += inner;
+      pgv = fmaf(a[k], outer, pgv);
+    }
+    c.pg[i] = pgv;
+    int u = c.xid[i];
+    if (WRITE_SCORES) scores_out[u] = pgv;
+    unsigned long long key = ((unsigned long long)__float_as_uint(pgv) << 32) | (0xFFFFFFFFu - (unsigned)u);
+    top2_insert(k1, k2, key);
+  }
+  block_top2(c, k1, k2);
+  const float drel = ahp_delta_rel(nf);
+  if (c.tid == 0) {
+    float s1 = __uint_as_float((unsigned)(s->key1 >> 32));
+    float s2 = __uint_as_float((unsigned)(s->key2 >> 32));
+    s->best = (int)(0xFFFFFFFFu - (unsigned)(s->key1 & 0xFFFFFFFFull));
+    s->amb = c.o.exact64 || (s->key2 != 0ull && s2 >= s1 * (1.0f - drel));
+  }
+  __syncthreads();
+  if (s->amb) {  // FP64: exact column sums, then PG of the near-max candidates
+    for (int k = 0; k < 4; ++k) {
+      if (s->ahp_const[k]) continue;
+      const float* x = c.xs + k * cap;
+      const double sc = s->ahp_scaled[k];
+      for (int j = c.tid; j < nf; j += c.B) {
+        double xj = x[j], sum = 0;
+        for (int i = 0; i < nf; ++i) sum += ahp_cell64(((double)x[i] - xj) * sc, rule);
+        c.w64[k * cap + j] = 1.0 / sum;
+      }
+    }
+    __syncthreads();
+    float s1 = __uint_as_float((unsigned)(s->key1 >> 32));
+    float thr = c.o.exact64 ? -1.0f : s1 * (1.0f - 2.0f * drel);
+    double bv = -DBL_MAX;
+    int bj = -1;
+    for (int i = c.tid; i < nf; i += c.B) {
+      if (c.pg[i] < thr) continue;
+      double pgv = 0;
+      for (int k = 0; k < 4; ++k) {
+        if (s->ahp_const[k]) { pgv += s->L1d[k] / (double)nf; continue; }
+        const float* x = c.xs + k * cap;
+        const double* w = c.w64 + k * cap;
+        const double sc = s->ahp_scaled[k];
+        double xi = x[i], sum = 0;
+        for (int j = 0; j < nf; ++j) sum += ahp_cell64((xi - (double)x[j]) * sc, rule) * w[j];
+        pgv += s->L1d[k] * (sum / (double)nf);
+      }
+      int u = c.xid[i];
+      if (pgv > bv || (pgv == bv && u < bj)) { bv = pgv; bj = u; }
+    }
+    block_argmax64(c, bv, bj);
+    if (c.tid == 0) s->c_fp64 += 1;
+  }
+}
+
+// ------------------------------------------------------------- request ------
+// Build the flows of pod p (R17): every vlink between p and a placed pod q on server v
+// adds bw^min to D_v; flows sorted by ascending v.  Thread 0.
+__device__ void build_flows(Ctx& c, const ReqsDev& R, int r, int p) {
+  Scratch* s = c.s;
+  int v0 = R.voff[r];
+  int nflow = 0, sumD = 0;
+  for (int e = 0; e < s->nV; ++e) {
+    int a = s->cpod[R.src[v0 + e]], b = s->cpod[R.dst[v0 + e]];
+    int other = -1;
+    if (a == p && b != p && s->pod_srv[b] >= 0) other = b;
+    else if (b == p && a != p && s->pod_srv[a] >= 0) other = a;
+    if (other < 0) continue;
+    int v = s->pod_srv[other], D = R.bw_min[v0 + e];
+    int i = 0;
+    while (i < nflow && s->fv[i] < v) ++i;
+    if (i < nflow && s->fv[i] == v) {
+      s->fD[i] += D;
+    } else {
+      for (int t = nflow; t > i; --t) { s->fv[t] = s->fv[t - 1]; s->fD[t] = s->fD[t - 1]; }
+      s->fv[i] = v;
+      s->fD[i] = D;
+      ++nflow;
+    }
+    sumD += D;
+  }
+  s->nflow = nflow;
+  s->sumD = sumD;
+}
+
+// Per-flow-server feasibility when u = v_f (its own flow uses the host bus) and the
+// all-flows access check G.  All threads; after fabric_tables.
+__device__ void flow_server_ok(Ctx& c) {
+  Scratch* s = c.s;
+  const int* acc = c.st + 3 * c.g.n;
+  for (int f = c.tid; f < s->nflow; f += c.B) {
+    int u = s->fv[f];
+    bool ok = acc[u] >= s->sumD - s->fD[f];
+    for (int h = 0; h < s->nflow; ++h)
+      if (h != f && acc[s->fv[h]] < s->fD[h]) ok = false;
+    unsigned e = div_h((unsigned)u, c.g.magic_h);
+    if ((c.edgebad[e >> 5] >> (e & 31)) & 1u) ok = false;
+    s->fok[f] = ok;
+    s->fexcl[f] = 0;
+    atomicOr(&c.special[u >> 5], 1u << (u & 31));
+  }
+  if (c.tid == 0) {
+    int G = 1;
+    for (int h = 0; h < s->nflow; ++h)
+      if (acc[s->fv[h]] < s->fD[h]) G = 0;
+    s->G = G;
+  }
+}
+
+__device__ void clear_bitmaps(Ctx& c) {
+  for (int w = c.tid; w < c.nW; w += c.B) c.special[w] = 0u;
+  for (int w = c.tid; w < c.nEW; w += c.B) c.edgebad[w] = 0u;
+}
+
+// Commit of the chosen server for pod p (a8; Eq. 4-5, R16-R18).  Warp 0.
+__device__ void commit(Ctx& c, const ReqsDev& R, int r, int p) {
+  Scratch* s = c.s;
+  const Geo& g = c.g;
+  const int n = g.n;
+  int u = s->best;
+  if (c.lane == 0) {
+    s->log_mark = s->log_n;
+    st_set(c, u, c.st[u] - s->dc);
+    st_set(c, n + u, c.st[n + u] - s->dr);
+    st_set(c, 2 * n + u, 1);
+  }
+  __syncwarp();
+  int fail = 0;
+  for (int f = 0; f < s->nflow; ++f) {
+    int v = s->fv[f], D = s->fD[f];
+    if (v == u) {
+      if (c.lane == 0) s->fpath[f] = -1;
+      continue;
+    }
+    int2 wp = widest_path_warp(c, u, v);
+    if (c.lane == 0) {
+      int bott = min(min(c.st[3 * n + u], c.st[3 * n + v]), wp.y);
+      if (bott < D) {
+        fail = 1;
+      } else {
+        st_set(c, 3 * n + u, c.st[3 * n + u] - D);
+        st_set(c, 3 * n + v, c.st[3 * n + v] - D);
+        int off[4];
+        int m = path_links(g, u, v, wp.x, off);
+        for (int t = 0; t < m; ++t) st_set(c, off[t], c.st[off[t]] - D);
+        s->fpath[f] = wp.x;
+      }
+    }
+    fail = __shfl_sync(FULL, fail, 0);
+    if (fail) break;
+  }
+  if (c.lane == 0) {
+    if (fail) {  // R18: undo this pod's commit, exclude u, redo the pod step
+      undo_to(c, s->log_mark);
+      int f = -1;
+      for (int i = 0; i < s->nflow; ++i) if (s->fv[i] == u) f = i;
+      if (f >= 0) s->fexcl[f] = 1;
+      c.special[u >> 5] |= 1u << (u & 31);
+      s->fail = 1;
+      s->c_retries += 1;
+    } else {
+      s->fail = 0;
+      s->pod_srv[p] = u;
+      int v0 = R.voff[r];
+      for (int e = 0; e < s->nV; ++e) {
+        int a = s->cpod[R.src[v0 + e]], b = s->cpod[R.dst[v0 + e]];
+        int other = -1;
+        if (a == p && b != p && b < p) other = b;
+        else if (b == p && a != p && a < p) other = a;
+        if (other < 0) continue;
+        int v = s->pod_srv[other];
+        int fp = -1;
+        for (int i = 0; i < s->nflow; ++i) if (s->fv[i] == v) fp = s->fpath[i];
+        s->vpath[e] = fp;
+      }
+    }
+  }
+}
+
+// Outputs of a non-accepted request (status 0 or -1).  All threads.
+__device__ void write_rejected(Ctx& c, const ReqsDev& R, const OutDev& O, int r, int status) {
+  int c0 = R.coff[r], nC = R.coff[r + 1] - c0;
+  int v0 = R.voff[r], nV = R.voff[r + 1] - v0;
+  for (int i = c.tid; i < nC; i += c.B) {
+    O.server[c0 + i] = -1;
+    O.cpu_a[c0 + i] = 0;
+    O.ram_a[c0 + i] = 0;
+  }
+  for (int e = c.tid; e < nV; e += c.B) {
+    O.bw_a[v0 + e] = 0;
+    O.path[v0 + e] = -1;
+  }
+  if (c.tid == 0) O.status[r] = status;
+}
+
+// One request (SURVEY §8(c) oracle algorithm, steps 1-3).  All threads.  On return the
+// state holds the accepted placement (sequential) or is restored (batch: keep=false).
+template <int METHOD>
+__device__ void run_request(Ctx& c, const ReqsDev& R, const OutDev& O, int r, bool keep) {
+  Scratch* s = c.s;
+  const Geo& g = c.g;
+  const int n = g.n;
+  if (c.tid == 0) {
+    int c0 = R.coff[r], v0 = R.voff[r];
+    int nC = R.coff[r + 1] - c0, nV = R.voff[r + 1] - v0;
+    int bad = validate_request(nC, nV, R.cpu_min + c0, R.cpu_max + c0, R.ram_min + c0, R.ram_max + c0,
+                               R.pod_of + c0, R.src + v0, R.dst + v0, R.bw_min + v0, R.bw_max + v0);
+    s->req_ok = bad == 0;
+    s->nC = nC;
+    s->nV = nV;
+    s->log_n = 0;
+    if (bad) {
+      s->c_invalid += 1;
+    } else {
+      int P = 0;
+      for (int i = 0; i < nC; ++i) {
+        int p = R.pod_of[c0 + i];
+        s->cpod[i] = p;
+        P = max(P, p + 1);
+      }
+      s->P = P;
+      for (int p = 0; p < P; ++p) { s->pod_cpu[p] = 0; s->pod_ram[p] = 0; s->pod_srv[p] = -1; }
+      for (int i = 0; i < nC; ++i) {
+        s->pod_cpu[s->cpod[i]] += R.cpu_min[c0 + i];
+        s->pod_ram[s->cpod[i]] += R.ram_min[c0 + i];
+      }
+      for (int e = 0; e < nV; ++e) s->vpath[e] = -1;
+    }
+  }
+  __syncthreads();
+  if (!s->req_ok) {
+    write_rejected(c, R, O, r, -1);
+    __syncthreads();
+    return;
+  }
+  const int P = s->P;
+  for (int p = 0; p < P; ++p) {
+    if (c.tid == 0) {
+      s->p = p;
+      s->dc = s->pod_cpu[p];
+      s->dr = s->pod_ram[p];
+      build_flows(c, R, r, p);
+    }
+    clear_bitmaps(c);
+    __syncthreads();
+    if (c.o.path_filter && s->nflow > 0) fabric_tables(c);
+    flow_server_ok(c);
+    __syncthreads();
+    for (;;) {
+      pass_filter<false>(c, nullptr, nullptr);
+      if (c.tid == 0) s->c_steps += 1;
+      if (s->nf == 0) {  // R20: reject the whole request atomically
+        if (c.tid == 0) undo_to(c, 0);
+        __syncthreads();
+        write_rejected(c, R, O, r, 0);
+        __syncthreads();
+        return;
+      }
+      if (METHOD == 1) select_topsis<false>(c, nullptr);
+      else select_ahp<false>(c, nullptr);
+      if (c.warp == 0) commit(c, R, r, p);
+      __syncthreads();
+      if (!s->fail) break;
+    }
+  }
+  // a9: top-up (R19) in container order, then vlink order; emit the placement.
+  if (c.tid == 0) {
+    int c0 = R.coff[r], v0 = R.voff[r];
+    for (int i = 0; i < s->nC; ++i) {
+      int u = s->pod_srv[s->cpod[i]];
+      int cmin = R.cpu_min[c0 + i], rmin = R.ram_min[c0 + i];
+      int ec = min(R.cpu_max[c0 + i] - cmin, c.st[u]);
+      int er = min(R.ram_max[c0 + i] - rmin, c.st[n + u]);
+      if (ec) st_set(c, u, c.st[u] - ec);
+      if (er) st_set(c, n + u, c.st[n + u] - er);
+      O.server[c0 + i] = u;
+      O.cpu_a[c0 + i] = cmin + ec;
+      O.ram_a[c0 + i] = rmin + er;
+    }
+    for (int e = 0; e < s->nV; ++e) {
+      int us = s->pod_srv[s->cpod[R.src[v0 + e]]], ud = s->pod_srv[s->cpod[R.dst[v0 + e]]];
+      int bmin = R.bw_min[v0 + e], bmax = R.bw_max[v0 + e];
+      if (us == ud) {
+        O.bw_a[v0 + e] = bmax;
+        O.path[v0 + e] = -1;
+        continue;
+      }
+      int pid = s->vpath[e];
+      int off[4];
+      int m = path_links(g, us, ud, pid, off);
+      int resid = min(c.st[3 * n + us], c.st[3 * n + ud]);
+      for (int t = 0; t < m; ++t) resid = min(resid, c.st[off[t]]);
+      int extra = min(bmax - bmin, resid);
+      if (extra) {
+        st_set(c, 3 * n + us, c.st[3 * n + us] - extra);
+        st_set(c, 3 * n + ud, c.st[3 * n + ud] - extra);
+        for (int t = 0; t < m; ++t) st_set(c, off[t], c.st[off[t]] - extra);
+      }
+      O.bw_a[v0 + e] = bmin + extra;
+      O.path[v0 + e] = pid;
+    }
+    O.status[r] = 1;
+    if (!keep) undo_to(c, 0);
+  }
+  __syncthreads();
+}
+
+// ------------------------------------------------------------- kernels ------
+__device__ void init_ctx(Ctx& c, const Geo& g, const Opt& o, Scratch* s) {
+  c.g = g;
+  c.o = o;
+  c.s = s;
+  c.tid = threadIdx.x;
+  c.B = blockDim.x;
+  c.NW = blockDim.x >> 5;
+  c.lane = threadIdx.x & 31;
+  c.warp = threadIdx.x >> 5;
+  c.nW = (g.n + 31) >> 5;
+  c.nEW = (g.E + 31) >> 5;
+  if (c.tid == 0) {
+    s->c_steps = s->c_retries = s->c_fp64 = s->c_invalid = s->c_feas = s->c_pairs = 0;
+    if (o.method == 0) {
+      double L1[4];
+      ahp_l1_dev(o, L1);
+      for (int k = 0; k < 4; ++k) { s->L1d[k] = L1[k]; s->L1[k] = (float)L1[k]; }
+    }
+  }
+}
+
+__device__ void flush_stats(Ctx& c, unsigned long long* stats) {
+  if (c.tid == 0) {
+    Scratch* s = c.s;
+    if (s->c_steps) atomicAdd(&stats[ST_POD_STEPS], s->c_steps);
+    if (s->c_retries) atomicAdd(&stats[ST_RETRIES], s->c_retries);
+    if (s->c_fp64) atomicAdd(&stats[ST_FP64], s->c_fp64);
+    if (s->c_invalid) atomicAdd(&stats[ST_INVALID], s->c_invalid);
+    if (s->c_feas) atomicAdd(&stats[ST_FEAS], s->c_feas);
+    if (s->c_pairs) atomicAdd(&stats[ST_PAIRS], s->c_pairs);
+  }
+}
+
+// dynamic shared memory layout of k_batch:
+//   state words (6n ints) | maskw[nW] | special[nW] | edgebad[nEW] | AHP arrays
+__host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
+
+template <int METHOD>
+__global__ void __launch_bounds__(1024) k_batch(Geo g, Opt o, const int* __restrict__ snap, ReqsDev R,
+                                                OutDev O, int2* ulog, double* w64, int* next,
+                                                unsigned long long* stats) {
+  extern __shared__ __align__(16) unsigned char dyn[];
+  __shared__ Scratch s;
+  __shared__ __align__(8) unsigned long long mbar;
+  Ctx c;
+  init_ctx(c, g, o, &s);
+  const int nW = c.nW, nEW = c.nEW, n = g.n;
+  size_t off = 0;
+  c.st = reinterpret_cast<int*>(dyn);
+  off = align16(off + sizeof(int) * (size_t)g.words());
+  c.maskw = reinterpret_cast<unsigned*>(dyn + off);
+  off = align16(off + sizeof(unsigned) * nW);
+  c.special = reinterpret_cast<unsigned*>(dyn + off);
+  off = align16(off + sizeof(unsigned) * nW);
+  c.edgebad = reinterpret_cast<unsigned*>(dyn + off);
+  off = align16(off + sizeof(unsigned) * nEW);
+  c.nfcap = n;
+  if (METHOD == 0) {
+    c.xs = reinterpret_cast<float*>(dyn + off);
+    off = align16(off + sizeof(float) * 4 * (size_t)n);
+    c.xid = reinterpret_cast<int*>(dyn + off);
+    off = align16(off + sizeof(int) * (size_t)n);
+    c.wcol = reinterpret_cast<float*>(dyn + off);
+    off = align16(off + sizeof(float) * 4 * (size_t)n);
+    c.pg = reinterpret_cast<float*>(dyn + off);
+    c.w64 = w64 + (size_t)blockIdx.x * 4 * n;
+  }
+  c.snap = snap;
+  c.ulog = ulog + (size_t)blockIdx.x * ULOG_CAP;
+
+  // a0: the snapshot into shared memory with TMA bulk copies (cp.async.bulk).
+  const unsigned bytes = (unsigned)(sizeof(int) * (size_t)g.words());  // 24 n, a multiple of 16
+  if (c.tid == 0) {
+    unsigned mb = smem_u32(&mbar);
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes) : "memory");
+    const unsigned chunk = 32768;
+    for (unsigned o2 = 0; o2 < bytes; o2 += chunk) {
+      unsigned sz = bytes - o2 < chunk ? bytes - o2 : chunk;
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              smem_u32(dyn + o2)),
+          "l"(reinterpret_cast<const unsigned char*>(snap) + o2), "r"(sz), "r"(mb)
+          : "memory");
+    }
+  }
+  __syncthreads();
+  {
+    unsigned mb = smem_u32(&mbar);
+    asm volatile(
+        "{\n .reg .pred P1;\n WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n"
+        " @!P1 bra WAIT_%=;\n}" ::"r"(mb)
+        : "memory");
+  }
+  for (int w = c.tid; w < nW; w += c.B) { c.maskw[w] = 0u; c.special[w] = 0u; }
+  for (int w = c.tid; w < nEW; w += c.B) c.edgebad[w] = 0u;
+  __syncthreads();
+
+  for (;;) {
+    if (c.tid == 0) s.next_req = atomicAdd(next, 1);
+    __syncthreads();
+    int r = s.next_req;
+    __syncthreads();
+    if (r >= R.n) break;
+    run_request<METHOD>(c, R, O, r, false);
+  }
+  flush_stats(c, stats);
+}
+
+template <int METHOD>
+__global__ void __launch_bounds__(1024) k_sequential(Geo g, Opt o, int* state, ReqsDev R, OutDev O, int2* ulog,
+                                                     float* ahp_ws, double* w64, unsigned long long* stats) {
+  extern __shared__ __align__(16) unsigned char dyn[];
+  __shared__ Scratch s;
+  Ctx c;
+  init_ctx(c, g, o, &s);
+  size_t off = 0;
+  c.maskw = reinterpret_cast<unsigned*>(dyn + off);
+  off = align16(off + sizeof(unsigned) * c.nW);
+  c.special = reinterpret_cast<unsigned*>(dyn + off);
+  off = align16(off + sizeof(unsigned) * c.nW);
+  c.edgebad = reinterpret_cast<unsigned*>(dyn + off);
+  c.st = state;
+  c.snap = state;
+  c.ulog = ulog;
+  c.nfcap = g.n;
+  if (METHOD == 0) {
+    c.xs = ahp_ws;
+    c.xid = reinterpret_cast<int*>(ahp_ws + 4 * (size_t)g.n);
+    c.wcol = ahp_ws + 5 * (size_t)g.n;
+    c.pg = ahp_ws + 9 * (size_t)g.n;
+    c.w64 = w64;
+  }
+  for (int w = c.tid; w < c.nW; w += c.B) { c.maskw[w] = 0u; c.special[w] = 0u; }
+  for (int w = c.tid; w < c.nEW; w += c.B) c.edgebad[w] = 0u;
+  __syncthreads();
+  for (int r = 0; r < R.n; ++r) run_request<METHOD>(c, R, O, r, true);
+  flush_stats(c, stats);
+}
+
+template <int METHOD>
+__global__ void __launch_bounds__(1024) k_rank(Geo g, Opt o, int* state, QueryDev q, float* ahp_ws, double* w64,
+                                               unsigned long long* stats) {
+  extern __shared__ __align__(16) unsigned char dyn[];
+  __shared__ Scratch s;
+  Ctx c;
+  init_ctx(c, g, o, &s);
+  size_t off = 0;
+  c.maskw = reinterpret_cast<unsigned*>(dyn + off);
+  off = align16(off + sizeof(unsigned) * c.nW);
+  c.special = reinterpret_cast<unsigned*>(dyn + off);
+  off = align16(off + sizeof(unsigned) * c.nW);
+  c.edgebad = reinterpret_cast<unsigned*>(dyn + off);
+  c.st = state;
+  c.snap = state;
+  c.nfcap = g.n;
+  if (METHOD == 0) {
+    c.xs = ahp_ws;
+    c.xid = reinterpret_cast<int*>(ahp_ws + 4 * (size_t)g.n);
+    c.wcol = ahp_ws + 5 * (size_t)g.n;
+    c.pg = ahp_ws + 9 * (size_t)g.n;
+    c.w64 = w64;
+  }
+  clear_bitmaps(c);
+  if (c.tid == 0) {
+    s.dc = q.dc;
+    s.dr = q.dr;
+    s.nflow = q.nflow;
+    int sumD = 0;
+    for (int f = 0; f < q.nflow; ++f) { s.fv[f] = q.fv[f]; s.fD[f] = q.fD[f]; sumD += q.fD[f]; }
+    s.sumD = sumD;
+  }
+  __syncthreads();
+  if (o.path_filter && s.nflow > 0) fabric_tables(c);
+  flow_server_ok(c);
+  __syncthreads();
+  // excluded servers (R18)
+  for (int i = c.tid; i < q.nex; i += c.B) {
+    int u = q.ex[i];
+    atomicOr(&c.special[u >> 5], 1u << (u & 31));
+    for (int f = 0; f < s.nflow; ++f)
+      if (s.fv[f] == u) s.fexcl[f] = 1;
+  }
+  __syncthreads();
+  bool wm = q.mask != nullptr && q.scores != nullptr;
+  if (wm) pass_filter<true>(c, q.mask, q.scores);
+  else pass_filter<false>(c, nullptr, nullptr);
+  if (c.tid == 0) s.c_steps += 1;
+  if (s.nf == 0) {
+    if (c.tid == 0) *q.best = -1;
+  } else {
+    if (METHOD == 1) {
+      if (wm) select_topsis<true>(c, q.scores);
+      else select_topsis<false>(c, nullptr);
+    } else {
+      if (wm) select_ahp<true>(c, q.scores);
+      else select_ahp<false>(c, nullptr);
+    }
+    if (c.tid == 0) *q.best = s.best;
+  }
+  flush_stats(c, stats);
+}
+
+__global__ void k_validate(ReqsDev R, int* status, unsigned long long* stats) {
+  int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= R.n) return;
+  int c0 = R.coff[r], v0 = R.voff[r];
+  int bad = validate_request(R.coff[r + 1] - c0, R.voff[r + 1] - v0, R.cpu_min + c0, R.cpu_max + c0,
+                             R.ram_min + c0, R.ram_max + c0, R.pod_of + c0, R.src + v0, R.dst + v0,
+                             R.bw_min + v0, R.bw_max + v0);
+  status[r] = bad ? -1 : 0;
+  if (bad) atomicAdd(&stats[ST_INVALID], 1ull);
+}
+
+// --------------------------------------------------------------- host -------
+int batch_block_size(const Geo& g) {
+  int b = ((g.n / 8 + 31) / 32) * 32;  // about 8 servers per thread
+  if (b < 64) b = 64;
+  if (b > 1024) b = 1024;
+  return b;
+}
+
+static size_t bitmap_bytes(const Geo& g) {
+  int nW = (g.n + 31) / 32, nEW = (g.E + 31) / 32;
+  return align16(4 * (size_t)nW) * 2 + align16(4 * (size_t)nEW);
+}
+
+size_t batch_smem_bytes(const Geo& g, int method) {
+  size_t b = align16(sizeof(int) * (size_t)g.words()) + bitmap_bytes(g);
+  if (method == 0) b += align16(16 * (size_t)g.n) * 2 + align16(4 * (size_t)g.n) * 2;
+  int dev = 0, optin = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if (b + sizeof(Scratch) + 64 > (size_t)optin) return 0;
+  return b;
+}
+
+cudaError_t batch_occupancy(const Geo& g, int method, int* blocks_per_sm) {
+  size_t smem = batch_smem_bytes(g, method);
+  if (!smem) { *blocks_per_sm = 0; return cudaSuccess; }
+  int B = batch_block_size(g);
+  cudaError_t e;
+  if (method == 1) {
+    e = cudaFuncSetAttribute(k_batch<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_batch<1>, B, smem);
+  }
+  e = cudaFuncSetAttribute(k_batch<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_batch<0>, B, smem);
+}
+
+cudaError_t launch_batch(const Geo& g, const Opt& o, const int* d_state, const ReqsDev& R, const OutDev& O,
+                         int2* ulog, double* w64, int* next, unsigned long long* stats, int grid,
+                         cudaStream_t st) {
+  size_t smem = batch_smem_bytes(g, o.method);
+  int B = batch_block_size(g);
+  if (o.method == 1) {
+    cudaFuncSetAttribute(k_batch<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_batch<1><<<grid, B, smem, st>>>(g, o, d_state, R, O, ulog, w64, next, stats);
+  } else {
+    cudaFuncSetAttribute(k_batch<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_batch<0><<<grid, B, smem, st>>>(g, o, d_state, R, O, ulog, w64, next, stats);
+  }
+  return cudaGetLastError();
+}
+
+static int single_block_size(const Geo& g) {
+  int b = ((g.n / 4 + 31) / 32) * 32;
+  if (b < 64) b = 64;
+  if (b > 1024) b = 1024;
+  return b;
+}
+
+cudaError_t launch_sequential(const Geo& g, const Opt& o, int* d_state, const ReqsDev& R, const OutDev& O,
+                              int2* ulog, float* ahp_ws, double* w64, unsigned long long* stats,
+                              cudaStream_t st) {
+  size_t smem = bitmap_bytes(g);
+  int B = single_block_size(g);
+  if (o.method == 1) k_sequential<1><<<1, B, smem, st>>>(g, o, d_state, R, O, ulog, ahp_ws, w64, stats);
+  else k_sequential<0><<<1, B, smem, st>>>(g, o, d_state, R, O, ulog, ahp_ws, w64, stats);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rank(const Geo& g, const Opt& o, int* d_state, const QueryDev& q, float* ahp_ws, double* w64,
+                        unsigned long long* stats, cudaStream_t st) {
+  size_t smem = bitmap_bytes(g);
+  int B = single_block_size(g);
+  if (o.method == 1) k_rank<1><<<1, B, smem, st>>>(g, o, d_state, q, ahp_ws, w64, stats);
+  else k_rank<0><<<1, B, smem, st>>>(g, o, d_state, q, ahp_ws, w64, stats);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_validate(const ReqsDev& R, int* status, unsigned long long* stats, cudaStream_t st) {
+  if (R.n <= 0) return cudaSuccess;
+  k_validate<<<(R.n + 255) / 256, 256, 0, st>>>(R, status, stats);
+  return cudaGetLastError();
+}
+
+}  // namespace nacs

@@ -1,0 +1,265 @@
+"""Thin ctypes binding of libnacs (include/nacs.h): argument marshalling only.
+
+Every step of the ranking and placement runs in the CUDA kernels of libnacs.so; this
+module converts numpy arrays / torch tensors to pointers and back.  There is no
+fallback: if libnacs.so is missing or no CUDA device is present the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libnacs.so")
+
+NACS_OK, NACS_EINVAL, NACS_ENOMEM, NACS_ECUDA, NACS_ENCCL, NACS_ENOTOPO, NACS_ETOOBIG = range(7)
+STATUS_NAMES = ["OK", "EINVAL", "ENOMEM", "ECUDA", "ENCCL", "ENOTOPO", "ETOOBIG"]
+NACS_AHP, NACS_TOPSIS = 0, 1
+NACS_DEVICE_PTRS, NACS_ASYNC, NACS_EXACT_FP64 = 1, 2, 4
+MAX_CONTAINERS, MAX_VLINKS, MAX_K = 128, 512, 64
+
+# Table 4: weights over (CPU, RAM, Fragmentation, Bandwidth)
+SCHEMAS = {"flat": (0.25, 0.25, 0.25, 0.25),
+           "clustering": (0.17, 0.17, 0.5, 0.16),
+           "network": (0.17, 0.17, 0.16, 0.5)}
+METHODS = {"ahp": NACS_AHP, "topsis": NACS_TOPSIS}
+
+P32 = C.POINTER(C.c_int32)
+PU8 = C.POINTER(C.c_uint8)
+PF = C.POINTER(C.c_float)
+
+
+class Topology(C.Structure):
+    _fields_ = [("k", C.c_int32), ("cpu_cap", C.c_int32), ("ram_cap", C.c_int32), ("link_cap", C.c_int32),
+                ("cpu_res", C.c_void_p), ("ram_res", C.c_void_p), ("active", C.c_void_p),
+                ("link_res", C.c_void_p)]
+
+
+class PodQuery(C.Structure):
+    _fields_ = [("cpu_demand", C.c_int32), ("ram_demand", C.c_int32), ("n_flows", C.c_int32),
+                ("flow_server", C.c_void_p), ("flow_bw", C.c_void_p), ("n_excluded", C.c_int32),
+                ("excluded", C.c_void_p)]
+
+
+class Requests(C.Structure):
+    _fields_ = [("n_requests", C.c_int32), ("container_off", C.c_void_p), ("cpu_min", C.c_void_p),
+                ("cpu_max", C.c_void_p), ("ram_min", C.c_void_p), ("ram_max", C.c_void_p),
+                ("pod_of", C.c_void_p), ("vlink_off", C.c_void_p), ("vl_src", C.c_void_p),
+                ("vl_dst", C.c_void_p), ("bw_min", C.c_void_p), ("bw_max", C.c_void_p)]
+
+
+class Placements(C.Structure):
+    _fields_ = [("status", C.c_void_p), ("server_of_container", C.c_void_p), ("cpu_alloc", C.c_void_p),
+                ("ram_alloc", C.c_void_p), ("bw_alloc", C.c_void_p), ("path_of_vlink", C.c_void_p)]
+
+
+class Options(C.Structure):
+    _fields_ = [("method", C.c_int), ("weights", C.c_double * 4), ("ahp_rule", C.c_int32),
+                ("l1_mode", C.c_int32), ("path_filter", C.c_int32), ("flags", C.c_uint32)]
+
+
+class Stats(C.Structure):
+    _fields_ = [("pod_steps", C.c_int64), ("servers_ranked", C.c_int64), ("retries", C.c_int64),
+                ("fp64_decisions", C.c_int64), ("invalid", C.c_int64), ("feasible", C.c_int64),
+                ("ahp_pairs", C.c_int64)]
+
+
+EXPORTS = ["nacs_create", "nacs_destroy", "nacs_load_topology", "nacs_read_topology", "nacs_rank_ahp",
+           "nacs_rank_topsis", "nacs_schedule_request", "nacs_schedule_batch", "nacs_last_stats",
+           "nacs_last_error"]
+
+_lib = None
+
+
+def lib():
+    """Load libnacs.so (raises if it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_1909_07673_b200.build` "
+                              "(there is no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        vp = C.c_void_p
+        L.nacs_create.argtypes = [C.POINTER(vp), C.c_int, vp]
+        L.nacs_destroy.argtypes = [vp]
+        L.nacs_destroy.restype = None
+        L.nacs_load_topology.argtypes = [vp, C.POINTER(Topology)]
+        L.nacs_read_topology.argtypes = [vp, vp, vp, vp, vp]
+        for f in (L.nacs_rank_ahp, L.nacs_rank_topsis):
+            f.argtypes = [vp, C.POINTER(Options), C.POINTER(PodQuery), vp, vp, vp]
+        for f in (L.nacs_schedule_request, L.nacs_schedule_batch):
+            f.argtypes = [vp, C.POINTER(Options), C.POINTER(Requests), C.POINTER(Placements)]
+        L.nacs_last_stats.argtypes = [vp, C.POINTER(Stats)]
+        L.nacs_last_error.argtypes = [vp]
+        L.nacs_last_error.restype = C.c_char_p
+        for name in EXPORTS:
+            if name not in ("nacs_destroy", "nacs_last_error"):
+                getattr(L, name).restype = C.c_int
+        _lib = L
+    return _lib
+
+
+class NacsError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS_NAMES[status] if 0 <= status < 7 else status}: {msg}")
+        self.status = status
+
+
+def _np_ptr(a):
+    return None if a is None else a.ctypes.data
+
+
+def _is_torch(a):
+    return type(a).__module__.startswith("torch")
+
+
+def _ptr(a):
+    if a is None:
+        return None
+    if _is_torch(a):
+        return a.data_ptr()
+    return a.ctypes.data
+
+
+def _i32(a):
+    return np.ascontiguousarray(a, dtype=np.int32)
+
+
+REQ_KEYS = ("container_off", "cpu_min", "cpu_max", "ram_min", "ram_max", "pod_of", "vlink_off", "vl_src",
+            "vl_dst", "bw_min", "bw_max")
+OUT_KEYS = ("status", "server_of_container", "cpu_alloc", "ram_alloc", "bw_alloc", "path_of_vlink")
+
+
+class Context:
+    """One libnacs context on one CUDA device (one per process / rank)."""
+
+    def __init__(self, device: int = 0, stream=None):
+        self._lib = lib()
+        self._h = C.c_void_p()
+        handle = None
+        if stream is not None:
+            handle = stream if isinstance(stream, int) else stream.cuda_stream
+        st = self._lib.nacs_create(C.byref(self._h), device, handle)
+        if st != NACS_OK:
+            raise NacsError(st, "nacs_create failed (no CUDA device?)")
+        self.device = device
+        self.k = None
+
+    def close(self):
+        if self._h:
+            self._lib.nacs_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, st):
+        if st != NACS_OK:
+            raise NacsError(st, self._lib.nacs_last_error(self._h).decode())
+
+    # ------------------------------------------------------------- topology --
+    def load_topology(self, snap: dict):
+        k = int(snap["k"])
+        keep = [None if snap.get(key) is None else np.ascontiguousarray(snap[key], dtype=dt)
+                for key, dt in (("cpu_res", np.int32), ("ram_res", np.int32), ("active", np.uint8),
+                                ("link_res", np.int32))]
+        t = Topology(k, int(snap["cpu_cap"]), int(snap["ram_cap"]), int(snap["link_cap"]),
+                     *[_np_ptr(a) for a in keep])
+        self._check(self._lib.nacs_load_topology(self._h, C.byref(t)))
+        self.k = k
+        self.n = k ** 3 // 4
+        self.L = 3 * self.n
+
+    def read_topology(self) -> dict:
+        cpu = np.zeros(self.n, np.int32)
+        ram = np.zeros(self.n, np.int32)
+        act = np.zeros(self.n, np.uint8)
+        link = np.zeros(self.L, np.int32)
+        self._check(self._lib.nacs_read_topology(self._h, _np_ptr(cpu), _np_ptr(ram), _np_ptr(act),
+                                                 _np_ptr(link)))
+        return dict(cpu_res=cpu, ram_res=ram, active=act, link_res=link)
+
+    # -------------------------------------------------------------- options --
+    @staticmethod
+    def options(method, weights, ahp_rule=0, l1_mode=0, path_filter=1, flags=0) -> Options:
+        if isinstance(weights, str):
+            weights = SCHEMAS[weights]
+        m = METHODS[method] if isinstance(method, str) else int(method)
+        return Options(m, (C.c_double * 4)(*[float(w) for w in weights]), ahp_rule, l1_mode, path_filter, flags)
+
+    # ---------------------------------------------------------------- rank ---
+    def rank(self, method, weights, dem_cpu, dem_ram, flows=(), excluded=(), exact64=False, **kw) -> dict:
+        """One pod step on the current state: returns mask (uint8[n]), scores (float32[n]), best."""
+        o = self.options(method, weights, flags=NACS_EXACT_FP64 if exact64 else 0, **kw)
+        fv = _i32([f[0] for f in flows]) if len(flows) else np.zeros(1, np.int32)
+        fd = _i32([f[1] for f in flows]) if len(flows) else np.zeros(1, np.int32)
+        ex = _i32(list(excluded)) if len(excluded) else np.zeros(1, np.int32)
+        q = PodQuery(int(dem_cpu), int(dem_ram), len(flows), _np_ptr(fv), _np_ptr(fd), len(excluded), _np_ptr(ex))
+        mask = np.zeros(self.n, np.uint8)
+        scores = np.zeros(self.n, np.float32)
+        best = np.zeros(1, np.int32)
+        fn = self._lib.nacs_rank_ahp if o.method == NACS_AHP else self._lib.nacs_rank_topsis
+        self._check(fn(self._h, C.byref(o), C.byref(q), _np_ptr(mask), _np_ptr(scores), _np_ptr(best)))
+        return dict(mask=mask, scores=scores, best=int(best[0]))
+
+    # ------------------------------------------------------------ schedule ---
+    def _requests(self, reqs: dict):
+        arrs = []
+        dev = None
+        for key in REQ_KEYS:
+            a = reqs[key]
+            if _is_torch(a):
+                dev = True if dev in (None, True) else "mixed"
+                arrs.append(a)
+            else:
+                dev = False if dev in (None, False) else "mixed"
+                arrs.append(_i32(a))
+        if dev == "mixed":
+            raise ValueError("request arrays must be all host or all device")
+        r = Requests(int(reqs["n_requests"]), *[_ptr(a) for a in arrs])
+        return r, arrs, bool(dev)
+
+    def _alloc_out(self, reqs: dict, device: bool):
+        R = int(reqs["n_requests"])
+        Cn = int(reqs["container_off"][-1])
+        Vn = int(reqs["vlink_off"][-1])
+        sizes = dict(status=R, server_of_container=Cn, cpu_alloc=Cn, ram_alloc=Cn, bw_alloc=Vn, path_of_vlink=Vn)
+        if device:
+            import torch
+            out = {k: torch.empty(max(v, 1), dtype=torch.int32, device=f"cuda:{self.device}") for k, v in sizes.items()}
+        else:
+            out = {k: np.zeros(max(v, 1), np.int32) for k, v in sizes.items()}
+        return out, sizes
+
+    def _schedule(self, fn, reqs, method, weights, out=None, flags=0, **kw) -> dict:
+        r, keep, dev = self._requests(reqs)
+        if dev:
+            flags |= NACS_DEVICE_PTRS
+        o = self.options(method, weights, flags=flags, **kw)
+        sizes = None
+        if out is None:
+            out, sizes = self._alloc_out(reqs, dev)
+        p = Placements(*[_ptr(out[k]) for k in OUT_KEYS])
+        self._check(fn(self._h, C.byref(o), C.byref(r), C.byref(p)))
+        del keep
+        if sizes is not None:
+            out = {k: out[k][: sizes[k]] for k in OUT_KEYS}
+        return out
+
+    def schedule_request(self, reqs: dict, method, weights, out=None, flags=0, **kw) -> dict:
+        """Requests in order against the live state; accepted requests stay committed."""
+        return self._schedule(self._lib.nacs_schedule_request, reqs, method, weights, out, flags, **kw)
+
+    def schedule_batch(self, reqs: dict, method, weights, out=None, flags=0, **kw) -> dict:
+        """Every request against the same snapshot (snapshot isolation); the state is unchanged."""
+        return self._schedule(self._lib.nacs_schedule_batch, reqs, method, weights, out, flags, **kw)
+
+    def last_stats(self) -> dict:
+        s = Stats()
+        self._check(self._lib.nacs_last_stats(self._h, C.byref(s)))
+        return {f: getattr(s, f) for f, _ in Stats._fields_}

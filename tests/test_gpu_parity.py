@@ -1,0 +1,243 @@
+"""GPU parity: the CUDA path through the C ABI against the CPU oracle (needs a B200)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from inputs import gen
+from oracle import oracle as O
+from tests.parity import assert_rank_parity, assert_schedule_parity, to_np
+
+pytestmark = pytest.mark.gpu
+SCHEMAS = ("flat", "clustering", "network")
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    from paper_1909_07673_b200 import nacs
+    c = nacs.Context(0)
+    yield c
+    c.close()
+
+
+def random_flows(rng, snap, nflow, dmax=60):
+    n = snap["k"] ** 3 // 4
+    vs = rng.choice(n, size=min(nflow, n), replace=False)
+    return [(int(v), int(rng.integers(1, dmax))) for v in vs]
+
+
+# ------------------------------------------------------------------ rank -----
+@pytest.mark.parametrize("k", [2, 4, 6, 8, 16])
+@pytest.mark.parametrize("method", ["topsis", "ahp"])
+def test_rank_parity_random(ctx, k, method):
+    rng = np.random.default_rng(1000 + k)
+    for trial in range(6):
+        snap = gen.snapshot(k, seed=200 + trial, quantised=trial % 3 == 2)
+        if trial % 2:
+            snap["link_res"] = rng.integers(0, 120, size=len(snap["link_res"])).astype(np.int32)
+        ctx.load_topology(snap)
+        flows = random_flows(rng, snap, int(rng.integers(0, 4)))
+        dc, dr = int(rng.integers(100, 8000)), int(rng.integers(128, 30000))
+        for schema in SCHEMAS:
+            for rule in ((0, 1) if method == "ahp" else (0,)):
+                g = ctx.rank(method, schema, dc, dr, flows, ahp_rule=rule)
+                o = O.rank(snap, method, schema, dc, dr, flows, ahp_rule=rule)
+                assert_rank_parity(g, o, (k, trial, schema, rule))
+
+
+def test_rank_golden_vectors(ctx):
+    gold = json.load(open(os.path.join(GOLDEN, "survey_4server.json")))
+    snap = gen.snapshot(4, warm=False)
+    for u, (c, r, a, b) in enumerate(gold["rows"]):
+        snap["cpu_res"][u], snap["ram_res"][u], snap["active"][u], snap["link_res"][u] = c, r, a, b
+    snap["cpu_res"][4:] = 0
+    snap["active"][4:] = 1
+    ctx.load_topology(snap)
+    for case in gold["cases"]:
+        g = ctx.rank(case["method"], case["schema"], 1, 1, ahp_rule=case["ahp_rule"])
+        assert g["mask"][:4].all() and not g["mask"][4:].any()
+        assert g["best"] == case["argmax"]
+        assert np.allclose(g["scores"][:4], case["scores"], rtol=1e-5, atol=0), case
+
+
+@pytest.mark.parametrize("method", ["topsis", "ahp"])
+def test_rank_excluded_and_exact64(ctx, method):
+    snap = gen.snapshot(8, seed=31)
+    ctx.load_topology(snap)
+    rng = np.random.default_rng(5)
+    flows = random_flows(rng, snap, 3)
+    g = ctx.rank(method, "network", 500, 1000, flows)
+    ex = [g["best"], flows[0][0]]
+    g2 = ctx.rank(method, "network", 500, 1000, flows, excluded=ex)
+    o2 = O.rank(snap, method, "network", 500, 1000, flows, excluded=ex)
+    assert_rank_parity(g2, o2)
+    g3 = ctx.rank(method, "network", 500, 1000, flows, excluded=ex, exact64=True)
+    assert g3["best"] == g2["best"] and np.array_equal(g3["mask"], g2["mask"])
+
+
+def test_rank_no_feasible(ctx):
+    ctx.load_topology(gen.snapshot(4, seed=1))
+    g = ctx.rank("topsis", "flat", 10 ** 6, 1)
+    assert g["best"] == -1 and not g["mask"].any()
+
+
+# -------------------------------------------------------------- schedule -----
+@pytest.mark.parametrize("method", ["topsis", "ahp"])
+@pytest.mark.parametrize("schema", SCHEMAS)
+def test_c1_sequential(ctx, method, schema):
+    snap, reqs = gen.config("C1")
+    ctx.load_topology(snap)
+    out = to_np(ctx.schedule_request(reqs, method, schema))
+    assert (out["server_of_container"] == 0).all()  # SURVEY §8(c) C1 expectation
+    assert_schedule_parity(snap, reqs, out, method, schema, True, gpu_state=ctx.read_topology())
+
+
+@pytest.mark.parametrize("method", ["topsis", "ahp"])
+@pytest.mark.parametrize("schema", SCHEMAS)
+def test_c2_sequential(ctx, method, schema):
+    snap, reqs = gen.config("C2")
+    ctx.load_topology(snap)
+    out = ctx.schedule_request(reqs, method, schema)
+    cnt = assert_schedule_parity(snap, reqs, out, method, schema, True, gpu_state=ctx.read_topology())
+    st = ctx.last_stats()
+    assert st["pod_steps"] == cnt["pod_steps"] and st["retries"] == cnt["retries"]
+
+
+@pytest.mark.parametrize("method", ["topsis", "ahp"])
+@pytest.mark.parametrize("rule", [0, 1])
+def test_c2_batch(ctx, method, rule):
+    snap, reqs = gen.config("C2")
+    ctx.load_topology(snap)
+    for schema in SCHEMAS:
+        out = ctx.schedule_batch(reqs, method, schema, ahp_rule=rule)
+        assert_schedule_parity(snap, reqs, out, method, schema, False, ahp_rule=rule)
+    st = ctx.read_topology()
+    for key in ("cpu_res", "ram_res", "active", "link_res"):
+        assert np.array_equal(st[key], snap[key])  # batch never mutates (R21)
+
+
+def test_congested_links_retries_and_rejections(ctx):
+    """Tight fabric: flows compete for links, exercising R18 retries and R20 rejections."""
+    snap = gen.snapshot(8, seed=77)
+    snap["link_res"] = np.random.default_rng(1).integers(0, 90, size=len(snap["link_res"])).astype(np.int32)
+    reqs = gen.requests(300, 78, bw_max_hi=60)
+    for method in ("topsis", "ahp"):
+        ctx.load_topology(snap)
+        out = ctx.schedule_batch(reqs, method, "network")
+        cnt = assert_schedule_parity(snap, reqs, out, method, "network", False)
+        assert (to_np(out)["status"] == 0).any()
+        out = ctx.schedule_request(reqs, method, "network")
+        cnt = assert_schedule_parity(snap, reqs, out, method, "network", True, gpu_state=ctx.read_topology())
+        assert cnt["retries"] == ctx.last_stats()["retries"]
+
+
+def test_quantised_ties(ctx):
+    snap = gen.snapshot(8, seed=9, quantised=True)
+    reqs = gen.requests(150, 10)
+    ctx.load_topology(snap)
+    for method in ("topsis", "ahp"):
+        out = ctx.schedule_batch(reqs, method, "clustering")
+        assert_schedule_parity(snap, reqs, out, method, "clustering", False)
+
+
+def test_c3_batch_subsample(ctx):
+    snap, reqs = gen.config("C3")
+    ctx.load_topology(snap)
+    sub = gen.subset(reqs, np.arange(0, 10_000, 25))  # 400 requests
+    out = ctx.schedule_batch(sub, "topsis", "flat")
+    assert_schedule_parity(snap, sub, out, "topsis", "flat", False)
+    sub2 = gen.subset(reqs, np.arange(0, 10_000, 200))  # 50 requests
+    out = ctx.schedule_batch(sub2, "ahp", "flat")
+    assert_schedule_parity(snap, sub2, out, "ahp", "flat", False)
+
+
+def test_c4_full_batch_sampled_parity(ctx):
+    """The bench launch configuration (C4, 100k requests, device pointers): parity on a
+    sample of requests (requests are independent under R21) plus invariants on all."""
+    import torch
+    snap, reqs = gen.config("C4")
+    ctx.load_topology(snap)
+    dreqs = {k: (torch.from_numpy(v).cuda() if isinstance(v, np.ndarray) else v) for k, v in reqs.items()}
+    out = to_np(ctx.schedule_batch(dreqs, "topsis", "flat"))
+    co, vo = reqs["container_off"], reqs["vlink_off"]
+    assert set(np.unique(out["status"]).tolist()) <= {0, 1}
+    ok = np.repeat(out["status"] == 1, np.diff(co))
+    assert (out["server_of_container"][ok] >= 0).all() and (out["server_of_container"][~ok] == -1).all()
+    assert (out["cpu_alloc"][ok] >= reqs["cpu_min"][ok]).all() and (out["cpu_alloc"][ok] <= reqs["cpu_max"][ok]).all()
+    idx = np.sort(np.random.default_rng(0).choice(reqs["n_requests"], 200, replace=False))
+    sub = gen.subset(reqs, idx)
+    cs = np.concatenate([np.arange(co[i], co[i + 1]) for i in idx])
+    vs = np.concatenate([np.arange(vo[i], vo[i + 1]) for i in idx])
+    gsub = dict(status=out["status"][idx], server_of_container=out["server_of_container"][cs],
+                cpu_alloc=out["cpu_alloc"][cs], ram_alloc=out["ram_alloc"][cs],
+                bw_alloc=out["bw_alloc"][vs], path_of_vlink=out["path_of_vlink"][vs])
+    assert_schedule_parity(snap, sub, gsub, "topsis", "flat", False)
+
+
+def test_determinism(ctx):
+    snap, reqs = gen.config("C2")
+    ctx.load_topology(snap)
+    a = to_np(ctx.schedule_batch(reqs, "ahp", "network"))
+    b = to_np(ctx.schedule_batch(reqs, "ahp", "network"))
+    for k in a:
+        assert np.array_equal(a[k], b[k])
+    g1 = ctx.rank("topsis", "flat", 300, 300)
+    g2 = ctx.rank("topsis", "flat", 300, 300)
+    assert np.array_equal(g1["scores"].view(np.uint32), g2["scores"].view(np.uint32))
+
+
+# ------------------------------------------------------------ edge cases -----
+def test_empty_batch_and_errors(ctx):
+    from paper_1909_07673_b200 import nacs
+    snap, reqs = gen.config("C2")
+    ctx.load_topology(snap)
+    empty = gen.subset(reqs, [])
+    out = ctx.schedule_batch(empty, "topsis", "flat")
+    assert len(out["status"]) == 0
+    bad = gen.subset(reqs, [0, 1])
+    bad["cpu_min"] = bad["cpu_min"].copy()
+    bad["cpu_min"][0] = bad["cpu_max"][0] + 1
+    with pytest.raises(nacs.NacsError) as ei:
+        ctx.schedule_batch(bad, "topsis", "flat")
+    assert ei.value.status == nacs.NACS_EINVAL and "request 0" in str(ei.value)
+    before = ctx.read_topology()
+    with pytest.raises(nacs.NacsError):
+        ctx.schedule_request(bad, "topsis", "flat")
+    after = ctx.read_topology()
+    for k in before:
+        assert np.array_equal(before[k], after[k])  # errors leave the state unchanged
+    with pytest.raises(nacs.NacsError):
+        ctx.schedule_batch(reqs, "topsis", (0.5, 0.5, 0.5, 0.5))  # weights do not sum to 1
+    with pytest.raises(nacs.NacsError) as ei:
+        ctx.load_topology(dict(snap, k=5))
+    assert ei.value.status == nacs.NACS_EINVAL
+
+
+def test_device_pointer_invalid_request_status(ctx):
+    import torch
+    from paper_1909_07673_b200 import nacs
+    snap, reqs = gen.config("C2")
+    ctx.load_topology(snap)
+    bad = gen.subset(reqs, [0, 1, 2])
+    bad["pod_of"] = bad["pod_of"].copy()
+    bad["pod_of"][0] = 50  # pod ids not 0..P-1
+    d = {k: (torch.from_numpy(v).cuda() if isinstance(v, np.ndarray) else v) for k, v in bad.items()}
+    out = ctx.schedule_batch(d, "topsis", "flat", flags=nacs.NACS_ASYNC)
+    torch.cuda.synchronize()
+    st = out["status"].cpu().numpy()
+    assert st[0] == -1 and (st[1:] == 1).all()
+    with pytest.raises(nacs.NacsError):
+        ctx.schedule_batch(d, "topsis", "flat")
+
+
+def test_rejected_request_is_atomic(ctx):
+    snap = gen.snapshot(8, seed=3)
+    reqs = gen.requests(3, 4)
+    reqs["cpu_min"][reqs["container_off"][1]:reqs["container_off"][2]] = 24000
+    reqs["cpu_max"][reqs["container_off"][1]:reqs["container_off"][2]] = 24000
+    ctx.load_topology(snap)
+    out = ctx.schedule_request(reqs, "topsis", "flat")
+    assert to_np(out)["status"][1] == 0
+    assert_schedule_parity(snap, reqs, out, "topsis", "flat", True, gpu_state=ctx.read_topology())
