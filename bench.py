@@ -132,7 +132,8 @@ def run_ours(args, rank, world, local):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
-    stream = torch.cuda.current_stream(dev)
+    stream = torch.cuda.Stream(dev)  # a dedicated stream: events and kernels on the same handle
+    torch.cuda.set_stream(stream)
     ctx = nacs.Context(local, stream)
     pk, pk_kind = peaks()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2

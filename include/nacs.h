@@ -136,8 +136,8 @@ typedef struct {
   int64_t ahp_pairs;       /* AHP: sum over pod steps and non-constant criteria of |F|(|F|-1)/2 */
 } nacs_stats;
 
-/* Create a context on CUDA device `device`.  cuda_stream: a cudaStream_t to order all
- * work on (NULL = the library creates its own non-blocking stream). */
+/* Create a context on CUDA device `device`.  cuda_stream: the cudaStream_t all work of
+ * the context is ordered on (NULL = the legacy default stream, as in the CUDA runtime). */
 nacs_status nacs_create(nacs_ctx **out, int device, void *cuda_stream);
 void nacs_destroy(nacs_ctx *ctx);
 

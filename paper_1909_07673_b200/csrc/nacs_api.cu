@@ -388,14 +388,7 @@ nacs_status nacs_create(nacs_ctx** out, int device, void* cuda_stream) {
   ctx->device = device;
   cudaError_t e = cudaSetDevice(device);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
-  if (e == cudaSuccess) {
-    if (cuda_stream) {
-      ctx->stream = static_cast<cudaStream_t>(cuda_stream);
-    } else {
-      e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
-      ctx->own_stream = true;
-    }
-  }
+  if (e == cudaSuccess) ctx->stream = static_cast<cudaStream_t>(cuda_stream);
   if (e != cudaSuccess) {
     delete ctx;
     cudaGetLastError();

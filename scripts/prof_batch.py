@@ -1,0 +1,35 @@
+"""One nacs_schedule_batch call (after warm-up) for ncu captures.
+
+usage: python scripts/prof_batch.py [topsis|ahp] [C3|C4] [n_requests]
+"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from inputs import gen  # noqa: E402
+from paper_1909_07673_b200 import nacs  # noqa: E402
+
+method = sys.argv[1] if len(sys.argv) > 1 else "topsis"
+cfg = sys.argv[2] if len(sys.argv) > 2 else "C4"
+nreq = int(sys.argv[3]) if len(sys.argv) > 3 else gen.CONFIG_REQUESTS[cfg]
+snap = gen.snapshot(gen.CONFIG_K[cfg], gen.CONFIG_SEEDS[cfg])
+reqs = gen.requests(nreq, gen.CONFIG_SEEDS[cfg] + 1000)
+s = torch.cuda.Stream()
+torch.cuda.set_stream(s)
+ctx = nacs.Context(0, s)
+ctx.load_topology(snap)
+d = {k: (torch.from_numpy(v).cuda() if isinstance(v, np.ndarray) else v) for k, v in reqs.items()}
+out = ctx._alloc_out(reqs, True)[0]
+for _ in range(2):
+    ctx.schedule_batch(d, method, "flat", out=out, flags=nacs.NACS_ASYNC)
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record(s)
+ctx.schedule_batch(d, method, "flat", out=out, flags=nacs.NACS_ASYNC)
+e1.record(s)
+torch.cuda.synchronize()
+st = ctx.last_stats()
+print(f"{method} {cfg} {nreq} requests: {e0.elapsed_time(e1):.3f} ms, stats {st}")
