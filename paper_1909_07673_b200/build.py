@@ -9,8 +9,9 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libnacs.so")
-SOURCES = [os.path.join(CSRC, f) for f in ("nacs_kernels.cu", "nacs_api.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, "nacs_internal.h"), os.path.join(ROOT, "include", "nacs.h")]
+SOURCES = [os.path.join(CSRC, f) for f in ("nacs_kernels.cu", "nacs_warp.cu", "nacs_api.cu")]
+DEPS = SOURCES + [os.path.join(CSRC, "nacs_internal.h"), os.path.join(CSRC, "nacs_device.cuh"),
+                  os.path.join(ROOT, "include", "nacs.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
          "-Xcompiler", "-fPIC", "-shared", "-cudart", "static", "-Xptxas", "-v"]

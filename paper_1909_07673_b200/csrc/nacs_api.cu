@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -70,6 +71,8 @@ struct nacs_ctx {
   DevArr<int> req_in;        // packed CSR inputs
   DevArr<int> req_out;       // packed outputs
   DevArr<int2> ulog;
+  DevArr<int4> wlog;         // per-warp undo logs of k_batch_warp
+  DevArr<int> deferred;      // requests k_batch_warp hands to k_batch
   DevArr<double> w64;
   DevArr<float> ahp_ws;
   DevArr<int> misc;          // next-request counter, query arrays, best
@@ -80,6 +83,7 @@ struct nacs_ctx {
   std::string err;
   nacs_stats last{};
   bool stats_pending = false;
+  bool cta_only = false;     // NACS_CTA_ONLY=1: force the CTA-per-request batch kernel (testing)
 };
 
 namespace {
@@ -386,6 +390,8 @@ nacs_status nacs_create(nacs_ctx** out, int device, void* cuda_stream) {
   if (device < 0 || device >= count) return NACS_EINVAL;
   nacs_ctx* ctx = new nacs_ctx();
   ctx->device = device;
+  const char* env = getenv("NACS_CTA_ONLY");
+  ctx->cta_only = env && env[0] == '1';
   cudaError_t e = cudaSetDevice(device);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
   if (e == cudaSuccess) ctx->stream = static_cast<cudaStream_t>(cuda_stream);
@@ -406,6 +412,8 @@ void nacs_destroy(nacs_ctx* ctx) {
   ctx->req_in.release();
   ctx->req_out.release();
   ctx->ulog.release();
+  ctx->wlog.release();
+  ctx->deferred.release();
   ctx->w64.release();
   ctx->ahp_ws.release();
   ctx->misc.release();
@@ -545,9 +553,21 @@ nacs_status nacs_schedule_batch(nacs_ctx* ctx, const nacs_options* opt, const na
   CK(ctx->ulog.reserve((size_t)grid * nacs::ULOG_CAP));
   if (o.method == 0) CK(ctx->w64.reserve((size_t)grid * 4 * g.n));
   CK(ctx->misc.reserve(8));
-  CK(cudaMemsetAsync(ctx->misc.p, 0, sizeof(int), ctx->stream));
-  CK(nacs::launch_batch(g, o, ctx->state.p, Rd, Od, ctx->ulog.p, ctx->w64.p, ctx->misc.p, ctx->stats.p, grid,
-                        ctx->stream));
+  CK(cudaMemsetAsync(ctx->misc.p, 0, 4 * sizeof(int), ctx->stream));
+  const int warps = o.method == NACS_TOPSIS && !ctx->cta_only ? nacs::warp_kernel_warps(g) : 0;
+  if (warps >= 4) {
+    // fast path: warp per request; requests beyond its limits are deferred to k_batch
+    int wgrid = ctx->num_sms;
+    CK(ctx->wlog.reserve(nacs::warp_ulog_entries(wgrid, warps)));
+    CK(ctx->deferred.reserve((size_t)R));
+    CK(nacs::launch_batch_warp(g, o, ctx->state.p, Rd, Od, ctx->wlog.p, ctx->misc.p, ctx->deferred.p,
+                               ctx->misc.p + 2, ctx->stats.p, wgrid, warps, ctx->stream));
+    CK(nacs::launch_batch(g, o, ctx->state.p, Rd, Od, ctx->ulog.p, ctx->w64.p, ctx->misc.p + 1, ctx->stats.p,
+                          grid, ctx->stream, ctx->deferred.p, ctx->misc.p + 2));
+  } else {
+    CK(nacs::launch_batch(g, o, ctx->state.p, Rd, Od, ctx->ulog.p, ctx->w64.p, ctx->misc.p, ctx->stats.p, grid,
+                          ctx->stream));
+  }
   if (!dev) {
     if ((st = unstage_outputs(ctx, R, C, V, out))) return st;
   }

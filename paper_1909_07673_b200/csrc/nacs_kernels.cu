@@ -23,42 +23,18 @@
 #include <climits>
 #include <cstdint>
 
-#include "nacs_internal.h"
+#include "nacs_device.cuh"
 
 namespace nacs {
 
 #define FULL 0xffffffffu
 
 // ---------------------------------------------------------------- helpers ----
-__device__ __forceinline__ float rcp_approx(float x) {
-  float r;
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
-  return r;
-}
-__device__ __forceinline__ float rsqrt_approx(float x) {
-  float r;
-  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
-  return r;
-}
-// s * d rounded once, for an integer 0 <= d < 2^23: (2^23 + d) is exact in FP32 and
-// fma(s, 2^23 + d, -s*2^23) = round(s * d).  s2p23 = s * 2^23 (exact).
-__device__ __forceinline__ float scaled_diff(float s, float s2p23, int d) {
-  return fmaf(s, __int_as_float(0x4B000000 | d), -s2p23);
-}
-__device__ __forceinline__ float exact_f(int d) {  // 0 <= d < 2^23, exact
-  return __int_as_float(0x4B000000 | d) - 8388608.0f;
-}
-__device__ __forceinline__ unsigned div_h(unsigned x, unsigned magic) { return __umulhi(x, magic); }
-
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
   return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
-
-// FP32 error-bound constants.  u = 2^-24.
-// TOPSIS: |r32 - r| <= 20u; ambiguous top-2 gap <= 2^-17 (> 4 x 40u).
-constexpr float kTopsisDelta = 7.62939453125e-06f;  // 2^-17
 // AHP: relative error of PG in FP32 <= (96 + 2*ceil(nf/32)) u; ambiguous if the
-// relative top-2 gap is <= 2 x that.
+// relative top-2 gap is <= 2 x that (DESIGN.md §5).
 __device__ __forceinline__ float ahp_delta_rel(int nf) {
   return 2.0f * (96.0f + 2.0f * (float)((nf + 31) / 32)) * 5.9604644775390625e-08f;
 }
@@ -139,20 +115,6 @@ __device__ __forceinline__ void undo_to(Ctx& c, int mark) {
 }
 
 // ------------------------------------------------------------ reductions -----
-__device__ __forceinline__ void top2_insert(unsigned long long& k1, unsigned long long& k2,
-                                            unsigned long long k) {
-  if (k > k1) { k2 = k1; k1 = k; }
-  else if (k > k2) { k2 = k; }
-}
-__device__ __forceinline__ void top2_merge(unsigned long long& a1, unsigned long long& a2,
-                                           unsigned long long b1, unsigned long long b2) {
-  unsigned long long hi = a1 > b1 ? a1 : b1;
-  unsigned long long lo = a1 > b1 ? b1 : a1;
-  unsigned long long s2 = a2 > b2 ? a2 : b2;
-  a1 = hi;
-  a2 = lo > s2 ? lo : s2;
-}
-
 // Block-wide top-2 of 64-bit keys; result in s->key1, s->key2.  All threads call.
 __device__ void block_top2(Ctx& c, unsigned long long k1, unsigned long long k2) {
   Scratch* s = c.s;
@@ -446,63 +408,22 @@ __device__ void pass_filter(Ctx& c, uint8_t* mask_out, float* scores_out) {
 }
 
 // ------------------------------------------------------------ TOPSIS --------
-// a5T: closeness of server u in FP32 (R12-R13): v_uc = w_c x_uc / ||x_c||;
-// Ed+ = ||v_u - A+||, Ed- = ||v_u - A-||, with A+ = max, A- = min over F (benefit
-// criteria, R3); differences taken in exact integers then scaled once.
-__device__ __forceinline__ float topsis32(const Scratch* s, int x0, int x1, int x2, int x3) {
-  float p0 = scaled_diff(s->sf[0], s->s2p23[0], s->mx[0] - x0);
-  float m0 = scaled_diff(s->sf[0], s->s2p23[0], x0 - s->mn[0]);
-  float p1 = scaled_diff(s->sf[1], s->s2p23[1], s->mx[1] - x1);
-  float m1 = scaled_diff(s->sf[1], s->s2p23[1], x1 - s->mn[1]);
-  float p2 = scaled_diff(s->sf[2], s->s2p23[2], s->mx[2] - x2);
-  float m2 = scaled_diff(s->sf[2], s->s2p23[2], x2 - s->mn[2]);
-  float p3 = scaled_diff(s->sf[3], s->s2p23[3], s->mx[3] - x3);
-  float m3 = scaled_diff(s->sf[3], s->s2p23[3], x3 - s->mn[3]);
-  float ep2 = fmaf(p3, p3, fmaf(p2, p2, fmaf(p1, p1, p0 * p0)));
-  float em2 = fmaf(m3, m3, fmaf(m2, m2, fmaf(m1, m1, m0 * m0)));
-  float ep = ep2 > 0.f ? ep2 * rsqrt_approx(ep2) : 0.f;
-  float em = em2 > 0.f ? em2 * rsqrt_approx(em2) : 0.f;
-  float den = ep + em;
-  return den > 0.f ? em * rcp_approx(den) : 0.f;
-}
-__device__ double topsis64(const Scratch* s, int x0, int x1, int x2, int x3) {
-  int x[4] = {x0, x1, x2, x3};
-  double ep = 0, em = 0;
-  for (int c = 0; c < 4; ++c) {
-    double p = s->sd[c] * (double)(s->mx[c] - x[c]);
-    double m = s->sd[c] * (double)(x[c] - s->mn[c]);
-    ep += p * p;
-    em += m * m;
-  }
-  ep = sqrt(ep);
-  em = sqrt(em);
-  return (ep + em) > 0 ? em / (ep + em) : 0.0;
-}
-
 template <bool WRITE_SCORES>
 __device__ void select_topsis(Ctx& c, float* scores_out) {
   Scratch* s = c.s;
   const int n = c.g.n;
   const int* st = c.st;
-  if (c.tid == 0) {
-    for (int k = 0; k < 4; ++k) {
-      double N = sqrt((double)s->sq[k]);
-      double sd = N > 0 ? c.o.wd[k] / N : 0.0;
-      s->sd[k] = sd;
-      s->sf[k] = (float)sd;
-      s->s2p23[k] = (float)sd * 8388608.0f;
-    }
-  }
-  __syncthreads();
+  TopsisP tp;
+  for (int k = 0; k < 4; ++k) { tp.mx[k] = s->mx[k]; tp.mn[k] = s->mn[k]; }
+  topsis_params(tp, c.o.wd, s->sq);
   unsigned long long k1 = 0, k2 = 0;
   for (int base = c.warp * 32; base < n; base += c.B) {
     unsigned bits = c.maskw[base >> 5];
     if (!((bits >> c.lane) & 1u)) continue;
     int u = base + c.lane;
-    float r = topsis32(s, st[u], st[n + u], st[2 * n + u], st[3 * n + u]);
+    float r = topsis32(tp, st[u], st[n + u], st[2 * n + u], st[3 * n + u]);
     if (WRITE_SCORES) scores_out[u] = r;
-    unsigned long long key = ((unsigned long long)__float_as_uint(r) << 32) | (0xFFFFFFFFu - (unsigned)u);
-    top2_insert(k1, k2, key);
+    top2_insert(k1, k2, score_key(r, u));
   }
   block_top2(c, k1, k2);
   if (c.tid == 0) {
@@ -522,8 +443,8 @@ __device__ void select_topsis(Ctx& c, float* scores_out) {
       if (!((bits >> c.lane) & 1u)) continue;
       int u = base + c.lane;
       int x0 = st[u], x1 = st[n + u], x2 = st[2 * n + u], x3 = st[3 * n + u];
-      if (topsis32(s, x0, x1, x2, x3) < thr) continue;
-      double r = topsis64(s, x0, x1, x2, x3);
+      if (topsis32(tp, x0, x1, x2, x3) < thr) continue;
+      double r = topsis64(tp, x0, x1, x2, x3);
       if (r > bv || (r == bv && u < bj)) { bv = r; bj = u; }
     }
     block_argmax64(c, bv, bj);
@@ -972,10 +893,12 @@ __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(
 template <int METHOD>
 __global__ void __launch_bounds__(1024) k_batch(Geo g, Opt o, const int* __restrict__ snap, ReqsDev R,
                                                 OutDev O, int2* ulog, double* w64, int* next,
-                                                unsigned long long* stats) {
+                                                unsigned long long* stats, const int* idx, const int* n_idx) {
   extern __shared__ __align__(16) unsigned char dyn[];
   __shared__ Scratch s;
   __shared__ __align__(8) unsigned long long mbar;
+  const int n_req = idx ? *n_idx : R.n;  // deferred list from k_batch_warp, or every request
+  if (n_req == 0) return;
   Ctx c;
   init_ctx(c, g, o, &s);
   const int nW = c.nW, nEW = c.nEW, n = g.n;
@@ -1037,7 +960,8 @@ __global__ void __launch_bounds__(1024) k_batch(Geo g, Opt o, const int* __restr
     __syncthreads();
     int r = s.next_req;
     __syncthreads();
-    if (r >= R.n) break;
+    if (r >= n_req) break;
+    if (idx) r = idx[r];
     run_request<METHOD>(c, R, O, r, false);
   }
   flush_stats(c, stats);
@@ -1188,15 +1112,15 @@ cudaError_t batch_occupancy(const Geo& g, int method, int* blocks_per_sm) {
 
 cudaError_t launch_batch(const Geo& g, const Opt& o, const int* d_state, const ReqsDev& R, const OutDev& O,
                          int2* ulog, double* w64, int* next, unsigned long long* stats, int grid,
-                         cudaStream_t st) {
+                         cudaStream_t st, const int* idx, const int* n_idx) {
   size_t smem = batch_smem_bytes(g, o.method);
   int B = batch_block_size(g);
   if (o.method == 1) {
     cudaFuncSetAttribute(k_batch<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_batch<1><<<grid, B, smem, st>>>(g, o, d_state, R, O, ulog, w64, next, stats);
+    k_batch<1><<<grid, B, smem, st>>>(g, o, d_state, R, O, ulog, w64, next, stats, idx, n_idx);
   } else {
     cudaFuncSetAttribute(k_batch<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_batch<0><<<grid, B, smem, st>>>(g, o, d_state, R, O, ulog, w64, next, stats);
+    k_batch<0><<<grid, B, smem, st>>>(g, o, d_state, R, O, ulog, w64, next, stats, idx, n_idx);
   }
   return cudaGetLastError();
 }

@@ -241,3 +241,45 @@ def test_rejected_request_is_atomic(ctx):
     out = ctx.schedule_request(reqs, "topsis", "flat")
     assert to_np(out)["status"][1] == 0
     assert_schedule_parity(snap, reqs, out, "topsis", "flat", True, gpu_state=ctx.read_topology())
+
+
+def _cta_only_ctx():
+    from paper_1909_07673_b200 import nacs
+    os.environ["NACS_CTA_ONLY"] = "1"
+    try:
+        return nacs.Context(0)
+    finally:
+        del os.environ["NACS_CTA_ONLY"]
+
+
+def test_warp_kernel_equals_cta_kernel(ctx):
+    """The warp-per-request fast path (k_batch_warp) and the CTA-per-request kernel
+    (k_batch) give identical placements (both also match the oracle elsewhere)."""
+    cta = _cta_only_ctx()
+    try:
+        cases = [(gen.config("C3")[0], gen.subset(gen.config("C3")[1], np.arange(0, 10_000, 10)))]
+        tight = gen.snapshot(8, seed=77)
+        tight["link_res"] = np.random.default_rng(1).integers(0, 90, size=len(tight["link_res"])).astype(np.int32)
+        cases.append((tight, gen.requests(400, 78, bw_max_hi=60)))
+        cases.append((gen.snapshot(6, seed=5, quantised=True), gen.requests(300, 6)))  # n = 54: ragged chunk
+        for snap, reqs in cases:
+            ctx.load_topology(snap)
+            cta.load_topology(snap)
+            for schema in SCHEMAS:
+                a = to_np(ctx.schedule_batch(reqs, "topsis", schema))
+                b = to_np(cta.schedule_batch(reqs, "topsis", schema))
+                for key in a:
+                    assert np.array_equal(a[key], b[key]), (schema, key)
+    finally:
+        cta.close()
+
+
+def test_large_requests_deferred_to_cta_kernel(ctx):
+    """Requests with more than 32 containers or 64 vlinks leave the warp fast path for the
+    CTA kernel; mixed batches stay exact."""
+    snap = gen.snapshot(8, seed=41)
+    reqs = gen.requests(120, 42, nc_lo=4, nc_hi=70, extra_edges=3)
+    assert (np.diff(reqs["container_off"]) > 32).any() and (np.diff(reqs["container_off"]) <= 32).any()
+    ctx.load_topology(snap)
+    out = ctx.schedule_batch(reqs, "topsis", "flat")
+    assert_schedule_parity(snap, reqs, out, "topsis", "flat", False)
