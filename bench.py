@@ -36,6 +36,9 @@ from inputs import gen  # noqa: E402
 # Algorithmic operation counts.
 TOPSIS_OPS_ALL = 3       # per server ranked: the CPU/RAM/access-bandwidth compares of the filter
 TOPSIS_OPS_FEAS = 45     # per feasible server: stats (14) + closeness (30) + argmax (1)
+# kernels launched per nacs_schedule_batch call: TOPSIS = k_order_lpt + k_batch_warp + k_batch
+# (deferred requests; exits at once when none); AHP = k_batch
+LAUNCHES = {"topsis": 3, "ahp": 1}
 AHP_RCP_PER_PAIR = 1     # per unordered pair per non-constant criterion per pass: one reciprocal
 
 
@@ -207,7 +210,7 @@ def run_ours(args, rank, world, local):
     ops = TOPSIS_OPS_ALL * st["servers_ranked"] + TOPSIS_OPS_FEAS * st["feasible"]
     achieved = ops / (topsis["kernel_ms"] / 1e3) / 1e12
     roofline = {"bound": "alu", "achieved": achieved, "peak": alu_peak, "unit": "Top/s",
-                "frac": achieved / alu_peak, "traffic": None, "kernel": "k_batch<TOPSIS>",
+                "frac": achieved / alu_peak, "traffic": None, "kernel": "k_batch_warp<TOPSIS> (whole call)",
                 "peak_source": f"148 SMs x 128 lanes x {mhz:.0f} MHz (sm_max_mhz, {pk_kind})"}
 
     ahp_obj = None
@@ -261,7 +264,7 @@ def run_ours(args, rank, world, local):
                 "pod_steps_per_step": topsis["pod_steps_per_step"],
                 "kernel_ms": topsis["kernel_ms"], "fp64_decisions": topsis["stats"]["fp64_decisions"],
                 "retries": topsis["stats"]["retries"],
-                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": args.steps,
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": args.steps * LAUNCHES["topsis"],
                 "clocks": clocks, "ahp": ahp_obj,
                 "paper_context": "T5 (P:416-426): TOPSIS 3.48-3.84 s, AHP 6.90-9.45 s per 6000-request k=20 campaign "
                                  "on an unnamed CUDA 10.1 GPU (~10-14 M / 4-7 M servers ranked/s derived)"}

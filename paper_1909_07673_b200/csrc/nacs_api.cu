@@ -559,9 +559,9 @@ nacs_status nacs_schedule_batch(nacs_ctx* ctx, const nacs_options* opt, const na
     // fast path: warp per request; requests beyond its limits are deferred to k_batch
     int wgrid = ctx->num_sms;
     CK(ctx->wlog.reserve(nacs::warp_ulog_entries(wgrid, warps)));
-    CK(ctx->deferred.reserve((size_t)R));
-    CK(nacs::launch_batch_warp(g, o, ctx->state.p, Rd, Od, ctx->wlog.p, ctx->misc.p, ctx->deferred.p,
-                               ctx->misc.p + 2, ctx->stats.p, wgrid, warps, ctx->stream));
+    CK(ctx->deferred.reserve(2 * (size_t)R));
+    CK(nacs::launch_batch_warp(g, o, ctx->state.p, Rd, Od, ctx->wlog.p, ctx->misc.p, ctx->deferred.p + R,
+                               ctx->deferred.p, ctx->misc.p + 2, ctx->stats.p, wgrid, warps, ctx->stream));
     CK(nacs::launch_batch(g, o, ctx->state.p, Rd, Od, ctx->ulog.p, ctx->w64.p, ctx->misc.p + 1, ctx->stats.p,
                           grid, ctx->stream, ctx->deferred.p, ctx->misc.p + 2));
   } else {

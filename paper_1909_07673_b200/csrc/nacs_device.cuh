@@ -37,6 +37,7 @@ constexpr float kTopsisDelta = 7.62939453125e-06f;  // 2^-17
 // TOPSIS parameters of one pod step (statistics over the feasible set F).
 struct TopsisP {
   float sf[4], s2p23[4];
+  float p2sq[2], m2sq[2];  // Fragmentation (f_u in {0,1}): squared weighted distances by f_u
   int mx[4], mn[4];
   double sd[4];
 };
@@ -48,12 +49,11 @@ __device__ __forceinline__ float topsis32(const TopsisP& t, int x0, int x1, int 
   float m0 = scaled_diff(t.sf[0], t.s2p23[0], x0 - t.mn[0]);
   float p1 = scaled_diff(t.sf[1], t.s2p23[1], t.mx[1] - x1);
   float m1 = scaled_diff(t.sf[1], t.s2p23[1], x1 - t.mn[1]);
-  float p2 = scaled_diff(t.sf[2], t.s2p23[2], t.mx[2] - x2);
-  float m2 = scaled_diff(t.sf[2], t.s2p23[2], x2 - t.mn[2]);
   float p3 = scaled_diff(t.sf[3], t.s2p23[3], t.mx[3] - x3);
   float m3 = scaled_diff(t.sf[3], t.s2p23[3], x3 - t.mn[3]);
-  float ep2 = fmaf(p3, p3, fmaf(p2, p2, fmaf(p1, p1, __fmul_rn(p0, p0))));
-  float em2 = fmaf(m3, m3, fmaf(m2, m2, fmaf(m1, m1, __fmul_rn(m0, m0))));
+  // f_u in {0,1}: its weighted distances are 0 or sf[2], squared once per pod step
+  float ep2 = fmaf(p3, p3, fmaf(p1, p1, fmaf(p0, p0, x2 ? t.p2sq[1] : t.p2sq[0])));
+  float em2 = fmaf(m3, m3, fmaf(m1, m1, fmaf(m0, m0, x2 ? t.m2sq[1] : t.m2sq[0])));
   float ep = ep2 > 0.f ? __fmul_rn(ep2, rsqrt_approx(ep2)) : 0.f;
   float em = em2 > 0.f ? __fmul_rn(em2, rsqrt_approx(em2)) : 0.f;
   float den = __fadd_rn(ep, em);
@@ -85,6 +85,11 @@ __device__ __forceinline__ void topsis_params(TopsisP& t, const double w[4], con
     t.sf[c] = (float)sd;
     t.s2p23[c] = (float)sd * 8388608.0f;
   }
+  const float q2 = __fmul_rn(t.sf[2], t.sf[2]);
+  t.p2sq[0] = t.mx[2] - 0 ? q2 : 0.f;
+  t.p2sq[1] = t.mx[2] - 1 ? q2 : 0.f;
+  t.m2sq[0] = 0 - t.mn[2] ? q2 : 0.f;
+  t.m2sq[1] = 1 - t.mn[2] ? q2 : 0.f;
 }
 
 __device__ __forceinline__ unsigned long long score_key(float r, int u) {

@@ -100,8 +100,8 @@ cudaError_t launch_batch(const Geo& g, const Opt& o, const int* d_state, const R
 int warp_kernel_warps(const Geo& g);
 size_t warp_ulog_entries(int grid, int warps);
 cudaError_t launch_batch_warp(const Geo& g, const Opt& o, const int* d_state, const ReqsDev& R, const OutDev& O,
-                              int4* ulog, int* next, int* deferred, int* n_deferred, unsigned long long* stats,
-                              int grid, int warps, cudaStream_t st);
+                              int4* ulog, int* next, int* order, int* deferred, int* n_deferred,
+                              unsigned long long* stats, int grid, int warps, cudaStream_t st);
 // sequential: one CTA, requests in order, in place on d_state
 cudaError_t launch_sequential(const Geo& g, const Opt& o, int* d_state, const ReqsDev& R, const OutDev& O,
                               int2* ulog, float* ahp_ws, double* w64, unsigned long long* stats,

@@ -53,25 +53,50 @@ struct WCtx {
   int4* ulog;
   int ulog_n;
   int lane;
+  int nDW;
+  unsigned a_cpu, a_ram, a_act, a_acc, a_edge;  // 32-bit shared addresses (+16*lane for the SoA)
   Opt o;
 };
 
-// ------------------------------------------------------------ overlay reads --
-// fabric link fid (per lane): overlay value if its row is dirty and it is overlaid
-template <typename LT>
-__device__ __forceinline__ int fab_val(const WCtx<LT>& c, int fid) {
-  int v = (int)c.fab[fid];
-  unsigned row = div_h((unsigned)fid, c.magic);
-  if ((c.dirty[row >> 5] >> (row & 31)) & 1u) {
-    const WScr* w = c.w;
-    for (int s = 0; s < w->nol; ++s)
-      if (w->ol_id[s] == fid) v = w->ol_val[s];
-  }
+__device__ __forceinline__ unsigned smem_addr(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+// read-only snapshot loads through explicit shared-window addresses
+__device__ __forceinline__ int4 lds128(unsigned a) {
+  int4 v;
+  asm("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
   return v;
+}
+__device__ __forceinline__ unsigned lds32v(unsigned a) {
+  unsigned v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
+
+// ------------------------------------------------------------ overlay reads --
+// The link overlay is kept sorted by fabric link id: per-lane lookups binary-search it.
+__device__ __forceinline__ int ol_find(const WScr* w, int fid) {
+  int lo = 0, hi = w->nol;
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if (w->ol_id[mid] < fid) lo = mid + 1;
+    else hi = mid;
+  }
+  return (lo < w->nol && w->ol_id[lo] == fid) ? lo : -1;
 }
 template <typename LT>
 __device__ __forceinline__ bool row_dirty(const WCtx<LT>& c, int row) {
   return (c.dirty[row >> 5] >> (row & 31)) & 1u;
+}
+// fabric link fid (per lane): the overlay value if its row is dirty and it is overlaid
+template <typename LT>
+__device__ __forceinline__ int fab_val(const WCtx<LT>& c, int fid) {
+  int v = (int)c.fab[fid];
+  if (row_dirty(c, (int)div_h((unsigned)fid, c.magic))) {
+    int s = ol_find(c.w, fid);
+    if (s >= 0) v = c.w->ol_val[s];
+  }
+  return v;
 }
 // overlay slot of server u, -1 if none (per lane)
 template <typename LT>
@@ -82,72 +107,141 @@ __device__ __forceinline__ int os_slot(const WCtx<LT>& c, int u) {
     if (w->os_u[i] == u) s = i;
   return s;
 }
+// overlay slot of server u, -1 if none (warp-cooperative, u uniform)
+template <typename LT>
+__device__ __forceinline__ int w_slot(const WCtx<LT>& c, int u) {
+  const WScr* w = c.w;
+  unsigned m = __ballot_sync(NACS_FULL, c.lane < w->nos && w->os_u[c.lane] == u);
+  return m ? __ffs(m) - 1 : -1;
+}
 template <typename LT>
 __device__ __forceinline__ int acc_val(const WCtx<LT>& c, int u) {
   int s = os_slot(c, u);
   return s >= 0 ? c.w->os_acc[s] : c.acc[u];
 }
 
-// ----------------------------------------------------- overlay writes (lane 0) --
-// returns false on overflow
+// -------------------------------------------- overlay writes (warp-cooperative) --
+// All lanes call with uniform arguments; lane 0 writes.  Returns false on overflow.
 template <typename LT>
-__device__ bool set_server(WCtx<LT>& c, int u, int cpu, int ram, int act, int acc, bool log = true) {
+__device__ bool w_set_server(WCtx<LT>& c, int u, int cpu, int ram, int act, int acc, bool log = true) {
   WScr* w = c.w;
-  int s = os_slot(c, u);
-  if (s < 0) {
-    if (w->nos >= WOS) return false;
-    s = w->nos++;
-    w->os_u[s] = u;
-  } else if (!log) {
-  } else if (c.ulog_n < WLOG) {
-    c.ulog[c.ulog_n++] = make_int4(s, w->os_cpu[s], w->os_ram[s], w->os_acc[s] * 2 + w->os_act[s]);
-  } else {
-    return false;
+  const int s0 = w_slot(c, u);  // uniform
+  bool ok = true;
+  if (s0 < 0 && w->nos >= WOS) ok = false;
+  if (s0 >= 0 && log && c.ulog_n >= WLOG) ok = false;
+  __syncwarp();
+  if (ok && c.lane == 0) {
+    int s = s0;
+    if (s < 0) {
+      s = w->nos++;
+      w->os_u[s] = u;
+    } else if (log) {
+      c.ulog[c.ulog_n] = make_int4(s, w->os_cpu[s], w->os_ram[s], w->os_acc[s] * 2 + w->os_act[s]);
+    }
+    w->os_cpu[s] = cpu;
+    w->os_ram[s] = ram;
+    w->os_act[s] = act;
+    w->os_acc[s] = acc;
   }
-  w->os_cpu[s] = cpu;
-  w->os_ram[s] = ram;
-  w->os_act[s] = act;
-  w->os_acc[s] = acc;
-  return true;
+  if (ok && log && s0 >= 0) c.ulog_n += 1;
+  __syncwarp();
+  return ok;
 }
 template <typename LT>
-__device__ bool set_link(WCtx<LT>& c, int fid, int val, bool log = true) {
+__device__ bool w_set_link(WCtx<LT>& c, int fid, int val, bool log = true) {
   WScr* w = c.w;
-  int s = -1;
-  for (int i = 0; i < w->nol; ++i)
-    if (w->ol_id[i] == fid) s = i;
-  if (s < 0) {
-    if (w->nol >= WOL) return false;
-    s = w->nol++;
-    w->ol_id[s] = fid;
-  } else if (!log) {
-  } else if (c.ulog_n < WLOG) {
-    c.ulog[c.ulog_n++] = make_int4(-1 - s, w->ol_val[s], 0, 0);
-  } else {
-    return false;
+  const int nol = w->nol;
+  int pos = 0;
+  bool found = false;
+#pragma unroll
+  for (int q = 0; q < WOL / 32; ++q) {
+    const int j = c.lane + 32 * q;
+    const int id = j < nol ? w->ol_id[j] : INT_MAX;
+    pos += __popc(__ballot_sync(NACS_FULL, id < fid));
+    found |= __any_sync(NACS_FULL, id == fid);
   }
-  w->ol_val[s] = val;
-  unsigned row = div_h((unsigned)fid, c.magic);
-  c.dirty[row >> 5] |= 1u << (row & 31);
-  return true;
-}
-template <typename LT>
-__device__ void undo_commit(WCtx<LT>& c, int nos0, int nol0) {
-  WScr* w = c.w;
-  for (int i = c.ulog_n - 1; i >= 0; --i) {
-    int4 e = c.ulog[i];
-    if (e.x >= 0) {
-      w->os_cpu[e.x] = e.y;
-      w->os_ram[e.x] = e.z;
-      w->os_acc[e.x] = e.w >> 1;
-      w->os_act[e.x] = e.w & 1;
-    } else {
-      w->ol_val[-1 - e.x] = e.y;
+  if (!found && nol >= WOL) return false;
+  if (log && c.ulog_n >= WLOG) return false;
+  if (found) {
+    if (c.lane == 0) {
+      if (log) c.ulog[c.ulog_n] = make_int4(-1, fid, w->ol_val[pos], 0);
+      w->ol_val[pos] = val;
+    }
+  } else {  // insert at pos, shifting the tail right
+    int ids[WOL / 32], vals[WOL / 32];
+#pragma unroll
+    for (int q = 0; q < WOL / 32; ++q) {
+      const int j = c.lane + 32 * q;
+      ids[q] = j < nol ? w->ol_id[j] : 0;
+      vals[q] = j < nol ? w->ol_val[j] : 0;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < WOL / 32; ++q) {
+      const int j = c.lane + 32 * q;
+      if (j < nol && j >= pos) { w->ol_id[j + 1] = ids[q]; w->ol_val[j + 1] = vals[q]; }
+    }
+    __syncwarp();
+    if (c.lane == 0) {
+      w->ol_id[pos] = fid;
+      w->ol_val[pos] = val;
+      w->nol = nol + 1;
+      if (log) c.ulog[c.ulog_n] = make_int4(-1, fid, 0, 1);
     }
   }
-  w->nos = nos0;
-  w->nol = nol0;
+  if (log) c.ulog_n += 1;
+  if (c.lane == 0) {
+    unsigned row = div_h((unsigned)fid, c.magic);
+    c.dirty[row >> 5] |= 1u << (row & 31);
+  }
+  __syncwarp();
+  return true;
+}
+// Undo this pod step's commit (R18): restore in reverse order.  Warp-cooperative.
+template <typename LT>
+__device__ void w_undo(WCtx<LT>& c, int nos0) {
+  WScr* w = c.w;
+  for (int i = c.ulog_n - 1; i >= 0; --i) {
+    int4 e = make_int4(0, 0, 0, 0);
+    if (c.lane == 0) e = c.ulog[i];
+    e.x = __shfl_sync(NACS_FULL, e.x, 0);
+    e.y = __shfl_sync(NACS_FULL, e.y, 0);
+    e.z = __shfl_sync(NACS_FULL, e.z, 0);
+    e.w = __shfl_sync(NACS_FULL, e.w, 0);
+    if (e.x >= 0) {
+      if (c.lane == 0) {
+        w->os_cpu[e.x] = e.y;
+        w->os_ram[e.x] = e.z;
+        w->os_acc[e.x] = e.w >> 1;
+        w->os_act[e.x] = e.w & 1;
+      }
+    } else {
+      const int pos = ol_find(w, e.y);
+      if (!e.w) {
+        if (c.lane == 0) w->ol_val[pos] = e.z;
+      } else {  // the link was inserted by this commit: remove it
+        const int nol = w->nol;
+        int ids[WOL / 32], vals[WOL / 32];
+#pragma unroll
+        for (int q = 0; q < WOL / 32; ++q) {
+          const int j = c.lane + 32 * q;
+          ids[q] = j < nol ? w->ol_id[j] : 0;
+          vals[q] = j < nol ? w->ol_val[j] : 0;
+        }
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < WOL / 32; ++q) {
+          const int j = c.lane + 32 * q;
+          if (j < nol && j > pos) { w->ol_id[j - 1] = ids[q]; w->ol_val[j - 1] = vals[q]; }
+        }
+        if (c.lane == 0) w->nol = nol - 1;
+      }
+    }
+    __syncwarp();
+  }
+  if (c.lane == 0) w->nos = nos0;
   c.ulog_n = 0;
+  __syncwarp();
 }
 
 // fabric link ids of path pid between servers u, v (same numbering as fab[])
@@ -202,85 +296,129 @@ __device__ int2 wpath(const WCtx<LT>& c, int u, int v) {
   return make_int2(pu == pv ? 1 + bt : 1 + h + bt, best);
 }
 
-// a2: edge switches some flow cannot reach with its demand (threshold bitmasks).
+// Is some core switch (a, b) joined to pods p and pv by links both >= D?  (per lane)
+template <typename LT>
+__device__ __forceinline__ bool core_ok(const WCtx<LT>& c, int p, int pv, int a, int D) {
+  const int h = c.h;
+  const int f1 = c.nfabea + (p * c.h + a) * h, f2 = c.nfabea + (pv * c.h + a) * h;
+  if (!row_dirty(c, c.E + p * h + a) && !row_dirty(c, c.E + pv * h + a)) {
+    const LT* r1 = c.fab + f1;
+    const LT* r2 = c.fab + f2;
+    for (int b = 0; b < h; ++b)
+      if ((int)r1[b] >= D && (int)r2[b] >= D) return true;
+    return false;
+  }
+  for (int b = 0; b < h; ++b)
+    if (fab_val(c, f1 + b) >= D && fab_val(c, f2 + b) >= D) return true;
+  return false;
+}
+
+// a2: mark the edge switches from which some flow's widest fabric bottleneck is below its
+// demand: edge e reaches edge(v) iff some aggregation index a has EA[e][a] >= D,
+// EA[ev][a] >= D and (other pod) some core (a, b) with both agg-core links >= D.
+// Each lane tests its edges with early exit on the first feasible (a, b).
 template <typename LT>
 __device__ void wfabric(WCtx<LT>& c) {
   WScr* w = c.w;
-  const int h = c.h, k = c.k, E = c.E;
+  const int h = c.h, E = c.E;
   const int nEW = (E + 31) >> 5;
   for (int i = c.lane; i < nEW; i += 32) c.edgebad[i] = 0u;
+  __syncwarp();
   for (int f = 0; f < w->nflow; ++f) {
     const int v = w->fv[f], D = w->fD[f];
     const int ev = (int)div_h(v, c.magic), pv = (int)div_h(ev, c.magic);
-    for (int p = c.lane; p < k; p += 32) c.pm[p] = 0u;
-    // vb: core columns b reachable from pod pv through aggregation a (lane a)
-    unsigned vb = 0;
-    bool vme = false;
-    if (c.lane < h) {
-      int a = c.lane;
-      int row = E + pv * h + a;
-      const LT* r = c.fab + c.nfabea + (pv * h + a) * h;
-      if (!row_dirty(c, row)) {
-        for (int b = 0; b < h; ++b) vb |= ((int)r[b] >= D ? 1u : 0u) << b;
-      } else {
-        for (int b = 0; b < h; ++b) vb |= (fab_val(c, c.nfabea + (pv * h + a) * h + b) >= D ? 1u : 0u) << b;
-      }
-      vme = fab_val(c, ev * h + a) >= D;
-    }
+    // vm: aggregation switches a with EA[ev][a] >= D
+    const bool vme = c.lane < h && fab_val(c, ev * h + c.lane) >= D;
     const unsigned vm = __ballot_sync(NACS_FULL, vme);
-    __syncwarp();
-    // pm[p] bit a: some core (a, b) joins pod p and pod pv with both links >= D
-    const int items = k * h;
-    for (int t0 = 0; t0 < items; t0 += 32) {
-      int t = t0 + c.lane;
-      int p = 0, a = 0;
-      bool ok = false;
-      if (t < items) {
-        p = (int)div_h(t, c.magic);
-        a = t - p * h;
-      }
-      unsigned vba = __shfl_sync(NACS_FULL, vb, a);
-      if (t < items && ((vm >> a) & 1u)) {
-        unsigned bits = 0;
-        int row = E + p * h + a;
-        const LT* r = c.fab + c.nfabea + (p * h + a) * h;
-        if (!row_dirty(c, row)) {
-          for (int b = 0; b < h; ++b) bits |= ((int)r[b] >= D ? 1u : 0u) << b;
-        } else {
-          for (int b = 0; b < h; ++b) bits |= (fab_val(c, c.nfabea + (p * h + a) * h + b) >= D ? 1u : 0u) << b;
-        }
-        ok = (bits & vba) != 0u;
-      }
-      if (ok) atomicOr(&c.pm[p], 1u << a);
-    }
-    __syncwarp();
     for (int e0 = 0; e0 < E; e0 += 32) {
-      int e = e0 + c.lane;
+      const int e = e0 + c.lane;
       bool bad = false;
       if (e < E && e != ev) {
-        unsigned em = 0;
-        if (!row_dirty(c, e)) {
-          const LT* r = c.fab + e * h;
-          for (int a = 0; a < h; ++a) em |= ((int)r[a] >= D ? 1u : 0u) << a;
-        } else {
-          for (int a = 0; a < h; ++a) em |= (fab_val(c, e * h + a) >= D ? 1u : 0u) << a;
+        const int pe = (int)div_h(e, c.magic);
+        const bool dirty = row_dirty(c, e);
+        bool ok = false;
+        for (unsigned m = vm; m && !ok; m &= m - 1) {
+          const int a = __ffs(m) - 1;
+          const int ea = dirty ? fab_val(c, e * h + a) : (int)c.fab[e * h + a];
+          if (ea < D) continue;
+          ok = pe == pv || core_ok(c, pe, pv, a, D);
         }
-        int pe = (int)div_h(e, c.magic);
-        unsigned ok = (pe == pv) ? (em & vm) : (em & vm & c.pm[pe]);
-        bad = ok == 0u;
+        bad = !ok;
       }
-      unsigned bw = __ballot_sync(NACS_FULL, bad);
+      const unsigned bw = __ballot_sync(NACS_FULL, bad);
       if (c.lane == 0) c.edgebad[e0 >> 5] |= bw;
     }
     __syncwarp();
   }
 }
 
-// Criteria of 4 consecutive servers (lane) with the pod step's special servers merged in.
-struct Four {
-  int4 c, r, a, q;
-  int info[4];  // 0 = ordinary, else special info word
+// ------------------------------------------------------------------ scans ----
+// Filter parameters of one pod step (a3).  For ordinary servers the network conditions
+// fold into thresholds: sumDp = sumD (INT_MIN without path filter) and dcp = dc
+// (INT_MAX when some flow's own access link is short, G false).
+struct StepP {
+  int dc, dr, dcp, sumDp;
+  bool net, pf, h4;
 };
+
+template <typename LT>
+__device__ __forceinline__ unsigned ebad(const WCtx<LT>& c, unsigned u) {
+  unsigned e = div_h(u, c.magic);
+  return (lds32v(c.a_edge + 4u * (e >> 5)) >> (e & 31)) & 1u;
+}
+// edge-infeasibility bits (bit j) of the lane's servers u0..u0+3
+template <typename LT>
+__device__ __forceinline__ unsigned ebad4(const WCtx<LT>& c, const StepP& sp, unsigned u0) {
+  if (!sp.net) return 0u;
+  if (sp.h4) return ebad(c, u0) ? 0xFu : 0u;
+  return ebad(c, u0) | (ebad(c, u0 + 1) << 1) | (ebad(c, u0 + 2) << 2) | (ebad(c, u0 + 3) << 3);
+}
+__device__ __forceinline__ bool ok_plain(const StepP& sp, int x0, int x1, int x3, unsigned bad) {
+  return (x0 >= sp.dcp) & (x1 >= sp.dr) & (x3 >= sp.sumDp) & (bad == 0u);
+}
+// a special server: excluded (R18), a flow endpoint (its own flow uses the host bus), or
+// only overlaid (ordinary rule on its overlay values)
+template <typename LT>
+__device__ __forceinline__ bool ok_special(const WCtx<LT>& c, const StepP& sp, int x0, int x1, int x3,
+                                           unsigned bad, int info) {
+  if (info & 64) return false;
+  int f = (info >> 7) - 1;
+  if (f >= 0) return (x0 >= sp.dc) & (x1 >= sp.dr) & (!sp.pf || c.w->fok[f]);
+  return ok_plain(sp, x0, x1, x3, bad);
+}
+
+struct AccA {
+  int nf, nact;
+  unsigned mn0, mn1, mn3, mx0, mx1, mx3;
+  unsigned long long q0, q1, q3;
+};
+// a4: statistics over F, branch-free
+__device__ __forceinline__ void acc_a(AccA& a, bool ok, int x0, int x1, int x2, int x3) {
+  unsigned o0 = ok ? (unsigned)x0 : 0u, o1 = ok ? (unsigned)x1 : 0u, o3 = ok ? (unsigned)x3 : 0u;
+  a.nf += ok ? 1 : 0;
+  a.nact += ok ? x2 : 0;
+  a.mx0 = max(a.mx0, o0);
+  a.mx1 = max(a.mx1, o1);
+  a.mx3 = max(a.mx3, o3);
+  a.mn0 = min(a.mn0, ok ? o0 : UINT_MAX);
+  a.mn1 = min(a.mn1, ok ? o1 : UINT_MAX);
+  a.mn3 = min(a.mn3, ok ? o3 : UINT_MAX);
+  a.q0 += (unsigned long long)o0 * o0;
+  a.q1 += (unsigned long long)o1 * o1;
+  a.q3 += (unsigned long long)o3 * o3;
+}
+// a7: per-lane best (score, lowest index) and second-best score
+struct AccB {
+  float b1, b2;
+  int i1;
+};
+__device__ __forceinline__ void acc_b(AccB& b, bool ok, float r, int u) {
+  float re = ok ? r : -1.0f;
+  bool gt = re > b.b1;
+  b.b2 = gt ? b.b1 : fmaxf(b.b2, re);
+  b.i1 = gt ? u : b.i1;
+  b.b1 = gt ? re : b.b1;
+}
 
 __device__ __forceinline__ void set_comp(int4& v, int j, int x) {
   if (j == 0) v.x = x;
@@ -292,59 +430,138 @@ __device__ __forceinline__ int get_comp(const int4& v, int j) {
   return j == 0 ? v.x : (j == 1 ? v.y : (j == 2 ? v.z : v.w));
 }
 
+// Substitute the chunk's special servers into the lane's 4 servers and force their
+// feasibility: info[j] = 1 | ok << 1 (0 = ordinary server).
 template <typename LT>
-__device__ __forceinline__ void load_four(const WCtx<LT>& c, int chunk, int base, int& sp_ptr, Four& f) {
-  const int li = chunk * 32 + c.lane;
-  f.c = c.cpu4[li];
-  f.r = c.ram4[li];
-  f.a = c.act4[li];
-  f.q = c.acc4[li];
-  f.info[0] = f.info[1] = f.info[2] = f.info[3] = 0;
+__device__ __forceinline__ void chunk_specials(const WCtx<LT>& c, const StepP& sp, int base, int& spp, int4& C,
+                                               int4& Rm, int4& A, int4& Q, int info[4]) {
   const WScr* w = c.w;
-  if (sp_ptr < w->nsp && w->sp_u[sp_ptr] < base + 128) {
-    while (sp_ptr < w->nsp && w->sp_u[sp_ptr] < base + 128) {
-      int u = w->sp_u[sp_ptr], info = w->sp_info[sp_ptr];
-      if (((u - base) >> 2) == c.lane) {
-        int j = (u - base) & 3;
-        int slot = (info & 63) - 1;
-        if (slot >= 0) {
-          set_comp(f.c, j, w->os_cpu[slot]);
-          set_comp(f.r, j, w->os_ram[slot]);
-          set_comp(f.a, j, w->os_act[slot]);
-          set_comp(f.q, j, w->os_acc[slot]);
-        }
-        f.info[j] = info;
+  info[0] = info[1] = info[2] = info[3] = 0;
+  while (spp < w->nsp && w->sp_u[spp] < base + 128) {
+    const int u = w->sp_u[spp], inf = w->sp_info[spp];
+    if (((u - base) >> 2) == c.lane) {
+      const int j = (u - base) & 3;
+      const int slot = (inf & 63) - 1;
+      if (slot >= 0) {
+        set_comp(C, j, w->os_cpu[slot]);
+        set_comp(Rm, j, w->os_ram[slot]);
+        set_comp(A, j, w->os_act[slot]);
+        set_comp(Q, j, w->os_acc[slot]);
       }
-      ++sp_ptr;
+      const unsigned bad = sp.net ? ebad(c, (unsigned)u) : 0u;
+      const bool ok = ok_special(c, sp, get_comp(C, j), get_comp(Rm, j), get_comp(Q, j), bad, inf);
+      info[j] = 1 | (ok ? 2 : 0);
+    }
+    ++spp;
+  }
+}
+
+// feasibility of one server: forced for special servers, the ordinary rule otherwise
+__device__ __forceinline__ bool ok_any(const StepP& sp, int x0, int x1, int x3, unsigned bad, int forced) {
+  const bool pl = ok_plain(sp, x0, x1, x3, bad);
+  return (forced & 1) ? (forced & 2) != 0 : pl;
+}
+
+// Load the lane's 4 servers of chunk ch; substitute the chunk's special servers.
+template <typename LT>
+__device__ __forceinline__ void load_chunk(const WCtx<LT>& c, const StepP& sp, int ch, int& spp, int& nxt, int4& C,
+                                           int4& Rm, int4& A, int4& Q, int4& I) {
+  const unsigned ao = (unsigned)ch << 9;
+  C = lds128(c.a_cpu + ao);
+  Rm = lds128(c.a_ram + ao);
+  A = lds128(c.a_act + ao);
+  Q = lds128(c.a_acc + ao);
+  I = make_int4(0, 0, 0, 0);
+  const int base = ch << 7;
+  if (nxt < base + 128) {  // warp-uniform
+    int info[4];
+    chunk_specials(c, sp, base, spp, C, Rm, A, Q, info);
+    I = make_int4(info[0], info[1], info[2], info[3]);
+    nxt = spp < c.w->nsp ? c.w->sp_u[spp] : INT_MAX;
+  }
+}
+
+// Pass A (a3 + a4): filter and statistics over all servers, 128 per warp iteration.
+// Chunks without special servers take a branch-free path; the others substitute and
+// force their special servers first.
+template <typename LT>
+__device__ void scan_stats(const WCtx<LT>& c, const StepP& sp, AccA& a) {
+  const int nch = c.npad >> 7;
+  int spp = 0;
+  int nxt = c.w->nsp > 0 ? c.w->sp_u[0] : INT_MAX;
+  for (int ch = 0; ch < nch; ++ch) {
+    const unsigned u0 = (unsigned)((ch << 7) + 4 * c.lane);
+    const unsigned eb = ebad4(c, sp, u0);
+    if (nxt >= (ch << 7) + 128) {
+      const unsigned ao = (unsigned)ch << 9;
+      const int4 C = lds128(c.a_cpu + ao), Rm = lds128(c.a_ram + ao), A = lds128(c.a_act + ao),
+                 Q = lds128(c.a_acc + ao);
+      acc_a(a, ok_plain(sp, C.x, Rm.x, Q.x, eb & 1u), C.x, Rm.x, A.x, Q.x);
+      acc_a(a, ok_plain(sp, C.y, Rm.y, Q.y, eb & 2u), C.y, Rm.y, A.y, Q.y);
+      acc_a(a, ok_plain(sp, C.z, Rm.z, Q.z, eb & 4u), C.z, Rm.z, A.z, Q.z);
+      acc_a(a, ok_plain(sp, C.w, Rm.w, Q.w, eb & 8u), C.w, Rm.w, A.w, Q.w);
+    } else {
+      int4 C, Rm, A, Q, I;
+      load_chunk(c, sp, ch, spp, nxt, C, Rm, A, Q, I);
+      acc_a(a, ok_any(sp, C.x, Rm.x, Q.x, eb & 1u, I.x), C.x, Rm.x, A.x, Q.x);
+      acc_a(a, ok_any(sp, C.y, Rm.y, Q.y, eb & 2u, I.y), C.y, Rm.y, A.y, Q.y);
+      acc_a(a, ok_any(sp, C.z, Rm.z, Q.z, eb & 4u, I.z), C.z, Rm.z, A.z, Q.z);
+      acc_a(a, ok_any(sp, C.w, Rm.w, Q.w, eb & 8u, I.w), C.w, Rm.w, A.w, Q.w);
     }
   }
 }
 
-struct StepP {
-  int dc, dr, sumD;
-  bool net, G, pf;
-};
-
-// a3: feasibility of server u with criteria (x0, x1, x3) and special info
+// Pass B (a5T + a7): closeness of every feasible server; per-lane best and second best.
 template <typename LT>
-__device__ __forceinline__ bool feasible(const WCtx<LT>& c, const StepP& sp, int u, int x0, int x1, int x3,
-                                         int info) {
-  bool ok = x0 >= sp.dc && x1 >= sp.dr;
-  if (info == 0) {
-    if (sp.net) {
-      unsigned e = div_h((unsigned)u, c.magic);
-      ok = ok && sp.G && x3 >= sp.sumD && !((c.edgebad[e >> 5] >> (e & 31)) & 1u);
+__device__ void scan_score(const WCtx<LT>& c, const StepP& sp, const TopsisP& tp, AccB& b) {
+  const int nch = c.npad >> 7;
+  int spp = 0;
+  int nxt = c.w->nsp > 0 ? c.w->sp_u[0] : INT_MAX;
+  for (int ch = 0; ch < nch; ++ch) {
+    const unsigned u0 = (unsigned)((ch << 7) + 4 * c.lane);
+    const unsigned eb = ebad4(c, sp, u0);
+    if (nxt >= (ch << 7) + 128) {
+      const unsigned ao = (unsigned)ch << 9;
+      const int4 C = lds128(c.a_cpu + ao), Rm = lds128(c.a_ram + ao), A = lds128(c.a_act + ao),
+                 Q = lds128(c.a_acc + ao);
+      acc_b(b, ok_plain(sp, C.x, Rm.x, Q.x, eb & 1u), topsis32(tp, C.x, Rm.x, A.x, Q.x), (int)u0);
+      acc_b(b, ok_plain(sp, C.y, Rm.y, Q.y, eb & 2u), topsis32(tp, C.y, Rm.y, A.y, Q.y), (int)u0 + 1);
+      acc_b(b, ok_plain(sp, C.z, Rm.z, Q.z, eb & 4u), topsis32(tp, C.z, Rm.z, A.z, Q.z), (int)u0 + 2);
+      acc_b(b, ok_plain(sp, C.w, Rm.w, Q.w, eb & 8u), topsis32(tp, C.w, Rm.w, A.w, Q.w), (int)u0 + 3);
+    } else {
+      int4 C, Rm, A, Q, I;
+      load_chunk(c, sp, ch, spp, nxt, C, Rm, A, Q, I);
+#pragma unroll 1
+      for (int j = 0; j < 4; ++j) {
+        const int x0 = get_comp(C, j), x1 = get_comp(Rm, j), x2 = get_comp(A, j), x3 = get_comp(Q, j);
+        const bool ok = ok_any(sp, x0, x1, x3, (eb >> j) & 1u, get_comp(I, j));
+        acc_b(b, ok, topsis32(tp, x0, x1, x2, x3), (int)u0 + j);
+      }
     }
-    return ok;
   }
-  if (info & 64) return false;  // excluded (R18)
-  int f = (info >> 7) - 1;
-  if (f >= 0) return ok && (!sp.pf || c.w->fok[f]);  // its own flow needs no network
-  if (sp.net) {
-    unsigned e = div_h((unsigned)u, c.magic);
-    ok = ok && sp.G && x3 >= sp.sumD && !((c.edgebad[e >> 5] >> (e & 31)) & 1u);
+}
+
+// FP64 re-decision (R14): exact closeness of the candidates within 2 delta of s1.
+template <typename LT>
+__device__ void scan_fp64(const WCtx<LT>& c, const StepP& sp, const TopsisP& tp, float thr, double& bv, int& bj) {
+  const int nch = c.npad >> 7;
+  int spp = 0;
+  int nxt = c.w->nsp > 0 ? c.w->sp_u[0] : INT_MAX;
+  for (int ch = 0; ch < nch; ++ch) {
+    const unsigned u0 = (unsigned)((ch << 7) + 4 * c.lane);
+    int4 C, Rm, A, Q, I;
+    load_chunk(c, sp, ch, spp, nxt, C, Rm, A, Q, I);
+    const unsigned eb = ebad4(c, sp, u0);
+#pragma unroll 1
+    for (int j = 0; j < 4; ++j) {
+      int x0 = get_comp(C, j), x1 = get_comp(Rm, j), x2 = get_comp(A, j), x3 = get_comp(Q, j);
+      if (ok_any(sp, x0, x1, x3, (eb >> j) & 1u, get_comp(I, j)) && topsis32(tp, x0, x1, x2, x3) >= thr) {
+        double rr = topsis64(tp, x0, x1, x2, x3);
+        int u = (int)u0 + j;
+        if (rr > bv || (rr == bv && u < bj)) { bv = rr; bj = u; }
+      }
+    }
   }
-  return ok;
 }
 
 // Build the sorted special list: overlay servers, excluded servers, flow servers.
@@ -370,7 +587,8 @@ __device__ void build_specials(WCtx<LT>& c) {
     if (!vbx) ub = INT_MAX;
   }
   int ra = 0, rb = 0;
-  for (int s = 0; s < 32; ++s) {
+  const int lim = max(w->nos, w->nex);
+  for (int s = 0; s < lim; ++s) {
     int xa = __shfl_sync(NACS_FULL, ua, s);
     int xb = __shfl_sync(NACS_FULL, ub, s);
     ra += (xa < ua) + (xb < ua);
@@ -387,10 +605,310 @@ struct WStats {
   unsigned long long steps, retries, fp64, invalid, feas;
 };
 
+// Registers of the request a warp is scheduling.
+struct WReq {
+  int r, c0, nC, v0, nV, P, p;
+  int cmin, cmax, rmin, rmax, cpod;        // container `lane`
+  bool hc, hv0, hv1;
+  int bn0, bx0, bn1, bx1;                  // vlinks `lane` and `lane + 32`
+  int pa0, pb0, pa1, pb1, path0, path1;    // endpoint pods, chosen paths
+  int pcpu, pram;                          // demand of pod `lane`
+};
+
+__device__ __forceinline__ void emit_failed(const OutDev& O, const WReq& q, int lane, int status) {
+  if (q.hc) { O.server[q.c0 + lane] = -1; O.cpu_a[q.c0 + lane] = 0; O.ram_a[q.c0 + lane] = 0; }
+  if (q.hv0) { O.bw_a[q.v0 + lane] = 0; O.path[q.v0 + lane] = -1; }
+  if (q.hv1) { O.bw_a[q.v0 + lane + 32] = 0; O.path[q.v0 + lane + 32] = -1; }
+  if (lane == 0) O.status[q.r] = status;
+}
+
+// Fetch requests until one is accepted into the fast path (returns false when the batch
+// is exhausted).  Oversized requests are deferred; invalid ones are emitted with -1.
+template <typename LT>
+__device__ bool acquire(WCtx<LT>& c, const ReqsDev& R, const OutDev& O, WReq& q, int* next, const int* order,
+                        int* deferred, int* n_deferred, WStats& ws) {
+  const int lane = c.lane;
+  WScr* w = c.w;
+  for (;;) {
+    int r = 0;
+    if (lane == 0) {
+      r = atomicAdd(next, 1);
+      if (r < R.n) r = order[r];
+    }
+    r = __shfl_sync(NACS_FULL, r, 0);
+    if (r >= R.n) return false;
+    q.r = r;
+    q.c0 = R.coff[r];
+    q.nC = R.coff[r + 1] - q.c0;
+    q.v0 = R.voff[r];
+    q.nV = R.voff[r + 1] - q.v0;
+    if (q.nC > WC || q.nV > WV) {
+      if (lane == 0) deferred[atomicAdd(n_deferred, 1)] = r;
+      continue;
+    }
+    q.hc = lane < q.nC;
+    q.cmin = q.cmax = q.rmin = q.rmax = 1;
+    q.cpod = 0;
+    if (q.hc) {
+      q.cmin = R.cpu_min[q.c0 + lane]; q.cmax = R.cpu_max[q.c0 + lane];
+      q.rmin = R.ram_min[q.c0 + lane]; q.rmax = R.ram_max[q.c0 + lane];
+      q.cpod = R.pod_of[q.c0 + lane];
+    }
+    q.hv0 = lane < q.nV;
+    q.hv1 = lane + 32 < q.nV;
+    int s0 = 0, d0 = 1, s1 = 0, d1 = 1;
+    q.bn0 = q.bx0 = q.bn1 = q.bx1 = 1;
+    if (q.hv0) { s0 = R.src[q.v0 + lane]; d0 = R.dst[q.v0 + lane]; q.bn0 = R.bw_min[q.v0 + lane]; q.bx0 = R.bw_max[q.v0 + lane]; }
+    if (q.hv1) {
+      s1 = R.src[q.v0 + lane + 32]; d1 = R.dst[q.v0 + lane + 32];
+      q.bn1 = R.bw_min[q.v0 + lane + 32]; q.bx1 = R.bw_max[q.v0 + lane + 32];
+    }
+    // validation (R24), in registers
+    const int nC = q.nC;
+    bool bad = q.hc && (q.cmin <= 0 || q.rmin <= 0 || q.cmin > q.cmax || q.rmin > q.rmax || q.cpod < 0 || q.cpod >= nC);
+    bad |= q.hv0 && (s0 < 0 || s0 >= nC || d0 < 0 || d0 >= nC || s0 == d0 || q.bn0 <= 0 || q.bn0 > q.bx0);
+    bad |= q.hv1 && (s1 < 0 || s1 >= nC || d1 < 0 || d1 >= nC || s1 == d1 || q.bn1 <= 0 || q.bn1 > q.bx1);
+    unsigned used = __reduce_or_sync(NACS_FULL, q.hc && q.cpod >= 0 && q.cpod < 32 ? (1u << q.cpod) : 0u);
+    int maxp = (int)__reduce_max_sync(NACS_FULL, q.hc && q.cpod >= 0 ? (unsigned)q.cpod : 0u);
+    bool invalid = __any_sync(NACS_FULL, bad) || nC <= 0 || maxp >= 32 ||
+                   used != (maxp == 31 ? 0xffffffffu : ((1u << (maxp + 1)) - 1u));
+    if (invalid) {
+      emit_failed(O, q, lane, -1);
+      if (lane == 0) ws.invalid += 1;
+      continue;
+    }
+    q.P = maxp + 1;
+    q.p = 0;
+    q.pcpu = q.pram = 0;
+    for (int i = 0; i < nC; ++i) {
+      int pd = __shfl_sync(NACS_FULL, q.cpod, i);
+      int cm = __shfl_sync(NACS_FULL, q.cmin, i);
+      int rm = __shfl_sync(NACS_FULL, q.rmin, i);
+      if (lane == pd) { q.pcpu += cm; q.pram += rm; }
+    }
+    q.pa0 = __shfl_sync(NACS_FULL, q.cpod, s0 & 31);
+    q.pb0 = __shfl_sync(NACS_FULL, q.cpod, d0 & 31);
+    q.pa1 = __shfl_sync(NACS_FULL, q.cpod, s1 & 31);
+    q.pb1 = __shfl_sync(NACS_FULL, q.cpod, d1 & 31);
+    q.path0 = q.path1 = -1;
+    w->pod_srv[lane] = -1;
+    if (lane == 0) { w->nos = 0; w->nol = 0; }
+    for (int i = lane; i < c.nDW; i += 32) c.dirty[i] = 0u;
+    __syncwarp();
+    return true;
+  }
+}
+
+// a1/a2: flows of pod q.p to placed peers (R17), fabric tables, flow-server feasibility.
+template <typename LT>
+__device__ void prepare_step(WCtx<LT>& c, WReq& q, StepP& sp) {
+  WScr* w = c.w;
+  const int lane = c.lane, p = q.p;
+  int ov0 = -1, ov1 = -1;
+  if (q.hv0) {
+    int other = (q.pa0 == p && q.pb0 != p) ? q.pb0 : ((q.pb0 == p && q.pa0 != p) ? q.pa0 : -1);
+    if (other >= 0) ov0 = w->pod_srv[other];
+  }
+  if (q.hv1) {
+    int other = (q.pa1 == p && q.pb1 != p) ? q.pb1 : ((q.pb1 == p && q.pa1 != p) ? q.pa1 : -1);
+    if (other >= 0) ov1 = w->pod_srv[other];
+  }
+  bool has0 = ov0 >= 0, has1 = ov1 >= 0;
+  if (lane == 0) { w->nflow = 0; w->nex = 0; }
+  __syncwarp();
+  int sumD = 0;
+  for (;;) {
+    unsigned m0 = __ballot_sync(NACS_FULL, has0), m1 = __ballot_sync(NACS_FULL, has1);
+    if (!(m0 | m1)) break;
+    int src_l = m0 ? __ffs(m0) - 1 : __ffs(m1) - 1;
+    int cand = m0 ? ov0 : ov1;
+    int vsel = __shfl_sync(NACS_FULL, cand, src_l);
+    bool mine0 = has0 && ov0 == vsel, mine1 = has1 && ov1 == vsel;
+    int D = (int)__reduce_add_sync(NACS_FULL, (mine0 ? (unsigned)q.bn0 : 0u) + (mine1 ? (unsigned)q.bn1 : 0u));
+    has0 &= !mine0;
+    has1 &= !mine1;
+    sumD += D;
+    if (lane == 0) {  // insert sorted by server
+      int nf = w->nflow, i = nf;
+      while (i > 0 && w->fv[i - 1] > vsel) { w->fv[i] = w->fv[i - 1]; w->fD[i] = w->fD[i - 1]; --i; }
+      w->fv[i] = vsel;
+      w->fD[i] = D;
+      w->nflow = nf + 1;
+    }
+    __syncwarp();
+  }
+  const int nflow = w->nflow;
+  const bool net = c.o.path_filter && nflow > 0;
+  if (net) wfabric(c);
+  bool Gl = true;
+  if (lane < nflow) {
+    int v = w->fv[lane], D = w->fD[lane];
+    int av = acc_val(c, v);
+    Gl = av >= D;
+    bool fk = av >= sumD - D;
+    for (int f2 = 0; f2 < nflow; ++f2)
+      if (f2 != lane && acc_val(c, w->fv[f2]) < w->fD[f2]) fk = false;
+    if (net && ebad(c, (unsigned)v)) fk = false;
+    w->fok[lane] = fk;
+  }
+  const bool G = __all_sync(NACS_FULL, Gl);
+  const int dc = __shfl_sync(NACS_FULL, q.pcpu, p), dr = __shfl_sync(NACS_FULL, q.pram, p);
+  sp.dc = dc;
+  sp.dr = dr;
+  sp.dcp = (net && !G) ? INT_MAX : dc;
+  sp.sumDp = net ? sumD : INT_MIN;
+  sp.net = net;
+  sp.pf = c.o.path_filter != 0;
+  sp.h4 = (c.h & 3) == 0;
+  if (lane == 0) w->sumD = sumD;
+  __syncwarp();
+}
+
+// a8: commit the chosen server.  Returns 0 ok, 1 routing failed (R18), 2 overlay full.
+// Warp-cooperative: every lane runs the same control flow, lane 0 writes.
+template <typename LT>
+__device__ int commit_step(WCtx<LT>& c, WReq& q, const StepP& sp, int best) {
+  WScr* w = c.w;
+  const int lane = c.lane;
+  const int nos0 = w->nos;
+  c.ulog_n = 0;
+  int fail = 0;
+  {
+    int s = w_slot(c, best);
+    int cu = s >= 0 ? w->os_cpu[s] : c.cpu[best];
+    int ru = s >= 0 ? w->os_ram[s] : c.ram[best];
+    int qu = s >= 0 ? w->os_acc[s] : c.acc[best];
+    if (!w_set_server(c, best, cu - sp.dc, ru - sp.dr, 1, qu)) fail = 2;
+  }
+  const int nflow = w->nflow;
+  for (int fi = 0; fi < nflow && !fail; ++fi) {
+    const int v = w->fv[fi], D = w->fD[fi];
+    if (v == best) {
+      if (lane == 0) w->fpath[fi] = -1;
+      __syncwarp();
+      continue;
+    }
+    const int2 wp = wpath(c, best, v);
+    const int su = w_slot(c, best), sv = w_slot(c, v);
+    const int au = w->os_acc[su];
+    const int av = sv >= 0 ? w->os_acc[sv] : c.acc[v];
+    if (min(min(au, av), wp.y) < D) {
+      fail = 1;
+      break;
+    }
+    bool ok = w_set_server(c, best, w->os_cpu[su], w->os_ram[su], w->os_act[su], au - D);
+    const int cv = sv >= 0 ? w->os_cpu[sv] : c.cpu[v], rv = sv >= 0 ? w->os_ram[sv] : c.ram[v];
+    const int tv = sv >= 0 ? w->os_act[sv] : c.act[v];
+    ok = ok && w_set_server(c, v, cv, rv, tv, av - D);
+    int fid[4];
+    const int m = path_fids(c, best, v, wp.x, fid);
+    for (int t = 0; t < m && ok; ++t) ok = w_set_link(c, fid[t], fab_val(c, fid[t]) - D);
+    if (!ok) fail = 2;
+    if (lane == 0) w->fpath[fi] = wp.x;
+    __syncwarp();
+  }
+  if (fail == 1) {
+    w_undo(c, nos0);
+    if (lane == 0) {
+      if (w->nex < WX) w->ex[w->nex] = best;
+      w->nex += 1;
+    }
+  }
+  if (fail == 0) {
+    const int p = q.p;
+    if (lane == 0) w->pod_srv[p] = best;
+    __syncwarp();
+    if (q.hv0) {
+      int other = (q.pa0 == p && q.pb0 < p) ? q.pb0 : ((q.pb0 == p && q.pa0 < p) ? q.pa0 : -1);
+      if (other >= 0) {
+        int v = w->pod_srv[other];
+        for (int i = 0; i < nflow; ++i) if (w->fv[i] == v) q.path0 = w->fpath[i];
+      }
+    }
+    if (q.hv1) {
+      int other = (q.pa1 == p && q.pb1 < p) ? q.pb1 : ((q.pb1 == p && q.pa1 < p) ? q.pa1 : -1);
+      if (other >= 0) {
+        int v = w->pod_srv[other];
+        for (int i = 0; i < nflow; ++i) if (w->fv[i] == v) q.path1 = w->fpath[i];
+      }
+    }
+  }
+  __syncwarp();
+  return fail;
+}
+
+// a9: top-up (R19) in container order then vlink order; emit M_c, M_ec, c^a, bw^a.
+// Warp-cooperative like commit_step.
+template <typename LT>
+__device__ void finish_request(WCtx<LT>& c, const WReq& q, const OutDev& O) {
+  WScr* w = c.w;
+  const int lane = c.lane;
+  int my_ec = 0, my_er = 0;
+  for (int i = 0; i < q.nC; ++i) {
+    const int pd = __shfl_sync(NACS_FULL, q.cpod, i);
+    const int xc = __shfl_sync(NACS_FULL, q.cmax - q.cmin, i), xr = __shfl_sync(NACS_FULL, q.rmax - q.rmin, i);
+    const int s = w_slot(c, w->pod_srv[pd]);  // a placed server is always overlaid
+    const int ec = min(xc, w->os_cpu[s]);
+    const int er = min(xr, w->os_ram[s]);
+    __syncwarp();
+    if (lane == 0) { w->os_cpu[s] -= ec; w->os_ram[s] -= er; }
+    __syncwarp();
+    if (lane == i) { my_ec = ec; my_er = er; }
+  }
+  int my_bw0 = 0, my_bw1 = 0;
+  for (int e = 0; e < q.nV; ++e) {
+    const int src_lane = e & 31;
+    const bool hi = e >= 32;
+    const int es = __shfl_sync(NACS_FULL, hi ? q.pa1 : q.pa0, src_lane);
+    const int ed = __shfl_sync(NACS_FULL, hi ? q.pb1 : q.pb0, src_lane);
+    const int bmin = __shfl_sync(NACS_FULL, hi ? q.bn1 : q.bn0, src_lane);
+    const int bmax = __shfl_sync(NACS_FULL, hi ? q.bx1 : q.bx0, src_lane);
+    const int pid = __shfl_sync(NACS_FULL, hi ? q.path1 : q.path0, src_lane);
+    const int us = w->pod_srv[es], ud = w->pod_srv[ed];
+    int bw = bmax;
+    if (us != ud) {
+      const int ss = w_slot(c, us), sd = w_slot(c, ud);
+      int fid[4];
+      const int m = path_fids(c, us, ud, pid, fid);
+      int resid = min(w->os_acc[ss], w->os_acc[sd]);
+      for (int t = 0; t < m; ++t) resid = min(resid, fab_val(c, fid[t]));
+      const int extra = min(bmax - bmin, resid);
+      if (extra) {
+        __syncwarp();
+        if (lane == 0) { w->os_acc[ss] -= extra; w->os_acc[sd] -= extra; }
+        __syncwarp();
+        for (int t = 0; t < m; ++t) w_set_link(c, fid[t], fab_val(c, fid[t]) - extra, false);
+      }
+      bw = bmin + extra;
+    }
+    if (lane == src_lane) { if (hi) my_bw1 = bw; else my_bw0 = bw; }
+  }
+  if (q.hc) {
+    O.server[q.c0 + lane] = w->pod_srv[q.cpod];
+    O.cpu_a[q.c0 + lane] = q.cmin + my_ec;
+    O.ram_a[q.c0 + lane] = q.rmin + my_er;
+  }
+  if (q.hv0) {
+    const bool intra = w->pod_srv[q.pa0] == w->pod_srv[q.pb0];
+    O.bw_a[q.v0 + lane] = my_bw0;
+    O.path[q.v0 + lane] = intra ? -1 : q.path0;
+  }
+  if (q.hv1) {
+    const bool intra = w->pod_srv[q.pa1] == w->pod_srv[q.pb1];
+    O.bw_a[q.v0 + lane + 32] = my_bw1;
+    O.path[q.v0 + lane + 32] = intra ? -1 : q.path1;
+  }
+  if (lane == 0) O.status[q.r] = 1;
+  __syncwarp();
+}
+
+// The warps of a CTA advance in lockstep phases (prepare | pass A | pass B | commit), each
+// on its own request, so that all warps run the same loop at the same time (one copy of
+// the hot code in the instruction caches); within a phase no warp waits for another.
 template <typename LT>
 __global__ void __launch_bounds__(512, 1) k_batch_warp(Geo g, Opt o, const int* __restrict__ state, ReqsDev R,
-                                                       OutDev O, int4* ulog_all, int* next, int* deferred,
-                                                       int* n_deferred, unsigned long long* stats) {
+                                                       OutDev O, int4* ulog_all, int* next, const int* order,
+                                                       int* deferred, int* n_deferred, unsigned long long* stats) {
   extern __shared__ __align__(16) unsigned char dyn[];
   const int n = g.n, h = g.h, k = g.k, E = g.E;
   const int npad = (n + 127) & ~127;
@@ -412,398 +930,119 @@ __global__ void __launch_bounds__(512, 1) k_batch_warp(Geo g, Opt o, const int* 
     sacc[i] = in ? state[3 * n + i] : 0;
   }
   for (int i = threadIdx.x; i < nfab; i += blockDim.x) sfab[i] = (LT)state[4 * n + i];
-  __syncthreads();  // the only block barrier: the snapshot is complete
+  __syncthreads();
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   WCtx<LT> c;
   c.k = k; c.h = h; c.n = n; c.npad = npad; c.E = E; c.nfabea = E * h;
   c.magic = g.magic_h;
   c.cpu = scpu; c.ram = sram; c.act = sact; c.acc = sacc;
-  c.cpu4 = reinterpret_cast<const int4*>(scpu);
-  c.ram4 = reinterpret_cast<const int4*>(sram);
-  c.act4 = reinterpret_cast<const int4*>(sact);
-  c.acc4 = reinterpret_cast<const int4*>(sacc);
+  c.a_cpu = smem_addr(scpu) + 16u * lane;
+  c.a_ram = smem_addr(sram) + 16u * lane;
+  c.a_act = smem_addr(sact) + 16u * lane;
+  c.a_acc = smem_addr(sacc) + 16u * lane;
   c.fab = sfab;
   unsigned char* wb = dyn + off + (size_t)warp * wbytes;
   c.w = reinterpret_cast<WScr*>(wb);
   c.dirty = reinterpret_cast<unsigned*>(wb + sizeof(WScr));
   c.edgebad = c.dirty + nDW;
   c.pm = c.edgebad + nEW;
+  c.a_edge = smem_addr(c.edgebad);
+  c.nDW = nDW;
   c.ulog = ulog_all + ((size_t)blockIdx.x * (blockDim.x >> 5) + warp) * WLOG;
   c.ulog_n = 0;
   c.lane = lane;
   c.o = o;
   WScr* w = c.w;
-  for (int i = lane; i < nDW; i += 32) c.dirty[i] = 0u;
-  if (lane == 0) { w->nos = 0; w->nol = 0; }
-  __syncwarp();
-  const int nchunks = npad >> 7;
-  const bool h4 = (h & 3) == 0;
+  const double wd[4] = {o.wd[0], o.wd[1], o.wd[2], o.wd[3]};
   WStats ws = {0, 0, 0, 0, 0};
-  double wd[4] = {o.wd[0], o.wd[1], o.wd[2], o.wd[3]};
+  WReq q;
+  q.r = -1;
+  StepP sp;
+  TopsisP tp;
+  bool active = false, done = false, prep = false;
+  int best = -1;
 
   for (;;) {
-    int r = 0;
-    if (lane == 0) r = atomicAdd(next, 1);
-    r = __shfl_sync(NACS_FULL, r, 0);
-    if (r >= R.n) break;
-    const int c0 = R.coff[r], nC = R.coff[r + 1] - c0;
-    const int v0 = R.voff[r], nV = R.voff[r + 1] - v0;
-    if (nC > WC || nV > WV || nC <= 0 || nV < 0) {
-      if (nC > WC || nV > WV) {
-        if (lane == 0) deferred[atomicAdd(n_deferred, 1)] = r;
-        continue;
-      }
+    // ---- phase P: acquire a request; flows and fabric tables of its pod step
+    if (!active && !done) {
+      active = acquire(c, R, O, q, next, order, deferred, n_deferred, ws);
+      done = !active;
+      prep = active;
     }
-    // request registers: container `lane`, vlinks `lane` and `lane + 32`
-    const bool hc = lane < nC;
-    int cmin = 1, cmax = 1, rmin = 1, rmax = 1, cpod = 0;
-    if (hc) {
-      cmin = R.cpu_min[c0 + lane]; cmax = R.cpu_max[c0 + lane];
-      rmin = R.ram_min[c0 + lane]; rmax = R.ram_max[c0 + lane];
-      cpod = R.pod_of[c0 + lane];
+    if (active && prep) {
+      prepare_step(c, q, sp);
+      prep = false;
     }
-    const bool hv0 = lane < nV, hv1 = lane + 32 < nV;
-    int s0 = 0, d0 = 1, bn0 = 1, bx0 = 1, s1 = 0, d1 = 1, bn1 = 1, bx1 = 1;
-    if (hv0) { s0 = R.src[v0 + lane]; d0 = R.dst[v0 + lane]; bn0 = R.bw_min[v0 + lane]; bx0 = R.bw_max[v0 + lane]; }
-    if (hv1) { s1 = R.src[v0 + lane + 32]; d1 = R.dst[v0 + lane + 32]; bn1 = R.bw_min[v0 + lane + 32]; bx1 = R.bw_max[v0 + lane + 32]; }
-    // validation (R24), all in registers
-    bool bad = hc && (cmin <= 0 || rmin <= 0 || cmin > cmax || rmin > rmax || cpod < 0 || cpod >= nC);
-    bad |= hv0 && (s0 < 0 || s0 >= nC || d0 < 0 || d0 >= nC || s0 == d0 || bn0 <= 0 || bn0 > bx0);
-    bad |= hv1 && (s1 < 0 || s1 >= nC || d1 < 0 || d1 >= nC || s1 == d1 || bn1 <= 0 || bn1 > bx1);
-    unsigned used = __reduce_or_sync(NACS_FULL, hc && cpod >= 0 && cpod < 32 ? (1u << cpod) : 0u);
-    int maxp = (int)__reduce_max_sync(NACS_FULL, hc && cpod >= 0 ? (unsigned)cpod : 0u);
-    bool invalid = __any_sync(NACS_FULL, bad) || nC <= 0 || maxp >= 32 ||
-                   used != (maxp == 31 ? 0xffffffffu : ((1u << (maxp + 1)) - 1u));
-    if (invalid) {
-      if (hc) { O.server[c0 + lane] = -1; O.cpu_a[c0 + lane] = 0; O.ram_a[c0 + lane] = 0; }
-      if (hv0) { O.bw_a[v0 + lane] = 0; O.path[v0 + lane] = -1; }
-      if (hv1) { O.bw_a[v0 + lane + 32] = 0; O.path[v0 + lane + 32] = -1; }
-      if (lane == 0) { O.status[r] = -1; ws.invalid += 1; }
-      continue;
-    }
-    const int P = maxp + 1;
-    // pod demands (lane p): sum of c^min over the pod's containers
-    int pcpu = 0, pram = 0;
-    for (int i = 0; i < nC; ++i) {
-      int pd = __shfl_sync(NACS_FULL, cpod, i);
-      int cm = __shfl_sync(NACS_FULL, cmin, i);
-      int rm = __shfl_sync(NACS_FULL, rmin, i);
-      if (lane == pd) { pcpu += cm; pram += rm; }
-    }
-    // pods of the vlink endpoints
-    const int pa0 = __shfl_sync(NACS_FULL, cpod, s0 & 31), pb0 = __shfl_sync(NACS_FULL, cpod, d0 & 31);
-    const int pa1 = __shfl_sync(NACS_FULL, cpod, s1 & 31), pb1 = __shfl_sync(NACS_FULL, cpod, d1 & 31);
-    int path0 = -1, path1 = -1;
-    w->pod_srv[lane] = -1;
-    if (lane == 0) { w->nos = 0; w->nol = 0; }
-    __syncwarp();
-    bool rejected = false, defer = false;
-
-    for (int p = 0; p < P && !rejected && !defer; ++p) {
-      // ---- a1/a2: flows of pod p to placed peers, aggregated per server (R17)
-      int ov0 = -1, ov1 = -1;
-      if (hv0) {
-        int other = (pa0 == p && pb0 != p) ? pb0 : ((pb0 == p && pa0 != p) ? pa0 : -1);
-        if (other >= 0) ov0 = w->pod_srv[other];
-      }
-      if (hv1) {
-        int other = (pa1 == p && pb1 != p) ? pb1 : ((pb1 == p && pa1 != p) ? pa1 : -1);
-        if (other >= 0) ov1 = w->pod_srv[other];
-      }
-      bool has0 = ov0 >= 0, has1 = ov1 >= 0;
-      if (lane == 0) { w->nflow = 0; w->nex = 0; }
-      __syncwarp();
-      int sumD = 0;
-      for (;;) {
-        unsigned m0 = __ballot_sync(NACS_FULL, has0), m1 = __ballot_sync(NACS_FULL, has1);
-        if (!(m0 | m1)) break;
-        int src_l = m0 ? __ffs(m0) - 1 : __ffs(m1) - 1;
-        int cand = m0 ? ov0 : ov1;
-        int vsel = __shfl_sync(NACS_FULL, cand, src_l);
-        bool mine0 = has0 && ov0 == vsel, mine1 = has1 && ov1 == vsel;
-        int D = (int)__reduce_add_sync(NACS_FULL, (mine0 ? (unsigned)bn0 : 0u) + (mine1 ? (unsigned)bn1 : 0u));
-        has0 &= !mine0;
-        has1 &= !mine1;
-        sumD += D;
-        if (lane == 0) {  // insert sorted by server
-          int nf = w->nflow, i = nf;
-          while (i > 0 && w->fv[i - 1] > vsel) { w->fv[i] = w->fv[i - 1]; w->fD[i] = w->fD[i - 1]; --i; }
-          w->fv[i] = vsel;
-          w->fD[i] = D;
-          w->nflow = nf + 1;
-        }
-        __syncwarp();
-      }
-      const int nflow = w->nflow;
-      const bool net = o.path_filter && nflow > 0;
-      if (net) wfabric(c);
-      // fok (lane f) and G
-      bool Gl = true;
-      if (lane < nflow) {
-        int v = w->fv[lane], D = w->fD[lane];
-        int av = acc_val(c, v);
-        Gl = av >= D;
-        bool fk = av >= sumD - D;
-        for (int f2 = 0; f2 < nflow; ++f2)
-          if (f2 != lane && acc_val(c, w->fv[f2]) < w->fD[f2]) fk = false;
-        if (net) {
-          unsigned e = div_h((unsigned)v, c.magic);
-          if ((c.edgebad[e >> 5] >> (e & 31)) & 1u) fk = false;
-        }
-        w->fok[lane] = fk;
-      }
-      const bool G = __all_sync(NACS_FULL, Gl);
-      const int dc = __shfl_sync(NACS_FULL, pcpu, p), dr = __shfl_sync(NACS_FULL, pram, p);
-      StepP sp{dc, dr, sumD, net, G, o.path_filter != 0};
-      __syncwarp();
-
-      for (;;) {  // attempts of this pod step (R18 retries)
-        build_specials(c);
-        // ---- a3 + a4: filter and statistics
-        int nf = 0, nact = 0;
-        unsigned mn0 = UINT_MAX, mn1 = UINT_MAX, mn3 = UINT_MAX, mx0 = 0, mx1 = 0, mx3 = 0;
-        unsigned long long q0 = 0, q1 = 0, q3 = 0;
-        int spp = 0;
-        for (int ch = 0; ch < nchunks; ++ch) {
-          const int base = ch << 7;
-          Four f;
-          load_four(c, ch, base, spp, f);
-          const int u0 = base + 4 * lane;
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            int x0 = get_comp(f.c, j), x1 = get_comp(f.r, j), x2 = get_comp(f.a, j), x3 = get_comp(f.q, j);
-            bool ok = feasible(c, sp, u0 + j, x0, x1, x3, f.info[j]);
-            if (ok) {
-              nf += 1;
-              nact += x2;
-              mn0 = min(mn0, (unsigned)x0); mx0 = max(mx0, (unsigned)x0);
-              mn1 = min(mn1, (unsigned)x1); mx1 = max(mx1, (unsigned)x1);
-              mn3 = min(mn3, (unsigned)x3); mx3 = max(mx3, (unsigned)x3);
-              q0 += (unsigned long long)(unsigned)x0 * (unsigned)x0;
-              q1 += (unsigned long long)(unsigned)x1 * (unsigned)x1;
-              q3 += (unsigned long long)(unsigned)x3 * (unsigned)x3;
-            }
-          }
-        }
-        (void)h4;
-        nf = (int)__reduce_add_sync(NACS_FULL, (unsigned)nf);
-        ws.steps += 1;
-        ws.feas += (unsigned long long)nf;
-        if (nf == 0) { rejected = true; break; }  // R20
-        nact = (int)__reduce_add_sync(NACS_FULL, (unsigned)nact);
-        TopsisP tp;
-        tp.mn[0] = (int)__reduce_min_sync(NACS_FULL, mn0); tp.mx[0] = (int)__reduce_max_sync(NACS_FULL, mx0);
-        tp.mn[1] = (int)__reduce_min_sync(NACS_FULL, mn1); tp.mx[1] = (int)__reduce_max_sync(NACS_FULL, mx1);
-        tp.mn[3] = (int)__reduce_min_sync(NACS_FULL, mn3); tp.mx[3] = (int)__reduce_max_sync(NACS_FULL, mx3);
+    if (active) build_specials(c);
+    if (__syncthreads_and(done)) break;
+    // ---- phase A (a3 + a4): filter and statistics
+    bool stepping = active;
+    if (stepping) {
+      AccA acc = {0, 0, UINT_MAX, UINT_MAX, UINT_MAX, 0u, 0u, 0u, 0ull, 0ull, 0ull};
+      scan_stats(c, sp, acc);
+      const int nf = (int)__reduce_add_sync(NACS_FULL, (unsigned)acc.nf);
+      ws.steps += 1;
+      ws.feas += (unsigned long long)nf;
+      if (nf == 0) {  // R20: reject the whole request
+        emit_failed(O, q, lane, 0);
+        active = false;
+        stepping = false;
+      } else {
+        const int nact = (int)__reduce_add_sync(NACS_FULL, (unsigned)acc.nact);
+        tp.mn[0] = (int)__reduce_min_sync(NACS_FULL, acc.mn0); tp.mx[0] = (int)__reduce_max_sync(NACS_FULL, acc.mx0);
+        tp.mn[1] = (int)__reduce_min_sync(NACS_FULL, acc.mn1); tp.mx[1] = (int)__reduce_max_sync(NACS_FULL, acc.mx1);
+        tp.mn[3] = (int)__reduce_min_sync(NACS_FULL, acc.mn3); tp.mx[3] = (int)__reduce_max_sync(NACS_FULL, acc.mx3);
         tp.mn[2] = nact == nf ? 1 : 0;
         tp.mx[2] = nact > 0 ? 1 : 0;
-        unsigned long long sq[4] = {warp_sum_u64(q0), warp_sum_u64(q1), (unsigned long long)nact, warp_sum_u64(q3)};
+        unsigned long long sq[4] = {warp_sum_u64(acc.q0), warp_sum_u64(acc.q1), (unsigned long long)nact,
+                                    warp_sum_u64(acc.q3)};
         topsis_params(tp, wd, sq);
-        // ---- a5T + a7: closeness and top-2 argmax key
-        unsigned long long k1 = 0, k2 = 0;
-        spp = 0;
-        for (int ch = 0; ch < nchunks; ++ch) {
-          const int base = ch << 7;
-          Four f;
-          load_four(c, ch, base, spp, f);
-          const int u0 = base + 4 * lane;
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            int x0 = get_comp(f.c, j), x1 = get_comp(f.r, j), x2 = get_comp(f.a, j), x3 = get_comp(f.q, j);
-            if (feasible(c, sp, u0 + j, x0, x1, x3, f.info[j])) {
-              float rr = topsis32(tp, x0, x1, x2, x3);
-              top2_insert(k1, k2, score_key(rr, u0 + j));
-            }
-          }
-        }
-        warp_top2(k1, k2);
-        int best = (int)(0xFFFFFFFFu - (unsigned)(k1 & 0xFFFFFFFFull));
-        const float s1 = __uint_as_float((unsigned)(k1 >> 32)), s2 = __uint_as_float((unsigned)(k2 >> 32));
-        if (o.exact64 || (k2 != 0ull && s1 - s2 <= kTopsisDelta)) {  // R14: FP64 near-tie re-decision
-          const float thr = o.exact64 ? -1.0f : s1 - 2.0f * kTopsisDelta;
-          double bv = -DBL_MAX;
-          int bj = -1;
-          spp = 0;
-          for (int ch = 0; ch < nchunks; ++ch) {
-            const int base = ch << 7;
-            Four f;
-            load_four(c, ch, base, spp, f);
-            const int u0 = base + 4 * lane;
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              int x0 = get_comp(f.c, j), x1 = get_comp(f.r, j), x2 = get_comp(f.a, j), x3 = get_comp(f.q, j);
-              if (feasible(c, sp, u0 + j, x0, x1, x3, f.info[j]) && topsis32(tp, x0, x1, x2, x3) >= thr) {
-                double rr = topsis64(tp, x0, x1, x2, x3);
-                if (rr > bv || (rr == bv && u0 + j < bj)) { bv = rr; bj = u0 + j; }
-              }
-            }
-          }
-          warp_argmax64(bv, bj);
-          best = bj;
-          ws.fp64 += 1;
-        }
-        // ---- a8: commit (lane 0 writes the overlay; paths searched warp-wide)
-        const int nos0 = w->nos, nol0 = w->nol;
-        c.ulog_n = 0;
-        int fail = 0;
-        if (lane == 0) {
-          int s = os_slot(c, best);
-          int cu = s >= 0 ? w->os_cpu[s] : c.cpu[best];
-          int ru = s >= 0 ? w->os_ram[s] : c.ram[best];
-          int qu = s >= 0 ? w->os_acc[s] : c.acc[best];
-          if (!set_server(c, best, cu - dc, ru - dr, 1, qu)) fail = 2;
-        }
-        fail = __shfl_sync(NACS_FULL, fail, 0);
-        __syncwarp();
-        for (int fi = 0; fi < nflow && !fail; ++fi) {
-          const int v = w->fv[fi], D = w->fD[fi];
-          if (v == best) {
-            if (lane == 0) w->fpath[fi] = -1;
-            __syncwarp();
-            continue;
-          }
-          int2 wp = wpath(c, best, v);
-          if (lane == 0) {
-            int su = os_slot(c, best), sv = os_slot(c, v);
-            int au = w->os_acc[su];  // best is overlaid above
-            int av = sv >= 0 ? w->os_acc[sv] : c.acc[v];
-            int bott = min(min(au, av), wp.y);
-            if (bott < D) {
-              fail = 1;
-            } else {
-              bool ok = set_server(c, best, w->os_cpu[su], w->os_ram[su], w->os_act[su], au - D);
-              int sv2 = os_slot(c, v);
-              int cv = sv2 >= 0 ? w->os_cpu[sv2] : c.cpu[v], rv = sv2 >= 0 ? w->os_ram[sv2] : c.ram[v];
-              int tv = sv2 >= 0 ? w->os_act[sv2] : c.act[v];
-              ok = ok && set_server(c, v, cv, rv, tv, av - D);
-              int fid[4];
-              int m = path_fids(c, best, v, wp.x, fid);
-              for (int t = 0; t < m && ok; ++t) ok = set_link(c, fid[t], fab_val(c, fid[t]) - D);
-              if (!ok) fail = 2;
-              w->fpath[fi] = wp.x;
-            }
-          }
-          fail = __shfl_sync(NACS_FULL, fail, 0);
-          __syncwarp();
-        }
-        if (fail == 2) { defer = true; break; }  // overlay overflow: the CTA kernel takes it
-        if (fail == 1) {  // R18: undo this pod's commit, exclude the server, redo the pod step
-          if (lane == 0) {
-            undo_commit(c, nos0, nol0);
-            if (w->nex < WX) w->ex[w->nex] = best;
-            w->nex += 1;
-          }
-          __syncwarp();
-          ws.retries += 1;
-          if (w->nex > WX || w->nos + w->nex > WSP) { defer = true; break; }
-          continue;
-        }
-        if (lane == 0) w->pod_srv[p] = best;
-        __syncwarp();
-        // vlinks of this pod step record their flow's path
-        if (hv0) {
-          int other = (pa0 == p && pb0 < p) ? pb0 : ((pb0 == p && pa0 < p) ? pa0 : -1);
-          if (other >= 0) {
-            int v = w->pod_srv[other];
-            for (int i = 0; i < nflow; ++i) if (w->fv[i] == v) path0 = w->fpath[i];
-          }
-        }
-        if (hv1) {
-          int other = (pa1 == p && pb1 < p) ? pb1 : ((pb1 == p && pa1 < p) ? pa1 : -1);
-          if (other >= 0) {
-            int v = w->pod_srv[other];
-            for (int i = 0; i < nflow; ++i) if (w->fv[i] == v) path1 = w->fpath[i];
-          }
-        }
-        break;
       }
     }
-    if (defer) {
-      if (lane == 0) deferred[atomicAdd(n_deferred, 1)] = r;
-      for (int i = lane; i < nDW; i += 32) c.dirty[i] = 0u;
-      __syncwarp();
-      continue;
-    }
-    if (rejected) {
-      if (hc) { O.server[c0 + lane] = -1; O.cpu_a[c0 + lane] = 0; O.ram_a[c0 + lane] = 0; }
-      if (hv0) { O.bw_a[v0 + lane] = 0; O.path[v0 + lane] = -1; }
-      if (hv1) { O.bw_a[v0 + lane + 32] = 0; O.path[v0 + lane + 32] = -1; }
-      if (lane == 0) O.status[r] = 0;
-      for (int i = lane; i < nDW; i += 32) c.dirty[i] = 0u;
-      __syncwarp();
-      continue;
-    }
-    // ---- a9: top-up (R19), containers in index order then vlinks in index order
-    int my_ec = 0, my_er = 0;
-    for (int i = 0; i < nC; ++i) {
-      int pd = __shfl_sync(NACS_FULL, cpod, i);
-      int xc = __shfl_sync(NACS_FULL, cmax - cmin, i), xr = __shfl_sync(NACS_FULL, rmax - rmin, i);
-      int ec = 0, er = 0;
-      if (lane == 0) {
-        int u = w->pod_srv[pd];
-        int s = os_slot(c, u);  // a placed server is always overlaid
-        ec = min(xc, w->os_cpu[s]);
-        er = min(xr, w->os_ram[s]);
-        w->os_cpu[s] -= ec;
-        w->os_ram[s] -= er;
+    __syncthreads();
+    // ---- phase B (a5T + a7): closeness, argmax (lowest index), FP64 near-tie re-decision
+    if (stepping) {
+      AccB bb = {-1.0f, -1.0f, -1};
+      scan_score(c, sp, tp, bb);
+      const unsigned key1 = bb.b1 >= 0.0f ? __float_as_uint(bb.b1) + 1u : 0u;
+      const unsigned m1 = __reduce_max_sync(NACS_FULL, key1);
+      best = (int)__reduce_min_sync(NACS_FULL, key1 == m1 ? (unsigned)bb.i1 : UINT_MAX);
+      const bool winner = key1 == m1 && bb.i1 == best;
+      const unsigned key2 = winner ? (bb.b2 >= 0.0f ? __float_as_uint(bb.b2) + 1u : 0u) : key1;
+      const unsigned m2 = __reduce_max_sync(NACS_FULL, key2);
+      const float s1 = __uint_as_float(m1 - 1u), s2 = m2 ? __uint_as_float(m2 - 1u) : -1.0f;
+      if (o.exact64 || (m2 != 0u && s1 - s2 <= kTopsisDelta)) {
+        const float thr = o.exact64 ? -1.0f : s1 - 2.0f * kTopsisDelta;
+        double bv = -DBL_MAX;
+        int bj = -1;
+        scan_fp64(c, sp, tp, thr, bv, bj);
+        warp_argmax64(bv, bj);
+        best = bj;
+        ws.fp64 += 1;
       }
-      ec = __shfl_sync(NACS_FULL, ec, 0);
-      er = __shfl_sync(NACS_FULL, er, 0);
-      if (lane == i) { my_ec = ec; my_er = er; }
     }
-    __syncwarp();
-    int my_bw0 = 0, my_bw1 = 0;
-    for (int e = 0; e < nV; ++e) {
-      const int src_lane = e & 31;
-      const bool hi = e >= 32;
-      int es = __shfl_sync(NACS_FULL, hi ? pa1 : pa0, src_lane);
-      int ed = __shfl_sync(NACS_FULL, hi ? pb1 : pb0, src_lane);
-      int bmin = __shfl_sync(NACS_FULL, hi ? bn1 : bn0, src_lane);
-      int bmax = __shfl_sync(NACS_FULL, hi ? bx1 : bx0, src_lane);
-      int pid = __shfl_sync(NACS_FULL, hi ? path1 : path0, src_lane);
-      int bw = 0;
-      if (lane == 0) {
-        int us = w->pod_srv[es], ud = w->pod_srv[ed];
-        if (us == ud) {
-          bw = bmax;
+    __syncthreads();
+    // ---- phase C (a8, a9): commit; next pod, retry (R18), or request end
+    if (stepping) {
+      int fail = commit_step(c, q, sp, best);
+      if (fail == 1) {
+        ws.retries += 1;
+        if (w->nex > WX || w->nos + w->nex > WSP) fail = 2;
+      }
+      if (fail == 2) {  // overlay full: the CTA kernel takes the request
+        if (lane == 0) deferred[atomicAdd(n_deferred, 1)] = q.r;
+        active = false;
+      } else if (fail == 0) {
+        q.p += 1;
+        if (q.p == q.P) {
+          finish_request(c, q, O);
+          active = false;
         } else {
-          int ss = os_slot(c, us), sd = os_slot(c, ud);
-          int fid[4];
-          int m = path_fids(c, us, ud, pid, fid);
-          int resid = min(w->os_acc[ss], w->os_acc[sd]);
-          for (int t = 0; t < m; ++t) resid = min(resid, fab_val(c, fid[t]));
-          int extra = min(bmax - bmin, resid);
-          if (extra) {
-            w->os_acc[ss] -= extra;
-            w->os_acc[sd] -= extra;
-            for (int t = 0; t < m; ++t) set_link(c, fid[t], fab_val(c, fid[t]) - extra, false);  // overlaid already
-          }
-          bw = bmin + extra;
+          prep = true;
         }
       }
-      bw = __shfl_sync(NACS_FULL, bw, 0);
-      if (lane == src_lane) { if (hi) my_bw1 = bw; else my_bw0 = bw; }
     }
-    // emit M_c, M_ec, c^a, bw^a
-    if (hc) {
-      O.server[c0 + lane] = w->pod_srv[cpod];
-      O.cpu_a[c0 + lane] = cmin + my_ec;
-      O.ram_a[c0 + lane] = rmin + my_er;
-    }
-    if (hv0) {
-      bool intra = w->pod_srv[pa0] == w->pod_srv[pb0];
-      O.bw_a[v0 + lane] = my_bw0;
-      O.path[v0 + lane] = intra ? -1 : path0;
-    }
-    if (hv1) {
-      bool intra = w->pod_srv[pa1] == w->pod_srv[pb1];
-      O.bw_a[v0 + lane + 32] = my_bw1;
-      O.path[v0 + lane + 32] = intra ? -1 : path1;
-    }
-    if (lane == 0) O.status[r] = 1;
-    for (int i = lane; i < nDW; i += 32) c.dirty[i] = 0u;
-    __syncwarp();
   }
   if (lane == 0) {
     if (ws.steps) atomicAdd(&stats[ST_POD_STEPS], ws.steps);
@@ -811,6 +1050,33 @@ __global__ void __launch_bounds__(512, 1) k_batch_warp(Geo g, Opt o, const int* 
     if (ws.fp64) atomicAdd(&stats[ST_FP64], ws.fp64);
     if (ws.invalid) atomicAdd(&stats[ST_INVALID], ws.invalid);
     if (ws.feas) atomicAdd(&stats[ST_FEAS], ws.feas);
+  }
+}
+
+// Largest requests first (LPT): a counting sort of request indices by descending container
+// count, so that the last requests handed out are the shortest and the warps of a CTA
+// run out of work together.  One CTA; the order within a size class is arbitrary (the
+// requests are independent, R21, so results do not depend on it).
+__global__ void __launch_bounds__(1024) k_order_lpt(ReqsDev R, int* order) {
+  __shared__ int hist[MAXC + 2];
+  __shared__ int base[MAXC + 2];
+  for (int i = threadIdx.x; i < MAXC + 2; i += blockDim.x) hist[i] = 0;
+  __syncthreads();
+  for (int r = threadIdx.x; r < R.n; r += blockDim.x) {
+    int s = R.coff[r + 1] - R.coff[r];
+    s = s < 0 ? 0 : (s > MAXC ? MAXC + 1 : s);
+    atomicAdd(&hist[s], 1);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int s = MAXC + 1; s >= 0; --s) { base[s] = acc; acc += hist[s]; }
+  }
+  __syncthreads();
+  for (int r = threadIdx.x; r < R.n; r += blockDim.x) {
+    int s = R.coff[r + 1] - R.coff[r];
+    s = s < 0 ? 0 : (s > MAXC ? MAXC + 1 : s);
+    order[atomicAdd(&base[s], 1)] = r;
   }
 }
 
@@ -839,17 +1105,19 @@ int warp_kernel_warps(const Geo& g) {
 size_t warp_ulog_entries(int grid, int warps) { return (size_t)grid * warps * WLOG; }
 
 cudaError_t launch_batch_warp(const Geo& g, const Opt& o, const int* d_state, const ReqsDev& R, const OutDev& O,
-                              int4* ulog, int* next, int* deferred, int* n_deferred, unsigned long long* stats,
-                              int grid, int warps, cudaStream_t st) {
+                              int4* ulog, int* next, int* order, int* deferred, int* n_deferred,
+                              unsigned long long* stats, int grid, int warps, cudaStream_t st) {
   bool u16 = g.link_cap <= 65535;
+  k_order_lpt<<<1, 1024, 0, st>>>(R, order);
   size_t smem = warp_snapshot_bytes(g, u16) + (size_t)warps * warp_scratch_bytes(g);
   if (u16) {
     cudaFuncSetAttribute(k_batch_warp<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_batch_warp<uint16_t><<<grid, warps * 32, smem, st>>>(g, o, d_state, R, O, ulog, next, deferred, n_deferred,
-                                                           stats);
+    k_batch_warp<uint16_t><<<grid, warps * 32, smem, st>>>(g, o, d_state, R, O, ulog, next, order, deferred,
+                                                           n_deferred, stats);
   } else {
     cudaFuncSetAttribute(k_batch_warp<int>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_batch_warp<int><<<grid, warps * 32, smem, st>>>(g, o, d_state, R, O, ulog, next, deferred, n_deferred, stats);
+    k_batch_warp<int><<<grid, warps * 32, smem, st>>>(g, o, d_state, R, O, ulog, next, order, deferred, n_deferred,
+                                                      stats);
   }
   return cudaGetLastError();
 }
