@@ -359,8 +359,8 @@ nacs_status rank_impl(nacs_ctx* ctx, const nacs_options* opt, const nacs_pod_que
   qd.scores = (dev && scores) ? scores : ctx->scores.p;
   qd.best = dev ? best : ctx->misc.p;
   if (method == 0) {
-    CK(ctx->ahp_ws.reserve(10 * (size_t)g.n));
-    CK(ctx->w64.reserve(4 * (size_t)g.n));
+    CK(ctx->ahp_ws.reserve(nacs::ahp_workspace_bytes(g.n) / 4 + 4));
+    CK(ctx->w64.reserve(nacs::ahp_workspace_doubles(g.n)));
   }
   CK(nacs::launch_rank(g, o, ctx->state.p, qd, ctx->ahp_ws.p, ctx->w64.p, ctx->stats.p, ctx->stream));
   if (!dev) {
@@ -551,7 +551,7 @@ nacs_status nacs_schedule_batch(nacs_ctx* ctx, const nacs_options* opt, const na
   int grid = ctx->num_sms * per_sm;
   if (grid > R) grid = R;
   CK(ctx->ulog.reserve((size_t)grid * nacs::ULOG_CAP));
-  if (o.method == 0) CK(ctx->w64.reserve((size_t)grid * 4 * g.n));
+  if (o.method == 0) CK(ctx->w64.reserve((size_t)grid * nacs::ahp_workspace_doubles(g.n)));
   CK(ctx->misc.reserve(8));
   CK(cudaMemsetAsync(ctx->misc.p, 0, 4 * sizeof(int), ctx->stream));
   const int warps = o.method == NACS_TOPSIS && !ctx->cta_only ? nacs::warp_kernel_warps(g) : 0;
@@ -619,8 +619,8 @@ nacs_status nacs_schedule_request(nacs_ctx* ctx, const nacs_options* opt, const 
   }
   CK(ctx->ulog.reserve(nacs::ULOG_CAP));
   if (o.method == 0) {
-    CK(ctx->ahp_ws.reserve(10 * (size_t)g.n));
-    CK(ctx->w64.reserve(4 * (size_t)g.n));
+    CK(ctx->ahp_ws.reserve(nacs::ahp_workspace_bytes(g.n) / 4 + 4));
+    CK(ctx->w64.reserve(nacs::ahp_workspace_doubles(g.n)));
   }
   CK(nacs::launch_sequential(g, o, ctx->state.p, Rd, Od, ctx->ulog.p, ctx->ahp_ws.p, ctx->w64.p, ctx->stats.p,
                              ctx->stream));

@@ -88,9 +88,13 @@ struct LaunchInfo {
   size_t dyn_smem;
 };
 
+// AHP workspaces (nacs_kernels.cu): bytes of the sorted-level arrays for n servers, and
+// doubles of the FP64 re-decision workspace (per CTA)
+size_t ahp_workspace_bytes(int n);
+size_t ahp_workspace_doubles(int n);
 // dynamic shared memory of the batch kernel, 0 if it does not fit
 size_t batch_smem_bytes(const Geo& g, int method);
-int batch_block_size(const Geo& g);
+int batch_block_size(const Geo& g, int method);
 cudaError_t batch_occupancy(const Geo& g, int method, int* blocks_per_sm);
 
 cudaError_t launch_batch(const Geo& g, const Opt& o, const int* d_state, const ReqsDev& R, const OutDev& O,

@@ -20,6 +20,7 @@
 // of squares (64-bit).  Scores are FP32; an argmax whose top-2 FP32 gap is inside the
 // derived FP32 error bound is re-decided in FP64 over the near-max candidates (R14).
 #include <cfloat>
+#include <cstdlib>
 #include <climits>
 #include <cstdint>
 
@@ -30,6 +31,7 @@ namespace nacs {
 #define FULL 0xffffffffu
 
 // ---------------------------------------------------------------- helpers ----
+__host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
   return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
@@ -72,6 +74,11 @@ struct Scratch {
   double red_d[MAXW];
   int red_j[MAXW];
   int scan[MAXW];
+  double scand[MAXW][2];
+  int lvK, m1, nd, ntouched, touch_over;
+  int touched[2 * MAXC];   // servers with changed criteria in the current request (AHP)
+  float dval[2 * MAXC];    // dirty feasible values / servers of a pod step, sorted
+  int dsrv[2 * MAXC];
   // request fetch (batch)
   int next_req;
   // counters (thread 0)
@@ -87,11 +94,22 @@ struct Ctx {
   unsigned* maskw;     // [nW] feasibility bitmap of the current pod step
   unsigned* special;   // [nW] flow servers and excluded servers of the pod step
   unsigned* edgebad;   // [nEW] edge switches some flow cannot reach with its demand
-  float* xs;           // AHP: [4][nfcap] feasible criteria values (compacted, server order)
-  int* xid;            // AHP: [nfcap] server of each compacted slot
-  float* wcol;         // AHP: [4][nfcap] 1 / column sums
-  float* pg;           // AHP: [nfcap] FP32 global priorities
-  double* w64;         // AHP FP64 rescore: [4][nfcap]
+  // AHP workspace (ahp_carve): presorted orders, sorted levels, prefix sums
+  unsigned short* perm;  // [3][n2] servers in ascending CPU, RAM, access-bandwidth order
+  unsigned* dirty;       // [nW] servers whose criteria the current request has changed
+  float* pg;             // [n] FP32 global priorities, by server
+  int* lvl;              // [n] level (rank of distinct value) of each server, current criterion
+  float* keys;           // [n2] sorted feasible values
+  int* sidx;             // [n2] their servers
+  float* keys2;          // [n2] merge buffer
+  int* sidx2;            // [n2]
+  int* lst;            // [n2+1] first sorted position of each level
+  float2* lvm;         // [n2] (value, multiplicity) per level
+  float2* lvw;         // [n2] (value, multiplicity / column sum) per level
+  double* pa;          // [n2+2] exclusive prefix sums (multiplicity-weighted)
+  double* pb;          // [n2+2] exclusive prefix sums (multiplicity-weighted values)
+  float* l2;           // [n2] L2 per level
+  double* w64;         // FP64 re-decision: [n2] per-level weights + [nfcap] priorities (global)
   int nfcap;
   int2* ulog;          // undo log (global)
   int tid, B, NW, lane, warp;
@@ -104,6 +122,15 @@ __device__ __forceinline__ void st_set(Ctx& c, int off, int val) {
   c.ulog[s->log_n] = make_int2(off, c.st[off]);
   s->log_n += 1;
   c.st[off] = val;
+  if (c.dirty && off < 4 * c.g.n) {  // AHP: the server leaves its presorted position
+    const int u = off % c.g.n;
+    if (!((c.dirty[u >> 5] >> (u & 31)) & 1u)) {
+      c.dirty[u >> 5] |= 1u << (u & 31);
+      if (s->ntouched < 2 * MAXC) s->touched[s->ntouched] = u;
+      else s->touch_over = 1;
+      s->ntouched += 1;
+    }
+  }
 }
 __device__ __forceinline__ void undo_to(Ctx& c, int mark) {
   Scratch* s = c.s;
@@ -184,6 +211,32 @@ __device__ int block_exscan(Ctx& c, int x) {
   int r = s->scan[c.warp] + inc - x;
   __syncthreads();
   return r;
+}
+
+// Exclusive block scan of two doubles per thread (returned in place).
+__device__ void block_exscan_d2(Ctx& c, double& a, double& b) {
+  Scratch* s = c.s;
+  double ia = a, ib = b;
+  for (int o = 1; o < 32; o <<= 1) {
+    double ya = __shfl_up_sync(FULL, ia, o), yb = __shfl_up_sync(FULL, ib, o);
+    if (c.lane >= o) { ia += ya; ib += yb; }
+  }
+  if (c.lane == 31) { s->scand[c.warp][0] = ia; s->scand[c.warp][1] = ib; }
+  __syncthreads();
+  if (c.warp == 0) {
+    double ta = c.lane < c.NW ? s->scand[c.lane][0] : 0.0, tb = c.lane < c.NW ? s->scand[c.lane][1] : 0.0;
+    double xa = ta, xb = tb;
+    for (int o = 1; o < 32; o <<= 1) {
+      double ya = __shfl_up_sync(FULL, xa, o), yb = __shfl_up_sync(FULL, xb, o);
+      if (c.lane >= o) { xa += ya; xb += yb; }
+    }
+    if (c.lane < c.NW) { s->scand[c.lane][0] = xa - ta; s->scand[c.lane][1] = xb - tb; }
+  }
+  __syncthreads();
+  const double ra = s->scand[c.warp][0] + ia - a, rb = s->scand[c.warp][1] + ib - b;
+  __syncthreads();
+  a = ra;
+  b = rb;
 }
 
 // ------------------------------------------------------ AHP L1 (Eq. 9, R10) --
@@ -453,43 +506,370 @@ __device__ void select_topsis(Ctx& c, float* scores_out) {
 }
 
 // --------------------------------------------------------------- AHP --------
-// a5A + a6A (Eq. 9-10, readings R7-R11): per criterion c with lo < hi over
-// F, d_ij = 9 (x_i - x_j) / (hi - lo), a_ij = cell(d_ij); colsum_j = sum_i a_ij;
-// L2_c[i] = (1/nf) sum_j a_ij / colsum_j; PG[i] = sum_c L1[c] L2_c[i].  The pairwise
-// matrix is never stored: each thread streams rows of the compacted criteria.
-__device__ __forceinline__ float ahp_cell32(float d, int rule) {
-  float pos = rule ? 1.0f + d : d;
-  float neg = rcp_approx(rule ? 1.0f - d : -d);
-  return d > 0.f ? pos : (d < 0.f ? neg : 1.0f);
+// a5A + a6A (Eq. 9-10, readings R7-R11).  Per criterion c with lo < hi over F,
+// d_ij = s (x_i - x_j) with s = 9 / (hi - lo), a_ij = cell(d_ij), colsum_j = sum_i a_ij,
+// L2_c[i] = (1/nf) sum_j a_ij / colsum_j, PG[i] = sum_c L1[c] L2_c[i].
+//
+// Sorted-level evaluation (no matrix, no compares).  The feasible values of c are sorted
+// and collapsed into K levels v_0 < ... < v_{K-1} with multiplicities m_l.  A cell depends
+// only on the two levels, so with the literal rule (R8: cell = d for d > 0, 1/(-d) for
+// d < 0, 1 for d = 0):
+//   colsum(l) = s * sum_{k>l} m_k (v_k - v_l) + m_l + (1/s) sum_{k<l} m_k / (v_l - v_k)
+//   nf L2(l)  = s * sum_{k<l} w_k (v_l - v_k) + w_l + (1/s) sum_{k>l} w_k / (v_k - v_l),
+// with w_k = m_k / colsum(k).  The linear sums come from exact double prefix sums; the
+// reciprocal sums cost one reciprocal per unordered pair of levels per pass.  The shifted
+// rule (1 + d, 1 / (1 - d)) adds the counts and uses 1 / (1 + s (v - v')).
+__host__ __device__ inline int next_pow2(int x) {
+  int p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+// doubles of the FP64 re-decision workspace (per-level weights, per-level L2, priorities)
+__host__ __device__ inline size_t ahp_w64_doubles(int n) { return 2 * (size_t)next_pow2(n) + (size_t)n; }
+// bytes of the AHP workspace for n servers (ahp_carve layout)
+__host__ __device__ inline size_t ahp_bytes(int n) {
+  size_t n2 = (size_t)next_pow2(n);
+  return align16(6 * n2) + align16(4 * (size_t)((n + 31) / 32)) + 2 * align16(4 * (size_t)n) + 4 * align16(4 * n2) +
+         align16(4 * (n2 + 1)) + 2 * align16(8 * n2) + 2 * align16(8 * (n2 + 2)) + align16(4 * n2);
+}
+__device__ void ahp_carve(Ctx& c, unsigned char* base, int n) {
+  size_t n2 = (size_t)next_pow2(n), off = 0;
+  auto take = [&](size_t bytes) { unsigned char* p = base + off; off += align16(bytes); return p; };
+  c.perm = reinterpret_cast<unsigned short*>(take(6 * n2));
+  c.dirty = reinterpret_cast<unsigned*>(take(4 * (size_t)((n + 31) / 32)));
+  c.pg = reinterpret_cast<float*>(take(4 * (size_t)n));
+  c.lvl = reinterpret_cast<int*>(take(4 * (size_t)n));
+  c.keys = reinterpret_cast<float*>(take(4 * n2));
+  c.sidx = reinterpret_cast<int*>(take(4 * n2));
+  c.keys2 = reinterpret_cast<float*>(take(4 * n2));
+  c.sidx2 = reinterpret_cast<int*>(take(4 * n2));
+  c.lst = reinterpret_cast<int*>(take(4 * (n2 + 1)));
+  c.lvm = reinterpret_cast<float2*>(take(8 * n2));
+  c.lvw = reinterpret_cast<float2*>(take(8 * n2));
+  c.pa = reinterpret_cast<double*>(take(8 * (n2 + 2)));
+  c.pb = reinterpret_cast<double*>(take(8 * (n2 + 2)));
+  c.l2 = reinterpret_cast<float*>(take(4 * n2));
+  c.nfcap = n;
+}
+
+// criterion index in the state (cpu 0, ram 1, access bandwidth 3) of presorted list ci
+__device__ __forceinline__ int crit_of(int ci) { return ci == 2 ? 3 : ci; }
+
+// Bitonic sort of keys[0..P2) ascending, payload sidx.  All threads.
+__device__ void bitonic(Ctx& c, int P2) {
+  for (int k = 2; k <= P2; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = c.tid; i < P2; i += c.B) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const float a = c.keys[i], b = c.keys[ixj];
+          if ((a > b) == ((i & k) == 0)) {
+            c.keys[i] = b;
+            c.keys[ixj] = a;
+            const int t = c.sidx[i];
+            c.sidx[i] = c.sidx[ixj];
+            c.sidx[ixj] = t;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// Presort all servers by CPU, RAM and access bandwidth on the current state, and forget
+// the dirty servers.  Once per snapshot (batch), per request (sequential), per query.
+__device__ void ahp_presort(Ctx& c) {
+  Scratch* s = c.s;
+  const int n = c.g.n, P2 = next_pow2(n);
+  for (int ci = 0; ci < 3; ++ci) {
+    const int* x = c.st + crit_of(ci) * n;
+    for (int i = c.tid; i < P2; i += c.B) {
+      c.keys[i] = i < n ? (float)x[i] : FLT_MAX;
+      c.sidx[i] = i;
+    }
+    __syncthreads();
+    bitonic(c, P2);
+    for (int i = c.tid; i < n; i += c.B) c.perm[ci * P2 + i] = (unsigned short)c.sidx[i];
+    __syncthreads();
+  }
+  for (int w = c.tid; w < c.nW; w += c.B) c.dirty[w] = 0u;
+  if (c.tid == 0) { s->ntouched = 0; s->touch_over = 0; }
+  __syncthreads();
+}
+
+// Forget the servers the finished request touched (the state is the snapshot again).
+__device__ void ahp_clear_dirty(Ctx& c) {
+  Scratch* s = c.s;
+  if (c.tid == 0) {
+    const int nt = min(s->ntouched, 2 * MAXC);
+    for (int i = 0; i < nt; ++i) {
+      const int u = s->touched[i];
+      c.dirty[u >> 5] &= ~(1u << (u & 31));
+    }
+    s->ntouched = 0;
+  }
+  __syncthreads();
+}
+
+// Levels of the m sorted values keys[0..m) (servers sidx): lvm[l] = (value, multiplicity),
+// lvl[server] = level.  Returns K.  All threads.
+__device__ int ahp_levels_sorted(Ctx& c, int m) {
+  Scratch* s = c.s;
+  const int B = c.B, tid = c.tid;
+  const int ipt = (m + B - 1) / B;
+  const int i0 = min(tid * ipt, m), i1 = min(i0 + ipt, m);
+  int cnt = 0;
+  for (int i = i0; i < i1; ++i) cnt += (i == 0 || c.keys[i] != c.keys[i - 1]);
+  int l = block_exscan(c, cnt);
+  if (tid == B - 1) s->lvK = l + cnt;
+  for (int i = i0; i < i1; ++i) {
+    if (i == 0 || c.keys[i] != c.keys[i - 1]) {
+      c.lvm[l].x = c.keys[i];
+      c.lst[l] = i;
+      ++l;
+    }
+    c.lvl[c.sidx[i]] = l - 1;
+  }
+  __syncthreads();
+  const int K = s->lvK;
+  for (int q = tid; q < K; q += B) c.lvm[q].y = (float)((q + 1 < K ? c.lst[q + 1] : m) - c.lst[q]);
+  __syncthreads();
+  return K;
+}
+
+__device__ __forceinline__ bool feas_bit(const Ctx& c, int u) { return (c.maskw[u >> 5] >> (u & 31)) & 1u; }
+
+// Sorted feasible values of presorted criterion ci: walk the presorted order keeping the
+// feasible servers not touched by this request, then merge in the touched feasible ones
+// (their current values).  Returns K (levels built).  All threads.
+__device__ int ahp_levels_presorted(Ctx& c, int ci) {
+  Scratch* s = c.s;
+  const int n = c.g.n, P2 = next_pow2(n);
+  const int* x = c.st + crit_of(ci) * n;
+  const unsigned short* perm = c.perm + ci * P2;
+  const int ipt = (n + c.B - 1) / c.B;
+  const int i0 = min(c.tid * ipt, n), i1 = min(i0 + ipt, n);
+  int cnt = 0;
+  for (int i = i0; i < i1; ++i) {
+    const int u = perm[i];
+    cnt += feas_bit(c, u) && !((c.dirty[u >> 5] >> (u & 31)) & 1u);
+  }
+  int pos = block_exscan(c, cnt);
+  if (c.tid == c.B - 1) s->m1 = pos + cnt;
+  for (int i = i0; i < i1; ++i) {
+    const int u = perm[i];
+    if (feas_bit(c, u) && !((c.dirty[u >> 5] >> (u & 31)) & 1u)) {
+      c.keys2[pos] = (float)x[u];
+      c.sidx2[pos] = u;
+      ++pos;
+    }
+  }
+  if (c.tid == 0) {  // touched feasible servers, insertion-sorted by current value
+    int d = 0;
+    for (int t = 0; t < s->ntouched; ++t) {
+      const int u = s->touched[t];
+      if (!feas_bit(c, u)) continue;
+      const float v = (float)x[u];
+      int j = d;
+      while (j > 0 && s->dval[j - 1] > v) { s->dval[j] = s->dval[j - 1]; s->dsrv[j] = s->dsrv[j - 1]; --j; }
+      s->dval[j] = v;
+      s->dsrv[j] = u;
+      ++d;
+    }
+    s->nd = d;
+  }
+  __syncthreads();
+  const int m1 = s->m1, d = s->nd;
+  for (int i = c.tid; i < m1; i += c.B) {  // main values shift past the touched ones below them
+    const float v = c.keys2[i];
+    int lo = 0, hi = d;
+    while (lo < hi) { int mid = (lo + hi) >> 1; if (s->dval[mid] < v) lo = mid + 1; else hi = mid; }
+    c.keys[i + lo] = v;
+    c.sidx[i + lo] = c.sidx2[i];
+  }
+  for (int j = c.tid; j < d; j += c.B) {  // touched values after the main ones <= them
+    const float v = s->dval[j];
+    int lo = 0, hi = m1;
+    while (lo < hi) { int mid = (lo + hi) >> 1; if (c.keys2[mid] <= v) lo = mid + 1; else hi = mid; }
+    c.keys[j + lo] = v;
+    c.sidx[j + lo] = s->dsrv[j];
+  }
+  __syncthreads();
+  return ahp_levels_sorted(c, m1 + d);
+}
+
+// Levels of the Fragmentation criterion f_u in {0,1}: no sort needed.
+__device__ int ahp_levels_active(Ctx& c) {
+  Scratch* s = c.s;
+  const int n = c.g.n;
+  const int nf = s->nf, nact = s->nact;
+  const int K = (nact > 0) + (nact < nf);
+  const int base = nact < nf ? 0 : 1;  // level of f_u = 0 is 0 when present
+  for (int u = c.tid; u < n; u += c.B)
+    if (feas_bit(c, u)) c.lvl[u] = c.st[2 * n + u] ? (nact < nf ? 1 : 0) : 0;
+  if (c.tid == 0) {
+    int l = 0;
+    if (nact < nf) c.lvm[l++] = make_float2(0.0f, (float)(nf - nact));
+    if (nact > 0) c.lvm[l++] = make_float2(1.0f, (float)nact);
+  }
+  (void)base;
+  __syncthreads();
+  return K;
+}
+
+// Exclusive prefix sums over K levels of (y, y * x) of lv[] into pa, pb (pa[K], pb[K] totals).
+__device__ void ahp_prefix(Ctx& c, int K, const float2* lv) {
+  const int ipt = (K + c.B - 1) / c.B;
+  const int i0 = min(c.tid * ipt, K), i1 = min(i0 + ipt, K);
+  double a = 0, b = 0;
+  for (int i = i0; i < i1; ++i) { a += (double)lv[i].y; b += (double)lv[i].y * (double)lv[i].x; }
+  double ea = a, eb = b;
+  block_exscan_d2(c, ea, eb);
+  for (int i = i0; i < i1; ++i) {
+    c.pa[i] = ea;
+    c.pb[i] = eb;
+    ea += (double)lv[i].y;
+    eb += (double)lv[i].y * (double)lv[i].x;
+  }
+  if (c.tid == c.B - 1) { c.pa[K] = ea; c.pb[K] = eb; }
+  __syncthreads();
+}
+
+// sum over k in [k0, k1) of arr[k].y / D(k), D = (v - arr[k].x) (pass 1, below) or
+// (arr[k].x - v) (pass 2, above), or 1 + s * that under the shifted rule.  FP32 with MUFU
+// reciprocals; four interleaved accumulators per chunk of 32 terms (error analysis in
+// DESIGN.md §5 covers any chunking of at most 32 terms).
+template <bool ABOVE>
+__device__ __forceinline__ float rsum_f32(const float2* arr, int k0, int k1, float v, float sc, int rule) {
+  float outer = 0.f;
+  int k = k0;
+  float h0 = 0.f;
+  for (; k < k1 && (k & 3); ++k) {  // head up to a multiple of 4
+    const float2 o = arr[k];
+    const float d = ABOVE ? o.x - v : v - o.x;
+    h0 += o.y * rcp_approx(rule ? fmaf(sc, d, 1.0f) : d);
+  }
+  outer += h0;
+  for (; k + 32 <= k1; k += 32) {
+    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+    const float4* q = reinterpret_cast<const float4*>(arr + k);
+#pragma unroll
+    for (int t = 0; t < 16; t += 2) {
+      const float4 x = q[t], y = q[t + 1];  // levels k+2t .. k+2t+3
+      const float d0 = ABOVE ? x.x - v : v - x.x, d1 = ABOVE ? x.z - v : v - x.z;
+      const float d2 = ABOVE ? y.x - v : v - y.x, d3 = ABOVE ? y.z - v : v - y.z;
+      a0 = fmaf(x.y, rcp_approx(rule ? fmaf(sc, d0, 1.0f) : d0), a0);
+      a1 = fmaf(x.w, rcp_approx(rule ? fmaf(sc, d1, 1.0f) : d1), a1);
+      a2 = fmaf(y.y, rcp_approx(rule ? fmaf(sc, d2, 1.0f) : d2), a2);
+      a3 = fmaf(y.w, rcp_approx(rule ? fmaf(sc, d3, 1.0f) : d3), a3);
+    }
+    outer += (a0 + a1) + (a2 + a3);
+  }
+  float t0 = 0.f;
+  for (; k < k1; ++k) {
+    const float2 o = arr[k];
+    const float d = ABOVE ? o.x - v : v - o.x;
+    t0 += o.y * rcp_approx(rule ? fmaf(sc, d, 1.0f) : d);
+  }
+  return outer + t0;
+}
+
+// FP32 passes over the K levels of criterion kc -> l2out[l] = L2 of level l.
+// Each thread takes level pairs (l, K-1-l) so every pair holds K-1 terms per pass.
+__device__ void ahp_passes_f32(Ctx& c, int kc, int K, int m, float* l2out) {
+  Scratch* s = c.s;
+  const int rule = c.o.ahp_rule;
+  const double sd = s->ahp_scaled[kc];
+  const float sc = (float)sd;
+  const double inv_sd = 1.0 / sd;
+  ahp_prefix(c, K, c.lvm);
+  const double PAK = c.pa[K], PBK = c.pb[K];
+  const int half = (K + 1) >> 1;
+  for (int t = c.tid; t < half; t += c.B) {
+    for (int side = 0; side < 2; ++side) {
+      const int l = side ? K - 1 - t : t;
+      if (side && l == t) break;
+      const float2 me = c.lvm[l];
+      const float rec = rsum_f32<false>(c.lvm, 0, l, me.x, sc, rule);
+      const double cgt = PAK - c.pa[l + 1];
+      const double G = (PBK - c.pb[l + 1]) - cgt * (double)me.x;  // sum_{k>l} m_k (v_k - v_l), exact
+      const double col = rule ? cgt + sd * G + (double)me.y + (double)rec
+                              : sd * G + (double)me.y + (double)rec * inv_sd;
+      c.lvw[l] = make_float2(me.x, (float)((double)me.y / col));
+    }
+  }
+  __syncthreads();
+  ahp_prefix(c, K, c.lvw);
+  for (int t = c.tid; t < half; t += c.B) {
+    for (int side = 0; side < 2; ++side) {
+      const int l = side ? K - 1 - t : t;
+      if (side && l == t) break;
+      const float2 me = c.lvw[l];
+      const float rec = rsum_f32<true>(c.lvw, l + 1, K, me.x, sc, rule);
+      const double lin = (double)me.x * c.pa[l] - c.pb[l];  // sum_{k<l} w_k (v_l - v_k)
+      const double L = rule ? c.pa[l] + sd * lin + (double)me.y + (double)rec
+                            : sd * lin + (double)me.y + (double)rec * inv_sd;
+      l2out[l] = (float)(L / (double)m);
+    }
+  }
+  __syncthreads();
+}
+
+// FP64 passes (the rare R14 re-decision): same formulation, IEEE reciprocals, exact
+// prefix sums of the FP64 weights.  w64[0..K) holds the weights.
+__device__ void ahp_passes_f64(Ctx& c, int kc, int K, int m, double* l2out) {
+  Scratch* s = c.s;
+  const int rule = c.o.ahp_rule;
+  const double sd = s->ahp_scaled[kc];
+  ahp_prefix(c, K, c.lvm);
+  const double PAK = c.pa[K], PBK = c.pb[K];
+  for (int l = c.tid; l < K; l += c.B) {
+    const double vl = c.lvm[l].x, ml = c.lvm[l].y;
+    double rec = 0;
+    for (int k = 0; k < l; ++k) {
+      const double d = vl - (double)c.lvm[k].x;
+      rec += (double)c.lvm[k].y / (rule ? 1.0 + sd * d : d);
+    }
+    const double cgt = PAK - c.pa[l + 1];
+    const double G = (PBK - c.pb[l + 1]) - cgt * vl;
+    const double col = rule ? cgt + sd * G + ml + rec : sd * G + ml + rec / sd;
+    c.w64[l] = ml / col;
+  }
+  __syncthreads();
+  for (int l = c.tid; l < K; l += c.B) {
+    const double vl = c.lvm[l].x;
+    double rec = 0, a = 0, b = 0;
+    for (int k = l + 1; k < K; ++k) {
+      const double d = (double)c.lvm[k].x - vl;
+      rec += c.w64[k] / (rule ? 1.0 + sd * d : d);
+    }
+    for (int q = 0; q < l; ++q) { a += c.w64[q]; b += c.w64[q] * (double)c.lvm[q].x; }
+    const double lin = vl * a - b;
+    const double L = rule ? a + sd * lin + c.w64[l] + rec : sd * lin + c.w64[l] + rec / sd;
+    l2out[l] = L / (double)m;
+  }
+  __syncthreads();
+}
+
+// levels of criterion k (0 cpu, 1 ram, 2 active, 3 access bandwidth) over F
+__device__ int ahp_levels_of(Ctx& c, int k) {
+  Scratch* s = c.s;
+  if (k == 2) return ahp_levels_active(c);
+  if (s->touch_over) {  // more touched servers than the merge list holds: presort again
+    ahp_presort(c);
+    if (c.tid == 0) s->touch_over = 2;  // the snapshot order must be rebuilt after the request
+    __syncthreads();
+  }
+  return ahp_levels_presorted(c, k == 3 ? 2 : k);
 }
 
 template <bool WRITE_SCORES>
 __device__ void select_ahp(Ctx& c, float* scores_out) {
   Scratch* s = c.s;
-  const Geo& g = c.g;
-  const int n = g.n;
+  const int n = c.g.n;
   const int nf = s->nf;
-  const int cap = c.nfcap;
-  // compaction of F in server order
-  int wpt = (c.nW + c.B - 1) / c.B;
-  int w0 = c.tid * wpt, w1 = min(w0 + wpt, c.nW);
-  int cnt = 0;
-  for (int w = w0; w < w1; ++w) cnt += __popc(c.maskw[w]);
-  int pos = block_exscan(c, cnt);
-  for (int w = w0; w < w1; ++w) {
-    unsigned bits = c.maskw[w];
-    while (bits) {
-      int b = __ffs(bits) - 1;
-      bits &= bits - 1;
-      int u = w * 32 + b;
-      c.xs[0 * cap + pos] = (float)c.st[u];
-      c.xs[1 * cap + pos] = (float)c.st[n + u];
-      c.xs[2 * cap + pos] = (float)c.st[2 * n + u];
-      c.xs[3 * cap + pos] = (float)c.st[3 * n + u];
-      c.xid[pos] = u;
-      ++pos;
-    }
-  }
+  for (int u = c.tid; u < n; u += c.B) c.pg[u] = 0.0f;
   if (c.tid == 0) {
     for (int k = 0; k < 4; ++k) {
       int lo = s->mn[k], hi = s->mx[k];
@@ -497,63 +877,30 @@ __device__ void select_ahp(Ctx& c, float* scores_out) {
       double sc = hi > lo ? 9.0 / (double)(hi - lo) : 0.0;
       s->ahp_scaled[k] = sc;
       s->ahp_scale[k] = (float)sc;
-      if (hi > lo) s->c_pairs += (unsigned long long)nf * (unsigned long long)(nf - 1) / 2;
     }
   }
   __syncthreads();
-  const int rule = c.o.ahp_rule;
-  // pass 1: 1 / column sums
+  const float inv_nf = rcp_approx((float)nf);
   for (int k = 0; k < 4; ++k) {
-    if (s->ahp_const[k]) continue;
-    const float* x = c.xs + k * cap;
-    const float sc = s->ahp_scale[k];
-    for (int j = c.tid; j < nf; j += c.B) {
-      float xj = x[j];
-      float outer = 0.f;
-      int i = 0;
-      for (; i + 32 <= nf; i += 32) {
-        float inner = 0.f;
-#pragma unroll 8
-        for (int t = 0; t < 32; ++t) inner += ahp_cell32((x[i + t] - xj) * sc, rule);
-        outer += inner;
-      }
-      float inner = 0.f;
-      for (; i < nf; ++i) inner += ahp_cell32((x[i] - xj) * sc, rule);
-      outer += inner;
-      c.wcol[k * cap + j] = rcp_approx(outer);
+    if (s->ahp_const[k]) {  // every value equal: L2 = 1/nf
+      const float add = s->L1[k] * inv_nf;
+      for (int u = c.tid; u < n; u += c.B) c.pg[u] += add;
+      __syncthreads();
+      continue;
     }
+    const int K = ahp_levels_of(c, k);
+    if (c.tid == 0) s->c_pairs += (unsigned long long)K * (unsigned long long)(K - 1) / 2;
+    ahp_passes_f32(c, k, K, nf, c.l2);
+    for (int u = c.tid; u < n; u += c.B)
+      if (feas_bit(c, u)) c.pg[u] = fmaf(s->L1[k], c.l2[c.lvl[u]], c.pg[u]);
+    __syncthreads();
   }
-  __syncthreads();
-  // pass 2: global priority
-  float a[4];
-  for (int k = 0; k < 4; ++k) a[k] = s->L1[k] * rcp_approx((float)nf);
   unsigned long long k1 = 0, k2 = 0;
-  for (int i = c.tid; i < nf; i += c.B) {
-    float pgv = 0.f;
-    for (int k = 0; k < 4; ++k) {
-      if (s->ahp_const[k]) { pgv += a[k]; continue; }
-      const float* x = c.xs + k * cap;
-      const float* w = c.wcol + k * cap;
-      const float sc = s->ahp_scale[k];
-      float xi = x[i];
-      float outer = 0.f;
-      int j = 0;
-      for (; j + 32 <= nf; j += 32) {
-        float inner = 0.f;
-#pragma unroll 8
-        for (int t = 0; t < 32; ++t) inner = fmaf(ahp_cell32((xi - x[j + t]) * sc, rule), w[j + t], inner);
-        outer += inner;
-      }
-      float inner = 0.f;
-      for (; j < nf; ++j) inner = fmaf(ahp_cell32((xi - x[j]) * sc, rule), w[j], inner);
-      outer += inner;
-      pgv = fmaf(a[k], outer, pgv);
-    }
-    c.pg[i] = pgv;
-    int u = c.xid[i];
+  for (int u = c.tid; u < n; u += c.B) {
+    if (!feas_bit(c, u)) continue;
+    const float pgv = c.pg[u];
     if (WRITE_SCORES) scores_out[u] = pgv;
-    unsigned long long key = ((unsigned long long)__float_as_uint(pgv) << 32) | (0xFFFFFFFFu - (unsigned)u);
-    top2_insert(k1, k2, key);
+    top2_insert(k1, k2, score_key(pgv, u));
   }
   block_top2(c, k1, k2);
   const float drel = ahp_delta_rel(nf);
@@ -564,36 +911,31 @@ __device__ void select_ahp(Ctx& c, float* scores_out) {
     s->amb = c.o.exact64 || (s->key2 != 0ull && s2 >= s1 * (1.0f - drel));
   }
   __syncthreads();
-  if (s->amb) {  // FP64: exact column sums, then PG of the near-max candidates
-    for (int k = 0; k < 4; ++k) {
-      if (s->ahp_const[k]) continue;
-      const float* x = c.xs + k * cap;
-      const double sc = s->ahp_scaled[k];
-      for (int j = c.tid; j < nf; j += c.B) {
-        double xj = x[j], sum = 0;
-        for (int i = 0; i < nf; ++i) sum += ahp_cell64(((double)x[i] - xj) * sc, rule);
-        c.w64[k * cap + j] = 1.0 / sum;
-      }
-    }
+  if (s->amb) {  // FP64 re-decision (R14): the same level formulation in double, all of F
+    const int n2 = next_pow2(n);
+    double* l2d = c.w64 + n2;      // w64: [n2] weights | [n2] L2 per level | [n] priorities
+    double* pg64 = c.w64 + 2 * n2;
+    for (int u = c.tid; u < n; u += c.B) pg64[u] = 0.0;
     __syncthreads();
-    float s1 = __uint_as_float((unsigned)(s->key1 >> 32));
-    float thr = c.o.exact64 ? -1.0f : s1 * (1.0f - 2.0f * drel);
+    for (int k = 0; k < 4; ++k) {
+      if (s->ahp_const[k]) {
+        const double add = s->L1d[k] / (double)nf;
+        for (int u = c.tid; u < n; u += c.B) pg64[u] += add;
+        __syncthreads();
+        continue;
+      }
+      const int K = ahp_levels_of(c, k);
+      ahp_passes_f64(c, k, K, nf, l2d);
+      for (int u = c.tid; u < n; u += c.B)
+        if (feas_bit(c, u)) pg64[u] += s->L1d[k] * l2d[c.lvl[u]];
+      __syncthreads();
+    }
     double bv = -DBL_MAX;
     int bj = -1;
-    for (int i = c.tid; i < nf; i += c.B) {
-      if (c.pg[i] < thr) continue;
-      double pgv = 0;
-      for (int k = 0; k < 4; ++k) {
-        if (s->ahp_const[k]) { pgv += s->L1d[k] / (double)nf; continue; }
-        const float* x = c.xs + k * cap;
-        const double* w = c.w64 + k * cap;
-        const double sc = s->ahp_scaled[k];
-        double xi = x[i], sum = 0;
-        for (int j = 0; j < nf; ++j) sum += ahp_cell64((xi - (double)x[j]) * sc, rule) * w[j];
-        pgv += s->L1d[k] * (sum / (double)nf);
-      }
-      int u = c.xid[i];
-      if (pgv > bv || (pgv == bv && u < bj)) { bv = pgv; bj = u; }
+    for (int u = c.tid; u < n; u += c.B) {
+      if (!feas_bit(c, u)) continue;
+      const double v = pg64[u];
+      if (v > bv || (v == bv && u < bj)) { bv = v; bj = u; }
     }
     block_argmax64(c, bv, bj);
     if (c.tid == 0) s->c_fp64 += 1;
@@ -775,6 +1117,10 @@ __device__ void run_request(Ctx& c, const ReqsDev& R, const OutDev& O, int r, bo
     }
   }
   __syncthreads();
+  if (METHOD == 0) {  // presorted criteria: per request when requests commit, else per snapshot
+    if (keep || s->touch_over) ahp_presort(c);
+    else ahp_clear_dirty(c);
+  }
   if (!s->req_ok) {
     write_rejected(c, R, O, r, -1);
     __syncthreads();
@@ -864,6 +1210,7 @@ __device__ void init_ctx(Ctx& c, const Geo& g, const Opt& o, Scratch* s) {
   c.warp = threadIdx.x >> 5;
   c.nW = (g.n + 31) >> 5;
   c.nEW = (g.E + 31) >> 5;
+  c.dirty = nullptr;
   if (c.tid == 0) {
     s->c_steps = s->c_retries = s->c_fp64 = s->c_invalid = s->c_feas = s->c_pairs = 0;
     if (o.method == 0) {
@@ -888,7 +1235,6 @@ __device__ void flush_stats(Ctx& c, unsigned long long* stats) {
 
 // dynamic shared memory layout of k_batch:
 //   state words (6n ints) | maskw[nW] | special[nW] | edgebad[nEW] | AHP arrays
-__host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
 template <int METHOD>
 __global__ void __launch_bounds__(1024) k_batch(Geo g, Opt o, const int* __restrict__ snap, ReqsDev R,
@@ -913,14 +1259,8 @@ __global__ void __launch_bounds__(1024) k_batch(Geo g, Opt o, const int* __restr
   off = align16(off + sizeof(unsigned) * nEW);
   c.nfcap = n;
   if (METHOD == 0) {
-    c.xs = reinterpret_cast<float*>(dyn + off);
-    off = align16(off + sizeof(float) * 4 * (size_t)n);
-    c.xid = reinterpret_cast<int*>(dyn + off);
-    off = align16(off + sizeof(int) * (size_t)n);
-    c.wcol = reinterpret_cast<float*>(dyn + off);
-    off = align16(off + sizeof(float) * 4 * (size_t)n);
-    c.pg = reinterpret_cast<float*>(dyn + off);
-    c.w64 = w64 + (size_t)blockIdx.x * 4 * n;
+    ahp_carve(c, dyn + off, n);
+    c.w64 = w64 + (size_t)blockIdx.x * ahp_w64_doubles(n);
   }
   c.snap = snap;
   c.ulog = ulog + (size_t)blockIdx.x * ULOG_CAP;
@@ -954,6 +1294,7 @@ __global__ void __launch_bounds__(1024) k_batch(Geo g, Opt o, const int* __restr
   for (int w = c.tid; w < nW; w += c.B) { c.maskw[w] = 0u; c.special[w] = 0u; }
   for (int w = c.tid; w < nEW; w += c.B) c.edgebad[w] = 0u;
   __syncthreads();
+  if (METHOD == 0) ahp_presort(c);  // the snapshot's order serves every request
 
   for (;;) {
     if (c.tid == 0) s.next_req = atomicAdd(next, 1);
@@ -985,10 +1326,7 @@ __global__ void __launch_bounds__(1024) k_sequential(Geo g, Opt o, int* state, R
   c.ulog = ulog;
   c.nfcap = g.n;
   if (METHOD == 0) {
-    c.xs = ahp_ws;
-    c.xid = reinterpret_cast<int*>(ahp_ws + 4 * (size_t)g.n);
-    c.wcol = ahp_ws + 5 * (size_t)g.n;
-    c.pg = ahp_ws + 9 * (size_t)g.n;
+    ahp_carve(c, reinterpret_cast<unsigned char*>(ahp_ws), g.n);
     c.w64 = w64;
   }
   for (int w = c.tid; w < c.nW; w += c.B) { c.maskw[w] = 0u; c.special[w] = 0u; }
@@ -1015,10 +1353,7 @@ __global__ void __launch_bounds__(1024) k_rank(Geo g, Opt o, int* state, QueryDe
   c.snap = state;
   c.nfcap = g.n;
   if (METHOD == 0) {
-    c.xs = ahp_ws;
-    c.xid = reinterpret_cast<int*>(ahp_ws + 4 * (size_t)g.n);
-    c.wcol = ahp_ws + 5 * (size_t)g.n;
-    c.pg = ahp_ws + 9 * (size_t)g.n;
+    ahp_carve(c, reinterpret_cast<unsigned char*>(ahp_ws), g.n);
     c.w64 = w64;
   }
   clear_bitmaps(c);
@@ -1053,6 +1388,7 @@ __global__ void __launch_bounds__(1024) k_rank(Geo g, Opt o, int* state, QueryDe
       if (wm) select_topsis<true>(c, q.scores);
       else select_topsis<false>(c, nullptr);
     } else {
+      ahp_presort(c);
       if (wm) select_ahp<true>(c, q.scores);
       else select_ahp<false>(c, nullptr);
     }
@@ -1073,7 +1409,13 @@ __global__ void k_validate(ReqsDev R, int* status, unsigned long long* stats) {
 }
 
 // --------------------------------------------------------------- host -------
-int batch_block_size(const Geo& g) {
+int batch_block_size(const Geo& g, int method) {
+  if (method == 0) {  // AHP: a warp per level pair in the passes
+    const char* e = getenv("NACS_AHP_BLOCK");
+    if (e) return atoi(e);
+    int b = next_pow2(g.n / 4);
+    return b < 128 ? 128 : (b > 512 ? 512 : b);
+  }
   int b = ((g.n / 8 + 31) / 32) * 32;  // about 8 servers per thread
   if (b < 64) b = 64;
   if (b > 1024) b = 1024;
@@ -1087,7 +1429,7 @@ static size_t bitmap_bytes(const Geo& g) {
 
 size_t batch_smem_bytes(const Geo& g, int method) {
   size_t b = align16(sizeof(int) * (size_t)g.words()) + bitmap_bytes(g);
-  if (method == 0) b += align16(16 * (size_t)g.n) * 2 + align16(4 * (size_t)g.n) * 2;
+  if (method == 0) b += ahp_bytes(g.n);
   int dev = 0, optin = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
@@ -1098,7 +1440,7 @@ size_t batch_smem_bytes(const Geo& g, int method) {
 cudaError_t batch_occupancy(const Geo& g, int method, int* blocks_per_sm) {
   size_t smem = batch_smem_bytes(g, method);
   if (!smem) { *blocks_per_sm = 0; return cudaSuccess; }
-  int B = batch_block_size(g);
+  int B = batch_block_size(g, method);
   cudaError_t e;
   if (method == 1) {
     e = cudaFuncSetAttribute(k_batch<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1114,7 +1456,7 @@ cudaError_t launch_batch(const Geo& g, const Opt& o, const int* d_state, const R
                          int2* ulog, double* w64, int* next, unsigned long long* stats, int grid,
                          cudaStream_t st, const int* idx, const int* n_idx) {
   size_t smem = batch_smem_bytes(g, o.method);
-  int B = batch_block_size(g);
+  int B = batch_block_size(g, o.method);
   if (o.method == 1) {
     cudaFuncSetAttribute(k_batch<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_batch<1><<<grid, B, smem, st>>>(g, o, d_state, R, O, ulog, w64, next, stats, idx, n_idx);
@@ -1150,6 +1492,9 @@ cudaError_t launch_rank(const Geo& g, const Opt& o, int* d_state, const QueryDev
   else k_rank<0><<<1, B, smem, st>>>(g, o, d_state, q, ahp_ws, w64, stats);
   return cudaGetLastError();
 }
+
+size_t ahp_workspace_bytes(int n) { return ahp_bytes(n); }
+size_t ahp_workspace_doubles(int n) { return ahp_w64_doubles(n); }
 
 cudaError_t launch_validate(const ReqsDev& R, int* status, unsigned long long* stats, cudaStream_t st) {
   if (R.n <= 0) return cudaSuccess;
