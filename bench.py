@@ -79,6 +79,7 @@ class ClockSampler:
         self.device = device
         self.samples = []
         self._stop = threading.Event()
+        self._first = threading.Event()
         self._t = None
 
     def _run(self):
@@ -91,11 +92,15 @@ class ClockSampler:
                     self.samples.append([x.strip() for x in out.split(",")])
             except Exception:
                 pass
+            self._first.set()
             self._stop.wait(0.2)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
+        # nvidia-smi start-up can hold the driver lock: let the first query finish before
+        # the timed region so it cannot starve the launch queue
+        self._first.wait(timeout=10)
         return self
 
     def __exit__(self, *a):

@@ -60,6 +60,23 @@ __device__ __forceinline__ float topsis32(const TopsisP& t, int x0, int x1, int 
   return den > 0.f ? __fmul_rn(em, rcp_approx(den)) : 0.f;
 }
 
+// The closeness r = Ed-/(Ed+ + Ed-) = 1 / (1 + sqrt(q)) with q = Ed+^2 / Ed-^2 is a
+// decreasing function of q, so an argmax of r is an argmin of q: one reciprocal instead
+// of two square roots and a division.  q = +inf when Ed- = 0 (r = 0).  FP32 relative
+// error of q <= 19u (Ed+^2, Ed-^2 8u each, reciprocal 2u, product u).
+__device__ __forceinline__ float topsis_q32(const TopsisP& t, int x0, int x1, int x2, int x3) {
+  float p0 = scaled_diff(t.sf[0], t.s2p23[0], t.mx[0] - x0);
+  float m0 = scaled_diff(t.sf[0], t.s2p23[0], x0 - t.mn[0]);
+  float p1 = scaled_diff(t.sf[1], t.s2p23[1], t.mx[1] - x1);
+  float m1 = scaled_diff(t.sf[1], t.s2p23[1], x1 - t.mn[1]);
+  float p3 = scaled_diff(t.sf[3], t.s2p23[3], t.mx[3] - x3);
+  float m3 = scaled_diff(t.sf[3], t.s2p23[3], x3 - t.mn[3]);
+  float ep2 = fmaf(p3, p3, fmaf(p1, p1, fmaf(p0, p0, x2 ? t.p2sq[1] : t.p2sq[0])));
+  float em2 = fmaf(m3, m3, fmaf(m1, m1, fmaf(m0, m0, x2 ? t.m2sq[1] : t.m2sq[0])));
+  return em2 > 0.f ? __fmul_rn(ep2, rcp_approx(em2)) : __int_as_float(0x7f800000);
+}
+constexpr float kTopsisDeltaQ = 1.52587890625e-05f;  // 2^-16 relative (> 6 x 2 x 19u)
+
 __device__ __forceinline__ double topsis64(const TopsisP& t, int x0, int x1, int x2, int x3) {
   int x[4] = {x0, x1, x2, x3};
   double ep = 0, em = 0;

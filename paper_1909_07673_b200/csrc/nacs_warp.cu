@@ -407,17 +407,17 @@ __device__ __forceinline__ void acc_a(AccA& a, bool ok, int x0, int x1, int x2, 
   a.q1 += (unsigned long long)o1 * o1;
   a.q3 += (unsigned long long)o3 * o3;
 }
-// a7: per-lane best (score, lowest index) and second-best score
+// a7: per-lane best (smallest q = largest closeness, lowest index) and second best
 struct AccB {
   float b1, b2;
   int i1;
 };
-__device__ __forceinline__ void acc_b(AccB& b, bool ok, float r, int u) {
-  float re = ok ? r : -1.0f;
-  bool gt = re > b.b1;
-  b.b2 = gt ? b.b1 : fmaxf(b.b2, re);
-  b.i1 = gt ? u : b.i1;
-  b.b1 = gt ? re : b.b1;
+__device__ __forceinline__ void acc_b(AccB& b, bool ok, float q, int u) {
+  const float qe = ok ? q : __int_as_float(0x7f800000);
+  const bool lt = qe < b.b1;
+  b.b2 = lt ? b.b1 : fminf(b.b2, qe);
+  b.i1 = lt ? u : b.i1;
+  b.b1 = lt ? qe : b.b1;
 }
 
 __device__ __forceinline__ void set_comp(int4& v, int j, int x) {
@@ -524,10 +524,10 @@ __device__ void scan_score(const WCtx<LT>& c, const StepP& sp, const TopsisP& tp
       const unsigned ao = (unsigned)ch << 9;
       const int4 C = lds128(c.a_cpu + ao), Rm = lds128(c.a_ram + ao), A = lds128(c.a_act + ao),
                  Q = lds128(c.a_acc + ao);
-      acc_b(b, ok_plain(sp, C.x, Rm.x, Q.x, eb & 1u), topsis32(tp, C.x, Rm.x, A.x, Q.x), (int)u0);
-      acc_b(b, ok_plain(sp, C.y, Rm.y, Q.y, eb & 2u), topsis32(tp, C.y, Rm.y, A.y, Q.y), (int)u0 + 1);
-      acc_b(b, ok_plain(sp, C.z, Rm.z, Q.z, eb & 4u), topsis32(tp, C.z, Rm.z, A.z, Q.z), (int)u0 + 2);
-      acc_b(b, ok_plain(sp, C.w, Rm.w, Q.w, eb & 8u), topsis32(tp, C.w, Rm.w, A.w, Q.w), (int)u0 + 3);
+      acc_b(b, ok_plain(sp, C.x, Rm.x, Q.x, eb & 1u), topsis_q32(tp, C.x, Rm.x, A.x, Q.x), (int)u0);
+      acc_b(b, ok_plain(sp, C.y, Rm.y, Q.y, eb & 2u), topsis_q32(tp, C.y, Rm.y, A.y, Q.y), (int)u0 + 1);
+      acc_b(b, ok_plain(sp, C.z, Rm.z, Q.z, eb & 4u), topsis_q32(tp, C.z, Rm.z, A.z, Q.z), (int)u0 + 2);
+      acc_b(b, ok_plain(sp, C.w, Rm.w, Q.w, eb & 8u), topsis_q32(tp, C.w, Rm.w, A.w, Q.w), (int)u0 + 3);
     } else {
       int4 C, Rm, A, Q, I;
       load_chunk(c, sp, ch, spp, nxt, C, Rm, A, Q, I);
@@ -535,7 +535,7 @@ __device__ void scan_score(const WCtx<LT>& c, const StepP& sp, const TopsisP& tp
       for (int j = 0; j < 4; ++j) {
         const int x0 = get_comp(C, j), x1 = get_comp(Rm, j), x2 = get_comp(A, j), x3 = get_comp(Q, j);
         const bool ok = ok_any(sp, x0, x1, x3, (eb >> j) & 1u, get_comp(I, j));
-        acc_b(b, ok, topsis32(tp, x0, x1, x2, x3), (int)u0 + j);
+        acc_b(b, ok, topsis_q32(tp, x0, x1, x2, x3), (int)u0 + j);
       }
     }
   }
@@ -555,7 +555,7 @@ __device__ void scan_fp64(const WCtx<LT>& c, const StepP& sp, const TopsisP& tp,
 #pragma unroll 1
     for (int j = 0; j < 4; ++j) {
       int x0 = get_comp(C, j), x1 = get_comp(Rm, j), x2 = get_comp(A, j), x3 = get_comp(Q, j);
-      if (ok_any(sp, x0, x1, x3, (eb >> j) & 1u, get_comp(I, j)) && topsis32(tp, x0, x1, x2, x3) >= thr) {
+      if (ok_any(sp, x0, x1, x3, (eb >> j) & 1u, get_comp(I, j)) && topsis_q32(tp, x0, x1, x2, x3) <= thr) {
         double rr = topsis64(tp, x0, x1, x2, x3);
         int u = (int)u0 + j;
         if (rr > bv || (rr == bv && u < bj)) { bv = rr; bj = u; }
@@ -1003,17 +1003,18 @@ __global__ void __launch_bounds__(512, 1) k_batch_warp(Geo g, Opt o, const int* 
     __syncthreads();
     // ---- phase B (a5T + a7): closeness, argmax (lowest index), FP64 near-tie re-decision
     if (stepping) {
-      AccB bb = {-1.0f, -1.0f, -1};
+      const float INF = __int_as_float(0x7f800000);
+      AccB bb = {INF, INF, -1};
       scan_score(c, sp, tp, bb);
-      const unsigned key1 = bb.b1 >= 0.0f ? __float_as_uint(bb.b1) + 1u : 0u;
-      const unsigned m1 = __reduce_max_sync(NACS_FULL, key1);
+      // smallest q (positive floats order like their bit patterns), lowest index on ties
+      const unsigned key1 = __float_as_uint(bb.b1);
+      const unsigned m1 = __reduce_min_sync(NACS_FULL, key1);
       best = (int)__reduce_min_sync(NACS_FULL, key1 == m1 ? (unsigned)bb.i1 : UINT_MAX);
       const bool winner = key1 == m1 && bb.i1 == best;
-      const unsigned key2 = winner ? (bb.b2 >= 0.0f ? __float_as_uint(bb.b2) + 1u : 0u) : key1;
-      const unsigned m2 = __reduce_max_sync(NACS_FULL, key2);
-      const float s1 = __uint_as_float(m1 - 1u), s2 = m2 ? __uint_as_float(m2 - 1u) : -1.0f;
-      if (o.exact64 || (m2 != 0u && s1 - s2 <= kTopsisDelta)) {
-        const float thr = o.exact64 ? -1.0f : s1 - 2.0f * kTopsisDelta;
+      const unsigned m2 = __reduce_min_sync(NACS_FULL, winner ? __float_as_uint(bb.b2) : key1);
+      const float q1 = __uint_as_float(m1), q2 = __uint_as_float(m2);
+      if (o.exact64 || m2 == m1 || q2 - q1 <= kTopsisDeltaQ * q1) {  // R14: FP64 near-tie re-decision
+        const float thr = o.exact64 ? INF : q1 * (1.0f + 2.0f * kTopsisDeltaQ);
         double bv = -DBL_MAX;
         int bj = -1;
         scan_fp64(c, sp, tp, thr, bv, bj);

@@ -33,3 +33,55 @@ e1.record(s)
 torch.cuda.synchronize()
 st = ctx.last_stats()
 print(f"{method} {cfg} {nreq} requests: {e0.elapsed_time(e1):.3f} ms, stats {st}")
+
+if len(sys.argv) > 4 and sys.argv[4] == "loop":
+    import time
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(6)]
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    a0 = torch.cuda.Event(enable_timing=True)
+    a1 = torch.cuda.Event(enable_timing=True)
+    a0.record(s)
+    for i in range(6):
+        flush.zero_()
+        evs[i][0].record(s)
+        ctx.schedule_batch(d, method, "flat", out=out, flags=nacs.NACS_ASYNC)
+        evs[i][1].record(s)
+    a1.record(s)
+    host = time.perf_counter() - t
+    torch.cuda.synchronize()
+    print("per-call ms:", [round(a.elapsed_time(b), 3) for a, b in evs], "total", round(a0.elapsed_time(a1), 3),
+          "host enqueue s", round(host, 4))
+
+if len(sys.argv) > 4 and sys.argv[4] == "loop":
+    import time
+    torch.cuda.synchronize()
+    ts = []
+    for i in range(6):
+        t = time.perf_counter()
+        ctx.schedule_batch(d, method, "flat", out=out, flags=nacs.NACS_ASYNC)
+        ts.append(round((time.perf_counter() - t) * 1e3, 3))
+    torch.cuda.synchronize()
+    print("host ms per call (async):", ts)
+    import cProfile, pstats, io
+    pr = cProfile.Profile()
+    pr.enable()
+    ctx.schedule_batch(d, method, "flat", out=out, flags=nacs.NACS_ASYNC)
+    pr.disable()
+    sio = io.StringIO()
+    pstats.Stats(pr, stream=sio).sort_stats("cumulative").print_stats(8)
+    print(sio.getvalue()[:2500])
+
+if len(sys.argv) > 4 and sys.argv[4] == "loop":
+    torch.cuda.synchronize()
+    tz, te, tc = [], [], []
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(12)]
+    for i in range(6):
+        t = time.perf_counter(); flush.zero_(); tz.append(round((time.perf_counter() - t) * 1e3, 3))
+        t = time.perf_counter(); ev[2 * i].record(s); te.append(round((time.perf_counter() - t) * 1e3, 3))
+        t = time.perf_counter(); ctx.schedule_batch(d, method, "flat", out=out, flags=nacs.NACS_ASYNC)
+        tc.append(round((time.perf_counter() - t) * 1e3, 3))
+        ev[2 * i + 1].record(s)
+    torch.cuda.synchronize()
+    print("host ms zero_", tz, "record", te, "call", tc)
