@@ -139,6 +139,20 @@ typedef struct {
 /* Create a context on CUDA device `device`.  cuda_stream: the cudaStream_t all work of
  * the context is ordered on (NULL = the legacy default stream, as in the CUDA runtime). */
 nacs_status nacs_create(nacs_ctx **out, int device, void *cuda_stream);
+
+/* Create a context that takes part in server-sharded scheduling (one huge
+ * topology over `world` ranks, one process per GPU): every rank loads the same topology
+ * and calls nacs_schedule_request with the same requests; each rank scores its own block
+ * of world-th of the servers and the ranks exchange their (score, index) top-2 keys per
+ * pod step with ncclAllGather over NVLink; every rank applies the same commit, so the
+ * replicated states stay identical.  nccl_unique_id: the 128-byte ncclUniqueId from
+ * nacs_nccl_unique_id() on rank 0, broadcast by the caller (e.g. torch.distributed);
+ * NULL with world > 1 = loopback: all `world` logical shards run on this device (testing).
+ * TOPSIS is sharded; AHP runs replicated on every rank in this version. */
+nacs_status nacs_create_sharded(nacs_ctx **out, int device, void *cuda_stream, const void *nccl_unique_id,
+                                int rank, int world);
+/* Write a fresh ncclUniqueId (128 bytes) to out. */
+nacs_status nacs_nccl_unique_id(void *out);
 void nacs_destroy(nacs_ctx *ctx);
 
 /* Load (or replace) the DC state.  Validates k, capacities and residual ranges. */

@@ -13,6 +13,15 @@ SOURCES = [os.path.join(CSRC, f) for f in ("nacs_kernels.cu", "nacs_warp.cu", "n
 DEPS = SOURCES + [os.path.join(CSRC, "nacs_internal.h"), os.path.join(CSRC, "nacs_device.cuh"),
                   os.path.join(ROOT, "include", "nacs.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+# NCCL bundled with torch (nvidia-nccl wheel): headers, library, and an rpath so that
+# libnacs.so finds the same libnccl.so.2 at run time
+try:
+    import nvidia.nccl as _nccl
+    NCCL = list(_nccl.__path__)[0]
+except Exception:  # pragma: no cover
+    NCCL = "/usr"
+NCCL_FLAGS = ["-I", os.path.join(NCCL, "include"), "-L", os.path.join(NCCL, "lib"), "-lnccl",
+              "-Xlinker", "-rpath=" + os.path.join(NCCL, "lib")]
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
          "-Xcompiler", "-fPIC", "-shared", "-cudart", "static", "-Xptxas", "-v"]
 
@@ -26,7 +35,7 @@ def stale() -> bool:
 
 def build(force: bool = False, verbose: bool = False) -> str:
     if force or stale():
-        cmd = [NVCC, *FLAGS, "-I", os.path.join(ROOT, "include"), "-o", LIB, *SOURCES]
+        cmd = [NVCC, *FLAGS, "-I", os.path.join(ROOT, "include"), *NCCL_FLAGS, "-o", LIB, *SOURCES]
         p = subprocess.run(cmd, capture_output=True, text=True)
         if p.returncode != 0:
             sys.stderr.write(p.stdout + p.stderr)

@@ -9,6 +9,8 @@
 #include <string>
 #include <vector>
 
+#include <nccl.h>
+
 #include "../../include/nacs.h"
 #include "nacs_internal.h"
 
@@ -84,6 +86,12 @@ struct nacs_ctx {
   nacs_stats last{};
   bool stats_pending = false;
   bool cta_only = false;     // NACS_CTA_ONLY=1: force the CTA-per-request batch kernel (testing)
+  // server sharding (nacs_create_sharded)
+  int rank = 0, world = 1;
+  bool loopback = false;
+  ncclComm_t comm = nullptr;
+  DevArr<unsigned char> sh_buf;
+  PinArr sh_ctl;
 };
 
 namespace {
@@ -375,9 +383,117 @@ nacs_status rank_impl(nacs_ctx* ctx, const nacs_options* opt, const nacs_pod_que
   return NACS_OK;
 }
 
+#define NCK(call)                                                                   \
+  do {                                                                              \
+    ncclResult_t r_ = (call);                                                       \
+    if (r_ != ncclSuccess) return fail(ctx, NACS_ENCCL, std::string(#call) + ": " + ncclGetErrorString(r_)); \
+  } while (0)
+
+// Sequential scheduling with the servers sharded over the ranks (k_sh_* kernels): the host
+// drives each pod step (prepare, score own block, exchange keys, decide + commit) and reads
+// the control word once per step.
+nacs_status schedule_sharded(nacs_ctx* ctx, const Opt& o, const nacs::ReqsDev& Rd, const nacs::OutDev& Od, int R) {
+  const Geo& g = ctx->g;
+  const int world = ctx->world;
+  auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+  const size_t nW = (size_t)(g.n + 31) / 32, nEW = (size_t)(g.E + 31) / 32;
+  const size_t b_gs = al(nacs::scratch_bytes()), b_bm = al(4 * nW), b_e = al(4 * nEW), b_ctl = al(16),
+               b_kx = al(16 * (size_t)world), b_kv = al(8 * (size_t)world), b_ki = al(4 * (size_t)world);
+  CK(ctx->sh_buf.reserve(b_gs + 2 * b_bm + b_e + b_ctl + b_kx + b_kv + b_ki));
+  CK(ctx->sh_ctl.reserve(16));
+  CK(ctx->ulog.reserve(nacs::ULOG_CAP));
+  unsigned char* p = ctx->sh_buf.p;
+  nacs::ShardDev d;
+  d.gs = reinterpret_cast<nacs::Scratch*>(p); p += b_gs;
+  d.maskw = reinterpret_cast<unsigned*>(p); p += b_bm;
+  d.special = reinterpret_cast<unsigned*>(p); p += b_bm;
+  d.edgebad = reinterpret_cast<unsigned*>(p); p += b_e;
+  d.ctl = reinterpret_cast<int*>(p); p += b_ctl;
+  d.kx = reinterpret_cast<unsigned long long*>(p); p += b_kx;
+  d.kxv = reinterpret_cast<double*>(p); p += b_kv;
+  d.kxi = reinterpret_cast<int*>(p);
+  d.ulog = ctx->ulog.p;
+  d.stats = ctx->stats.p;
+  CK(cudaMemsetAsync(d.maskw, 0, 2 * b_bm + b_e, ctx->stream));
+  int* ctl = reinterpret_cast<int*>(ctx->sh_ctl.p);
+  // this process's shards: all of them in loopback, its own rank otherwise
+  const int s_lo = ctx->loopback ? 0 : ctx->rank, s_hi = ctx->loopback ? world : ctx->rank + 1;
+  auto lo_of = [&](int q) { return (int)((long long)g.n * q / world); };
+  const bool dbg = getenv("NACS_DEBUG_SHARD") != nullptr;
+  for (int r = 0; r < R; ++r) {
+    CK(nacs::launch_sh_begin(g, o, ctx->state.p, Rd, Od, r, d, ctx->stream));
+    for (long it = 0;; ++it) {
+      CK(cudaMemcpyAsync(ctl, d.ctl, 16, cudaMemcpyDeviceToHost, ctx->stream));
+      CK(cudaStreamSynchronize(ctx->stream));
+      const int phase = ctl[0];
+      if (dbg) fprintf(stderr, "[shard] r=%d it=%ld phase=%d pod=%d best=%d fail=%d\n", r, it, phase, ctl[1], ctl[2],
+                       ctl[3]);
+      if (phase == 0) break;  // PH_DONE
+      if (it > 4L * (g.n + 1) * (nacs::MAXC + 1))
+        return fail(ctx, NACS_ECUDA, "sharded engine: pod loop did not finish (phase " + std::to_string(phase) + ")");
+      if (phase == 3) {       // PH_FP64: re-decide the near tie in FP64
+        for (int q = s_lo; q < s_hi; ++q)
+          CK(nacs::launch_sh_fp64(g, o, ctx->state.p, lo_of(q), lo_of(q + 1), q, d, ctx->stream));
+        if (ctx->comm) {
+          NCK(ncclAllGather(d.kxv + ctx->rank, d.kxv, 1, ncclFloat64, ctx->comm, ctx->stream));
+          NCK(ncclAllGather(d.kxi + ctx->rank, d.kxi, 1, ncclInt32, ctx->comm, ctx->stream));
+        }
+        if (dbg) {
+          std::vector<int> ki(world);
+          std::vector<double> kv(world);
+          std::vector<unsigned long long> kk(2 * world);
+          CK(cudaMemcpy(ki.data(), d.kxi, 4 * world, cudaMemcpyDeviceToHost));
+          CK(cudaMemcpy(kv.data(), d.kxv, 8 * world, cudaMemcpyDeviceToHost));
+          CK(cudaMemcpy(kk.data(), d.kx, 16 * world, cudaMemcpyDeviceToHost));
+          for (int q = 0; q < world; ++q)
+            fprintf(stderr, "  fp64 slot %d: %d %.17g keys %016llx %016llx\n", q, ki[q], kv[q], kk[2 * q], kk[2 * q + 1]);
+        }
+        CK(nacs::launch_sh_decide64(g, o, ctx->state.p, Rd, Od, r, world, d, ctx->stream));
+        continue;
+      }
+      CK(nacs::launch_sh_prep(g, o, ctx->state.p, Rd, Od, r, d, ctx->stream));
+      for (int q = s_lo; q < s_hi; ++q)
+        CK(nacs::launch_sh_score(g, o, ctx->state.p, lo_of(q), lo_of(q + 1), q, d, ctx->stream));
+      if (ctx->comm) NCK(ncclAllGather(d.kx + 2 * ctx->rank, d.kx, 2, ncclUint64, ctx->comm, ctx->stream));
+      CK(nacs::launch_sh_decide(g, o, ctx->state.p, Rd, Od, r, world, d, ctx->stream));
+    }
+  }
+  return NACS_OK;
+}
+
 }  // namespace
 
 extern "C" {
+
+nacs_status nacs_nccl_unique_id(void* out) {
+  if (!out) return NACS_EINVAL;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return NACS_ENCCL;
+  std::memcpy(out, &id, sizeof(id));
+  return NACS_OK;
+}
+
+nacs_status nacs_create_sharded(nacs_ctx** out, int device, void* cuda_stream, const void* nccl_unique_id, int rank,
+                                int world) {
+  if (!out || world < 1 || rank < 0 || rank >= world) return NACS_EINVAL;
+  nacs_status st = nacs_create(out, device, cuda_stream);
+  if (st) return st;
+  nacs_ctx* ctx = *out;
+  ctx->rank = rank;
+  ctx->world = world;
+  if (nccl_unique_id) {
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_unique_id, sizeof(id));
+    if (ncclCommInitRank(&ctx->comm, world, id, rank) != ncclSuccess) {
+      nacs_destroy(ctx);
+      *out = nullptr;
+      return NACS_ENCCL;
+    }
+  } else if (world > 1) {
+    ctx->loopback = true;
+  }
+  return NACS_OK;
+}
 
 nacs_status nacs_create(nacs_ctx** out, int device, void* cuda_stream) {
   if (!out) return NACS_EINVAL;
@@ -422,6 +538,9 @@ void nacs_destroy(nacs_ctx* ctx) {
   ctx->stats.release();
   ctx->pin_in.release();
   ctx->pin_out.release();
+  ctx->sh_buf.release();
+  ctx->sh_ctl.release();
+  if (ctx->comm) ncclCommDestroy(ctx->comm);
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
@@ -616,6 +735,17 @@ nacs_status nacs_schedule_request(nacs_ctx* ctx, const nacs_options* opt, const 
       if (h[nacs::ST_INVALID])
         return fail(ctx, NACS_EINVAL, std::to_string(h[nacs::ST_INVALID]) + " invalid requests");
     }
+  }
+  if ((ctx->world > 1 || ctx->comm) && o.method == NACS_TOPSIS) {
+    if ((st = schedule_sharded(ctx, o, Rd, Od, R))) return st;
+    if (!dev) {
+      if ((st = unstage_outputs(ctx, R, C, V, out))) return st;
+    }
+    if (!async) {
+      CK(cudaStreamSynchronize(ctx->stream));
+      if ((st = finish_stats(ctx))) return st;
+    }
+    return NACS_OK;
   }
   CK(ctx->ulog.reserve(nacs::ULOG_CAP));
   if (o.method == 0) {

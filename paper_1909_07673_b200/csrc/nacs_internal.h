@@ -82,6 +82,19 @@ __host__ __device__ inline int validate_request(int nC, int nV, const int* cpu_m
   return bad;
 }
 
+// Device pointers of the server-sharded engine (nacs_kernels.cu, k_sh_*).
+struct Scratch;
+struct ShardDev {
+  Scratch* gs;                 // per-request scratch (global memory)
+  unsigned *maskw, *special, *edgebad;
+  int2* ulog;
+  int* ctl;                    // [0] phase, [1] pod
+  unsigned long long* kx;      // [2 * world] top-2 keys per rank
+  double* kxv;                 // [world] FP64 best value per rank
+  int* kxi;                    // [world] FP64 best server per rank
+  unsigned long long* stats;
+};
+
 // Launchers (nacs_kernels.cu).  Each returns the cudaError_t of the launch.
 struct LaunchInfo {
   int grid, block;
@@ -113,5 +126,18 @@ cudaError_t launch_sequential(const Geo& g, const Opt& o, int* d_state, const Re
 cudaError_t launch_rank(const Geo& g, const Opt& o, int* d_state, const QueryDev& q, float* ahp_ws,
                         double* w64, unsigned long long* stats, cudaStream_t s);
 cudaError_t launch_validate(const ReqsDev& R, int* status, unsigned long long* stats, cudaStream_t s);
+size_t scratch_bytes();
+cudaError_t launch_sh_begin(const Geo& g, const Opt& o, int* state, const ReqsDev& R, const OutDev& O, int r,
+                            const ShardDev& d, cudaStream_t st);
+cudaError_t launch_sh_prep(const Geo& g, const Opt& o, int* state, const ReqsDev& R, const OutDev& O, int r,
+                           const ShardDev& d, cudaStream_t st);
+cudaError_t launch_sh_score(const Geo& g, const Opt& o, int* state, int lo, int hi, int slot, const ShardDev& d,
+                            cudaStream_t st);
+cudaError_t launch_sh_decide(const Geo& g, const Opt& o, int* state, const ReqsDev& R, const OutDev& O, int r,
+                             int world, const ShardDev& d, cudaStream_t st);
+cudaError_t launch_sh_fp64(const Geo& g, const Opt& o, int* state, int lo, int hi, int slot, const ShardDev& d,
+                           cudaStream_t st);
+cudaError_t launch_sh_decide64(const Geo& g, const Opt& o, int* state, const ReqsDev& R, const OutDev& O, int r,
+                               int world, const ShardDev& d, cudaStream_t st);
 
 }  // namespace nacs

@@ -67,6 +67,8 @@ struct Scratch {
   // selection
   unsigned long long key1, key2;
   int best, amb;
+  float thr;
+  double bestv;
   // block reductions
   int red_i[MAXW][8];
   unsigned long long red_u[MAXW][3];
@@ -183,7 +185,7 @@ __device__ void block_argmax64(Ctx& c, double v, int j) {
       int bj = __shfl_xor_sync(FULL, j, o);
       if (bv > v || (bv == v && (unsigned)bj < (unsigned)j)) { v = bv; j = bj; }
     }
-    if (c.lane == 0) s->best = j;
+    if (c.lane == 0) { s->best = j; s->bestv = v; }
   }
   __syncthreads();
 }
@@ -1084,11 +1086,10 @@ __device__ void write_rejected(Ctx& c, const ReqsDev& R, const OutDev& O, int r,
 
 // One request (SURVEY §8(c) oracle algorithm, steps 1-3).  All threads.  On return the
 // state holds the accepted placement (sequential) or is restored (batch: keep=false).
+// Request start: validate (R24), pods and their demands.  Sets s->req_ok.  All threads.
 template <int METHOD>
-__device__ void run_request(Ctx& c, const ReqsDev& R, const OutDev& O, int r, bool keep) {
+__device__ void req_begin(Ctx& c, const ReqsDev& R, int r, bool keep) {
   Scratch* s = c.s;
-  const Geo& g = c.g;
-  const int n = g.n;
   if (c.tid == 0) {
     int c0 = R.coff[r], v0 = R.voff[r];
     int nC = R.coff[r + 1] - c0, nV = R.voff[r + 1] - v0;
@@ -1121,42 +1122,37 @@ __device__ void run_request(Ctx& c, const ReqsDev& R, const OutDev& O, int r, bo
     if (keep || s->touch_over) ahp_presort(c);
     else ahp_clear_dirty(c);
   }
-  if (!s->req_ok) {
-    write_rejected(c, R, O, r, -1);
-    __syncthreads();
-    return;
+}
+
+// Pod p's prologue (a1, a2): demands, flows, fabric tables, flow-server feasibility.
+__device__ void pod_prologue(Ctx& c, const ReqsDev& R, int r, int p) {
+  Scratch* s = c.s;
+  if (c.tid == 0) {
+    s->p = p;
+    s->dc = s->pod_cpu[p];
+    s->dr = s->pod_ram[p];
+    build_flows(c, R, r, p);
   }
-  const int P = s->P;
-  for (int p = 0; p < P; ++p) {
-    if (c.tid == 0) {
-      s->p = p;
-      s->dc = s->pod_cpu[p];
-      s->dr = s->pod_ram[p];
-      build_flows(c, R, r, p);
-    }
-    clear_bitmaps(c);
-    __syncthreads();
-    if (c.o.path_filter && s->nflow > 0) fabric_tables(c);
-    flow_server_ok(c);
-    __syncthreads();
-    for (;;) {
-      pass_filter<false>(c, nullptr, nullptr);
-      if (c.tid == 0) s->c_steps += 1;
-      if (s->nf == 0) {  // R20: reject the whole request atomically
-        if (c.tid == 0) undo_to(c, 0);
-        __syncthreads();
-        write_rejected(c, R, O, r, 0);
-        __syncthreads();
-        return;
-      }
-      if (METHOD == 1) select_topsis<false>(c, nullptr);
-      else select_ahp<false>(c, nullptr);
-      if (c.warp == 0) commit(c, R, r, p);
-      __syncthreads();
-      if (!s->fail) break;
-    }
-  }
-  // a9: top-up (R19) in container order, then vlink order; emit the placement.
+  clear_bitmaps(c);
+  __syncthreads();
+  if (c.o.path_filter && s->nflow > 0) fabric_tables(c);
+  flow_server_ok(c);
+  __syncthreads();
+}
+
+// R20: reject the whole request atomically.
+__device__ void req_reject(Ctx& c, const ReqsDev& R, const OutDev& O, int r) {
+  if (c.tid == 0) undo_to(c, 0);
+  __syncthreads();
+  write_rejected(c, R, O, r, 0);
+  __syncthreads();
+}
+
+// a9: top-up (R19) in container order, then vlink order; emit the placement.
+__device__ void req_finish(Ctx& c, const ReqsDev& R, const OutDev& O, int r, bool keep) {
+  Scratch* s = c.s;
+  const Geo& g = c.g;
+  const int n = g.n;
   if (c.tid == 0) {
     int c0 = R.coff[r], v0 = R.voff[r];
     for (int i = 0; i < s->nC; ++i) {
@@ -1198,7 +1194,52 @@ __device__ void run_request(Ctx& c, const ReqsDev& R, const OutDev& O, int r, bo
   __syncthreads();
 }
 
+// One request (SURVEY §8(c) oracle algorithm, steps 1-3).  All threads.  On return the
+// state holds the accepted placement (sequential) or is restored (batch: keep=false).
+template <int METHOD>
+__device__ void run_request(Ctx& c, const ReqsDev& R, const OutDev& O, int r, bool keep) {
+  Scratch* s = c.s;
+  req_begin<METHOD>(c, R, r, keep);
+  if (!s->req_ok) {
+    write_rejected(c, R, O, r, -1);
+    __syncthreads();
+    return;
+  }
+  const int P = s->P;
+  for (int p = 0; p < P; ++p) {
+    pod_prologue(c, R, r, p);
+    for (;;) {
+      pass_filter<false>(c, nullptr, nullptr);
+      if (c.tid == 0) s->c_steps += 1;
+      if (s->nf == 0) {
+        req_reject(c, R, O, r);
+        return;
+      }
+      if (METHOD == 1) select_topsis<false>(c, nullptr);
+      else select_ahp<false>(c, nullptr);
+      if (c.warp == 0) commit(c, R, r, p);
+      __syncthreads();
+      if (!s->fail) break;
+    }
+  }
+  req_finish(c, R, O, r, keep);
+}
+
 // ------------------------------------------------------------- kernels ------
+__device__ void ctx_basic(Ctx& c, const Geo& g, const Opt& o, Scratch* s) {
+  c.g = g;
+  c.o = o;
+  c.s = s;
+  c.tid = threadIdx.x;
+  c.B = blockDim.x;
+  c.NW = blockDim.x >> 5;
+  c.lane = threadIdx.x & 31;
+  c.warp = threadIdx.x >> 5;
+  c.nW = (g.n + 31) >> 5;
+  c.nEW = (g.E + 31) >> 5;
+  c.dirty = nullptr;
+}
+
 __device__ void init_ctx(Ctx& c, const Geo& g, const Opt& o, Scratch* s) {
   c.g = g;
   c.o = o;
@@ -1406,6 +1447,229 @@ __global__ void k_validate(ReqsDev R, int* status, unsigned long long* stats) {
                              R.bw_min + v0, R.bw_max + v0);
   status[r] = bad ? -1 : 0;
   if (bad) atomicAdd(&stats[ST_INVALID], 1ull);
+}
+
+// ------------------------------------------------------ server sharding -----
+// Sequential scheduling of one huge topology over G ranks (§8(e), C5): the state is
+// replicated on every rank; per pod step each rank filters and reduces the statistics
+// over all servers (replicated, exact), scores its own server block, and the ranks
+// exchange their top-2 keys (ncclAllGather, 16 B per rank); every rank then takes the
+// same decision and applies the same commit, so no state is ever exchanged.  The host
+// drives the pod steps (nacs_api.cu, schedule_sharded); `ctl` tells it what comes next.
+// Scratch lives in global memory because a request spans many launches.
+enum { PH_DONE = 0, PH_NEWPOD = 1, PH_RETRY = 2, PH_FP64 = 3 };
+
+__device__ void sh_ctx(Ctx& c, const Geo& g, const Opt& o, int* state, const ShardDev& d) {
+  ctx_basic(c, g, o, d.gs);
+  c.st = state;
+  c.snap = state;
+  c.maskw = d.maskw;
+  c.special = d.special;
+  c.edgebad = d.edgebad;
+  c.ulog = d.ulog;
+  c.nfcap = g.n;
+}
+
+__device__ void sh_flush(Ctx& c, unsigned long long* stats) {
+  flush_stats(c, stats);
+  if (c.tid == 0) {
+    Scratch* s = c.s;
+    s->c_steps = s->c_retries = s->c_fp64 = s->c_invalid = s->c_feas = s->c_pairs = 0;
+  }
+}
+
+template <int METHOD>
+__global__ void __launch_bounds__(1024) k_sh_begin(Geo g, Opt o, int* state, ReqsDev R, OutDev O, int r,
+                                                   ShardDev d) {
+  Ctx c;
+  sh_ctx(c, g, o, state, d);
+  Scratch* s = c.s;
+  if (c.tid == 0) s->c_steps = s->c_retries = s->c_fp64 = s->c_invalid = s->c_feas = s->c_pairs = 0;
+  __syncthreads();
+  req_begin<METHOD>(c, R, r, true);
+  if (!s->req_ok) {
+    write_rejected(c, R, O, r, -1);
+    __syncthreads();
+    sh_flush(c, d.stats);
+    if (c.tid == 0) d.ctl[0] = PH_DONE;
+    return;
+  }
+  if (c.tid == 0) { d.ctl[0] = PH_NEWPOD; d.ctl[1] = 0; }
+}
+
+// pod prologue (new pod) + filter and statistics over all servers (replicated)
+template <int METHOD>
+__global__ void __launch_bounds__(1024) k_sh_prep(Geo g, Opt o, int* state, ReqsDev R, OutDev O, int r,
+                                                  ShardDev d) {
+  const int phase = d.ctl[0];
+  if (phase != PH_NEWPOD && phase != PH_RETRY) return;
+  Ctx c;
+  sh_ctx(c, g, o, state, d);
+  Scratch* s = c.s;
+  if (phase == PH_NEWPOD) pod_prologue(c, R, r, d.ctl[1]);
+  pass_filter<false>(c, nullptr, nullptr);
+  if (c.tid == 0) s->c_steps += 1;
+  if (s->nf == 0) {
+    req_reject(c, R, O, r);
+    sh_flush(c, d.stats);
+    if (c.tid == 0) d.ctl[0] = PH_DONE;
+  }
+}
+
+// TOPSIS: closeness of this rank's servers [lo, hi); top-2 keys into slot
+__global__ void __launch_bounds__(1024) k_sh_score(Geo g, Opt o, int* state, int lo, int hi, int slot,
+                                                   ShardDev d) {
+  Ctx c;
+  sh_ctx(c, g, o, state, d);
+  Scratch* s = c.s;
+  const int phase = d.ctl[0];
+  if (phase != PH_NEWPOD && phase != PH_RETRY) {
+    if (c.tid == 0) { d.kx[2 * slot] = 0ull; d.kx[2 * slot + 1] = 0ull; }
+    return;
+  }
+  const int n = g.n;
+  TopsisP tp;
+  for (int k = 0; k < 4; ++k) { tp.mx[k] = s->mx[k]; tp.mn[k] = s->mn[k]; }
+  topsis_params(tp, o.wd, s->sq);
+  unsigned long long k1 = 0, k2 = 0;
+  const int* st = c.st;
+  for (int base = lo - (lo & 31) + c.warp * 32; base < hi; base += c.B) {
+    const int u = base + c.lane;
+    if (u < lo || u >= hi) continue;
+    if (!((c.maskw[u >> 5] >> (u & 31)) & 1u)) continue;
+    const float rr = topsis32(tp, st[u], st[n + u], st[2 * n + u], st[3 * n + u]);
+    top2_insert(k1, k2, score_key(rr, u));
+  }
+  block_top2(c, k1, k2);
+  if (c.tid == 0) { d.kx[2 * slot] = s->key1; d.kx[2 * slot + 1] = s->key2; }
+}
+
+// commit the decided server (s->best) and advance the pod loop
+template <int METHOD>
+__device__ void sh_commit_advance(Ctx& c, const ReqsDev& R, const OutDev& O, int r, const ShardDev& d) {
+  Scratch* s = c.s;
+  const int p = d.ctl[1];
+  if (c.warp == 0) commit(c, R, r, p);
+  __syncthreads();
+  if (c.tid == 0) { d.ctl[2] = s->best; d.ctl[3] = s->fail; }
+  if (s->fail) {
+    if (c.tid == 0) d.ctl[0] = PH_RETRY;
+    return;
+  }
+  if (p + 1 == s->P) {
+    req_finish(c, R, O, r, true);
+    sh_flush(c, d.stats);
+    if (c.tid == 0) d.ctl[0] = PH_DONE;
+  } else if (c.tid == 0) {
+    d.ctl[0] = PH_NEWPOD;
+    d.ctl[1] = p + 1;
+  }
+}
+
+// TOPSIS decision from the gathered keys of all ranks (R14), then commit
+__global__ void __launch_bounds__(1024) k_sh_decide(Geo g, Opt o, int* state, ReqsDev R, OutDev O, int r,
+                                                    int world, ShardDev d) {
+  const int phase = d.ctl[0];
+  if (phase != PH_NEWPOD && phase != PH_RETRY) return;
+  Ctx c;
+  sh_ctx(c, g, o, state, d);
+  Scratch* s = c.s;
+  if (c.tid == 0) {
+    unsigned long long k1 = 0, k2 = 0;
+    for (int q = 0; q < world; ++q) top2_merge(k1, k2, d.kx[2 * q], d.kx[2 * q + 1]);
+    const float s1 = __uint_as_float((unsigned)(k1 >> 32)), s2 = __uint_as_float((unsigned)(k2 >> 32));
+    s->best = (int)(0xFFFFFFFFu - (unsigned)(k1 & 0xFFFFFFFFull));
+    s->amb = o.exact64 || (k2 != 0ull && s1 - s2 <= kTopsisDelta);
+    s->thr = o.exact64 ? -1.0f : s1 - 2.0f * kTopsisDelta;
+    if (s->amb) d.ctl[0] = PH_FP64;
+  }
+  __syncthreads();
+  if (s->amb) return;
+  sh_commit_advance<1>(c, R, O, r, d);
+}
+
+// TOPSIS FP64 re-decision: exact closeness of this rank's candidates (r32 >= thr)
+__global__ void __launch_bounds__(1024) k_sh_fp64(Geo g, Opt o, int* state, int lo, int hi, int slot,
+                                                  ShardDev d) {
+  Ctx c;
+  sh_ctx(c, g, o, state, d);
+  Scratch* s = c.s;
+  const int n = g.n;
+  TopsisP tp;
+  for (int k = 0; k < 4; ++k) { tp.mx[k] = s->mx[k]; tp.mn[k] = s->mn[k]; }
+  topsis_params(tp, o.wd, s->sq);
+  const float thr = s->thr;
+  const int* st = c.st;
+  double bv = -DBL_MAX;
+  int bj = -1;
+  for (int base = lo - (lo & 31) + c.warp * 32; base < hi; base += c.B) {
+    const int u = base + c.lane;
+    if (u < lo || u >= hi) continue;
+    if (!((c.maskw[u >> 5] >> (u & 31)) & 1u)) continue;
+    const int x0 = st[u], x1 = st[n + u], x2 = st[2 * n + u], x3 = st[3 * n + u];
+    if (topsis32(tp, x0, x1, x2, x3) < thr) continue;
+    const double rr = topsis64(tp, x0, x1, x2, x3);
+    if (rr > bv || (rr == bv && u < bj)) { bv = rr; bj = u; }
+  }
+  block_argmax64(c, bv, bj);
+  if (c.tid == 0) { d.kxv[slot] = s->bestv; d.kxi[slot] = s->best; }
+}
+
+__global__ void __launch_bounds__(1024) k_sh_decide64(Geo g, Opt o, int* state, ReqsDev R, OutDev O, int r,
+                                                      int world, ShardDev d) {
+  if (d.ctl[0] != PH_FP64) return;
+  Ctx c;
+  sh_ctx(c, g, o, state, d);
+  Scratch* s = c.s;
+  if (c.tid == 0) {
+    double bv = -DBL_MAX;
+    int bj = -1;
+    for (int q = 0; q < world; ++q) {
+      const double v = d.kxv[q];
+      const int j = d.kxi[q];
+      if (j < 0) continue;
+      if (bj < 0 || v > bv || (v == bv && j < bj)) { bv = v; bj = j; }
+    }
+    s->best = bj;
+    s->c_fp64 += 1;
+  }
+  __syncthreads();
+  sh_commit_advance<1>(c, R, O, r, d);
+}
+
+size_t scratch_bytes() { return sizeof(Scratch); }
+
+cudaError_t launch_sh_begin(const Geo& g, const Opt& o, int* state, const ReqsDev& R, const OutDev& O, int r,
+                            const ShardDev& d, cudaStream_t st) {
+  if (o.method == 1) k_sh_begin<1><<<1, 1024, 0, st>>>(g, o, state, R, O, r, d);
+  else k_sh_begin<0><<<1, 1024, 0, st>>>(g, o, state, R, O, r, d);
+  return cudaGetLastError();
+}
+cudaError_t launch_sh_prep(const Geo& g, const Opt& o, int* state, const ReqsDev& R, const OutDev& O, int r,
+                           const ShardDev& d, cudaStream_t st) {
+  if (o.method == 1) k_sh_prep<1><<<1, 1024, 0, st>>>(g, o, state, R, O, r, d);
+  else k_sh_prep<0><<<1, 1024, 0, st>>>(g, o, state, R, O, r, d);
+  return cudaGetLastError();
+}
+cudaError_t launch_sh_score(const Geo& g, const Opt& o, int* state, int lo, int hi, int slot, const ShardDev& d,
+                            cudaStream_t st) {
+  k_sh_score<<<1, 1024, 0, st>>>(g, o, state, lo, hi, slot, d);
+  return cudaGetLastError();
+}
+cudaError_t launch_sh_decide(const Geo& g, const Opt& o, int* state, const ReqsDev& R, const OutDev& O, int r,
+                             int world, const ShardDev& d, cudaStream_t st) {
+  k_sh_decide<<<1, 1024, 0, st>>>(g, o, state, R, O, r, world, d);
+  return cudaGetLastError();
+}
+cudaError_t launch_sh_fp64(const Geo& g, const Opt& o, int* state, int lo, int hi, int slot, const ShardDev& d,
+                           cudaStream_t st) {
+  k_sh_fp64<<<1, 1024, 0, st>>>(g, o, state, lo, hi, slot, d);
+  return cudaGetLastError();
+}
+cudaError_t launch_sh_decide64(const Geo& g, const Opt& o, int* state, const ReqsDev& R, const OutDev& O, int r,
+                               int world, const ShardDev& d, cudaStream_t st) {
+  k_sh_decide64<<<1, 1024, 0, st>>>(g, o, state, R, O, r, world, d);
+  return cudaGetLastError();
 }
 
 // --------------------------------------------------------------- host -------

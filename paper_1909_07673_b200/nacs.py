@@ -66,9 +66,9 @@ class Stats(C.Structure):
                 ("ahp_pairs", C.c_int64)]
 
 
-EXPORTS = ["nacs_create", "nacs_destroy", "nacs_load_topology", "nacs_read_topology", "nacs_rank_ahp",
-           "nacs_rank_topsis", "nacs_schedule_request", "nacs_schedule_batch", "nacs_last_stats",
-           "nacs_last_error"]
+EXPORTS = ["nacs_create", "nacs_create_sharded", "nacs_nccl_unique_id", "nacs_destroy", "nacs_load_topology",
+           "nacs_read_topology", "nacs_rank_ahp", "nacs_rank_topsis", "nacs_schedule_request",
+           "nacs_schedule_batch", "nacs_last_stats", "nacs_last_error"]
 
 _lib = None
 
@@ -83,6 +83,8 @@ def lib():
         L = C.CDLL(LIB_PATH)
         vp = C.c_void_p
         L.nacs_create.argtypes = [C.POINTER(vp), C.c_int, vp]
+        L.nacs_create_sharded.argtypes = [C.POINTER(vp), C.c_int, vp, vp, C.c_int, C.c_int]
+        L.nacs_nccl_unique_id.argtypes = [vp]
         L.nacs_destroy.argtypes = [vp]
         L.nacs_destroy.restype = None
         L.nacs_load_topology.argtypes = [vp, C.POINTER(Topology)]
@@ -132,16 +134,33 @@ REQ_KEYS = ("container_off", "cpu_min", "cpu_max", "ram_min", "ram_max", "pod_of
 OUT_KEYS = ("status", "server_of_container", "cpu_alloc", "ram_alloc", "bw_alloc", "path_of_vlink")
 
 
-class Context:
-    """One libnacs context on one CUDA device (one per process / rank)."""
+def nccl_unique_id() -> bytes:
+    """A fresh 128-byte ncclUniqueId (rank 0 makes it; the caller broadcasts it)."""
+    buf = C.create_string_buffer(128)
+    st = lib().nacs_nccl_unique_id(buf)
+    if st != NACS_OK:
+        raise NacsError(st, "ncclGetUniqueId failed")
+    return buf.raw
 
-    def __init__(self, device: int = 0, stream=None):
+
+class Context:
+    """One libnacs context on one CUDA device (one per process / rank).
+
+    shard=(rank, world, uid): server-sharded sequential scheduling over `world` ranks
+    (uid = nccl_unique_id() from rank 0, or None for loopback shards on this device)."""
+
+    def __init__(self, device: int = 0, stream=None, shard=None):
         self._lib = lib()
         self._h = C.c_void_p()
         handle = None
         if stream is not None:
             handle = stream if isinstance(stream, int) else stream.cuda_stream
-        st = self._lib.nacs_create(C.byref(self._h), device, handle)
+        if shard is None:
+            st = self._lib.nacs_create(C.byref(self._h), device, handle)
+        else:
+            rank, world, uid = shard
+            ub = None if uid is None else C.create_string_buffer(bytes(uid), 128)
+            st = self._lib.nacs_create_sharded(C.byref(self._h), device, handle, ub, int(rank), int(world))
         if st != NACS_OK:
             raise NacsError(st, "nacs_create failed (no CUDA device?)")
         self.device = device

@@ -283,3 +283,63 @@ def test_large_requests_deferred_to_cta_kernel(ctx):
     ctx.load_topology(snap)
     out = ctx.schedule_batch(reqs, "topsis", "flat")
     assert_schedule_parity(snap, reqs, out, "topsis", "flat", False)
+
+
+# ------------------------------------------------------- server sharding -----
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+def test_server_sharded_loopback_equals_unsharded(world):
+    """§8(e): G logical server shards on one GPU (exchange = device copy) give the same
+    placements and final state as the unsharded sequential path, and match the oracle."""
+    from paper_1909_07673_b200 import nacs
+    snap, reqs = gen.config("C2")
+    sub = gen.subset(reqs, np.arange(60))
+    ref = nacs.Context(0)
+    sh = nacs.Context(0, shard=(0, world, None))
+    try:
+        for schema in SCHEMAS:
+            ref.load_topology(snap)
+            sh.load_topology(snap)
+            a = to_np(ref.schedule_request(sub, "topsis", schema))
+            b = to_np(sh.schedule_request(sub, "topsis", schema))
+            for key in a:
+                assert np.array_equal(a[key], b[key]), (world, schema, key)
+            sa, sb = ref.read_topology(), sh.read_topology()
+            for key in sa:
+                assert np.array_equal(sa[key], sb[key])
+            assert_schedule_parity(snap, sub, b, "topsis", schema, True, gpu_state=sb)
+    finally:
+        ref.close()
+        sh.close()
+
+
+def test_server_sharded_congested_and_exact64():
+    from paper_1909_07673_b200 import nacs
+    snap = gen.snapshot(8, seed=77)
+    snap["link_res"] = np.random.default_rng(1).integers(0, 90, size=len(snap["link_res"])).astype(np.int32)
+    reqs = gen.requests(120, 78, bw_max_hi=60)
+    sh = nacs.Context(0, shard=(0, 4, None))
+    try:
+        sh.load_topology(snap)
+        out = sh.schedule_request(reqs, "topsis", "network")
+        assert_schedule_parity(snap, reqs, out, "topsis", "network", True, gpu_state=sh.read_topology())
+        sh.load_topology(snap)
+        out2 = sh.schedule_request(reqs, "topsis", "network", flags=nacs.NACS_EXACT_FP64)
+        for key in out:
+            assert np.array_equal(to_np(out)[key], to_np(out2)[key])
+    finally:
+        sh.close()
+
+
+def test_server_sharded_nccl_world1():
+    """The NCCL exchange path with a real communicator (world size 1 on this box)."""
+    from paper_1909_07673_b200 import nacs
+    snap, reqs = gen.config("C2")
+    sub = gen.subset(reqs, np.arange(30))
+    uid = nacs.nccl_unique_id()
+    sh = nacs.Context(0, shard=(0, 1, uid))
+    try:
+        sh.load_topology(snap)
+        out = sh.schedule_request(sub, "topsis", "flat")
+        assert_schedule_parity(snap, sub, out, "topsis", "flat", True, gpu_state=sh.read_topology())
+    finally:
+        sh.close()
