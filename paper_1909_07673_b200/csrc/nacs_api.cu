@@ -399,9 +399,17 @@ nacs_status schedule_sharded(nacs_ctx* ctx, const Opt& o, const nacs::ReqsDev& R
   const size_t nW = (size_t)(g.n + 31) / 32, nEW = (size_t)(g.E + 31) / 32;
   const size_t b_gs = al(nacs::scratch_bytes()), b_bm = al(4 * nW), b_e = al(4 * nEW), b_ctl = al(16),
                b_kx = al(16 * (size_t)world), b_kv = al(8 * (size_t)world), b_ki = al(4 * (size_t)world);
-  CK(ctx->sh_buf.reserve(b_gs + 2 * b_bm + b_e + b_ctl + b_kx + b_kv + b_ki));
+  const bool ahp = o.method == NACS_AHP;
+  size_t n2 = 1;
+  while (n2 < (size_t)g.n) n2 <<= 1;
+  const size_t b_ws = ahp ? al(nacs::ahp_workspace_bytes(g.n)) : 0, b_lv = ahp ? al(4 * 8 * n2) : 0,
+               b_pp = ahp ? al(4 * 8 * (n2 + 2)) : 0, b_lvl = ahp ? al(4 * 4 * (size_t)g.n) : 0,
+               b_f = ahp ? al(4 * 4 * n2) : 0, b_d = ahp ? al(4 * 8 * n2) : 0, b_K = ahp ? al(16) : 0;
+  CK(ctx->sh_buf.reserve(b_gs + 2 * b_bm + b_e + b_ctl + b_kx + b_kv + b_ki + b_ws + 2 * b_lv + 2 * b_pp + b_lvl +
+                         2 * b_f + 2 * b_d + b_K));
   CK(ctx->sh_ctl.reserve(16));
   CK(ctx->ulog.reserve(nacs::ULOG_CAP));
+  CK(ctx->misc.reserve(8));
   unsigned char* p = ctx->sh_buf.p;
   nacs::ShardDev d;
   d.gs = reinterpret_cast<nacs::Scratch*>(p); p += b_gs;
@@ -411,7 +419,27 @@ nacs_status schedule_sharded(nacs_ctx* ctx, const Opt& o, const nacs::ReqsDev& R
   d.ctl = reinterpret_cast<int*>(p); p += b_ctl;
   d.kx = reinterpret_cast<unsigned long long*>(p); p += b_kx;
   d.kxv = reinterpret_cast<double*>(p); p += b_kv;
-  d.kxi = reinterpret_cast<int*>(p);
+  d.kxi = reinterpret_cast<int*>(p); p += b_ki;
+  d.ahp_ws = nullptr;
+  d.lvmC = d.lvwC = nullptr;
+  d.paC = d.pbC = nullptr;
+  d.lvlC = nullptr;
+  d.wq = d.l2q = nullptr;
+  d.wq64 = d.l2q64 = nullptr;
+  d.Kc = nullptr;
+  if (ahp) {
+    d.ahp_ws = p; p += b_ws;
+    d.lvmC = reinterpret_cast<float2*>(p); p += b_lv;
+    d.lvwC = reinterpret_cast<float2*>(p); p += b_lv;
+    d.paC = reinterpret_cast<double*>(p); p += b_pp;
+    d.pbC = reinterpret_cast<double*>(p); p += b_pp;
+    d.lvlC = reinterpret_cast<int*>(p); p += b_lvl;
+    d.wq = reinterpret_cast<float*>(p); p += b_f;
+    d.l2q = reinterpret_cast<float*>(p); p += b_f;
+    d.wq64 = reinterpret_cast<double*>(p); p += b_d;
+    d.l2q64 = reinterpret_cast<double*>(p); p += b_d;
+    d.Kc = reinterpret_cast<int*>(p);
+  }
   d.ulog = ctx->ulog.p;
   d.stats = ctx->stats.p;
   CK(cudaMemsetAsync(d.maskw, 0, 2 * b_bm + b_e, ctx->stream));
@@ -431,6 +459,24 @@ nacs_status schedule_sharded(nacs_ctx* ctx, const Opt& o, const nacs::ReqsDev& R
       if (phase == 0) break;  // PH_DONE
       if (it > 4L * (g.n + 1) * (nacs::MAXC + 1))
         return fail(ctx, NACS_ECUDA, "sharded engine: pod loop did not finish (phase " + std::to_string(phase) + ")");
+      if (ahp) {  // AHP: passes over this process's share of level pairs, sum-allreduce between
+        const bool f64 = phase == 3;
+        const int q0 = ctx->loopback ? 0 : ctx->rank, q1 = ctx->loopback ? world : ctx->rank + 1;
+        if (!f64) CK(nacs::launch_sh_prep(g, o, ctx->state.p, Rd, Od, r, d, ctx->stream));
+        CK(nacs::launch_ahp_pass(1, f64, g, o, ctx->state.p, q0, q1, world, d, ctx->stream));
+        if (ctx->comm) {
+          if (f64) NCK(ncclAllReduce(d.wq64, d.wq64, 4 * n2, ncclFloat64, ncclSum, ctx->comm, ctx->stream));
+          else NCK(ncclAllReduce(d.wq, d.wq, 4 * n2, ncclFloat32, ncclSum, ctx->comm, ctx->stream));
+        }
+        CK(nacs::launch_ahp_mid(f64, g, o, ctx->state.p, d, ctx->stream));
+        CK(nacs::launch_ahp_pass(2, f64, g, o, ctx->state.p, q0, q1, world, d, ctx->stream));
+        if (ctx->comm) {
+          if (f64) NCK(ncclAllReduce(d.l2q64, d.l2q64, 4 * n2, ncclFloat64, ncclSum, ctx->comm, ctx->stream));
+          else NCK(ncclAllReduce(d.l2q, d.l2q, 4 * n2, ncclFloat32, ncclSum, ctx->comm, ctx->stream));
+        }
+        CK(nacs::launch_ahp_decide(f64, g, o, ctx->state.p, Rd, Od, r, d, ctx->stream));
+        continue;
+      }
       if (phase == 3) {       // PH_FP64: re-decide the near tie in FP64
         for (int q = s_lo; q < s_hi; ++q)
           CK(nacs::launch_sh_fp64(g, o, ctx->state.p, lo_of(q), lo_of(q + 1), q, d, ctx->stream));
@@ -736,7 +782,8 @@ nacs_status nacs_schedule_request(nacs_ctx* ctx, const nacs_options* opt, const 
         return fail(ctx, NACS_EINVAL, std::to_string(h[nacs::ST_INVALID]) + " invalid requests");
     }
   }
-  if ((ctx->world > 1 || ctx->comm) && o.method == NACS_TOPSIS) {
+  // the sharded engine: server-sharded contexts, and (grid-wide level passes) AHP on big topologies
+  if (ctx->world > 1 || ctx->comm || (o.method == NACS_AHP && g.n >= 4096)) {
     if ((st = schedule_sharded(ctx, o, Rd, Od, R))) return st;
     if (!dev) {
       if ((st = unstage_outputs(ctx, R, C, V, out))) return st;

@@ -93,6 +93,14 @@ struct ShardDev {
   double* kxv;                 // [world] FP64 best value per rank
   int* kxi;                    // [world] FP64 best server per rank
   unsigned long long* stats;
+  // AHP (sorted levels of every criterion at once, see nacs_kernels.cu)
+  unsigned char* ahp_ws;       // ahp_carve region: presort, merge buffers, priorities
+  float2 *lvmC, *lvwC;         // [4][n2] (value, multiplicity), (value, weight) per level
+  double *paC, *pbC;           // [4][n2+2] prefix sums
+  int* lvlC;                   // [4][n] level of each server
+  float *wq, *l2q;             // [4][n2] pass-1 weights, L2 per level (allreduced)
+  double *wq64, *l2q64;        // [4][n2] FP64 re-decision
+  int* Kc;                     // [4] levels per criterion (0 = constant criterion)
 };
 
 // Launchers (nacs_kernels.cu).  Each returns the cudaError_t of the launch.
@@ -139,5 +147,12 @@ cudaError_t launch_sh_fp64(const Geo& g, const Opt& o, int* state, int lo, int h
                            cudaStream_t st);
 cudaError_t launch_sh_decide64(const Geo& g, const Opt& o, int* state, const ReqsDev& R, const OutDev& O, int r,
                                int world, const ShardDev& d, cudaStream_t st);
+// AHP pod step over the grid and the ranks: passes over this process's share of level
+// pairs (ranks q in [q0, q1) of world), then the 1-CTA middle / decide kernels.
+cudaError_t launch_ahp_pass(int pass, bool fp64, const Geo& g, const Opt& o, int* state, int q0, int q1, int world,
+                            const ShardDev& d, cudaStream_t st);
+cudaError_t launch_ahp_mid(bool fp64, const Geo& g, const Opt& o, int* state, const ShardDev& d, cudaStream_t st);
+cudaError_t launch_ahp_decide(bool fp64, const Geo& g, const Opt& o, int* state, const ReqsDev& R, const OutDev& O,
+                              int r, const ShardDev& d, cudaStream_t st);
 
 }  // namespace nacs

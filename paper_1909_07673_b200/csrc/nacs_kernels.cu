@@ -1468,6 +1468,17 @@ __device__ void sh_ctx(Ctx& c, const Geo& g, const Opt& o, int* state, const Sha
   c.edgebad = d.edgebad;
   c.ulog = d.ulog;
   c.nfcap = g.n;
+  if (o.method == 0 && d.ahp_ws) ahp_carve(c, d.ahp_ws, g.n);
+}
+
+// point the per-criterion level arrays of c at criterion k's slices
+__device__ void ahp_slice(Ctx& c, const ShardDev& d, int k) {
+  const int n2 = next_pow2(c.g.n);
+  c.lvm = d.lvmC + (size_t)k * n2;
+  c.lvw = d.lvwC + (size_t)k * n2;
+  c.pa = d.paC + (size_t)k * (n2 + 2);
+  c.pb = d.pbC + (size_t)k * (n2 + 2);
+  c.lvl = d.lvlC + (size_t)k * c.g.n;
 }
 
 __device__ void sh_flush(Ctx& c, unsigned long long* stats) {
@@ -1484,7 +1495,14 @@ __global__ void __launch_bounds__(1024) k_sh_begin(Geo g, Opt o, int* state, Req
   Ctx c;
   sh_ctx(c, g, o, state, d);
   Scratch* s = c.s;
-  if (c.tid == 0) s->c_steps = s->c_retries = s->c_fp64 = s->c_invalid = s->c_feas = s->c_pairs = 0;
+  if (c.tid == 0) {
+    s->c_steps = s->c_retries = s->c_fp64 = s->c_invalid = s->c_feas = s->c_pairs = 0;
+    if (METHOD == 0) {
+      double L1[4];
+      ahp_l1_dev(o, L1);
+      for (int k = 0; k < 4; ++k) { s->L1d[k] = L1[k]; s->L1[k] = (float)L1[k]; }
+    }
+  }
   __syncthreads();
   req_begin<METHOD>(c, R, r, true);
   if (!s->req_ok) {
@@ -1513,6 +1531,35 @@ __global__ void __launch_bounds__(1024) k_sh_prep(Geo g, Opt o, int* state, Reqs
     req_reject(c, R, O, r);
     sh_flush(c, d.stats);
     if (c.tid == 0) d.ctl[0] = PH_DONE;
+    return;
+  }
+  if (METHOD == 0) {  // levels and pass-1 prefix sums of every non-constant criterion
+    if (c.tid == 0) {
+      for (int k = 0; k < 4; ++k) {
+        const int lo = s->mn[k], hi = s->mx[k];
+        s->ahp_const[k] = hi == lo;
+        const double sc = hi > lo ? 9.0 / (double)(hi - lo) : 0.0;
+        s->ahp_scaled[k] = sc;
+        s->ahp_scale[k] = (float)sc;
+      }
+    }
+    __syncthreads();
+    const int n2 = next_pow2(g.n);
+    for (int k = 0; k < 4; ++k) {
+      if (s->ahp_const[k]) {
+        if (c.tid == 0) d.Kc[k] = 0;
+        continue;
+      }
+      ahp_slice(c, d, k);
+      const int K = ahp_levels_of(c, k);
+      ahp_prefix(c, K, c.lvm);
+      for (int l = c.tid; l < K; l += c.B) { d.wq[k * n2 + l] = 0.f; d.l2q[k * n2 + l] = 0.f; }
+      if (c.tid == 0) {
+        d.Kc[k] = K;
+        s->c_pairs += (unsigned long long)K * (unsigned long long)(K - 1) / 2;
+      }
+      __syncthreads();
+    }
   }
 }
 
@@ -1635,6 +1682,199 @@ __global__ void __launch_bounds__(1024) k_sh_decide64(Geo g, Opt o, int* state, 
   }
   __syncthreads();
   sh_commit_advance<1>(c, R, O, r, d);
+}
+
+// ---- AHP over the grid and the ranks.  The pairs (t, K-1-t) of criterion k's levels are
+// split into `world` equal shares; a thread takes one pair.  Pass 1 writes the weights
+// w_l = m_l / colsum(l) of its levels, pass 2 their L2; every other entry stays 0 so
+// that a sum-allreduce over the ranks assembles the full arrays.
+__device__ __forceinline__ bool sh_live(const ShardDev& d, bool fp64) {
+  const int ph = d.ctl[0];
+  return fp64 ? ph == PH_FP64 : (ph == PH_NEWPOD || ph == PH_RETRY);
+}
+
+template <int PASS, bool FP64>
+__global__ void __launch_bounds__(256) k_ahp_pass(Geo g, Opt o, int q0, int q1, int world, ShardDev d) {
+  if (!sh_live(d, FP64)) return;
+  const Scratch* s = d.gs;
+  const int n2 = next_pow2(g.n);
+  const int m = s->nf;
+  const int rule = o.ahp_rule;
+  int a[4], b[4], total = 0;
+  for (int k = 0; k < 4; ++k) {
+    const int K = d.Kc[k], half = (K + 1) >> 1;
+    a[k] = (int)((long long)half * q0 / world);
+    b[k] = (int)((long long)half * q1 / world);
+    total += b[k] - a[k];
+  }
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    int k = 0, t = i;
+    while (t >= b[k] - a[k]) { t -= b[k] - a[k]; ++k; }
+    t += a[k];
+    const int K = d.Kc[k];
+    const double sd = s->ahp_scaled[k];
+    const float sc = (float)sd;
+    const float2* lvm = d.lvmC + (size_t)k * n2;
+    const float2* lvw = d.lvwC + (size_t)k * n2;
+    const double* pa = d.paC + (size_t)k * (n2 + 2);
+    const double* pb = d.pbC + (size_t)k * (n2 + 2);
+    for (int side = 0; side < 2; ++side) {
+      const int l = side ? K - 1 - t : t;
+      if (side && l == t) break;
+      if (PASS == 1) {
+        const double vl = lvm[l].x, ml = lvm[l].y;
+        double rec;
+        if (FP64) {
+          rec = 0;
+          for (int q = 0; q < l; ++q) {
+            const double dd = vl - (double)lvm[q].x;
+            rec += (double)lvm[q].y / (rule ? 1.0 + sd * dd : dd);
+          }
+        } else {
+          rec = (double)rsum_f32<false>(lvm, 0, l, lvm[l].x, sc, rule);
+        }
+        const double cgt = pa[K] - pa[l + 1];
+        const double G = (pb[K] - pb[l + 1]) - cgt * vl;  // sum_{k>l} m_k (v_k - v_l), exact
+        const double col = rule ? cgt + sd * G + ml + rec : sd * G + ml + rec / sd;
+        if (FP64) d.wq64[k * n2 + l] = ml / col;
+        else d.wq[k * n2 + l] = (float)(ml / col);
+      } else {
+        const double vl = lvw[l].x;
+        double rec, wl;
+        if (FP64) {
+          wl = d.wq64[k * n2 + l];
+          rec = 0;
+          for (int q = l + 1; q < K; ++q) {
+            const double dd = (double)lvw[q].x - vl;
+            rec += d.wq64[k * n2 + q] / (rule ? 1.0 + sd * dd : dd);
+          }
+        } else {
+          wl = (double)lvw[l].y;
+          rec = (double)rsum_f32<true>(lvw, l + 1, K, lvw[l].x, sc, rule);
+        }
+        const double lin = vl * pa[l] - pb[l];  // sum_{k<l} w_k (v_l - v_k)
+        const double L = rule ? pa[l] + sd * lin + wl + rec : sd * lin + wl + rec / sd;
+        if (FP64) d.l2q64[k * n2 + l] = L / (double)m;
+        else d.l2q[k * n2 + l] = (float)(L / (double)m);
+      }
+    }
+  }
+}
+
+// between the passes (1 CTA): (value, weight) levels and their prefix sums
+template <bool FP64>
+__global__ void __launch_bounds__(1024) k_ahp_mid(Geo g, Opt o, int* state, ShardDev d) {
+  if (!sh_live(d, FP64)) return;
+  Ctx c;
+  sh_ctx(c, g, o, state, d);
+  const int n2 = next_pow2(g.n);
+  for (int k = 0; k < 4; ++k) {
+    const int K = d.Kc[k];
+    if (K == 0) continue;
+    ahp_slice(c, d, k);
+    for (int l = c.tid; l < K; l += c.B)
+      c.lvw[l] = make_float2(c.lvm[l].x, FP64 ? 0.f : d.wq[k * n2 + l]);
+    __syncthreads();
+    if (!FP64) {
+      ahp_prefix(c, K, c.lvw);
+    } else {  // exact prefix sums of the FP64 weights (serial in level order: rare path)
+      if (c.tid == 0) {
+        double a = 0, b = 0;
+        for (int l = 0; l < K; ++l) {
+          c.pa[l] = a;
+          c.pb[l] = b;
+          a += d.wq64[k * n2 + l];
+          b += d.wq64[k * n2 + l] * (double)c.lvm[l].x;
+        }
+        c.pa[K] = a;
+        c.pb[K] = b;
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// decide (1 CTA): PG over F, argmax (top-2 and near-tie test in FP32), commit
+template <bool FP64>
+__global__ void __launch_bounds__(1024) k_ahp_decide(Geo g, Opt o, int* state, ReqsDev R, OutDev O, int r,
+                                                     ShardDev d) {
+  if (!sh_live(d, FP64)) return;
+  Ctx c;
+  sh_ctx(c, g, o, state, d);
+  Scratch* s = c.s;
+  const int n = g.n, n2 = next_pow2(n), nf = s->nf;
+  if (!FP64) {
+    const float inv_nf = rcp_approx((float)nf);
+    unsigned long long k1 = 0, k2 = 0;
+    for (int u = c.tid; u < n; u += c.B) {
+      if (!feas_bit(c, u)) continue;
+      float pgv = 0.f;
+      for (int k = 0; k < 4; ++k) {
+        if (s->ahp_const[k]) pgv += s->L1[k] * inv_nf;
+        else pgv = fmaf(s->L1[k], d.l2q[k * n2 + d.lvlC[(size_t)k * n + u]], pgv);
+      }
+      top2_insert(k1, k2, score_key(pgv, u));
+    }
+    block_top2(c, k1, k2);
+    const float drel = ahp_delta_rel(nf);
+    if (c.tid == 0) {
+      const float s1 = __uint_as_float((unsigned)(s->key1 >> 32));
+      const float s2 = __uint_as_float((unsigned)(s->key2 >> 32));
+      s->best = (int)(0xFFFFFFFFu - (unsigned)(s->key1 & 0xFFFFFFFFull));
+      s->amb = o.exact64 || (s->key2 != 0ull && s2 >= s1 * (1.0f - drel));
+      if (s->amb) d.ctl[0] = PH_FP64;
+    }
+    __syncthreads();
+    if (s->amb) {  // the FP64 passes start from zeroed weights and the pass-1 prefix sums
+      for (int k = 0; k < 4; ++k) {
+        const int K = d.Kc[k];
+        if (K == 0) continue;
+        for (int l = c.tid; l < K; l += c.B) { d.wq64[k * n2 + l] = 0.0; d.l2q64[k * n2 + l] = 0.0; }
+        ahp_slice(c, d, k);
+        ahp_prefix(c, K, c.lvm);
+      }
+      return;
+    }
+  } else {
+    double bv = -DBL_MAX;
+    int bj = -1;
+    for (int u = c.tid; u < n; u += c.B) {
+      if (!feas_bit(c, u)) continue;
+      double v = 0;
+      for (int k = 0; k < 4; ++k) {
+        if (s->ahp_const[k]) v += s->L1d[k] / (double)nf;
+        else v += s->L1d[k] * d.l2q64[k * n2 + d.lvlC[(size_t)k * n + u]];
+      }
+      if (v > bv || (v == bv && u < bj)) { bv = v; bj = u; }
+    }
+    block_argmax64(c, bv, bj);
+    if (c.tid == 0) s->c_fp64 += 1;
+  }
+  sh_commit_advance<0>(c, R, O, r, d);
+}
+
+cudaError_t launch_ahp_pass(int pass, bool fp64, const Geo& g, const Opt& o, int* state, int q0, int q1, int world,
+                            const ShardDev& d, cudaStream_t st) {
+  (void)state;
+  int blocks = 0;
+  cudaDeviceGetAttribute(&blocks, cudaDevAttrMultiProcessorCount, 0);
+  blocks *= 8;
+  if (pass == 1 && !fp64) k_ahp_pass<1, false><<<blocks, 256, 0, st>>>(g, o, q0, q1, world, d);
+  else if (pass == 1) k_ahp_pass<1, true><<<blocks, 256, 0, st>>>(g, o, q0, q1, world, d);
+  else if (!fp64) k_ahp_pass<2, false><<<blocks, 256, 0, st>>>(g, o, q0, q1, world, d);
+  else k_ahp_pass<2, true><<<blocks, 256, 0, st>>>(g, o, q0, q1, world, d);
+  return cudaGetLastError();
+}
+cudaError_t launch_ahp_mid(bool fp64, const Geo& g, const Opt& o, int* state, const ShardDev& d, cudaStream_t st) {
+  if (fp64) k_ahp_mid<true><<<1, 1024, 0, st>>>(g, o, state, d);
+  else k_ahp_mid<false><<<1, 1024, 0, st>>>(g, o, state, d);
+  return cudaGetLastError();
+}
+cudaError_t launch_ahp_decide(bool fp64, const Geo& g, const Opt& o, int* state, const ReqsDev& R, const OutDev& O,
+                              int r, const ShardDev& d, cudaStream_t st) {
+  if (fp64) k_ahp_decide<true><<<1, 1024, 0, st>>>(g, o, state, R, O, r, d);
+  else k_ahp_decide<false><<<1, 1024, 0, st>>>(g, o, state, R, O, r, d);
+  return cudaGetLastError();
 }
 
 size_t scratch_bytes() { return sizeof(Scratch); }

@@ -343,3 +343,49 @@ def test_server_sharded_nccl_world1():
         assert_schedule_parity(snap, sub, out, "topsis", "flat", True, gpu_state=sh.read_topology())
     finally:
         sh.close()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("rule", [0, 1])
+def test_server_sharded_ahp_loopback(world, rule):
+    """AHP with the level-pair passes split over G logical ranks (sum-allreduce between
+    passes = shared buffers in loopback) equals the single-CTA sequential path."""
+    from paper_1909_07673_b200 import nacs
+    snap, reqs = gen.config("C2")
+    sub = gen.subset(reqs, np.arange(40))
+    ref = nacs.Context(0)
+    sh = nacs.Context(0, shard=(0, world, None))
+    try:
+        for schema in ("flat", "network"):
+            ref.load_topology(snap)
+            sh.load_topology(snap)
+            a = to_np(ref.schedule_request(sub, "ahp", schema, ahp_rule=rule))
+            b = to_np(sh.schedule_request(sub, "ahp", schema, ahp_rule=rule))
+            assert_schedule_parity(snap, sub, b, "ahp", schema, True, gpu_state=sh.read_topology(), ahp_rule=rule)
+            for key in a:
+                assert np.array_equal(a[key], b[key]), (world, schema, key)
+    finally:
+        ref.close()
+        sh.close()
+
+
+def test_ahp_grid_engine_large_topology(ctx):
+    """k=26 (4394 servers): sequential AHP runs through the grid-wide level passes."""
+    snap = gen.snapshot(26, seed=26)
+    reqs = gen.requests(3, 27)
+    ctx.load_topology(snap)
+    out = ctx.schedule_request(reqs, "ahp", "clustering")
+    assert_schedule_parity(snap, reqs, out, "ahp", "clustering", True, gpu_state=ctx.read_topology())
+
+
+def test_server_sharded_ahp_nccl_world1():
+    from paper_1909_07673_b200 import nacs
+    snap, reqs = gen.config("C2")
+    sub = gen.subset(reqs, np.arange(20))
+    sh = nacs.Context(0, shard=(0, 1, nacs.nccl_unique_id()))
+    try:
+        sh.load_topology(snap)
+        out = sh.schedule_request(sub, "ahp", "flat")
+        assert_schedule_parity(snap, sub, out, "ahp", "flat", True, gpu_state=sh.read_topology())
+    finally:
+        sh.close()
