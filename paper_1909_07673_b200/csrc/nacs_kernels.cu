@@ -37,8 +37,11 @@ __device__ __forceinline__ unsigned smem_u32(const void* p) {
 }
 // AHP: relative error of PG in FP32 <= (96 + 2*ceil(nf/32)) u; ambiguous if the
 // relative top-2 gap is <= 2 x that.
+// (u = 2^-24; reciprocal sums in FP32 chunks of <= 32 terms accumulated in FP64, linear
+// parts from exact prefix sums: PG relative error <= 82u, independent of nf)
 __device__ __forceinline__ float ahp_delta_rel(int nf) {
-  return 2.0f * (96.0f + 2.0f * (float)((nf + 31) / 32)) * 5.9604644775390625e-08f;
+  (void)nf;
+  return 2.0f * 96.0f * 5.9604644775390625e-08f;
 }
 
 // ------------------------------------------------------------ scratch -------
@@ -77,7 +80,9 @@ struct Scratch {
   int red_j[MAXW];
   int scan[MAXW];
   double scand[MAXW][2];
-  int lvK, m1, nd, ntouched, touch_over;
+  double scand_total[2];
+  int scan_total;
+  int lvK, m1, nd, ntouched, touch_over, presorted;
   int touched[2 * MAXC];   // servers with changed criteria in the current request (AHP)
   float dval[2 * MAXC];    // dirty feasible values / servers of a pod step, sorted
   int dsrv[2 * MAXC];
@@ -239,6 +244,57 @@ __device__ void block_exscan_d2(Ctx& c, double& a, double& b) {
   __syncthreads();
   a = ra;
   b = rb;
+}
+
+// Warp segments for coalesced, stable block-wide scans: warp w owns a contiguous range
+// [s0, s1) of [0, N), 32 elements per step; positions inside a step come from ballots.
+__device__ __forceinline__ void warp_seg(const Ctx& c, int N, int& s0, int& s1) {
+  const int seg = ((N + c.NW - 1) / c.NW + 31) & ~31;
+  s0 = min(c.warp * seg, N);
+  s1 = min(s0 + seg, N);
+}
+// Exclusive scan over the warps of one int per warp; *total = the sum.  All threads.
+__device__ int warp_exscan(Ctx& c, int x, int* total) {
+  Scratch* s = c.s;
+  if (c.lane == 0) s->scan[c.warp] = x;
+  __syncthreads();
+  if (c.warp == 0) {
+    const int t = c.lane < c.NW ? s->scan[c.lane] : 0;
+    int ti = t;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(FULL, ti, o);
+      if (c.lane >= o) ti += y;
+    }
+    if (c.lane < c.NW) s->scan[c.lane] = ti - t;
+    if (c.lane == 31) s->scan_total = ti;
+  }
+  __syncthreads();
+  const int r = s->scan[c.warp];
+  *total = s->scan_total;
+  __syncthreads();
+  return r;
+}
+// Same for two doubles per warp.
+__device__ void warp_exscan_d2(Ctx& c, double& a, double& b, double* ta, double* tb) {
+  Scratch* s = c.s;
+  if (c.lane == 0) { s->scand[c.warp][0] = a; s->scand[c.warp][1] = b; }
+  __syncthreads();
+  if (c.warp == 0) {
+    const double xa = c.lane < c.NW ? s->scand[c.lane][0] : 0.0, xb = c.lane < c.NW ? s->scand[c.lane][1] : 0.0;
+    double ia = xa, ib = xb;
+    for (int o = 1; o < 32; o <<= 1) {
+      const double ya = __shfl_up_sync(FULL, ia, o), yb = __shfl_up_sync(FULL, ib, o);
+      if (c.lane >= o) { ia += ya; ib += yb; }
+    }
+    if (c.lane < c.NW) { s->scand[c.lane][0] = ia - xa; s->scand[c.lane][1] = ib - xb; }
+    if (c.lane == 31) { s->scand_total[0] = ia; s->scand_total[1] = ib; }
+  }
+  __syncthreads();
+  a = s->scand[c.warp][0];
+  b = s->scand[c.warp][1];
+  *ta = s->scand_total[0];
+  *tb = s->scand_total[1];
+  __syncthreads();
 }
 
 // ------------------------------------------------------ AHP L1 (Eq. 9, R10) --
@@ -596,7 +652,7 @@ __device__ void ahp_presort(Ctx& c) {
     __syncthreads();
   }
   for (int w = c.tid; w < c.nW; w += c.B) c.dirty[w] = 0u;
-  if (c.tid == 0) { s->ntouched = 0; s->touch_over = 0; }
+  if (c.tid == 0) { s->ntouched = 0; s->touch_over = 0; s->presorted = 1; }
   __syncthreads();
 }
 
@@ -615,63 +671,77 @@ __device__ void ahp_clear_dirty(Ctx& c) {
 }
 
 // Levels of the m sorted values keys[0..m) (servers sidx): lvm[l] = (value, multiplicity),
-// lvl[server] = level.  Returns K.  All threads.
+// lvl[server] = level.  Returns K.  All threads (warp-segmented, coalesced).
 __device__ int ahp_levels_sorted(Ctx& c, int m) {
-  Scratch* s = c.s;
-  const int B = c.B, tid = c.tid;
-  const int ipt = (m + B - 1) / B;
-  const int i0 = min(tid * ipt, m), i1 = min(i0 + ipt, m);
+  int s0, s1;
+  warp_seg(c, m, s0, s1);
   int cnt = 0;
-  for (int i = i0; i < i1; ++i) cnt += (i == 0 || c.keys[i] != c.keys[i - 1]);
-  int l = block_exscan(c, cnt);
-  if (tid == B - 1) s->lvK = l + cnt;
-  for (int i = i0; i < i1; ++i) {
-    if (i == 0 || c.keys[i] != c.keys[i - 1]) {
-      c.lvm[l].x = c.keys[i];
-      c.lst[l] = i;
-      ++l;
+  for (int base = s0; base < s1; base += 32) {
+    const int i = base + c.lane;
+    const bool f = i < s1 && (i == 0 || c.keys[i] != c.keys[i - 1]);
+    cnt += __popc(__ballot_sync(FULL, f));
+  }
+  int K;
+  int l0 = warp_exscan(c, cnt, &K);
+  for (int base = s0; base < s1; base += 32) {
+    const int i = base + c.lane;
+    const bool in = i < s1;
+    const bool f = in && (i == 0 || c.keys[i] != c.keys[i - 1]);
+    const unsigned bal = __ballot_sync(FULL, f);
+    const int q = l0 + __popc(bal & (0xffffffffu >> (31 - c.lane))) - 1;  // level of element i
+    if (f) {
+      c.lvm[q].x = c.keys[i];
+      c.lst[q] = i;
     }
-    c.lvl[c.sidx[i]] = l - 1;
+    if (in) c.lvl[c.sidx[i]] = q;
+    l0 += __popc(bal);
   }
   __syncthreads();
-  const int K = s->lvK;
-  for (int q = tid; q < K; q += B) c.lvm[q].y = (float)((q + 1 < K ? c.lst[q + 1] : m) - c.lst[q]);
+  for (int q = c.tid; q < K; q += c.B) c.lvm[q].y = (float)((q + 1 < K ? c.lst[q + 1] : m) - c.lst[q]);
   __syncthreads();
   return K;
 }
 
 __device__ __forceinline__ bool feas_bit(const Ctx& c, int u) { return (c.maskw[u >> 5] >> (u & 31)) & 1u; }
 
-// Sorted feasible values of presorted criterion ci: walk the presorted order keeping the
-// feasible servers not touched by this request, then merge in the touched feasible ones
-// (their current values).  Returns K (levels built).  All threads.
-__device__ int ahp_levels_presorted(Ctx& c, int ci) {
+// Sorted values of presorted criterion ci into keys / sidx: walk the presorted order keeping
+// the servers not touched by this request (only the feasible ones if feasible_only), then
+// merge in the touched ones at their current values.  Returns the count.  All threads.
+__device__ int presorted_collect(Ctx& c, int ci, bool feasible_only) {
   Scratch* s = c.s;
   const int n = c.g.n, P2 = next_pow2(n);
   const int* x = c.st + crit_of(ci) * n;
   const unsigned short* perm = c.perm + ci * P2;
-  const int ipt = (n + c.B - 1) / c.B;
-  const int i0 = min(c.tid * ipt, n), i1 = min(i0 + ipt, n);
+  int s0, s1;
+  warp_seg(c, n, s0, s1);
   int cnt = 0;
-  for (int i = i0; i < i1; ++i) {
-    const int u = perm[i];
-    cnt += feas_bit(c, u) && !((c.dirty[u >> 5] >> (u & 31)) & 1u);
+  for (int base = s0; base < s1; base += 32) {
+    const int i = base + c.lane;
+    const int u = i < s1 ? perm[i] : 0;
+    const bool k = i < s1 && (!feasible_only || feas_bit(c, u)) && !((c.dirty[u >> 5] >> (u & 31)) & 1u);
+    cnt += __popc(__ballot_sync(FULL, k));
   }
-  int pos = block_exscan(c, cnt);
-  if (c.tid == c.B - 1) s->m1 = pos + cnt;
-  for (int i = i0; i < i1; ++i) {
-    const int u = perm[i];
-    if (feas_bit(c, u) && !((c.dirty[u >> 5] >> (u & 31)) & 1u)) {
-      c.keys2[pos] = (float)x[u];
-      c.sidx2[pos] = u;
-      ++pos;
+  int mtot;
+  int pos = warp_exscan(c, cnt, &mtot);
+  if (c.tid == 0) s->m1 = mtot;
+  for (int base = s0; base < s1; base += 32) {
+    const int i = base + c.lane;
+    const int u = i < s1 ? perm[i] : 0;
+    const bool k = i < s1 && (!feasible_only || feas_bit(c, u)) && !((c.dirty[u >> 5] >> (u & 31)) & 1u);
+    const unsigned bal = __ballot_sync(FULL, k);
+    if (k) {
+      const int q = pos + __popc(bal & ((1u << c.lane) - 1u));
+      c.keys2[q] = (float)x[u];
+      c.sidx2[q] = u;
     }
+    pos += __popc(bal);
   }
-  if (c.tid == 0) {  // touched feasible servers, insertion-sorted by current value
+  if (c.tid == 0) {  // touched servers, insertion-sorted by current value
     int d = 0;
-    for (int t = 0; t < s->ntouched; ++t) {
+    const int nt = min(s->ntouched, 2 * MAXC);
+    for (int t = 0; t < nt; ++t) {
       const int u = s->touched[t];
-      if (!feas_bit(c, u)) continue;
+      if (feasible_only && !feas_bit(c, u)) continue;
       const float v = (float)x[u];
       int j = d;
       while (j > 0 && s->dval[j - 1] > v) { s->dval[j] = s->dval[j - 1]; s->dsrv[j] = s->dsrv[j - 1]; --j; }
@@ -683,14 +753,14 @@ __device__ int ahp_levels_presorted(Ctx& c, int ci) {
   }
   __syncthreads();
   const int m1 = s->m1, d = s->nd;
-  for (int i = c.tid; i < m1; i += c.B) {  // main values shift past the touched ones below them
+  for (int i = c.tid; i < m1; i += c.B) {  // untouched values shift past the touched ones below them
     const float v = c.keys2[i];
     int lo = 0, hi = d;
     while (lo < hi) { int mid = (lo + hi) >> 1; if (s->dval[mid] < v) lo = mid + 1; else hi = mid; }
     c.keys[i + lo] = v;
     c.sidx[i + lo] = c.sidx2[i];
   }
-  for (int j = c.tid; j < d; j += c.B) {  // touched values after the main ones <= them
+  for (int j = c.tid; j < d; j += c.B) {  // touched values after the untouched ones <= them
     const float v = s->dval[j];
     int lo = 0, hi = m1;
     while (lo < hi) { int mid = (lo + hi) >> 1; if (c.keys2[mid] <= v) lo = mid + 1; else hi = mid; }
@@ -698,7 +768,31 @@ __device__ int ahp_levels_presorted(Ctx& c, int ci) {
     c.sidx[j + lo] = s->dsrv[j];
   }
   __syncthreads();
-  return ahp_levels_sorted(c, m1 + d);
+  return m1 + d;
+}
+
+// Sorted feasible values of presorted criterion ci and their levels.  Returns K.
+__device__ int ahp_levels_presorted(Ctx& c, int ci) {
+  return ahp_levels_sorted(c, presorted_collect(c, ci, true));
+}
+
+// After an accepted request (sequential modes) the touched servers take their new values:
+// re-merge them into the presorted orders instead of sorting again.
+__device__ void ahp_presort_update(Ctx& c) {
+  Scratch* s = c.s;
+  if (s->touch_over) {  // more than the merge list holds: sort again at the next request
+    __syncthreads();
+    if (c.tid == 0) s->presorted = 0;
+    __syncthreads();
+    return;
+  }
+  const int n = c.g.n, P2 = next_pow2(n);
+  for (int ci = 0; ci < 3; ++ci) {
+    const int m = presorted_collect(c, ci, false);
+    for (int i = c.tid; i < m; i += c.B) c.perm[ci * P2 + i] = (unsigned short)c.sidx[i];
+    __syncthreads();
+  }
+  ahp_clear_dirty(c);
 }
 
 // Levels of the Fragmentation criterion f_u in {0,1}: no sort needed.
@@ -720,31 +814,46 @@ __device__ int ahp_levels_active(Ctx& c) {
   return K;
 }
 
-// Exclusive prefix sums over K levels of (y, y * x) of lv[] into pa, pb (pa[K], pb[K] totals).
+// Exclusive prefix sums over K levels of (y, y * x) of lv[] into pa, pb (pa[K], pb[K]
+// totals), in double, warp-segmented (fixed summation order for a given block size).
 __device__ void ahp_prefix(Ctx& c, int K, const float2* lv) {
-  const int ipt = (K + c.B - 1) / c.B;
-  const int i0 = min(c.tid * ipt, K), i1 = min(i0 + ipt, K);
-  double a = 0, b = 0;
-  for (int i = i0; i < i1; ++i) { a += (double)lv[i].y; b += (double)lv[i].y * (double)lv[i].x; }
-  double ea = a, eb = b;
-  block_exscan_d2(c, ea, eb);
-  for (int i = i0; i < i1; ++i) {
-    c.pa[i] = ea;
-    c.pb[i] = eb;
-    ea += (double)lv[i].y;
-    eb += (double)lv[i].y * (double)lv[i].x;
+  int s0, s1;
+  warp_seg(c, K, s0, s1);
+  double ta = 0, tb = 0;
+  for (int base = s0; base < s1; base += 32) {
+    const int i = base + c.lane;
+    if (i < s1) { const float2 e = lv[i]; ta += (double)e.y; tb += (double)e.y * (double)e.x; }
   }
-  if (c.tid == c.B - 1) { c.pa[K] = ea; c.pb[K] = eb; }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) { ta += __shfl_xor_sync(FULL, ta, o); tb += __shfl_xor_sync(FULL, tb, o); }
+  double TA, TB;
+  warp_exscan_d2(c, ta, tb, &TA, &TB);
+  double ra = ta, rb = tb;  // running exclusive prefix of this warp
+  for (int base = s0; base < s1; base += 32) {
+    const int i = base + c.lane;
+    double a = 0, b = 0;
+    if (i < s1) { const float2 e = lv[i]; a = (double)e.y; b = (double)e.y * (double)e.x; }
+    double ia = a, ib = b;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double ya = __shfl_up_sync(FULL, ia, o), yb = __shfl_up_sync(FULL, ib, o);
+      if (c.lane >= o) { ia += ya; ib += yb; }
+    }
+    if (i < s1) { c.pa[i] = ra + (ia - a); c.pb[i] = rb + (ib - b); }
+    ra += __shfl_sync(FULL, ia, 31);
+    rb += __shfl_sync(FULL, ib, 31);
+  }
+  if (c.tid == 0) { c.pa[K] = TA; c.pb[K] = TB; }
   __syncthreads();
 }
 
 // sum over k in [k0, k1) of arr[k].y / D(k), D = (v - arr[k].x) (pass 1, below) or
-// (arr[k].x - v) (pass 2, above), or 1 + s * that under the shifted rule.  FP32 with MUFU
-// reciprocals; four interleaved accumulators per chunk of 32 terms (error analysis in
-// DESIGN.md §5 covers any chunking of at most 32 terms).
+// (arr[k].x - v) (pass 2, above), or 1 + s * that under the shifted rule.  Terms in FP32
+// with MUFU reciprocals, summed in chunks of 32 (four interleaved accumulators); the
+// chunk sums accumulate in FP64, so the error does not grow with the number of levels.
 template <bool ABOVE>
-__device__ __forceinline__ float rsum_f32(const float2* arr, int k0, int k1, float v, float sc, int rule) {
-  float outer = 0.f;
+__device__ __forceinline__ double rsum_f32(const float2* arr, int k0, int k1, float v, float sc, int rule) {
+  double outer = 0.0;
   int k = k0;
   float h0 = 0.f;
   for (; k < k1 && (k & 3); ++k) {  // head up to a multiple of 4
@@ -752,7 +861,7 @@ __device__ __forceinline__ float rsum_f32(const float2* arr, int k0, int k1, flo
     const float d = ABOVE ? o.x - v : v - o.x;
     h0 += o.y * rcp_approx(rule ? fmaf(sc, d, 1.0f) : d);
   }
-  outer += h0;
+  outer += (double)h0;
   for (; k + 32 <= k1; k += 32) {
     float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
     const float4* q = reinterpret_cast<const float4*>(arr + k);
@@ -766,7 +875,7 @@ __device__ __forceinline__ float rsum_f32(const float2* arr, int k0, int k1, flo
       a2 = fmaf(y.y, rcp_approx(rule ? fmaf(sc, d2, 1.0f) : d2), a2);
       a3 = fmaf(y.w, rcp_approx(rule ? fmaf(sc, d3, 1.0f) : d3), a3);
     }
-    outer += (a0 + a1) + (a2 + a3);
+    outer += (double)((a0 + a1) + (a2 + a3));
   }
   float t0 = 0.f;
   for (; k < k1; ++k) {
@@ -774,7 +883,37 @@ __device__ __forceinline__ float rsum_f32(const float2* arr, int k0, int k1, flo
     const float d = ABOVE ? o.x - v : v - o.x;
     t0 += o.y * rcp_approx(rule ? fmaf(sc, d, 1.0f) : d);
   }
-  return outer + t0;
+  return outer + (double)t0;
+}
+
+// Warp-cooperative version for long level lists (grid passes): lane takes terms
+// k0 + lane + 32 j, FP32 chunks of 32 terms per lane into an FP64 lane sum, then a
+// fixed-order shuffle tree (deterministic).
+template <bool ABOVE>
+__device__ __forceinline__ double rsum_warp(const float2* arr, int k0, int k1, float v, float sc, int rule,
+                                            int lane) {
+  double outer = 0.0;
+  int k = k0 + lane;
+  while (k < k1) {
+    float a0 = 0.f, a1 = 0.f;
+    int j = 0;
+    for (; j < 32 && k + 32 < k1; j += 2, k += 64) {
+      const float2 o = arr[k], p = arr[k + 32];
+      const float d0 = ABOVE ? o.x - v : v - o.x, d1 = ABOVE ? p.x - v : v - p.x;
+      a0 = fmaf(o.y, rcp_approx(rule ? fmaf(sc, d0, 1.0f) : d0), a0);
+      a1 = fmaf(p.y, rcp_approx(rule ? fmaf(sc, d1, 1.0f) : d1), a1);
+    }
+    if (j < 32 && k < k1) {
+      const float2 o = arr[k];
+      const float d0 = ABOVE ? o.x - v : v - o.x;
+      a0 = fmaf(o.y, rcp_approx(rule ? fmaf(sc, d0, 1.0f) : d0), a0);
+      k += 32;
+    }
+    outer += (double)(a0 + a1);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) outer += __shfl_xor_sync(FULL, outer, o);
+  return outer;
 }
 
 // FP32 passes over the K levels of criterion kc -> l2out[l] = L2 of level l.
@@ -793,7 +932,7 @@ __device__ void ahp_passes_f32(Ctx& c, int kc, int K, int m, float* l2out) {
       const int l = side ? K - 1 - t : t;
       if (side && l == t) break;
       const float2 me = c.lvm[l];
-      const float rec = rsum_f32<false>(c.lvm, 0, l, me.x, sc, rule);
+      const double rec = rsum_f32<false>(c.lvm, 0, l, me.x, sc, rule);
       const double cgt = PAK - c.pa[l + 1];
       const double G = (PBK - c.pb[l + 1]) - cgt * (double)me.x;  // sum_{k>l} m_k (v_k - v_l), exact
       const double col = rule ? cgt + sd * G + (double)me.y + (double)rec
@@ -808,7 +947,7 @@ __device__ void ahp_passes_f32(Ctx& c, int kc, int K, int m, float* l2out) {
       const int l = side ? K - 1 - t : t;
       if (side && l == t) break;
       const float2 me = c.lvw[l];
-      const float rec = rsum_f32<true>(c.lvw, l + 1, K, me.x, sc, rule);
+      const double rec = rsum_f32<true>(c.lvw, l + 1, K, me.x, sc, rule);
       const double lin = (double)me.x * c.pa[l] - c.pb[l];  // sum_{k<l} w_k (v_l - v_k)
       const double L = rule ? c.pa[l] + sd * lin + (double)me.y + (double)rec
                             : sd * lin + (double)me.y + (double)rec * inv_sd;
@@ -1118,8 +1257,8 @@ __device__ void req_begin(Ctx& c, const ReqsDev& R, int r, bool keep) {
     }
   }
   __syncthreads();
-  if (METHOD == 0) {  // presorted criteria: per request when requests commit, else per snapshot
-    if (keep || s->touch_over) ahp_presort(c);
+  if (METHOD == 0) {  // presorted criteria: sort once, then keep the order (see ahp_presort_update)
+    if (s->touch_over || !s->presorted) ahp_presort(c);
     else ahp_clear_dirty(c);
   }
 }
@@ -1223,6 +1362,7 @@ __device__ void run_request(Ctx& c, const ReqsDev& R, const OutDev& O, int r, bo
     }
   }
   req_finish(c, R, O, r, keep);
+  if (METHOD == 0 && keep) ahp_presort_update(c);
 }
 
 // ------------------------------------------------------------- kernels ------
@@ -1254,6 +1394,9 @@ __device__ void init_ctx(Ctx& c, const Geo& g, const Opt& o, Scratch* s) {
   c.dirty = nullptr;
   if (c.tid == 0) {
     s->c_steps = s->c_retries = s->c_fp64 = s->c_invalid = s->c_feas = s->c_pairs = 0;
+    s->presorted = 0;
+    s->touch_over = 0;
+    s->ntouched = 0;
     if (o.method == 0) {
       double L1[4];
       ahp_l1_dev(o, L1);
@@ -1491,12 +1634,13 @@ __device__ void sh_flush(Ctx& c, unsigned long long* stats) {
 
 template <int METHOD>
 __global__ void __launch_bounds__(1024) k_sh_begin(Geo g, Opt o, int* state, ReqsDev R, OutDev O, int r,
-                                                   ShardDev d) {
+                                                   ShardDev d, int first) {
   Ctx c;
   sh_ctx(c, g, o, state, d);
   Scratch* s = c.s;
   if (c.tid == 0) {
     s->c_steps = s->c_retries = s->c_fp64 = s->c_invalid = s->c_feas = s->c_pairs = 0;
+    if (first) { s->presorted = 0; s->touch_over = 0; s->ntouched = 0; }
     if (METHOD == 0) {
       double L1[4];
       ahp_l1_dev(o, L1);
@@ -1605,6 +1749,7 @@ __device__ void sh_commit_advance(Ctx& c, const ReqsDev& R, const OutDev& O, int
   }
   if (p + 1 == s->P) {
     req_finish(c, R, O, r, true);
+    if (METHOD == 0) ahp_presort_update(c);
     sh_flush(c, d.stats);
     if (c.tid == 0) d.ctl[0] = PH_DONE;
   } else if (c.tid == 0) {
@@ -1700,6 +1845,7 @@ __global__ void __launch_bounds__(256) k_ahp_pass(Geo g, Opt o, int q0, int q1, 
   const int n2 = next_pow2(g.n);
   const int m = s->nf;
   const int rule = o.ahp_rule;
+  const int lane = threadIdx.x & 31;
   int a[4], b[4], total = 0;
   for (int k = 0; k < 4; ++k) {
     const int K = d.Kc[k], half = (K + 1) >> 1;
@@ -1707,7 +1853,9 @@ __global__ void __launch_bounds__(256) k_ahp_pass(Geo g, Opt o, int q0, int q1, 
     b[k] = (int)((long long)half * q1 / world);
     total += b[k] - a[k];
   }
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+  // one warp per level pair (t, K-1-t): lanes split the K-1 terms
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < total; i += nwarps) {
     int k = 0, t = i;
     while (t >= b[k] - a[k]) { t -= b[k] - a[k]; ++k; }
     t += a[k];
@@ -1723,39 +1871,45 @@ __global__ void __launch_bounds__(256) k_ahp_pass(Geo g, Opt o, int q0, int q1, 
       if (side && l == t) break;
       if (PASS == 1) {
         const double vl = lvm[l].x, ml = lvm[l].y;
-        double rec;
+        double rec = 0;
         if (FP64) {
-          rec = 0;
-          for (int q = 0; q < l; ++q) {
+          for (int q = lane; q < l; q += 32) {
             const double dd = vl - (double)lvm[q].x;
             rec += (double)lvm[q].y / (rule ? 1.0 + sd * dd : dd);
           }
+#pragma unroll
+          for (int off = 16; off > 0; off >>= 1) rec += __shfl_xor_sync(FULL, rec, off);
         } else {
-          rec = (double)rsum_f32<false>(lvm, 0, l, lvm[l].x, sc, rule);
+          rec = rsum_warp<false>(lvm, 0, l, lvm[l].x, sc, rule, lane);
         }
-        const double cgt = pa[K] - pa[l + 1];
-        const double G = (pb[K] - pb[l + 1]) - cgt * vl;  // sum_{k>l} m_k (v_k - v_l), exact
-        const double col = rule ? cgt + sd * G + ml + rec : sd * G + ml + rec / sd;
-        if (FP64) d.wq64[k * n2 + l] = ml / col;
-        else d.wq[k * n2 + l] = (float)(ml / col);
+        if (lane == 0) {
+          const double cgt = pa[K] - pa[l + 1];
+          const double G = (pb[K] - pb[l + 1]) - cgt * vl;  // sum_{k>l} m_k (v_k - v_l), exact
+          const double col = rule ? cgt + sd * G + ml + rec : sd * G + ml + rec / sd;
+          if (FP64) d.wq64[k * n2 + l] = ml / col;
+          else d.wq[k * n2 + l] = (float)(ml / col);
+        }
       } else {
         const double vl = lvw[l].x;
-        double rec, wl;
+        double rec = 0, wl;
         if (FP64) {
           wl = d.wq64[k * n2 + l];
-          rec = 0;
-          for (int q = l + 1; q < K; ++q) {
+          for (int q = l + 1 + lane; q < K; q += 32) {
             const double dd = (double)lvw[q].x - vl;
             rec += d.wq64[k * n2 + q] / (rule ? 1.0 + sd * dd : dd);
           }
+#pragma unroll
+          for (int off = 16; off > 0; off >>= 1) rec += __shfl_xor_sync(FULL, rec, off);
         } else {
           wl = (double)lvw[l].y;
-          rec = (double)rsum_f32<true>(lvw, l + 1, K, lvw[l].x, sc, rule);
+          rec = rsum_warp<true>(lvw, l + 1, K, lvw[l].x, sc, rule, lane);
         }
-        const double lin = vl * pa[l] - pb[l];  // sum_{k<l} w_k (v_l - v_k)
-        const double L = rule ? pa[l] + sd * lin + wl + rec : sd * lin + wl + rec / sd;
-        if (FP64) d.l2q64[k * n2 + l] = L / (double)m;
-        else d.l2q[k * n2 + l] = (float)(L / (double)m);
+        if (lane == 0) {
+          const double lin = vl * pa[l] - pb[l];  // sum_{k<l} w_k (v_l - v_k)
+          const double L = rule ? pa[l] + sd * lin + wl + rec : sd * lin + wl + rec / sd;
+          if (FP64) d.l2q64[k * n2 + l] = L / (double)m;
+          else d.l2q[k * n2 + l] = (float)(L / (double)m);
+        }
       }
     }
   }
@@ -1881,8 +2035,8 @@ size_t scratch_bytes() { return sizeof(Scratch); }
 
 cudaError_t launch_sh_begin(const Geo& g, const Opt& o, int* state, const ReqsDev& R, const OutDev& O, int r,
                             const ShardDev& d, cudaStream_t st) {
-  if (o.method == 1) k_sh_begin<1><<<1, 1024, 0, st>>>(g, o, state, R, O, r, d);
-  else k_sh_begin<0><<<1, 1024, 0, st>>>(g, o, state, R, O, r, d);
+  if (o.method == 1) k_sh_begin<1><<<1, 1024, 0, st>>>(g, o, state, R, O, r, d, r == 0);
+  else k_sh_begin<0><<<1, 1024, 0, st>>>(g, o, state, R, O, r, d, r == 0);
   return cudaGetLastError();
 }
 cudaError_t launch_sh_prep(const Geo& g, const Opt& o, int* state, const ReqsDev& R, const OutDev& O, int r,
