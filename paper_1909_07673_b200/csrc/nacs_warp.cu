@@ -45,8 +45,7 @@ template <typename LT>
 struct WCtx {
   int k, h, n, npad, E, nfabea;  // nfabea = E*h (start of agg-core links in fab[])
   unsigned magic;
-  const int4 *cpu4, *ram4, *act4, *acc4;  // criteria SoA (shared)
-  const int *cpu, *ram, *act, *acc;
+  const int* snap;  // criteria in 128-server tiles: tile t = cpu[128] | ram[128] | act[128] | acc[128] (shared)
   const LT* fab;                           // edge-agg[E*h] | agg-core[k*h*h] (shared)
   WScr* w;
   unsigned *dirty, *edgebad, *pm;
@@ -54,9 +53,12 @@ struct WCtx {
   int ulog_n;
   int lane;
   int nDW;
-  unsigned a_cpu, a_ram, a_act, a_acc, a_edge;  // 32-bit shared addresses (+16*lane for the SoA)
+  unsigned a_snap, a_edge;  // 32-bit shared addresses (a_snap: + 16 * lane)
   Opt o;
 };
+
+// criterion j (0 cpu, 1 ram, 2 act, 3 acc) of server u in the tiled shared snapshot
+__device__ __forceinline__ int tile_idx(int u, int j) { return ((u >> 7) << 9) + (j << 7) + (u & 127); }
 
 __device__ __forceinline__ unsigned smem_addr(const void* p) {
   return static_cast<unsigned>(__cvta_generic_to_shared(p));
@@ -117,7 +119,7 @@ __device__ __forceinline__ int w_slot(const WCtx<LT>& c, int u) {
 template <typename LT>
 __device__ __forceinline__ int acc_val(const WCtx<LT>& c, int u) {
   int s = os_slot(c, u);
-  return s >= 0 ? c.w->os_acc[s] : c.acc[u];
+  return s >= 0 ? c.w->os_acc[s] : c.snap[tile_idx(u, 3)];
 }
 
 // -------------------------------------------- overlay writes (warp-cooperative) --
@@ -420,6 +422,14 @@ __device__ __forceinline__ void acc_b(AccB& b, bool ok, float q, int u) {
   b.b1 = lt ? qe : b.b1;
 }
 
+// merge accumulator o (a disjoint set of servers) into a: lowest index on equal q
+__device__ __forceinline__ void merge_b(AccB& a, const AccB& o) {
+  const bool lt = o.b1 < a.b1 || (o.b1 == a.b1 && (unsigned)o.i1 < (unsigned)a.i1);
+  a.b2 = fminf(fminf(a.b2, o.b2), lt ? a.b1 : o.b1);
+  a.i1 = lt ? o.i1 : a.i1;
+  a.b1 = lt ? o.b1 : a.b1;
+}
+
 __device__ __forceinline__ void set_comp(int4& v, int j, int x) {
   if (j == 0) v.x = x;
   else if (j == 1) v.y = x;
@@ -466,11 +476,11 @@ __device__ __forceinline__ bool ok_any(const StepP& sp, int x0, int x1, int x3, 
 template <typename LT>
 __device__ __forceinline__ void load_chunk(const WCtx<LT>& c, const StepP& sp, int ch, int& spp, int& nxt, int4& C,
                                            int4& Rm, int4& A, int4& Q, int4& I) {
-  const unsigned ao = (unsigned)ch << 9;
-  C = lds128(c.a_cpu + ao);
-  Rm = lds128(c.a_ram + ao);
-  A = lds128(c.a_act + ao);
-  Q = lds128(c.a_acc + ao);
+  const unsigned ao = c.a_snap + ((unsigned)ch << 11);
+  C = lds128(ao);
+  Rm = lds128(ao + 512);
+  A = lds128(ao + 1024);
+  Q = lds128(ao + 1536);
   I = make_int4(0, 0, 0, 0);
   const int base = ch << 7;
   if (nxt < base + 128) {  // warp-uniform
@@ -493,9 +503,8 @@ __device__ void scan_stats(const WCtx<LT>& c, const StepP& sp, AccA& a) {
     const unsigned u0 = (unsigned)((ch << 7) + 4 * c.lane);
     const unsigned eb = ebad4(c, sp, u0);
     if (nxt >= (ch << 7) + 128) {
-      const unsigned ao = (unsigned)ch << 9;
-      const int4 C = lds128(c.a_cpu + ao), Rm = lds128(c.a_ram + ao), A = lds128(c.a_act + ao),
-                 Q = lds128(c.a_acc + ao);
+      const unsigned ao = c.a_snap + ((unsigned)ch << 11);
+      const int4 C = lds128(ao), Rm = lds128(ao + 512), A = lds128(ao + 1024), Q = lds128(ao + 1536);
       acc_a(a, ok_plain(sp, C.x, Rm.x, Q.x, eb & 1u), C.x, Rm.x, A.x, Q.x);
       acc_a(a, ok_plain(sp, C.y, Rm.y, Q.y, eb & 2u), C.y, Rm.y, A.y, Q.y);
       acc_a(a, ok_plain(sp, C.z, Rm.z, Q.z, eb & 4u), C.z, Rm.z, A.z, Q.z);
@@ -517,17 +526,17 @@ __device__ void scan_score(const WCtx<LT>& c, const StepP& sp, const TopsisP& tp
   const int nch = c.npad >> 7;
   int spp = 0;
   int nxt = c.w->nsp > 0 ? c.w->sp_u[0] : INT_MAX;
+  AccB b2 = {__int_as_float(0x7f800000), __int_as_float(0x7f800000), -1};  // odd servers: shorter chains
   for (int ch = 0; ch < nch; ++ch) {
     const unsigned u0 = (unsigned)((ch << 7) + 4 * c.lane);
     const unsigned eb = ebad4(c, sp, u0);
     if (nxt >= (ch << 7) + 128) {
-      const unsigned ao = (unsigned)ch << 9;
-      const int4 C = lds128(c.a_cpu + ao), Rm = lds128(c.a_ram + ao), A = lds128(c.a_act + ao),
-                 Q = lds128(c.a_acc + ao);
+      const unsigned ao = c.a_snap + ((unsigned)ch << 11);
+      const int4 C = lds128(ao), Rm = lds128(ao + 512), A = lds128(ao + 1024), Q = lds128(ao + 1536);
       acc_b(b, ok_plain(sp, C.x, Rm.x, Q.x, eb & 1u), topsis_q32(tp, C.x, Rm.x, A.x, Q.x), (int)u0);
-      acc_b(b, ok_plain(sp, C.y, Rm.y, Q.y, eb & 2u), topsis_q32(tp, C.y, Rm.y, A.y, Q.y), (int)u0 + 1);
+      acc_b(b2, ok_plain(sp, C.y, Rm.y, Q.y, eb & 2u), topsis_q32(tp, C.y, Rm.y, A.y, Q.y), (int)u0 + 1);
       acc_b(b, ok_plain(sp, C.z, Rm.z, Q.z, eb & 4u), topsis_q32(tp, C.z, Rm.z, A.z, Q.z), (int)u0 + 2);
-      acc_b(b, ok_plain(sp, C.w, Rm.w, Q.w, eb & 8u), topsis_q32(tp, C.w, Rm.w, A.w, Q.w), (int)u0 + 3);
+      acc_b(b2, ok_plain(sp, C.w, Rm.w, Q.w, eb & 8u), topsis_q32(tp, C.w, Rm.w, A.w, Q.w), (int)u0 + 3);
     } else {
       int4 C, Rm, A, Q, I;
       load_chunk(c, sp, ch, spp, nxt, C, Rm, A, Q, I);
@@ -539,6 +548,7 @@ __device__ void scan_score(const WCtx<LT>& c, const StepP& sp, const TopsisP& tp
       }
     }
   }
+  merge_b(b, b2);
 }
 
 // FP64 re-decision (R14): exact closeness of the candidates within 2 delta of s1.
@@ -775,9 +785,9 @@ __device__ int commit_step(WCtx<LT>& c, WReq& q, const StepP& sp, int best) {
   int fail = 0;
   {
     int s = w_slot(c, best);
-    int cu = s >= 0 ? w->os_cpu[s] : c.cpu[best];
-    int ru = s >= 0 ? w->os_ram[s] : c.ram[best];
-    int qu = s >= 0 ? w->os_acc[s] : c.acc[best];
+    int cu = s >= 0 ? w->os_cpu[s] : c.snap[tile_idx(best, 0)];
+    int ru = s >= 0 ? w->os_ram[s] : c.snap[tile_idx(best, 1)];
+    int qu = s >= 0 ? w->os_acc[s] : c.snap[tile_idx(best, 3)];
     if (!w_set_server(c, best, cu - sp.dc, ru - sp.dr, 1, qu)) fail = 2;
   }
   const int nflow = w->nflow;
@@ -791,14 +801,15 @@ __device__ int commit_step(WCtx<LT>& c, WReq& q, const StepP& sp, int best) {
     const int2 wp = wpath(c, best, v);
     const int su = w_slot(c, best), sv = w_slot(c, v);
     const int au = w->os_acc[su];
-    const int av = sv >= 0 ? w->os_acc[sv] : c.acc[v];
+    const int av = sv >= 0 ? w->os_acc[sv] : c.snap[tile_idx(v, 3)];
     if (min(min(au, av), wp.y) < D) {
       fail = 1;
       break;
     }
     bool ok = w_set_server(c, best, w->os_cpu[su], w->os_ram[su], w->os_act[su], au - D);
-    const int cv = sv >= 0 ? w->os_cpu[sv] : c.cpu[v], rv = sv >= 0 ? w->os_ram[sv] : c.ram[v];
-    const int tv = sv >= 0 ? w->os_act[sv] : c.act[v];
+    const int cv = sv >= 0 ? w->os_cpu[sv] : c.snap[tile_idx(v, 0)];
+    const int rv = sv >= 0 ? w->os_ram[sv] : c.snap[tile_idx(v, 1)];
+    const int tv = sv >= 0 ? w->os_act[sv] : c.snap[tile_idx(v, 2)];
     ok = ok && w_set_server(c, v, cv, rv, tv, av - D);
     int fid[4];
     const int m = path_fids(c, best, v, wp.x, fid);
@@ -902,45 +913,85 @@ __device__ void finish_request(WCtx<LT>& c, const WReq& q, const OutDev& O) {
   __syncwarp();
 }
 
+// Named barrier over the nt threads of one warp group (id >= 1; 0 is __syncthreads).
+__device__ __forceinline__ void group_sync(int id, int nt) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nt) : "memory");
+}
+__device__ __forceinline__ bool group_sync_and(int id, int nt, bool p) {
+  int r;
+  asm volatile(
+      "{\n .reg .pred a, b;\n setp.ne.u32 a, %1, 0;\n bar.red.and.pred b, %2, %3, a;\n selp.u32 %0, 1, 0, b;\n}"
+      : "=r"(r)
+      : "r"((int)p), "r"(id), "r"(nt)
+      : "memory");
+  return r != 0;
+}
+
 // The warps of a CTA advance in lockstep phases (prepare | pass A | pass B | commit), each
 // on its own request, so that all warps run the same loop at the same time (one copy of
 // the hot code in the instruction caches); within a phase no warp waits for another.
 template <typename LT>
 __global__ void __launch_bounds__(512, 1) k_batch_warp(Geo g, Opt o, const int* __restrict__ state, ReqsDev R,
                                                        OutDev O, int4* ulog_all, int* next, const int* order,
-                                                       int* deferred, int* n_deferred, unsigned long long* stats) {
+                                                       int* deferred, int* n_deferred, unsigned long long* stats,
+                                                       int group) {
   extern __shared__ __align__(16) unsigned char dyn[];
   const int n = g.n, h = g.h, k = g.k, E = g.E;
   const int npad = (n + 127) & ~127;
   // ---- a0: shared snapshot (read-only for the whole kernel)
-  int* scpu = reinterpret_cast<int*>(dyn);
-  int* sram = scpu + npad;
-  int* sact = sram + npad;
-  int* sacc = sact + npad;
-  LT* sfab = reinterpret_cast<LT*>(sacc + npad);
+  int* ssnap = reinterpret_cast<int*>(dyn);
+  LT* sfab = reinterpret_cast<LT*>(ssnap + 4 * npad);
   const int nfab = E * h + k * h * h;
   size_t off = (size_t)16 * npad + (((size_t)sizeof(LT) * nfab + 15) & ~(size_t)15);
   const int nDW = (E + k * h + 31) >> 5, nEW = (E + 31) >> 5;
   const size_t wbytes = ((sizeof(WScr) + 4 * (nDW + nEW + k)) + 15) & ~(size_t)15;
-  for (int i = threadIdx.x; i < npad; i += blockDim.x) {
-    bool in = i < n;
-    scpu[i] = in ? state[i] : -1;  // padding is never feasible (demands are > 0)
-    sram[i] = in ? state[n + i] : -1;
-    sact[i] = in ? state[2 * n + i] : 0;
-    sacc[i] = in ? state[3 * n + i] : 0;
+  __shared__ __align__(8) unsigned long long mbar;
+  // criteria rows -> 128-server tiles: one 512-byte TMA bulk copy per (tile, criterion)
+  const bool bulk = npad == n;
+  const int ncp = 4 * (npad >> 7);
+  if (bulk && threadIdx.x == 0) {
+    const unsigned mb = smem_addr(&mbar);
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(16u * (unsigned)n) : "memory");
   }
-  for (int i = threadIdx.x; i < nfab; i += blockDim.x) sfab[i] = (LT)state[4 * n + i];
   __syncthreads();
+  if (bulk) {
+    const unsigned mb = smem_addr(&mbar);
+    for (int i = threadIdx.x; i < ncp; i += blockDim.x) {
+      const int t = i >> 2, j = i & 3;
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 512, [%2];" ::"r"(
+                       smem_addr(ssnap + (t << 9) + (j << 7))),
+                   "l"(state + (size_t)j * n + (t << 7)), "r"(mb)
+                   : "memory");
+    }
+  } else {
+    for (int i = threadIdx.x; i < 4 * npad; i += blockDim.x) {
+      const int j = i / npad, u = i - j * npad;
+      // padding is never feasible (demands are > 0): cpu = ram = -1
+      ssnap[tile_idx(u, j)] = u < n ? state[(size_t)j * n + u] : (j < 2 ? -1 : 0);
+    }
+  }
+  for (int i = threadIdx.x; i < nfab; i += blockDim.x) sfab[i] = (LT)__ldg(state + 4 * n + i);
+  __syncthreads();
+  if (bulk) {
+    const unsigned mb = smem_addr(&mbar);
+    asm volatile(
+        "{\n .reg .pred P1;\n WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n"
+        " @!P1 bra WAIT_%=;\n}" ::"r"(mb)
+        : "memory");
+  }
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // warp groups advance in lockstep independently (named barrier 1 + group index)
+  const int nwarps = blockDim.x >> 5, gid = warp / group;
+  const int bar_id = 1 + gid, bar_nt = 32 * min(group, nwarps - gid * group);
   WCtx<LT> c;
   c.k = k; c.h = h; c.n = n; c.npad = npad; c.E = E; c.nfabea = E * h;
   c.magic = g.magic_h;
-  c.cpu = scpu; c.ram = sram; c.act = sact; c.acc = sacc;
-  c.a_cpu = smem_addr(scpu) + 16u * lane;
-  c.a_ram = smem_addr(sram) + 16u * lane;
-  c.a_act = smem_addr(sact) + 16u * lane;
-  c.a_acc = smem_addr(sacc) + 16u * lane;
+  c.snap = ssnap;
+  c.a_snap = smem_addr(ssnap) + 16u * lane;
   c.fab = sfab;
   unsigned char* wb = dyn + off + (size_t)warp * wbytes;
   c.w = reinterpret_cast<WScr*>(wb);
@@ -975,7 +1026,7 @@ __global__ void __launch_bounds__(512, 1) k_batch_warp(Geo g, Opt o, const int* 
       prep = false;
     }
     if (active) build_specials(c);
-    if (__syncthreads_and(done)) break;
+    if (group_sync_and(bar_id, bar_nt, done)) break;
     // ---- phase A (a3 + a4): filter and statistics
     bool stepping = active;
     if (stepping) {
@@ -1000,7 +1051,7 @@ __global__ void __launch_bounds__(512, 1) k_batch_warp(Geo g, Opt o, const int* 
         topsis_params(tp, wd, sq);
       }
     }
-    __syncthreads();
+    group_sync(bar_id, bar_nt);
     // ---- phase B (a5T + a7): closeness, argmax (lowest index), FP64 near-tie re-decision
     if (stepping) {
       const float INF = __int_as_float(0x7f800000);
@@ -1023,7 +1074,7 @@ __global__ void __launch_bounds__(512, 1) k_batch_warp(Geo g, Opt o, const int* 
         ws.fp64 += 1;
       }
     }
-    __syncthreads();
+    group_sync(bar_id, bar_nt);
     // ---- phase C (a8, a9): commit; next pod, retry (R18), or request end
     if (stepping) {
       int fail = commit_step(c, q, sp, best);
@@ -1110,15 +1161,20 @@ cudaError_t launch_batch_warp(const Geo& g, const Opt& o, const int* d_state, co
                               unsigned long long* stats, int grid, int warps, cudaStream_t st) {
   bool u16 = g.link_cap <= 65535;
   k_order_lpt<<<1, 1024, 0, st>>>(R, order);
+  static const int group = [] {
+    const char* e = getenv("NACS_WARP_GROUP");
+    int v = e ? atoi(e) : 8;
+    return v < 1 ? 1 : (v > 16 ? 16 : v);
+  }();
   size_t smem = warp_snapshot_bytes(g, u16) + (size_t)warps * warp_scratch_bytes(g);
   if (u16) {
     cudaFuncSetAttribute(k_batch_warp<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_batch_warp<uint16_t><<<grid, warps * 32, smem, st>>>(g, o, d_state, R, O, ulog, next, order, deferred,
-                                                           n_deferred, stats);
+                                                           n_deferred, stats, group);
   } else {
     cudaFuncSetAttribute(k_batch_warp<int>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_batch_warp<int><<<grid, warps * 32, smem, st>>>(g, o, d_state, R, O, ulog, next, order, deferred, n_deferred,
-                                                      stats);
+                                                      stats, group);
   }
   return cudaGetLastError();
 }
