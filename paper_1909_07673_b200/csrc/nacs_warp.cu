@@ -38,6 +38,8 @@ struct WScr {
   int fv[WF], fD[WF], fok[WF], fpath[WF];
   int sp_u[WSP], sp_info[WSP];
   int ex[WX];
+  unsigned slow[4];  // chunks of 128 servers the scans take on the slow path (<= 128 chunks)
+  int net;
   // dynamic tail: dirty[(E + k*h + 31)/32] | edgebad[(E+31)/32] | pm[k]
 };
 
@@ -499,17 +501,21 @@ __device__ void scan_stats(const WCtx<LT>& c, const StepP& sp, AccA& a) {
   const int nch = c.npad >> 7;
   int spp = 0;
   int nxt = c.w->nsp > 0 ? c.w->sp_u[0] : INT_MAX;
+  unsigned sl = 0;
   for (int ch = 0; ch < nch; ++ch) {
     const unsigned u0 = (unsigned)((ch << 7) + 4 * c.lane);
-    const unsigned eb = ebad4(c, sp, u0);
-    if (nxt >= (ch << 7) + 128) {
+    if ((ch & 31) == 0) sl = c.w->slow[ch >> 5];
+    const bool fast = !(sl & 1u);
+    sl >>= 1;
+    if (fast) {
       const unsigned ao = c.a_snap + ((unsigned)ch << 11);
       const int4 C = lds128(ao), Rm = lds128(ao + 512), A = lds128(ao + 1024), Q = lds128(ao + 1536);
-      acc_a(a, ok_plain(sp, C.x, Rm.x, Q.x, eb & 1u), C.x, Rm.x, A.x, Q.x);
-      acc_a(a, ok_plain(sp, C.y, Rm.y, Q.y, eb & 2u), C.y, Rm.y, A.y, Q.y);
-      acc_a(a, ok_plain(sp, C.z, Rm.z, Q.z, eb & 4u), C.z, Rm.z, A.z, Q.z);
-      acc_a(a, ok_plain(sp, C.w, Rm.w, Q.w, eb & 8u), C.w, Rm.w, A.w, Q.w);
+      acc_a(a, ok_plain(sp, C.x, Rm.x, Q.x, 0u), C.x, Rm.x, A.x, Q.x);
+      acc_a(a, ok_plain(sp, C.y, Rm.y, Q.y, 0u), C.y, Rm.y, A.y, Q.y);
+      acc_a(a, ok_plain(sp, C.z, Rm.z, Q.z, 0u), C.z, Rm.z, A.z, Q.z);
+      acc_a(a, ok_plain(sp, C.w, Rm.w, Q.w, 0u), C.w, Rm.w, A.w, Q.w);
     } else {
+      const unsigned eb = ebad4(c, sp, u0);
       int4 C, Rm, A, Q, I;
       load_chunk(c, sp, ch, spp, nxt, C, Rm, A, Q, I);
       acc_a(a, ok_any(sp, C.x, Rm.x, Q.x, eb & 1u, I.x), C.x, Rm.x, A.x, Q.x);
@@ -527,17 +533,21 @@ __device__ void scan_score(const WCtx<LT>& c, const StepP& sp, const TopsisP& tp
   int spp = 0;
   int nxt = c.w->nsp > 0 ? c.w->sp_u[0] : INT_MAX;
   AccB b2 = {__int_as_float(0x7f800000), __int_as_float(0x7f800000), -1};  // odd servers: shorter chains
+  unsigned sl = 0;
   for (int ch = 0; ch < nch; ++ch) {
     const unsigned u0 = (unsigned)((ch << 7) + 4 * c.lane);
-    const unsigned eb = ebad4(c, sp, u0);
-    if (nxt >= (ch << 7) + 128) {
+    if ((ch & 31) == 0) sl = c.w->slow[ch >> 5];
+    const bool fast = !(sl & 1u);
+    sl >>= 1;
+    if (fast) {
       const unsigned ao = c.a_snap + ((unsigned)ch << 11);
       const int4 C = lds128(ao), Rm = lds128(ao + 512), A = lds128(ao + 1024), Q = lds128(ao + 1536);
-      acc_b(b, ok_plain(sp, C.x, Rm.x, Q.x, eb & 1u), topsis_q32(tp, C.x, Rm.x, A.x, Q.x), (int)u0);
-      acc_b(b2, ok_plain(sp, C.y, Rm.y, Q.y, eb & 2u), topsis_q32(tp, C.y, Rm.y, A.y, Q.y), (int)u0 + 1);
-      acc_b(b, ok_plain(sp, C.z, Rm.z, Q.z, eb & 4u), topsis_q32(tp, C.z, Rm.z, A.z, Q.z), (int)u0 + 2);
-      acc_b(b2, ok_plain(sp, C.w, Rm.w, Q.w, eb & 8u), topsis_q32(tp, C.w, Rm.w, A.w, Q.w), (int)u0 + 3);
+      acc_b(b, ok_plain(sp, C.x, Rm.x, Q.x, 0u), topsis_q32(tp, C.x, Rm.x, A.x, Q.x), (int)u0);
+      acc_b(b2, ok_plain(sp, C.y, Rm.y, Q.y, 0u), topsis_q32(tp, C.y, Rm.y, A.y, Q.y), (int)u0 + 1);
+      acc_b(b, ok_plain(sp, C.z, Rm.z, Q.z, 0u), topsis_q32(tp, C.z, Rm.z, A.z, Q.z), (int)u0 + 2);
+      acc_b(b2, ok_plain(sp, C.w, Rm.w, Q.w, 0u), topsis_q32(tp, C.w, Rm.w, A.w, Q.w), (int)u0 + 3);
     } else {
+      const unsigned eb = ebad4(c, sp, u0);
       int4 C, Rm, A, Q, I;
       load_chunk(c, sp, ch, spp, nxt, C, Rm, A, Q, I);
 #pragma unroll 1
@@ -608,6 +618,23 @@ __device__ void build_specials(WCtx<LT>& c) {
   if (vbx) { w->sp_u[rb] = ub; w->sp_info[rb] = 64; }
   int cnt = __popc(__ballot_sync(NACS_FULL, va)) + __popc(__ballot_sync(NACS_FULL, vbx));
   if (l == 0) w->nsp = cnt;
+  if (l < 4) w->slow[l] = 0u;
+  __syncwarp();
+  // slow chunks: those holding a special server or, with the path filter on, a server
+  // under an edge switch without a feasible fabric path (all others skip both tests)
+  for (int i = l; i < cnt; i += 32) {
+    const int u = w->sp_u[i];
+    atomicOr(&w->slow[u >> 12], 1u << ((u >> 7) & 31));
+  }
+  if (w->net) {
+    const int nEW = (c.E + 31) >> 5;
+    for (int i = l; i < nEW; i += 32) {
+      for (unsigned m = c.edgebad[i]; m; m &= m - 1) {
+        const int e = 32 * i + __ffs(m) - 1;
+        for (int ch = (e * c.h) >> 7; ch <= (e * c.h + c.h - 1) >> 7; ++ch) atomicOr(&w->slow[ch >> 5], 1u << (ch & 31));
+      }
+    }
+  }
   __syncwarp();
 }
 
@@ -770,7 +797,7 @@ __device__ void prepare_step(WCtx<LT>& c, WReq& q, StepP& sp) {
   sp.net = net;
   sp.pf = c.o.path_filter != 0;
   sp.h4 = (c.h & 3) == 0;
-  if (lane == 0) w->sumD = sumD;
+  if (lane == 0) { w->sumD = sumD; w->net = net; }
   __syncwarp();
 }
 
@@ -1149,7 +1176,7 @@ int warp_kernel_warps(const Geo& g) {
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   bool u16 = g.link_cap <= 65535;
   size_t snap = warp_snapshot_bytes(g, u16), per = warp_scratch_bytes(g);
-  if (snap + 4 * per + 64 > (size_t)optin) return 0;
+  if (snap + 4 * per + 64 > (size_t)optin || ((g.n + 127) >> 7) > 128) return 0;
   int W = (int)(((size_t)optin - snap - 64) / per);
   return W > 16 ? 16 : W;
 }
