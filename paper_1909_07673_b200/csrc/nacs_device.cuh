@@ -39,6 +39,7 @@ struct TopsisP {
   float sf[4], s2p23[4];
   float p2sq[2], m2sq[2];  // Fragmentation (f_u in {0,1}): squared weighted distances by f_u
   int mx[4], mn[4];
+  int mxb[4], mnb[4];  // 0x4B000000 + mx, 0x4B000000 - mn: the bits of 2^23 + d in one integer add
   double sd[4];
 };
 
@@ -75,6 +76,21 @@ __device__ __forceinline__ float topsis_q32(const TopsisP& t, int x0, int x1, in
   float em2 = fmaf(m3, m3, fmaf(m1, m1, fmaf(m0, m0, x2 ? t.m2sq[1] : t.m2sq[0])));
   return em2 > 0.f ? __fmul_rn(ep2, rcp_approx(em2)) : __int_as_float(0x7f800000);
 }
+// Same q for the scan: (2^23 + d) as one integer add on pre-biased bounds (d >= 0 on F; off
+// F the value is finite garbage that the feasibility mask drops), and no Ed- = 0 guard:
+// Ed+ = Ed- = 0 only when every feasible server is identical (q = NaN for all, never
+// selected; the caller's FP64 re-decision then sees q1 = q2 = inf and decides).
+__device__ __forceinline__ float topsis_q32_scan(const TopsisP& t, int x0, int x1, int x2, int x3) {
+  float p0 = fmaf(t.sf[0], __int_as_float(t.mxb[0] - x0), -t.s2p23[0]);
+  float m0 = fmaf(t.sf[0], __int_as_float(x0 + t.mnb[0]), -t.s2p23[0]);
+  float p1 = fmaf(t.sf[1], __int_as_float(t.mxb[1] - x1), -t.s2p23[1]);
+  float m1 = fmaf(t.sf[1], __int_as_float(x1 + t.mnb[1]), -t.s2p23[1]);
+  float p3 = fmaf(t.sf[3], __int_as_float(t.mxb[3] - x3), -t.s2p23[3]);
+  float m3 = fmaf(t.sf[3], __int_as_float(x3 + t.mnb[3]), -t.s2p23[3]);
+  float ep2 = fmaf(p3, p3, fmaf(p1, p1, fmaf(p0, p0, x2 ? t.p2sq[1] : t.p2sq[0])));
+  float em2 = fmaf(m3, m3, fmaf(m1, m1, fmaf(m0, m0, x2 ? t.m2sq[1] : t.m2sq[0])));
+  return __fmul_rn(ep2, rcp_approx(em2));
+}
 constexpr float kTopsisDeltaQ = 1.52587890625e-05f;  // 2^-16 relative (> 6 x 2 x 19u)
 
 __device__ __forceinline__ double topsis64(const TopsisP& t, int x0, int x1, int x2, int x3) {
@@ -101,6 +117,8 @@ __device__ __forceinline__ void topsis_params(TopsisP& t, const double w[4], con
     t.sd[c] = sd;
     t.sf[c] = (float)sd;
     t.s2p23[c] = (float)sd * 8388608.0f;
+    t.mxb[c] = 0x4B000000 + t.mx[c];
+    t.mnb[c] = 0x4B000000 - t.mn[c];
   }
   const float q2 = __fmul_rn(t.sf[2], t.sf[2]);
   t.p2sq[0] = t.mx[2] - 0 ? q2 : 0.f;

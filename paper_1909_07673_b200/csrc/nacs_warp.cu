@@ -542,10 +542,10 @@ __device__ void scan_score(const WCtx<LT>& c, const StepP& sp, const TopsisP& tp
     if (fast) {
       const unsigned ao = c.a_snap + ((unsigned)ch << 11);
       const int4 C = lds128(ao), Rm = lds128(ao + 512), A = lds128(ao + 1024), Q = lds128(ao + 1536);
-      acc_b(b, ok_plain(sp, C.x, Rm.x, Q.x, 0u), topsis_q32(tp, C.x, Rm.x, A.x, Q.x), (int)u0);
-      acc_b(b2, ok_plain(sp, C.y, Rm.y, Q.y, 0u), topsis_q32(tp, C.y, Rm.y, A.y, Q.y), (int)u0 + 1);
-      acc_b(b, ok_plain(sp, C.z, Rm.z, Q.z, 0u), topsis_q32(tp, C.z, Rm.z, A.z, Q.z), (int)u0 + 2);
-      acc_b(b2, ok_plain(sp, C.w, Rm.w, Q.w, 0u), topsis_q32(tp, C.w, Rm.w, A.w, Q.w), (int)u0 + 3);
+      acc_b(b, ok_plain(sp, C.x, Rm.x, Q.x, 0u), topsis_q32_scan(tp, C.x, Rm.x, A.x, Q.x), (int)u0);
+      acc_b(b2, ok_plain(sp, C.y, Rm.y, Q.y, 0u), topsis_q32_scan(tp, C.y, Rm.y, A.y, Q.y), (int)u0 + 1);
+      acc_b(b, ok_plain(sp, C.z, Rm.z, Q.z, 0u), topsis_q32_scan(tp, C.z, Rm.z, A.z, Q.z), (int)u0 + 2);
+      acc_b(b2, ok_plain(sp, C.w, Rm.w, Q.w, 0u), topsis_q32_scan(tp, C.w, Rm.w, A.w, Q.w), (int)u0 + 3);
     } else {
       const unsigned eb = ebad4(c, sp, u0);
       int4 C, Rm, A, Q, I;
@@ -554,7 +554,7 @@ __device__ void scan_score(const WCtx<LT>& c, const StepP& sp, const TopsisP& tp
       for (int j = 0; j < 4; ++j) {
         const int x0 = get_comp(C, j), x1 = get_comp(Rm, j), x2 = get_comp(A, j), x3 = get_comp(Q, j);
         const bool ok = ok_any(sp, x0, x1, x3, (eb >> j) & 1u, get_comp(I, j));
-        acc_b(b, ok, topsis_q32(tp, x0, x1, x2, x3), (int)u0 + j);
+        acc_b(b, ok, topsis_q32_scan(tp, x0, x1, x2, x3), (int)u0 + j);
       }
     }
   }
