@@ -55,6 +55,7 @@ struct WCtx {
   int ulog_n;
   int lane;
   int nDW;
+  int fabmin;  // smallest fabric residual of the snapshot
   unsigned a_snap, a_edge;  // 32-bit shared addresses (a_snap: + 16 * lane)
   Opt o;
 };
@@ -327,9 +328,14 @@ __device__ void wfabric(WCtx<LT>& c) {
   const int h = c.h, E = c.E;
   const int nEW = (E + 31) >> 5;
   for (int i = c.lane; i < nEW; i += 32) c.edgebad[i] = 0u;
+  // every fabric link (snapshot and overlay) >= D: no edge is cut off for that flow
+  int lmin = c.fabmin;
+  for (int i = c.lane; i < w->nol; i += 32) lmin = min(lmin, w->ol_val[i]);
+  lmin = __reduce_min_sync(NACS_FULL, lmin);
   __syncwarp();
   for (int f = 0; f < w->nflow; ++f) {
     const int v = w->fv[f], D = w->fD[f];
+    if (D <= lmin) continue;
     const int ev = (int)div_h(v, c.magic), pv = (int)div_h(ev, c.magic);
     // vm: aggregation switches a with EA[ev][a] >= D
     const bool vme = c.lane < h && fab_val(c, ev * h + c.lane) >= D;
@@ -999,7 +1005,19 @@ __global__ void __launch_bounds__(512, 1) k_batch_warp(Geo g, Opt o, const int* 
       ssnap[tile_idx(u, j)] = u < n ? state[(size_t)j * n + u] : (j < 2 ? -1 : 0);
     }
   }
-  for (int i = threadIdx.x; i < nfab; i += blockDim.x) sfab[i] = (LT)__ldg(state + 4 * n + i);
+  __shared__ int s_fabmin;
+  if (threadIdx.x == 0) s_fabmin = INT_MAX;
+  __syncthreads();
+  {
+    int m = INT_MAX;
+    for (int i = threadIdx.x; i < nfab; i += blockDim.x) {
+      const int v = __ldg(state + 4 * n + i);
+      sfab[i] = (LT)v;
+      m = min(m, v);
+    }
+    m = __reduce_min_sync(NACS_FULL, m);
+    if ((threadIdx.x & 31) == 0) atomicMin(&s_fabmin, m);
+  }
   __syncthreads();
   if (bulk) {
     const unsigned mb = smem_addr(&mbar);
@@ -1027,6 +1045,7 @@ __global__ void __launch_bounds__(512, 1) k_batch_warp(Geo g, Opt o, const int* 
   c.pm = c.edgebad + nEW;
   c.a_edge = smem_addr(c.edgebad);
   c.nDW = nDW;
+  c.fabmin = s_fabmin;
   c.ulog = ulog_all + ((size_t)blockIdx.x * (blockDim.x >> 5) + warp) * WLOG;
   c.ulog_n = 0;
   c.lane = lane;
