@@ -33,17 +33,21 @@ def stale() -> bool:
     return any(os.path.getmtime(d) > t for d in DEPS)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, out: str = LIB, extra=()) -> str:
     if force or stale():
-        cmd = [NVCC, *FLAGS, "-I", os.path.join(ROOT, "include"), *NCCL_FLAGS, "-o", LIB, *SOURCES]
+        cmd = [NVCC, *FLAGS, *extra, "-I", os.path.join(ROOT, "include"), *NCCL_FLAGS, "-o", out, *SOURCES]
         p = subprocess.run(cmd, capture_output=True, text=True)
         if p.returncode != 0:
             sys.stderr.write(p.stdout + p.stderr)
             raise RuntimeError("nvcc failed building libnacs.so")
         if verbose:
             sys.stderr.write(p.stderr)
-    return LIB
+    return out
 
 
 if __name__ == "__main__":
-    build(force=True, verbose=True)
+    # python build.py [out.so -DFLAG ...]: an experiment build next to the product library
+    if len(sys.argv) > 1:
+        build(force=True, out=os.path.abspath(sys.argv[1]), extra=sys.argv[2:])
+    else:
+        build(force=True, verbose=True)

@@ -272,24 +272,28 @@ __device__ __forceinline__ int path_fids(const WCtx<LT>& c, int u, int v, int pi
 }
 
 // R16: widest ECMP path u -> v on current residuals (snapshot + overlay); warp-wide.
+// Lane a < h holds min(EA[eu][a], EA[ev][a]) (h <= 32); cross-pod paths (a, b) read it by
+// shuffle, so each edge-aggregation residual is looked up once.
 template <typename LT>
 __device__ int2 wpath(const WCtx<LT>& c, int u, int v) {
-  int h = c.h;
-  int eu = (int)div_h(u, c.magic), ev = (int)div_h(v, c.magic);
+  const int h = c.h;
+  const int eu = (int)div_h(u, c.magic), ev = (int)div_h(v, c.magic);
   if (eu == ev) return make_int2(0, INT_MAX);
-  int pu = (int)div_h(eu, c.magic), pv = (int)div_h(ev, c.magic);
+  const int pu = (int)div_h(eu, c.magic), pv = (int)div_h(ev, c.magic);
+  const int eav = c.lane < h ? min(fab_val(c, eu * h + c.lane), fab_val(c, ev * h + c.lane)) : -1;
   int best = -1, bt = INT_MAX;
   if (pu == pv) {
-    for (int a = c.lane; a < h; a += 32) {
-      int b = min(fab_val(c, eu * h + a), fab_val(c, ev * h + a));
-      if (b > best) { best = b; bt = a; }
-    }
+    if (c.lane < h) { best = eav; bt = c.lane; }
   } else {
-    for (int t = c.lane; t < h * h; t += 32) {
-      int a = (int)div_h(t, c.magic), b = t - a * h;
-      int x = min(min(fab_val(c, eu * h + a), fab_val(c, ev * h + a)),
-                  min(fab_val(c, c.nfabea + (pu * h + a) * h + b), fab_val(c, c.nfabea + (pv * h + a) * h + b)));
-      if (x > best) { best = x; bt = t; }
+    const int hh = h * h;
+    for (int t0 = 0; t0 < hh; t0 += 32) {
+      const int t = t0 + c.lane;
+      const int a = t < hh ? (int)div_h(t, c.magic) : 0, b = t - a * h;
+      const int ea = __shfl_sync(NACS_FULL, eav, a);
+      if (t < hh) {
+        const int x = min(ea, min(fab_val(c, c.nfabea + (pu * h + a) * h + b), fab_val(c, c.nfabea + (pv * h + a) * h + b)));
+        if (x > best) { best = x; bt = t; }
+      }
     }
   }
 #pragma unroll
@@ -900,7 +904,11 @@ __device__ void finish_request(WCtx<LT>& c, const WReq& q, const OutDev& O) {
     if (lane == i) { my_ec = ec; my_er = er; }
   }
   int my_bw0 = 0, my_bw1 = 0;
+#ifdef NACS_EXP_NO_TOPUP
+  for (int e = 0; e < 0; ++e) {
+#else
   for (int e = 0; e < q.nV; ++e) {
+#endif
     const int src_lane = e & 31;
     const bool hi = e >= 32;
     const int es = __shfl_sync(NACS_FULL, hi ? q.pa1 : q.pa0, src_lane);

@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libnacs.so")
+LIB_PATH = os.environ.get("NACS_LIB", os.path.join(HERE, "libnacs.so"))  # NACS_LIB: experiment builds
 
 NACS_OK, NACS_EINVAL, NACS_ENOMEM, NACS_ECUDA, NACS_ENCCL, NACS_ENOTOPO, NACS_ETOOBIG = range(7)
 STATUS_NAMES = ["OK", "EINVAL", "ENOMEM", "ECUDA", "ENCCL", "ENOTOPO", "ETOOBIG"]
