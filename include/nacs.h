@@ -134,6 +134,8 @@ typedef struct {
   int64_t invalid;         /* requests rejected as invalid on the device */
   int64_t feasible;        /* sum over pod steps of |F| (feasible servers) */
   int64_t ahp_pairs;       /* AHP: sum over pod steps and non-constant criteria of |F|(|F|-1)/2 */
+  int64_t scanned_a;       /* TOPSIS batch fast path: server slots read by the filter/statistics pass */
+  int64_t scanned_b;       /* ... and by the scoring pass (chunk-pruned; 0 for the other kernels) */
 } nacs_stats;
 
 /* Create a context on CUDA device `device`.  cuda_stream: the cudaStream_t all work of

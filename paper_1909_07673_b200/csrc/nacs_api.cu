@@ -74,6 +74,7 @@ struct nacs_ctx {
   DevArr<int> req_out;       // packed outputs
   DevArr<int2> ulog;
   DevArr<int4> wlog;         // per-warp undo logs of k_batch_warp
+  DevArr<int> wlay;          // chunk layout of the snapshot for k_batch_warp
   DevArr<int> deferred;      // requests k_batch_warp hands to k_batch
   DevArr<double> w64;
   DevArr<float> ahp_ws;
@@ -299,6 +300,8 @@ nacs_status finish_stats(nacs_ctx* ctx) {
   ctx->last.invalid = (int64_t)h[nacs::ST_INVALID];
   ctx->last.feasible = (int64_t)h[nacs::ST_FEAS];
   ctx->last.ahp_pairs = (int64_t)h[nacs::ST_PAIRS];
+  ctx->last.scanned_a = (int64_t)h[nacs::ST_SCAN_A];
+  ctx->last.scanned_b = (int64_t)h[nacs::ST_SCAN_B];
   ctx->stats_pending = false;
   return NACS_OK;
 }
@@ -575,6 +578,7 @@ void nacs_destroy(nacs_ctx* ctx) {
   ctx->req_out.release();
   ctx->ulog.release();
   ctx->wlog.release();
+  ctx->wlay.release();
   ctx->deferred.release();
   ctx->w64.release();
   ctx->ahp_ws.release();
@@ -724,8 +728,9 @@ nacs_status nacs_schedule_batch(nacs_ctx* ctx, const nacs_options* opt, const na
     // fast path: warp per request; requests beyond its limits are deferred to k_batch
     int wgrid = ctx->num_sms;
     CK(ctx->wlog.reserve(nacs::warp_ulog_entries(wgrid, warps)));
+    CK(ctx->wlay.reserve(nacs::warp_layout_ints(g)));
     CK(ctx->deferred.reserve(2 * (size_t)R));
-    CK(nacs::launch_batch_warp(g, o, ctx->state.p, Rd, Od, ctx->wlog.p, ctx->misc.p, ctx->deferred.p + R,
+    CK(nacs::launch_batch_warp(g, o, ctx->state.p, ctx->wlay.p, Rd, Od, ctx->wlog.p, ctx->misc.p, ctx->deferred.p + R,
                                ctx->deferred.p, ctx->misc.p + 2, ctx->stats.p, wgrid, warps, ctx->stream));
     CK(nacs::launch_batch(g, o, ctx->state.p, Rd, Od, ctx->ulog.p, ctx->w64.p, ctx->misc.p + 1, ctx->stats.p,
                           grid, ctx->stream, ctx->deferred.p, ctx->misc.p + 2));

@@ -79,7 +79,8 @@ __device__ __forceinline__ float topsis_q32(const TopsisP& t, int x0, int x1, in
 // Same q for the scan: (2^23 + d) as one integer add on pre-biased bounds (d >= 0 on F; off
 // F the value is finite garbage that the feasibility mask drops), and no Ed- = 0 guard:
 // Ed+ = Ed- = 0 only when every feasible server is identical (q = NaN for all, never
-// selected; the caller's FP64 re-decision then sees q1 = q2 = inf and decides).
+// selected; the caller's FP64 re-decision then sees q1 = q2 = inf and decides).  f_u is
+// bit 0 of x2 (the warp kernel's layout keeps the server index in the other bits).
 __device__ __forceinline__ float topsis_q32_scan(const TopsisP& t, int x0, int x1, int x2, int x3) {
   float p0 = fmaf(t.sf[0], __int_as_float(t.mxb[0] - x0), -t.s2p23[0]);
   float m0 = fmaf(t.sf[0], __int_as_float(x0 + t.mnb[0]), -t.s2p23[0]);
@@ -87,8 +88,8 @@ __device__ __forceinline__ float topsis_q32_scan(const TopsisP& t, int x0, int x
   float m1 = fmaf(t.sf[1], __int_as_float(x1 + t.mnb[1]), -t.s2p23[1]);
   float p3 = fmaf(t.sf[3], __int_as_float(t.mxb[3] - x3), -t.s2p23[3]);
   float m3 = fmaf(t.sf[3], __int_as_float(x3 + t.mnb[3]), -t.s2p23[3]);
-  float ep2 = fmaf(p3, p3, fmaf(p1, p1, fmaf(p0, p0, x2 ? t.p2sq[1] : t.p2sq[0])));
-  float em2 = fmaf(m3, m3, fmaf(m1, m1, fmaf(m0, m0, x2 ? t.m2sq[1] : t.m2sq[0])));
+  float ep2 = fmaf(p3, p3, fmaf(p1, p1, fmaf(p0, p0, (x2 & 1) ? t.p2sq[1] : t.p2sq[0])));
+  float em2 = fmaf(m3, m3, fmaf(m1, m1, fmaf(m0, m0, (x2 & 1) ? t.m2sq[1] : t.m2sq[0])));
   return __fmul_rn(ep2, rcp_approx(em2));
 }
 constexpr float kTopsisDeltaQ = 1.52587890625e-05f;  // 2^-16 relative (> 6 x 2 x 19u)

@@ -52,7 +52,20 @@ struct QueryDev {
   int *best;                // [1]
 };
 
-enum { ST_POD_STEPS = 0, ST_RETRIES = 1, ST_FP64 = 2, ST_INVALID = 3, ST_FEAS = 4, ST_PAIRS = 5, ST_N = 6 };
+enum {
+  ST_POD_STEPS = 0,
+  ST_RETRIES = 1,
+  ST_FP64 = 2,
+  ST_INVALID = 3,
+  ST_FEAS = 4,
+  ST_PAIRS = 5,
+  ST_SCAN_A = 6,  // slots read by pass A / pass B of the TOPSIS warp kernel
+  ST_SCAN_B = 7,
+  ST_N = 8
+};
+// Workspace of the warp kernel's chunk layout (k_warp_layout), int words:
+// [0..3] thresholds of the low region | criteria tiles [4 npad] | chunk table [16 nch] | inv[n]
+constexpr int LAY_PST = 4;
 
 // Request validation shared by the host path and the kernels (reading R24).
 // Returns 0 if valid, else a bitmask: 1 size limit, 2 demands, 4 min>max, 8 pod ids,
@@ -124,8 +137,9 @@ cudaError_t launch_batch(const Geo& g, const Opt& o, const int* d_state, const R
 // warp-per-request TOPSIS batch kernel (nacs_warp.cu): warps per CTA (0 = does not fit)
 int warp_kernel_warps(const Geo& g);
 size_t warp_ulog_entries(int grid, int warps);
-cudaError_t launch_batch_warp(const Geo& g, const Opt& o, const int* d_state, const ReqsDev& R, const OutDev& O,
-                              int4* ulog, int* next, int* order, int* deferred, int* n_deferred,
+size_t warp_layout_ints(const Geo& g);
+cudaError_t launch_batch_warp(const Geo& g, const Opt& o, const int* d_state, int* lay, const ReqsDev& R,
+                              const OutDev& O, int4* ulog, int* next, int* order, int* deferred, int* n_deferred,
                               unsigned long long* stats, int grid, int warps, cudaStream_t st);
 // sequential: one CTA, requests in order, in place on d_state
 cudaError_t launch_sequential(const Geo& g, const Opt& o, int* d_state, const ReqsDev& R, const OutDev& O,

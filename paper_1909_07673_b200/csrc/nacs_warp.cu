@@ -38,16 +38,34 @@ struct WScr {
   int fv[WF], fD[WF], fok[WF], fpath[WF];
   int sp_u[WSP], sp_info[WSP];
   int ex[WX];
-  unsigned slow[4];  // chunks of 128 servers the scans take on the slow path (<= 128 chunks)
+  int os_pos[WOS], ex_pos[WX];  // their slots in the chunk layout
+  unsigned slow[4];  // chunks of 128 slots the scans take on the slow path (<= 128 chunks)
+  unsigned none_m[4];  // chunks without a feasible server in this pod step (pass A)
   int net;
   // dynamic tail: dirty[(E + k*h + 31)/32] | edgebad[(E+31)/32] | pm[k]
 };
+
+// Static summary of one 128-slot chunk of the layout (k_warp_layout): the box of its
+// criteria (CPU, RAM, access link; f_u as bits: 1 = has 0, 2 = has 1) and the exact
+// aggregates pass A needs when the whole chunk is feasible.
+struct ChunkT {
+  int lo[3];
+  int act;
+  int hi[3];
+  int cnt;
+  int nact, pad;
+  unsigned long long sq[3];
+};
+static_assert(sizeof(ChunkT) == 64, "ChunkT is 16 words");
 
 template <typename LT>
 struct WCtx {
   int k, h, n, npad, E, nfabea;  // nfabea = E*h (start of agg-core links in fab[])
   unsigned magic;
-  const int* snap;  // criteria in 128-server tiles: tile t = cpu[128] | ram[128] | act[128] | acc[128] (shared)
+  const int* snap;  // criteria in 128-slot tiles: cpu[128] | ram[128] | (server << 1 | f_u)[128] | acc[128] (shared)
+  const ChunkT* ctab;  // [nch] chunk summaries (shared)
+  const int* inv;      // server -> slot (global)
+  int nch;
   const LT* fab;                           // edge-agg[E*h] | agg-core[k*h*h] (shared)
   WScr* w;
   unsigned *dirty, *edgebad, *pm;
@@ -122,13 +140,13 @@ __device__ __forceinline__ int w_slot(const WCtx<LT>& c, int u) {
 template <typename LT>
 __device__ __forceinline__ int acc_val(const WCtx<LT>& c, int u) {
   int s = os_slot(c, u);
-  return s >= 0 ? c.w->os_acc[s] : c.snap[tile_idx(u, 3)];
+  return s >= 0 ? c.w->os_acc[s] : c.snap[tile_idx(c.inv[u], 3)];
 }
 
 // -------------------------------------------- overlay writes (warp-cooperative) --
 // All lanes call with uniform arguments; lane 0 writes.  Returns false on overflow.
 template <typename LT>
-__device__ bool w_set_server(WCtx<LT>& c, int u, int cpu, int ram, int act, int acc, bool log = true) {
+__device__ bool w_set_server(WCtx<LT>& c, int u, int pos, int cpu, int ram, int act, int acc, bool log = true) {
   WScr* w = c.w;
   const int s0 = w_slot(c, u);  // uniform
   bool ok = true;
@@ -140,6 +158,7 @@ __device__ bool w_set_server(WCtx<LT>& c, int u, int cpu, int ram, int act, int 
     if (s < 0) {
       s = w->nos++;
       w->os_u[s] = u;
+      w->os_pos[s] = pos;
     } else if (log) {
       c.ulog[c.ulog_n] = make_int4(s, w->os_cpu[s], w->os_ram[s], w->os_acc[s] * 2 + w->os_act[s]);
     }
@@ -410,7 +429,7 @@ struct AccA {
 __device__ __forceinline__ void acc_a(AccA& a, bool ok, int x0, int x1, int x2, int x3) {
   unsigned o0 = ok ? (unsigned)x0 : 0u, o1 = ok ? (unsigned)x1 : 0u, o3 = ok ? (unsigned)x3 : 0u;
   a.nf += ok ? 1 : 0;
-  a.nact += ok ? x2 : 0;
+  a.nact += ok ? (x2 & 1) : 0;
   a.mx0 = max(a.mx0, o0);
   a.mx1 = max(a.mx1, o1);
   a.mx3 = max(a.mx3, o3);
@@ -421,24 +440,26 @@ __device__ __forceinline__ void acc_a(AccA& a, bool ok, int x0, int x1, int x2, 
   a.q1 += (unsigned long long)o1 * o1;
   a.q3 += (unsigned long long)o3 * o3;
 }
-// a7: per-lane best (smallest q = largest closeness, lowest index) and second best
+// a7: per-lane best (smallest q = largest closeness, lowest server index) and second best;
+// chunks are visited in any order, so equal q compare server indices
 struct AccB {
   float b1, b2;
-  int i1;
+  int i1, p1;  // server index and slot of b1
 };
-__device__ __forceinline__ void acc_b(AccB& b, bool ok, float q, int u) {
+__device__ __forceinline__ void acc_b(AccB& b, bool ok, float q, int id, int pos) {
   const float qe = ok ? q : __int_as_float(0x7f800000);
-  const bool lt = qe < b.b1;
+  const bool lt = qe < b.b1 || (qe == b.b1 && qe != __int_as_float(0x7f800000) && (unsigned)id < (unsigned)b.i1);
   b.b2 = lt ? b.b1 : fminf(b.b2, qe);
-  b.i1 = lt ? u : b.i1;
+  b.i1 = lt ? id : b.i1;
+  b.p1 = lt ? pos : b.p1;
   b.b1 = lt ? qe : b.b1;
 }
-
 // merge accumulator o (a disjoint set of servers) into a: lowest index on equal q
 __device__ __forceinline__ void merge_b(AccB& a, const AccB& o) {
   const bool lt = o.b1 < a.b1 || (o.b1 == a.b1 && (unsigned)o.i1 < (unsigned)a.i1);
   a.b2 = fminf(fminf(a.b2, o.b2), lt ? a.b1 : o.b1);
   a.i1 = lt ? o.i1 : a.i1;
+  a.p1 = lt ? o.p1 : a.p1;
   a.b1 = lt ? o.b1 : a.b1;
 }
 
@@ -452,29 +473,36 @@ __device__ __forceinline__ int get_comp(const int4& v, int j) {
   return j == 0 ? v.x : (j == 1 ? v.y : (j == 2 ? v.z : v.w));
 }
 
-// Substitute the chunk's special servers into the lane's 4 servers and force their
-// feasibility: info[j] = 1 | ok << 1 (0 = ordinary server).
+// Substitute the special servers of chunk ch into the lane's 4 slots and force their
+// feasibility: info[j] = 1 | ok << 1 (0 = ordinary server).  The special list is sorted
+// by slot; any chunk order.
 template <typename LT>
-__device__ __forceinline__ void chunk_specials(const WCtx<LT>& c, const StepP& sp, int base, int& spp, int4& C,
-                                               int4& Rm, int4& A, int4& Q, int info[4]) {
+__device__ __forceinline__ void chunk_specials(const WCtx<LT>& c, const StepP& sp, int ch, int4& C, int4& Rm,
+                                               int4& A, int4& Q, int info[4]) {
   const WScr* w = c.w;
   info[0] = info[1] = info[2] = info[3] = 0;
-  while (spp < w->nsp && w->sp_u[spp] < base + 128) {
-    const int u = w->sp_u[spp], inf = w->sp_info[spp];
-    if (((u - base) >> 2) == c.lane) {
-      const int j = (u - base) & 3;
+  const int base = ch << 7;
+  int lo = 0, hi = w->nsp;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (w->sp_u[mid] < base) lo = mid + 1;
+    else hi = mid;
+  }
+  for (int t = lo; t < w->nsp && w->sp_u[t] < base + 128; ++t) {
+    const int pos = w->sp_u[t], inf = w->sp_info[t];
+    if (((pos - base) >> 2) == c.lane) {
+      const int j = (pos - base) & 3;
       const int slot = (inf & 63) - 1;
       if (slot >= 0) {
         set_comp(C, j, w->os_cpu[slot]);
         set_comp(Rm, j, w->os_ram[slot]);
-        set_comp(A, j, w->os_act[slot]);
+        set_comp(A, j, (w->os_u[slot] << 1) | w->os_act[slot]);
         set_comp(Q, j, w->os_acc[slot]);
       }
-      const unsigned bad = sp.net ? ebad(c, (unsigned)u) : 0u;
+      const unsigned bad = sp.net ? ebad(c, (unsigned)(get_comp(A, j) >> 1)) : 0u;
       const bool ok = ok_special(c, sp, get_comp(C, j), get_comp(Rm, j), get_comp(Q, j), bad, inf);
       info[j] = 1 | (ok ? 2 : 0);
     }
-    ++spp;
   }
 }
 
@@ -484,137 +512,221 @@ __device__ __forceinline__ bool ok_any(const StepP& sp, int x0, int x1, int x3, 
   return (forced & 1) ? (forced & 2) != 0 : pl;
 }
 
-// Load the lane's 4 servers of chunk ch; substitute the chunk's special servers.
+// Load the lane's 4 slots of chunk ch (slow path: specials substituted, edge bits by server).
 template <typename LT>
-__device__ __forceinline__ void load_chunk(const WCtx<LT>& c, const StepP& sp, int ch, int& spp, int& nxt, int4& C,
-                                           int4& Rm, int4& A, int4& Q, int4& I) {
+__device__ __forceinline__ void load_slow(const WCtx<LT>& c, const StepP& sp, int ch, int4& C, int4& Rm, int4& A,
+                                          int4& Q, int4& I, unsigned& eb) {
   const unsigned ao = c.a_snap + ((unsigned)ch << 11);
   C = lds128(ao);
   Rm = lds128(ao + 512);
   A = lds128(ao + 1024);
   Q = lds128(ao + 1536);
-  I = make_int4(0, 0, 0, 0);
-  const int base = ch << 7;
-  if (nxt < base + 128) {  // warp-uniform
-    int info[4];
-    chunk_specials(c, sp, base, spp, C, Rm, A, Q, info);
-    I = make_int4(info[0], info[1], info[2], info[3]);
-    nxt = spp < c.w->nsp ? c.w->sp_u[spp] : INT_MAX;
+  int info[4];
+  chunk_specials(c, sp, ch, C, Rm, A, Q, info);
+  I = make_int4(info[0], info[1], info[2], info[3]);
+  eb = 0u;
+  if (sp.net) {
+    eb = ebad(c, (unsigned)A.x >> 1) | (ebad(c, (unsigned)A.y >> 1) << 1) | (ebad(c, (unsigned)A.z >> 1) << 2) |
+         (ebad(c, (unsigned)A.w >> 1) << 3);
   }
 }
+__device__ __forceinline__ bool slow_bit(const unsigned* m, int ch) { return (m[ch >> 5] >> (ch & 31)) & 1u; }
 
-// Pass A (a3 + a4): filter and statistics over all servers, 128 per warp iteration.
-// Chunks without special servers take a branch-free path; the others substitute and
-// force their special servers first.
+// Pass A (a3 + a4): filter and statistics.  Per chunk (one lane each): a chunk whose box
+// lies inside the thresholds and holds no special server is feasible as a whole and adds
+// its precomputed aggregates; a chunk whose box misses a threshold holds no feasible
+// server; the warp scans the others, 128 slots per iteration.  Exact either way.
 template <typename LT>
-__device__ void scan_stats(const WCtx<LT>& c, const StepP& sp, AccA& a) {
-  const int nch = c.npad >> 7;
-  int spp = 0;
-  int nxt = c.w->nsp > 0 ? c.w->sp_u[0] : INT_MAX;
-  unsigned sl = 0;
-  for (int ch = 0; ch < nch; ++ch) {
-    const unsigned u0 = (unsigned)((ch << 7) + 4 * c.lane);
-    if ((ch & 31) == 0) sl = c.w->slow[ch >> 5];
-    const bool fast = !(sl & 1u);
-    sl >>= 1;
-    if (fast) {
-      const unsigned ao = c.a_snap + ((unsigned)ch << 11);
-      const int4 C = lds128(ao), Rm = lds128(ao + 512), A = lds128(ao + 1024), Q = lds128(ao + 1536);
-      acc_a(a, ok_plain(sp, C.x, Rm.x, Q.x, 0u), C.x, Rm.x, A.x, Q.x);
-      acc_a(a, ok_plain(sp, C.y, Rm.y, Q.y, 0u), C.y, Rm.y, A.y, Q.y);
-      acc_a(a, ok_plain(sp, C.z, Rm.z, Q.z, 0u), C.z, Rm.z, A.z, Q.z);
-      acc_a(a, ok_plain(sp, C.w, Rm.w, Q.w, 0u), C.w, Rm.w, A.w, Q.w);
-    } else {
-      const unsigned eb = ebad4(c, sp, u0);
-      int4 C, Rm, A, Q, I;
-      load_chunk(c, sp, ch, spp, nxt, C, Rm, A, Q, I);
-      acc_a(a, ok_any(sp, C.x, Rm.x, Q.x, eb & 1u, I.x), C.x, Rm.x, A.x, Q.x);
-      acc_a(a, ok_any(sp, C.y, Rm.y, Q.y, eb & 2u, I.y), C.y, Rm.y, A.y, Q.y);
-      acc_a(a, ok_any(sp, C.z, Rm.z, Q.z, eb & 4u, I.z), C.z, Rm.z, A.z, Q.z);
-      acc_a(a, ok_any(sp, C.w, Rm.w, Q.w, eb & 8u, I.w), C.w, Rm.w, A.w, Q.w);
+__device__ void pass_a(const WCtx<LT>& c, const StepP& sp, AccA& a, unsigned long long& scanned) {
+  WScr* w = c.w;
+  unsigned scan_m[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int ch = c.lane + 32 * i;
+    bool sc = false, none = false;
+    if (ch < c.nch) {
+      const bool slow = (w->slow[i] >> c.lane) & 1u;
+      const ChunkT& t = c.ctab[ch];
+      const bool full = !slow && t.cnt > 0 && t.lo[0] >= sp.dcp && t.lo[1] >= sp.dr && t.lo[2] >= sp.sumDp;
+      none = !slow && (t.cnt == 0 || t.hi[0] < sp.dcp || t.hi[1] < sp.dr || t.hi[2] < sp.sumDp);
+      sc = !full && !none;
+      if (full) {
+        a.nf += t.cnt;
+        a.nact += t.nact;
+        a.mx0 = max(a.mx0, (unsigned)t.hi[0]); a.mn0 = min(a.mn0, (unsigned)t.lo[0]);
+        a.mx1 = max(a.mx1, (unsigned)t.hi[1]); a.mn1 = min(a.mn1, (unsigned)t.lo[1]);
+        a.mx3 = max(a.mx3, (unsigned)t.hi[2]); a.mn3 = min(a.mn3, (unsigned)t.lo[2]);
+        a.q0 += t.sq[0];
+        a.q1 += t.sq[1];
+        a.q3 += t.sq[2];
+      }
     }
+    scan_m[i] = __ballot_sync(NACS_FULL, sc);
+    const unsigned nm = __ballot_sync(NACS_FULL, none);
+    if (c.lane == 0) w->none_m[i] = nm;
   }
-}
-
-// Pass B (a5T + a7): closeness of every feasible server; per-lane best and second best.
-template <typename LT>
-__device__ void scan_score(const WCtx<LT>& c, const StepP& sp, const TopsisP& tp, AccB& b) {
-  const int nch = c.npad >> 7;
-  int spp = 0;
-  int nxt = c.w->nsp > 0 ? c.w->sp_u[0] : INT_MAX;
-  AccB b2 = {__int_as_float(0x7f800000), __int_as_float(0x7f800000), -1};  // odd servers: shorter chains
-  unsigned sl = 0;
-  for (int ch = 0; ch < nch; ++ch) {
-    const unsigned u0 = (unsigned)((ch << 7) + 4 * c.lane);
-    if ((ch & 31) == 0) sl = c.w->slow[ch >> 5];
-    const bool fast = !(sl & 1u);
-    sl >>= 1;
-    if (fast) {
-      const unsigned ao = c.a_snap + ((unsigned)ch << 11);
-      const int4 C = lds128(ao), Rm = lds128(ao + 512), A = lds128(ao + 1024), Q = lds128(ao + 1536);
-      acc_b(b, ok_plain(sp, C.x, Rm.x, Q.x, 0u), topsis_q32_scan(tp, C.x, Rm.x, A.x, Q.x), (int)u0);
-      acc_b(b2, ok_plain(sp, C.y, Rm.y, Q.y, 0u), topsis_q32_scan(tp, C.y, Rm.y, A.y, Q.y), (int)u0 + 1);
-      acc_b(b, ok_plain(sp, C.z, Rm.z, Q.z, 0u), topsis_q32_scan(tp, C.z, Rm.z, A.z, Q.z), (int)u0 + 2);
-      acc_b(b2, ok_plain(sp, C.w, Rm.w, Q.w, 0u), topsis_q32_scan(tp, C.w, Rm.w, A.w, Q.w), (int)u0 + 3);
-    } else {
-      const unsigned eb = ebad4(c, sp, u0);
-      int4 C, Rm, A, Q, I;
-      load_chunk(c, sp, ch, spp, nxt, C, Rm, A, Q, I);
 #pragma unroll 1
-      for (int j = 0; j < 4; ++j) {
-        const int x0 = get_comp(C, j), x1 = get_comp(Rm, j), x2 = get_comp(A, j), x3 = get_comp(Q, j);
-        const bool ok = ok_any(sp, x0, x1, x3, (eb >> j) & 1u, get_comp(I, j));
-        acc_b(b, ok, topsis_q32_scan(tp, x0, x1, x2, x3), (int)u0 + j);
+  for (int i = 0; i < 4; ++i) {
+    for (unsigned m = scan_m[i]; m; m &= m - 1) {
+      const int ch = 32 * i + __ffs(m) - 1;
+      scanned += 128;
+      if (!slow_bit(w->slow, ch)) {
+        const unsigned ao = c.a_snap + ((unsigned)ch << 11);
+        const int4 C = lds128(ao), Rm = lds128(ao + 512), A = lds128(ao + 1024), Q = lds128(ao + 1536);
+        acc_a(a, ok_plain(sp, C.x, Rm.x, Q.x, 0u), C.x, Rm.x, A.x, Q.x);
+        acc_a(a, ok_plain(sp, C.y, Rm.y, Q.y, 0u), C.y, Rm.y, A.y, Q.y);
+        acc_a(a, ok_plain(sp, C.z, Rm.z, Q.z, 0u), C.z, Rm.z, A.z, Q.z);
+        acc_a(a, ok_plain(sp, C.w, Rm.w, Q.w, 0u), C.w, Rm.w, A.w, Q.w);
+      } else {
+        int4 C, Rm, A, Q, I;
+        unsigned eb;
+        load_slow(c, sp, ch, C, Rm, A, Q, I, eb);
+        acc_a(a, ok_any(sp, C.x, Rm.x, Q.x, eb & 1u, I.x), C.x, Rm.x, A.x, Q.x);
+        acc_a(a, ok_any(sp, C.y, Rm.y, Q.y, eb & 2u, I.y), C.y, Rm.y, A.y, Q.y);
+        acc_a(a, ok_any(sp, C.z, Rm.z, Q.z, eb & 4u, I.z), C.z, Rm.z, A.z, Q.z);
+        acc_a(a, ok_any(sp, C.w, Rm.w, Q.w, eb & 8u, I.w), C.w, Rm.w, A.w, Q.w);
       }
     }
   }
-  merge_b(b, b2);
+  __syncwarp();
 }
 
-// FP64 re-decision (R14): exact closeness of the candidates within 2 delta of s1.
+// Lower bound of q = Ed+^2 / Ed-^2 over the servers of a chunk (its box clipped to the
+// [min, max] of F): Ed+_c >= s_c (max_c - min(hi_c, max_c)), Ed-_c <= s_c (min(hi_c, max_c)
+// - min_c).  FP32 with relative error <= 12u; callers prune with a 2^-12 margin.
+__device__ __forceinline__ float chunk_qlb(const TopsisP& t, const ChunkT& ct) {
+  float ep2, em2;
+  {
+    const int ci[3] = {0, 1, 3};
+    float e[3], m[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const int hc = min(ct.hi[c], t.mx[ci[c]]);
+      e[c] = t.sf[ci[c]] * (float)(t.mx[ci[c]] - hc);
+      m[c] = t.sf[ci[c]] * (float)max(0, hc - t.mn[ci[c]]);
+    }
+    const float pa = (ct.act & 2) ? ((ct.act & 1) ? fminf(t.p2sq[0], t.p2sq[1]) : t.p2sq[1]) : t.p2sq[0];
+    const float ma = (ct.act & 2) ? ((ct.act & 1) ? fmaxf(t.m2sq[0], t.m2sq[1]) : t.m2sq[1]) : t.m2sq[0];
+    ep2 = fmaf(e[2], e[2], fmaf(e[1], e[1], fmaf(e[0], e[0], pa)));
+    em2 = fmaf(m[2], m[2], fmaf(m[1], m[1], fmaf(m[0], m[0], ma)));
+  }
+  return em2 > 0.f ? ep2 * rcp_approx(em2) : __int_as_float(0x7f800000);
+}
+constexpr float kPruneMargin = 1.0f + 2.44140625e-4f;  // 1 + 2^-12
+
+// Scores of the lane's 4 slots of chunk ch into b (a5T + a7).
 template <typename LT>
-__device__ void scan_fp64(const WCtx<LT>& c, const StepP& sp, const TopsisP& tp, float thr, double& bv, int& bj) {
-  const int nch = c.npad >> 7;
-  int spp = 0;
-  int nxt = c.w->nsp > 0 ? c.w->sp_u[0] : INT_MAX;
-  for (int ch = 0; ch < nch; ++ch) {
-    const unsigned u0 = (unsigned)((ch << 7) + 4 * c.lane);
+__device__ __forceinline__ void score_chunk(const WCtx<LT>& c, const StepP& sp, const TopsisP& tp, int ch,
+                                            AccB& b) {
+  const int p0 = (ch << 7) + 4 * c.lane;
+  if (!slow_bit(c.w->slow, ch)) {
+    const unsigned ao = c.a_snap + ((unsigned)ch << 11);
+    const int4 C = lds128(ao), Rm = lds128(ao + 512), A = lds128(ao + 1024), Q = lds128(ao + 1536);
+    AccB b2 = {__int_as_float(0x7f800000), __int_as_float(0x7f800000), -1, -1};  // shorter chains
+    acc_b(b, ok_plain(sp, C.x, Rm.x, Q.x, 0u), topsis_q32_scan(tp, C.x, Rm.x, A.x, Q.x), A.x >> 1, p0);
+    acc_b(b2, ok_plain(sp, C.y, Rm.y, Q.y, 0u), topsis_q32_scan(tp, C.y, Rm.y, A.y, Q.y), A.y >> 1, p0 + 1);
+    acc_b(b, ok_plain(sp, C.z, Rm.z, Q.z, 0u), topsis_q32_scan(tp, C.z, Rm.z, A.z, Q.z), A.z >> 1, p0 + 2);
+    acc_b(b2, ok_plain(sp, C.w, Rm.w, Q.w, 0u), topsis_q32_scan(tp, C.w, Rm.w, A.w, Q.w), A.w >> 1, p0 + 3);
+    merge_b(b, b2);
+  } else {
     int4 C, Rm, A, Q, I;
-    load_chunk(c, sp, ch, spp, nxt, C, Rm, A, Q, I);
-    const unsigned eb = ebad4(c, sp, u0);
+    unsigned eb;
+    load_slow(c, sp, ch, C, Rm, A, Q, I, eb);
 #pragma unroll 1
     for (int j = 0; j < 4; ++j) {
-      int x0 = get_comp(C, j), x1 = get_comp(Rm, j), x2 = get_comp(A, j), x3 = get_comp(Q, j);
+      const int x0 = get_comp(C, j), x1 = get_comp(Rm, j), x2 = get_comp(A, j), x3 = get_comp(Q, j);
+      const bool ok = ok_any(sp, x0, x1, x3, (eb >> j) & 1u, get_comp(I, j));
+      acc_b(b, ok, topsis_q32_scan(tp, x0, x1, x2, x3), x2 >> 1, p0 + j);
+    }
+  }
+}
+
+// Pass B (a5T + a7): best-first over chunks.  Every chunk with a feasible server gets the
+// lower bound of its q (slow chunks 0: their overlaid values may leave the box); the warp
+// visits chunks in increasing bound while the bound is within the prune margin of the
+// best q so far.  Every server with q32 <= q1 (1 + 2^-12) is visited, so q1, its server
+// and the second best q2 (where q2 - q1 <= delta q1 matters) are those of a full scan.
+template <typename LT>
+__device__ void pass_b(const WCtx<LT>& c, const StepP& sp, const TopsisP& tp, AccB& b,
+                       unsigned long long& scanned) {
+  const WScr* w = c.w;
+  const float INF = __int_as_float(0x7f800000);
+  float lb[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int ch = c.lane + 32 * i;
+    lb[i] = INF;
+    if (ch < c.nch && !((w->none_m[i] >> c.lane) & 1u))
+      lb[i] = ((w->slow[i] >> c.lane) & 1u) ? 0.f : chunk_qlb(tp, c.ctab[ch]);
+  }
+  float best = INF;
+  for (;;) {
+    float m = lb[0];
+    int mi = 0;
+#pragma unroll
+    for (int i = 1; i < 4; ++i)
+      if (lb[i] < m) { m = lb[i]; mi = i; }
+    // warp argmin of the bounds (non-negative floats order like their bit patterns)
+    const unsigned key = __float_as_uint(m);
+    const unsigned km = __reduce_min_sync(NACS_FULL, key);
+    const float mf = __uint_as_float(km);
+    if (!(mf <= best * kPruneMargin) || mf == INF) break;
+    const int ch = (int)__reduce_min_sync(NACS_FULL, key == km ? (unsigned)(c.lane + 32 * mi) : 0xffffffffu);
+    if (ch == c.lane + 32 * mi) lb[mi] = INF;
+    scanned += 128;
+    score_chunk(c, sp, tp, ch, b);
+    best = __uint_as_float(__reduce_min_sync(NACS_FULL, __float_as_uint(b.b1)));
+  }
+}
+
+// FP64 re-decision (R14): exact closeness of every feasible server with q32 <= thr (chunks
+// whose bound exceeds thr are skipped by the same margin).
+template <typename LT>
+__device__ void scan_fp64(const WCtx<LT>& c, const StepP& sp, const TopsisP& tp, float thr, double& bv, int& bj,
+                          int& bp) {
+  const WScr* w = c.w;
+  for (int ch = 0; ch < c.nch; ++ch) {
+    if (slow_bit(w->none_m, ch)) continue;
+    if (!slow_bit(w->slow, ch) && !(chunk_qlb(tp, c.ctab[ch]) <= thr * kPruneMargin) &&
+        thr != __int_as_float(0x7f800000))
+      continue;
+    const int p0 = (ch << 7) + 4 * c.lane;
+    int4 C, Rm, A, Q, I;
+    unsigned eb;
+    load_slow(c, sp, ch, C, Rm, A, Q, I, eb);
+#pragma unroll 1
+    for (int j = 0; j < 4; ++j) {
+      int x0 = get_comp(C, j), x1 = get_comp(Rm, j), x2 = get_comp(A, j) & 1, x3 = get_comp(Q, j);
       if (ok_any(sp, x0, x1, x3, (eb >> j) & 1u, get_comp(I, j)) && topsis_q32(tp, x0, x1, x2, x3) <= thr) {
         double rr = topsis64(tp, x0, x1, x2, x3);
-        int u = (int)u0 + j;
-        if (rr > bv || (rr == bv && u < bj)) { bv = rr; bj = u; }
+        int u = get_comp(A, j) >> 1;
+        if (rr > bv || (rr == bv && u < bj)) { bv = rr; bj = u; bp = p0 + j; }
       }
     }
   }
 }
 
-// Build the sorted special list: overlay servers, excluded servers, flow servers.
+// Build the special list, sorted by slot: overlay servers, excluded servers, flow servers.
 template <typename LT>
 __device__ void build_specials(WCtx<LT>& c) {
   WScr* w = c.w;
   const int l = c.lane;
   // entry A: overlay slot l; entry B: excluded server l not in the overlay
   bool va = l < w->nos, vbx = false;
-  int ua = va ? w->os_u[l] : INT_MAX, ia = 0;
+  int ua = va ? w->os_pos[l] : INT_MAX, ia = 0;
   if (va) {
+    const int su = w->os_u[l];
     bool ex = false;
-    for (int i = 0; i < w->nex; ++i) ex |= w->ex[i] == ua;
+    for (int i = 0; i < w->nex; ++i) ex |= w->ex[i] == su;
     int f = -1;
     for (int i = 0; i < w->nflow; ++i)
-      if (w->fv[i] == ua) f = i;
+      if (w->fv[i] == su) f = i;
     ia = (l + 1) | (ex ? 64 : 0) | ((f + 1) << 7);
   }
   int ub = INT_MAX;
   if (l < w->nex) {
-    ub = w->ex[l];
-    vbx = os_slot(c, ub) < 0;
-    if (!vbx) ub = INT_MAX;
+    vbx = os_slot(c, w->ex[l]) < 0;
+    ub = vbx ? w->ex_pos[l] : INT_MAX;
   }
   int ra = 0, rb = 0;
   const int lim = max(w->nos, w->nex);
@@ -641,7 +753,10 @@ __device__ void build_specials(WCtx<LT>& c) {
     for (int i = l; i < nEW; i += 32) {
       for (unsigned m = c.edgebad[i]; m; m &= m - 1) {
         const int e = 32 * i + __ffs(m) - 1;
-        for (int ch = (e * c.h) >> 7; ch <= (e * c.h + c.h - 1) >> 7; ++ch) atomicOr(&w->slow[ch >> 5], 1u << (ch & 31));
+        for (int u = e * c.h; u < (e + 1) * c.h; ++u) {
+          const int ch = __ldg(c.inv + u) >> 7;
+          atomicOr(&w->slow[ch >> 5], 1u << (ch & 31));
+        }
       }
     }
   }
@@ -649,7 +764,7 @@ __device__ void build_specials(WCtx<LT>& c) {
 }
 
 struct WStats {
-  unsigned long long steps, retries, fp64, invalid, feas;
+  unsigned long long steps, retries, fp64, invalid, feas, scan_a, scan_b;
 };
 
 // Registers of the request a warp is scheduling.
@@ -814,7 +929,7 @@ __device__ void prepare_step(WCtx<LT>& c, WReq& q, StepP& sp) {
 // a8: commit the chosen server.  Returns 0 ok, 1 routing failed (R18), 2 overlay full.
 // Warp-cooperative: every lane runs the same control flow, lane 0 writes.
 template <typename LT>
-__device__ int commit_step(WCtx<LT>& c, WReq& q, const StepP& sp, int best) {
+__device__ int commit_step(WCtx<LT>& c, WReq& q, const StepP& sp, int best, int best_pos) {
   WScr* w = c.w;
   const int lane = c.lane;
   const int nos0 = w->nos;
@@ -822,10 +937,10 @@ __device__ int commit_step(WCtx<LT>& c, WReq& q, const StepP& sp, int best) {
   int fail = 0;
   {
     int s = w_slot(c, best);
-    int cu = s >= 0 ? w->os_cpu[s] : c.snap[tile_idx(best, 0)];
-    int ru = s >= 0 ? w->os_ram[s] : c.snap[tile_idx(best, 1)];
-    int qu = s >= 0 ? w->os_acc[s] : c.snap[tile_idx(best, 3)];
-    if (!w_set_server(c, best, cu - sp.dc, ru - sp.dr, 1, qu)) fail = 2;
+    int cu = s >= 0 ? w->os_cpu[s] : c.snap[tile_idx(best_pos, 0)];
+    int ru = s >= 0 ? w->os_ram[s] : c.snap[tile_idx(best_pos, 1)];
+    int qu = s >= 0 ? w->os_acc[s] : c.snap[tile_idx(best_pos, 3)];
+    if (!w_set_server(c, best, best_pos, cu - sp.dc, ru - sp.dr, 1, qu)) fail = 2;
   }
   const int nflow = w->nflow;
   for (int fi = 0; fi < nflow && !fail; ++fi) {
@@ -838,16 +953,17 @@ __device__ int commit_step(WCtx<LT>& c, WReq& q, const StepP& sp, int best) {
     const int2 wp = wpath(c, best, v);
     const int su = w_slot(c, best), sv = w_slot(c, v);
     const int au = w->os_acc[su];
-    const int av = sv >= 0 ? w->os_acc[sv] : c.snap[tile_idx(v, 3)];
+    const int pv = sv >= 0 ? w->os_pos[sv] : __ldg(c.inv + v);
+    const int av = sv >= 0 ? w->os_acc[sv] : c.snap[tile_idx(pv, 3)];
     if (min(min(au, av), wp.y) < D) {
       fail = 1;
       break;
     }
-    bool ok = w_set_server(c, best, w->os_cpu[su], w->os_ram[su], w->os_act[su], au - D);
-    const int cv = sv >= 0 ? w->os_cpu[sv] : c.snap[tile_idx(v, 0)];
-    const int rv = sv >= 0 ? w->os_ram[sv] : c.snap[tile_idx(v, 1)];
-    const int tv = sv >= 0 ? w->os_act[sv] : c.snap[tile_idx(v, 2)];
-    ok = ok && w_set_server(c, v, cv, rv, tv, av - D);
+    bool ok = w_set_server(c, best, best_pos, w->os_cpu[su], w->os_ram[su], w->os_act[su], au - D);
+    const int cv = sv >= 0 ? w->os_cpu[sv] : c.snap[tile_idx(pv, 0)];
+    const int rv = sv >= 0 ? w->os_ram[sv] : c.snap[tile_idx(pv, 1)];
+    const int tv = sv >= 0 ? w->os_act[sv] : (c.snap[tile_idx(pv, 2)] & 1);
+    ok = ok && w_set_server(c, v, pv, cv, rv, tv, av - D);
     int fid[4];
     const int m = path_fids(c, best, v, wp.x, fid);
     for (int t = 0; t < m && ok; ++t) ok = w_set_link(c, fid[t], fab_val(c, fid[t]) - D);
@@ -858,7 +974,7 @@ __device__ int commit_step(WCtx<LT>& c, WReq& q, const StepP& sp, int best) {
   if (fail == 1) {
     w_undo(c, nos0);
     if (lane == 0) {
-      if (w->nex < WX) w->ex[w->nex] = best;
+      if (w->nex < WX) { w->ex[w->nex] = best; w->ex_pos[w->nex] = best_pos; }
       w->nex += 1;
     }
   }
@@ -972,49 +1088,41 @@ __device__ __forceinline__ bool group_sync_and(int id, int nt, bool p) {
 // on its own request, so that all warps run the same loop at the same time (one copy of
 // the hot code in the instruction caches); within a phase no warp waits for another.
 template <typename LT>
-__global__ void __launch_bounds__(512, 1) k_batch_warp(Geo g, Opt o, const int* __restrict__ state, ReqsDev R,
-                                                       OutDev O, int4* ulog_all, int* next, const int* order,
-                                                       int* deferred, int* n_deferred, unsigned long long* stats,
-                                                       int group) {
+__global__ void __launch_bounds__(512, 1) k_batch_warp(Geo g, Opt o, const int* __restrict__ state,
+                                                       const int* __restrict__ lay, ReqsDev R, OutDev O,
+                                                       int4* ulog_all, int* next, const int* order, int* deferred,
+                                                       int* n_deferred, unsigned long long* stats, int group,
+                                                       int sync_mask) {
   extern __shared__ __align__(16) unsigned char dyn[];
   const int n = g.n, h = g.h, k = g.k, E = g.E;
-  const int npad = (n + 127) & ~127;
-  // ---- a0: shared snapshot (read-only for the whole kernel)
+  const int npad = (n + 127) & ~127, nch = npad >> 7;
+  // ---- a0: shared snapshot (read-only for the whole kernel): the chunk layout of the
+  // criteria and the chunk table (k_warp_layout), the fabric links in switch order
   int* ssnap = reinterpret_cast<int*>(dyn);
-  LT* sfab = reinterpret_cast<LT*>(ssnap + 4 * npad);
+  ChunkT* stab = reinterpret_cast<ChunkT*>(ssnap + 4 * npad);
+  LT* sfab = reinterpret_cast<LT*>(stab + nch);
   const int nfab = E * h + k * h * h;
-  size_t off = (size_t)16 * npad + (((size_t)sizeof(LT) * nfab + 15) & ~(size_t)15);
+  size_t off = (size_t)16 * npad + sizeof(ChunkT) * nch + (((size_t)sizeof(LT) * nfab + 15) & ~(size_t)15);
   const int nDW = (E + k * h + 31) >> 5, nEW = (E + 31) >> 5;
   const size_t wbytes = ((sizeof(WScr) + 4 * (nDW + nEW + k)) + 15) & ~(size_t)15;
   __shared__ __align__(8) unsigned long long mbar;
-  // criteria rows -> 128-server tiles: one 512-byte TMA bulk copy per (tile, criterion)
-  const bool bulk = npad == n;
-  const int ncp = 4 * (npad >> 7);
-  if (bulk && threadIdx.x == 0) {
-    const unsigned mb = smem_addr(&mbar);
+  __shared__ int s_fabmin;
+  // criteria tiles and chunk table are contiguous in `lay` and in shared memory: TMA bulk
+  const unsigned bytes = 16u * (unsigned)npad + (unsigned)sizeof(ChunkT) * (unsigned)nch;
+  if (threadIdx.x == 0) {
+    const unsigned mb = smem_addr(&mbar), chunk = 32768;
+    s_fabmin = INT_MAX;
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(16u * (unsigned)n) : "memory");
-  }
-  __syncthreads();
-  if (bulk) {
-    const unsigned mb = smem_addr(&mbar);
-    for (int i = threadIdx.x; i < ncp; i += blockDim.x) {
-      const int t = i >> 2, j = i & 3;
-      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 512, [%2];" ::"r"(
-                       smem_addr(ssnap + (t << 9) + (j << 7))),
-                   "l"(state + (size_t)j * n + (t << 7)), "r"(mb)
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes) : "memory");
+    for (unsigned o2 = 0; o2 < bytes; o2 += chunk) {
+      const unsigned sz = bytes - o2 < chunk ? bytes - o2 : chunk;
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       smem_addr(dyn) + o2),
+                   "l"(reinterpret_cast<const unsigned char*>(lay + LAY_PST) + o2), "r"(sz), "r"(mb)
                    : "memory");
     }
-  } else {
-    for (int i = threadIdx.x; i < 4 * npad; i += blockDim.x) {
-      const int j = i / npad, u = i - j * npad;
-      // padding is never feasible (demands are > 0): cpu = ram = -1
-      ssnap[tile_idx(u, j)] = u < n ? state[(size_t)j * n + u] : (j < 2 ? -1 : 0);
-    }
   }
-  __shared__ int s_fabmin;
-  if (threadIdx.x == 0) s_fabmin = INT_MAX;
   __syncthreads();
   {
     int m = INT_MAX;
@@ -1027,7 +1135,7 @@ __global__ void __launch_bounds__(512, 1) k_batch_warp(Geo g, Opt o, const int* 
     if ((threadIdx.x & 31) == 0) atomicMin(&s_fabmin, m);
   }
   __syncthreads();
-  if (bulk) {
+  {
     const unsigned mb = smem_addr(&mbar);
     asm volatile(
         "{\n .reg .pred P1;\n WAIT_%=:\n"
@@ -1044,6 +1152,9 @@ __global__ void __launch_bounds__(512, 1) k_batch_warp(Geo g, Opt o, const int* 
   c.k = k; c.h = h; c.n = n; c.npad = npad; c.E = E; c.nfabea = E * h;
   c.magic = g.magic_h;
   c.snap = ssnap;
+  c.ctab = stab;
+  c.inv = lay + LAY_PST + 4 * npad + 16 * nch;
+  c.nch = nch;
   c.a_snap = smem_addr(ssnap) + 16u * lane;
   c.fab = sfab;
   unsigned char* wb = dyn + off + (size_t)warp * wbytes;
@@ -1060,13 +1171,13 @@ __global__ void __launch_bounds__(512, 1) k_batch_warp(Geo g, Opt o, const int* 
   c.o = o;
   WScr* w = c.w;
   const double wd[4] = {o.wd[0], o.wd[1], o.wd[2], o.wd[3]};
-  WStats ws = {0, 0, 0, 0, 0};
+  WStats ws = {0, 0, 0, 0, 0, 0, 0};
   WReq q;
   q.r = -1;
   StepP sp;
   TopsisP tp;
   bool active = false, done = false, prep = false;
-  int best = -1;
+  int best = -1, best_pos = -1;
 
   for (;;) {
     // ---- phase P: acquire a request; flows and fabric tables of its pod step
@@ -1085,7 +1196,7 @@ __global__ void __launch_bounds__(512, 1) k_batch_warp(Geo g, Opt o, const int* 
     bool stepping = active;
     if (stepping) {
       AccA acc = {0, 0, UINT_MAX, UINT_MAX, UINT_MAX, 0u, 0u, 0u, 0ull, 0ull, 0ull};
-      scan_stats(c, sp, acc);
+      pass_a(c, sp, acc, ws.scan_a);
       const int nf = (int)__reduce_add_sync(NACS_FULL, (unsigned)acc.nf);
       ws.steps += 1;
       ws.feas += (unsigned long long)nf;
@@ -1105,33 +1216,40 @@ __global__ void __launch_bounds__(512, 1) k_batch_warp(Geo g, Opt o, const int* 
         topsis_params(tp, wd, sq);
       }
     }
-    group_sync(bar_id, bar_nt);
+    if (sync_mask & 1) group_sync(bar_id, bar_nt);
     // ---- phase B (a5T + a7): closeness, argmax (lowest index), FP64 near-tie re-decision
     if (stepping) {
       const float INF = __int_as_float(0x7f800000);
-      AccB bb = {INF, INF, -1};
-      scan_score(c, sp, tp, bb);
+      AccB bb = {INF, INF, -1, -1};
+      pass_b(c, sp, tp, bb, ws.scan_b);
       // smallest q (positive floats order like their bit patterns), lowest index on ties
       const unsigned key1 = __float_as_uint(bb.b1);
       const unsigned m1 = __reduce_min_sync(NACS_FULL, key1);
       best = (int)__reduce_min_sync(NACS_FULL, key1 == m1 ? (unsigned)bb.i1 : UINT_MAX);
       const bool winner = key1 == m1 && bb.i1 == best;
+      {
+        const unsigned wl = __ballot_sync(NACS_FULL, winner);
+        best_pos = __shfl_sync(NACS_FULL, bb.p1, wl ? __ffs(wl) - 1 : 0);
+      }
       const unsigned m2 = __reduce_min_sync(NACS_FULL, winner ? __float_as_uint(bb.b2) : key1);
       const float q1 = __uint_as_float(m1), q2 = __uint_as_float(m2);
       if (o.exact64 || m2 == m1 || q2 - q1 <= kTopsisDeltaQ * q1) {  // R14: FP64 near-tie re-decision
         const float thr = o.exact64 ? INF : q1 * (1.0f + 2.0f * kTopsisDeltaQ);
         double bv = -DBL_MAX;
-        int bj = -1;
-        scan_fp64(c, sp, tp, thr, bv, bj);
+        int bj = -1, bp = -1;
+        scan_fp64(c, sp, tp, thr, bv, bj, bp);
+        const int mine = bj;
         warp_argmax64(bv, bj);
         best = bj;
+        const unsigned wl = __ballot_sync(NACS_FULL, mine == bj && bj >= 0);
+        best_pos = __shfl_sync(NACS_FULL, bp, wl ? __ffs(wl) - 1 : 0);
         ws.fp64 += 1;
       }
     }
-    group_sync(bar_id, bar_nt);
+    if (sync_mask & 2) group_sync(bar_id, bar_nt);
     // ---- phase C (a8, a9): commit; next pod, retry (R18), or request end
     if (stepping) {
-      int fail = commit_step(c, q, sp, best);
+      int fail = commit_step(c, q, sp, best, best_pos);
       if (fail == 1) {
         ws.retries += 1;
         if (w->nex > WX || w->nos + w->nex > WSP) fail = 2;
@@ -1156,6 +1274,8 @@ __global__ void __launch_bounds__(512, 1) k_batch_warp(Geo g, Opt o, const int* 
     if (ws.fp64) atomicAdd(&stats[ST_FP64], ws.fp64);
     if (ws.invalid) atomicAdd(&stats[ST_INVALID], ws.invalid);
     if (ws.feas) atomicAdd(&stats[ST_FEAS], ws.feas);
+    if (ws.scan_a) atomicAdd(&stats[ST_SCAN_A], ws.scan_a);
+    if (ws.scan_b) atomicAdd(&stats[ST_SCAN_B], ws.scan_b);
   }
 }
 
@@ -1186,11 +1306,176 @@ __global__ void __launch_bounds__(1024) k_order_lpt(ReqsDev R, int* order) {
   }
 }
 
+// ------------------------------------------------------------ chunk layout ----
+// The scans of k_batch_warp read the criteria in 128-slot chunks whose static boxes and
+// aggregates let pass A take whole chunks at once and let pass B skip chunks by a bound.
+// k_warp_layout orders the servers for tight boxes: first the "low" servers (some
+// criterion below the largest pod demand of the batch, or the access link below a tenth
+// of its capacity: the ones the thresholds actually cut), then by f_u, then along a
+// Z-order curve of (CPU, RAM, access link) quantised to 10 bits; ties by server index.
+// The order changes only which servers share a chunk, never a result.
+
+// Largest pod CPU / RAM demand (sum of c^min over a pod's containers) of the batch.
+__global__ void k_pod_max(ReqsDev R, int* lay) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  int mc = 0, mr = 0;
+  if (r < R.n) {
+    const int c0 = R.coff[r], c1 = R.coff[r + 1];
+    if (c1 > c0 && c1 - c0 <= WC) {
+      for (int i = c0; i < c1; ++i) {
+        const int p = R.pod_of[i];
+        bool first = true;
+        for (int j = c0; j < i; ++j) first &= R.pod_of[j] != p;
+        if (!first) continue;
+        long long sc = 0, sr = 0;
+        for (int j = i; j < c1; ++j)
+          if (R.pod_of[j] == p) { sc += R.cpu_min[j]; sr += R.ram_min[j]; }
+        mc = (int)max((long long)mc, min(sc, (long long)INT_MAX));
+        mr = (int)max((long long)mr, min(sr, (long long)INT_MAX));
+      }
+    }
+  }
+  mc = (int)__reduce_max_sync(NACS_FULL, (unsigned)mc);
+  mr = (int)__reduce_max_sync(NACS_FULL, (unsigned)mr);
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(lay + 0, mc);
+    atomicMax(lay + 1, mr);
+  }
+}
+
+__device__ __forceinline__ unsigned spread3(unsigned x) {  // bits 0..9 -> every third bit
+  x &= 0x3ffu;
+  x = (x | (x << 16)) & 0x030000FFu;
+  x = (x | (x << 8)) & 0x0300F00Fu;
+  x = (x | (x << 4)) & 0x030C30C3u;
+  x = (x | (x << 2)) & 0x09249249u;
+  return x;
+}
+__device__ __forceinline__ unsigned quant10(int v, int vmax) {
+  return (unsigned)(((long long)max(v, 0) << 10) / ((long long)vmax + 1));
+}
+
+// One CTA: sort the servers by layout key, write the criteria tiles, inv and the chunk table.
+__global__ void __launch_bounds__(1024) k_warp_layout(Geo g, const int* __restrict__ state, int* lay) {
+  extern __shared__ unsigned long long key[];
+  __shared__ int smax[3];
+  const int n = g.n, npad = (n + 127) & ~127, nch = npad >> 7;
+  int P2 = 1;
+  while (P2 < npad) P2 <<= 1;
+  int* pst = lay + LAY_PST;
+  ChunkT* tab = reinterpret_cast<ChunkT*>(pst + 4 * npad);
+  int* inv = pst + 4 * npad + 16 * nch;
+  const int* cpu = state;
+  const int* ram = state + n;
+  const int* act = state + 2 * n;
+  const int* acc = state + 3 * n;
+  if (threadIdx.x < 3) smax[threadIdx.x] = 0;
+  __syncthreads();
+  {
+    int m0 = 0, m1 = 0, m2 = 0;
+    for (int u = threadIdx.x; u < n; u += blockDim.x) {
+      m0 = max(m0, cpu[u]);
+      m1 = max(m1, ram[u]);
+      m2 = max(m2, acc[u]);
+    }
+    m0 = (int)__reduce_max_sync(NACS_FULL, (unsigned)max(m0, 0));
+    m1 = (int)__reduce_max_sync(NACS_FULL, (unsigned)max(m1, 0));
+    m2 = (int)__reduce_max_sync(NACS_FULL, (unsigned)max(m2, 0));
+    if ((threadIdx.x & 31) == 0) { atomicMax(&smax[0], m0); atomicMax(&smax[1], m1); atomicMax(&smax[2], m2); }
+  }
+  __syncthreads();
+  const int Tc = lay[0], Tr = lay[1], Ta = max(1, g.link_cap / 10);
+  for (int i = threadIdx.x; i < P2; i += blockDim.x) {
+    unsigned long long kk = ~0ull;
+    if (i < n) {
+      const bool high = cpu[i] >= Tc && ram[i] >= Tr && acc[i] >= Ta;
+      const unsigned z = (spread3(quant10(cpu[i], smax[0])) << 2) | (spread3(quant10(ram[i], smax[1])) << 1) |
+                         spread3(quant10(acc[i], smax[2]));
+      kk = ((unsigned long long)high << 63) | ((unsigned long long)(act[i] & 1) << 62) |
+           ((unsigned long long)z << 32) | (unsigned)i;
+    }
+    key[i] = kk;
+  }
+  __syncthreads();
+  for (int kb = 2; kb <= P2; kb <<= 1) {
+    for (int j = kb >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < P2; i += blockDim.x) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const unsigned long long x = key[i], y = key[ixj];
+          const bool up = (i & kb) == 0;
+          if ((x > y) == up) { key[i] = y; key[ixj] = x; }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int i = threadIdx.x; i < npad; i += blockDim.x) {
+    const int t = i >> 7, l = i & 127;
+    int* tile = pst + (t << 9);
+    if (i < n) {
+      const int u = (int)(key[i] & 0xffffffffu);
+      tile[l] = cpu[u];
+      tile[128 + l] = ram[u];
+      tile[256 + l] = (u << 1) | (act[u] & 1);
+      tile[384 + l] = acc[u];
+      inv[u] = i;
+    } else {  // padding is never feasible (demands are > 0)
+      tile[l] = -1;
+      tile[128 + l] = -1;
+      tile[256 + l] = 0;
+      tile[384 + l] = 0;
+    }
+  }
+  __syncthreads();
+  // chunk table: one warp per chunk, 4 slots per lane
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int ch = warp; ch < nch; ch += blockDim.x >> 5) {
+    int lo[3] = {INT_MAX, INT_MAX, INT_MAX}, hi[3] = {INT_MIN, INT_MIN, INT_MIN};
+    int cnt = 0, nact = 0, am = 0;
+    unsigned long long sq[3] = {0, 0, 0};
+    for (int j = 0; j < 4; ++j) {
+      const int i = (ch << 7) + 4 * lane + j;
+      if (i >= n) continue;
+      const int u = (int)(key[i] & 0xffffffffu);
+      const int x[3] = {cpu[u], ram[u], acc[u]};
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        lo[c] = min(lo[c], x[c]);
+        hi[c] = max(hi[c], x[c]);
+        sq[c] += (unsigned long long)((long long)x[c] * x[c]);
+      }
+      cnt += 1;
+      nact += act[u] & 1;
+      am |= 1 << (act[u] & 1);
+    }
+    ChunkT t;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      t.lo[c] = __reduce_min_sync(NACS_FULL, lo[c]);
+      t.hi[c] = __reduce_max_sync(NACS_FULL, hi[c]);
+      unsigned long long v = sq[c];
+#pragma unroll
+      for (int o2 = 16; o2 > 0; o2 >>= 1) v += __shfl_xor_sync(NACS_FULL, v, o2);
+      t.sq[c] = v;
+    }
+    t.cnt = (int)__reduce_add_sync(NACS_FULL, (unsigned)cnt);
+    t.nact = (int)__reduce_add_sync(NACS_FULL, (unsigned)nact);
+    t.act = (int)__reduce_or_sync(NACS_FULL, (unsigned)am);
+    t.pad = 0;
+    if (lane == 0) tab[ch] = t;
+  }
+}
+
 // ------------------------------------------------------------------- host ----
 static size_t warp_snapshot_bytes(const Geo& g, bool u16) {
   size_t npad = (size_t)((g.n + 127) & ~127);
   size_t nfab = (size_t)g.E * g.h + (size_t)g.k * g.h * g.h;
-  return 16 * npad + (((u16 ? 2 : 4) * nfab + 15) & ~(size_t)15);
+  return 16 * npad + sizeof(ChunkT) * (npad >> 7) + (((u16 ? 2 : 4) * nfab + 15) & ~(size_t)15);
+}
+size_t warp_layout_ints(const Geo& g) {
+  size_t npad = (size_t)((g.n + 127) & ~127);
+  return LAY_PST + 4 * npad + 16 * (npad >> 7) + (size_t)g.n;
 }
 static size_t warp_scratch_bytes(const Geo& g) {
   int nDW = (g.E + g.k * g.h + 31) >> 5, nEW = (g.E + 31) >> 5;
@@ -1210,25 +1495,40 @@ int warp_kernel_warps(const Geo& g) {
 
 size_t warp_ulog_entries(int grid, int warps) { return (size_t)grid * warps * WLOG; }
 
-cudaError_t launch_batch_warp(const Geo& g, const Opt& o, const int* d_state, const ReqsDev& R, const OutDev& O,
-                              int4* ulog, int* next, int* order, int* deferred, int* n_deferred,
+cudaError_t launch_batch_warp(const Geo& g, const Opt& o, const int* d_state, int* lay, const ReqsDev& R,
+                              const OutDev& O, int4* ulog, int* next, int* order, int* deferred, int* n_deferred,
                               unsigned long long* stats, int grid, int warps, cudaStream_t st) {
   bool u16 = g.link_cap <= 65535;
+  cudaError_t e = cudaMemsetAsync(lay, 0, 4 * sizeof(int), st);
+  if (e != cudaSuccess) return e;
+  if (R.n > 0) k_pod_max<<<(R.n + 255) / 256, 256, 0, st>>>(R, lay);
+  {
+    const int npad = (g.n + 127) & ~127;
+    int P2 = 1;
+    while (P2 < npad) P2 <<= 1;
+    const size_t lsm = sizeof(unsigned long long) * (size_t)P2;
+    cudaFuncSetAttribute(k_warp_layout, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsm);
+    k_warp_layout<<<1, 1024, lsm, st>>>(g, d_state, lay);
+  }
   k_order_lpt<<<1, 1024, 0, st>>>(R, order);
   static const int group = [] {
     const char* e = getenv("NACS_WARP_GROUP");
     int v = e ? atoi(e) : 8;
     return v < 1 ? 1 : (v > 16 ? 16 : v);
   }();
+  static const int sync_mask = [] {
+    const char* e = getenv("NACS_WARP_SYNC");
+    return e ? atoi(e) : 3;
+  }();
   size_t smem = warp_snapshot_bytes(g, u16) + (size_t)warps * warp_scratch_bytes(g);
   if (u16) {
     cudaFuncSetAttribute(k_batch_warp<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_batch_warp<uint16_t><<<grid, warps * 32, smem, st>>>(g, o, d_state, R, O, ulog, next, order, deferred,
-                                                           n_deferred, stats, group);
+    k_batch_warp<uint16_t><<<grid, warps * 32, smem, st>>>(g, o, d_state, lay, R, O, ulog, next, order, deferred,
+                                                           n_deferred, stats, group, sync_mask);
   } else {
     cudaFuncSetAttribute(k_batch_warp<int>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_batch_warp<int><<<grid, warps * 32, smem, st>>>(g, o, d_state, R, O, ulog, next, order, deferred, n_deferred,
-                                                      stats, group);
+    k_batch_warp<int><<<grid, warps * 32, smem, st>>>(g, o, d_state, lay, R, O, ulog, next, order, deferred, n_deferred,
+                                                      stats, group, sync_mask);
   }
   return cudaGetLastError();
 }

@@ -63,7 +63,7 @@ class Options(C.Structure):
 class Stats(C.Structure):
     _fields_ = [("pod_steps", C.c_int64), ("servers_ranked", C.c_int64), ("retries", C.c_int64),
                 ("fp64_decisions", C.c_int64), ("invalid", C.c_int64), ("feasible", C.c_int64),
-                ("ahp_pairs", C.c_int64)]
+                ("ahp_pairs", C.c_int64), ("scanned_a", C.c_int64), ("scanned_b", C.c_int64)]
 
 
 EXPORTS = ["nacs_create", "nacs_create_sharded", "nacs_nccl_unique_id", "nacs_destroy", "nacs_load_topology",
