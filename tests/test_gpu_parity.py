@@ -274,6 +274,37 @@ def test_warp_kernel_equals_cta_kernel(ctx):
         cta.close()
 
 
+def test_warp_kernel_pruned_scans_at_scale(ctx):
+    """The warp kernel's chunk layout, whole-chunk statistics and best-first pruned scoring
+    at k=32 (64 chunks): identical to the CTA kernel (which reads every server in index
+    order) on exact-tie (quantised), congested-fabric (slow chunks) and exact-FP64 runs,
+    and to the oracle on a sample."""
+    from paper_1909_07673_b200 import nacs
+    cta = _cta_only_ctx()
+    try:
+        quant = gen.snapshot(32, seed=21, quantised=True)
+        tight = gen.snapshot(32, seed=22)
+        tight["link_res"] = np.random.default_rng(3).integers(0, 120, size=len(tight["link_res"])).astype(np.int32)
+        cases = [(quant, gen.requests(1500, 23), 0), (tight, gen.requests(1500, 24, bw_max_hi=60), 0),
+                 (gen.config("C4")[0], gen.requests(600, 25), nacs.NACS_EXACT_FP64)]
+        for snap, reqs, flags in cases:
+            ctx.load_topology(snap)
+            cta.load_topology(snap)
+            for schema in SCHEMAS:
+                a = to_np(ctx.schedule_batch(reqs, "topsis", schema, flags=flags))
+                sa = ctx.last_stats()
+                b = to_np(cta.schedule_batch(reqs, "topsis", schema, flags=flags))
+                for key in a:
+                    assert np.array_equal(a[key], b[key]), (schema, key)
+                assert sa["scanned_b"] < sa["servers_ranked"] or flags
+        sub = gen.subset(cases[0][1], np.arange(0, 1500, 15))
+        ctx.load_topology(quant)
+        out = ctx.schedule_batch(sub, "topsis", "clustering")
+        assert_schedule_parity(quant, sub, out, "topsis", "clustering", False)
+    finally:
+        cta.close()
+
+
 def test_large_requests_deferred_to_cta_kernel(ctx):
     """Requests with more than 32 containers or 64 vlinks leave the warp fast path for the
     CTA kernel; mixed batches stay exact."""
