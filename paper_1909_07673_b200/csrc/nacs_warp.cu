@@ -172,7 +172,8 @@ __device__ bool w_set_server(WCtx<LT>& c, int u, int pos, int cpu, int ram, int 
   return ok;
 }
 template <typename LT>
-__device__ bool w_set_link(WCtx<LT>& c, int fid, int val, bool log = true) {
+// Link fid (fabric) += delta on the current residual (overlay value, else the snapshot's).
+__device__ bool w_add_link(WCtx<LT>& c, int fid, int delta, bool log = true) {
   WScr* w = c.w;
   const int nol = w->nol;
   int pos = 0;
@@ -189,9 +190,10 @@ __device__ bool w_set_link(WCtx<LT>& c, int fid, int val, bool log = true) {
   if (found) {
     if (c.lane == 0) {
       if (log) c.ulog[c.ulog_n] = make_int4(-1, fid, w->ol_val[pos], 0);
-      w->ol_val[pos] = val;
+      w->ol_val[pos] += delta;
     }
   } else {  // insert at pos, shifting the tail right
+    const int val = (int)c.fab[fid] + delta;
     int ids[WOL / 32], vals[WOL / 32];
 #pragma unroll
     for (int q = 0; q < WOL / 32; ++q) {
@@ -594,7 +596,7 @@ __device__ void pass_a(const WCtx<LT>& c, const StepP& sp, AccA& a, unsigned lon
 // Lower bound of q = Ed+^2 / Ed-^2 over the servers of a chunk (its box clipped to the
 // [min, max] of F): Ed+_c >= s_c (max_c - min(hi_c, max_c)), Ed-_c <= s_c (min(hi_c, max_c)
 // - min_c).  FP32 with relative error <= 12u; callers prune with a 2^-12 margin.
-__device__ __forceinline__ float chunk_qlb(const TopsisP& t, const ChunkT& ct) {
+__device__ __forceinline__ float chunk_qlb(const TopsisP& t, const ChunkT& ct, int act_or = 0) {
   float ep2, em2;
   {
     const int ci[3] = {0, 1, 3};
@@ -605,8 +607,9 @@ __device__ __forceinline__ float chunk_qlb(const TopsisP& t, const ChunkT& ct) {
       e[c] = t.sf[ci[c]] * (float)(t.mx[ci[c]] - hc);
       m[c] = t.sf[ci[c]] * (float)max(0, hc - t.mn[ci[c]]);
     }
-    const float pa = (ct.act & 2) ? ((ct.act & 1) ? fminf(t.p2sq[0], t.p2sq[1]) : t.p2sq[1]) : t.p2sq[0];
-    const float ma = (ct.act & 2) ? ((ct.act & 1) ? fmaxf(t.m2sq[0], t.m2sq[1]) : t.m2sq[1]) : t.m2sq[0];
+    const int am = ct.act | act_or;
+    const float pa = (am & 2) ? ((am & 1) ? fminf(t.p2sq[0], t.p2sq[1]) : t.p2sq[1]) : t.p2sq[0];
+    const float ma = (am & 2) ? ((am & 1) ? fmaxf(t.m2sq[0], t.m2sq[1]) : t.m2sq[1]) : t.m2sq[0];
     ep2 = fmaf(e[2], e[2], fmaf(e[1], e[1], fmaf(e[0], e[0], pa)));
     em2 = fmaf(m[2], m[2], fmaf(m[1], m[1], fmaf(m[0], m[0], ma)));
   }
@@ -642,7 +645,8 @@ __device__ __forceinline__ void score_chunk(const WCtx<LT>& c, const StepP& sp, 
 }
 
 // Pass B (a5T + a7): best-first over chunks.  Every chunk with a feasible server gets the
-// lower bound of its q (slow chunks 0: their overlaid values may leave the box); the warp
+// lower bound of its q (slow chunks too: a commit only lowers residuals and sets f_u = 1,
+// so an overlaid server stays under the box's upper corner once f_u = 1 joins it); the warp
 // visits chunks in increasing bound while the bound is within the prune margin of the
 // best q so far.  Every server with q32 <= q1 (1 + 2^-12) is visited, so q1, its server
 // and the second best q2 (where q2 - q1 <= delta q1 matters) are those of a full scan.
@@ -657,7 +661,7 @@ __device__ void pass_b(const WCtx<LT>& c, const StepP& sp, const TopsisP& tp, Ac
     const int ch = c.lane + 32 * i;
     lb[i] = INF;
     if (ch < c.nch && !((w->none_m[i] >> c.lane) & 1u))
-      lb[i] = ((w->slow[i] >> c.lane) & 1u) ? 0.f : chunk_qlb(tp, c.ctab[ch]);
+      lb[i] = chunk_qlb(tp, c.ctab[ch], ((w->slow[i] >> c.lane) & 1u) ? 2 : 0);
   }
   float best = INF;
   for (;;) {
@@ -687,9 +691,7 @@ __device__ void scan_fp64(const WCtx<LT>& c, const StepP& sp, const TopsisP& tp,
   const WScr* w = c.w;
   for (int ch = 0; ch < c.nch; ++ch) {
     if (slow_bit(w->none_m, ch)) continue;
-    if (!slow_bit(w->slow, ch) && !(chunk_qlb(tp, c.ctab[ch]) <= thr * kPruneMargin) &&
-        thr != __int_as_float(0x7f800000))
-      continue;
+    if (!(chunk_qlb(tp, c.ctab[ch], slow_bit(w->slow, ch) ? 2 : 0) <= thr * kPruneMargin)) continue;
     const int p0 = (ch << 7) + 4 * c.lane;
     int4 C, Rm, A, Q, I;
     unsigned eb;
@@ -966,7 +968,7 @@ __device__ int commit_step(WCtx<LT>& c, WReq& q, const StepP& sp, int best, int 
     ok = ok && w_set_server(c, v, pv, cv, rv, tv, av - D);
     int fid[4];
     const int m = path_fids(c, best, v, wp.x, fid);
-    for (int t = 0; t < m && ok; ++t) ok = w_set_link(c, fid[t], fab_val(c, fid[t]) - D);
+    for (int t = 0; t < m && ok; ++t) ok = w_add_link(c, fid[t], -D);
     if (!ok) fail = 2;
     if (lane == 0) w->fpath[fi] = wp.x;
     __syncwarp();
@@ -1045,7 +1047,7 @@ __device__ void finish_request(WCtx<LT>& c, const WReq& q, const OutDev& O) {
         __syncwarp();
         if (lane == 0) { w->os_acc[ss] -= extra; w->os_acc[sd] -= extra; }
         __syncwarp();
-        for (int t = 0; t < m; ++t) w_set_link(c, fid[t], fab_val(c, fid[t]) - extra, false);
+        for (int t = 0; t < m; ++t) w_add_link(c, fid[t], -extra, false);
       }
       bw = bmin + extra;
     }
