@@ -36,9 +36,11 @@ from inputs import gen  # noqa: E402
 # Algorithmic operation counts.
 TOPSIS_OPS_ALL = 3       # per server ranked: the CPU/RAM/access-bandwidth compares of the filter
 TOPSIS_OPS_FEAS = 45     # per feasible server: stats (14) + closeness (30) + argmax (1)
-# kernels launched per nacs_schedule_batch call: TOPSIS = k_order_lpt + k_batch_warp + k_batch
-# (deferred requests; exits at once when none); AHP = k_batch
-LAUNCHES = {"topsis": 3, "ahp": 1}
+# kernels launched per nacs_schedule_batch call: TOPSIS = k_pod_max + k_warp_layout + k_order_lpt +
+# k_batch_warp + k_batch (deferred requests; exits at once when none); AHP = k_batch
+LAUNCHES = {"topsis": 5, "ahp": 1}
+# DRAM bytes per launch of k_batch_warp from the committed `ncu --set full` capture
+TRAFFIC = os.path.join(ROOT, "profiles", "ncu_traffic.json")
 AHP_RCP_PER_PAIR = 1     # per unordered pair per non-constant criterion per pass: one reciprocal
 
 
@@ -70,7 +72,10 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+    """SM clocks and throttle reasons sampled during the timed region through NVML (the
+    library behind nvidia-smi), in-process every 20 ms: spawning nvidia-smi inside the
+    timed region takes the driver lock and stalls the launch queue.  Falls back to
+    nvidia-smi when NVML is unavailable."""
 
     FIELDS = "clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown," \
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"
@@ -81,25 +86,43 @@ class ClockSampler:
         self._stop = threading.Event()
         self._first = threading.Event()
         self._t = None
+        self._nvml = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nvml = (pynvml, pynvml.nvmlDeviceGetHandleByIndex(device))
+        except Exception:
+            self._nvml = None
+
+    def _sample_nvml(self):
+        nv, h = self._nvml
+        sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+        bits = [nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap]
+        return [str(sm), str(mx)] + ["Active" if r & b else "Not Active" for b in bits]
 
     def _run(self):
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
+                if self._nvml is not None:
+                    self.samples.append(self._sample_nvml())
+                else:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                         timeout=5).stdout.strip()
+                    if out:
+                        self.samples.append([x.strip() for x in out.split(",")])
             except Exception:
                 pass
             self._first.set()
-            self._stop.wait(0.2)
+            self._stop.wait(0.02 if self._nvml is not None else 0.2)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
-        # nvidia-smi start-up can hold the driver lock: let the first query finish before
-        # the timed region so it cannot starve the launch queue
+        # let the first query finish before the timed region
         self._first.wait(timeout=10)
         return self
 
@@ -115,7 +138,8 @@ class ClockSampler:
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+                "reasons": reasons, "samples": len(self.samples),
+                "source": "nvml" if self._nvml is not None else "nvidia-smi"}
 
 
 def workload(rank: int, method: str):
@@ -173,7 +197,8 @@ def run_ours(args, rank, world, local):
         ctx.load_topology(snap)
         d = {k: (torch.from_numpy(v).to(dev) if isinstance(v, np.ndarray) else v) for k, v in reqs.items()}
         out = ctx._alloc_out(reqs, True)[0]
-        for _ in range(args.warmup):
+        for _ in range(args.warmup):  # warm-up includes the flush (its first launch loads torch's module)
+            flush.zero_()
             ctx.schedule_batch(d, method, "flat", out=out, flags=nacs.NACS_ASYNC)
         torch.cuda.synchronize(dev)
         st0 = ctx.last_stats()
@@ -214,8 +239,16 @@ def run_ours(args, rank, world, local):
     st = topsis["stats"]
     ops = TOPSIS_OPS_ALL * st["servers_ranked"] + TOPSIS_OPS_FEAS * st["feasible"]
     achieved = ops / (topsis["kernel_ms"] / 1e3) / 1e12
+    traffic = None
+    if os.path.exists(TRAFFIC):
+        traffic = json.load(open(TRAFFIC)).get("k_batch_warp", {}).get("dram_bytes_per_launch")
+    # the kernel reads only part of the slots (whole-chunk statistics, pruned scoring):
+    # the fraction of the 2 x servers_ranked slot reads a full two-pass scan would make
+    read_frac = (st["scanned_a"] + st["scanned_b"]) / max(1, 2 * st["servers_ranked"])
     roofline = {"bound": "alu", "achieved": achieved, "peak": alu_peak, "unit": "Top/s",
-                "frac": achieved / alu_peak, "traffic": None, "kernel": "k_batch_warp<TOPSIS> (whole call)",
+                "frac": achieved / alu_peak, "traffic": traffic, "kernel": "k_batch_warp<TOPSIS> (whole call)",
+                "ops": "method-algorithmic: 3 per server ranked + 45 per feasible server (SURVEY 8(d))",
+                "slots_read_frac": read_frac,
                 "peak_source": f"148 SMs x 128 lanes x {mhz:.0f} MHz (sm_max_mhz, {pk_kind})"}
 
     ahp_obj = None
