@@ -36,11 +36,18 @@ struct WScr {
   int ol_id[WOL], ol_val[WOL];
   int pod_srv[WC];
   int fv[WF], fD[WF], fok[WF], fpath[WF];
-  int sp_u[WSP], sp_info[WSP];
+  union {
+    struct {
+      int sp_u[WSP], sp_info[WSP];
+    };
+    int dem[WOL + WOS];  // finish_request: top-up demands (the special list is free by then)
+  };
   int ex[WX];
   int os_pos[WOS], ex_pos[WX];  // their slots in the chunk layout
   unsigned slow[4];  // chunks of 128 slots the scans take on the slow path (<= 128 chunks)
   unsigned none_m[4];  // chunks without a feasible server in this pod step (pass A)
+  unsigned sp_has[4];  // chunks holding a special server
+  unsigned char sp_first[128];  // index in sp_u of a chunk's first special (valid where sp_has)
   int net;
   // dynamic tail: dirty[(E + k*h + 31)/32] | edgebad[(E+31)/32] | pm[k]
 };
@@ -484,13 +491,8 @@ __device__ __forceinline__ void chunk_specials(const WCtx<LT>& c, const StepP& s
   const WScr* w = c.w;
   info[0] = info[1] = info[2] = info[3] = 0;
   const int base = ch << 7;
-  int lo = 0, hi = w->nsp;
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (w->sp_u[mid] < base) lo = mid + 1;
-    else hi = mid;
-  }
-  for (int t = lo; t < w->nsp && w->sp_u[t] < base + 128; ++t) {
+  if (!((w->sp_has[ch >> 5] >> (ch & 31)) & 1u)) return;
+  for (int t = w->sp_first[ch]; t < w->nsp && w->sp_u[t] < base + 128; ++t) {
     const int pos = w->sp_u[t], inf = w->sp_info[t];
     if (((pos - base) >> 2) == c.lane) {
       const int j = (pos - base) & 3;
@@ -747,9 +749,12 @@ __device__ void build_specials(WCtx<LT>& c) {
   // slow chunks: those holding a special server or, with the path filter on, a server
   // under an edge switch without a feasible fabric path (all others skip both tests)
   for (int i = l; i < cnt; i += 32) {
-    const int u = w->sp_u[i];
-    atomicOr(&w->slow[u >> 12], 1u << ((u >> 7) & 31));
+    const int u = w->sp_u[i], ch = u >> 7;
+    atomicOr(&w->slow[ch >> 5], 1u << (ch & 31));
+    if (i == 0 || (w->sp_u[i - 1] >> 7) != ch) w->sp_first[ch] = (unsigned char)i;
   }
+  __syncwarp();
+  if (l < 4) w->sp_has[l] = w->slow[l];
   if (w->net) {
     const int nEW = (c.E + 31) >> 5;
     for (int i = l; i < nEW; i += 32) {
@@ -1009,24 +1014,74 @@ template <typename LT>
 __device__ void finish_request(WCtx<LT>& c, const WReq& q, const OutDev& O) {
   WScr* w = c.w;
   const int lane = c.lane;
+  // R19 containers, in container order: greedy per server = clamp of prefix sums.  Lane i
+  // holds container i; with P = the extras wanted by the earlier containers on its server,
+  // it gets min(P + x, R) - min(P, R) of the server's residual R.
   int my_ec = 0, my_er = 0;
-  for (int i = 0; i < q.nC; ++i) {
-    const int pd = __shfl_sync(NACS_FULL, q.cpod, i);
-    const int xc = __shfl_sync(NACS_FULL, q.cmax - q.cmin, i), xr = __shfl_sync(NACS_FULL, q.rmax - q.rmin, i);
-    const int s = w_slot(c, w->pod_srv[pd]);  // a placed server is always overlaid
-    const int ec = min(xc, w->os_cpu[s]);
-    const int er = min(xr, w->os_ram[s]);
+  {
+    const bool hc = lane < q.nC;
+    const int s = hc ? os_slot(c, w->pod_srv[q.cpod]) : -1;  // a placed server is always overlaid
+    const int xc = q.cmax - q.cmin, xr = q.rmax - q.rmin;
+    if (hc) { w->dem[lane] = xc; w->dem[32 + lane] = xr; }
+    const unsigned peers = __match_any_sync(NACS_FULL, s) & __ballot_sync(NACS_FULL, hc);
     __syncwarp();
-    if (lane == 0) { w->os_cpu[s] -= ec; w->os_ram[s] -= er; }
+    if (hc) {
+      int pc = 0, pr = 0;
+      for (unsigned m = peers & ((1u << lane) - 1u); m; m &= m - 1) {
+        const int j = __ffs(m) - 1;
+        pc += w->dem[j];
+        pr += w->dem[32 + j];
+      }
+      const int Rc = w->os_cpu[s], Rr = w->os_ram[s];
+      my_ec = min(pc + xc, Rc) - min(pc, Rc);
+      my_er = min(pr + xr, Rr) - min(pr, Rr);
+      if (lane == 31 - __clz(peers)) {  // the server's last container writes its residual
+        w->os_cpu[s] = Rc - min(pc + xc, Rc);
+        w->os_ram[s] = Rr - min(pr + xr, Rr);
+      }
+    }
     __syncwarp();
-    if (lane == i) { my_ec = ec; my_er = er; }
   }
+  // R19 vlinks, in vlink order.  When no access link or fabric link is asked for more than
+  // its residual by all the vlinks together, every vlink gets its whole extra and the
+  // greedy order cannot matter: apply the sums in parallel.  Otherwise the sequential loop.
   int my_bw0 = 0, my_bw1 = 0;
-#ifdef NACS_EXP_NO_TOPUP
-  for (int e = 0; e < 0; ++e) {
-#else
-  for (int e = 0; e < q.nV; ++e) {
-#endif
+  bool par = true;
+  {
+    int* dem_l = w->dem;        // [WOL] per overlay link position
+    int* dem_s = w->dem + WOL;  // [WOS] per overlay server slot (its access link)
+    for (int i = lane; i < WOL + WOS; i += 32) w->dem[i] = 0;
+    __syncwarp();
+#pragma unroll
+    for (int hv = 0; hv < 2; ++hv) {
+      const bool has = hv ? q.hv1 : q.hv0;
+      if (!has) continue;
+      const int us = w->pod_srv[hv ? q.pa1 : q.pa0], ud = w->pod_srv[hv ? q.pb1 : q.pb0];
+      const int want = (hv ? q.bx1 - q.bn1 : q.bx0 - q.bn0);
+      if (us == ud || want == 0) continue;
+      atomicAdd(&dem_s[os_slot(c, us)], want);
+      atomicAdd(&dem_s[os_slot(c, ud)], want);
+      int fid[4];
+      const int m = path_fids(c, us, ud, hv ? q.path1 : q.path0, fid);
+      for (int t = 0; t < m; ++t) {
+        const int p = ol_find(w, fid[t]);  // a reserved path's links are in the overlay
+        if (p < 0) par = false;
+        else atomicAdd(&dem_l[p], want);
+      }
+    }
+    __syncwarp();
+    for (int i = lane; i < w->nos; i += 32) par &= dem_s[i] <= w->os_acc[i];
+    for (int i = lane; i < w->nol; i += 32) par &= dem_l[i] <= w->ol_val[i];
+    par = __all_sync(NACS_FULL, par);
+    if (par) {
+      for (int i = lane; i < w->nos; i += 32) w->os_acc[i] -= dem_s[i];
+      for (int i = lane; i < w->nol; i += 32) w->ol_val[i] -= dem_l[i];
+      my_bw0 = q.bx0;
+      my_bw1 = q.bx1;
+    }
+    __syncwarp();
+  }
+  for (int e = 0; e < (par ? 0 : q.nV); ++e) {
     const int src_lane = e & 31;
     const bool hi = e >= 32;
     const int es = __shfl_sync(NACS_FULL, hi ? q.pa1 : q.pa0, src_lane);
@@ -1313,8 +1368,9 @@ __global__ void __launch_bounds__(1024) k_order_lpt(ReqsDev R, int* order) {
 // aggregates let pass A take whole chunks at once and let pass B skip chunks by a bound.
 // k_warp_layout orders the servers for tight boxes: first the "low" servers (some
 // criterion below the largest pod demand of the batch, or the access link below a tenth
-// of its capacity: the ones the thresholds actually cut), then by f_u, then along a
-// Z-order curve of (CPU, RAM, access link) quantised to 10 bits; ties by server index.
+// of its capacity: the ones the thresholds actually cut) in 4 buckets of how low, then by
+// f_u, then along a Z-order curve of (CPU, RAM, access link) quantised to 10 bits; ties by
+// server index.
 // The order changes only which servers share a chunk, never a result.
 
 // Largest pod CPU / RAM demand (sum of c^min over a pod's containers) of the batch.
@@ -1393,8 +1449,16 @@ __global__ void __launch_bounds__(1024) k_warp_layout(Geo g, const int* __restri
       const bool high = cpu[i] >= Tc && ram[i] >= Tr && acc[i] >= Ta;
       const unsigned z = (spread3(quant10(cpu[i], smax[0])) << 2) | (spread3(quant10(ram[i], smax[1])) << 1) |
                          spread3(quant10(acc[i], smax[2]));
-      kk = ((unsigned long long)high << 63) | ((unsigned long long)(act[i] & 1) << 62) |
-           ((unsigned long long)z << 32) | (unsigned)i;
+      // low servers: by how low (4 buckets of min_c x_c / T_c), so that the low tiles of a
+      // pod step are mostly wholly feasible or wholly cut
+      unsigned bucket = 0;
+      if (!high) {
+        const float r = fminf(fminf((float)cpu[i] / (float)max(Tc, 1), (float)ram[i] / (float)max(Tr, 1)),
+                              (float)acc[i] / (float)Ta);
+        bucket = (unsigned)min(3, max(0, (int)(r * 4.0f)));
+      }
+      kk = ((unsigned long long)high << 63) | ((unsigned long long)bucket << 61) |
+           ((unsigned long long)(act[i] & 1) << 60) | ((unsigned long long)z << 30) | (unsigned)i;
     }
     key[i] = kk;
   }
@@ -1416,7 +1480,7 @@ __global__ void __launch_bounds__(1024) k_warp_layout(Geo g, const int* __restri
     const int t = i >> 7, l = i & 127;
     int* tile = pst + (t << 9);
     if (i < n) {
-      const int u = (int)(key[i] & 0xffffffffu);
+      const int u = (int)(key[i] & 0x3fffffffu);
       tile[l] = cpu[u];
       tile[128 + l] = ram[u];
       tile[256 + l] = (u << 1) | (act[u] & 1);
@@ -1439,7 +1503,7 @@ __global__ void __launch_bounds__(1024) k_warp_layout(Geo g, const int* __restri
     for (int j = 0; j < 4; ++j) {
       const int i = (ch << 7) + 4 * lane + j;
       if (i >= n) continue;
-      const int u = (int)(key[i] & 0xffffffffu);
+      const int u = (int)(key[i] & 0x3fffffffu);
       const int x[3] = {cpu[u], ram[u], acc[u]};
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
