@@ -1,14 +1,17 @@
 // nacs_warp.cu — warp-per-request TOPSIS batch kernel (nacs_schedule_batch fast path).
 //
-// Every warp schedules whole requests on its own (no block barrier anywhere): all warps
-// of a CTA share one read-only copy of the snapshot in shared memory (criteria table as
-// padded int32 SoA, fabric links as u16), and each warp keeps a private *overlay* of
-// the servers and links its current request has modified (R21 snapshot isolation).
-// Scans of the n servers go 128 servers per warp iteration (4 consecutive servers per
-// lane, int4 loads); the few servers that are special in a pod step (overlaid, excluded
-// or flow endpoints) are merged into the scan through a sorted list.  Fabric-table rows
-// (edge-agg rows, agg-core rows) touched by the overlay are flagged dirty and read
-// through the overlay; clean rows are read straight from the snapshot.
+// Every warp schedules whole requests on its own: all warps of a CTA share one read-only
+// copy of the snapshot in shared memory (criteria in 128-slot tiles of a chunk layout with
+// a summary per tile, fabric links as u16), and each warp keeps a private *overlay* of the
+// servers and links its current request has modified (R21 snapshot isolation).  Pass A
+// (filter + statistics) takes wholly feasible tiles from their summaries and scans the
+// others, 128 slots per warp iteration (4 slots per lane, int4 loads); pass B (closeness +
+// argmax) visits tiles best-first by a lower bound of q and stops when no unvisited tile
+// can hold the best.  The few servers that are special in a pod step (overlaid, excluded
+// or flow endpoints) are masked out of the tiles and handled in a parallel specials pass.
+// Fabric-table rows touched by the overlay are flagged dirty and read through it.  The
+// warps advance in lockstep groups of 8 (named barriers) so that a group runs one code
+// region at a time.
 //
 // Requests beyond the fast-path limits (containers > 32, vlinks > 64, or overlay /
 // exclusion overflow) are appended to a deferred list that the CTA-per-request kernel
@@ -47,6 +50,7 @@ struct WScr {
   unsigned slow[4];  // chunks of 128 slots the scans take on the slow path (<= 128 chunks)
   unsigned none_m[4];  // chunks without a feasible server in this pod step (pass A)
   unsigned sp_has[4];  // chunks holding a special server
+  unsigned eb_has[4];  // chunks holding a server under a fabric-blocked edge switch
   unsigned char sp_first[128];  // index in sp_u of a chunk's first special (valid where sp_has)
   int net;
   // dynamic tail: dirty[(E + k*h + 31)/32] | edgebad[(E+31)/32] | pm[k]
@@ -472,74 +476,62 @@ __device__ __forceinline__ void merge_b(AccB& a, const AccB& o) {
   a.b1 = lt ? o.b1 : a.b1;
 }
 
-__device__ __forceinline__ void set_comp(int4& v, int j, int x) {
-  if (j == 0) v.x = x;
-  else if (j == 1) v.y = x;
-  else if (j == 2) v.z = x;
-  else v.w = x;
-}
-__device__ __forceinline__ int get_comp(const int4& v, int j) {
-  return j == 0 ? v.x : (j == 1 ? v.y : (j == 2 ? v.z : v.w));
-}
 
-// Substitute the special servers of chunk ch into the lane's 4 slots and force their
-// feasibility: info[j] = 1 | ok << 1 (0 = ordinary server).  The special list is sorted
-// by slot; any chunk order.
+__device__ __forceinline__ bool slow_bit(const unsigned* m, int ch) { return (m[ch >> 5] >> (ch & 31)) & 1u; }
+
+// Masks of the lane's 4 slots of chunk ch (bit j = slot 4 lane + j): `skip` = special
+// servers (taken by the specials pass instead), `bad` = servers under an edge switch
+// without a feasible fabric path.  Both 0 for clean chunks.
 template <typename LT>
-__device__ __forceinline__ void chunk_specials(const WCtx<LT>& c, const StepP& sp, int ch, int4& C, int4& Rm,
-                                               int4& A, int4& Q, int info[4]) {
+__device__ __forceinline__ void chunk_masks(const WCtx<LT>& c, const StepP& sp, int ch, const int4& A,
+                                            unsigned& skip, unsigned& bad) {
   const WScr* w = c.w;
-  info[0] = info[1] = info[2] = info[3] = 0;
+  skip = 0u;
+  bad = 0u;
+  if (!slow_bit(w->slow, ch)) return;
   const int base = ch << 7;
-  if (!((w->sp_has[ch >> 5] >> (ch & 31)) & 1u)) return;
-  for (int t = w->sp_first[ch]; t < w->nsp && w->sp_u[t] < base + 128; ++t) {
-    const int pos = w->sp_u[t], inf = w->sp_info[t];
-    if (((pos - base) >> 2) == c.lane) {
-      const int j = (pos - base) & 3;
-      const int slot = (inf & 63) - 1;
-      if (slot >= 0) {
-        set_comp(C, j, w->os_cpu[slot]);
-        set_comp(Rm, j, w->os_ram[slot]);
-        set_comp(A, j, (w->os_u[slot] << 1) | w->os_act[slot]);
-        set_comp(Q, j, w->os_acc[slot]);
-      }
-      const unsigned bad = sp.net ? ebad(c, (unsigned)(get_comp(A, j) >> 1)) : 0u;
-      const bool ok = ok_special(c, sp, get_comp(C, j), get_comp(Rm, j), get_comp(Q, j), bad, inf);
-      info[j] = 1 | (ok ? 2 : 0);
+  if (slow_bit(w->sp_has, ch)) {
+    for (int t = w->sp_first[ch]; t < w->nsp && w->sp_u[t] < base + 128; ++t) {
+      const int d = w->sp_u[t] - base;
+      if ((d >> 2) == c.lane) skip |= 1u << (d & 3);
     }
   }
-}
-
-// feasibility of one server: forced for special servers, the ordinary rule otherwise
-__device__ __forceinline__ bool ok_any(const StepP& sp, int x0, int x1, int x3, unsigned bad, int forced) {
-  const bool pl = ok_plain(sp, x0, x1, x3, bad);
-  return (forced & 1) ? (forced & 2) != 0 : pl;
-}
-
-// Load the lane's 4 slots of chunk ch (slow path: specials substituted, edge bits by server).
-template <typename LT>
-__device__ __forceinline__ void load_slow(const WCtx<LT>& c, const StepP& sp, int ch, int4& C, int4& Rm, int4& A,
-                                          int4& Q, int4& I, unsigned& eb) {
-  const unsigned ao = c.a_snap + ((unsigned)ch << 11);
-  C = lds128(ao);
-  Rm = lds128(ao + 512);
-  A = lds128(ao + 1024);
-  Q = lds128(ao + 1536);
-  int info[4];
-  chunk_specials(c, sp, ch, C, Rm, A, Q, info);
-  I = make_int4(info[0], info[1], info[2], info[3]);
-  eb = 0u;
-  if (sp.net) {
-    eb = ebad(c, (unsigned)A.x >> 1) | (ebad(c, (unsigned)A.y >> 1) << 1) | (ebad(c, (unsigned)A.z >> 1) << 2) |
-         (ebad(c, (unsigned)A.w >> 1) << 3);
+  if (sp.net && slow_bit(w->eb_has, ch)) {
+    bad = ebad(c, (unsigned)A.x >> 1) | (ebad(c, (unsigned)A.y >> 1) << 1) | (ebad(c, (unsigned)A.z >> 1) << 2) |
+          (ebad(c, (unsigned)A.w >> 1) << 3);
   }
 }
-__device__ __forceinline__ bool slow_bit(const unsigned* m, int ch) { return (m[ch >> 5] >> (ch & 31)) & 1u; }
+
+// Special server t of the step (lanes in parallel): current values (overlay, else the
+// snapshot at its slot), server index, feasibility by the special rules.
+template <typename LT>
+__device__ __forceinline__ bool special_vals(const WCtx<LT>& c, const StepP& sp, int t, int& x0, int& x1, int& x2,
+                                            int& x3, int& id) {
+  const WScr* w = c.w;
+  const int pos = w->sp_u[t], inf = w->sp_info[t];
+  const int slot = (inf & 63) - 1;
+  if (slot >= 0) {
+    x0 = w->os_cpu[slot];
+    x1 = w->os_ram[slot];
+    id = w->os_u[slot];
+    x2 = (id << 1) | w->os_act[slot];
+    x3 = w->os_acc[slot];
+  } else {
+    x0 = c.snap[tile_idx(pos, 0)];
+    x1 = c.snap[tile_idx(pos, 1)];
+    x2 = c.snap[tile_idx(pos, 2)];
+    x3 = c.snap[tile_idx(pos, 3)];
+    id = x2 >> 1;
+  }
+  const unsigned bad = sp.net ? ebad(c, (unsigned)id) : 0u;
+  return ok_special(c, sp, x0, x1, x3, bad, inf);
+}
 
 // Pass A (a3 + a4): filter and statistics.  Per chunk (one lane each): a chunk whose box
 // lies inside the thresholds and holds no special server is feasible as a whole and adds
 // its precomputed aggregates; a chunk whose box misses a threshold holds no feasible
-// server; the warp scans the others, 128 slots per iteration.  Exact either way.
+// server; the warp scans the others, 128 slots per iteration, and the special servers
+// in one parallel pass.  Exact either way.
 template <typename LT>
 __device__ void pass_a(const WCtx<LT>& c, const StepP& sp, AccA& a, unsigned long long& scanned) {
   WScr* w = c.w;
@@ -574,23 +566,21 @@ __device__ void pass_a(const WCtx<LT>& c, const StepP& sp, AccA& a, unsigned lon
     for (unsigned m = scan_m[i]; m; m &= m - 1) {
       const int ch = 32 * i + __ffs(m) - 1;
       scanned += 128;
-      if (!slow_bit(w->slow, ch)) {
-        const unsigned ao = c.a_snap + ((unsigned)ch << 11);
-        const int4 C = lds128(ao), Rm = lds128(ao + 512), A = lds128(ao + 1024), Q = lds128(ao + 1536);
-        acc_a(a, ok_plain(sp, C.x, Rm.x, Q.x, 0u), C.x, Rm.x, A.x, Q.x);
-        acc_a(a, ok_plain(sp, C.y, Rm.y, Q.y, 0u), C.y, Rm.y, A.y, Q.y);
-        acc_a(a, ok_plain(sp, C.z, Rm.z, Q.z, 0u), C.z, Rm.z, A.z, Q.z);
-        acc_a(a, ok_plain(sp, C.w, Rm.w, Q.w, 0u), C.w, Rm.w, A.w, Q.w);
-      } else {
-        int4 C, Rm, A, Q, I;
-        unsigned eb;
-        load_slow(c, sp, ch, C, Rm, A, Q, I, eb);
-        acc_a(a, ok_any(sp, C.x, Rm.x, Q.x, eb & 1u, I.x), C.x, Rm.x, A.x, Q.x);
-        acc_a(a, ok_any(sp, C.y, Rm.y, Q.y, eb & 2u, I.y), C.y, Rm.y, A.y, Q.y);
-        acc_a(a, ok_any(sp, C.z, Rm.z, Q.z, eb & 4u, I.z), C.z, Rm.z, A.z, Q.z);
-        acc_a(a, ok_any(sp, C.w, Rm.w, Q.w, eb & 8u, I.w), C.w, Rm.w, A.w, Q.w);
-      }
+      const unsigned ao = c.a_snap + ((unsigned)ch << 11);
+      const int4 C = lds128(ao), Rm = lds128(ao + 512), A = lds128(ao + 1024), Q = lds128(ao + 1536);
+      unsigned skip, bad;
+      chunk_masks(c, sp, ch, A, skip, bad);
+      const unsigned off = skip | bad;
+      acc_a(a, ok_plain(sp, C.x, Rm.x, Q.x, off & 1u), C.x, Rm.x, A.x, Q.x);
+      acc_a(a, ok_plain(sp, C.y, Rm.y, Q.y, off & 2u), C.y, Rm.y, A.y, Q.y);
+      acc_a(a, ok_plain(sp, C.z, Rm.z, Q.z, off & 4u), C.z, Rm.z, A.z, Q.z);
+      acc_a(a, ok_plain(sp, C.w, Rm.w, Q.w, off & 8u), C.w, Rm.w, A.w, Q.w);
     }
+  }
+  for (int t = c.lane; t < w->nsp; t += 32) {
+    int x0, x1, x2, x3, id;
+    const bool ok = special_vals(c, sp, t, x0, x1, x2, x3, id);
+    acc_a(a, ok, x0, x1, x2, x3);
   }
   __syncwarp();
 }
@@ -619,36 +609,28 @@ __device__ __forceinline__ float chunk_qlb(const TopsisP& t, const ChunkT& ct, i
 }
 constexpr float kPruneMargin = 1.0f + 2.44140625e-4f;  // 1 + 2^-12
 
-// Scores of the lane's 4 slots of chunk ch into b (a5T + a7).
+// Scores of the lane's 4 slots of chunk ch into b (a5T + a7); special slots are skipped
+// (the specials pass scores them).
 template <typename LT>
 __device__ __forceinline__ void score_chunk(const WCtx<LT>& c, const StepP& sp, const TopsisP& tp, int ch,
                                             AccB& b) {
   const int p0 = (ch << 7) + 4 * c.lane;
-  if (!slow_bit(c.w->slow, ch)) {
-    const unsigned ao = c.a_snap + ((unsigned)ch << 11);
-    const int4 C = lds128(ao), Rm = lds128(ao + 512), A = lds128(ao + 1024), Q = lds128(ao + 1536);
-    AccB b2 = {__int_as_float(0x7f800000), __int_as_float(0x7f800000), -1, -1};  // shorter chains
-    acc_b(b, ok_plain(sp, C.x, Rm.x, Q.x, 0u), topsis_q32_scan(tp, C.x, Rm.x, A.x, Q.x), A.x >> 1, p0);
-    acc_b(b2, ok_plain(sp, C.y, Rm.y, Q.y, 0u), topsis_q32_scan(tp, C.y, Rm.y, A.y, Q.y), A.y >> 1, p0 + 1);
-    acc_b(b, ok_plain(sp, C.z, Rm.z, Q.z, 0u), topsis_q32_scan(tp, C.z, Rm.z, A.z, Q.z), A.z >> 1, p0 + 2);
-    acc_b(b2, ok_plain(sp, C.w, Rm.w, Q.w, 0u), topsis_q32_scan(tp, C.w, Rm.w, A.w, Q.w), A.w >> 1, p0 + 3);
-    merge_b(b, b2);
-  } else {
-    int4 C, Rm, A, Q, I;
-    unsigned eb;
-    load_slow(c, sp, ch, C, Rm, A, Q, I, eb);
-#pragma unroll 1
-    for (int j = 0; j < 4; ++j) {
-      const int x0 = get_comp(C, j), x1 = get_comp(Rm, j), x2 = get_comp(A, j), x3 = get_comp(Q, j);
-      const bool ok = ok_any(sp, x0, x1, x3, (eb >> j) & 1u, get_comp(I, j));
-      acc_b(b, ok, topsis_q32_scan(tp, x0, x1, x2, x3), x2 >> 1, p0 + j);
-    }
-  }
+  const unsigned ao = c.a_snap + ((unsigned)ch << 11);
+  const int4 C = lds128(ao), Rm = lds128(ao + 512), A = lds128(ao + 1024), Q = lds128(ao + 1536);
+  unsigned skip, bad;
+  chunk_masks(c, sp, ch, A, skip, bad);
+  const unsigned off = skip | bad;
+  AccB b2 = {__int_as_float(0x7f800000), __int_as_float(0x7f800000), -1, -1};  // shorter chains
+  acc_b(b, ok_plain(sp, C.x, Rm.x, Q.x, off & 1u), topsis_q32_scan(tp, C.x, Rm.x, A.x, Q.x), A.x >> 1, p0);
+  acc_b(b2, ok_plain(sp, C.y, Rm.y, Q.y, off & 2u), topsis_q32_scan(tp, C.y, Rm.y, A.y, Q.y), A.y >> 1, p0 + 1);
+  acc_b(b, ok_plain(sp, C.z, Rm.z, Q.z, off & 4u), topsis_q32_scan(tp, C.z, Rm.z, A.z, Q.z), A.z >> 1, p0 + 2);
+  acc_b(b2, ok_plain(sp, C.w, Rm.w, Q.w, off & 8u), topsis_q32_scan(tp, C.w, Rm.w, A.w, Q.w), A.w >> 1, p0 + 3);
+  merge_b(b, b2);
 }
 
-// Pass B (a5T + a7): best-first over chunks.  Every chunk with a feasible server gets the
-// lower bound of its q (slow chunks too: a commit only lowers residuals and sets f_u = 1,
-// so an overlaid server stays under the box's upper corner once f_u = 1 joins it); the warp
+// Pass B (a5T + a7): the special servers first (lanes in parallel), then best-first over
+// chunks.  Every chunk with a feasible server gets the lower bound of its q from its box
+// (its special slots are skipped, so the box holds what the chunk scores); the warp
 // visits chunks in increasing bound while the bound is within the prune margin of the
 // best q so far.  Every server with q32 <= q1 (1 + 2^-12) is visited, so q1, its server
 // and the second best q2 (where q2 - q1 <= delta q1 matters) are those of a full scan.
@@ -657,15 +639,19 @@ __device__ void pass_b(const WCtx<LT>& c, const StepP& sp, const TopsisP& tp, Ac
                        unsigned long long& scanned) {
   const WScr* w = c.w;
   const float INF = __int_as_float(0x7f800000);
+  for (int t = c.lane; t < w->nsp; t += 32) {
+    int x0, x1, x2, x3, id;
+    const bool ok = special_vals(c, sp, t, x0, x1, x2, x3, id);
+    acc_b(b, ok, topsis_q32_scan(tp, x0, x1, x2, x3), id, w->sp_u[t]);
+  }
   float lb[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int ch = c.lane + 32 * i;
     lb[i] = INF;
-    if (ch < c.nch && !((w->none_m[i] >> c.lane) & 1u))
-      lb[i] = chunk_qlb(tp, c.ctab[ch], ((w->slow[i] >> c.lane) & 1u) ? 2 : 0);
+    if (ch < c.nch && !((w->none_m[i] >> c.lane) & 1u)) lb[i] = chunk_qlb(tp, c.ctab[ch]);
   }
-  float best = INF;
+  float best = __uint_as_float(__reduce_min_sync(NACS_FULL, __float_as_uint(b.b1)));
   for (;;) {
     float m = lb[0];
     int mi = 0;
@@ -686,27 +672,36 @@ __device__ void pass_b(const WCtx<LT>& c, const StepP& sp, const TopsisP& tp, Ac
 }
 
 // FP64 re-decision (R14): exact closeness of every feasible server with q32 <= thr (chunks
-// whose bound exceeds thr are skipped by the same margin).
+// whose bound exceeds thr are skipped by the same margin; specials in parallel).
+__device__ __forceinline__ void fp64_take(const TopsisP& tp, float thr, bool ok, int x0, int x1, int x2, int x3,
+                                          int u, int pos, double& bv, int& bj, int& bp) {
+  if (ok && topsis_q32(tp, x0, x1, x2 & 1, x3) <= thr) {
+    const double rr = topsis64(tp, x0, x1, x2 & 1, x3);
+    if (rr > bv || (rr == bv && u < bj)) { bv = rr; bj = u; bp = pos; }
+  }
+}
 template <typename LT>
 __device__ void scan_fp64(const WCtx<LT>& c, const StepP& sp, const TopsisP& tp, float thr, double& bv, int& bj,
                           int& bp) {
   const WScr* w = c.w;
+  for (int t = c.lane; t < w->nsp; t += 32) {
+    int x0, x1, x2, x3, id;
+    const bool ok = special_vals(c, sp, t, x0, x1, x2, x3, id);
+    fp64_take(tp, thr, ok, x0, x1, x2, x3, id, w->sp_u[t], bv, bj, bp);
+  }
   for (int ch = 0; ch < c.nch; ++ch) {
     if (slow_bit(w->none_m, ch)) continue;
-    if (!(chunk_qlb(tp, c.ctab[ch], slow_bit(w->slow, ch) ? 2 : 0) <= thr * kPruneMargin)) continue;
+    if (!(chunk_qlb(tp, c.ctab[ch]) <= thr * kPruneMargin)) continue;
     const int p0 = (ch << 7) + 4 * c.lane;
-    int4 C, Rm, A, Q, I;
-    unsigned eb;
-    load_slow(c, sp, ch, C, Rm, A, Q, I, eb);
-#pragma unroll 1
-    for (int j = 0; j < 4; ++j) {
-      int x0 = get_comp(C, j), x1 = get_comp(Rm, j), x2 = get_comp(A, j) & 1, x3 = get_comp(Q, j);
-      if (ok_any(sp, x0, x1, x3, (eb >> j) & 1u, get_comp(I, j)) && topsis_q32(tp, x0, x1, x2, x3) <= thr) {
-        double rr = topsis64(tp, x0, x1, x2, x3);
-        int u = get_comp(A, j) >> 1;
-        if (rr > bv || (rr == bv && u < bj)) { bv = rr; bj = u; bp = p0 + j; }
-      }
-    }
+    const unsigned ao = c.a_snap + ((unsigned)ch << 11);
+    const int4 C = lds128(ao), Rm = lds128(ao + 512), A = lds128(ao + 1024), Q = lds128(ao + 1536);
+    unsigned skip, bad;
+    chunk_masks(c, sp, ch, A, skip, bad);
+    const unsigned off = skip | bad;
+    fp64_take(tp, thr, ok_plain(sp, C.x, Rm.x, Q.x, off & 1u), C.x, Rm.x, A.x, Q.x, A.x >> 1, p0, bv, bj, bp);
+    fp64_take(tp, thr, ok_plain(sp, C.y, Rm.y, Q.y, off & 2u), C.y, Rm.y, A.y, Q.y, A.y >> 1, p0 + 1, bv, bj, bp);
+    fp64_take(tp, thr, ok_plain(sp, C.z, Rm.z, Q.z, off & 4u), C.z, Rm.z, A.z, Q.z, A.z >> 1, p0 + 2, bv, bj, bp);
+    fp64_take(tp, thr, ok_plain(sp, C.w, Rm.w, Q.w, off & 8u), C.w, Rm.w, A.w, Q.w, A.w >> 1, p0 + 3, bv, bj, bp);
   }
 }
 
@@ -754,7 +749,8 @@ __device__ void build_specials(WCtx<LT>& c) {
     if (i == 0 || (w->sp_u[i - 1] >> 7) != ch) w->sp_first[ch] = (unsigned char)i;
   }
   __syncwarp();
-  if (l < 4) w->sp_has[l] = w->slow[l];
+  if (l < 4) { w->sp_has[l] = w->slow[l]; w->eb_has[l] = 0u; }
+  __syncwarp();
   if (w->net) {
     const int nEW = (c.E + 31) >> 5;
     for (int i = l; i < nEW; i += 32) {
@@ -763,6 +759,7 @@ __device__ void build_specials(WCtx<LT>& c) {
         for (int u = e * c.h; u < (e + 1) * c.h; ++u) {
           const int ch = __ldg(c.inv + u) >> 7;
           atomicOr(&w->slow[ch >> 5], 1u << (ch & 31));
+          atomicOr(&w->eb_has[ch >> 5], 1u << (ch & 31));
         }
       }
     }
