@@ -31,9 +31,12 @@ constexpr int WSP = 64;   // specials per pod step
 constexpr int WF = 32;    // flows per pod step
 constexpr int WX = 32;    // exclusions per pod step
 constexpr int WLOG = 256; // undo-log entries per commit
+constexpr int WDW = 64;   // dirty-row bitmap words: fabric rows E + k*h <= 2048
+constexpr int WEW = 32;   // edge bitmap words: E <= 1024
+constexpr int WWARPS = 16; // warps per CTA (static per-warp scratch)
 }  // namespace
 
-struct WScr {
+struct __align__(16) WScr {
   int nos, nol, nflow, sumD, G, nsp, nex, pad0;
   int os_u[WOS], os_cpu[WOS], os_ram[WOS], os_act[WOS], os_acc[WOS];
   int ol_id[WOL], ol_val[WOL];
@@ -53,7 +56,8 @@ struct WScr {
   unsigned eb_has[4];  // chunks holding a server under a fabric-blocked edge switch
   unsigned char sp_first[128];  // index in sp_u of a chunk's first special (valid where sp_has)
   int net;
-  // dynamic tail: dirty[(E + k*h + 31)/32] | edgebad[(E+31)/32] | pm[k]
+  unsigned dirty[WDW];    // fabric rows (edge-agg rows, then agg-core rows) the overlay touched
+  unsigned edgebad[WEW];  // edge switches without a feasible fabric path this pod step
 };
 
 // Static summary of one 128-slot chunk of the layout (k_warp_layout): the box of its
@@ -79,13 +83,12 @@ struct WCtx {
   int nch;
   const LT* fab;                           // edge-agg[E*h] | agg-core[k*h*h] (shared)
   WScr* w;
-  unsigned *dirty, *edgebad, *pm;
   int4* ulog;
   int ulog_n;
   int lane;
   int nDW;
   int fabmin;  // smallest fabric residual of the snapshot
-  unsigned a_snap, a_edge;  // 32-bit shared addresses (a_snap: + 16 * lane)
+  unsigned a_snap;  // 32-bit shared address of the criteria tiles + 16 * lane
   Opt o;
 };
 
@@ -120,7 +123,7 @@ __device__ __forceinline__ int ol_find(const WScr* w, int fid) {
 }
 template <typename LT>
 __device__ __forceinline__ bool row_dirty(const WCtx<LT>& c, int row) {
-  return (c.dirty[row >> 5] >> (row & 31)) & 1u;
+  return (c.w->dirty[row >> 5] >> (row & 31)) & 1u;
 }
 // fabric link fid (per lane): the overlay value if its row is dirty and it is overlaid
 template <typename LT>
@@ -229,7 +232,7 @@ __device__ bool w_add_link(WCtx<LT>& c, int fid, int delta, bool log = true) {
   if (log) c.ulog_n += 1;
   if (c.lane == 0) {
     unsigned row = div_h((unsigned)fid, c.magic);
-    c.dirty[row >> 5] |= 1u << (row & 31);
+    c.w->dirty[row >> 5] |= 1u << (row & 31);
   }
   __syncwarp();
   return true;
@@ -363,7 +366,7 @@ __device__ void wfabric(WCtx<LT>& c) {
   WScr* w = c.w;
   const int h = c.h, E = c.E;
   const int nEW = (E + 31) >> 5;
-  for (int i = c.lane; i < nEW; i += 32) c.edgebad[i] = 0u;
+  for (int i = c.lane; i < nEW; i += 32) c.w->edgebad[i] = 0u;
   // every fabric link (snapshot and overlay) >= D: no edge is cut off for that flow
   int lmin = c.fabmin;
   for (int i = c.lane; i < w->nol; i += 32) lmin = min(lmin, w->ol_val[i]);
@@ -392,7 +395,7 @@ __device__ void wfabric(WCtx<LT>& c) {
         bad = !ok;
       }
       const unsigned bw = __ballot_sync(NACS_FULL, bad);
-      if (c.lane == 0) c.edgebad[e0 >> 5] |= bw;
+      if (c.lane == 0) c.w->edgebad[e0 >> 5] |= bw;
     }
     __syncwarp();
   }
@@ -410,7 +413,7 @@ struct StepP {
 template <typename LT>
 __device__ __forceinline__ unsigned ebad(const WCtx<LT>& c, unsigned u) {
   unsigned e = div_h(u, c.magic);
-  return (lds32v(c.a_edge + 4u * (e >> 5)) >> (e & 31)) & 1u;
+  return (c.w->edgebad[e >> 5] >> (e & 31)) & 1u;
 }
 // edge-infeasibility bits (bit j) of the lane's servers u0..u0+3
 template <typename LT>
@@ -754,7 +757,7 @@ __device__ void build_specials(WCtx<LT>& c) {
   if (w->net) {
     const int nEW = (c.E + 31) >> 5;
     for (int i = l; i < nEW; i += 32) {
-      for (unsigned m = c.edgebad[i]; m; m &= m - 1) {
+      for (unsigned m = c.w->edgebad[i]; m; m &= m - 1) {
         const int e = 32 * i + __ffs(m) - 1;
         for (int u = e * c.h; u < (e + 1) * c.h; ++u) {
           const int ch = __ldg(c.inv + u) >> 7;
@@ -859,7 +862,7 @@ __device__ bool acquire(WCtx<LT>& c, const ReqsDev& R, const OutDev& O, WReq& q,
     q.path0 = q.path1 = -1;
     w->pod_srv[lane] = -1;
     if (lane == 0) { w->nos = 0; w->nol = 0; }
-    for (int i = lane; i < c.nDW; i += 32) c.dirty[i] = 0u;
+    for (int i = lane; i < c.nDW; i += 32) c.w->dirty[i] = 0u;
     __syncwarp();
     return true;
   }
@@ -1152,13 +1155,12 @@ __global__ void __launch_bounds__(512, 1) k_batch_warp(Geo g, Opt o, const int* 
   const int npad = (n + 127) & ~127, nch = npad >> 7;
   // ---- a0: shared snapshot (read-only for the whole kernel): the chunk layout of the
   // criteria and the chunk table (k_warp_layout), the fabric links in switch order
-  int* ssnap = reinterpret_cast<int*>(dyn);
+  // per-warp scratch first (a compile-time stride), then the snapshot
+  int* ssnap = reinterpret_cast<int*>(dyn + sizeof(WScr) * WWARPS);
   ChunkT* stab = reinterpret_cast<ChunkT*>(ssnap + 4 * npad);
   LT* sfab = reinterpret_cast<LT*>(stab + nch);
   const int nfab = E * h + k * h * h;
-  size_t off = (size_t)16 * npad + sizeof(ChunkT) * nch + (((size_t)sizeof(LT) * nfab + 15) & ~(size_t)15);
-  const int nDW = (E + k * h + 31) >> 5, nEW = (E + 31) >> 5;
-  const size_t wbytes = ((sizeof(WScr) + 4 * (nDW + nEW + k)) + 15) & ~(size_t)15;
+  const int nDW = (E + k * h + 31) >> 5;
   __shared__ __align__(8) unsigned long long mbar;
   __shared__ int s_fabmin;
   // criteria tiles and chunk table are contiguous in `lay` and in shared memory: TMA bulk
@@ -1172,7 +1174,7 @@ __global__ void __launch_bounds__(512, 1) k_batch_warp(Geo g, Opt o, const int* 
     for (unsigned o2 = 0; o2 < bytes; o2 += chunk) {
       const unsigned sz = bytes - o2 < chunk ? bytes - o2 : chunk;
       asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                       smem_addr(dyn) + o2),
+                       smem_addr(ssnap) + o2),
                    "l"(reinterpret_cast<const unsigned char*>(lay + LAY_PST) + o2), "r"(sz), "r"(mb)
                    : "memory");
     }
@@ -1211,12 +1213,7 @@ __global__ void __launch_bounds__(512, 1) k_batch_warp(Geo g, Opt o, const int* 
   c.nch = nch;
   c.a_snap = smem_addr(ssnap) + 16u * lane;
   c.fab = sfab;
-  unsigned char* wb = dyn + off + (size_t)warp * wbytes;
-  c.w = reinterpret_cast<WScr*>(wb);
-  c.dirty = reinterpret_cast<unsigned*>(wb + sizeof(WScr));
-  c.edgebad = c.dirty + nDW;
-  c.pm = c.edgebad + nEW;
-  c.a_edge = smem_addr(c.edgebad);
+  c.w = reinterpret_cast<WScr*>(dyn) + warp;
   c.nDW = nDW;
   c.fabmin = s_fabmin;
   c.ulog = ulog_all + ((size_t)blockIdx.x * (blockDim.x >> 5) + warp) * WLOG;
@@ -1540,20 +1537,17 @@ size_t warp_layout_ints(const Geo& g) {
   size_t npad = (size_t)((g.n + 127) & ~127);
   return LAY_PST + 4 * npad + 16 * (npad >> 7) + (size_t)g.n;
 }
-static size_t warp_scratch_bytes(const Geo& g) {
-  int nDW = (g.E + g.k * g.h + 31) >> 5, nEW = (g.E + 31) >> 5;
-  return ((sizeof(WScr) + 4 * (size_t)(nDW + nEW + g.k)) + 15) & ~(size_t)15;
-}
 
 int warp_kernel_warps(const Geo& g) {
   int dev = 0, optin = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   bool u16 = g.link_cap <= 65535;
-  size_t snap = warp_snapshot_bytes(g, u16), per = warp_scratch_bytes(g);
-  if (snap + 4 * per + 64 > (size_t)optin || ((g.n + 127) >> 7) > 128) return 0;
-  int W = (int)(((size_t)optin - snap - 64) / per);
-  return W > 16 ? 16 : W;
+  // dynamic shared memory: WWARPS per-warp scratch areas + the snapshot (+ static words)
+  const size_t stat = sizeof(WScr) * WWARPS + 64;
+  if (warp_snapshot_bytes(g, u16) + stat > (size_t)optin || ((g.n + 127) >> 7) > 128) return 0;
+  if (g.E > 32 * WEW || g.E + g.k * g.h > 32 * WDW || g.k > 64) return 0;
+  return WWARPS;
 }
 
 size_t warp_ulog_entries(int grid, int warps) { return (size_t)grid * warps * WLOG; }
@@ -1583,7 +1577,7 @@ cudaError_t launch_batch_warp(const Geo& g, const Opt& o, const int* d_state, in
     const char* e = getenv("NACS_WARP_SYNC");
     return e ? atoi(e) : 3;
   }();
-  size_t smem = warp_snapshot_bytes(g, u16) + (size_t)warps * warp_scratch_bytes(g);
+  size_t smem = warp_snapshot_bytes(g, u16) + sizeof(WScr) * WWARPS;
   if (u16) {
     cudaFuncSetAttribute(k_batch_warp<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_batch_warp<uint16_t><<<grid, warps * 32, smem, st>>>(g, o, d_state, lay, R, O, ulog, next, order, deferred,
