@@ -2071,7 +2071,8 @@ int batch_block_size(const Geo& g, int method) {
   if (method == 0) {  // AHP: a warp per level pair in the passes
     const char* e = getenv("NACS_AHP_BLOCK");
     if (e) return atoi(e);
-    int b = next_pow2(g.n / 4);
+    // about one (l, K-1-l) level pair per thread in the passes when K ~ n_f ~ n (C3: 512)
+    int b = next_pow2(g.n / 2);
     return b < 128 ? 128 : (b > 512 ? 512 : b);
   }
   int b = ((g.n / 8 + 31) / 32) * 32;  // about 8 servers per thread
