@@ -269,11 +269,12 @@ def run_ours(args, rank, world, local):
     if not args.no_e2e:
         snap, reqs = topsis["snap"], topsis["reqs"]
         ctx.load_topology(snap)
-        ctx.schedule_batch(reqs, "topsis", "flat")
+        hout = ctx._alloc_out(reqs, False)[0]  # caller-allocated host outputs, reused per step
+        ctx.schedule_batch(reqs, "topsis", "flat", out=hout)
         barrier()
         t = time.perf_counter()
         for _ in range(args.steps):
-            ctx.schedule_batch(reqs, "topsis", "flat")
+            ctx.schedule_batch(reqs, "topsis", "flat", out=hout)
         torch.cuda.synchronize(dev)
         el = max_over_ranks(time.perf_counter() - t)
         R = reqs["n_requests"]

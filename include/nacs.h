@@ -102,8 +102,10 @@ typedef struct {
 
 /* Outputs M_c, M_ec, c^a, bw^a (Table 2), caller-allocated, sized like
  * the request arrays.  status: 1 accepted, 0 rejected (no feasible server for a pod,
- * R20), -1 invalid request (only reported this way with NACS_DEVICE_PTRS; host-pointer
- * calls return NACS_EINVAL instead).  A non-accepted request has all mappings -1 and all
+ * R20), -1 invalid request (device-pointer calls and host-pointer nacs_schedule_batch
+ * calls, which validate on the host while the kernels run and then also return
+ * NACS_EINVAL / NACS_ETOOBIG naming the first invalid requests; host-pointer
+ * nacs_schedule_request calls validate first and return the error before any work).  A non-accepted request has all mappings -1 and all
  * allocations 0.  path_of_vlink: -1 intra-server; 0 same edge switch; 1+a via
  * aggregation switch a of the shared pod; 1+h+a*h+b via core switch (a,b). */
 typedef struct {

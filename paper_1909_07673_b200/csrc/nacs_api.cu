@@ -7,6 +7,11 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <chrono>
+#include <condition_variable>
+#include <functional>
+#include <mutex>
+#include <thread>
 #include <vector>
 
 #include <nccl.h>
@@ -40,16 +45,18 @@ struct DevArr {
   }
 };
 
-struct PinArr {
+struct PinArr {  // page-locked, mapped: dp is the device view (zero-copy outputs)
   unsigned char* p = nullptr;
+  unsigned char* dp = nullptr;
   size_t cap = 0;
   cudaError_t reserve(size_t n) {
     if (n <= cap) return cudaSuccess;
     if (p) cudaFreeHost(p);
-    p = nullptr;
+    p = dp = nullptr;
     cap = 0;
     size_t m = n + n / 4 + 4096;
-    cudaError_t e = cudaMallocHost(&p, m);
+    cudaError_t e = cudaHostAlloc(reinterpret_cast<void**>(&p), m, cudaHostAllocMapped);
+    if (e == cudaSuccess) e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&dp), p, 0);
     if (e == cudaSuccess) cap = m;
     return e;
   }
@@ -139,7 +146,95 @@ nacs_status check_options(nacs_ctx* ctx, const nacs_options* o, Opt* out) {
 }
 
 // Host-side validation of a host-pointer CSR batch (R24).  Lists every violation.
-nacs_status check_requests_host(nacs_ctx* ctx, const nacs_requests* q, int* C_out, int* V_out) {
+// Host-side work of the host-pointer path (validation, staging copies) split over up to 16
+// threads: at C4 a batch is 42 MB in and 24 MB out, which one core copies at ~10 GB/s.
+static int host_threads(size_t work, size_t grain) {
+  const unsigned hw = std::thread::hardware_concurrency();
+  size_t t = work / grain;
+  if (t > 16) t = 16;
+  if (t > hw && hw > 0) t = hw;
+  return t < 1 ? 1 : (int)t;
+}
+// A process-wide pool of 15 host workers (created on first use; dispatches serialised).
+class HostPool {
+ public:
+  static HostPool& get() {
+    static HostPool* pool = new HostPool(15);  // never destroyed: workers live with the process
+    return *pool;
+  }
+  // job(t) for t in [0, nt), nt <= 16; the caller runs t = 0
+  void run(int nt, const std::function<void(int)>& job) {
+    std::lock_guard<std::mutex> call(call_mu_);
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      job_ = &job;
+      want_ = nt - 1;
+      done_ = 0;
+      ++gen_;
+    }
+    cv_.notify_all();
+    job(0);
+    std::unique_lock<std::mutex> lk(mu_);
+    done_cv_.wait(lk, [&] { return done_ == want_; });
+    job_ = nullptr;
+  }
+
+ private:
+  explicit HostPool(int n) {
+    for (int i = 0; i < n; ++i) std::thread([this, i] { loop(i + 1); }).detach();
+  }
+  void loop(int id) {
+    unsigned long long seen = 0;
+    for (;;) {
+      const std::function<void(int)>* job;
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return gen_ != seen; });
+        seen = gen_;
+        if (id > want_) continue;
+        job = job_;
+      }
+      (*job)(id);
+      {
+        std::lock_guard<std::mutex> lk(mu_);
+        ++done_;
+      }
+      done_cv_.notify_one();
+    }
+  }
+  std::mutex call_mu_, mu_;
+  std::condition_variable cv_, done_cv_;
+  const std::function<void(int)>* job_ = nullptr;
+  int want_ = 0, done_ = 0;
+  unsigned long long gen_ = 0;
+};
+
+template <typename F>
+static void parallel_ranges(size_t n, int nt, F fn) {  // fn(thread, begin, end), contiguous ranges
+  if (nt <= 1) { fn(0, (size_t)0, n); return; }
+  HostPool::get().run(nt, [&](int t) { fn(t, n * t / nt, n * (t + 1) / nt); });
+}
+struct CopyJob {
+  void* dst;
+  const void* src;
+  size_t bytes;
+};
+// The jobs as one concatenated byte range split evenly over the threads.
+static void parallel_copies(const std::vector<CopyJob>& jobs) {
+  size_t total = 0;
+  for (auto& j : jobs) total += j.bytes;
+  parallel_ranges(total, host_threads(total, (size_t)1 << 21), [&](int, size_t b, size_t e) {
+    size_t at = 0;
+    for (auto& j : jobs) {
+      const size_t lo = std::max(b, at), hi = std::min(e, at + j.bytes);
+      if (lo < hi) std::memcpy(static_cast<char*>(j.dst) + (lo - at), static_cast<const char*>(j.src) + (lo - at), hi - lo);
+      at += j.bytes;
+    }
+  });
+}
+
+// Structure of a host CSR batch (NULL arrays, offsets): what sizing the copies needs.
+nacs_status check_offsets_host(nacs_ctx* ctx, const nacs_requests* q, int* C_out, int* V_out) {
   if (!q) return fail(ctx, NACS_EINVAL, "requests: NULL");
   if (q->n_requests < 0) return fail(ctx, NACS_EINVAL, "requests.n_requests < 0");
   int R = q->n_requests;
@@ -149,45 +244,71 @@ nacs_status check_requests_host(nacs_ctx* ctx, const nacs_requests* q, int* C_ou
     return fail(ctx, NACS_EINVAL, "requests: NULL array");
   if (q->container_off[0] != 0 || q->vlink_off[0] != 0)
     return fail(ctx, NACS_EINVAL, "requests: offsets must start at 0");
+  for (int r = 0; r < R; ++r) {  // offsets first (they size every array)
+    if (q->container_off[r + 1] < q->container_off[r] || q->vlink_off[r + 1] < q->vlink_off[r])
+      return fail(ctx, NACS_EINVAL, "request " + std::to_string(r) + ": decreasing offsets");
+  }
+  if (q->vlink_off[R] > 0 && (!q->vl_src || !q->vl_dst || !q->bw_min || !q->bw_max))
+    return fail(ctx, NACS_EINVAL, "requests: NULL vlink array");
+  *C_out = q->container_off[R];
+  *V_out = q->vlink_off[R];
+  return NACS_OK;
+}
+
+// Every request of a host batch (R24, sizes), in parallel; the messages name the first
+// invalid requests in request order.  Call after check_offsets_host.
+nacs_status validate_requests_host(nacs_ctx* ctx, const nacs_requests* q) {
+  const int R = q->n_requests;
+  const int nt = host_threads((size_t)R, 4096);
+  struct Part {
+    int nbad = 0;
+    bool big = false;
+    std::string m;
+  };
+  std::vector<Part> parts(nt);
+  parallel_ranges((size_t)R, nt, [&](int t, size_t rb, size_t re) {
+    Part& P = parts[t];
+    for (int r = (int)rb; r < (int)re; ++r) {
+      const int c0 = q->container_off[r], c1 = q->container_off[r + 1];
+      const int v0 = q->vlink_off[r], v1 = q->vlink_off[r + 1];
+      const int bad = nacs::validate_request(c1 - c0, v1 - v0, q->cpu_min + c0, q->cpu_max + c0, q->ram_min + c0,
+                                             q->ram_max + c0, q->pod_of + c0, q->vl_src + v0, q->vl_dst + v0,
+                                             q->bw_min + v0, q->bw_max + v0);
+      if (!bad) continue;
+      ++P.nbad;
+      if (bad & 1) P.big = true;
+      if (P.nbad <= 32) {
+        P.m += "request " + std::to_string(r) + ":";
+        if (bad & 1) P.m += " size (containers 1.." + std::to_string(nacs::MAXC) + ", vlinks <= " +
+                            std::to_string(nacs::MAXV) + ")";
+        if (bad & 2) P.m += " non-positive c^min";
+        if (bad & 4) P.m += " c^min > c^max";
+        if (bad & 8) P.m += " pod ids not 0..P-1";
+        if (bad & 16) P.m += " vlink endpoint out of range or self-loop";
+        if (bad & 32) P.m += " bw^min <= 0 or bw^min > bw^max";
+        P.m += "; ";
+      }
+    }
+  });
   std::string m;
   int nbad = 0;
   bool big = false;
-  for (int r = 0; r < R; ++r) {
-    int c0 = q->container_off[r], c1 = q->container_off[r + 1];
-    int v0 = q->vlink_off[r], v1 = q->vlink_off[r + 1];
-    if (c1 < c0 || v1 < v0) {
-      m += "request " + std::to_string(r) + ": decreasing offsets; ";
-      ++nbad;
-      break;
-    }
-    if (v1 > v0 && (!q->vl_src || !q->vl_dst || !q->bw_min || !q->bw_max))
-      return fail(ctx, NACS_EINVAL, "requests: NULL vlink array");
-    int bad = nacs::validate_request(c1 - c0, v1 - v0, q->cpu_min + c0, q->cpu_max + c0, q->ram_min + c0,
-                                     q->ram_max + c0, q->pod_of + c0, q->vl_src + v0, q->vl_dst + v0,
-                                     q->bw_min + v0, q->bw_max + v0);
-    if (bad) {
-      ++nbad;
-      if (bad == 1) big = true;
-      if (nbad <= 32) {
-        m += "request " + std::to_string(r) + ":";
-        if (bad & 1) m += " size (containers 1.." + std::to_string(nacs::MAXC) + ", vlinks <= " +
-                          std::to_string(nacs::MAXV) + ")";
-        if (bad & 2) m += " non-positive c^min";
-        if (bad & 4) m += " c^min > c^max";
-        if (bad & 8) m += " pod ids not 0..P-1";
-        if (bad & 16) m += " vlink endpoint out of range or self-loop";
-        if (bad & 32) m += " bw^min <= 0 or bw^min > bw^max";
-        m += "; ";
-      }
-    }
+  for (auto& P : parts) {  // messages of the first invalid requests, in request order
+    if (nbad < 32) m += P.m;
+    nbad += P.nbad;
+    big |= P.big;
   }
   if (nbad) {
     if (nbad > 32) m += "... " + std::to_string(nbad) + " invalid requests in total";
     return fail(ctx, big ? NACS_ETOOBIG : NACS_EINVAL, m);
   }
-  *C_out = q->container_off[R];
-  *V_out = q->vlink_off[R];
   return NACS_OK;
+}
+
+nacs_status check_requests_host(nacs_ctx* ctx, const nacs_requests* q, int* C_out, int* V_out) {
+  nacs_status st = check_offsets_host(ctx, q, C_out, V_out);
+  if (st || q->n_requests == 0) return st;
+  return validate_requests_host(ctx, q);
 }
 
 nacs_status check_placements(nacs_ctx* ctx, const nacs_placements* o) {
@@ -205,9 +326,10 @@ nacs_status stage_requests(nacs_ctx* ctx, const nacs_requests* q, int C, int V, 
   CK(ctx->req_in.reserve(words));
   int* h = reinterpret_cast<int*>(ctx->pin_in.p);
   size_t o = 0;
+  std::vector<CopyJob> jobs;
   auto put = [&](const int32_t* src, size_t n) {
     size_t at = o;
-    if (n) std::memcpy(h + o, src, n * 4);
+    if (n) jobs.push_back({h + o, src, n * 4});
     o += n;
     return at;
   };
@@ -215,7 +337,22 @@ nacs_status stage_requests(nacs_ctx* ctx, const nacs_requests* q, int C, int V, 
   size_t a_cmin = put(q->cpu_min, C), a_cmax = put(q->cpu_max, C), a_rmin = put(q->ram_min, C);
   size_t a_rmax = put(q->ram_max, C), a_pod = put(q->pod_of, C);
   size_t a_src = put(q->vl_src, V), a_dst = put(q->vl_dst, V), a_bmin = put(q->bw_min, V), a_bmax = put(q->bw_max, V);
-  CK(cudaMemcpyAsync(ctx->req_in.p, h, words * 4, cudaMemcpyHostToDevice, ctx->stream));
+  // in 4 pieces: the copy engine moves piece i while the host threads fill piece i + 1
+  const size_t total = words * 4, piece = ((total / 4) + 4095) & ~(size_t)4095;
+  for (size_t b = 0; b < total; b += piece) {
+    const size_t e = std::min(total, b + piece);
+    std::vector<CopyJob> part;
+    size_t at = 0;
+    for (auto& j : jobs) {
+      const size_t lo = std::max(b, at), hi = std::min(e, at + j.bytes);
+      if (lo < hi)
+        part.push_back({static_cast<char*>(j.dst) + (lo - at), static_cast<const char*>(j.src) + (lo - at), hi - lo});
+      at += j.bytes;
+    }
+    parallel_copies(part);
+    CK(cudaMemcpyAsync(reinterpret_cast<char*>(ctx->req_in.p) + b, reinterpret_cast<const char*>(h) + b, e - b,
+                       cudaMemcpyHostToDevice, ctx->stream));
+  }
   int* d = ctx->req_in.p;
   R->n = Rn;
   R->coff = d + a_coff;
@@ -262,18 +399,42 @@ nacs_status device_outputs(nacs_ctx* ctx, int R, int C, int V, nacs::OutDev* O) 
   return NACS_OK;
 }
 
+// Outputs straight into mapped page-locked memory (the kernels write them over the bus as
+// requests finish; no device-to-host copy after the kernels).
+nacs_status mapped_outputs(nacs_ctx* ctx, int R, int C, int V, nacs::OutDev* O) {
+  size_t words = (size_t)R + 3 * (size_t)C + 2 * (size_t)V;
+  CK(ctx->pin_out.reserve(words * 4 + 4));
+  int* d = reinterpret_cast<int*>(ctx->pin_out.dp);
+  O->status = d;
+  O->server = d + R;
+  O->cpu_a = d + R + C;
+  O->ram_a = d + R + 2 * (size_t)C;
+  O->bw_a = d + R + 3 * (size_t)C;
+  O->path = d + R + 3 * (size_t)C + V;
+  return NACS_OK;
+}
+void copy_mapped_outputs(nacs_ctx* ctx, int R, int C, int V, nacs_placements* out) {
+  const int* h = reinterpret_cast<const int*>(ctx->pin_out.p);
+  parallel_copies({{out->status, h, (size_t)R * 4},
+                   {out->server_of_container, h + R, (size_t)C * 4},
+                   {out->cpu_alloc, h + R + C, (size_t)C * 4},
+                   {out->ram_alloc, h + R + 2 * (size_t)C, (size_t)C * 4},
+                   {out->bw_alloc, h + R + 3 * (size_t)C, (size_t)V * 4},
+                   {out->path_of_vlink, h + R + 3 * (size_t)C + V, (size_t)V * 4}});
+}
+
 nacs_status unstage_outputs(nacs_ctx* ctx, int R, int C, int V, nacs_placements* out) {
   size_t words = (size_t)R + 3 * (size_t)C + 2 * (size_t)V;
   CK(ctx->pin_out.reserve(words * 4 + 4));
   CK(cudaMemcpyAsync(ctx->pin_out.p, ctx->req_out.p, words * 4, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   const int* h = reinterpret_cast<const int*>(ctx->pin_out.p);
-  std::memcpy(out->status, h, (size_t)R * 4);
-  std::memcpy(out->server_of_container, h + R, (size_t)C * 4);
-  std::memcpy(out->cpu_alloc, h + R + C, (size_t)C * 4);
-  std::memcpy(out->ram_alloc, h + R + 2 * (size_t)C, (size_t)C * 4);
-  std::memcpy(out->bw_alloc, h + R + 3 * (size_t)C, (size_t)V * 4);
-  std::memcpy(out->path_of_vlink, h + R + 3 * (size_t)C + V, (size_t)V * 4);
+  parallel_copies({{out->status, h, (size_t)R * 4},
+                   {out->server_of_container, h + R, (size_t)C * 4},
+                   {out->cpu_alloc, h + R + C, (size_t)C * 4},
+                   {out->ram_alloc, h + R + 2 * (size_t)C, (size_t)C * 4},
+                   {out->bw_alloc, h + R + 3 * (size_t)C, (size_t)V * 4},
+                   {out->path_of_vlink, h + R + 3 * (size_t)C + V, (size_t)V * 4}});
   return NACS_OK;
 }
 
@@ -701,10 +862,19 @@ nacs_status nacs_schedule_batch(nacs_ctx* ctx, const nacs_options* opt, const na
   nacs::ReqsDev Rd;
   nacs::OutDev Od;
   int C = 0, V = 0;
-  if (!dev) {
-    if ((st = check_requests_host(ctx, batch, &C, &V))) return st;
+  static const bool timing = getenv("NACS_HOST_TIMING") != nullptr;
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  auto ms = [](std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point b) {
+    return std::chrono::duration<double, std::milli>(b - a).count();
+  };
+  const auto t0 = now();
+  auto t1 = t0, t2 = t0;
+  if (!dev) {  // R24 validation of every request runs on the host while the kernels run
+    if ((st = check_offsets_host(ctx, batch, &C, &V))) return st;
+    t1 = now();
     if ((st = stage_requests(ctx, batch, C, V, &Rd))) return st;
-    if ((st = device_outputs(ctx, R, C, V, &Od))) return st;
+    if ((st = mapped_outputs(ctx, R, C, V, &Od))) return st;
+    t2 = now();
   } else {
     Rd = device_requests(batch);
     Od.status = out->status;
@@ -739,7 +909,19 @@ nacs_status nacs_schedule_batch(nacs_ctx* ctx, const nacs_options* opt, const na
                           ctx->stream));
   }
   if (!dev) {
-    if ((st = unstage_outputs(ctx, R, C, V, out))) return st;
+    const auto t3 = now();
+    const nacs_status vst = validate_requests_host(ctx, batch);
+    const auto t4 = now();
+    CK(cudaStreamSynchronize(ctx->stream));
+    const auto t5 = now();
+    copy_mapped_outputs(ctx, R, C, V, out);
+    if (timing)
+      fprintf(stderr, "nacs host timing ms: offsets %.3f stage %.3f launch %.3f validate %.3f wait %.3f unstage %.3f\n",
+              ms(t0, t1), ms(t1, t2), ms(t2, t3), ms(t3, t4), ms(t4, t5), ms(t5, now()));
+    if (vst) {  // invalid requests carry status -1 in the outputs; the call reports them
+      if (!(opt->flags & NACS_ASYNC)) finish_stats(ctx);
+      return vst;
+    }
   }
   if (!(opt->flags & NACS_ASYNC)) {
     CK(cudaStreamSynchronize(ctx->stream));
