@@ -112,6 +112,7 @@ struct Opts {
   int ahp_rule;     // 0 literal (R8), 1 shifted
   int l1_mode;      // 0 pairwise comparison on W (R10), 1 L1 = W
   int path_filter;  // 1 filter on paths (R6), 0 paper-literal select-then-route
+  int rank_once;    // 0 re-rank every pod step (R15); 1 rank once per request (R25)
 };
 
 // AHP pairwise cell for a scaled difference d (reading R8).
@@ -335,6 +336,12 @@ Placement schedule_one(DC& dc, const Opts& o, const Req& q, const int32_t* hint,
   DC saved = dc;  // for the atomic rollback of a rejected request (R20)
   std::vector<int> srv(P, -1);
   std::vector<int> vpath(q.nV, -1);
+  // R25 (rank once, "the resulting array is sorted on decreasing
+  // order"): the ranking of the request's first pod step (pod 0, no flows, the
+  // state at request start) orders the servers once; every pod step takes the first
+  // server of that order that its own filter (R6, current residuals) admits.
+  RankOut r0;
+  if (o.rank_once) r0 = rank(dc, o, pcpu[0], pram[0], std::vector<Flow>(), std::vector<int>());
 
   for (int p = 0; p < P; ++p) {  // pods in ascending id (R15)
     std::vector<int> excluded;
@@ -354,6 +361,15 @@ Placement schedule_one(DC& dc, const Opts& o, const Req& q, const int32_t* hint,
       RankOut r = rank(dc, o, pcpu[p], pram[p], flows, excluded);
       cnt.pod_steps += 1;
       cnt.servers_ranked += dc.n;
+      if (o.rank_once) {  // walk the request's order: best pod-0 score among the admitted servers
+        int b = -1;
+        for (int u = 0; u < dc.n; ++u)
+          if (r.mask[u] && r0.mask[u] && (b < 0 || r0.score[u] > r0.score[b])) b = u;
+        r.best = b;
+        for (int u = 0; u < dc.n; ++u)
+          r.tie[u] = b >= 0 && r.mask[u] && r0.mask[u] &&
+                     r0.score[u] >= r0.score[b] - 1e-9 * std::fabs(r0.score[b]);
+      }
       if (r.best < 0) {  // F empty: reject the whole request (R20)
         dc = saved;
         pl.status = 0;
@@ -466,8 +482,9 @@ DC make_dc(int k, int cpu_cap, int ram_cap, int link_cap, const int32_t* cpu, co
   return dc;
 }
 
-Opts make_opts(int method, const double* w, int ahp_rule, int l1_mode, int path_filter) {
+Opts make_opts(int method, const double* w, int ahp_rule, int l1_mode, int path_filter, int rank_once = 0) {
   Opts o;
+  o.rank_once = rank_once;
   o.method = method;
   for (int c = 0; c < 4; ++c) o.w[c] = w[c];
   o.ahp_rule = ahp_rule;
@@ -533,14 +550,14 @@ int orc_widest_path(int k, const int32_t* link, int u, int v, double* fabric_out
 // counters: [pod_steps, retries, excused_ties, hint_mismatch, servers_ranked].
 int orc_schedule(int k, int cpu_cap, int ram_cap, int link_cap, int32_t* cpu, int32_t* ram, uint8_t* active,
                  int32_t* link, int method, const double* w, int ahp_rule, int l1_mode, int path_filter,
-                 int sequential, int n_req, const int32_t* coff, const int32_t* cpu_min,
+                 int rank_once, int sequential, int n_req, const int32_t* coff, const int32_t* cpu_min,
                  const int32_t* cpu_max, const int32_t* ram_min, const int32_t* ram_max,
                  const int32_t* pod_of, const int32_t* voff, const int32_t* vsrc, const int32_t* vdst,
                  const int32_t* bw_min, const int32_t* bw_max, const int32_t* hint, int32_t* status,
                  int32_t* server, int32_t* cpu_a, int32_t* ram_a, int32_t* bw_a, int32_t* path,
                  int64_t* counters, int nthreads) {
   DC base = make_dc(k, cpu_cap, ram_cap, link_cap, cpu, ram, active, link);
-  Opts o = make_opts(method, w, ahp_rule, l1_mode, path_filter);
+  Opts o = make_opts(method, w, ahp_rule, l1_mode, path_filter, rank_once);
   auto mkreq = [&](int r) {
     Req q;
     q.nC = coff[r + 1] - coff[r];

@@ -48,7 +48,7 @@ def lib():
         _lib.orc_widest_path.argtypes = [C.c_int, P, C.c_int, C.c_int, P, P, P]
         _lib.orc_schedule.restype = C.c_int
         _lib.orc_schedule.argtypes = [C.c_int] * 4 + [P] * 4 + [C.c_int, P, C.c_int, C.c_int, C.c_int,
-                                                          C.c_int, C.c_int] + [P] * 19 + [C.c_int]
+                                                          C.c_int, C.c_int, C.c_int] + [P] * 19 + [C.c_int]
     return _lib
 
 
@@ -113,8 +113,10 @@ def widest_path(k: int, link_res, u: int, v: int):
 
 
 def schedule(snap: dict, reqs: dict, method: str, weights, sequential: bool, hint=None,
-             ahp_rule: int = 0, l1_mode: int = 0, path_filter: int = 1, nthreads: int | None = None):
+             ahp_rule: int = 0, l1_mode: int = 0, path_filter: int = 1, nthreads: int | None = None,
+             rank_once: bool = False):
     """Schedule a CSR batch.  Returns (placements, counters, final_state).
+    rank_once: R25 (rank once per request, pods walk the order) instead of R15.
 
     final_state is the state after the batch (sequential) or the unchanged snapshot (batch).
     counters: pod_steps, retries, excused_ties, hint_mismatch, servers_ranked.
@@ -137,7 +139,8 @@ def schedule(snap: dict, reqs: dict, method: str, weights, sequential: bool, hin
         nthreads = len(os.sched_getaffinity(0))
     w = _weights(weights)
     lib().orc_schedule(k, snap["cpu_cap"], snap["ram_cap"], snap["link_cap"], _p(cpu), _p(ram), _p(act),
-                       _p(link), METHOD[method], _p(w), ahp_rule, l1_mode, path_filter, int(sequential), R,
+                       _p(link), METHOD[method], _p(w), ahp_rule, l1_mode, path_filter, int(rank_once),
+                       int(sequential), R,
                        _p(arr["container_off"]), _p(arr["cpu_min"]), _p(arr["cpu_max"]), _p(arr["ram_min"]),
                        _p(arr["ram_max"]), _p(arr["pod_of"]), _p(arr["vlink_off"]), _p(arr["vl_src"]),
                        _p(arr["vl_dst"]), _p(arr["bw_min"]), _p(arr["bw_max"]), _p(hint_a), _p(out["status"]),

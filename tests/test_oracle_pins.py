@@ -278,6 +278,68 @@ def test_fresh_dc_first_pod_on_server_0():
         assert out["status"][0] == 1 and out["server_of_container"][0] == 0
 
 
+def _request(cpu, ram, pods, vlinks=()):
+    """One CSR request: per-container (cpu, ram) with c^min = c^max, pod ids, vlinks (src, dst, bw)."""
+    nC, nV = len(cpu), len(vlinks)
+    i32 = lambda x: np.asarray(x, np.int32)
+    return {"n_requests": 1, "container_off": i32([0, nC]), "cpu_min": i32(cpu), "cpu_max": i32(cpu),
+            "ram_min": i32(ram), "ram_max": i32(ram), "pod_of": i32(pods), "vlink_off": i32([0, nV]),
+            "vl_src": i32([v[0] for v in vlinks]), "vl_dst": i32([v[1] for v in vlinks]),
+            "bw_min": i32([v[2] for v in vlinks]), "bw_max": i32([v[2] for v in vlinks])}
+
+
+def test_rank_once_fresh_dc_colocates_on_rank_1():
+    """R25: a request that fits on the rank-1 server goes there
+    whole: on a fresh DC every server scores the same, server 0 is first in the order and stays
+    admissible for every pod."""
+    s = gen.snapshot(4, warm=False)
+    req = _request([1000, 1500, 800, 1200, 900], [1024, 2048, 512, 1024, 4096], [0, 0, 1, 2, 2],
+                   [(0, 2, 10), (2, 3, 5), (1, 4, 20)])
+    for m in ("ahp", "topsis"):
+        out, _, state = O.schedule(s, req, m, "flat", sequential=True, rank_once=True)
+        assert out["status"][0] == 1 and (out["server_of_container"] == 0).all()
+        assert (out["path_of_vlink"] == -1).all() and (out["bw_alloc"] == [10, 5, 20]).all()
+        assert state["cpu_res"][0] == 24000 - 5400
+
+
+def test_rank_once_walks_the_order_across_a_dominating_class():
+    """R25 on two server classes: A (servers 0-3) dominates B in every criterion, so the order is
+    A by index, then B (TOPSIS closeness 1 / 0, AHP by dominance).  Six single-container pods of
+    2000 mc walk it first-fit: each A server takes two pods (5000 mc), in index order."""
+    s = gen.snapshot(4, warm=False)
+    for u in range(16):
+        a = u < 4
+        s["cpu_res"][u], s["ram_res"][u] = (5000, 50000) if a else (3000, 30000)
+        s["active"][u] = 1 if a else 0
+        s["link_res"][u] = 1000 if a else 500
+    req = _request([2000] * 6, [1000] * 6, list(range(6)))
+    for m in ("ahp", "topsis"):
+        out, _, _ = O.schedule(s, req, m, "flat", sequential=True, rank_once=True)
+        assert out["server_of_container"].tolist() == [0, 0, 1, 1, 2, 2], m
+
+
+@pytest.mark.parametrize("method", ["ahp", "topsis"])
+def test_rank_once_equals_per_pod_for_single_pod_requests(method):
+    """With one pod per request the first pod step's order is the only ranking: R25 = R15."""
+    snap, reqs = gen.config("C2")
+    one = dict(reqs, pod_of=np.zeros_like(reqs["pod_of"]))
+    a, _, sa = O.schedule(snap, one, method, "network", sequential=True)
+    b, _, sb = O.schedule(snap, one, method, "network", sequential=True, rank_once=True)
+    for key in a:
+        assert np.array_equal(a[key], b[key]), key
+    for key in ("cpu_res", "ram_res", "link_res"):
+        assert np.array_equal(sa[key], sb[key])
+
+
+@pytest.mark.parametrize("method", ["ahp", "topsis"])
+def test_rank_once_invariants(method):
+    snap, reqs = gen.config("C2")
+    out, _, state = O.schedule(snap, reqs, method, "flat", sequential=True, rank_once=True)
+    _check_invariants(snap, reqs, out, state, sequential=True)
+    outb, _, stb = O.schedule(snap, reqs, method, "flat", sequential=False, rank_once=True)
+    _check_invariants(snap, reqs, outb, stb, sequential=False)
+
+
 @pytest.mark.parametrize("alpha", [0.0, 0.5, 1.0])
 def test_c1_heuristic_is_milp_optimal(alpha):
     """SURVEY.md §8(c) C1 expectation: both methods and all schemas put the 3 pods on server 0,
