@@ -125,7 +125,14 @@ typedef struct {
   int32_t l1_mode;      /* 0 L1 = AHP pairwise priority of W (R10, default); 1 L1 = W */
   int32_t path_filter;  /* 1 filter on path bandwidth (R6, default); 0 CPU/RAM-only filter */
   uint32_t flags;       /* NACS_DEVICE_PTRS | NACS_ASYNC | NACS_EXACT_FP64 */
+  int32_t rank_mode;    /* NACS_RANK_PER_POD (R15, default): re-rank at every pod step;
+                         * NACS_RANK_ONCE (R25, "sorted on decreasing order"
+                         * P:375): the request's first pod step ranks the servers once and every
+                         * pod takes the first server of that order its own filter (R6) admits.
+                         * Schedule calls only; not on server-sharded contexts (NACS_EINVAL). */
 } nacs_options;
+
+enum { NACS_RANK_PER_POD = 0, NACS_RANK_ONCE = 1 };
 
 /* Counters of the last rank/schedule call (reading them synchronises the context stream). */
 typedef struct {

@@ -135,6 +135,7 @@ nacs_status check_options(nacs_ctx* ctx, const nacs_options* o, Opt* out) {
   if (o->l1_mode != 0 && o->l1_mode != 1) m += "options.l1_mode not 0/1; ";
   if (o->path_filter != 0 && o->path_filter != 1) m += "options.path_filter not 0/1; ";
   if (o->flags & ~(NACS_DEVICE_PTRS | NACS_ASYNC | NACS_EXACT_FP64)) m += "options.flags has unknown bits; ";
+  if (o->rank_mode != NACS_RANK_PER_POD && o->rank_mode != NACS_RANK_ONCE) m += "options.rank_mode not 0/1; ";
   if (!m.empty()) return fail(ctx, NACS_EINVAL, m);
   out->method = (int)o->method;
   for (int k = 0; k < 4; ++k) out->wd[k] = o->weights[k];
@@ -142,6 +143,7 @@ nacs_status check_options(nacs_ctx* ctx, const nacs_options* o, Opt* out) {
   out->l1_mode = o->l1_mode;
   out->path_filter = o->path_filter;
   out->exact64 = (o->flags & NACS_EXACT_FP64) ? 1 : 0;
+  out->rank_once = o->rank_mode == NACS_RANK_ONCE;
   return NACS_OK;
 }
 
@@ -890,10 +892,10 @@ nacs_status nacs_schedule_batch(nacs_ctx* ctx, const nacs_options* opt, const na
   int grid = ctx->num_sms * per_sm;
   if (grid > R) grid = R;
   CK(ctx->ulog.reserve((size_t)grid * nacs::ULOG_CAP));
-  if (o.method == 0) CK(ctx->w64.reserve((size_t)grid * nacs::ahp_workspace_doubles(g.n)));
+  if (o.method == 0 || o.rank_once) CK(ctx->w64.reserve((size_t)grid * nacs::ahp_workspace_doubles(g.n)));
   CK(ctx->misc.reserve(8));
   CK(cudaMemsetAsync(ctx->misc.p, 0, 4 * sizeof(int), ctx->stream));
-  const int warps = o.method == NACS_TOPSIS && !ctx->cta_only ? nacs::warp_kernel_warps(g) : 0;
+  const int warps = o.method == NACS_TOPSIS && !ctx->cta_only && !o.rank_once ? nacs::warp_kernel_warps(g) : 0;
   if (warps >= 4) {
     // fast path: warp per request; requests beyond its limits are deferred to k_batch
     int wgrid = ctx->num_sms;
@@ -970,7 +972,9 @@ nacs_status nacs_schedule_request(nacs_ctx* ctx, const nacs_options* opt, const 
     }
   }
   // the sharded engine: server-sharded contexts, and (grid-wide level passes) AHP on big topologies
-  if (ctx->world > 1 || ctx->comm || (o.method == NACS_AHP && g.n >= 4096)) {
+  if (o.rank_once && (ctx->world > 1 || ctx->comm))
+    return fail(ctx, NACS_EINVAL, "options.rank_mode = NACS_RANK_ONCE is not available on server-sharded contexts");
+  if (ctx->world > 1 || ctx->comm || (o.method == NACS_AHP && g.n >= 4096 && !o.rank_once)) {
     if ((st = schedule_sharded(ctx, o, Rd, Od, R))) return st;
     if (!dev) {
       if ((st = unstage_outputs(ctx, R, C, V, out))) return st;
@@ -982,10 +986,8 @@ nacs_status nacs_schedule_request(nacs_ctx* ctx, const nacs_options* opt, const 
     return NACS_OK;
   }
   CK(ctx->ulog.reserve(nacs::ULOG_CAP));
-  if (o.method == 0) {
-    CK(ctx->ahp_ws.reserve(nacs::ahp_workspace_bytes(g.n) / 4 + 4));
-    CK(ctx->w64.reserve(nacs::ahp_workspace_doubles(g.n)));
-  }
+  if (o.method == 0) CK(ctx->ahp_ws.reserve(nacs::ahp_workspace_bytes(g.n) / 4 + 4));
+  if (o.method == 0 || o.rank_once) CK(ctx->w64.reserve(nacs::ahp_workspace_doubles(g.n)));
   CK(nacs::launch_sequential(g, o, ctx->state.p, Rd, Od, ctx->ulog.p, ctx->ahp_ws.p, ctx->w64.p, ctx->stats.p,
                              ctx->stream));
   if (!dev) {

@@ -32,6 +32,7 @@ struct Opt {
   int l1_mode;       // 0 pairwise on W, 1 L1 = W
   int path_filter;   // 1 filter on path bandwidth, 0 CPU/RAM only
   int exact64;       // decide every argmax in FP64
+  int rank_once;     // R25: rank once per request (the first pod step's order), pods walk it
 };
 
 struct ReqsDev {

@@ -99,6 +99,7 @@ struct Ctx {
   const int* snap;     // global snapshot (k_batch) for reference
   Scratch* s;
   unsigned* maskw;     // [nW] feasibility bitmap of the current pod step
+  unsigned* f0w;       // [nW] R25: the feasible set of the request's first pod step
   unsigned* special;   // [nW] flow servers and excluded servers of the pod step
   unsigned* edgebad;   // [nEW] edge switches some flow cannot reach with its demand
   // AHP workspace (ahp_carve): presorted orders, sorted levels, prefix sums
@@ -519,14 +520,46 @@ __device__ void pass_filter(Ctx& c, uint8_t* mask_out, float* scores_out) {
 }
 
 // ------------------------------------------------------------ TOPSIS --------
+// R25 walk: the best exact (FP64) score of the request's first pod step among the servers
+// the current filter admits and that step admitted (scores in w64 + 2 n2, kept per request).
+__device__ __forceinline__ double* rank_once_scores(const Ctx& c) {
+  int n2 = 1;
+  while (n2 < c.g.n) n2 <<= 1;
+  return c.w64 + 2 * n2;  // after the AHP FP64 weights and level L2 (ahp_w64_doubles)
+}
+__device__ void rank_once_walk(Ctx& c) {
+  const int n = c.g.n;
+  const double* sc0 = rank_once_scores(c);
+  double bv = -DBL_MAX;
+  int bj = -1;
+  for (int u = c.tid; u < n; u += c.B) {
+    if (!(((c.maskw[u >> 5] & c.f0w[u >> 5]) >> (u & 31)) & 1u)) continue;
+    const double v = sc0[u];
+    if (v > bv || (v == bv && u < bj)) { bv = v; bj = u; }
+  }
+  block_argmax64(c, bv, bj);
+}
+
 template <bool WRITE_SCORES>
 __device__ void select_topsis(Ctx& c, float* scores_out) {
   Scratch* s = c.s;
   const int n = c.g.n;
   const int* st = c.st;
+  // R25: the first pod step ranks with its own statistics and keeps them with its feasible
+  // set; later pod steps take the best of that order among the servers their filter admits
+  if (c.o.rank_once && s->p > 0) {
+    rank_once_walk(c);
+    return;
+  }
   TopsisP tp;
   for (int k = 0; k < 4; ++k) { tp.mx[k] = s->mx[k]; tp.mn[k] = s->mn[k]; }
   topsis_params(tp, c.o.wd, s->sq);
+  if (c.o.rank_once) {  // keep the first pod step's feasible set and exact closeness
+    double* sc0 = rank_once_scores(c);
+    for (int w = c.tid; w < c.nW; w += c.B) c.f0w[w] = c.maskw[w];
+    for (int u = c.tid; u < n; u += c.B)
+      if ((c.maskw[u >> 5] >> (u & 31)) & 1u) sc0[u] = topsis64(tp, st[u], st[n + u], st[2 * n + u], st[3 * n + u]);
+  }
   unsigned long long k1 = 0, k2 = 0;
   for (int base = c.warp * 32; base < n; base += c.B) {
     unsigned bits = c.maskw[base >> 5];
@@ -540,8 +573,8 @@ __device__ void select_topsis(Ctx& c, float* scores_out) {
   if (c.tid == 0) {
     float s1 = __uint_as_float((unsigned)(s->key1 >> 32));
     float s2 = __uint_as_float((unsigned)(s->key2 >> 32));
-    s->best = (int)(0xFFFFFFFFu - (unsigned)(s->key1 & 0xFFFFFFFFull));
-    s->amb = c.o.exact64 || (s->key2 != 0ull && s1 - s2 <= kTopsisDelta);
+    s->best = s->key1 ? (int)(0xFFFFFFFFu - (unsigned)(s->key1 & 0xFFFFFFFFull)) : -1;
+    s->amb = s->key1 && (c.o.exact64 || (s->key2 != 0ull && s1 - s2 <= kTopsisDelta));
   }
   __syncthreads();
   if (s->amb) {  // FP64 re-decision over the near-max candidates (R14)
@@ -1010,6 +1043,12 @@ __device__ void select_ahp(Ctx& c, float* scores_out) {
   Scratch* s = c.s;
   const int n = c.g.n;
   const int nf = s->nf;
+  if (c.o.rank_once && s->p > 0) {  // R25: best FP64 priority of the first pod step, admitted now
+    rank_once_walk(c);
+    return;
+  }
+  if (c.o.rank_once)  // the first pod step keeps its feasible set and exact priorities
+    for (int w = c.tid; w < c.nW; w += c.B) c.f0w[w] = c.maskw[w];
   for (int u = c.tid; u < n; u += c.B) c.pg[u] = 0.0f;
   if (c.tid == 0) {
     for (int k = 0; k < 4; ++k) {
@@ -1049,7 +1088,7 @@ __device__ void select_ahp(Ctx& c, float* scores_out) {
     float s1 = __uint_as_float((unsigned)(s->key1 >> 32));
     float s2 = __uint_as_float((unsigned)(s->key2 >> 32));
     s->best = (int)(0xFFFFFFFFu - (unsigned)(s->key1 & 0xFFFFFFFFull));
-    s->amb = c.o.exact64 || (s->key2 != 0ull && s2 >= s1 * (1.0f - drel));
+    s->amb = c.o.exact64 || c.o.rank_once || (s->key2 != 0ull && s2 >= s1 * (1.0f - drel));
   }
   __syncthreads();
   if (s->amb) {  // FP64 re-decision (R14): the same level formulation in double, all of F
@@ -1356,6 +1395,10 @@ __device__ void run_request(Ctx& c, const ReqsDev& R, const OutDev& O, int r, bo
       }
       if (METHOD == 1) select_topsis<false>(c, nullptr);
       else select_ahp<false>(c, nullptr);
+      if (s->best < 0) {  // R25: no server of the request's order is admitted (R20)
+        req_reject(c, R, O, r);
+        return;
+      }
       if (c.warp == 0) commit(c, R, r, p);
       __syncthreads();
       if (!s->fail) break;
@@ -1439,13 +1482,13 @@ __global__ void __launch_bounds__(1024) k_batch(Geo g, Opt o, const int* __restr
   off = align16(off + sizeof(unsigned) * nW);
   c.special = reinterpret_cast<unsigned*>(dyn + off);
   off = align16(off + sizeof(unsigned) * nW);
+  c.f0w = reinterpret_cast<unsigned*>(dyn + off);
+  off = align16(off + sizeof(unsigned) * nW);
   c.edgebad = reinterpret_cast<unsigned*>(dyn + off);
   off = align16(off + sizeof(unsigned) * nEW);
   c.nfcap = n;
-  if (METHOD == 0) {
-    ahp_carve(c, dyn + off, n);
-    c.w64 = w64 + (size_t)blockIdx.x * ahp_w64_doubles(n);
-  }
+  if (METHOD == 0) ahp_carve(c, dyn + off, n);
+  if (w64) c.w64 = w64 + (size_t)blockIdx.x * ahp_w64_doubles(n);  // AHP FP64; R25 scores
   c.snap = snap;
   c.ulog = ulog + (size_t)blockIdx.x * ULOG_CAP;
 
@@ -1504,15 +1547,15 @@ __global__ void __launch_bounds__(1024) k_sequential(Geo g, Opt o, int* state, R
   off = align16(off + sizeof(unsigned) * c.nW);
   c.special = reinterpret_cast<unsigned*>(dyn + off);
   off = align16(off + sizeof(unsigned) * c.nW);
+  c.f0w = reinterpret_cast<unsigned*>(dyn + off);
+  off = align16(off + sizeof(unsigned) * c.nW);
   c.edgebad = reinterpret_cast<unsigned*>(dyn + off);
   c.st = state;
   c.snap = state;
   c.ulog = ulog;
   c.nfcap = g.n;
-  if (METHOD == 0) {
-    ahp_carve(c, reinterpret_cast<unsigned char*>(ahp_ws), g.n);
-    c.w64 = w64;
-  }
+  if (METHOD == 0) ahp_carve(c, reinterpret_cast<unsigned char*>(ahp_ws), g.n);
+  c.w64 = w64;
   for (int w = c.tid; w < c.nW; w += c.B) { c.maskw[w] = 0u; c.special[w] = 0u; }
   for (int w = c.tid; w < c.nEW; w += c.B) c.edgebad[w] = 0u;
   __syncthreads();
@@ -1531,6 +1574,8 @@ __global__ void __launch_bounds__(1024) k_rank(Geo g, Opt o, int* state, QueryDe
   c.maskw = reinterpret_cast<unsigned*>(dyn + off);
   off = align16(off + sizeof(unsigned) * c.nW);
   c.special = reinterpret_cast<unsigned*>(dyn + off);
+  off = align16(off + sizeof(unsigned) * c.nW);
+  c.f0w = reinterpret_cast<unsigned*>(dyn + off);
   off = align16(off + sizeof(unsigned) * c.nW);
   c.edgebad = reinterpret_cast<unsigned*>(dyn + off);
   c.st = state;
@@ -1608,6 +1653,7 @@ __device__ void sh_ctx(Ctx& c, const Geo& g, const Opt& o, int* state, const Sha
   c.snap = state;
   c.maskw = d.maskw;
   c.special = d.special;
+  c.f0w = nullptr;  // R25 is not available on the sharded engine
   c.edgebad = d.edgebad;
   c.ulog = d.ulog;
   c.nfcap = g.n;
@@ -2083,7 +2129,7 @@ int batch_block_size(const Geo& g, int method) {
 
 static size_t bitmap_bytes(const Geo& g) {
   int nW = (g.n + 31) / 32, nEW = (g.E + 31) / 32;
-  return align16(4 * (size_t)nW) * 2 + align16(4 * (size_t)nEW);
+  return align16(4 * (size_t)nW) * 3 + align16(4 * (size_t)nEW);
 }
 
 size_t batch_smem_bytes(const Geo& g, int method) {

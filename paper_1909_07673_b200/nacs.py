@@ -18,6 +18,7 @@ NACS_OK, NACS_EINVAL, NACS_ENOMEM, NACS_ECUDA, NACS_ENCCL, NACS_ENOTOPO, NACS_ET
 STATUS_NAMES = ["OK", "EINVAL", "ENOMEM", "ECUDA", "ENCCL", "ENOTOPO", "ETOOBIG"]
 NACS_AHP, NACS_TOPSIS = 0, 1
 NACS_DEVICE_PTRS, NACS_ASYNC, NACS_EXACT_FP64 = 1, 2, 4
+NACS_RANK_PER_POD, NACS_RANK_ONCE = 0, 1
 MAX_CONTAINERS, MAX_VLINKS, MAX_K = 128, 512, 64
 
 # Table 4: weights over (CPU, RAM, Fragmentation, Bandwidth)
@@ -57,7 +58,8 @@ class Placements(C.Structure):
 
 class Options(C.Structure):
     _fields_ = [("method", C.c_int), ("weights", C.c_double * 4), ("ahp_rule", C.c_int32),
-                ("l1_mode", C.c_int32), ("path_filter", C.c_int32), ("flags", C.c_uint32)]
+                ("l1_mode", C.c_int32), ("path_filter", C.c_int32), ("flags", C.c_uint32),
+                ("rank_mode", C.c_int32)]
 
 
 class Stats(C.Structure):
@@ -205,11 +207,12 @@ class Context:
 
     # -------------------------------------------------------------- options --
     @staticmethod
-    def options(method, weights, ahp_rule=0, l1_mode=0, path_filter=1, flags=0) -> Options:
+    def options(method, weights, ahp_rule=0, l1_mode=0, path_filter=1, flags=0, rank_once=False) -> Options:
         if isinstance(weights, str):
             weights = SCHEMAS[weights]
         m = METHODS[method] if isinstance(method, str) else int(method)
-        return Options(m, (C.c_double * 4)(*[float(w) for w in weights]), ahp_rule, l1_mode, path_filter, flags)
+        return Options(m, (C.c_double * 4)(*[float(w) for w in weights]), ahp_rule, l1_mode, path_filter, flags,
+                       NACS_RANK_ONCE if rank_once else NACS_RANK_PER_POD)
 
     # ---------------------------------------------------------------- rank ---
     def rank(self, method, weights, dem_cpu, dem_ram, flows=(), excluded=(), exact64=False, **kw) -> dict:

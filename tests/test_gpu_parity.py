@@ -420,3 +420,50 @@ def test_server_sharded_ahp_nccl_world1():
         assert_schedule_parity(snap, sub, out, "ahp", "flat", True, gpu_state=sh.read_topology())
     finally:
         sh.close()
+
+
+# ------------------------------------------------ R25: rank once per request -----
+@pytest.mark.parametrize("method", ["topsis", "ahp"])
+def test_rank_once_c2_sequential_and_batch(ctx, method):
+    """the first pod step's order, pods walk it (nacs_options.rank_mode)."""
+    snap, reqs = gen.config("C2")
+    for schema in SCHEMAS:
+        ctx.load_topology(snap)
+        out = ctx.schedule_request(reqs, method, schema, rank_once=True)
+        cnt = assert_schedule_parity(snap, reqs, out, method, schema, True, gpu_state=ctx.read_topology(),
+                                     rank_once=True)
+        assert ctx.last_stats()["pod_steps"] == cnt["pod_steps"]
+        ctx.load_topology(snap)
+        out = ctx.schedule_batch(reqs, method, schema, rank_once=True)
+        assert_schedule_parity(snap, reqs, out, method, schema, False, rank_once=True)
+
+
+def test_rank_once_congested_and_c3(ctx):
+    tight = gen.snapshot(8, seed=77)
+    tight["link_res"] = np.random.default_rng(1).integers(0, 90, size=len(tight["link_res"])).astype(np.int32)
+    reqs = gen.requests(300, 78, bw_max_hi=60)
+    for method in ("topsis", "ahp"):
+        ctx.load_topology(tight)
+        out = ctx.schedule_request(reqs, method, "network", rank_once=True)
+        cnt = assert_schedule_parity(tight, reqs, out, method, "network", True, gpu_state=ctx.read_topology(),
+                                     rank_once=True)
+        assert cnt["retries"] == ctx.last_stats()["retries"]
+    snap, c3 = gen.config("C3")
+    ctx.load_topology(snap)
+    sub = gen.subset(c3, np.arange(0, 10_000, 50))
+    for method in ("topsis", "ahp"):
+        out = ctx.schedule_batch(sub, method, "clustering", rank_once=True)
+        assert_schedule_parity(snap, sub, out, method, "clustering", False, rank_once=True)
+
+
+def test_rank_once_not_on_sharded_contexts():
+    from paper_1909_07673_b200 import nacs
+    snap, reqs = gen.config("C2")
+    sh = nacs.Context(0, shard=(0, 2, None))
+    try:
+        sh.load_topology(snap)
+        with pytest.raises(nacs.NacsError) as ei:
+            sh.schedule_request(reqs, "topsis", "flat", rank_once=True)
+        assert ei.value.status == nacs.NACS_EINVAL
+    finally:
+        sh.close()
