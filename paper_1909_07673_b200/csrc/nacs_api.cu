@@ -895,7 +895,7 @@ nacs_status nacs_schedule_batch(nacs_ctx* ctx, const nacs_options* opt, const na
   if (o.method == 0 || o.rank_once) CK(ctx->w64.reserve((size_t)grid * nacs::ahp_workspace_doubles(g.n)));
   CK(ctx->misc.reserve(8));
   CK(cudaMemsetAsync(ctx->misc.p, 0, 4 * sizeof(int), ctx->stream));
-  const int warps = o.method == NACS_TOPSIS && !ctx->cta_only && !o.rank_once ? nacs::warp_kernel_warps(g) : 0;
+  const int warps = o.method == NACS_TOPSIS && !ctx->cta_only ? nacs::warp_kernel_warps(g) : 0;
   if (warps >= 4) {
     // fast path: warp per request; requests beyond its limits are deferred to k_batch
     int wgrid = ctx->num_sms;

@@ -31,8 +31,9 @@ constexpr int WSP = 64;   // specials per pod step
 constexpr int WF = 32;    // flows per pod step
 constexpr int WX = 32;    // exclusions per pod step
 constexpr int WLOG = 256; // undo-log entries per commit
-constexpr int WDW = 64;   // dirty-row bitmap words: fabric rows E + k*h <= 2048
-constexpr int WEW = 32;   // edge bitmap words: E <= 1024
+constexpr int WDW = 40;   // dirty-row bitmap words: fabric rows E + k*h = k^2 <= 1280 (k <= 35)
+constexpr int WEW = 20;   // edge bitmap words: E = k^2/2 <= 640
+constexpr int WCH = 96;   // chunks of 128 slots: n <= 12288
 constexpr int WWARPS = 16; // warps per CTA (static per-warp scratch)
 }  // namespace
 
@@ -54,8 +55,10 @@ struct __align__(16) WScr {
   unsigned none_m[4];  // chunks without a feasible server in this pod step (pass A)
   unsigned sp_has[4];  // chunks holding a special server
   unsigned eb_has[4];  // chunks holding a server under a fabric-blocked edge switch
-  unsigned char sp_first[128];  // index in sp_u of a chunk's first special (valid where sp_has)
+  unsigned char sp_first[WCH];  // index in sp_u of a chunk's first special (valid where sp_has)
   int net;
+  TopsisP tp0;            // R25: the first pod step's TOPSIS parameters
+  int dc0, dr0;           // and its CPU / RAM demand (its feasible set, no flows yet)
   unsigned dirty[WDW];    // fabric rows (edge-agg rows, then agg-core rows) the overlay touched
   unsigned edgebad[WEW];  // edge switches without a feasible fabric path this pod step
 };
@@ -408,6 +411,11 @@ __device__ void wfabric(WCtx<LT>& c) {
 struct StepP {
   int dc, dr, dcp, sumDp;
   bool net, pf, h4;
+  // R25 walk (pod steps after the first): ordinary servers must also be in the first pod
+  // step's feasible set (snapshot CPU >= f0c, RAM >= f0r) -- folded into tc, tr
+  bool walk;
+  int f0c, f0r;
+  int tc, tr;  // CPU / RAM thresholds of ordinary servers: max(dcp, f0c), max(dr, f0r)
 };
 
 template <typename LT>
@@ -423,7 +431,7 @@ __device__ __forceinline__ unsigned ebad4(const WCtx<LT>& c, const StepP& sp, un
   return ebad(c, u0) | (ebad(c, u0 + 1) << 1) | (ebad(c, u0 + 2) << 2) | (ebad(c, u0 + 3) << 3);
 }
 __device__ __forceinline__ bool ok_plain(const StepP& sp, int x0, int x1, int x3, unsigned bad) {
-  return (x0 >= sp.dcp) & (x1 >= sp.dr) & (x3 >= sp.sumDp) & (bad == 0u);
+  return (x0 >= sp.tc) & (x1 >= sp.tr) & (x3 >= sp.sumDp) & (bad == 0u);
 }
 // a special server: excluded (R18), a flow endpoint (its own flow uses the host bus), or
 // only overlaid (ordinary rule on its overlay values)
@@ -530,6 +538,18 @@ __device__ __forceinline__ bool special_vals(const WCtx<LT>& c, const StepP& sp,
   return ok_special(c, sp, x0, x1, x3, bad, inf);
 }
 
+// R25 walk: a special server is scored on its snapshot values (the request-start state
+// the first pod step ranked) and must have been in that step's feasible set.
+template <typename LT>
+__device__ __forceinline__ void walk_vals(const WCtx<LT>& c, const StepP& sp, int pos, bool& ok, int& x0, int& x1,
+                                          int& x2, int& x3) {
+  x0 = c.snap[tile_idx(pos, 0)];
+  x1 = c.snap[tile_idx(pos, 1)];
+  x2 = c.snap[tile_idx(pos, 2)];
+  x3 = c.snap[tile_idx(pos, 3)];
+  ok = ok && x0 >= sp.f0c && x1 >= sp.f0r;
+}
+
 // Pass A (a3 + a4): filter and statistics.  Per chunk (one lane each): a chunk whose box
 // lies inside the thresholds and holds no special server is feasible as a whole and adds
 // its precomputed aggregates; a chunk whose box misses a threshold holds no feasible
@@ -546,8 +566,8 @@ __device__ void pass_a(const WCtx<LT>& c, const StepP& sp, AccA& a, unsigned lon
     if (ch < c.nch) {
       const bool slow = (w->slow[i] >> c.lane) & 1u;
       const ChunkT& t = c.ctab[ch];
-      const bool full = !slow && t.cnt > 0 && t.lo[0] >= sp.dcp && t.lo[1] >= sp.dr && t.lo[2] >= sp.sumDp;
-      none = !slow && (t.cnt == 0 || t.hi[0] < sp.dcp || t.hi[1] < sp.dr || t.hi[2] < sp.sumDp);
+      const bool full = !slow && t.cnt > 0 && t.lo[0] >= sp.tc && t.lo[1] >= sp.tr && t.lo[2] >= sp.sumDp;
+      none = !slow && (t.cnt == 0 || t.hi[0] < sp.tc || t.hi[1] < sp.tr || t.hi[2] < sp.sumDp);
       sc = !full && !none;
       if (full) {
         a.nf += t.cnt;
@@ -584,6 +604,26 @@ __device__ void pass_a(const WCtx<LT>& c, const StepP& sp, AccA& a, unsigned lon
     int x0, x1, x2, x3, id;
     const bool ok = special_vals(c, sp, t, x0, x1, x2, x3, id);
     acc_a(a, ok, x0, x1, x2, x3);
+  }
+  __syncwarp();
+}
+
+// R25 walk, pass A: no statistics (the first pod step's order is fixed); only the chunks
+// that cannot hold an admitted server of that order.
+template <typename LT>
+__device__ void pass_a_walk(const WCtx<LT>& c, const StepP& sp) {
+  WScr* w = c.w;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int ch = c.lane + 32 * i;
+    bool none = false;
+    if (ch < c.nch) {
+      const bool slow = (w->slow[i] >> c.lane) & 1u;
+      const ChunkT& t = c.ctab[ch];
+      none = !slow && (t.cnt == 0 || t.hi[0] < sp.tc || t.hi[1] < sp.tr || t.hi[2] < sp.sumDp);
+    }
+    const unsigned nm = __ballot_sync(NACS_FULL, none);
+    if (c.lane == 0) w->none_m[i] = nm;
   }
   __syncwarp();
 }
@@ -644,7 +684,8 @@ __device__ void pass_b(const WCtx<LT>& c, const StepP& sp, const TopsisP& tp, Ac
   const float INF = __int_as_float(0x7f800000);
   for (int t = c.lane; t < w->nsp; t += 32) {
     int x0, x1, x2, x3, id;
-    const bool ok = special_vals(c, sp, t, x0, x1, x2, x3, id);
+    bool ok = special_vals(c, sp, t, x0, x1, x2, x3, id);
+    if (sp.walk) walk_vals(c, sp, w->sp_u[t], ok, x0, x1, x2, x3);
     acc_b(b, ok, topsis_q32_scan(tp, x0, x1, x2, x3), id, w->sp_u[t]);
   }
   float lb[4];
@@ -689,7 +730,8 @@ __device__ void scan_fp64(const WCtx<LT>& c, const StepP& sp, const TopsisP& tp,
   const WScr* w = c.w;
   for (int t = c.lane; t < w->nsp; t += 32) {
     int x0, x1, x2, x3, id;
-    const bool ok = special_vals(c, sp, t, x0, x1, x2, x3, id);
+    bool ok = special_vals(c, sp, t, x0, x1, x2, x3, id);
+    if (sp.walk) walk_vals(c, sp, w->sp_u[t], ok, x0, x1, x2, x3);
     fp64_take(tp, thr, ok, x0, x1, x2, x3, id, w->sp_u[t], bv, bj, bp);
   }
   for (int ch = 0; ch < c.nch; ++ch) {
@@ -925,6 +967,10 @@ __device__ void prepare_step(WCtx<LT>& c, WReq& q, StepP& sp) {
   sp.dc = dc;
   sp.dr = dr;
   sp.dcp = (net && !G) ? INT_MAX : dc;
+  sp.walk = false;
+  sp.f0c = sp.f0r = INT_MIN;
+  sp.tc = sp.dcp;
+  sp.tr = dr;
   sp.sumDp = net ? sumD : INT_MIN;
   sp.net = net;
   sp.pf = c.o.path_filter != 0;
@@ -1245,7 +1291,17 @@ __global__ void __launch_bounds__(512, 1) k_batch_warp(Geo g, Opt o, const int* 
     if (group_sync_and(bar_id, bar_nt, done)) break;
     // ---- phase A (a3 + a4): filter and statistics
     bool stepping = active;
-    if (stepping) {
+    const bool walk = o.rank_once && q.p > 0;  // R25: later pod steps walk the first step's order
+    if (stepping && walk) {
+      sp.walk = true;
+      sp.f0c = w->dc0;
+      sp.f0r = w->dr0;
+      sp.tc = max(sp.dcp, sp.f0c);
+      sp.tr = max(sp.dr, sp.f0r);
+      pass_a_walk(c, sp);
+      ws.steps += 1;
+      tp = w->tp0;
+    } else if (stepping) {
       AccA acc = {0, 0, UINT_MAX, UINT_MAX, UINT_MAX, 0u, 0u, 0u, 0ull, 0ull, 0ull};
       pass_a(c, sp, acc, ws.scan_a);
       const int nf = (int)__reduce_add_sync(NACS_FULL, (unsigned)acc.nf);
@@ -1265,6 +1321,12 @@ __global__ void __launch_bounds__(512, 1) k_batch_warp(Geo g, Opt o, const int* 
         unsigned long long sq[4] = {warp_sum_u64(acc.q0), warp_sum_u64(acc.q1), (unsigned long long)nact,
                                     warp_sum_u64(acc.q3)};
         topsis_params(tp, wd, sq);
+        if (o.rank_once && lane == 0) {  // the first pod step: keep its order's parameters
+          w->tp0 = tp;
+          w->dc0 = sp.dc;
+          w->dr0 = sp.dr;
+        }
+        __syncwarp();
       }
     }
     if (sync_mask & 1) group_sync(bar_id, bar_nt);
@@ -1295,6 +1357,11 @@ __global__ void __launch_bounds__(512, 1) k_batch_warp(Geo g, Opt o, const int* 
         const unsigned wl = __ballot_sync(NACS_FULL, mine == bj && bj >= 0);
         best_pos = __shfl_sync(NACS_FULL, bp, wl ? __ffs(wl) - 1 : 0);
         ws.fp64 += 1;
+      }
+      if (best < 0) {  // R25: no server of the first step's order is admitted (R20)
+        emit_failed(O, q, lane, 0);
+        active = false;
+        stepping = false;
       }
     }
     if (sync_mask & 2) group_sync(bar_id, bar_nt);
@@ -1545,7 +1612,7 @@ int warp_kernel_warps(const Geo& g) {
   bool u16 = g.link_cap <= 65535;
   // dynamic shared memory: WWARPS per-warp scratch areas + the snapshot (+ static words)
   const size_t stat = sizeof(WScr) * WWARPS + 64;
-  if (warp_snapshot_bytes(g, u16) + stat > (size_t)optin || ((g.n + 127) >> 7) > 128) return 0;
+  if (warp_snapshot_bytes(g, u16) + stat > (size_t)optin || ((g.n + 127) >> 7) > WCH) return 0;
   if (g.E > 32 * WEW || g.E + g.k * g.h > 32 * WDW || g.k > 64) return 0;
   return WWARPS;
 }

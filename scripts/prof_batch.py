@@ -1,6 +1,6 @@
 """One nacs_schedule_batch call (after warm-up) for ncu captures.
 
-usage: python scripts/prof_batch.py [topsis|ahp] [C3|C4] [n_requests]
+usage: python scripts/prof_batch.py [topsis|ahp] [C3|C4] [n_requests]   (NACS_RANK_ONCE=1: R25 mode)
 """
 import os
 import sys
@@ -13,6 +13,7 @@ from inputs import gen  # noqa: E402
 from paper_1909_07673_b200 import nacs  # noqa: E402
 
 method = sys.argv[1] if len(sys.argv) > 1 else "topsis"
+KW = {"rank_once": True} if os.environ.get("NACS_RANK_ONCE") == "1" else {}
 cfg = sys.argv[2] if len(sys.argv) > 2 else "C4"
 nreq = int(sys.argv[3]) if len(sys.argv) > 3 else gen.CONFIG_REQUESTS[cfg]
 snap = gen.snapshot(gen.CONFIG_K[cfg], gen.CONFIG_SEEDS[cfg])
@@ -24,11 +25,11 @@ ctx.load_topology(snap)
 d = {k: (torch.from_numpy(v).cuda() if isinstance(v, np.ndarray) else v) for k, v in reqs.items()}
 out = ctx._alloc_out(reqs, True)[0]
 for _ in range(2):
-    ctx.schedule_batch(d, method, "flat", out=out, flags=nacs.NACS_ASYNC)
+    ctx.schedule_batch(d, method, "flat", out=out, flags=nacs.NACS_ASYNC, **KW)
 torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record(s)
-ctx.schedule_batch(d, method, "flat", out=out, flags=nacs.NACS_ASYNC)
+ctx.schedule_batch(d, method, "flat", out=out, flags=nacs.NACS_ASYNC, **KW)
 e1.record(s)
 torch.cuda.synchronize()
 st = ctx.last_stats()
@@ -46,7 +47,7 @@ if len(sys.argv) > 4 and sys.argv[4] == "loop":
     for i in range(6):
         flush.zero_()
         evs[i][0].record(s)
-        ctx.schedule_batch(d, method, "flat", out=out, flags=nacs.NACS_ASYNC)
+        ctx.schedule_batch(d, method, "flat", out=out, flags=nacs.NACS_ASYNC, **KW)
         evs[i][1].record(s)
     a1.record(s)
     host = time.perf_counter() - t
@@ -60,14 +61,14 @@ if len(sys.argv) > 4 and sys.argv[4] == "loop":
     ts = []
     for i in range(6):
         t = time.perf_counter()
-        ctx.schedule_batch(d, method, "flat", out=out, flags=nacs.NACS_ASYNC)
+        ctx.schedule_batch(d, method, "flat", out=out, flags=nacs.NACS_ASYNC, **KW)
         ts.append(round((time.perf_counter() - t) * 1e3, 3))
     torch.cuda.synchronize()
     print("host ms per call (async):", ts)
     import cProfile, pstats, io
     pr = cProfile.Profile()
     pr.enable()
-    ctx.schedule_batch(d, method, "flat", out=out, flags=nacs.NACS_ASYNC)
+    ctx.schedule_batch(d, method, "flat", out=out, flags=nacs.NACS_ASYNC, **KW)
     pr.disable()
     sio = io.StringIO()
     pstats.Stats(pr, stream=sio).sort_stats("cumulative").print_stats(8)
@@ -80,7 +81,7 @@ if len(sys.argv) > 4 and sys.argv[4] == "loop":
     for i in range(6):
         t = time.perf_counter(); flush.zero_(); tz.append(round((time.perf_counter() - t) * 1e3, 3))
         t = time.perf_counter(); ev[2 * i].record(s); te.append(round((time.perf_counter() - t) * 1e3, 3))
-        t = time.perf_counter(); ctx.schedule_batch(d, method, "flat", out=out, flags=nacs.NACS_ASYNC)
+        t = time.perf_counter(); ctx.schedule_batch(d, method, "flat", out=out, flags=nacs.NACS_ASYNC, **KW)
         tc.append(round((time.perf_counter() - t) * 1e3, 3))
         ev[2 * i + 1].record(s)
     torch.cuda.synchronize()

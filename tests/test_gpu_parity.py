@@ -467,3 +467,27 @@ def test_rank_once_not_on_sharded_contexts():
         assert ei.value.status == nacs.NACS_EINVAL
     finally:
         sh.close()
+
+
+def test_rank_once_warp_kernel_equals_cta_kernel(ctx):
+    """R25 on the warp fast path (no statistics after the first pod step, pruned walk over the
+    first step's order on snapshot values) equals the CTA kernel and the oracle, at k=32."""
+    cta = _cta_only_ctx()
+    try:
+        quant = gen.snapshot(32, seed=31, quantised=True)
+        tight = gen.snapshot(16, seed=32)
+        tight["link_res"] = np.random.default_rng(4).integers(0, 100, size=len(tight["link_res"])).astype(np.int32)
+        for snap, reqs in ((gen.config("C4")[0], gen.requests(1200, 33)), (quant, gen.requests(800, 34)),
+                           (tight, gen.requests(800, 35, bw_max_hi=60))):
+            ctx.load_topology(snap)
+            cta.load_topology(snap)
+            for schema in SCHEMAS:
+                a = to_np(ctx.schedule_batch(reqs, "topsis", schema, rank_once=True))
+                b = to_np(cta.schedule_batch(reqs, "topsis", schema, rank_once=True))
+                for key in a:
+                    assert np.array_equal(a[key], b[key]), (schema, key)
+            sub = gen.subset(reqs, np.arange(0, reqs["n_requests"], 20))
+            out = ctx.schedule_batch(sub, "topsis", "network", rank_once=True)
+            assert_schedule_parity(snap, sub, out, "topsis", "network", False, rank_once=True)
+    finally:
+        cta.close()
