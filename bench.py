@@ -53,6 +53,7 @@ def parse():
     ap.add_argument("--no-ahp", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-once", action="store_true")
     return ap.parse_args()
 
 
@@ -192,14 +193,14 @@ def run_ours(args, rank, world, local):
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
         return float(t.item())
 
-    def measure(method):
+    def measure(method, **kw):
         snap, reqs, name = workload(rank, method)
         ctx.load_topology(snap)
         d = {k: (torch.from_numpy(v).to(dev) if isinstance(v, np.ndarray) else v) for k, v in reqs.items()}
         out = ctx._alloc_out(reqs, True)[0]
         for _ in range(args.warmup):  # warm-up includes the flush (its first launch loads torch's module)
             flush.zero_()
-            ctx.schedule_batch(d, method, "flat", out=out, flags=nacs.NACS_ASYNC)
+            ctx.schedule_batch(d, method, "flat", out=out, flags=nacs.NACS_ASYNC, **kw)
         torch.cuda.synchronize(dev)
         st0 = ctx.last_stats()
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
@@ -212,7 +213,7 @@ def run_ours(args, rank, world, local):
             for i in range(args.steps):
                 flush.zero_()
                 ev[i][0].record(stream)
-                ctx.schedule_batch(d, method, "flat", out=out, flags=nacs.NACS_ASYNC)
+                ctx.schedule_batch(d, method, "flat", out=out, flags=nacs.NACS_ASYNC, **kw)
                 ev[i][1].record(stream)
             t1.record(stream)
             torch.cuda.synchronize(dev)
@@ -231,6 +232,8 @@ def run_ours(args, rank, world, local):
 
     topsis = measure("topsis")
     ahp = None if args.no_ahp else measure("ahp")
+    # rank once per request, pods walk the first pod step's order
+    once = None if args.no_once else measure("topsis", rank_once=True)
 
     # roofline of the dominant kernel (k_batch<TOPSIS>): issue-bound ALU
     clocks = topsis["clocks"]
@@ -305,6 +308,12 @@ def run_ours(args, rank, world, local):
                 "retries": topsis["stats"]["retries"],
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": args.steps * LAUNCHES["topsis"],
                 "clocks": clocks, "ahp": ahp_obj,
+                "rank_once": None if once is None else {
+                    "workload": once["name"].replace("batch", "batch, rank once per request (R25)"),
+                    "value": once["value"], "unit": "pods/s", "ms_per_step": once["ms_per_step"],
+                    "kernel_ms": once["kernel_ms"], "pod_steps_per_step": once["pod_steps_per_step"],
+                    "slots_read_frac": (once["stats"]["scanned_a"] + once["stats"]["scanned_b"])
+                    / max(1, 2 * once["stats"]["servers_ranked"])},
                 "paper_context": "T5 (P:416-426): TOPSIS 3.48-3.84 s, AHP 6.90-9.45 s per 6000-request k=20 campaign "
                                  "on an unnamed CUDA 10.1 GPU (~10-14 M / 4-7 M servers ranked/s derived)"}
         print(json.dumps(line))
