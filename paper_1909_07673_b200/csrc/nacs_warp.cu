@@ -1190,7 +1190,7 @@ __device__ __forceinline__ bool group_sync_and(int id, int nt, bool p) {
 // The warps of a CTA advance in lockstep phases (prepare | pass A | pass B | commit), each
 // on its own request, so that all warps run the same loop at the same time (one copy of
 // the hot code in the instruction caches); within a phase no warp waits for another.
-template <typename LT>
+template <typename LT, bool RO>  // RO: R25 rank-once instantiation
 __global__ void __launch_bounds__(512, 1) k_batch_warp(Geo g, Opt o, const int* __restrict__ state,
                                                        const int* __restrict__ lay, ReqsDev R, OutDev O,
                                                        int4* ulog_all, int* next, const int* order, int* deferred,
@@ -1291,7 +1291,7 @@ __global__ void __launch_bounds__(512, 1) k_batch_warp(Geo g, Opt o, const int* 
     if (group_sync_and(bar_id, bar_nt, done)) break;
     // ---- phase A (a3 + a4): filter and statistics
     bool stepping = active;
-    const bool walk = o.rank_once && q.p > 0;  // R25: later pod steps walk the first step's order
+    const bool walk = RO && q.p > 0;  // R25: later pod steps walk the first step's order
     if (stepping && walk) {
       sp.walk = true;
       sp.f0c = w->dc0;
@@ -1321,7 +1321,7 @@ __global__ void __launch_bounds__(512, 1) k_batch_warp(Geo g, Opt o, const int* 
         unsigned long long sq[4] = {warp_sum_u64(acc.q0), warp_sum_u64(acc.q1), (unsigned long long)nact,
                                     warp_sum_u64(acc.q3)};
         topsis_params(tp, wd, sq);
-        if (o.rank_once && lane == 0) {  // the first pod step: keep its order's parameters
+        if (RO && lane == 0) {  // the first pod step: keep its order's parameters
           w->tp0 = tp;
           w->dc0 = sp.dc;
           w->dr0 = sp.dr;
@@ -1645,14 +1645,17 @@ cudaError_t launch_batch_warp(const Geo& g, const Opt& o, const int* d_state, in
     return e ? atoi(e) : 3;
   }();
   size_t smem = warp_snapshot_bytes(g, u16) + sizeof(WScr) * WWARPS;
+  auto go = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<grid, warps * 32, smem, st>>>(g, o, d_state, lay, R, O, ulog, next, order, deferred, n_deferred, stats,
+                                         group, sync_mask);
+  };
   if (u16) {
-    cudaFuncSetAttribute(k_batch_warp<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_batch_warp<uint16_t><<<grid, warps * 32, smem, st>>>(g, o, d_state, lay, R, O, ulog, next, order, deferred,
-                                                           n_deferred, stats, group, sync_mask);
+    if (o.rank_once) go(k_batch_warp<uint16_t, true>);
+    else go(k_batch_warp<uint16_t, false>);
   } else {
-    cudaFuncSetAttribute(k_batch_warp<int>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_batch_warp<int><<<grid, warps * 32, smem, st>>>(g, o, d_state, lay, R, O, ulog, next, order, deferred, n_deferred,
-                                                      stats, group, sync_mask);
+    if (o.rank_once) go(k_batch_warp<int, true>);
+    else go(k_batch_warp<int, false>);
   }
   return cudaGetLastError();
 }
