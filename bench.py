@@ -54,6 +54,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-once", action="store_true")
+    ap.add_argument("--no-variants", action="store_true")
     return ap.parse_args()
 
 
@@ -234,6 +235,18 @@ def run_ours(args, rank, world, local):
     ahp = None if args.no_ahp else measure("ahp")
     # rank once per request, pods walk the first pod step's order
     once = None if args.no_once else measure("topsis", rank_once=True)
+    # the paper-literal variant flags as benchmarked modes
+    variants = None
+    if not args.no_variants:
+        variants = {}
+        for name, meth, kw in (("topsis_path_filter_0 (select then route, R6 flag)", "topsis", {"path_filter": 0}),
+                               ("ahp_shifted_rule (R8 flag)", "ahp", {"ahp_rule": 1}),
+                               ("ahp_l1_weights (R10 flag)", "ahp", {"l1_mode": 1})):
+            if meth == "ahp" and args.no_ahp:
+                continue
+            v = measure(meth, **kw)
+            variants[name] = {"workload": v["name"], "value": v["value"], "unit": "pods/s",
+                              "ms_per_step": v["ms_per_step"]}
 
     # roofline of the dominant kernel (k_batch<TOPSIS>): issue-bound ALU
     clocks = topsis["clocks"]
@@ -307,7 +320,7 @@ def run_ours(args, rank, world, local):
                 "kernel_ms": topsis["kernel_ms"], "fp64_decisions": topsis["stats"]["fp64_decisions"],
                 "retries": topsis["stats"]["retries"],
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": args.steps * LAUNCHES["topsis"],
-                "clocks": clocks, "ahp": ahp_obj,
+                "clocks": clocks, "ahp": ahp_obj, "variants": variants,
                 "rank_once": None if once is None else {
                     "workload": once["name"].replace("batch", "batch, rank once per request (R25)"),
                     "value": once["value"], "unit": "pods/s", "ms_per_step": once["ms_per_step"],

@@ -491,3 +491,26 @@ def test_rank_once_warp_kernel_equals_cta_kernel(ctx):
             assert_schedule_parity(snap, sub, out, "topsis", "network", False, rank_once=True)
     finally:
         cta.close()
+
+
+@pytest.mark.parametrize("k", [10, 12, 14, 20])
+def test_warp_kernel_ragged_chunk_layouts(ctx, k):
+    """n = k^3/4 not a multiple of 128 (250, 432, 686) and a mid size (2000): the chunk layout's
+    padded last tile, whole-tile statistics and pruning give the CTA kernel's placements, in
+    both ranking modes, and the oracle's on a sample."""
+    cta = _cta_only_ctx()
+    try:
+        snap = gen.snapshot(k, seed=40 + k)
+        reqs = gen.requests(600, 50 + k)
+        ctx.load_topology(snap)
+        cta.load_topology(snap)
+        for ro in (False, True):
+            a = to_np(ctx.schedule_batch(reqs, "topsis", "clustering", rank_once=ro))
+            b = to_np(cta.schedule_batch(reqs, "topsis", "clustering", rank_once=ro))
+            for key in a:
+                assert np.array_equal(a[key], b[key]), (ro, key)
+        sub = gen.subset(reqs, np.arange(0, 600, 30))
+        out = ctx.schedule_batch(sub, "topsis", "flat")
+        assert_schedule_parity(snap, sub, out, "topsis", "flat", False)
+    finally:
+        cta.close()
