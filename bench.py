@@ -278,7 +278,8 @@ def run_ours(args, rank, world, local):
                    "pod_steps_per_step": ahp["pod_steps_per_step"], "fp64_decisions": sa["fp64_decisions"],
                    "roofline": {"bound": "mufu", "achieved": ach, "peak": mufu_peak, "unit": "T rcp/s",
                                 "frac": ach / mufu_peak, "kernel": "k_batch<AHP>",
-                                "peak_source": f"16 MUFU/clk/SM x 148 x {mhz:.0f} MHz"}}
+                                "peak_source": f"16 MUFU.RCP/clk/SM (measured 15.9: scripts/micro/mufu_rcp.cu, "
+                                               f"profiles/r01_micro_mufu_rcp.txt) x 148 x {mhz:.0f} MHz"}}
 
     # e2e: the public API with host buffers (staging copies inside the timed region)
     e2e = None
