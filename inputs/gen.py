@@ -205,3 +205,69 @@ def config(name: str) -> tuple[dict, dict]:
         return snapshot(k, warm=False), c1_request(seed)
     snap = snapshot(k, seed)
     return snap, requests(CONFIG_REQUESTS[name], seed + 1000)
+
+
+# ---------------------------------------------------------------------------
+# General topologies: G^s(N^s, E^s) as an explicit undirected
+# graph, vertices 0..n_servers-1 are the servers (§II-A: "N^s ... all servers
+# and switches", E^s "all physical links").  Only layout and random draws here.
+# ---------------------------------------------------------------------------
+
+def fat_tree_graph(snap: dict) -> dict:
+    """The fat-tree of `snap` as an explicit graph.  Vertex ids: servers 0..n-1, edge
+    switch e at n + e, aggregation switch a of pod p at n + E + p*h + a, core switch (a, b)
+    at n + E + k*h + a*h + b.  Link l is the canonical link l of include/nacs.h, so
+    link_res is the snapshot's link_res unchanged."""
+    s = sizes(int(snap["k"]))
+    k, h, n, E = s["k"], s["h"], s["n"], s["E"]
+    agg0, core0 = n + E, n + E + k * h
+    u = np.arange(n)
+    acc_u, acc_v = u, n + u // h
+    e, a = np.divmod(np.arange(E * h), h)
+    ea_u, ea_v = n + e, agg0 + (e // h) * h + a
+    p, ab = np.divmod(np.arange(k * h * h), h * h)
+    a2, b2 = np.divmod(ab, h)
+    ac_u, ac_v = agg0 + p * h + a2, core0 + a2 * h + b2
+    i32 = lambda x: np.ascontiguousarray(x, dtype=np.int32)
+    return dict(n_vertices=n + E + k * h + h * h, n_servers=n,
+                link_u=i32(np.concatenate([acc_u, ea_u, ac_u])), link_v=i32(np.concatenate([acc_v, ea_v, ac_v])),
+                link_res=i32(snap["link_res"]), link_cap=int(snap["link_cap"]))
+
+
+def random_graph(n_switches: int, degree: int, servers_per_switch: int, seed: int, warm: bool = True,
+                 link_cap: int = LINK_CAP) -> dict:
+    """A Jellyfish-style DC: a random `degree`-regular graph over the switches (configuration
+    model, redrawn until simple) with `servers_per_switch` servers on each switch.  Vertex ids:
+    servers 0..ns-1 (server s on switch s // servers_per_switch), switches ns.. .  Residuals
+    ~ link_cap - U{0..950} when warm (as the fat-tree snapshots), else link_cap."""
+    if (n_switches * degree) % 2 or degree >= n_switches:
+        raise ValueError("need n_switches * degree even and degree < n_switches")
+    rng = _rng(seed)
+    ns = n_switches * servers_per_switch
+    while True:
+        stubs = rng.permutation(np.repeat(np.arange(n_switches), degree))
+        a, b = stubs[0::2], stubs[1::2]
+        lo, hi = np.minimum(a, b), np.maximum(a, b)
+        if np.all(lo != hi) and np.unique(lo * n_switches + hi).size == lo.size:
+            break
+    srv = np.arange(ns)
+    lu = np.concatenate([srv, ns + lo])
+    lv = np.concatenate([ns + srv // servers_per_switch, ns + hi])
+    res = np.full(lu.size, link_cap, dtype=np.int64)
+    if warm:
+        res = link_cap - rng.integers(0, min(950, link_cap), size=lu.size, endpoint=True)
+    i32 = lambda x: np.ascontiguousarray(x, dtype=np.int32)
+    return dict(n_vertices=ns + n_switches, n_servers=ns, link_u=i32(lu), link_v=i32(lv), link_res=i32(res),
+                link_cap=link_cap)
+
+
+def path_queries(graph: dict, n_queries: int, seed: int, bw_hi: int = 50) -> dict:
+    """(src, dst, demand) server pairs, src != dst, demand ~ U{1..bw_hi} Mbps (the pair
+    bandwidth "up to 50 Mbps", P:398)."""
+    rng = _rng(seed)
+    ns = int(graph["n_servers"])
+    src = rng.integers(0, ns, size=n_queries)
+    dst = (src + rng.integers(1, ns, size=n_queries)) % ns
+    dem = rng.integers(1, bw_hi, size=n_queries, endpoint=True)
+    i32 = lambda x: np.ascontiguousarray(x, dtype=np.int32)
+    return dict(src=i32(src), dst=i32(dst), demand=i32(dem))

@@ -624,3 +624,141 @@ int orc_schedule(int k, int cpu_cap, int ram_cap, int link_cap, int32_t* cpu, in
 }
 
 }  // extern "C"
+
+
+// ===========================================================================
+// General topology: the "modified Dijkstra" of P:383-386
+// (§V-D) on an arbitrary undirected graph G^s(N^s, E^s) (§II-A), not
+// only the fat-tree closed form above.  "A modified Dijkstra algorithm is used
+// to compute the shortest path that has the maximum available bandwidth
+// between the hosting servers"; links are undirected and u->v equals
+// v->u.  Reading R26: a link is usable for a flow of
+// demand D iff its residual >= D; among the usable paths the path has the
+// fewest hops, then the largest bottleneck (min residual over its links), then
+// the lexicographically smallest vertex sequence.
+// ===========================================================================
+namespace {
+
+struct Graph {
+  int V = 0;
+  std::vector<std::vector<std::pair<int, long>>> adj;  // (neighbour, residual), both directions
+};
+
+Graph make_graph(int V, int nl, const int32_t* lu, const int32_t* lv, const int32_t* lr) {
+  Graph G;
+  G.V = V;
+  G.adj.assign(V, {});
+  for (int l = 0; l < nl; ++l) {
+    G.adj[lu[l]].push_back({lv[l], (long)lr[l]});
+    G.adj[lv[l]].push_back({lu[l], (long)lr[l]});
+  }
+  return G;
+}
+
+// Label of a vertex = the best (hops, width) over usable paths from the vertex to
+// the root; better = fewer hops, then wider.  The order is isotone (extending two
+// paths by the same link keeps their order), so Dijkstra's label-setting is exact.
+struct Label {
+  long hops;     // -1 = unreached
+  double width;  // bottleneck; the root has +inf
+};
+
+bool better(long h1, double w1, long h2, double w2) { return h1 < h2 || (h1 == h2 && w1 > w2); }
+
+// Modified Dijkstra from `root` over the links with residual >= demand.
+std::vector<Label> dijkstra(const Graph& G, int root, long demand) {
+  std::vector<Label> lab(G.V, Label{-1, 0.0});
+  std::vector<char> done(G.V, 0);
+  // priority queue ordered by label (a plain O(V^2) selection: slow and obviously right)
+  lab[root] = Label{0, kInf};
+  for (;;) {
+    int v = -1;
+    for (int x = 0; x < G.V; ++x)
+      if (!done[x] && lab[x].hops >= 0 &&
+          (v < 0 || better(lab[x].hops, lab[x].width, lab[v].hops, lab[v].width)))
+        v = x;
+    if (v < 0) break;
+    done[v] = 1;
+    for (const auto& e : G.adj[v]) {
+      if (e.second < demand) continue;  // link not usable for this demand (R26)
+      long h = lab[v].hops + 1;
+      double w = std::min(lab[v].width, (double)e.second);
+      Label& t = lab[e.first];
+      if (!done[e.first] && (t.hops < 0 || better(h, w, t.hops, t.width))) t = Label{h, w};
+    }
+  }
+  return lab;
+}
+
+// One (src, dst, demand) query: labels from dst, then the walk from src that takes, at
+// every vertex, the smallest-id neighbour through which an optimal path continues
+// (one hop closer to dst, bottleneck still >= the optimum): the lexicographically
+// smallest vertex sequence among the optimal paths.  Returns hops (-1 if no usable path).
+long widest_shortest(const Graph& G, int src, int dst, long demand, double* bottleneck, std::vector<int>* path) {
+  std::vector<Label> lab = dijkstra(G, dst, demand);
+  path->clear();
+  if (lab[src].hops < 0) {
+    *bottleneck = -1;
+    return -1;
+  }
+  const double B = lab[src].width;
+  int v = src;
+  path->push_back(v);
+  while (v != dst) {
+    int next = -1;
+    for (const auto& e : G.adj[v]) {
+      int w = e.first;
+      if (e.second < demand || lab[w].hops != lab[v].hops - 1) continue;
+      if (std::min((double)e.second, lab[w].width) < B) continue;
+      if (next < 0 || w < next) next = w;
+    }
+    v = next;
+    path->push_back(v);
+  }
+  *bottleneck = B;
+  return lab[src].hops;
+}
+
+}  // namespace
+
+extern "C" {
+
+// Batch of widest-shortest path queries on one immutable graph (element-wise
+// identical to sequential calls).  Vertices 0..V-1; link l joins lu[l] and lv[l] with
+// residual lr[l].  Outputs per query q: bn[q] bottleneck (-1 infeasible), hops[q] (-1
+// infeasible), path[q * (max_hops + 1) ...] the vertex sequence src..dst (-1 padded).
+void orc_graph_paths(int V, int nl, const int32_t* lu, const int32_t* lv, const int32_t* lr, int nq,
+                     const int32_t* src, const int32_t* dst, const int32_t* demand, int32_t* bn, int32_t* hops,
+                     int32_t* path, int max_hops, int nthreads) {
+  Graph G = make_graph(V, nl, lu, lv, lr);
+#pragma omp parallel for schedule(dynamic, 1) num_threads(nthreads > 0 ? nthreads : 1)
+  for (int q = 0; q < nq; ++q) {
+    double b = 0;
+    std::vector<int> p;
+    long h = widest_shortest(G, src[q], dst[q], demand[q], &b, &p);
+    bn[q] = (int32_t)b;
+    hops[q] = (int32_t)h;
+    if (path) {
+      for (int i = 0; i <= max_hops; ++i) path[(size_t)q * (max_hops + 1) + i] = i < (int)p.size() ? p[i] : -1;
+    }
+  }
+}
+
+// Logical bandwidth criterion (reading R2, alternative `bw_criterion=logical`:
+// "sum of all bandwidth capacity bw^s_uv with source on u"): for each server
+// u < ns, the sum over servers v != u of the bottleneck of the widest shortest path
+// u -> v with every link usable (demand 0); unreachable servers add 0.
+void orc_logical_bandwidth(int V, int ns, int nl, const int32_t* lu, const int32_t* lv, const int32_t* lr,
+                           int64_t* out, int nthreads) {
+  Graph G = make_graph(V, nl, lu, lv, lr);
+#pragma omp parallel for schedule(dynamic, 1) num_threads(nthreads > 0 ? nthreads : 1)
+  for (int u = 0; u < ns; ++u) {
+    std::vector<Label> lab = dijkstra(G, u, 0);
+    int64_t s = 0;
+    for (int v = 0; v < ns; ++v)
+      if (v != u && lab[v].hops >= 0) s += (int64_t)lab[v].width;
+    out[u] = s;
+  }
+}
+
+}  // extern "C"

@@ -49,6 +49,10 @@ def lib():
         _lib.orc_schedule.restype = C.c_int
         _lib.orc_schedule.argtypes = [C.c_int] * 4 + [P] * 4 + [C.c_int, P, C.c_int, C.c_int, C.c_int,
                                                           C.c_int, C.c_int, C.c_int] + [P] * 19 + [C.c_int]
+        _lib.orc_graph_paths.restype = None
+        _lib.orc_graph_paths.argtypes = [C.c_int, C.c_int, P, P, P, C.c_int, P, P, P, P, P, P, C.c_int, C.c_int]
+        _lib.orc_logical_bandwidth.restype = None
+        _lib.orc_logical_bandwidth.argtypes = [C.c_int, C.c_int, C.c_int, P, P, P, P, C.c_int]
     return _lib
 
 
@@ -154,3 +158,35 @@ def schedule(snap: dict, reqs: dict, method: str, weights, sequential: bool, hin
                         cnt.tolist()))
     state = dict(snap, cpu_res=cpu, ram_res=ram, active=act, link_res=link)
     return out, counters, state
+
+
+def graph_paths(graph: dict, src, dst, demand, max_hops: int | None = None, nthreads: int | None = None):
+    """Widest-shortest paths on a general graph (modified Dijkstra, reading R26).
+    graph: dict(n_vertices, n_servers, link_u, link_v, link_res).  Returns (bottleneck, hops,
+    path[nq, max_hops + 1]) with -1 for infeasible queries and -1 padding."""
+    V = int(graph["n_vertices"])
+    lu, lv, lr = _i32(graph["link_u"]), _i32(graph["link_v"]), _i32(graph["link_res"])
+    src, dst, dem = _i32(src), _i32(dst), _i32(demand)
+    nq = src.size
+    if max_hops is None:
+        max_hops = V - 1
+    bn = np.zeros(max(nq, 1), np.int32)
+    hops = np.zeros(max(nq, 1), np.int32)
+    path = np.zeros((max(nq, 1), max_hops + 1), np.int32)
+    if nthreads is None:
+        nthreads = len(os.sched_getaffinity(0))
+    lib().orc_graph_paths(V, lu.size, _p(lu), _p(lv), _p(lr), nq, _p(src), _p(dst), _p(dem), _p(bn), _p(hops),
+                          _p(path), max_hops, int(nthreads))
+    return bn[:nq], hops[:nq], path[:nq]
+
+
+def logical_bandwidth(graph: dict, nthreads: int | None = None) -> np.ndarray:
+    """R2 alternative: per server u, sum over servers v != u of the widest-shortest
+    bottleneck u -> v with every link usable; int64[n_servers]."""
+    V, ns = int(graph["n_vertices"]), int(graph["n_servers"])
+    lu, lv, lr = _i32(graph["link_u"]), _i32(graph["link_v"]), _i32(graph["link_res"])
+    out = np.zeros(ns, np.int64)
+    if nthreads is None:
+        nthreads = len(os.sched_getaffinity(0))
+    lib().orc_logical_bandwidth(V, ns, lu.size, _p(lu), _p(lv), _p(lr), _p(out), int(nthreads))
+    return out
