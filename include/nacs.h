@@ -145,6 +145,8 @@ typedef struct {
   int64_t ahp_pairs;       /* AHP: sum over pod steps and non-constant criteria of |F|(|F|-1)/2 */
   int64_t scanned_a;       /* TOPSIS batch fast path: server slots read by the filter/statistics pass */
   int64_t scanned_b;       /* ... and by the scoring pass (chunk-pruned; 0 for the other kernels) */
+  int64_t edges_scanned;   /* general-topology calls: adjacency entries read by the BFS levels */
+  int64_t bfs_runs;        /* ... and BFS traversals run (one per destination group + deferred queries) */
 } nacs_stats;
 
 /* Create a context on CUDA device `device`.  cuda_stream: the cudaStream_t all work of
@@ -196,6 +198,57 @@ nacs_status nacs_schedule_request(nacs_ctx *ctx, const nacs_options *opt, const 
  * private overlay (R21): requests do not see each other and the state is not modified. */
 nacs_status nacs_schedule_batch(nacs_ctx *ctx, const nacs_options *opt, const nacs_requests *batch,
                                 nacs_placements *out);
+
+/* ---------------------------------------------------------------------------------------
+ * General topology.  "A modified Dijkstra algorithm is used to compute
+ * the shortest path that has the maximum available bandwidth between the hosting servers
+ * ... each thread calculates a different source and destination pair" (§V-D),
+ * for a DC G^s(N^s, E^s) given as an arbitrary undirected graph (§II-A) instead of
+ * a fat-tree.  Reading R26: a link is usable by a flow of demand D iff its residual >= D;
+ * the returned path has the fewest hops over usable links, then the largest bottleneck
+ * (minimum residual along it), then the lexicographically smallest vertex sequence.
+ * ------------------------------------------------------------------------------------- */
+#define NACS_MAX_GRAPH_VERTICES 16777216  /* 2^24 */
+#define NACS_MAX_GRAPH_LINKS 268435456    /* 2^28 */
+
+/* Vertices 0..n_vertices-1, of which 0..n_servers-1 are the servers; link l joins link_u[l]
+ * and link_v[l] (undirected; parallel links allowed, no self-loops) with residual
+ * bandwidth link_res[l] in [0, NACS_MAX_CAP] Mbps.  Host pointers.  Independent of the
+ * fat-tree state of nacs_load_topology; a context holds one of each. */
+typedef struct {
+  int32_t n_vertices;   /* 2..NACS_MAX_GRAPH_VERTICES */
+  int32_t n_servers;    /* 1..n_vertices */
+  int32_t n_links;      /* 0..NACS_MAX_GRAPH_LINKS */
+  const int32_t *link_u, *link_v, *link_res;
+} nacs_graph;
+
+/* Queries: path i goes from src[i] to dst[i] (vertex ids, src != dst) for a flow of
+ * demand[i] in [0, NACS_MAX_CAP] Mbps. */
+typedef struct {
+  int32_t n_queries;
+  const int32_t *src, *dst, *demand;
+} nacs_path_query;
+
+/* Load (or replace) the graph.  Validates endpoints, self-loops and residual ranges. */
+nacs_status nacs_load_graph(nacs_ctx *ctx, const nacs_graph *g);
+
+/* Widest-shortest path of every query on the loaded graph, all against the same graph
+ * (queries are independent).  Outputs (caller-allocated, [n_queries]):
+ * bottleneck[i] = minimum residual along the path, hops[i] = its link count; both -1 when
+ * no usable path exists.  path (may be NULL): [n_queries][max_hops + 1] vertex ids
+ * src..dst, -1 padded; a row is all -1 if the query is infeasible or hops[i] > max_hops.
+ * flags: NACS_DEVICE_PTRS (all five arrays on the device; invalid queries then get
+ * hops = -2 and the call returns NACS_EINVAL after the kernel unless NACS_ASYNC) |
+ * NACS_ASYNC.  Host pointers: invalid queries (endpoint out of range, src == dst, demand
+ * out of range) fail the call with NACS_EINVAL before any work. */
+nacs_status nacs_widest_paths(nacs_ctx *ctx, const nacs_path_query *q, uint32_t flags, int32_t *bottleneck,
+                              int32_t *hops, int32_t *path, int32_t max_hops);
+
+/* Logical bandwidth criterion (reading R2's alternative: "sum of all bandwidth capacity
+ * bw^s_uv with source on u"): out[u] (int64, [n_servers]) = sum over the servers
+ * v != u of the bottleneck of the widest shortest u-v path with every link usable;
+ * unreachable servers add 0.  flags: NACS_DEVICE_PTRS | NACS_ASYNC. */
+nacs_status nacs_logical_bandwidth(nacs_ctx *ctx, uint32_t flags, int64_t *out);
 
 nacs_status nacs_last_stats(nacs_ctx *ctx, nacs_stats *out);
 const char *nacs_last_error(const nacs_ctx *ctx);

@@ -237,19 +237,31 @@ def fat_tree_graph(snap: dict) -> dict:
 def random_graph(n_switches: int, degree: int, servers_per_switch: int, seed: int, warm: bool = True,
                  link_cap: int = LINK_CAP) -> dict:
     """A Jellyfish-style DC: a random `degree`-regular graph over the switches (configuration
-    model, redrawn until simple) with `servers_per_switch` servers on each switch.  Vertex ids:
+    model; the stubs of self-loops and repeated pairs are re-paired with random other pairs
+    until the graph is simple) with `servers_per_switch` servers on each switch.  Vertex ids:
     servers 0..ns-1 (server s on switch s // servers_per_switch), switches ns.. .  Residuals
     ~ link_cap - U{0..950} when warm (as the fat-tree snapshots), else link_cap."""
     if (n_switches * degree) % 2 or degree >= n_switches:
         raise ValueError("need n_switches * degree even and degree < n_switches")
     rng = _rng(seed)
     ns = n_switches * servers_per_switch
+    stubs = rng.permutation(np.repeat(np.arange(n_switches), degree))
     while True:
-        stubs = rng.permutation(np.repeat(np.arange(n_switches), degree))
         a, b = stubs[0::2], stubs[1::2]
         lo, hi = np.minimum(a, b), np.maximum(a, b)
-        if np.all(lo != hi) and np.unique(lo * n_switches + hi).size == lo.size:
+        key = lo * n_switches + hi
+        _, first = np.unique(key, return_index=True)
+        bad = np.ones(key.size, bool)
+        bad[first] = False
+        bad |= lo == hi
+        if not bad.any():
             break
+        # re-pair the stubs of the bad pairs together with as many random good pairs
+        redo = np.nonzero(bad)[0]
+        good = np.nonzero(~bad)[0]
+        redo = np.concatenate([redo, rng.choice(good, size=min(good.size, redo.size), replace=False)])
+        pos = np.concatenate([2 * redo, 2 * redo + 1])
+        stubs[pos] = rng.permutation(stubs[pos])
     srv = np.arange(ns)
     lu = np.concatenate([srv, ns + lo])
     lv = np.concatenate([ns + srv // servers_per_switch, ns + hi])

@@ -726,7 +726,8 @@ extern "C" {
 // Batch of widest-shortest path queries on one immutable graph (element-wise
 // identical to sequential calls).  Vertices 0..V-1; link l joins lu[l] and lv[l] with
 // residual lr[l].  Outputs per query q: bn[q] bottleneck (-1 infeasible), hops[q] (-1
-// infeasible), path[q * (max_hops + 1) ...] the vertex sequence src..dst (-1 padded).
+// infeasible), path[q * (max_hops + 1) ...] the vertex sequence src..dst (-1 padded; all -1
+// when infeasible or when the path has more than max_hops links).
 void orc_graph_paths(int V, int nl, const int32_t* lu, const int32_t* lv, const int32_t* lr, int nq,
                      const int32_t* src, const int32_t* dst, const int32_t* demand, int32_t* bn, int32_t* hops,
                      int32_t* path, int max_hops, int nthreads) {
@@ -738,8 +739,10 @@ void orc_graph_paths(int V, int nl, const int32_t* lu, const int32_t* lv, const 
     long h = widest_shortest(G, src[q], dst[q], demand[q], &b, &p);
     bn[q] = (int32_t)b;
     hops[q] = (int32_t)h;
-    if (path) {
-      for (int i = 0; i <= max_hops; ++i) path[(size_t)q * (max_hops + 1) + i] = i < (int)p.size() ? p[i] : -1;
+    if (path) {  // the row holds the whole path, or is all -1 (infeasible, or longer than max_hops)
+      const bool fits = h >= 0 && h <= max_hops;
+      for (int i = 0; i <= max_hops; ++i)
+        path[(size_t)q * (max_hops + 1) + i] = (fits && i < (int)p.size()) ? p[i] : -1;
     }
   }
 }

@@ -100,6 +100,17 @@ struct nacs_ctx {
   ncclComm_t comm = nullptr;
   DevArr<unsigned char> sh_buf;
   PinArr sh_ctl;
+  // general topology (nacs_load_graph): CSR adjacency, path-kernel scratch and staging
+  bool has_graph = false;
+  int gV = 0, gns = 0, gL = 0;
+  DevArr<int> g_off;
+  DevArr<int2> g_adj;
+  DevArr<unsigned> g_adj16;
+  bool g_packed = false;
+  DevArr<unsigned> g_scratch;
+  DevArr<int> g_io;
+  DevArr<long long> g_out;
+  DevArr<int> g_ws;
 };
 
 namespace {
@@ -465,6 +476,8 @@ nacs_status finish_stats(nacs_ctx* ctx) {
   ctx->last.ahp_pairs = (int64_t)h[nacs::ST_PAIRS];
   ctx->last.scanned_a = (int64_t)h[nacs::ST_SCAN_A];
   ctx->last.scanned_b = (int64_t)h[nacs::ST_SCAN_B];
+  ctx->last.edges_scanned = (int64_t)h[nacs::ST_EDGES];
+  ctx->last.bfs_runs = (int64_t)h[nacs::ST_BFS];
   ctx->stats_pending = false;
   return NACS_OK;
 }
@@ -753,6 +766,13 @@ void nacs_destroy(nacs_ctx* ctx) {
   ctx->pin_out.release();
   ctx->sh_buf.release();
   ctx->sh_ctl.release();
+  ctx->g_off.release();
+  ctx->g_adj.release();
+  ctx->g_adj16.release();
+  ctx->g_scratch.release();
+  ctx->g_io.release();
+  ctx->g_out.release();
+  ctx->g_ws.release();
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
@@ -994,6 +1014,199 @@ nacs_status nacs_schedule_request(nacs_ctx* ctx, const nacs_options* opt, const 
     if ((st = unstage_outputs(ctx, R, C, V, out))) return st;
   }
   if (!async) {
+    CK(cudaStreamSynchronize(ctx->stream));
+    if ((st = finish_stats(ctx))) return st;
+  }
+  return NACS_OK;
+}
+
+// ---------------------------------------------------------------------------------------
+// General topology: nacs_load_graph, nacs_widest_paths,
+// nacs_logical_bandwidth.  The host builds the CSR layout once per graph; the modified
+// Dijkstra runs in nacs_paths.cu.
+// ---------------------------------------------------------------------------------------
+static nacs::GraphDev graph_dev(nacs_ctx* ctx) {
+  nacs::GraphDev G;
+  G.V = ctx->gV;
+  G.ns = ctx->gns;
+  G.n_adj = 2 * ctx->gL;
+  G.off = ctx->g_off.p;
+  G.adj = ctx->g_adj.p;
+  G.adj16 = ctx->g_packed ? ctx->g_adj16.p : nullptr;
+  return G;
+}
+
+nacs_status nacs_load_graph(nacs_ctx* ctx, const nacs_graph* gr) {
+  if (!ctx) return NACS_EINVAL;
+  ctx->err.clear();
+  if (!gr) return fail(ctx, NACS_EINVAL, "graph: NULL");
+  std::string m;
+  const int V = gr->n_vertices, ns = gr->n_servers, nl = gr->n_links;
+  if (V < 2) m += "n_vertices must be >= 2; ";
+  if (ns < 1 || ns > V) m += "n_servers out of 1..n_vertices; ";
+  if (nl < 0) m += "n_links < 0; ";
+  if (nl > 0 && (!gr->link_u || !gr->link_v || !gr->link_res)) m += "link arrays NULL; ";
+  if (!m.empty()) return fail(ctx, NACS_EINVAL, m);
+  if (V > NACS_MAX_GRAPH_VERTICES || nl > NACS_MAX_GRAPH_LINKS)
+    return fail(ctx, NACS_ETOOBIG, "graph exceeds NACS_MAX_GRAPH_VERTICES / NACS_MAX_GRAPH_LINKS");
+  int bad_end = 0, bad_loop = 0, bad_res = 0;
+  std::vector<int> deg((size_t)V + 1, 0);
+  for (int l = 0; l < nl; ++l) {
+    const int a = gr->link_u[l], b = gr->link_v[l], r = gr->link_res[l];
+    if (a < 0 || a >= V || b < 0 || b >= V) { ++bad_end; continue; }
+    if (a == b) ++bad_loop;
+    if (r < 0 || r > NACS_MAX_CAP) ++bad_res;
+    ++deg[a];
+    ++deg[b];
+  }
+  if (bad_end) m += std::to_string(bad_end) + " link endpoints out of range; ";
+  if (bad_loop) m += std::to_string(bad_loop) + " self-loops; ";
+  if (bad_res) m += std::to_string(bad_res) + " link_res outside [0, NACS_MAX_CAP]; ";
+  if (!m.empty()) return fail(ctx, NACS_EINVAL, m);
+  std::vector<int> off((size_t)V + 1, 0);
+  for (int v = 0; v < V; ++v) off[v + 1] = off[v] + deg[v];
+  std::vector<int> at(off.begin(), off.end() - 1);
+  std::vector<int2> adj((size_t)2 * nl + 1);
+  int max_res = 0;
+  for (int l = 0; l < nl; ++l) {
+    const int a = gr->link_u[l], b = gr->link_v[l], r = gr->link_res[l];
+    adj[at[a]++] = make_int2(b, r);
+    adj[at[b]++] = make_int2(a, r);
+    max_res = std::max(max_res, r);
+  }
+  // packed 4-byte entries for the shared-memory layout (nacs_paths.cu)
+  const bool packed = V <= 65536 && max_res <= 65535;
+  std::vector<unsigned> adj16;
+  if (packed) {
+    adj16.resize(adj.size());
+    for (size_t j = 0; j < adj.size(); ++j) adj16[j] = (unsigned)adj[j].x | ((unsigned)adj[j].y << 16);
+  }
+  CK(cudaSetDevice(ctx->device));
+  CK(ctx->g_off.reserve(off.size()));
+  CK(ctx->g_adj.reserve(adj.size()));
+  CK(cudaMemcpyAsync(ctx->g_off.p, off.data(), off.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->g_adj.p, adj.data(), adj.size() * sizeof(int2), cudaMemcpyHostToDevice, ctx->stream));
+  if (packed) {
+    CK(ctx->g_adj16.reserve(adj16.size()));
+    CK(cudaMemcpyAsync(ctx->g_adj16.p, adj16.data(), adj16.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
+  }
+  CK(cudaStreamSynchronize(ctx->stream));
+  ctx->gV = V;
+  ctx->gns = ns;
+  ctx->gL = nl;
+  ctx->g_packed = packed;
+  ctx->has_graph = true;
+  const nacs::PathLaunch c = nacs::path_launch_config(graph_dev(ctx), ctx->num_sms);
+  if (c.global_bytes) CK(ctx->g_scratch.reserve(c.global_bytes / 4 + 1));
+  return NACS_OK;
+}
+
+static nacs_status begin_graph_call(nacs_ctx* ctx, uint32_t flags) {
+  if (!ctx) return NACS_EINVAL;
+  ctx->err.clear();
+  CK(cudaSetDevice(ctx->device));
+  if (!ctx->has_graph) return fail(ctx, NACS_ENOTOPO, "no graph loaded (nacs_load_graph)");
+  if (flags & ~(NACS_DEVICE_PTRS | NACS_ASYNC)) return fail(ctx, NACS_EINVAL, "flags: only NACS_DEVICE_PTRS | NACS_ASYNC");
+  CK(ctx->stats.reserve(nacs::ST_N));
+  CK(cudaMemsetAsync(ctx->stats.p, 0, sizeof(unsigned long long) * nacs::ST_N, ctx->stream));
+  ctx->stats_pending = true;
+  return NACS_OK;
+}
+
+
+nacs_status nacs_widest_paths(nacs_ctx* ctx, const nacs_path_query* q, uint32_t flags, int32_t* bottleneck,
+                              int32_t* hops, int32_t* path, int32_t max_hops) {
+  nacs_status st = begin_graph_call(ctx, flags);
+  if (st) return st;
+  if (!q || !bottleneck || !hops) return fail(ctx, NACS_EINVAL, "query/bottleneck/hops: NULL");
+  const int nq = q->n_queries;
+  std::string m;
+  if (nq < 0) m += "n_queries < 0; ";
+  if (nq > 0 && (!q->src || !q->dst || !q->demand)) m += "query arrays NULL; ";
+  if (path && max_hops < 0) m += "max_hops < 0; ";
+  if (!m.empty()) return fail(ctx, NACS_EINVAL, m);
+  const bool dev = flags & NACS_DEVICE_PTRS;
+  const int V = ctx->gV;
+  const size_t prow = path ? (size_t)max_hops + 1 : 0;
+  if (!dev) {
+    int bad = 0, first = -1;
+    for (int i = 0; i < nq; ++i) {
+      const int s = q->src[i], t = q->dst[i], d = q->demand[i];
+      if (s < 0 || s >= V || t < 0 || t >= V || s == t || d < 0 || d > NACS_MAX_CAP) {
+        if (first < 0) first = i;
+        ++bad;
+      }
+    }
+    if (bad)
+      return fail(ctx, NACS_EINVAL, std::to_string(bad) + " invalid queries (endpoint out of range, src == dst or demand "
+                                    "outside [0, NACS_MAX_CAP]), first at " + std::to_string(first));
+  }
+  if (nq == 0) return finish_stats(ctx);
+  const nacs::GraphDev G = graph_dev(ctx);
+  const nacs::PathLaunch c = nacs::path_launch_config(G, ctx->num_sms);
+  if (c.global_bytes) CK(ctx->g_scratch.reserve(c.global_bytes / 4 + 1));
+  const int *dsrc, *ddst, *ddem;
+  int *dbn, *dhops, *dpath;
+  if (dev) {
+    dsrc = q->src;
+    ddst = q->dst;
+    ddem = q->demand;
+    dbn = bottleneck;
+    dhops = hops;
+    dpath = path;
+  } else {
+    const size_t in = 3 * (size_t)nq, out = 2 * (size_t)nq + (size_t)nq * prow;
+    CK(ctx->g_io.reserve(in + out));
+    CK(ctx->pin_in.reserve(in * 4));
+    CK(ctx->pin_out.reserve(out * 4));
+    int* hin = reinterpret_cast<int*>(ctx->pin_in.p);
+    parallel_copies({{hin, q->src, (size_t)nq * 4}, {hin + nq, q->dst, (size_t)nq * 4},
+                     {hin + 2 * (size_t)nq, q->demand, (size_t)nq * 4}});
+    CK(cudaMemcpyAsync(ctx->g_io.p, hin, in * 4, cudaMemcpyHostToDevice, ctx->stream));
+    dsrc = ctx->g_io.p;
+    ddst = dsrc + nq;
+    ddem = dsrc + 2 * (size_t)nq;
+    dbn = ctx->g_io.p + in;
+    dhops = dbn + nq;
+    dpath = path ? dhops + nq : nullptr;
+  }
+  CK(ctx->g_ws.reserve(nacs::path_group_ints(V, nq)));
+  CK(nacs::launch_paths(G, c, nq, dsrc, ddst, ddem, dbn, dhops, dpath, max_hops, ctx->g_ws.p, ctx->g_scratch.p,
+                        ctx->stats.p, ctx->stream));
+  if (!dev) {
+    const size_t out = 2 * (size_t)nq + (size_t)nq * prow;
+    int* hout = reinterpret_cast<int*>(ctx->pin_out.p);
+    CK(cudaMemcpyAsync(hout, dbn, out * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    std::vector<CopyJob> jobs{{bottleneck, hout, (size_t)nq * 4}, {hops, hout + nq, (size_t)nq * 4}};
+    if (path) jobs.push_back({path, hout + 2 * (size_t)nq, (size_t)nq * prow * 4});
+    parallel_copies(jobs);
+  }
+  if (!(flags & NACS_ASYNC)) {
+    CK(cudaStreamSynchronize(ctx->stream));
+    if ((st = finish_stats(ctx))) return st;
+    if (dev && ctx->last.invalid)
+      return fail(ctx, NACS_EINVAL, std::to_string(ctx->last.invalid) + " invalid queries (hops = -2)");
+  }
+  return NACS_OK;
+}
+
+nacs_status nacs_logical_bandwidth(nacs_ctx* ctx, uint32_t flags, int64_t* out) {
+  nacs_status st = begin_graph_call(ctx, flags);
+  if (st) return st;
+  if (!out) return fail(ctx, NACS_EINVAL, "out: NULL");
+  const bool dev = flags & NACS_DEVICE_PTRS;
+  const nacs::GraphDev G = graph_dev(ctx);
+  const nacs::PathLaunch c = nacs::path_launch_config(G, ctx->num_sms);
+  if (c.global_bytes) CK(ctx->g_scratch.reserve(c.global_bytes / 4 + 1));
+  long long* dout = reinterpret_cast<long long*>(out);
+  if (!dev) {
+    CK(ctx->g_out.reserve(ctx->gns));
+    dout = ctx->g_out.p;
+  }
+  CK(nacs::launch_logical_bw(G, c, dout, ctx->g_scratch.p, ctx->stats.p, ctx->stream));
+  if (!dev) CK(cudaMemcpyAsync(out, dout, (size_t)ctx->gns * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  if (!(flags & NACS_ASYNC)) {
     CK(cudaStreamSynchronize(ctx->stream));
     if ((st = finish_stats(ctx))) return st;
   }

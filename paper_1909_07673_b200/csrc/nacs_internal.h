@@ -62,7 +62,9 @@ enum {
   ST_PAIRS = 5,
   ST_SCAN_A = 6,  // slots read by pass A / pass B of the TOPSIS warp kernel
   ST_SCAN_B = 7,
-  ST_N = 8
+  ST_EDGES = 8,   // general-topology path kernels: adjacency entries scanned
+  ST_BFS = 9,     // ... and BFS traversals run
+  ST_N = 10
 };
 // Workspace of the warp kernel's chunk layout (k_warp_layout), int words:
 // [0..3] thresholds of the low region | criteria tiles [4 npad] | chunk table [16 nch] | inv[n]
@@ -169,5 +171,32 @@ cudaError_t launch_ahp_pass(int pass, bool fp64, const Geo& g, const Opt& o, int
 cudaError_t launch_ahp_mid(bool fp64, const Geo& g, const Opt& o, int* state, const ShardDev& d, cudaStream_t st);
 cudaError_t launch_ahp_decide(bool fp64, const Geo& g, const Opt& o, int* state, const ReqsDev& R, const OutDev& O,
                               int r, const ShardDev& d, cudaStream_t st);
+
+// General-topology graph (nacs_load_graph, nacs_paths.cu): CSR adjacency of the undirected
+// links, both directions; adj[j] = (neighbour, residual); adj16[j] = neighbour | residual << 16
+// (only when V <= 65536 and every residual <= 65535, else null).
+struct GraphDev {
+  int V, ns;
+  int n_adj;              // 2 * n_links
+  const int* off;         // [V+1]
+  const int2* adj;        // [n_adj]
+  const unsigned* adj16;  // [n_adj] or null
+};
+struct PathLaunch {
+  int grid, warps;
+  bool smem_graph;       // graph + per-warp scratch in shared memory
+  size_t dyn_smem;
+  size_t global_bytes;   // per-warp scratch in global memory (grid * warps * path_warp_bytes) when V is too large
+};
+__host__ __device__ size_t path_warp_bytes(int V, bool smem_mode);
+PathLaunch path_launch_config(const GraphDev& G, int num_sms);
+// queries grouped by destination (one BFS per destination) + per-query BFS for the deferred
+// ones; ws: path_group_ints(V, nq) ints of device workspace
+size_t path_group_ints(int V, int nq);
+cudaError_t launch_paths(const GraphDev& G, const PathLaunch& c, int nq, const int* src, const int* dst,
+                         const int* demand, int* bn, int* hops, int* path, int max_hops, int* ws,
+                         unsigned* gscratch, unsigned long long* stats, cudaStream_t st);
+cudaError_t launch_logical_bw(const GraphDev& G, const PathLaunch& c, long long* out, unsigned* gscratch,
+                              unsigned long long* stats, cudaStream_t st);
 
 }  // namespace nacs

@@ -65,12 +65,23 @@ class Options(C.Structure):
 class Stats(C.Structure):
     _fields_ = [("pod_steps", C.c_int64), ("servers_ranked", C.c_int64), ("retries", C.c_int64),
                 ("fp64_decisions", C.c_int64), ("invalid", C.c_int64), ("feasible", C.c_int64),
-                ("ahp_pairs", C.c_int64), ("scanned_a", C.c_int64), ("scanned_b", C.c_int64)]
+                ("ahp_pairs", C.c_int64), ("scanned_a", C.c_int64), ("scanned_b", C.c_int64),
+                ("edges_scanned", C.c_int64), ("bfs_runs", C.c_int64)]
+
+
+class Graph(C.Structure):
+    _fields_ = [("n_vertices", C.c_int32), ("n_servers", C.c_int32), ("n_links", C.c_int32),
+                ("link_u", C.c_void_p), ("link_v", C.c_void_p), ("link_res", C.c_void_p)]
+
+
+class PathQuery(C.Structure):
+    _fields_ = [("n_queries", C.c_int32), ("src", C.c_void_p), ("dst", C.c_void_p), ("demand", C.c_void_p)]
 
 
 EXPORTS = ["nacs_create", "nacs_create_sharded", "nacs_nccl_unique_id", "nacs_destroy", "nacs_load_topology",
            "nacs_read_topology", "nacs_rank_ahp", "nacs_rank_topsis", "nacs_schedule_request",
-           "nacs_schedule_batch", "nacs_last_stats", "nacs_last_error"]
+           "nacs_schedule_batch", "nacs_last_stats", "nacs_last_error", "nacs_load_graph", "nacs_widest_paths",
+           "nacs_logical_bandwidth"]
 
 _lib = None
 
@@ -96,6 +107,9 @@ def lib():
         for f in (L.nacs_schedule_request, L.nacs_schedule_batch):
             f.argtypes = [vp, C.POINTER(Options), C.POINTER(Requests), C.POINTER(Placements)]
         L.nacs_last_stats.argtypes = [vp, C.POINTER(Stats)]
+        L.nacs_load_graph.argtypes = [vp, C.POINTER(Graph)]
+        L.nacs_widest_paths.argtypes = [vp, C.POINTER(PathQuery), C.c_uint32, vp, vp, vp, C.c_int32]
+        L.nacs_logical_bandwidth.argtypes = [vp, C.c_uint32, vp]
         L.nacs_last_error.argtypes = [vp]
         L.nacs_last_error.restype = C.c_char_p
         for name in EXPORTS:
@@ -280,6 +294,49 @@ class Context:
     def schedule_batch(self, reqs: dict, method, weights, out=None, flags=0, **kw) -> dict:
         """Every request against the same snapshot (snapshot isolation); the state is unchanged."""
         return self._schedule(self._lib.nacs_schedule_batch, reqs, method, weights, out, flags, **kw)
+
+    # ----------------------------------------------------- general topology ---
+    def load_graph(self, graph: dict):
+        """An arbitrary undirected DC graph: dict(n_vertices, n_servers, link_u, link_v, link_res)."""
+        keep = [_i32(graph[k]) for k in ("link_u", "link_v", "link_res")]
+        g = Graph(int(graph["n_vertices"]), int(graph["n_servers"]), keep[0].size, *[_np_ptr(a) for a in keep])
+        self._check(self._lib.nacs_load_graph(self._h, C.byref(g)))
+        self.graph_V = int(graph["n_vertices"])
+        self.graph_ns = int(graph["n_servers"])
+
+    def widest_paths(self, src, dst, demand, max_hops=None, with_path=True, out=None, flags=0):
+        """Widest-shortest path per (src, dst, demand) query (modified Dijkstra).
+        numpy inputs -> numpy outputs (bottleneck, hops, path[nq, max_hops+1] or None); torch CUDA
+        inputs -> torch outputs (device pointers).  out: preallocated (bn, hops, path) to reuse."""
+        dev = _is_torch(src)
+        if not dev:
+            src, dst, demand = _i32(src), _i32(dst), _i32(demand)
+        nq = int(src.numel() if dev else src.size)
+        if max_hops is None:
+            max_hops = 16
+        if out is None:
+            if dev:
+                import torch
+                mk = lambda *shape: torch.empty(shape, dtype=torch.int32, device=src.device)
+            else:
+                mk = lambda *shape: np.zeros(shape, np.int32)
+            out = (mk(max(nq, 1)), mk(max(nq, 1)), mk(max(nq, 1), max_hops + 1) if with_path else None)
+        bn, hops, path = out
+        q = PathQuery(nq, _ptr(src), _ptr(dst), _ptr(demand))
+        if dev:
+            flags |= NACS_DEVICE_PTRS
+        self._check(self._lib.nacs_widest_paths(self._h, C.byref(q), flags, _ptr(bn), _ptr(hops), _ptr(path),
+                                                int(max_hops)))
+        return bn[:nq], hops[:nq], (None if path is None else path[:nq])
+
+    def logical_bandwidth(self, out=None, flags=0):
+        """R2 alternative criterion: int64[n_servers], sum of widest-shortest bottlenecks."""
+        if out is None:
+            out = np.zeros(self.graph_ns, np.int64)
+        if _is_torch(out):
+            flags |= NACS_DEVICE_PTRS
+        self._check(self._lib.nacs_logical_bandwidth(self._h, flags, _ptr(out)))
+        return out
 
     def last_stats(self) -> dict:
         s = Stats()

@@ -229,3 +229,12 @@ def test_hops_equal_scipy_bfs_random_dc():
         assert hops[i] == (-1 if np.isinf(t) else int(t))
         detours += bool(hops[i] > free[i, q["dst"][i]])
     assert detours > 0
+
+
+def test_path_rows_longer_than_max_hops_are_empty():
+    """Output convention (include/nacs.h): a path with more links than max_hops is not
+    truncated; its row is all -1 while bottleneck and hops are still reported."""
+    g = gen.fat_tree_graph(gen.snapshot(4, warm=False))
+    bn, hops, path = O.graph_paths(g, [0, 0], [1, 15], [0, 0], max_hops=4)
+    assert hops.tolist() == [2, 6] and bn.tolist() == [1000, 1000]
+    assert path[0].tolist() == [0, 16, 1, -1, -1] and path[1].tolist() == [-1] * 5
