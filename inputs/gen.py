@@ -283,3 +283,20 @@ def path_queries(graph: dict, n_queries: int, seed: int, bw_hi: int = 50) -> dic
     dem = rng.integers(1, bw_hi, size=n_queries, endpoint=True)
     i32 = lambda x: np.ascontiguousarray(x, dtype=np.int32)
     return dict(src=i32(src), dst=i32(dst), demand=i32(dem))
+
+
+
+# ---------------------------------------------------------------------------
+# Discrete-event workload: the E2 campaign of P:396-398 — a fresh
+# k=20 fat-tree, 6000 requests of 4 containers "with a running time up to 250 events from a
+# complete execution of 500 events", up to 50% of containers in pods, pair bandwidth up to
+# 50 Mbps.  Arrival ticks ~U{0..horizon-1}, durations ~U{1..max_duration} (reading R28).
+# ---------------------------------------------------------------------------
+
+def sim_workload(n_req: int = 6000, seed: int = 6, horizon: int = 500, max_duration: int = 250,
+                 n_containers: int = 4) -> tuple[dict, np.ndarray, np.ndarray]:
+    reqs = requests(n_req, seed, nc_lo=n_containers, nc_hi=n_containers)
+    rng = _rng(seed + 500)
+    arrival = rng.integers(0, horizon, size=n_req).astype(np.int32)
+    duration = rng.integers(1, max_duration, size=n_req, endpoint=True).astype(np.int32)
+    return reqs, arrival, duration

@@ -107,7 +107,7 @@ double fabric_widest_from_edge(const DC& dc, int e, int v) {
 // Options (DESIGN.md readings).
 // ---------------------------------------------------------------------------
 struct Opts {
-  int method;       // 0 AHP, 1 TOPSIS
+  int method;       // 0 AHP, 1 TOPSIS, 2 BF (bin packing), 3 WF (spread): baselines of P:207-209
   double w[4];      // W over (CPU, RAM, Fragmentation, Bandwidth), T4 P:319-330 (R1)
   int ahp_rule;     // 0 literal (R8), 1 shifted
   int l1_mode;      // 0 pairwise comparison on W (R10), 1 L1 = W
@@ -220,6 +220,22 @@ RankOut rank(const DC& dc, const Opts& o, long dem_cpu, long dem_ram,
     }
   };
 
+  if (o.method >= 2) {
+    // BF / WF baselines ("the native algorithms offered by containers
+    // orchestrators, BF (binpacking) and WF (spread)"; reading R27): the server's load is
+    // the mean residual fraction of CPU and RAM, (cpu/cpu_cap + ram/ram_cap) / 2,
+    // compared exactly as the integer cpu*ram_cap + ram*cpu_cap.  BF takes the most loaded
+    // feasible server (smallest residual), WF the least loaded; ties lowest index.
+    for (int u : F) {
+      double key = (double)dc.cpu[u] * (double)dc.ram_cap + (double)dc.ram[u] * (double)dc.cpu_cap;
+      r.score[u] = o.method == 2 ? -key : key;
+    }
+    int best = F[0];
+    for (int u : F) if (r.score[u] > r.score[best]) best = u;
+    r.best = best;
+    for (int u : F) r.tie[u] = r.score[u] == r.score[best];  // integer keys: exact ties only
+    return r;
+  }
   if (o.method == 1) {
     // TOPSIS (readings R12-R13) over the feasible set F (R4).
     double N[4];
@@ -489,7 +505,9 @@ Opts make_opts(int method, const double* w, int ahp_rule, int l1_mode, int path_
   for (int c = 0; c < 4; ++c) o.w[c] = w[c];
   o.ahp_rule = ahp_rule;
   o.l1_mode = l1_mode;
-  o.path_filter = path_filter;
+  // BF and WF "natively ignore the network requirements"; "a shortest-path search after the
+  // allocation of servers": the CPU/RAM-only filter, then routing (R6 flag 0)
+  o.path_filter = method >= 2 ? 0 : path_filter;
   return o;
 }
 
@@ -625,6 +643,176 @@ int orc_schedule(int k, int cpu_cap, int ram_cap, int link_cap, int32_t* cpu, in
 
 }  // extern "C"
 
+
+// ===========================================================================
+// Departures and the discrete-event simulator (P:206 and P:391
+// "a discrete event simulator"; P:396-398 the E2 campaign; T5 P:416-426 its metrics).
+// ===========================================================================
+namespace {
+
+// Release an accepted placement: the exact inverse of its commit and top-up.
+// f_u is re-derived as "some residual below capacity" (R22), so on a DC whose activity
+// flags follow R22 apply-then-release is the identity.
+void release_one(DC& dc, const Req& q, const Placement& pl) {
+  for (int i = 0; i < q.nC; ++i) {
+    int u = pl.server[i];
+    dc.cpu[u] += pl.cpu_a[i];
+    dc.ram[u] += pl.ram_a[i];
+  }
+  for (int e = 0; e < q.nV; ++e) {
+    int us = pl.server[q.src[e]], ud = pl.server[q.dst[e]];
+    if (us == ud) continue;  // host bus: no link carried it
+    std::vector<Path> cands = candidate_paths(dc, us, ud);
+    for (const Path& c : cands)
+      if (c.id == pl.path[e]) {
+        dc.link[dc.access(us)] += pl.bw_a[e];
+        dc.link[dc.access(ud)] += pl.bw_a[e];
+        for (int l : c.fabric) dc.link[l] += pl.bw_a[e];
+      }
+  }
+  for (int i = 0; i < q.nC; ++i) {
+    int u = pl.server[i];
+    dc.active[u] = (dc.cpu[u] < dc.cpu_cap || dc.ram[u] < dc.ram_cap) ? 1 : 0;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+// Release the accepted requests (status 1) of a batch against the state, in request order.
+void orc_release(int k, int cpu_cap, int ram_cap, int link_cap, int32_t* cpu, int32_t* ram, uint8_t* active,
+                 int32_t* link, int n_req, const int32_t* coff, const int32_t* cpu_min, const int32_t* cpu_max,
+                 const int32_t* ram_min, const int32_t* ram_max, const int32_t* pod_of, const int32_t* voff,
+                 const int32_t* vsrc, const int32_t* vdst, const int32_t* bw_min, const int32_t* bw_max,
+                 const int32_t* status, const int32_t* server, const int32_t* cpu_a, const int32_t* ram_a,
+                 const int32_t* bw_a, const int32_t* path) {
+  DC dc = make_dc(k, cpu_cap, ram_cap, link_cap, cpu, ram, active, link);
+  for (int r = 0; r < n_req; ++r) {
+    if (status[r] != 1) continue;
+    Req q{coff[r + 1] - coff[r], voff[r + 1] - voff[r], cpu_min + coff[r], cpu_max + coff[r], ram_min + coff[r],
+          ram_max + coff[r], pod_of + coff[r], vsrc + voff[r], vdst + voff[r], bw_min + voff[r], bw_max + voff[r]};
+    Placement pl;
+    pl.server.assign(server + coff[r], server + coff[r + 1]);
+    pl.cpu_a.assign(cpu_a + coff[r], cpu_a + coff[r + 1]);
+    pl.ram_a.assign(ram_a + coff[r], ram_a + coff[r + 1]);
+    pl.bw_a.assign(bw_a + voff[r], bw_a + voff[r + 1]);
+    pl.path.assign(path + voff[r], path + voff[r + 1]);
+    release_one(dc, q, pl);
+  }
+  for (int u = 0; u < dc.n; ++u) {
+    cpu[u] = (int32_t)dc.cpu[u];
+    ram[u] = (int32_t)dc.ram[u];
+    active[u] = (uint8_t)dc.active[u];
+  }
+  for (int l = 0; l < dc.L; ++l) link[l] = (int32_t)dc.link[l];
+}
+
+// Discrete-event simulation (reading R28; SPEC S:519 event loop).  Ticks
+// t = 0, 1, 2, ...: (1) release the requests whose start + duration == t; (2) enqueue the
+// requests arriving at t (ascending id); (3) offer queued requests in FIFO order to the
+// scheduler on the live state (sequential semantics): an accepted request leaves
+// the queue and holds its resources for `duration` ticks; a refused one stays queued
+// (with hol = 1 the scan of this tick stops at it, head-of-line blocking).  The run ends
+// after the first tick at which no request is queued or still to arrive ("events", T5
+// "# Events"), or after max_ticks ticks (requests still queued are then rejected).
+// Per request: start tick (-1 never), attempts, and its final placement; per tick:
+// active servers |N^s'|, active links |E^s'| (residual below capacity) and
+// the queue length after the tick.  totals: [events, attempts, accepted, pod_steps,
+// retries, excused_ties, hint_mismatch].
+void orc_simulate(int k, int cpu_cap, int ram_cap, int link_cap, int32_t* cpu, int32_t* ram, uint8_t* active,
+                  int32_t* link, int method, const double* w, int ahp_rule, int l1_mode, int path_filter,
+                  int n_req, const int32_t* coff, const int32_t* cpu_min, const int32_t* cpu_max,
+                  const int32_t* ram_min, const int32_t* ram_max, const int32_t* pod_of, const int32_t* voff,
+                  const int32_t* vsrc, const int32_t* vdst, const int32_t* bw_min, const int32_t* bw_max,
+                  const int32_t* arrival, const int32_t* duration, int max_ticks, int hol, const int32_t* hint,
+                  int32_t* start, int32_t* attempts, int32_t* status, int32_t* server, int32_t* cpu_a,
+                  int32_t* ram_a, int32_t* bw_a, int32_t* path, int32_t* tick_servers, int32_t* tick_links,
+                  int32_t* tick_queue, int64_t* totals) {
+  DC dc = make_dc(k, cpu_cap, ram_cap, link_cap, cpu, ram, active, link);
+  Opts o = make_opts(method, w, ahp_rule, l1_mode, path_filter);
+  auto mkreq = [&](int r) {
+    return Req{coff[r + 1] - coff[r], voff[r + 1] - voff[r], cpu_min + coff[r], cpu_max + coff[r], ram_min + coff[r],
+               ram_max + coff[r], pod_of + coff[r], vsrc + voff[r], vdst + voff[r], bw_min + voff[r], bw_max + voff[r]};
+  };
+  std::vector<Placement> placed(n_req);
+  std::vector<int> order(n_req);
+  for (int r = 0; r < n_req; ++r) {
+    order[r] = r;
+    start[r] = -1;
+    attempts[r] = 0;
+    status[r] = 0;
+  }
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return arrival[a] < arrival[b]; });
+  std::vector<int> queue;
+  Counters cnt;
+  long n_attempts = 0, accepted = 0;
+  size_t next_arrival = 0;
+  int t = 0;
+  for (; t < max_ticks; ++t) {
+    // (1) departures first
+    for (int r = 0; r < n_req; ++r)
+      if (start[r] >= 0 && start[r] + duration[r] == t) release_one(dc, mkreq(r), placed[r]);
+    // (2) arrivals
+    while (next_arrival < order.size() && arrival[order[next_arrival]] == t) queue.push_back(order[next_arrival++]);
+    // (3) FIFO scan of the queue
+    std::vector<int> left;
+    bool blocked = false;
+    for (int r : queue) {
+      if (blocked) { left.push_back(r); continue; }
+      Req q = mkreq(r);
+      Placement pl = schedule_one(dc, o, q, hint ? hint + coff[r] : nullptr, cnt);
+      ++n_attempts;
+      ++attempts[r];
+      if (pl.status == 1) {
+        placed[r] = pl;
+        start[r] = t;
+        status[r] = 1;
+        ++accepted;
+      } else {
+        if (pl.status == -1) status[r] = -1;
+        if (pl.status == -1) continue;  // invalid: dropped from the queue
+        left.push_back(r);
+        if (hol) blocked = true;
+      }
+    }
+    queue.swap(left);
+    int as = 0, al = 0;
+    for (int u = 0; u < dc.n; ++u) as += dc.active[u] ? 1 : 0;
+    for (int l = 0; l < dc.L; ++l) al += dc.link[l] < dc.link_cap ? 1 : 0;
+    tick_servers[t] = as;
+    tick_links[t] = al;
+    tick_queue[t] = (int)queue.size();
+    if (queue.empty() && next_arrival == order.size()) { ++t; break; }
+  }
+  for (int r = 0; r < n_req; ++r) {
+    const Placement& pl = placed[r];
+    for (int i = 0; i < coff[r + 1] - coff[r]; ++i) {
+      server[coff[r] + i] = status[r] == 1 ? pl.server[i] : -1;
+      cpu_a[coff[r] + i] = status[r] == 1 ? pl.cpu_a[i] : 0;
+      ram_a[coff[r] + i] = status[r] == 1 ? pl.ram_a[i] : 0;
+    }
+    for (int e = 0; e < voff[r + 1] - voff[r]; ++e) {
+      bw_a[voff[r] + e] = status[r] == 1 ? pl.bw_a[e] : 0;
+      path[voff[r] + e] = status[r] == 1 ? pl.path[e] : -1;
+    }
+  }
+  for (int u = 0; u < dc.n; ++u) {
+    cpu[u] = (int32_t)dc.cpu[u];
+    ram[u] = (int32_t)dc.ram[u];
+    active[u] = (uint8_t)dc.active[u];
+  }
+  for (int l = 0; l < dc.L; ++l) link[l] = (int32_t)dc.link[l];
+  totals[0] = t;
+  totals[1] = n_attempts;
+  totals[2] = accepted;
+  totals[3] = cnt.pod_steps;
+  totals[4] = cnt.retries;
+  totals[5] = cnt.excused_ties;
+  totals[6] = cnt.hint_mismatch;
+}
+
+}  // extern "C"
 
 // ===========================================================================
 // General topology: the "modified Dijkstra" of P:383-386

@@ -16,7 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(HERE, "nacs_oracle.cpp")
 LIB = os.path.join(HERE, "liboracle.so")
 
-METHOD = {"ahp": 0, "topsis": 1}
+METHOD = {"ahp": 0, "topsis": 1, "bf": 2, "wf": 3}
 # Table 4: (CPU, RAM, Fragmentation, Bandwidth)
 SCHEMAS = {"flat": (0.25, 0.25, 0.25, 0.25),
            "clustering": (0.17, 0.17, 0.5, 0.16),
@@ -49,6 +49,11 @@ def lib():
         _lib.orc_schedule.restype = C.c_int
         _lib.orc_schedule.argtypes = [C.c_int] * 4 + [P] * 4 + [C.c_int, P, C.c_int, C.c_int, C.c_int,
                                                           C.c_int, C.c_int, C.c_int] + [P] * 19 + [C.c_int]
+        _lib.orc_release.restype = None
+        _lib.orc_release.argtypes = [C.c_int] * 4 + [P] * 4 + [C.c_int] + [P] * 17
+        _lib.orc_simulate.restype = None
+        _lib.orc_simulate.argtypes = ([C.c_int] * 4 + [P] * 4 + [C.c_int, P, C.c_int, C.c_int, C.c_int, C.c_int]
+                                      + [P] * 13 + [C.c_int, C.c_int] + [P] * 13)
         _lib.orc_graph_paths.restype = None
         _lib.orc_graph_paths.argtypes = [C.c_int, C.c_int, P, P, P, C.c_int, P, P, P, P, P, P, C.c_int, C.c_int]
         _lib.orc_logical_bandwidth.restype = None
@@ -190,3 +195,52 @@ def logical_bandwidth(graph: dict, nthreads: int | None = None) -> np.ndarray:
         nthreads = len(os.sched_getaffinity(0))
     lib().orc_logical_bandwidth(V, ns, lu.size, _p(lu), _p(lv), _p(lr), _p(out), int(nthreads))
     return out
+
+
+REQ_KEYS = ("container_off", "cpu_min", "cpu_max", "ram_min", "ram_max", "pod_of", "vlink_off", "vl_src", "vl_dst",
+            "bw_min", "bw_max")
+OUT_KEYS = ("status", "server_of_container", "cpu_alloc", "ram_alloc", "bw_alloc", "path_of_vlink")
+
+
+def _state(snap):
+    return (_i32(snap["cpu_res"]).copy(), _i32(snap["ram_res"]).copy(),
+            np.ascontiguousarray(snap["active"], dtype=np.uint8).copy(), _i32(snap["link_res"]).copy())
+
+
+def release(snap: dict, reqs: dict, placements: dict) -> dict:
+    """Departure of every accepted request (status 1): the state after releasing them."""
+    cpu, ram, act, link = _state(snap)
+    arr = [_i32(reqs[k]) for k in REQ_KEYS]
+    out = [_i32(placements[k]) for k in OUT_KEYS]
+    lib().orc_release(snap["k"], snap["cpu_cap"], snap["ram_cap"], snap["link_cap"], _p(cpu), _p(ram), _p(act),
+                      _p(link), int(reqs["n_requests"]), *[_p(a) for a in arr], *[_p(a) for a in out])
+    return dict(snap, cpu_res=cpu, ram_res=ram, active=act, link_res=link)
+
+
+def simulate(snap: dict, reqs: dict, arrival, duration, method: str, weights, max_ticks: int, hol: int = 1,
+             hint=None, ahp_rule: int = 0, l1_mode: int = 0, path_filter: int = 1) -> dict:
+    """Discrete-event simulation (reading R28).  Returns per-request start / attempts / status,
+    the final placements, per-tick series and totals."""
+    cpu, ram, act, link = _state(snap)
+    R = int(reqs["n_requests"])
+    Cn, Vn = int(reqs["container_off"][-1]), int(reqs["vlink_off"][-1])
+    arr = [_i32(reqs[k]) for k in REQ_KEYS]
+    start, attempts, status = (np.zeros(max(R, 1), np.int32) for _ in range(3))
+    server, cpu_a, ram_a = (np.zeros(max(Cn, 1), np.int32) for _ in range(3))
+    bw_a, path = np.zeros(max(Vn, 1), np.int32), np.zeros(max(Vn, 1), np.int32)
+    ts, tl, tq = (np.zeros(max_ticks, np.int32) for _ in range(3))
+    tot = np.zeros(7, np.int64)
+    hint_a = None if hint is None else _i32(hint)
+    lib().orc_simulate(snap["k"], snap["cpu_cap"], snap["ram_cap"], snap["link_cap"], _p(cpu), _p(ram), _p(act),
+                       _p(link), METHOD[method], _p(_weights(weights)), ahp_rule, l1_mode, path_filter, R,
+                       *[_p(a) for a in arr], _p(_i32(arrival)), _p(_i32(duration)), int(max_ticks), int(hol),
+                       _p(hint_a), _p(start), _p(attempts), _p(status), _p(server), _p(cpu_a), _p(ram_a), _p(bw_a),
+                       _p(path), _p(ts), _p(tl), _p(tq), _p(tot))
+    T = int(tot[0])
+    return dict(start=start[:R], attempts=attempts[:R], status=status[:R],
+                placements=dict(status=status[:R], server_of_container=server[:Cn], cpu_alloc=cpu_a[:Cn],
+                                ram_alloc=ram_a[:Cn], bw_alloc=bw_a[:Vn], path_of_vlink=path[:Vn]),
+                tick_servers=ts[:T], tick_links=tl[:T], tick_queue=tq[:T],
+                totals=dict(zip(("events", "attempts", "accepted", "pod_steps", "retries", "excused_ties",
+                                 "hint_mismatch"), tot.tolist())),
+                state=dict(snap, cpu_res=cpu, ram_res=ram, active=act, link_res=link))
