@@ -45,7 +45,13 @@ typedef enum {
   NACS_ETOOBIG = 6   /* a size limit below is exceeded */
 } nacs_status;
 
-typedef enum { NACS_AHP = 0, NACS_TOPSIS = 1 } nacs_method;
+/* NACS_BF / NACS_WF: the container orchestrators' native baselines the paper compares
+ * against, "BF (binpacking) and WF (spread)" with "a shortest-path search after the
+ * allocation of servers" (§IV; T5 P:416-426; reading R27): the feasible server
+ * (CPU/RAM filter; options.path_filter is ignored and taken as 0) of smallest (BF) or
+ * largest (WF) mean residual fraction (cpu/cpu_cap + ram/ram_cap)/2, ties lowest index;
+ * routing, R18 retries and the R19 top-up as for the heuristics.  Schedule calls only. */
+typedef enum { NACS_AHP = 0, NACS_TOPSIS = 1, NACS_BF = 2, NACS_WF = 3 } nacs_method;
 
 /* nacs_options.flags */
 #define NACS_DEVICE_PTRS 1u  /* arrays are device pointers */
@@ -198,6 +204,54 @@ nacs_status nacs_schedule_request(nacs_ctx *ctx, const nacs_options *opt, const 
  * private overlay (R21): requests do not see each other and the state is not modified. */
 nacs_status nacs_schedule_batch(nacs_ctx *ctx, const nacs_options *opt, const nacs_requests *batch,
                                 nacs_placements *out);
+
+/* ---------------------------------------------------------------------------------------
+ * Departures and the discrete-event simulator: "a discrete event
+ * simulator" drives the scheduler; the E2 campaign and its
+ * metrics "# Events", runtime, U(ij), U(i) (T5 P:416-426), fragmentation F(N^s), F(E^s)
+ * (P:111-112).
+ * ------------------------------------------------------------------------------------- */
+
+/* Release the accepted requests (status 1) of a batch the context scheduled earlier
+ * (nacs_schedule_request): every container's c^a and every vlink's bw^a return to the
+ * state (the exact inverse of commit and top-up); f_u of the touched servers is re-derived
+ * as "some residual below capacity" (R22).  reqs/pl: the batch and its placements as
+ * returned.  flags: NACS_DEVICE_PTRS | NACS_ASYNC.  A placement that does not match the
+ * fat-tree, or a release that would raise a residual above its capacity (e.g. released
+ * twice), fails with NACS_EINVAL and changes nothing (without NACS_ASYNC). */
+nacs_status nacs_release(nacs_ctx *ctx, uint32_t flags, const nacs_requests *reqs, const nacs_placements *pl);
+
+typedef struct {
+  int32_t max_ticks;     /* the run ends after this many ticks at the latest (>= 1) */
+  int32_t hol_blocking;  /* 1: FIFO with head-of-line blocking; 0: scan the whole queue */
+} nacs_sim_config;
+
+typedef struct {  /* caller-allocated arrays; scalars written by the call */
+  int32_t *start_tick;    /* [n_requests] tick of acceptance, -1 if never accepted */
+  int32_t *attempts;      /* [n_requests] scheduling attempts */
+  int32_t *tick_servers;  /* [max_ticks] active servers |N^s'| after each tick */
+  int32_t *tick_links;    /* [max_ticks] active links |E^s'| (residual below capacity) */
+  int32_t *tick_queue;    /* [max_ticks] queued requests after each tick */
+  int64_t events;         /* ticks simulated (T5 "# Events"; entries >= events untouched) */
+  int64_t attempts_total; /* scheduler invocations */
+  int64_t accepted;
+  double sched_seconds;   /* wall time inside the scheduling attempts (T5 "runtime") */
+  double wall_seconds;    /* wall time of the whole call */
+} nacs_sim_report;
+
+/* Discrete-event simulation on the context's live state (reading R28).  Ticks t = 0, 1, ...:
+ * (1) the requests whose start + duration == t depart (nacs_release); (2) the requests with
+ * arrival == t join the queue in ascending id; (3) queued requests are offered in FIFO order
+ * to the scheduler (nacs_schedule_request semantics with opt); an accepted request leaves
+ * the queue and holds its resources for duration ticks; a refused one stays queued (with
+ * hol_blocking the scan of the tick stops there).  The run ends after the first tick with
+ * an empty queue and no arrival left, or after max_ticks (still-queued requests are then
+ * rejected).  out: the final placements (status 1 accepted, 0 never accepted, -1 invalid).
+ * Afterwards the state holds the requests that have not departed.  Host pointers only;
+ * synchronous; arrival >= 0, duration >= 1; AHP/TOPSIS/BF/WF with rank_mode per pod. */
+nacs_status nacs_simulate(nacs_ctx *ctx, const nacs_options *opt, const nacs_requests *reqs, const int32_t *arrival,
+                          const int32_t *duration, const nacs_sim_config *cfg, nacs_placements *out,
+                          nacs_sim_report *rep);
 
 /* ---------------------------------------------------------------------------------------
  * General topology.  "A modified Dijkstra algorithm is used to compute

@@ -398,10 +398,8 @@ Placement schedule_one(DC& dc, const Opts& o, const Req& q, const int32_t* hint,
       }
       int u = r.best;
       int hp = hint_pod[p];
-      if (hp >= 0 && hp < dc.n && hp != u) {
-        if (r.tie[hp]) { u = hp; cnt.excused_ties += 1; }
-        else cnt.hint_mismatch += 1;
-      }
+      // R14 resync on floating-point near-ties only: BF / WF decide on exact integer keys
+      if (o.method < 2 && hp >= 0 && hp < dc.n && hp != u && r.tie[hp]) { u = hp; cnt.excused_ties += 1; }
 
       // a8 commit (Eq. 4-5; readings R16-R18).
       DC before = dc;
@@ -427,6 +425,9 @@ Placement schedule_one(DC& dc, const Opts& o, const Req& q, const int32_t* hint,
         cnt.retries += 1;
         continue;
       }
+      // the hint names the server the other implementation finally committed the pod to: an
+      // attempt that an R18 routing failure discards is no mismatch
+      if (hp >= 0 && hp < dc.n && hp != u) cnt.hint_mismatch += 1;
       srv[p] = u;
       for (int e = 0; e < q.nV; ++e) {
         int pa = q.pod_of[q.src[e]], pb = q.pod_of[q.dst[e]];

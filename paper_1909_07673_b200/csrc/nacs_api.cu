@@ -111,6 +111,10 @@ struct nacs_ctx {
   DevArr<int> g_io;
   DevArr<long long> g_out;
   DevArr<int> g_ws;
+  // departures / simulator
+  DevArr<long long> rel_delta;
+  DevArr<int> sim_buf;
+  PinArr sim_pin;
 };
 
 namespace {
@@ -135,7 +139,7 @@ nacs_status cuda_fail(nacs_ctx* c, cudaError_t e, const char* where) {
 nacs_status check_options(nacs_ctx* ctx, const nacs_options* o, Opt* out) {
   if (!o) return fail(ctx, NACS_EINVAL, "options: NULL");
   std::string m;
-  if (o->method != NACS_AHP && o->method != NACS_TOPSIS) m += "options.method not AHP/TOPSIS; ";
+  if (o->method < NACS_AHP || o->method > NACS_WF) m += "options.method not AHP/TOPSIS/BF/WF; ";
   double sum = 0;
   for (int k = 0; k < 4; ++k) {
     if (!std::isfinite(o->weights[k]) || o->weights[k] < 0) m += "options.weights[" + std::to_string(k) + "] not finite and >= 0; ";
@@ -147,12 +151,14 @@ nacs_status check_options(nacs_ctx* ctx, const nacs_options* o, Opt* out) {
   if (o->path_filter != 0 && o->path_filter != 1) m += "options.path_filter not 0/1; ";
   if (o->flags & ~(NACS_DEVICE_PTRS | NACS_ASYNC | NACS_EXACT_FP64)) m += "options.flags has unknown bits; ";
   if (o->rank_mode != NACS_RANK_PER_POD && o->rank_mode != NACS_RANK_ONCE) m += "options.rank_mode not 0/1; ";
+  if (o->method >= NACS_BF && o->rank_mode == NACS_RANK_ONCE) m += "options.rank_mode = NACS_RANK_ONCE needs AHP/TOPSIS; ";
   if (!m.empty()) return fail(ctx, NACS_EINVAL, m);
   out->method = (int)o->method;
   for (int k = 0; k < 4; ++k) out->wd[k] = o->weights[k];
   out->ahp_rule = o->ahp_rule;
   out->l1_mode = o->l1_mode;
-  out->path_filter = o->path_filter;
+  // BF / WF ignore the network at selection and route afterwards (R27)
+  out->path_filter = o->method >= NACS_BF ? 0 : o->path_filter;
   out->exact64 = (o->flags & NACS_EXACT_FP64) ? 1 : 0;
   out->rank_once = o->rank_mode == NACS_RANK_ONCE;
   return NACS_OK;
@@ -773,6 +779,9 @@ void nacs_destroy(nacs_ctx* ctx) {
   ctx->g_io.release();
   ctx->g_out.release();
   ctx->g_ws.release();
+  ctx->rel_delta.release();
+  ctx->sim_buf.release();
+  ctx->sim_pin.release();
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
@@ -994,6 +1003,8 @@ nacs_status nacs_schedule_request(nacs_ctx* ctx, const nacs_options* opt, const 
   // the sharded engine: server-sharded contexts, and (grid-wide level passes) AHP on big topologies
   if (o.rank_once && (ctx->world > 1 || ctx->comm))
     return fail(ctx, NACS_EINVAL, "options.rank_mode = NACS_RANK_ONCE is not available on server-sharded contexts");
+  if (o.method >= NACS_BF && (ctx->world > 1 || ctx->comm))
+    return fail(ctx, NACS_EINVAL, "BF / WF are not available on server-sharded contexts");
   if (ctx->world > 1 || ctx->comm || (o.method == NACS_AHP && g.n >= 4096 && !o.rank_once)) {
     if ((st = schedule_sharded(ctx, o, Rd, Od, R))) return st;
     if (!dev) {
@@ -1018,6 +1029,190 @@ nacs_status nacs_schedule_request(nacs_ctx* ctx, const nacs_options* opt, const 
     if ((st = finish_stats(ctx))) return st;
   }
   return NACS_OK;
+}
+
+// ---------------------------------------------------------------------------------------
+// Departures and the discrete-event simulator.
+// ---------------------------------------------------------------------------------------
+nacs_status nacs_release(nacs_ctx* ctx, uint32_t flags, const nacs_requests* reqs, const nacs_placements* pl) {
+  nacs_status st = begin_call(ctx);
+  if (st) return st;
+  if (flags & ~(NACS_DEVICE_PTRS | NACS_ASYNC)) return fail(ctx, NACS_EINVAL, "flags: only NACS_DEVICE_PTRS | NACS_ASYNC");
+  if ((st = check_placements(ctx, pl))) return st;
+  if (!reqs) return fail(ctx, NACS_EINVAL, "requests: NULL");
+  if (ctx->world > 1 || ctx->comm) return fail(ctx, NACS_EINVAL, "nacs_release is not available on server-sharded contexts");
+  const Geo& g = ctx->g;
+  const bool dev = flags & NACS_DEVICE_PTRS;
+  const int R = reqs->n_requests;
+  if (R < 0) return fail(ctx, NACS_EINVAL, "requests.n_requests < 0");
+  if (R == 0) return finish_stats(ctx);
+  nacs::ReqsDev Rd;
+  nacs::OutDev Pd;
+  if (dev) {
+    Rd = device_requests(reqs);
+    Pd.status = pl->status;
+    Pd.server = pl->server_of_container;
+    Pd.cpu_a = pl->cpu_alloc;
+    Pd.ram_a = pl->ram_alloc;
+    Pd.bw_a = pl->bw_alloc;
+    Pd.path = pl->path_of_vlink;
+  } else {
+    int C = 0, V = 0;
+    if ((st = check_offsets_host(ctx, reqs, &C, &V))) return st;
+    if ((st = stage_requests(ctx, reqs, C, V, &Rd))) return st;
+    if ((st = device_outputs(ctx, R, C, V, &Pd))) return st;
+    CK(cudaMemcpyAsync(Pd.status, pl->status, (size_t)R * 4, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(Pd.server, pl->server_of_container, (size_t)C * 4, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(Pd.cpu_a, pl->cpu_alloc, (size_t)C * 4, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(Pd.ram_a, pl->ram_alloc, (size_t)C * 4, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(Pd.bw_a, pl->bw_alloc, (size_t)V * 4, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(Pd.path, pl->path_of_vlink, (size_t)V * 4, cudaMemcpyHostToDevice, ctx->stream));
+  }
+  CK(ctx->rel_delta.reserve((size_t)g.words()));
+  CK(ctx->misc.reserve(8));
+  CK(nacs::launch_release(g, ctx->state.p, Rd, Pd, nullptr, 0, ctx->rel_delta.p, ctx->misc.p, ctx->stream));
+  if (!(flags & NACS_ASYNC)) {
+    int bad = 0;
+    CK(cudaMemcpyAsync(&bad, ctx->misc.p, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if ((st = finish_stats(ctx))) return st;
+    if (bad & 1) return fail(ctx, NACS_EINVAL, "placements: a server, path or allocation does not match the fat-tree");
+    if (bad & 2) return fail(ctx, NACS_EINVAL, "release would raise a residual above its capacity (released twice?)");
+  }
+  return NACS_OK;
+}
+
+nacs_status nacs_simulate(nacs_ctx* ctx, const nacs_options* opt, const nacs_requests* reqs, const int32_t* arrival,
+                          const int32_t* duration, const nacs_sim_config* cfg, nacs_placements* out,
+                          nacs_sim_report* rep) {
+  nacs_status st = begin_call(ctx);
+  if (st) return st;
+  Opt o;
+  if ((st = check_options(ctx, opt, &o))) return st;
+  if (opt->flags & (NACS_DEVICE_PTRS | NACS_ASYNC))
+    return fail(ctx, NACS_EINVAL, "nacs_simulate takes host pointers and is synchronous");
+  if (o.rank_once) return fail(ctx, NACS_EINVAL, "nacs_simulate: rank_mode must be NACS_RANK_PER_POD");
+  if (ctx->world > 1 || ctx->comm) return fail(ctx, NACS_EINVAL, "nacs_simulate is not available on server-sharded contexts");
+  if (!cfg || !rep || !arrival || !duration) return fail(ctx, NACS_EINVAL, "config/report/arrival/duration: NULL");
+  if ((st = check_placements(ctx, out))) return st;
+  if (!rep->start_tick || !rep->attempts || !rep->tick_servers || !rep->tick_links || !rep->tick_queue)
+    return fail(ctx, NACS_EINVAL, "report arrays: NULL");
+  if (cfg->max_ticks < 1) return fail(ctx, NACS_EINVAL, "config.max_ticks < 1");
+  if (cfg->hol_blocking != 0 && cfg->hol_blocking != 1) return fail(ctx, NACS_EINVAL, "config.hol_blocking not 0/1");
+  int C = 0, V = 0;
+  if ((st = check_requests_host(ctx, reqs, &C, &V))) return st;
+  const int R = reqs->n_requests;
+  for (int r = 0; r < R; ++r)
+    if (arrival[r] < 0 || duration[r] < 1)
+      return fail(ctx, NACS_EINVAL, "request " + std::to_string(r) + ": arrival < 0 or duration < 1");
+  const Geo& g = ctx->g;
+  const auto t_start = std::chrono::steady_clock::now();
+  nacs::ReqsDev Rd;
+  nacs::OutDev Od;
+  if ((st = stage_requests(ctx, reqs, C, V, &Rd))) return st;
+  if ((st = device_outputs(ctx, R, C, V, &Od))) return st;
+  // requests never offered keep status 0, mappings -1, allocations 0
+  CK(cudaMemsetAsync(Od.status, 0, sizeof(int) * (size_t)R, ctx->stream));
+  CK(cudaMemsetAsync(Od.server, 0xFF, sizeof(int) * (size_t)C, ctx->stream));
+  CK(cudaMemsetAsync(Od.cpu_a, 0, sizeof(int) * 2 * (size_t)C + sizeof(int) * (size_t)V, ctx->stream));
+  CK(cudaMemsetAsync(Od.path, 0xFF, sizeof(int) * (size_t)V, ctx->stream));
+  CK(ctx->ulog.reserve(nacs::ULOG_CAP));
+  if (o.method == 0) CK(ctx->ahp_ws.reserve(nacs::ahp_workspace_bytes(g.n) / 4 + 4));
+  if (o.method == 0) CK(ctx->w64.reserve(nacs::ahp_workspace_doubles(g.n)));
+  CK(ctx->rel_delta.reserve((size_t)g.words()));
+  // device scratch: tick counters [max_ticks][2] | release flag | departing ids [R]
+  const int T = cfg->max_ticks;
+  CK(ctx->sim_buf.reserve(2 * (size_t)T + 4 + (size_t)R));
+  int* d_ticks = ctx->sim_buf.p;
+  int* d_bad = d_ticks + 2 * (size_t)T;
+  int* d_dep = d_bad + 4;
+  CK(ctx->sim_pin.reserve(4 * ((size_t)R + 16)));
+  int* h_pin = reinterpret_cast<int*>(ctx->sim_pin.p);  // [0] status of the last attempt | departing ids
+  // requests by arrival tick (ascending id within a tick)
+  std::vector<int> order(R);
+  for (int r = 0; r < R; ++r) order[r] = r;
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return arrival[a] < arrival[b]; });
+  std::vector<int> start(R, -1), attempts(R, 0), queue, left;
+  std::vector<std::vector<int>> departs;  // departs[t - t0]: requests ending at tick t
+  std::vector<int> tick_queue(T, 0);
+  size_t next = 0;
+  int64_t n_attempts = 0, accepted = 0;
+  double sched_s = 0;
+  int t = 0;
+  for (; t < T; ++t) {
+    // (1) departures first
+    if ((size_t)t < departs.size() && !departs[t].empty()) {
+      const std::vector<int>& dl = departs[t];
+      std::memcpy(h_pin + 16, dl.data(), dl.size() * 4);
+      CK(cudaMemcpyAsync(d_dep, h_pin + 16, dl.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
+      CK(nacs::launch_release(g, ctx->state.p, Rd, Od, d_dep, (int)dl.size(), ctx->rel_delta.p, d_bad, ctx->stream));
+    }
+    // (2) arrivals
+    while (next < order.size() && arrival[order[next]] == t) queue.push_back(order[next++]);
+    // (3) FIFO scan of the queue against the live state
+    left.clear();
+    bool blocked = false;
+    for (int r : queue) {
+      if (blocked) {
+        left.push_back(r);
+        continue;
+      }
+      nacs::ReqsDev R1 = Rd;
+      R1.n = 1;
+      R1.coff = Rd.coff + r;
+      R1.voff = Rd.voff + r;
+      nacs::OutDev O1 = Od;
+      O1.status = Od.status + r;
+      const auto t0 = std::chrono::steady_clock::now();
+      CK(nacs::launch_sequential(g, o, ctx->state.p, R1, O1, ctx->ulog.p, ctx->ahp_ws.p, ctx->w64.p, ctx->stats.p,
+                                 ctx->stream));
+      CK(cudaMemcpyAsync(h_pin, O1.status, 4, cudaMemcpyDeviceToHost, ctx->stream));
+      CK(cudaStreamSynchronize(ctx->stream));
+      sched_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      ++n_attempts;
+      ++attempts[r];
+      if (h_pin[0] == 1) {
+        start[r] = t;
+        ++accepted;
+        const int end = t + duration[r];
+        if (end < T) {
+          if ((size_t)end >= departs.size()) departs.resize(end + 1);
+          departs[end].push_back(r);
+        }
+      } else {
+        left.push_back(r);
+        if (cfg->hol_blocking) blocked = true;
+      }
+    }
+    queue.swap(left);
+    CK(nacs::launch_tick_counts(g, ctx->state.p, d_ticks + 2 * (size_t)t, ctx->stream));
+    tick_queue[t] = (int)queue.size();
+    if (queue.empty() && next == order.size()) {
+      ++t;
+      break;
+    }
+  }
+  // requests still queued at the end are rejected: their (rejected-attempt) outputs stand
+  if ((st = unstage_outputs(ctx, R, C, V, out))) return st;
+  std::vector<int> ticks(2 * (size_t)t);
+  if (t) CK(cudaMemcpyAsync(ticks.data(), d_ticks, ticks.size() * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  for (int r = 0; r < R; ++r) {
+    rep->start_tick[r] = start[r];
+    rep->attempts[r] = attempts[r];
+    if (start[r] < 0) out->status[r] = 0;
+  }
+  for (int i = 0; i < t; ++i) {
+    rep->tick_servers[i] = ticks[2 * i];
+    rep->tick_links[i] = ticks[2 * i + 1];
+    rep->tick_queue[i] = tick_queue[i];
+  }
+  rep->events = t;
+  rep->attempts_total = n_attempts;
+  rep->accepted = accepted;
+  rep->sched_seconds = sched_s;
+  rep->wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+  return finish_stats(ctx);
 }
 
 // ---------------------------------------------------------------------------------------

@@ -172,6 +172,14 @@ cudaError_t launch_ahp_mid(bool fp64, const Geo& g, const Opt& o, int* state, co
 cudaError_t launch_ahp_decide(bool fp64, const Geo& g, const Opt& o, int* state, const ReqsDev& R, const OutDev& O,
                               int r, const ShardDev& d, cudaStream_t st);
 
+// departures (nacs_release, nacs_simulate): idx = null releases every request of R with
+// status 1, else the requests idx[0 .. n_idx); delta: g.words() int64 scratch; bad: 1 int
+// (1 malformed placement, 2 a residual would exceed its capacity; nothing applied then)
+cudaError_t launch_release(const Geo& g, int* state, const ReqsDev& R, const OutDev& P, const int* idx, int n_idx,
+                           long long* delta, int* bad, cudaStream_t st);
+// active servers and active links of the current state into out[0..1]
+cudaError_t launch_tick_counts(const Geo& g, const int* state, int* out, cudaStream_t st);
+
 // General-topology graph (nacs_load_graph, nacs_paths.cu): CSR adjacency of the undirected
 // links, both directions; adj[j] = (neighbour, residual); adj16[j] = neighbour | residual << 16
 // (only when V <= 65536 and every residual <= 65535, else null).

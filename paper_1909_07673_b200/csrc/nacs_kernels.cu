@@ -596,6 +596,39 @@ __device__ void select_topsis(Ctx& c, float* scores_out) {
   }
 }
 
+// ------------------------------------------------------------ BF / WF -------
+// The orchestrators' native baselines ("BF (binpacking) and WF (spread)", reading
+// R27): the feasible server (CPU/RAM filter: they "natively ignore the network
+// requirements", routing follows at commit) of smallest (BF) or largest (WF) mean residual
+// fraction (cpu/cpu_cap + ram/ram_cap) / 2, compared exactly as the integer
+// cpu*ram_cap + ram*cpu_cap < 2^47; ties to the lowest index.  One packed 64-bit key per
+// server, (key or its complement) << 17 | u, and a block-wide unsigned min.
+template <bool WF>
+__device__ void select_fit(Ctx& c) {
+  Scratch* s = c.s;
+  const int n = c.g.n;
+  const int* st = c.st;
+  constexpr unsigned long long KMAX = (1ull << 47) - 1;
+  if (c.tid == 0) s->key1 = ~0ull;
+  __syncthreads();
+  unsigned long long best = ~0ull;
+  for (int u = c.tid; u < n; u += c.B) {
+    if (!((c.maskw[u >> 5] >> (u & 31)) & 1u)) continue;
+    const unsigned long long key = (unsigned long long)st[u] * (unsigned)c.g.ram_cap +
+                                   (unsigned long long)st[n + u] * (unsigned)c.g.cpu_cap;
+    const unsigned long long k = WF ? KMAX - key : key;
+    best = min(best, (k << 17) | (unsigned long long)u);
+  }
+  for (int o = 16; o; o >>= 1) best = min(best, __shfl_xor_sync(0xFFFFFFFFu, best, o));
+  if (c.lane == 0 && best != ~0ull) atomicMin(&s->key1, best);
+  __syncthreads();
+  if (c.tid == 0) {
+    s->best = s->key1 == ~0ull ? -1 : (int)(s->key1 & 0x1FFFFull);
+    s->amb = 0;
+  }
+  __syncthreads();
+}
+
 // --------------------------------------------------------------- AHP --------
 // a5A + a6A (Eq. 9-10, readings R7-R11).  Per criterion c with lo < hi over F,
 // d_ij = s (x_i - x_j) with s = 9 / (hi - lo), a_ij = cell(d_ij), colsum_j = sum_i a_ij,
@@ -1394,7 +1427,8 @@ __device__ void run_request(Ctx& c, const ReqsDev& R, const OutDev& O, int r, bo
         return;
       }
       if (METHOD == 1) select_topsis<false>(c, nullptr);
-      else select_ahp<false>(c, nullptr);
+      else if (METHOD == 0) select_ahp<false>(c, nullptr);
+      else select_fit<METHOD == 3>(c);
       if (s->best < 0) {  // R25: no server of the request's order is admitted (R20)
         req_reject(c, R, O, r);
         return;
@@ -2112,6 +2146,115 @@ cudaError_t launch_sh_decide64(const Geo& g, const Opt& o, int* state, const Req
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------------ departures ---
+// nacs_release: the accepted requests' allocations return to
+// the state — the exact inverse of commit + top-up.  Phase 1 accumulates per-word deltas
+// (a thread per request, atomics) and checks each placement's structure; phase 2 checks
+// residual <= capacity on every touched word; phase 3 applies the deltas and re-derives f_u
+// of the touched servers (R22).  Nothing is applied when phase 1 or 2 found a violation.
+__global__ void k_release_delta(Geo g, ReqsDev R, OutDev P, const int* idx, int n_idx, long long* delta,
+                                int* bad) {
+  const int n = g.n, h = g.h;
+  const int cnt = idx ? n_idx : R.n;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < cnt; t += gridDim.x * blockDim.x) {
+    const int r = idx ? idx[t] : t;
+    if (P.status[r] != 1) continue;
+    const int c0 = R.coff[r], c1 = R.coff[r + 1], v0 = R.voff[r], v1 = R.voff[r + 1];
+    int b = 0;
+    for (int i = c0; i < c1; ++i) {
+      const int u = P.server[i];
+      if (u < 0 || u >= n || P.cpu_a[i] < 0 || P.ram_a[i] < 0) { b = 1; continue; }
+      atomicAdd(reinterpret_cast<unsigned long long*>(delta + u), (unsigned long long)(long long)P.cpu_a[i]);
+      atomicAdd(reinterpret_cast<unsigned long long*>(delta + n + u), (unsigned long long)(long long)P.ram_a[i]);
+    }
+    for (int e = v0; e < v1; ++e) {
+      const int a = R.src[e], d = R.dst[e], bw = P.bw_a[e], pid = P.path[e];
+      if (a < 0 || a >= c1 - c0 || d < 0 || d >= c1 - c0 || bw < 0) { b = 1; continue; }
+      const int us = P.server[c0 + a], ud = P.server[c0 + d];
+      if (us < 0 || us >= n || ud < 0 || ud >= n) { b = 1; continue; }
+      if (us == ud) {  // host bus: no link carried it
+        if (pid != -1) b = 1;
+        continue;
+      }
+      const int eu = us / h, ev = ud / h;
+      const bool ok = eu == ev ? pid == 0 : (eu / h == ev / h ? (pid >= 1 && pid <= h) : (pid > h && pid <= h + h * h));
+      if (!ok) { b = 1; continue; }
+      int off[4];
+      const int m = path_links(g, us, ud, pid, off);
+      atomicAdd(reinterpret_cast<unsigned long long*>(delta + 3 * n + us), (unsigned long long)(long long)bw);
+      atomicAdd(reinterpret_cast<unsigned long long*>(delta + 3 * n + ud), (unsigned long long)(long long)bw);
+      for (int k = 0; k < m; ++k)
+        atomicAdd(reinterpret_cast<unsigned long long*>(delta + off[k]), (unsigned long long)(long long)bw);
+    }
+    if (b) atomicOr(bad, 1);
+  }
+}
+
+__device__ __forceinline__ long long word_cap(const Geo& g, int w) {
+  return w < g.n ? g.cpu_cap : (w < 2 * g.n ? g.ram_cap : (w < 3 * g.n ? 1 : g.link_cap));
+}
+
+__global__ void k_release_check(Geo g, const int* state, const long long* delta, int* bad) {
+  const int W = g.words();
+  for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < W; w += gridDim.x * blockDim.x)
+    if (delta[w] && (long long)state[w] + delta[w] > word_cap(g, w)) atomicOr(bad, 2);
+}
+
+__global__ void k_release_apply(Geo g, int* state, const long long* delta, const int* bad) {
+  if (*bad) return;
+  const int n = g.n, W = g.words();
+  for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < W; w += gridDim.x * blockDim.x) {
+    if (w < n) {
+      if (delta[w] || delta[n + w]) {
+        const int c = state[w] + (int)delta[w], r = state[n + w] + (int)delta[n + w];
+        state[w] = c;
+        state[n + w] = r;
+        state[2 * n + w] = (c < g.cpu_cap || r < g.ram_cap) ? 1 : 0;
+      }
+    } else if (w >= 3 * n && delta[w]) {
+      state[w] += (int)delta[w];
+    }
+  }
+}
+
+cudaError_t launch_release(const Geo& g, int* state, const ReqsDev& R, const OutDev& P, const int* idx, int n_idx,
+                           long long* delta, int* bad, cudaStream_t st) {
+  const int W = g.words();
+  cudaError_t e = cudaMemsetAsync(delta, 0, sizeof(long long) * (size_t)W, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(bad, 0, sizeof(int), st);
+  if (e != cudaSuccess) return e;
+  const int cnt = idx ? n_idx : R.n;
+  if (cnt > 0) k_release_delta<<<std::min(1184, (cnt + 127) / 128), 128, 0, st>>>(g, R, P, idx, n_idx, delta, bad);
+  const int gw = std::min(1184, (W + 255) / 256);
+  k_release_check<<<gw, 256, 0, st>>>(g, state, delta, bad);
+  k_release_apply<<<gw, 256, 0, st>>>(g, state, delta, bad);
+  return cudaGetLastError();
+}
+
+// Fragmentation counters of one simulator tick: active servers |N^s'| (f_u = 1)
+// and active links |E^s'| (residual below capacity) into out[0], out[1] (zeroed by the caller).
+__global__ void k_tick_counts(Geo g, const int* state, int* out) {
+  int as = 0, al = 0;
+  for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < g.n; u += gridDim.x * blockDim.x) as += state[2 * g.n + u];
+  for (int l = blockIdx.x * blockDim.x + threadIdx.x; l < g.L; l += gridDim.x * blockDim.x)
+    al += state[3 * g.n + l] < g.link_cap ? 1 : 0;
+  for (int o = 16; o; o >>= 1) {
+    as += __shfl_xor_sync(0xFFFFFFFFu, as, o);
+    al += __shfl_xor_sync(0xFFFFFFFFu, al, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (as) atomicAdd(out, as);
+    if (al) atomicAdd(out + 1, al);
+  }
+}
+
+cudaError_t launch_tick_counts(const Geo& g, const int* state, int* out, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(out, 0, 2 * sizeof(int), st);
+  if (e != cudaSuccess) return e;
+  k_tick_counts<<<std::min(148, (g.L + 255) / 256), 256, 0, st>>>(g, state, out);
+  return cudaGetLastError();
+}
+
 // --------------------------------------------------------------- host -------
 int batch_block_size(const Geo& g, int method) {
   if (method == 0) {  // AHP: a warp per level pair in the passes
@@ -2142,32 +2285,41 @@ size_t batch_smem_bytes(const Geo& g, int method) {
   return b;
 }
 
-cudaError_t batch_occupancy(const Geo& g, int method, int* blocks_per_sm) {
-  size_t smem = batch_smem_bytes(g, method);
+template <int M>
+static cudaError_t batch_occupancy_t(const Geo& g, int* blocks_per_sm) {
+  size_t smem = batch_smem_bytes(g, M);
   if (!smem) { *blocks_per_sm = 0; return cudaSuccess; }
-  int B = batch_block_size(g, method);
-  cudaError_t e;
-  if (method == 1) {
-    e = cudaFuncSetAttribute(k_batch<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_batch<1>, B, smem);
-  }
-  e = cudaFuncSetAttribute(k_batch<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = cudaFuncSetAttribute(k_batch<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_batch<0>, B, smem);
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_batch<M>, batch_block_size(g, M), smem);
+}
+
+cudaError_t batch_occupancy(const Geo& g, int method, int* blocks_per_sm) {
+  switch (method) {
+    case 0: return batch_occupancy_t<0>(g, blocks_per_sm);
+    case 1: return batch_occupancy_t<1>(g, blocks_per_sm);
+    case 2: return batch_occupancy_t<2>(g, blocks_per_sm);
+    default: return batch_occupancy_t<3>(g, blocks_per_sm);
+  }
+}
+
+template <int M>
+static void launch_batch_t(const Geo& g, const Opt& o, const int* d_state, const ReqsDev& R, const OutDev& O,
+                           int2* ulog, double* w64, int* next, unsigned long long* stats, int grid, cudaStream_t st,
+                           const int* idx, const int* n_idx) {
+  size_t smem = batch_smem_bytes(g, M);
+  cudaFuncSetAttribute(k_batch<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_batch<M><<<grid, batch_block_size(g, M), smem, st>>>(g, o, d_state, R, O, ulog, w64, next, stats, idx, n_idx);
 }
 
 cudaError_t launch_batch(const Geo& g, const Opt& o, const int* d_state, const ReqsDev& R, const OutDev& O,
                          int2* ulog, double* w64, int* next, unsigned long long* stats, int grid,
                          cudaStream_t st, const int* idx, const int* n_idx) {
-  size_t smem = batch_smem_bytes(g, o.method);
-  int B = batch_block_size(g, o.method);
-  if (o.method == 1) {
-    cudaFuncSetAttribute(k_batch<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_batch<1><<<grid, B, smem, st>>>(g, o, d_state, R, O, ulog, w64, next, stats, idx, n_idx);
-  } else {
-    cudaFuncSetAttribute(k_batch<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_batch<0><<<grid, B, smem, st>>>(g, o, d_state, R, O, ulog, w64, next, stats, idx, n_idx);
+  switch (o.method) {
+    case 0: launch_batch_t<0>(g, o, d_state, R, O, ulog, w64, next, stats, grid, st, idx, n_idx); break;
+    case 1: launch_batch_t<1>(g, o, d_state, R, O, ulog, w64, next, stats, grid, st, idx, n_idx); break;
+    case 2: launch_batch_t<2>(g, o, d_state, R, O, ulog, w64, next, stats, grid, st, idx, n_idx); break;
+    default: launch_batch_t<3>(g, o, d_state, R, O, ulog, w64, next, stats, grid, st, idx, n_idx); break;
   }
   return cudaGetLastError();
 }
@@ -2184,8 +2336,12 @@ cudaError_t launch_sequential(const Geo& g, const Opt& o, int* d_state, const Re
                               cudaStream_t st) {
   size_t smem = bitmap_bytes(g);
   int B = single_block_size(g);
-  if (o.method == 1) k_sequential<1><<<1, B, smem, st>>>(g, o, d_state, R, O, ulog, ahp_ws, w64, stats);
-  else k_sequential<0><<<1, B, smem, st>>>(g, o, d_state, R, O, ulog, ahp_ws, w64, stats);
+  switch (o.method) {
+    case 0: k_sequential<0><<<1, B, smem, st>>>(g, o, d_state, R, O, ulog, ahp_ws, w64, stats); break;
+    case 1: k_sequential<1><<<1, B, smem, st>>>(g, o, d_state, R, O, ulog, ahp_ws, w64, stats); break;
+    case 2: k_sequential<2><<<1, B, smem, st>>>(g, o, d_state, R, O, ulog, ahp_ws, w64, stats); break;
+    default: k_sequential<3><<<1, B, smem, st>>>(g, o, d_state, R, O, ulog, ahp_ws, w64, stats); break;
+  }
   return cudaGetLastError();
 }
 

@@ -16,7 +16,7 @@ LIB_PATH = os.environ.get("NACS_LIB", os.path.join(HERE, "libnacs.so"))  # NACS_
 
 NACS_OK, NACS_EINVAL, NACS_ENOMEM, NACS_ECUDA, NACS_ENCCL, NACS_ENOTOPO, NACS_ETOOBIG = range(7)
 STATUS_NAMES = ["OK", "EINVAL", "ENOMEM", "ECUDA", "ENCCL", "ENOTOPO", "ETOOBIG"]
-NACS_AHP, NACS_TOPSIS = 0, 1
+NACS_AHP, NACS_TOPSIS, NACS_BF, NACS_WF = 0, 1, 2, 3
 NACS_DEVICE_PTRS, NACS_ASYNC, NACS_EXACT_FP64 = 1, 2, 4
 NACS_RANK_PER_POD, NACS_RANK_ONCE = 0, 1
 MAX_CONTAINERS, MAX_VLINKS, MAX_K = 128, 512, 64
@@ -25,7 +25,7 @@ MAX_CONTAINERS, MAX_VLINKS, MAX_K = 128, 512, 64
 SCHEMAS = {"flat": (0.25, 0.25, 0.25, 0.25),
            "clustering": (0.17, 0.17, 0.5, 0.16),
            "network": (0.17, 0.17, 0.16, 0.5)}
-METHODS = {"ahp": NACS_AHP, "topsis": NACS_TOPSIS}
+METHODS = {"ahp": NACS_AHP, "topsis": NACS_TOPSIS, "bf": NACS_BF, "wf": NACS_WF}
 
 P32 = C.POINTER(C.c_int32)
 PU8 = C.POINTER(C.c_uint8)
@@ -69,6 +69,17 @@ class Stats(C.Structure):
                 ("edges_scanned", C.c_int64), ("bfs_runs", C.c_int64)]
 
 
+class SimConfig(C.Structure):
+    _fields_ = [("max_ticks", C.c_int32), ("hol_blocking", C.c_int32)]
+
+
+class SimReport(C.Structure):
+    _fields_ = [("start_tick", C.c_void_p), ("attempts", C.c_void_p), ("tick_servers", C.c_void_p),
+                ("tick_links", C.c_void_p), ("tick_queue", C.c_void_p), ("events", C.c_int64),
+                ("attempts_total", C.c_int64), ("accepted", C.c_int64), ("sched_seconds", C.c_double),
+                ("wall_seconds", C.c_double)]
+
+
 class Graph(C.Structure):
     _fields_ = [("n_vertices", C.c_int32), ("n_servers", C.c_int32), ("n_links", C.c_int32),
                 ("link_u", C.c_void_p), ("link_v", C.c_void_p), ("link_res", C.c_void_p)]
@@ -81,7 +92,7 @@ class PathQuery(C.Structure):
 EXPORTS = ["nacs_create", "nacs_create_sharded", "nacs_nccl_unique_id", "nacs_destroy", "nacs_load_topology",
            "nacs_read_topology", "nacs_rank_ahp", "nacs_rank_topsis", "nacs_schedule_request",
            "nacs_schedule_batch", "nacs_last_stats", "nacs_last_error", "nacs_load_graph", "nacs_widest_paths",
-           "nacs_logical_bandwidth"]
+           "nacs_logical_bandwidth", "nacs_release", "nacs_simulate"]
 
 _lib = None
 
@@ -107,6 +118,9 @@ def lib():
         for f in (L.nacs_schedule_request, L.nacs_schedule_batch):
             f.argtypes = [vp, C.POINTER(Options), C.POINTER(Requests), C.POINTER(Placements)]
         L.nacs_last_stats.argtypes = [vp, C.POINTER(Stats)]
+        L.nacs_release.argtypes = [vp, C.c_uint32, C.POINTER(Requests), C.POINTER(Placements)]
+        L.nacs_simulate.argtypes = [vp, C.POINTER(Options), C.POINTER(Requests), vp, vp, C.POINTER(SimConfig),
+                                    C.POINTER(Placements), C.POINTER(SimReport)]
         L.nacs_load_graph.argtypes = [vp, C.POINTER(Graph)]
         L.nacs_widest_paths.argtypes = [vp, C.POINTER(PathQuery), C.c_uint32, vp, vp, vp, C.c_int32]
         L.nacs_logical_bandwidth.argtypes = [vp, C.c_uint32, vp]
@@ -294,6 +308,44 @@ class Context:
     def schedule_batch(self, reqs: dict, method, weights, out=None, flags=0, **kw) -> dict:
         """Every request against the same snapshot (snapshot isolation); the state is unchanged."""
         return self._schedule(self._lib.nacs_schedule_batch, reqs, method, weights, out, flags, **kw)
+
+    # ------------------------------------------------- departures, simulator ---
+    def release(self, reqs: dict, placements: dict, flags=0):
+        """Departure of every accepted request (status 1) of `reqs` (placements as returned)."""
+        r, keep, dev = self._requests(reqs)
+        if dev:
+            flags |= NACS_DEVICE_PTRS
+            outs = [placements[k] for k in OUT_KEYS]
+        else:
+            outs = [_i32(placements[k]) for k in OUT_KEYS]
+        p = Placements(*[_ptr(a) for a in outs])
+        self._check(self._lib.nacs_release(self._h, flags, C.byref(r), C.byref(p)))
+        del keep
+
+    def simulate(self, reqs: dict, arrival, duration, method, weights, max_ticks: int, hol: int = 1, **kw) -> dict:
+        """Discrete-event simulation on the live state (reading R28): per-request start / attempts,
+        final placements, per-tick |N^s'|, |E^s'|, queue length, and totals."""
+        r, keep, dev = self._requests(reqs)
+        if dev:
+            raise ValueError("simulate takes host arrays")
+        o = self.options(method, weights, **kw)
+        R = int(reqs["n_requests"])
+        out, sizes = self._alloc_out(reqs, False)
+        p = Placements(*[_ptr(out[k]) for k in OUT_KEYS])
+        arr, dur = _i32(arrival), _i32(duration)
+        start, att = np.zeros(max(R, 1), np.int32), np.zeros(max(R, 1), np.int32)
+        ts, tl, tq = (np.zeros(max_ticks, np.int32) for _ in range(3))
+        rep = SimReport(_np_ptr(start), _np_ptr(att), _np_ptr(ts), _np_ptr(tl), _np_ptr(tq), 0, 0, 0, 0.0, 0.0)
+        cfg = SimConfig(int(max_ticks), int(hol))
+        self._check(self._lib.nacs_simulate(self._h, C.byref(o), C.byref(r), _np_ptr(arr), _np_ptr(dur),
+                                            C.byref(cfg), C.byref(p), C.byref(rep)))
+        del keep
+        T = int(rep.events)
+        return dict(start=start[:R], attempts=att[:R], status=out["status"][:R],
+                    placements={k: out[k][: sizes[k]] for k in OUT_KEYS},
+                    tick_servers=ts[:T], tick_links=tl[:T], tick_queue=tq[:T],
+                    totals=dict(events=T, attempts=int(rep.attempts_total), accepted=int(rep.accepted)),
+                    sched_seconds=rep.sched_seconds, wall_seconds=rep.wall_seconds)
 
     # ----------------------------------------------------- general topology ---
     def load_graph(self, graph: dict):

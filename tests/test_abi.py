@@ -22,7 +22,7 @@ def test_library_builds_and_exports_header_symbols():
     path = nbuild.build()
     assert os.path.exists(path)
     declared = header_functions()
-    assert len(declared) == 15, declared
+    assert len(declared) == 17, declared
     out = subprocess.run(["nm", "-D", "--defined-only", path], capture_output=True, text=True).stdout
     exported = set(re.findall(r"\bT (nacs_[a-z_]+)\b", out))
     assert set(declared) <= exported, set(declared) - exported
@@ -44,7 +44,8 @@ def test_struct_layouts_match_header(tmp_path):
     structs = {"nacs_topology": nacs.Topology, "nacs_pod_query": nacs.PodQuery,
                "nacs_requests": nacs.Requests, "nacs_placements": nacs.Placements,
                "nacs_options": nacs.Options, "nacs_stats": nacs.Stats, "nacs_graph": nacs.Graph,
-               "nacs_path_query": nacs.PathQuery}
+               "nacs_path_query": nacs.PathQuery, "nacs_sim_config": nacs.SimConfig,
+               "nacs_sim_report": nacs.SimReport}
     lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "nacs.h"', "int main(void) {"]
     for cname, py in structs.items():
         lines.append(f'printf("{cname} size %zu\\n", sizeof({cname}));')
