@@ -56,6 +56,7 @@ def parse():
     ap.add_argument("--no-once", action="store_true")
     ap.add_argument("--no-variants", action="store_true")
     ap.add_argument("--no-paths", action="store_true")
+    ap.add_argument("--no-sim", action="store_true")
     return ap.parse_args()
 
 
@@ -253,6 +254,9 @@ def run_ours(args, rank, world, local):
     paths = None if args.no_paths else measure_paths(args, ctx, dev, stream, flush, barrier, max_over_ranks,
                                                      sum_over_ranks, rank, local)
 
+    # the E2 campaign through the discrete-event simulator (T5-shaped rows)
+    sim = None if (args.no_sim or rank != 0) else measure_sim(ctx)
+
     # roofline of the dominant kernel (k_batch<TOPSIS>): issue-bound ALU
     clocks = topsis["clocks"]
     mhz = float(pk.get("sm_max_mhz", 1965.0))
@@ -326,7 +330,7 @@ def run_ours(args, rank, world, local):
                 "kernel_ms": topsis["kernel_ms"], "fp64_decisions": topsis["stats"]["fp64_decisions"],
                 "retries": topsis["stats"]["retries"],
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": args.steps * LAUNCHES["topsis"],
-                "clocks": clocks, "ahp": ahp_obj, "variants": variants, "paths": paths,
+                "clocks": clocks, "ahp": ahp_obj, "variants": variants, "paths": paths, "simulator": sim,
                 "rank_once": None if once is None else {
                     "workload": once["name"].replace("batch", "batch, rank once per request (R25)"),
                     "value": once["value"], "unit": "pods/s", "ms_per_step": once["ms_per_step"],
@@ -400,6 +404,53 @@ def measure_paths(args, ctx, dev, stream, flush, barrier, max_over_ranks, sum_ov
             "logical_bandwidth": {"value": sum_over_ranks(ns * (ns - 1)) / (ms_lb / 1e3), "unit": "server pairs/s",
                                   "ms_per_step": ms_lb, "edges_scanned_per_source": edges_lb / ns},
             "kernel": "k_paths (warp per query, level-synchronous BFS, smem atomicMin labels)"}
+
+
+# T5: events, average runtime (s), U(ij), U(i) per algorithm on the paper's GPU
+T5 = {"bf": (2462, 79.38, 1.0, 0.9689), "wf": (1007, 47.80, 1.0, 0.9941),
+      "ahp flat": (949, 9.45, 1.0, 0.9822), "ahp clustering": (936, 7.51, 1.0, 0.9910),
+      "ahp network": (928, 6.90, 1.0, 0.9841), "topsis flat": (894, 3.67, 1.0, 0.9885),
+      "topsis clustering": (916, 3.84, 1.0, 0.9901), "topsis network": (892, 3.48, 1.0, 0.9894)}
+
+
+def measure_sim(ctx):
+    """The E2 campaign: fresh k=20 fat-tree, 6000 requests of 4 containers arriving
+    over 500 ticks, durations up to 250 ticks, through nacs_simulate for the 8 rows of T5.
+    Runtime = wall time inside the scheduling attempts (T5 "Average Runtime"), U(i) = mean over
+    accepted containers of Eq. 1, U(ij) = mean over accepted inter-container vlinks of Eq. 2."""
+    snap = gen.snapshot(20, warm=False)
+    reqs, arrival, duration = gen.sim_workload()
+    rows = {}
+    for name in ("bf", "wf", "ahp flat", "ahp clustering", "ahp network", "topsis flat", "topsis clustering",
+                 "topsis network"):
+        method, schema = (name.split() + ["flat"])[:2]
+        ctx.load_topology(snap)
+        r = ctx.simulate(reqs, arrival, duration, method, schema, max_ticks=5000)
+        pl = r["placements"]
+        acc_c = pl["server_of_container"] >= 0
+        ui = 0.5 * (pl["cpu_alloc"][acc_c] / reqs["cpu_max"][acc_c] + pl["ram_alloc"][acc_c] / reqs["ram_max"][acc_c])
+        vsrv = pl["server_of_container"][reqs["container_off"][:-1].repeat(np.diff(reqs["vlink_off"]))
+                                         + reqs["vl_src"]]
+        acc_v = vsrv >= 0
+        uij = pl["bw_alloc"][acc_v] / reqs["bw_max"][acc_v]
+        st = r["start"]
+        ok = st >= 0
+        t5 = T5[name]
+        rows[name] = {"events": r["totals"]["events"], "attempts": r["totals"]["attempts"],
+                      "accepted": r["totals"]["accepted"], "runtime_s": r["sched_seconds"],
+                      "wall_s": r["wall_seconds"], "U_ij": float(uij.mean()) if uij.size else None,
+                      "U_i": float(ui.mean()) if ui.size else None,
+                      "mean_delay": float((st[ok] - arrival[ok]).mean()) if ok.any() else None,
+                      "max_F_servers": float(r["tick_servers"].max() / 2000),
+                      "max_F_links": float(r["tick_links"].max() / 6000),
+                      "pod_steps": ctx.last_stats()["pod_steps"], "retries": ctx.last_stats()["retries"],
+                      "paper_T5": {"events": t5[0], "runtime_s": t5[1], "U_ij": t5[2], "U_i": t5[3]}}
+    return {"workload": "E2 (P:396-398): fresh fat-tree k=20 (2000 servers), 6000 requests x 4 containers, "
+                        "arrivals U{0..499}, durations U{1..250} ticks, pairs <= 50 Mbps; nacs_simulate, "
+                        "FIFO with head-of-line blocking (R28)",
+            "rows": rows,
+            "note": "paper_T5 = the paper's numbers on its unnamed CUDA 10.1 GPU with its own unpublished "
+                    "workload draw: context, not a like-for-like target"}
 
 
 def cpu_baseline(snap, reqs, budget_s=15.0, method="topsis"):
