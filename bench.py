@@ -159,6 +159,27 @@ def workload(rank: int, method: str):
     return snap, reqs, name
 
 
+def quality(reqs: dict, out: dict) -> dict:
+    """SURVEY 8(d) reporting: acceptance rate, accepted pods, mean U(i) (Eq. 1) over the
+    accepted containers and mean U(ij) (Eq. 2, R23: bw^a / bw^max) over their vlinks."""
+    o = {k: (v.cpu().numpy() if hasattr(v, "cpu") else np.asarray(v)) for k, v in out.items()}
+    R = int(reqs["n_requests"])
+    co, vo = reqs["container_off"].astype(np.int64), reqs["vlink_off"].astype(np.int64)
+    st = o["status"][:R]
+    acc_r = st == 1
+    req_of_c = np.repeat(np.arange(R), np.diff(co))
+    req_of_v = np.repeat(np.arange(R), np.diff(vo))
+    acc_c = acc_r[req_of_c]
+    acc_v = acc_r[req_of_v]
+    Cn, Vn = int(co[-1]), int(vo[-1])
+    ui = 0.5 * (o["cpu_alloc"][:Cn][acc_c] / reqs["cpu_max"][acc_c] + o["ram_alloc"][:Cn][acc_c] / reqs["ram_max"][acc_c])
+    uij = o["bw_alloc"][:Vn][acc_v] / reqs["bw_max"][acc_v]
+    pods = np.zeros(R, np.int64)
+    np.maximum.at(pods, req_of_c, reqs["pod_of"].astype(np.int64) + 1)
+    return {"acceptance": float(acc_r.mean()) if R else None, "accepted_pods": int(pods[acc_r].sum()),
+            "U_i": float(ui.mean()) if ui.size else None, "U_ij": float(uij.mean()) if uij.size else None}
+
+
 def run_ours(args, rank, world, local):
     import torch
     from paper_1909_07673_b200 import nacs
@@ -228,7 +249,9 @@ def run_ours(args, rank, world, local):
         pod_steps = sum_over_ranks(st["pod_steps"])
         value = pod_steps * args.steps / (total_ms / 1e3)
         n = snap["k"] ** 3 // 4
-        res = dict(name=name, value=value, ms_per_step=total_ms / args.steps, kernel_ms=kern_avg,
+        q = quality(reqs, out)
+        q["accepted_pods_per_s"] = sum_over_ranks(q["accepted_pods"]) * args.steps / (total_ms / 1e3)
+        res = dict(name=name, value=value, ms_per_step=total_ms / args.steps, kernel_ms=kern_avg, quality=q,
                    pod_steps_per_step=pod_steps, servers_ranked_per_s=value * n, n=n, stats=st,
                    clocks=sampler.summary(), snap=snap, reqs=reqs, out=out, d=d)
         return res
@@ -285,6 +308,7 @@ def run_ours(args, rank, world, local):
         ahp_obj = {"workload": ahp["name"], "value": ahp["value"], "unit": "pods/s",
                    "servers_ranked_per_s": ahp["servers_ranked_per_s"], "ms_per_step": ahp["ms_per_step"],
                    "pod_steps_per_step": ahp["pod_steps_per_step"], "fp64_decisions": sa["fp64_decisions"],
+                   "quality": ahp["quality"],
                    "roofline": {"bound": "mufu", "achieved": ach, "peak": mufu_peak, "unit": "T rcp/s",
                                 "frac": ach / mufu_peak, "kernel": "k_batch<AHP>",
                                 "peak_source": f"16 MUFU.RCP/clk/SM (measured 15.9: scripts/micro/mufu_rcp.cu, "
@@ -328,13 +352,14 @@ def run_ours(args, rank, world, local):
                 "servers_ranked_per_s": topsis["servers_ranked_per_s"],
                 "pod_steps_per_step": topsis["pod_steps_per_step"],
                 "kernel_ms": topsis["kernel_ms"], "fp64_decisions": topsis["stats"]["fp64_decisions"],
-                "retries": topsis["stats"]["retries"],
+                "retries": topsis["stats"]["retries"], "quality": topsis["quality"],
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": args.steps * LAUNCHES["topsis"],
                 "clocks": clocks, "ahp": ahp_obj, "variants": variants, "paths": paths, "simulator": sim,
                 "rank_once": None if once is None else {
                     "workload": once["name"].replace("batch", "batch, rank once per request (R25)"),
                     "value": once["value"], "unit": "pods/s", "ms_per_step": once["ms_per_step"],
                     "kernel_ms": once["kernel_ms"], "pod_steps_per_step": once["pod_steps_per_step"],
+                    "quality": once["quality"],
                     "slots_read_frac": (once["stats"]["scanned_a"] + once["stats"]["scanned_b"])
                     / max(1, 2 * once["stats"]["servers_ranked"])},
                 "paper_context": "T5 (P:416-426): TOPSIS 3.48-3.84 s, AHP 6.90-9.45 s per 6000-request k=20 campaign "

@@ -64,3 +64,51 @@ def schedule_batch_sharded(reqs: dict, schedule, rank: int, world: int, group=No
     out = {k: np.concatenate([p[k] for p in parts]).astype(np.int32)
            for k in OUT_R + OUT_C + OUT_V}
     return out
+
+
+# ---------------------------------------------------------------------------------------
+# Path queries (general topology): queries are independent, and the GPU
+# answers all queries to one destination from one BFS, so they shard by
+# DESTINATION: each rank owns whole destination groups and no BFS is repeated across ranks.
+# ---------------------------------------------------------------------------------------
+
+def shard_queries_by_destination(dst: np.ndarray, world: int) -> list[np.ndarray]:
+    """Per-rank query index arrays (ascending): destination groups assigned largest-first to
+    the least-loaded rank (deterministic: ties by destination id, then rank id)."""
+    dst = np.asarray(dst, dtype=np.int64)
+    if world == 1:
+        return [np.arange(dst.size)]
+    ids, counts = np.unique(dst, return_counts=True)
+    order = np.lexsort((ids, -counts))
+    load = np.zeros(world, np.int64)
+    owner = np.empty(ids.size, np.int64)
+    for g in order:
+        r = int(np.argmin(load))
+        owner[g] = r
+        load[r] += counts[g]
+    rank_of_query = owner[np.searchsorted(ids, dst)]
+    return [np.nonzero(rank_of_query == r)[0] for r in range(world)]
+
+
+def widest_paths_sharded(q: dict, solve, rank: int, world: int, group=None):
+    """Answer the queries q = dict(src, dst, demand) across `world` ranks; every rank returns
+    the full (bottleneck, hops, path).  solve(src, dst, demand) -> (bn, hops, path) for this
+    rank's queries (e.g. a bound Context.widest_paths)."""
+    parts_idx = shard_queries_by_destination(q["dst"], world)
+    idx = parts_idx[rank]
+    mine = solve(*(np.ascontiguousarray(np.asarray(q[k])[idx], dtype=np.int32) for k in ("src", "dst", "demand")))
+    mine = tuple(_np(x) for x in mine)
+    if world == 1:
+        parts = [mine]
+    else:
+        import torch.distributed as dist
+        parts = [None] * world
+        dist.all_gather_object(parts, mine, group=group)
+    n = np.asarray(q["src"]).size
+    bn = np.empty(n, np.int32)
+    hops = np.empty(n, np.int32)
+    path = np.empty((n, parts[0][2].shape[1]), np.int32)
+    for r in range(world):
+        ir = parts_idx[r]
+        bn[ir], hops[ir], path[ir] = parts[r][0], parts[r][1], parts[r][2]
+    return bn, hops, path

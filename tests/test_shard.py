@@ -72,3 +72,53 @@ def test_sharded_batch_equals_single_process():
     for rank in range(world):
         for key, val in ref.items():
             assert np.array_equal(np.asarray(results[rank][key]), val), (rank, key)
+
+
+def test_query_shards_cover_and_keep_destinations_whole():
+    g = gen.fat_tree_graph(gen.snapshot(8, 3))
+    q = gen.path_queries(g, 5000, 9)
+    for world in (1, 2, 3, 8):
+        parts = shard.shard_queries_by_destination(q["dst"], world)
+        allq = np.sort(np.concatenate(parts))
+        assert np.array_equal(allq, np.arange(5000))
+        owners = [set(q["dst"][p].tolist()) for p in parts]
+        for a in range(world):
+            for b in range(a + 1, world):
+                assert not owners[a] & owners[b]  # a destination lives on one rank
+        loads = [p.size for p in parts]
+        assert max(loads) - min(loads) <= np.bincount(q["dst"]).max()
+
+
+def _paths_worker(rank, world, port, g, q, out):
+    import torch.distributed as dist
+    from oracle import oracle as O
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        res = shard.widest_paths_sharded(
+            q, lambda s, d, dm: O.graph_paths(g, s, d, dm, max_hops=8, nthreads=1), rank, world)
+        out.put((rank, [x.tolist() for x in res]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_paths_equal_single_process():
+    from oracle import oracle as O
+    g = gen.fat_tree_graph(gen.snapshot(4, 5))
+    q = gen.path_queries(g, 400, 6, bw_hi=600)
+    world = 2
+    ctx = mp.get_context("spawn")
+    out = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_paths_worker, args=(r, world, port, g, q, out)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = dict(out.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    ref = O.graph_paths(g, q["src"], q["dst"], q["demand"], max_hops=8, nthreads=1)
+    for rank in range(world):
+        for a, b in zip(results[rank], ref):
+            assert np.array_equal(np.asarray(a), b)
