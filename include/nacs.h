@@ -235,7 +235,7 @@ typedef struct {  /* caller-allocated arrays; scalars written by the call */
   int64_t events;         /* ticks simulated (T5 "# Events"; entries >= events untouched) */
   int64_t attempts_total; /* scheduler invocations */
   int64_t accepted;
-  double sched_seconds;   /* wall time inside the scheduling attempts (T5 "runtime") */
+  double sched_seconds;   /* device time of the event loop (one kernel: every attempt and departure; T5 "runtime") */
   double wall_seconds;    /* wall time of the whole call */
 } nacs_sim_report;
 
@@ -247,8 +247,10 @@ typedef struct {  /* caller-allocated arrays; scalars written by the call */
  * hol_blocking the scan of the tick stops there).  The run ends after the first tick with
  * an empty queue and no arrival left, or after max_ticks (still-queued requests are then
  * rejected).  out: the final placements (status 1 accepted, 0 never accepted, -1 invalid).
- * Afterwards the state holds the requests that have not departed.  Host pointers only;
- * synchronous; arrival >= 0, duration >= 1; AHP/TOPSIS/BF/WF with rank_mode per pod. */
+ * Afterwards the state holds the requests that have not departed.  The whole event loop
+ * runs on the device in one launch (one CTA: queue, running set and every attempt on-chip).
+ * Host pointers only; synchronous; arrival >= 0, duration >= 1; AHP/TOPSIS/BF/WF with
+ * rank_mode per pod. */
 nacs_status nacs_simulate(nacs_ctx *ctx, const nacs_options *opt, const nacs_requests *reqs, const int32_t *arrival,
                           const int32_t *duration, const nacs_sim_config *cfg, nacs_placements *out,
                           nacs_sim_report *rep);

@@ -1119,98 +1119,63 @@ nacs_status nacs_simulate(nacs_ctx* ctx, const nacs_options* opt, const nacs_req
   CK(ctx->ulog.reserve(nacs::ULOG_CAP));
   if (o.method == 0) CK(ctx->ahp_ws.reserve(nacs::ahp_workspace_bytes(g.n) / 4 + 4));
   if (o.method == 0) CK(ctx->w64.reserve(nacs::ahp_workspace_doubles(g.n)));
-  CK(ctx->rel_delta.reserve((size_t)g.words()));
-  // device scratch: tick counters [max_ticks][2] | release flag | departing ids [R]
+  // the whole event loop runs on the device in one launch (k_simulate)
   const int T = cfg->max_ticks;
-  CK(ctx->sim_buf.reserve(2 * (size_t)T + 4 + (size_t)R));
-  int* d_ticks = ctx->sim_buf.p;
-  int* d_bad = d_ticks + 2 * (size_t)T;
-  int* d_dep = d_bad + 4;
-  CK(ctx->sim_pin.reserve(4 * ((size_t)R + 16)));
-  int* h_pin = reinterpret_cast<int*>(ctx->sim_pin.p);  // [0] status of the last attempt | departing ids
-  // requests by arrival tick (ascending id within a tick)
   std::vector<int> order(R);
   for (int r = 0; r < R; ++r) order[r] = r;
   std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return arrival[a] < arrival[b]; });
-  std::vector<int> start(R, -1), attempts(R, 0), queue, left;
-  std::vector<std::vector<int>> departs;  // departs[t - t0]: requests ending at tick t
-  std::vector<int> tick_queue(T, 0);
-  size_t next = 0;
-  int64_t n_attempts = 0, accepted = 0;
-  double sched_s = 0;
-  int t = 0;
-  for (; t < T; ++t) {
-    // (1) departures first
-    if ((size_t)t < departs.size() && !departs[t].empty()) {
-      const std::vector<int>& dl = departs[t];
-      std::memcpy(h_pin + 16, dl.data(), dl.size() * 4);
-      CK(cudaMemcpyAsync(d_dep, h_pin + 16, dl.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
-      CK(nacs::launch_release(g, ctx->state.p, Rd, Od, d_dep, (int)dl.size(), ctx->rel_delta.p, d_bad, ctx->stream));
-    }
-    // (2) arrivals
-    while (next < order.size() && arrival[order[next]] == t) queue.push_back(order[next++]);
-    // (3) FIFO scan of the queue against the live state
-    left.clear();
-    bool blocked = false;
-    for (int r : queue) {
-      if (blocked) {
-        left.push_back(r);
-        continue;
-      }
-      nacs::ReqsDev R1 = Rd;
-      R1.n = 1;
-      R1.coff = Rd.coff + r;
-      R1.voff = Rd.voff + r;
-      nacs::OutDev O1 = Od;
-      O1.status = Od.status + r;
-      const auto t0 = std::chrono::steady_clock::now();
-      CK(nacs::launch_sequential(g, o, ctx->state.p, R1, O1, ctx->ulog.p, ctx->ahp_ws.p, ctx->w64.p, ctx->stats.p,
-                                 ctx->stream));
-      CK(cudaMemcpyAsync(h_pin, O1.status, 4, cudaMemcpyDeviceToHost, ctx->stream));
-      CK(cudaStreamSynchronize(ctx->stream));
-      sched_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-      ++n_attempts;
-      ++attempts[r];
-      if (h_pin[0] == 1) {
-        start[r] = t;
-        ++accepted;
-        const int end = t + duration[r];
-        if (end < T) {
-          if ((size_t)end >= departs.size()) departs.resize(end + 1);
-          departs[end].push_back(r);
-        }
-      } else {
-        left.push_back(r);
-        if (cfg->hol_blocking) blocked = true;
-      }
-    }
-    queue.swap(left);
-    CK(nacs::launch_tick_counts(g, ctx->state.p, d_ticks + 2 * (size_t)t, ctx->stream));
-    tick_queue[t] = (int)queue.size();
-    if (queue.empty() && next == order.size()) {
-      ++t;
-      break;
-    }
-  }
-  // requests still queued at the end are rejected: their (rejected-attempt) outputs stand
+  // device: order | arrival | duration | start | attempts | qbuf | qtmp | run [R each] | ticks [3T] |
+  // head [T] | totals
+  CK(ctx->sim_buf.reserve(8 * (size_t)R + 4 * (size_t)T + 8));
+  int* d = ctx->sim_buf.p;
+  nacs::SimDev S;
+  S.order = d;
+  S.arrival = d + R;
+  S.duration = d + 2 * (size_t)R;
+  S.start = d + 3 * (size_t)R;
+  S.attempts = d + 4 * (size_t)R;
+  S.qbuf = d + 5 * (size_t)R;
+  S.qtmp = d + 6 * (size_t)R;
+  S.run = d + 7 * (size_t)R;
+  S.ticks = d + 8 * (size_t)R;
+  S.head = d + 8 * (size_t)R + 3 * (size_t)T;
+  S.totals = reinterpret_cast<long long*>(d + ((8 * (size_t)R + 4 * (size_t)T + 1) & ~(size_t)1));
+  S.max_ticks = T;
+  S.hol = cfg->hol_blocking;
+  CK(cudaMemcpyAsync(d, order.data(), (size_t)R * 4, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(d + R, arrival, (size_t)R * 4, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(d + 2 * (size_t)R, duration, (size_t)R * 4, cudaMemcpyHostToDevice, ctx->stream));
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaEventRecord(e0, ctx->stream));
+  CK(nacs::launch_simulate(g, o, ctx->state.p, Rd, Od, ctx->ulog.p, ctx->ahp_ws.p, ctx->w64.p, ctx->stats.p, S,
+                           ctx->stream));
+  CK(cudaEventRecord(e1, ctx->stream));
   if ((st = unstage_outputs(ctx, R, C, V, out))) return st;
-  std::vector<int> ticks(2 * (size_t)t);
-  if (t) CK(cudaMemcpyAsync(ticks.data(), d_ticks, ticks.size() * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  long long tot[3];
+  CK(cudaMemcpyAsync(tot, S.totals, sizeof(tot), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(rep->start_tick, S.start, (size_t)R * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(rep->attempts, S.attempts, (size_t)R * 4, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
-  for (int r = 0; r < R; ++r) {
-    rep->start_tick[r] = start[r];
-    rep->attempts[r] = attempts[r];
-    if (start[r] < 0) out->status[r] = 0;
-  }
+  const int t = (int)tot[0];
+  std::vector<int> ticks(3 * (size_t)t + 1);
+  if (t) CK(cudaMemcpy(ticks.data(), S.ticks, 3 * (size_t)t * 4, cudaMemcpyDeviceToHost));
+  float ms = 0;
+  CK(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  for (int r = 0; r < R; ++r)
+    if (rep->start_tick[r] < 0) out->status[r] = 0;
   for (int i = 0; i < t; ++i) {
-    rep->tick_servers[i] = ticks[2 * i];
-    rep->tick_links[i] = ticks[2 * i + 1];
-    rep->tick_queue[i] = tick_queue[i];
+    rep->tick_servers[i] = ticks[3 * i];
+    rep->tick_links[i] = ticks[3 * i + 1];
+    rep->tick_queue[i] = ticks[3 * i + 2];
   }
   rep->events = t;
-  rep->attempts_total = n_attempts;
-  rep->accepted = accepted;
-  rep->sched_seconds = sched_s;
+  rep->attempts_total = tot[1];
+  rep->accepted = tot[2];
+  rep->sched_seconds = ms / 1e3;
   rep->wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
   return finish_stats(ctx);
 }

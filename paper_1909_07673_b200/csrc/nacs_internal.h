@@ -177,6 +177,19 @@ cudaError_t launch_ahp_decide(bool fp64, const Geo& g, const Opt& o, int* state,
 // (1 malformed placement, 2 a residual would exceed its capacity; nothing applied then)
 cudaError_t launch_release(const Geo& g, int* state, const ReqsDev& R, const OutDev& P, const int* idx, int n_idx,
                            long long* delta, int* bad, cudaStream_t st);
+// the discrete-event run on the device (k_simulate, one CTA, one launch)
+struct SimDev {
+  const int *order, *arrival, *duration;  // order: requests by arrival tick, then id
+  int max_ticks, hol;
+  int *start, *attempts;                  // [R]
+  int* ticks;                             // [max_ticks][3]: active servers, active links, queue
+  int *qbuf, *qtmp, *run;                 // [R] each: queue, next queue, departure-bucket links
+  int* head;                              // [max_ticks] first request departing at each tick (-1)
+  long long* totals;                      // [3]: events (ticks), attempts, accepted
+};
+cudaError_t launch_simulate(const Geo& g, const Opt& o, int* d_state, const ReqsDev& R, const OutDev& O,
+                            int2* ulog, float* ahp_ws, double* w64, unsigned long long* stats, const SimDev& S,
+                            cudaStream_t st);
 // active servers and active links of the current state into out[0..1]
 cudaError_t launch_tick_counts(const Geo& g, const int* state, int* out, cudaStream_t st);
 

@@ -1597,9 +1597,26 @@ __global__ void __launch_bounds__(1024) k_batch(Geo g, Opt o, const int* __restr
   flush_stats(c, stats);
 }
 
+// Sequential kernels keep the live state in shared memory when it fits (k <= 32 with the
+// bitmaps: every serial step of a pod step — flows, commit, top-up — then reads on-chip
+// words instead of L2), copied in at the start and back at the end of the launch.
+__device__ int* load_state_smem(Ctx& c, unsigned char* base, const int* state) {
+  int* sst = reinterpret_cast<int*>(base);
+  const int W = c.g.words();
+  for (int i = c.tid; i < W; i += c.B) sst[i] = state[i];
+  __syncthreads();
+  return sst;
+}
+__device__ void store_state_smem(Ctx& c, const int* sst, int* state) {
+  __syncthreads();
+  const int W = c.g.words();
+  for (int i = c.tid; i < W; i += c.B) state[i] = sst[i];
+}
+
 template <int METHOD>
 __global__ void __launch_bounds__(1024) k_sequential(Geo g, Opt o, int* state, ReqsDev R, OutDev O, int2* ulog,
-                                                     float* ahp_ws, double* w64, unsigned long long* stats) {
+                                                     float* ahp_ws, double* w64, unsigned long long* stats,
+                                                     int smem_state) {
   extern __shared__ __align__(16) unsigned char dyn[];
   __shared__ Scratch s;
   Ctx c;
@@ -1612,8 +1629,10 @@ __global__ void __launch_bounds__(1024) k_sequential(Geo g, Opt o, int* state, R
   c.f0w = reinterpret_cast<unsigned*>(dyn + off);
   off = align16(off + sizeof(unsigned) * c.nW);
   c.edgebad = reinterpret_cast<unsigned*>(dyn + off);
-  c.st = state;
-  c.snap = state;
+  off = align16(off + sizeof(unsigned) * c.nEW);
+  int* sst = smem_state ? load_state_smem(c, dyn + off, state) : state;
+  c.st = sst;
+  c.snap = sst;
   c.ulog = ulog;
   c.nfcap = g.n;
   if (METHOD == 0) ahp_carve(c, reinterpret_cast<unsigned char*>(ahp_ws), g.n);
@@ -1622,6 +1641,159 @@ __global__ void __launch_bounds__(1024) k_sequential(Geo g, Opt o, int* state, R
   for (int w = c.tid; w < c.nEW; w += c.B) c.edgebad[w] = 0u;
   __syncthreads();
   for (int r = 0; r < R.n; ++r) run_request<METHOD>(c, R, O, r, true);
+  if (smem_state) store_state_smem(c, sst, state);
+  flush_stats(c, stats);
+}
+
+// ------------------------------------------------------- simulator kernel ---
+// Departure of accepted request r on the live state (thread 0): the exact inverse of its
+// commit and top-up; f_u of its servers re-derived (R22).  st_set keeps the AHP presorted
+// orders informed (touched servers).
+__device__ void release_request(Ctx& c, const ReqsDev& R, const OutDev& O, int r) {
+  const Geo& g = c.g;
+  const int n = g.n;
+  const int c0 = R.coff[r], c1 = R.coff[r + 1], v0 = R.voff[r], v1 = R.voff[r + 1];
+  c.s->log_n = 0;  // releases are never undone
+  for (int i = c0; i < c1; ++i) {
+    const int u = O.server[i];
+    st_set(c, u, c.st[u] + O.cpu_a[i]);
+    st_set(c, n + u, c.st[n + u] + O.ram_a[i]);
+  }
+  for (int e = v0; e < v1; ++e) {
+    const int us = O.server[c0 + R.src[e]], ud = O.server[c0 + R.dst[e]];
+    if (us == ud) continue;  // host bus
+    const int bw = O.bw_a[e];
+    st_set(c, 3 * n + us, c.st[3 * n + us] + bw);
+    st_set(c, 3 * n + ud, c.st[3 * n + ud] + bw);
+    int off[4];
+    const int m = path_links(g, us, ud, O.path[e], off);
+    for (int t = 0; t < m; ++t) st_set(c, off[t], c.st[off[t]] + bw);
+  }
+  for (int i = c0; i < c1; ++i) {
+    const int u = O.server[i];
+    const int a = (c.st[u] < g.cpu_cap || c.st[n + u] < g.ram_cap) ? 1 : 0;
+    if (c.st[2 * n + u] != a) st_set(c, 2 * n + u, a);
+  }
+  c.s->log_n = 0;
+}
+
+// The whole discrete-event run (reading R28) in ONE launch: one CTA keeps the event loop,
+// the queue and the running set on the device, and schedules every attempt with the
+// sequential machinery (run_request, keep) on the live state — no host round trip per
+// attempt.  Per tick: departures (start + duration == t, in acceptance order), arrivals (in
+// `order`, ascending arrival then id), FIFO scan (head-of-line blocking if hol), counters.
+template <int METHOD>
+__global__ void __launch_bounds__(1024) k_simulate(Geo g, Opt o, int* state, ReqsDev R, OutDev O, int2* ulog,
+                                                   float* ahp_ws, double* w64, unsigned long long* stats, SimDev S,
+                                                   int smem_state) {
+  extern __shared__ __align__(16) unsigned char dyn[];
+  __shared__ Scratch s;
+  __shared__ int qn, nq2, next, blocked, done, cnt_s, cnt_l;
+  __shared__ long long n_att, n_acc;
+  Ctx c;
+  init_ctx(c, g, o, &s);
+  size_t off = 0;
+  c.maskw = reinterpret_cast<unsigned*>(dyn + off);
+  off = align16(off + sizeof(unsigned) * c.nW);
+  c.special = reinterpret_cast<unsigned*>(dyn + off);
+  off = align16(off + sizeof(unsigned) * c.nW);
+  c.f0w = reinterpret_cast<unsigned*>(dyn + off);
+  off = align16(off + sizeof(unsigned) * c.nW);
+  c.edgebad = reinterpret_cast<unsigned*>(dyn + off);
+  off = align16(off + sizeof(unsigned) * c.nEW);
+  int* sst = smem_state ? load_state_smem(c, dyn + off, state) : state;
+  c.st = sst;
+  c.snap = sst;
+  c.ulog = ulog;
+  c.nfcap = g.n;
+  if (METHOD == 0) ahp_carve(c, reinterpret_cast<unsigned char*>(ahp_ws), g.n);
+  c.w64 = w64;
+  for (int w = c.tid; w < c.nW; w += c.B) { c.maskw[w] = 0u; c.special[w] = 0u; }
+  for (int w = c.tid; w < c.nEW; w += c.B) c.edgebad[w] = 0u;
+  for (int r = c.tid; r < R.n; r += c.B) { S.start[r] = -1; S.attempts[r] = 0; }
+  for (int i = c.tid; i < S.max_ticks; i += c.B) S.head[i] = -1;
+  if (c.tid == 0) { qn = 0; next = 0; done = 0; n_att = 0; n_acc = 0; }
+  __syncthreads();
+  int* qa = S.qbuf;
+  int* qb = S.qtmp;
+  int t = 0;
+  for (; t < S.max_ticks; ++t) {
+    // (1) departures first: the requests accepted with start + duration == t, kept in a
+    // per-tick bucket (a linked list through S.run) so that a tick touches only its own
+    if (c.tid == 0) {
+      for (int r = S.head[t]; r >= 0; r = S.run[r]) release_request(c, R, O, r);
+    }
+    __syncthreads();
+    // the presorted orders learn the released servers (before the first request there is
+    // no presort yet: the first req_begin sorts the current state)
+    if (METHOD == 0 && s.presorted) ahp_presort_update(c);
+    // (2) arrivals
+    if (c.tid == 0) {
+      while (next < R.n && S.arrival[S.order[next]] == t) qa[qn++] = S.order[next++];
+      nq2 = 0;
+      blocked = 0;
+    }
+    __syncthreads();
+    // (3) FIFO scan of the queue against the live state
+    const int nq = qn;
+    for (int i = 0; i < nq; ++i) {
+      const int r = qa[i];
+      if (blocked) {
+        if (c.tid == 0) qb[nq2++] = r;
+        continue;
+      }
+      run_request<METHOD>(c, R, O, r, true);
+      if (c.tid == 0) {
+        S.attempts[r] += 1;
+        n_att += 1;
+        if (O.status[r] == 1) {
+          S.start[r] = t;
+          const int end = t + S.duration[r];
+          if (end < S.max_ticks) {
+            S.run[r] = S.head[end];
+            S.head[end] = r;
+          }
+          n_acc += 1;
+        } else {
+          qb[nq2++] = r;
+          if (S.hol) blocked = 1;
+        }
+      }
+      __syncthreads();
+    }
+    // (4) counters: active servers |N^s'|, active links |E^s'|, queue length
+    if (c.tid == 0) { cnt_s = 0; cnt_l = 0; }
+    __syncthreads();
+    int as = 0, al = 0;
+    for (int u = c.tid; u < g.n; u += c.B) as += c.st[2 * g.n + u];
+    for (int l = c.tid; l < g.L; l += c.B) al += c.st[3 * g.n + l] < g.link_cap ? 1 : 0;
+    for (int o2 = 16; o2; o2 >>= 1) {
+      as += __shfl_xor_sync(FULL, as, o2);
+      al += __shfl_xor_sync(FULL, al, o2);
+    }
+    if (c.lane == 0) { atomicAdd(&cnt_s, as); atomicAdd(&cnt_l, al); }
+    __syncthreads();
+    if (c.tid == 0) {
+      qn = nq2;
+      S.ticks[3 * t] = cnt_s;
+      S.ticks[3 * t + 1] = cnt_l;
+      S.ticks[3 * t + 2] = qn;
+      done = qn == 0 && next == R.n;
+    }
+    {  // the survivors (qb) are the queue of the next tick; every thread swaps its copy
+      int* tmp = qa;
+      qa = qb;
+      qb = tmp;
+    }
+    __syncthreads();
+    if (done) { ++t; break; }
+  }
+  if (c.tid == 0) {
+    S.totals[0] = t;
+    S.totals[1] = n_att;
+    S.totals[2] = n_acc;
+  }
+  if (smem_state) store_state_smem(c, sst, state);
   flush_stats(c, stats);
 }
 
@@ -2359,16 +2531,47 @@ static int single_block_size(const Geo& g) {
   return b;
 }
 
+// dynamic shared memory of the sequential kernels: bitmaps, plus the live state when it fits
+static size_t seq_smem_bytes(const Geo& g, int* smem_state) {
+  const size_t b = bitmap_bytes(g), st = align16(sizeof(int) * (size_t)g.words());
+  int dev = 0, optin = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  *smem_state = b + st + sizeof(Scratch) + 1024 <= (size_t)optin;
+  return *smem_state ? b + st : b;
+}
+
+template <int M, class K>
+static void set_smem(K kernel, size_t smem) {
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+}
+
 cudaError_t launch_sequential(const Geo& g, const Opt& o, int* d_state, const ReqsDev& R, const OutDev& O,
                               int2* ulog, float* ahp_ws, double* w64, unsigned long long* stats,
                               cudaStream_t st) {
-  size_t smem = bitmap_bytes(g);
+  int ss = 0;
+  const size_t smem = seq_smem_bytes(g, &ss);
   int B = single_block_size(g);
   switch (o.method) {
-    case 0: k_sequential<0><<<1, B, smem, st>>>(g, o, d_state, R, O, ulog, ahp_ws, w64, stats); break;
-    case 1: k_sequential<1><<<1, B, smem, st>>>(g, o, d_state, R, O, ulog, ahp_ws, w64, stats); break;
-    case 2: k_sequential<2><<<1, B, smem, st>>>(g, o, d_state, R, O, ulog, ahp_ws, w64, stats); break;
-    default: k_sequential<3><<<1, B, smem, st>>>(g, o, d_state, R, O, ulog, ahp_ws, w64, stats); break;
+    case 0: set_smem<0>(k_sequential<0>, smem); k_sequential<0><<<1, B, smem, st>>>(g, o, d_state, R, O, ulog, ahp_ws, w64, stats, ss); break;
+    case 1: set_smem<1>(k_sequential<1>, smem); k_sequential<1><<<1, B, smem, st>>>(g, o, d_state, R, O, ulog, ahp_ws, w64, stats, ss); break;
+    case 2: set_smem<2>(k_sequential<2>, smem); k_sequential<2><<<1, B, smem, st>>>(g, o, d_state, R, O, ulog, ahp_ws, w64, stats, ss); break;
+    default: set_smem<3>(k_sequential<3>, smem); k_sequential<3><<<1, B, smem, st>>>(g, o, d_state, R, O, ulog, ahp_ws, w64, stats, ss); break;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_simulate(const Geo& g, const Opt& o, int* d_state, const ReqsDev& R, const OutDev& O,
+                            int2* ulog, float* ahp_ws, double* w64, unsigned long long* stats, const SimDev& S,
+                            cudaStream_t st) {
+  int ss = 0;
+  const size_t smem = seq_smem_bytes(g, &ss);
+  int B = single_block_size(g);
+  switch (o.method) {
+    case 0: set_smem<0>(k_simulate<0>, smem); k_simulate<0><<<1, B, smem, st>>>(g, o, d_state, R, O, ulog, ahp_ws, w64, stats, S, ss); break;
+    case 1: set_smem<1>(k_simulate<1>, smem); k_simulate<1><<<1, B, smem, st>>>(g, o, d_state, R, O, ulog, ahp_ws, w64, stats, S, ss); break;
+    case 2: set_smem<2>(k_simulate<2>, smem); k_simulate<2><<<1, B, smem, st>>>(g, o, d_state, R, O, ulog, ahp_ws, w64, stats, S, ss); break;
+    default: set_smem<3>(k_simulate<3>, smem); k_simulate<3><<<1, B, smem, st>>>(g, o, d_state, R, O, ulog, ahp_ws, w64, stats, S, ss); break;
   }
   return cudaGetLastError();
 }
