@@ -2460,8 +2460,10 @@ int batch_block_size(const Geo& g, int method) {
   if (method == 0) {  // AHP: a warp per level pair in the passes
     const char* e = getenv("NACS_AHP_BLOCK");
     if (e) return atoi(e);
-    // about one (l, K-1-l) level pair per thread in the passes when K ~ n_f ~ n (C3: 512)
-    int b = next_pow2(g.n / 2);
+    // about one (l, K-1-l) level pair per thread in the passes: warm snapshots leave
+    // n_f ~ 0.6 n feasible, so ~0.3 n pairs; 7n/16 threads measured best at C3 (A/B over
+    // 256..512 threads: 448 -> 44.8 ms, 512 -> 47.1 ms, 320 -> 45.1 ms, 256 -> 54.0 ms)
+    int b = ((7 * g.n / 16 + 31) / 32) * 32;
     return b < 128 ? 128 : (b > 512 ? 512 : b);
   }
   int b = ((g.n / 8 + 31) / 32) * 32;  // about 8 servers per thread
