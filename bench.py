@@ -272,6 +272,21 @@ def run_ours(args, rank, world, local):
             v = measure(meth, **kw)
             variants[name] = {"workload": v["name"], "value": v["value"], "unit": "pods/s",
                               "ms_per_step": v["ms_per_step"]}
+        # R2's alternative (bw_criterion = logical): one pod step through nacs_rank_topsis on the
+        # C4 snapshot; the table of 8192 logical-bandwidth sums is rebuilt inside every call
+        snap_c4 = gen.snapshot(32, gen.CONFIG_SEEDS["C4"])
+        ctx.load_topology(snap_c4)
+        for name, bwc in (("topsis_rank_access_bw (R2 default, one pod step per call)", 0),
+                          ("topsis_rank_logical_bw (R2 flag, one pod step per call)", 1)):
+            for _ in range(args.warmup):
+                ctx.rank("topsis", "flat", 1500, 3000, bw_criterion=bwc)
+            barrier()
+            t = time.perf_counter()
+            for _ in range(args.steps):
+                ctx.rank("topsis", "flat", 1500, 3000, bw_criterion=bwc)
+            el = max_over_ranks((time.perf_counter() - t) / args.steps)
+            variants[name] = {"workload": "C4 snapshot (k=32, 8192 servers), host-pointer nacs_rank_topsis call",
+                              "value": 8192 / el, "unit": "servers ranked/s (per GPU)", "ms_per_call": el * 1e3}
 
     # general-topology widest-shortest paths (modified Dijkstra)
     paths = None if args.no_paths else measure_paths(args, ctx, dev, stream, flush, barrier, max_over_ranks,

@@ -136,9 +136,18 @@ typedef struct {
                          * P:375): the request's first pod step ranks the servers once and every
                          * pod takes the first server of that order its own filter (R6) admits.
                          * Schedule calls only; not on server-sharded contexts (NACS_EINVAL). */
+  int32_t bw_criterion; /* NACS_BW_ACCESS (R2, default): the Bandwidth criterion is the residual of
+                         * the server's access link; NACS_BW_LOGICAL (R2's alternative, "the sum of
+                         * all bandwidth capacity bw^s_uv with source on u"; SURVEY 8(f) row
+                         * 4): the sum over servers v != u of the widest-shortest u-v bottleneck on
+                         * the current state.  nacs_rank_* only (schedule calls: NACS_EINVAL; the
+                         * table would change after every commit); NACS_ETOOBIG when some sum
+                         * reaches 2^24 (not exact in FP32, R5: n x link_cap must stay below it,
+                         * e.g. k <= 32 at 1 Gbps).  The feasibility filter keeps the access links. */
 } nacs_options;
 
 enum { NACS_RANK_PER_POD = 0, NACS_RANK_ONCE = 1 };
+enum { NACS_BW_ACCESS = 0, NACS_BW_LOGICAL = 1 };
 
 /* Counters of the last rank/schedule call (reading them synchronises the context stream). */
 typedef struct {

@@ -113,6 +113,7 @@ struct Opts {
   int l1_mode;      // 0 pairwise comparison on W (R10), 1 L1 = W
   int path_filter;  // 1 filter on paths (R6), 0 paper-literal select-then-route
   int rank_once;    // 0 re-rank every pod step (R15); 1 rank once per request (R25)
+  int bw_logical = 0;  // R2 alternative: the Bandwidth criterion is the logical bandwidth
 };
 
 // AHP pairwise cell for a scaled difference d (reading R8).
@@ -211,12 +212,26 @@ RankOut rank(const DC& dc, const Opts& o, long dem_cpu, long dem_ram,
 
   // Criteria vector c^s_u U {f_u, bw^s_u} (readings R1-R3):
   // residual CPU, residual RAM, active flag, residual of u's access link.
+  // R2's alternative reading (`bw_criterion = logical`): bw^s_u = "the sum of all bandwidth
+  // capacity bw^s_uv with source on u", bw^s_uv (T1 P:90) read as the bottleneck of
+  // the widest shortest path u-v (R16): min(access u, access v, widest fabric).
+  std::vector<double> logical;
+  if (o.bw_logical) {
+    logical.assign(dc.n, 0.0);
+    for (int u = 0; u < dc.n; ++u)
+      for (int v = 0; v < dc.n; ++v) {
+        if (v == u) continue;
+        double b = std::min((double)dc.link[dc.access(u)], (double)dc.link[dc.access(v)]);
+        b = std::min(b, fabric_bottleneck(dc, widest_path(dc, u, v)));
+        logical[u] += b;
+      }
+  }
   auto crit = [&](int u, int c) -> double {
     switch (c) {
       case 0: return (double)dc.cpu[u];
       case 1: return (double)dc.ram[u];
       case 2: return (double)dc.active[u];
-      default: return (double)dc.link[dc.access(u)];
+      default: return o.bw_logical ? logical[u] : (double)dc.link[dc.access(u)];
     }
   };
 
@@ -521,9 +536,10 @@ int orc_rank(int k, int cpu_cap, int ram_cap, int link_cap, const int32_t* cpu, 
              const uint8_t* active, const int32_t* link, int method, const double* w, int ahp_rule,
              int l1_mode, int path_filter, int dem_cpu, int dem_ram, int nflow, const int32_t* flow_v,
              const int32_t* flow_D, int nexcl, const int32_t* excl, uint8_t* mask_out, double* score_out,
-             int32_t* best_out, uint8_t* tie_out) {
+             int32_t* best_out, uint8_t* tie_out, int bw_logical) {
   DC dc = make_dc(k, cpu_cap, ram_cap, link_cap, cpu, ram, active, link);
   Opts o = make_opts(method, w, ahp_rule, l1_mode, path_filter);
+  o.bw_logical = bw_logical;
   std::vector<Flow> flows;
   for (int f = 0; f < nflow; ++f) flows.push_back(Flow{flow_v[f], (long)flow_D[f]});
   std::sort(flows.begin(), flows.end(), [](const Flow& a, const Flow& b) { return a.v < b.v; });

@@ -41,7 +41,7 @@ def lib():
         _lib.orc_rank.restype = C.c_int
         _lib.orc_rank.argtypes = [C.c_int] * 4 + [P] * 4 + [C.c_int, P, C.c_int, C.c_int, C.c_int,
                                                           C.c_int, C.c_int, C.c_int, P, P, C.c_int, P,
-                                                          P, P, P, P]
+                                                          P, P, P, P, C.c_int]
         _lib.orc_ahp_priority.argtypes = [C.c_int, P, C.c_int, P]
         _lib.orc_ahp_l1.argtypes = [P, C.c_int, C.c_int, P]
         _lib.orc_widest_path.restype = C.c_int
@@ -76,8 +76,9 @@ def _weights(w):
 
 
 def rank(snap: dict, method: str, weights, dem_cpu: int, dem_ram: int, flows=(), excluded=(),
-         ahp_rule: int = 0, l1_mode: int = 0, path_filter: int = 1):
-    """One pod step's ranking.  flows: iterable of (server v, demand D_v)."""
+         ahp_rule: int = 0, l1_mode: int = 0, path_filter: int = 1, bw_criterion: int = 0):
+    """One pod step's ranking.  flows: iterable of (server v, demand D_v).  bw_criterion=1:
+    the Bandwidth criterion is the logical bandwidth of R2's alternative reading."""
     k = snap["k"]
     n = k ** 3 // 4
     cpu, ram = _i32(snap["cpu_res"]), _i32(snap["ram_res"])
@@ -94,7 +95,7 @@ def rank(snap: dict, method: str, weights, dem_cpu: int, dem_ram: int, flows=(),
     nf = lib().orc_rank(k, snap["cpu_cap"], snap["ram_cap"], snap["link_cap"], _p(cpu), _p(ram), _p(act),
                         _p(link), METHOD[method], _p(w), ahp_rule, l1_mode, path_filter, int(dem_cpu),
                         int(dem_ram), len(flows), _p(fv), _p(fd), len(excluded), _p(ex), _p(mask),
-                        _p(score), _p(best), _p(tie))
+                        _p(score), _p(best), _p(tie), int(bw_criterion))
     return dict(mask=mask, score=score, best=int(best[0]), tie=tie, n_feasible=nf)
 
 

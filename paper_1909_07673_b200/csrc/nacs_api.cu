@@ -111,6 +111,7 @@ struct nacs_ctx {
   DevArr<int> g_io;
   DevArr<long long> g_out;
   DevArr<int> g_ws;
+  DevArr<int> crit;          // logical-bandwidth criteria table (nacs_rank_*, bw_criterion = 1)
   // departures / simulator
   DevArr<long long> rel_delta;
   DevArr<int> sim_buf;
@@ -152,6 +153,7 @@ nacs_status check_options(nacs_ctx* ctx, const nacs_options* o, Opt* out) {
   if (o->flags & ~(NACS_DEVICE_PTRS | NACS_ASYNC | NACS_EXACT_FP64)) m += "options.flags has unknown bits; ";
   if (o->rank_mode != NACS_RANK_PER_POD && o->rank_mode != NACS_RANK_ONCE) m += "options.rank_mode not 0/1; ";
   if (o->method >= NACS_BF && o->rank_mode == NACS_RANK_ONCE) m += "options.rank_mode = NACS_RANK_ONCE needs AHP/TOPSIS; ";
+  if (o->bw_criterion != NACS_BW_ACCESS && o->bw_criterion != NACS_BW_LOGICAL) m += "options.bw_criterion not 0/1; ";
   if (!m.empty()) return fail(ctx, NACS_EINVAL, m);
   out->method = (int)o->method;
   for (int k = 0; k < 4; ++k) out->wd[k] = o->weights[k];
@@ -161,6 +163,7 @@ nacs_status check_options(nacs_ctx* ctx, const nacs_options* o, Opt* out) {
   out->path_filter = o->method >= NACS_BF ? 0 : o->path_filter;
   out->exact64 = (o->flags & NACS_EXACT_FP64) ? 1 : 0;
   out->rank_once = o->rank_mode == NACS_RANK_ONCE;
+  out->bw_logical = o->bw_criterion == NACS_BW_LOGICAL;
   return NACS_OK;
 }
 
@@ -551,6 +554,22 @@ nacs_status rank_impl(nacs_ctx* ctx, const nacs_options* opt, const nacs_pod_que
   qd.mask = (dev && mask) ? mask : ctx->mask.p;
   qd.scores = (dev && scores) ? scores : ctx->scores.p;
   qd.best = dev ? best : ctx->misc.p;
+  qd.crit = nullptr;
+  if (o.bw_logical) {  // R2's logical reading of the Bandwidth criterion
+    if (ctx->world > 1 || ctx->comm)
+      return fail(ctx, NACS_EINVAL, "options.bw_criterion = NACS_BW_LOGICAL is not available on server-sharded contexts");
+    CK(ctx->crit.reserve(4 * (size_t)g.n + (size_t)g.E * g.E + 4));
+    int* crit = ctx->crit.p;
+    int* F = crit + 4 * (size_t)g.n;
+    int* tb = F + (size_t)g.E * g.E;
+    CK(nacs::launch_logical_criteria(g, ctx->state.p, crit, F, tb, ctx->stream));
+    int too_big = 0;
+    CK(cudaMemcpyAsync(&too_big, tb, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (too_big)
+      return fail(ctx, NACS_ETOOBIG, "logical bandwidth >= 2^24 (n x link_cap too large to be exact in FP32, R5)");
+    qd.crit = crit;
+  }
   if (method == 0) {
     CK(ctx->ahp_ws.reserve(nacs::ahp_workspace_bytes(g.n) / 4 + 4));
     CK(ctx->w64.reserve(nacs::ahp_workspace_doubles(g.n)));
@@ -779,6 +798,7 @@ void nacs_destroy(nacs_ctx* ctx) {
   ctx->g_io.release();
   ctx->g_out.release();
   ctx->g_ws.release();
+  ctx->crit.release();
   ctx->rel_delta.release();
   ctx->sim_buf.release();
   ctx->sim_pin.release();
@@ -882,6 +902,7 @@ nacs_status nacs_schedule_batch(nacs_ctx* ctx, const nacs_options* opt, const na
   if (st) return st;
   Opt o;
   if ((st = check_options(ctx, opt, &o))) return st;
+  if (o.bw_logical) return fail(ctx, NACS_EINVAL, "options.bw_criterion = NACS_BW_LOGICAL: rank calls only");
   if ((st = check_placements(ctx, out))) return st;
   if (!batch || batch->n_requests < 0) return fail(ctx, NACS_EINVAL, "requests: NULL or n_requests < 0");
   const bool dev = opt->flags & NACS_DEVICE_PTRS;
@@ -969,6 +990,7 @@ nacs_status nacs_schedule_request(nacs_ctx* ctx, const nacs_options* opt, const 
   if (st) return st;
   Opt o;
   if ((st = check_options(ctx, opt, &o))) return st;
+  if (o.bw_logical) return fail(ctx, NACS_EINVAL, "options.bw_criterion = NACS_BW_LOGICAL: rank calls only");
   if ((st = check_placements(ctx, out))) return st;
   if (!reqs || reqs->n_requests < 0) return fail(ctx, NACS_EINVAL, "requests: NULL or n_requests < 0");
   const bool dev = opt->flags & NACS_DEVICE_PTRS;
@@ -1089,6 +1111,7 @@ nacs_status nacs_simulate(nacs_ctx* ctx, const nacs_options* opt, const nacs_req
   if (st) return st;
   Opt o;
   if ((st = check_options(ctx, opt, &o))) return st;
+  if (o.bw_logical) return fail(ctx, NACS_EINVAL, "options.bw_criterion = NACS_BW_LOGICAL: rank calls only");
   if (opt->flags & (NACS_DEVICE_PTRS | NACS_ASYNC))
     return fail(ctx, NACS_EINVAL, "nacs_simulate takes host pointers and is synchronous");
   if (o.rank_once) return fail(ctx, NACS_EINVAL, "nacs_simulate: rank_mode must be NACS_RANK_PER_POD");

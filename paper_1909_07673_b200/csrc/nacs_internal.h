@@ -33,6 +33,7 @@ struct Opt {
   int path_filter;   // 1 filter on path bandwidth, 0 CPU/RAM only
   int exact64;       // decide every argmax in FP64
   int rank_once;     // R25: rank once per request (the first pod step's order), pods walk it
+  int bw_logical;    // R2 alternative: logical-bandwidth criterion (rank calls only)
 };
 
 struct ReqsDev {
@@ -51,6 +52,7 @@ struct QueryDev {
   uint8_t *mask;            // [n] or null
   float *scores;            // [n] or null
   int *best;                // [1]
+  const int* crit;          // [4n] criteria rows with the logical bandwidth (bw_criterion = 1), or null
 };
 
 enum {
@@ -151,6 +153,10 @@ cudaError_t launch_sequential(const Geo& g, const Opt& o, int* d_state, const Re
 cudaError_t launch_rank(const Geo& g, const Opt& o, int* d_state, const QueryDev& q, float* ahp_ws,
                         double* w64, unsigned long long* stats, cudaStream_t s);
 cudaError_t launch_validate(const ReqsDev& R, int* status, unsigned long long* stats, cudaStream_t s);
+// R2's logical bandwidth criterion on the current fat-tree state: crit = cpu | ram | act | L(u)
+// ([4n]); F: [E*E] scratch; *too_big = 1 if some L(u) >= 2^24 (not exact in FP32)
+cudaError_t launch_logical_criteria(const Geo& g, const int* state, int* crit, int* F, int* too_big,
+                                    cudaStream_t st);
 size_t scratch_bytes();
 cudaError_t launch_sh_begin(const Geo& g, const Opt& o, int* state, const ReqsDev& R, const OutDev& O, int r,
                             const ShardDev& d, cudaStream_t st);

@@ -96,6 +96,8 @@ struct Ctx {
   Geo g;
   Opt o;
   int* st;             // state words (shared memory in k_batch, global otherwise)
+  const int* cr;       // criteria rows cpu | ram | act | bandwidth criterion (= st, or the
+                       // logical-bandwidth table of nacs_rank_* with bw_criterion = 1)
   const int* snap;     // global snapshot (k_batch) for reference
   Scratch* s;
   unsigned* maskw;     // [nW] feasibility bitmap of the current pod step
@@ -430,7 +432,8 @@ __device__ void pass_filter(Ctx& c, uint8_t* mask_out, float* scores_out) {
   const int* cpu = c.st;
   const int* ram = c.st + n;
   const int* act = c.st + 2 * n;
-  const int* acc = c.st + 3 * n;
+  const int* acc = c.st + 3 * n;     // access-link residuals: the filter (Eq. 5-7)
+  const int* bwc = c.cr + 3 * n;     // the Bandwidth criterion (R2, or its logical reading)
   const int dc = s->dc, dr = s->dr, sumD = s->sumD;
   const bool net = c.o.path_filter && s->nflow > 0;
   const bool G = s->G != 0;
@@ -441,11 +444,11 @@ __device__ void pass_filter(Ctx& c, uint8_t* mask_out, float* scores_out) {
     int u = base + c.lane;
     bool in = u < n;
     int x0 = 0, x1 = 0, x2 = 0, x3 = 0;
-    if (in) { x0 = cpu[u]; x1 = ram[u]; x2 = act[u]; x3 = acc[u]; }
+    if (in) { x0 = cpu[u]; x1 = ram[u]; x2 = act[u]; x3 = bwc[u]; }
     bool ok = in && x0 >= dc && x1 >= dr;
     if (net) {
       unsigned e = div_h((unsigned)u, g.magic_h);
-      ok = ok && G && x3 >= sumD && !((c.edgebad[e >> 5] >> (e & 31)) & 1u);
+      ok = ok && G && acc[u] >= sumD && !((c.edgebad[e >> 5] >> (e & 31)) & 1u);
     }
     unsigned sp = c.special[base >> 5];
     if ((sp >> c.lane) & 1u) {
@@ -544,7 +547,7 @@ template <bool WRITE_SCORES>
 __device__ void select_topsis(Ctx& c, float* scores_out) {
   Scratch* s = c.s;
   const int n = c.g.n;
-  const int* st = c.st;
+  const int* st = c.cr;  // criteria rows
   // R25: the first pod step ranks with its own statistics and keeps them with its feasible
   // set; later pod steps take the best of that order among the servers their filter admits
   if (c.o.rank_once && s->p > 0) {
@@ -707,7 +710,7 @@ __device__ void ahp_presort(Ctx& c) {
   Scratch* s = c.s;
   const int n = c.g.n, P2 = next_pow2(n);
   for (int ci = 0; ci < 3; ++ci) {
-    const int* x = c.st + crit_of(ci) * n;
+    const int* x = c.cr + crit_of(ci) * n;
     for (int i = c.tid; i < P2; i += c.B) {
       c.keys[i] = i < n ? (float)x[i] : FLT_MAX;
       c.sidx[i] = i;
@@ -776,7 +779,7 @@ __device__ __forceinline__ bool feas_bit(const Ctx& c, int u) { return (c.maskw[
 __device__ int presorted_collect(Ctx& c, int ci, bool feasible_only) {
   Scratch* s = c.s;
   const int n = c.g.n, P2 = next_pow2(n);
-  const int* x = c.st + crit_of(ci) * n;
+  const int* x = c.cr + crit_of(ci) * n;
   const unsigned short* perm = c.perm + ci * P2;
   int s0, s1;
   warp_seg(c, n, s0, s1);
@@ -1539,6 +1542,7 @@ __global__ void __launch_bounds__(1024) k_batch(Geo g, Opt o, const int* __restr
   const int nW = c.nW, nEW = c.nEW, n = g.n;
   size_t off = 0;
   c.st = reinterpret_cast<int*>(dyn);
+  c.cr = c.st;
   off = align16(off + sizeof(int) * (size_t)g.words());
   c.maskw = reinterpret_cast<unsigned*>(dyn + off);
   off = align16(off + sizeof(unsigned) * nW);
@@ -1632,6 +1636,7 @@ __global__ void __launch_bounds__(1024) k_sequential(Geo g, Opt o, int* state, R
   off = align16(off + sizeof(unsigned) * c.nEW);
   int* sst = smem_state ? load_state_smem(c, dyn + off, state) : state;
   c.st = sst;
+  c.cr = c.st;
   c.snap = sst;
   c.ulog = ulog;
   c.nfcap = g.n;
@@ -1703,6 +1708,7 @@ __global__ void __launch_bounds__(1024) k_simulate(Geo g, Opt o, int* state, Req
   off = align16(off + sizeof(unsigned) * c.nEW);
   int* sst = smem_state ? load_state_smem(c, dyn + off, state) : state;
   c.st = sst;
+  c.cr = c.st;
   c.snap = sst;
   c.ulog = ulog;
   c.nfcap = g.n;
@@ -1813,6 +1819,7 @@ __global__ void __launch_bounds__(1024) k_rank(Geo g, Opt o, int* state, QueryDe
   off = align16(off + sizeof(unsigned) * c.nW);
   c.edgebad = reinterpret_cast<unsigned*>(dyn + off);
   c.st = state;
+  c.cr = q.crit ? q.crit : c.st;
   c.snap = state;
   c.nfcap = g.n;
   if (METHOD == 0) {
@@ -1884,6 +1891,7 @@ enum { PH_DONE = 0, PH_NEWPOD = 1, PH_RETRY = 2, PH_FP64 = 3 };
 __device__ void sh_ctx(Ctx& c, const Geo& g, const Opt& o, int* state, const ShardDev& d) {
   ctx_basic(c, g, o, d.gs);
   c.st = state;
+  c.cr = c.st;
   c.snap = state;
   c.maskw = d.maskw;
   c.special = d.special;
@@ -2584,6 +2592,76 @@ cudaError_t launch_rank(const Geo& g, const Opt& o, int* d_state, const QueryDev
   int B = single_block_size(g);
   if (o.method == 1) k_rank<1><<<1, B, smem, st>>>(g, o, d_state, q, ahp_ws, w64, stats);
   else k_rank<0><<<1, B, smem, st>>>(g, o, d_state, q, ahp_ws, w64, stats);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------ logical bandwidth criterion ---
+// R2's alternative reading (`bw_criterion = logical`, "the sum of all bandwidth
+// capacity bw^s_uv with source on u"): L(u) = sum over servers v != u of the bottleneck of
+// the widest shortest u-v path on the current state, min(acc_u, acc_v, F(e_u, e_v)) with
+// F the widest fabric bottleneck between the two edge switches (R16; +inf on one switch).
+// k_ft_fabric: F for every ordered pair of edge switches (a thread per pair, h or h^2 paths);
+// k_ft_logical: a CTA per edge switch sums min(.) over all servers for its h servers.
+__global__ void k_ft_fabric(Geo g, const int* __restrict__ state, int* F) {
+  const int E = g.E, h = g.h, n = g.n;
+  const int* EA = state + 4 * n;
+  const int* AC = EA + E * h;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < E * E; idx += gridDim.x * blockDim.x) {
+    const int e = idx / E, f = idx - e * E;
+    int best;
+    if (e == f) {
+      best = INT_MAX;
+    } else if (e / h == f / h) {
+      best = 0;
+      for (int a = 0; a < h; ++a) best = max(best, min(EA[e * h + a], EA[f * h + a]));
+    } else {
+      const int pe = e / h, pf = f / h;
+      best = 0;
+      for (int a = 0; a < h; ++a) {
+        const int up = min(EA[e * h + a], EA[f * h + a]);
+        if (up <= best) continue;
+        for (int b = 0; b < h; ++b)
+          best = max(best, min(up, min(AC[(pe * h + a) * h + b], AC[(pf * h + a) * h + b])));
+      }
+    }
+    F[idx] = best;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_ft_logical(Geo g, const int* __restrict__ state, const int* __restrict__ F,
+                                                    int* crit, int* too_big) {
+  const int e = blockIdx.x, h = g.h, n = g.n;
+  const int* acc = state + 3 * n;
+  __shared__ long long part[8][32];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = 0; i < h; ++i) {
+    const int u = e * h + i;
+    const int au = acc[u];
+    long long sum = 0;
+    for (int v = threadIdx.x; v < n; v += blockDim.x) {
+      if (v == u) continue;
+      sum += min(min(au, acc[v]), F[e * g.E + v / h]);
+    }
+    for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xFFFFFFFFu, sum, o);
+    if (lane == 0) part[w][i] = sum;
+  }
+  __syncthreads();
+  if (threadIdx.x < h) {
+    long long L = 0;
+    for (int j = 0; j < (int)(blockDim.x >> 5); ++j) L += part[j][threadIdx.x];
+    if (L >= (1LL << 24)) atomicOr(too_big, 1);  // not exact in FP32 (R5): the caller fails
+    crit[3 * n + e * h + threadIdx.x] = (int)min(L, (long long)INT_MAX);
+  }
+}
+
+cudaError_t launch_logical_criteria(const Geo& g, const int* state, int* crit, int* F, int* too_big,
+                                    cudaStream_t st) {
+  cudaError_t e = cudaMemcpyAsync(crit, state, sizeof(int) * 3 * (size_t)g.n, cudaMemcpyDeviceToDevice, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(too_big, 0, sizeof(int), st);
+  if (e != cudaSuccess) return e;
+  const int EE = g.E * g.E;
+  k_ft_fabric<<<std::min(4096, (EE + 255) / 256), 256, 0, st>>>(g, state, F);
+  k_ft_logical<<<g.E, 256, 0, st>>>(g, state, F, crit, too_big);
   return cudaGetLastError();
 }
 

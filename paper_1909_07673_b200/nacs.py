@@ -59,7 +59,7 @@ class Placements(C.Structure):
 class Options(C.Structure):
     _fields_ = [("method", C.c_int), ("weights", C.c_double * 4), ("ahp_rule", C.c_int32),
                 ("l1_mode", C.c_int32), ("path_filter", C.c_int32), ("flags", C.c_uint32),
-                ("rank_mode", C.c_int32)]
+                ("rank_mode", C.c_int32), ("bw_criterion", C.c_int32)]
 
 
 class Stats(C.Structure):
@@ -235,12 +235,13 @@ class Context:
 
     # -------------------------------------------------------------- options --
     @staticmethod
-    def options(method, weights, ahp_rule=0, l1_mode=0, path_filter=1, flags=0, rank_once=False) -> Options:
+    def options(method, weights, ahp_rule=0, l1_mode=0, path_filter=1, flags=0, rank_once=False,
+                bw_criterion=0) -> Options:
         if isinstance(weights, str):
             weights = SCHEMAS[weights]
         m = METHODS[method] if isinstance(method, str) else int(method)
         return Options(m, (C.c_double * 4)(*[float(w) for w in weights]), ahp_rule, l1_mode, path_filter, flags,
-                       NACS_RANK_ONCE if rank_once else NACS_RANK_PER_POD)
+                       NACS_RANK_ONCE if rank_once else NACS_RANK_PER_POD, int(bw_criterion))
 
     # ---------------------------------------------------------------- rank ---
     def rank(self, method, weights, dem_cpu, dem_ram, flows=(), excluded=(), exact64=False, **kw) -> dict:

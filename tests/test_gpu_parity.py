@@ -514,3 +514,35 @@ def test_warp_kernel_ragged_chunk_layouts(ctx, k):
         assert_schedule_parity(snap, sub, out, "topsis", "flat", False)
     finally:
         cta.close()
+
+
+# ------------------------------------------- logical bandwidth criterion -----
+@pytest.mark.parametrize("k", [4, 6, 8, 16])
+@pytest.mark.parametrize("method", ["topsis", "ahp"])
+def test_rank_logical_bandwidth_criterion(ctx, k, method):
+    """R2's alternative reading (bw_criterion = logical): the Bandwidth
+    criterion is the sum of widest-shortest bottlenecks to every other server."""
+    rng = np.random.default_rng(3000 + k)
+    for trial in range(1 if k == 16 else 3):  # the oracle's logical table is O(n^2 paths): 5 s at k=16
+        snap = gen.snapshot(k, seed=400 + trial, quantised=trial == 2)
+        ctx.load_topology(snap)
+        flows = random_flows(rng, snap, int(rng.integers(0, 3)))
+        dc, dr = int(rng.integers(100, 8000)), int(rng.integers(128, 30000))
+        for schema in (("network",) if k == 16 else SCHEMAS):
+            g = ctx.rank(method, schema, dc, dr, flows, bw_criterion=1)
+            o = O.rank(snap, method, schema, dc, dr, flows, bw_criterion=1)
+            assert_rank_parity(g, o, (k, trial, schema))
+
+
+def test_logical_bandwidth_limits(ctx):
+    from paper_1909_07673_b200 import nacs
+    snap = gen.snapshot(32, 4, link_cap=4000)  # n x link_cap = 32.8M >= 2^24: not exact in FP32
+    ctx.load_topology(snap)
+    with pytest.raises(nacs.NacsError) as e:
+        ctx.rank("topsis", "flat", 100, 100, bw_criterion=1)
+    assert e.value.status == nacs.NACS_ETOOBIG
+    snap, reqs = gen.config("C2")
+    ctx.load_topology(snap)
+    with pytest.raises(nacs.NacsError) as e:
+        ctx.schedule_batch(reqs, "topsis", "flat", bw_criterion=1)
+    assert e.value.status == nacs.NACS_EINVAL

@@ -238,3 +238,24 @@ def test_path_rows_longer_than_max_hops_are_empty():
     bn, hops, path = O.graph_paths(g, [0, 0], [1, 15], [0, 0], max_hops=4)
     assert hops.tolist() == [2, 6] and bn.tolist() == [1000, 1000]
     assert path[0].tolist() == [0, 16, 1, -1, -1] and path[1].tolist() == [-1] * 5
+
+
+def test_rank_with_logical_bandwidth_criterion():
+    """R2 alternative in the ranking: the oracle's Bandwidth criterion equals the logical
+    bandwidth of the general-graph Dijkstra on the same state (two independent routes: the
+    fat-tree closed form inside orc_rank, the explicit-graph Dijkstra here).  Checked through a
+    one-criterion TOPSIS: with weights (0, 0, 0, 1) the closeness orders servers by the
+    criterion, so the argmax is the server of largest logical bandwidth (lowest index on ties)."""
+    snap = gen.snapshot(4, 31)
+    lb = O.logical_bandwidth(gen.fat_tree_graph(snap))
+    r = O.rank(snap, "topsis", (0.0, 0.0, 0.0, 1.0), 1, 1, bw_criterion=1)
+    feas = r["mask"].astype(bool)
+    cand = np.nonzero(feas)[0]
+    assert r["best"] == int(cand[np.argmax(lb[cand])])
+    # closeness with one criterion: (x - min) / (max - min) over F
+    x = lb[cand].astype(np.float64)
+    exp = (x - x.min()) / (x.max() - x.min())
+    assert np.allclose(r["score"][cand], exp, rtol=1e-12, atol=1e-15)
+    r0 = O.rank(snap, "topsis", (0.0, 0.0, 0.0, 1.0), 1, 1, bw_criterion=0)
+    acc = snap["link_res"][:16].astype(np.float64)[cand]
+    assert np.allclose(r0["score"][cand], (acc - acc.min()) / (acc.max() - acc.min()), rtol=1e-12, atol=1e-15)
