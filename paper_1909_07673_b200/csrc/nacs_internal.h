@@ -214,6 +214,8 @@ struct PathLaunch {
   bool smem_graph;       // graph + per-warp scratch in shared memory
   size_t dyn_smem;
   size_t global_bytes;   // per-warp scratch in global memory (grid * warps * path_warp_bytes) when V is too large
+  int cta_grid;          // CTA-cooperative grouped kernel (shared-memory layout), 0 = not used
+  size_t cta_smem;
 };
 __host__ __device__ size_t path_warp_bytes(int V, bool smem_mode);
 PathLaunch path_launch_config(const GraphDev& G, int num_sms);

@@ -519,6 +519,199 @@ __global__ void __launch_bounds__(512) k_logical_bw(GraphDev G, long long* out, 
   if (lane == 0 && edges) atomicAdd(stats + ST_EDGES, edges);
 }
 
+// ---- CTA-cooperative grouped kernel (shared-memory layout) ------------------------------
+// One destination group per CTA at a time (work counter), all warps on its BFS: a frontier
+// of a fat-tree level is hundreds of vertices, so 8 warps share it; per-CTA scratch is one
+// key[V] + queue[V], so 3 CTAs (24 warps) fit an SM beside the graph copy, against 11 warps
+// of private per-warp scratch, and 2000 groups spread over 444 CTAs instead of 1628 warps
+// (the per-warp kernel ran 7.2 of 11 warps active: one or two groups per warp).
+template <class GR, class QT>
+__device__ int cta_bfs(const GR& G, unsigned* key, QT* queue, int* tailp, int root, int demand,
+                       unsigned long long* edges) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, NW = blockDim.x >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  if (threadIdx.x == 0) {
+    key[root] = 0u;
+    queue[0] = (QT)root;
+    *tailp = 1;
+  }
+  __syncthreads();
+  int head = 0, tail = 1, level = 0;
+  unsigned long long cnt = 0;
+  for (;;) {
+    const unsigned nl = (unsigned)(level + 1) & 255u;
+    for (int base = head + warp * 32; base < tail; base += NW * 32) {
+      const int i = base + lane;
+      int b = 0, e = 0;
+      unsigned Wv = 0;
+      if (i < tail) {
+        const int v = (int)queue[i];
+        Wv = width_of(((volatile unsigned*)key)[v]);
+        b = G.begin(v);
+        e = G.end(v);
+        cnt += (unsigned)(e - b);
+      }
+      if (e - b <= HEAVY) {
+        for (int j = b; j < e; ++j) {
+          const int2 a = G.edge(j);
+          if (relax(key, a, Wv, nl, demand)) queue[atomicAdd(tailp, 1)] = (QT)a.x;
+        }
+      }
+      unsigned heavy = __ballot_sync(FULL, e - b > HEAVY);
+      while (heavy) {
+        const int l = __ffs(heavy) - 1;
+        heavy &= heavy - 1;
+        const int hb = __shfl_sync(FULL, b, l), he = __shfl_sync(FULL, e, l);
+        const unsigned hW = __shfl_sync(FULL, Wv, l);
+        for (int j0 = hb; j0 < he; j0 += 32) {
+          const int j = j0 + lane;
+          bool nw = false;
+          int2 a = make_int2(-1, 0);
+          if (j < he) {
+            a = G.edge(j);
+            nw = relax(key, a, hW, nl, demand);
+          }
+          const unsigned m = __ballot_sync(FULL, nw);
+          if (m) {
+            int at = 0;
+            if (lane == 0) at = atomicAdd(tailp, __popc(m));
+            at = __shfl_sync(FULL, at, 0);
+            if (nw) queue[at + __popc(m & lt)] = (QT)a.x;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    const int nt = *(volatile int*)tailp;
+    head = tail;
+    tail = nt;
+    ++level;
+    __syncthreads();  // every thread has read the tail before the next level appends
+    if (head == tail) {
+      --level;
+      break;
+    }
+  }
+  for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(FULL, cnt, o);
+  if (lane == 0 && edges) *edges += cnt;
+  return level;
+}
+
+__global__ void __launch_bounds__(256) k_paths_grouped_cta(GraphDev G, const int* __restrict__ src,
+                                                           const int* __restrict__ demand, const int* dmin,
+                                                           const int* start, const int* groups, const int* order,
+                                                           int* ctr, int* deferred, int* bn, int* hops, int* path,
+                                                           int max_hops, unsigned long long* stats) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ int gi_s, tail_s;
+  int* off = reinterpret_cast<int*>(smem);
+  unsigned* adj = reinterpret_cast<unsigned*>(off + G.V + 1);
+  for (int i = threadIdx.x; i <= G.V; i += blockDim.x) off[i] = __ldg(G.off + i);
+  for (int i = threadIdx.x; i < G.n_adj; i += blockDim.x) adj[i] = __ldg(G.adj16 + i);
+  unsigned* key = reinterpret_cast<unsigned*>(
+      reinterpret_cast<unsigned char*>(smem) + ((4 * ((size_t)G.V + 1) + 4 * (size_t)G.n_adj + 15) & ~(size_t)15));
+  uint16_t* queue = reinterpret_cast<uint16_t*>(key + G.V);
+  for (int i = threadIdx.x; i < G.V; i += blockDim.x) key[i] = UNVIS;
+  SmemGraph gr;
+  gr.off = off;
+  gr.adj = adj;
+  __syncthreads();
+  const int ngroups = ctr[0];
+  unsigned long long edges = 0, runs = 0;
+  for (;;) {
+    if (threadIdx.x == 0) gi_s = atomicAdd(ctr + 1, 1);
+    __syncthreads();
+    const int gi = gi_s;
+    if (gi >= ngroups) break;
+    const int t = groups[gi];
+    const int d0 = dmin[t];
+    const int depth = cta_bfs(gr, key, queue, &tail_s, t, d0, &edges);
+    ++runs;
+    const int tail = tail_s;
+    const bool exact = depth <= 255;
+    for (int i = start[t] + threadIdx.x; i < start[t + 1]; i += blockDim.x) {
+      const int q = order[i];
+      const int s = __ldg(src + q), d = __ldg(demand + q);
+      const unsigned ks = ((volatile unsigned*)key)[s];
+      const unsigned B = width_of(ks);
+      if (!exact || (ks != UNVIS && B < (unsigned)d)) {
+        deferred[atomicAdd(ctr + 2, 1)] = q;
+        continue;
+      }
+      const int L = ks == UNVIS ? -1 : (int)(ks >> 24);
+      bn[q] = L < 0 ? -1 : (int)B;
+      hops[q] = L;
+      if (path) {
+        int* prow = path + (size_t)q * (max_hops + 1);
+        int at = 0;
+        if (L >= 0 && L <= max_hops) {
+          int v = s;
+          prow[at++] = v;
+          for (int step = 1; step <= L; ++step) {
+            const unsigned want = (unsigned)(L - step) & 255u;
+            int best = INT_MAX;
+            for (int j = gr.begin(v), e = gr.end(v); j < e; ++j) {
+              const int2 a = gr.edge(j);
+              if (a.y < d0 || a.x >= best) continue;
+              const unsigned kw = ((volatile unsigned*)key)[a.x];
+              if (kw == UNVIS || (kw >> 24) != want || min((unsigned)a.y, width_of(kw)) < B) continue;
+              best = a.x;
+            }
+            v = best;
+            prow[at++] = v;
+          }
+        }
+        for (; at <= max_hops; ++at) prow[at] = -1;
+      }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < tail; i += blockDim.x) key[(int)queue[i]] = UNVIS;
+    __syncthreads();
+  }
+  if ((threadIdx.x & 31) == 0 && edges) atomicAdd(stats + ST_EDGES, edges);
+  if (threadIdx.x == 0 && runs) atomicAdd(stats + ST_BFS, runs);
+}
+
+// Logical bandwidth with the CTA-cooperative BFS (shared-memory layout): a CTA per server u.
+__global__ void __launch_bounds__(256) k_logical_bw_cta(GraphDev G, long long* out, unsigned long long* stats) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ int tail_s;
+  __shared__ long long part[8];
+  int* off = reinterpret_cast<int*>(smem);
+  unsigned* adj = reinterpret_cast<unsigned*>(off + G.V + 1);
+  for (int i = threadIdx.x; i <= G.V; i += blockDim.x) off[i] = __ldg(G.off + i);
+  for (int i = threadIdx.x; i < G.n_adj; i += blockDim.x) adj[i] = __ldg(G.adj16 + i);
+  unsigned* key = reinterpret_cast<unsigned*>(
+      reinterpret_cast<unsigned char*>(smem) + ((4 * ((size_t)G.V + 1) + 4 * (size_t)G.n_adj + 15) & ~(size_t)15));
+  uint16_t* queue = reinterpret_cast<uint16_t*>(key + G.V);
+  for (int i = threadIdx.x; i < G.V; i += blockDim.x) key[i] = UNVIS;
+  SmemGraph gr;
+  gr.off = off;
+  gr.adj = adj;
+  __syncthreads();
+  unsigned long long edges = 0;
+  for (int u = blockIdx.x; u < G.ns; u += gridDim.x) {
+    cta_bfs(gr, key, queue, &tail_s, u, 0, &edges);
+    const int tail = tail_s;
+    long long sum = 0;
+    for (int i = 1 + threadIdx.x; i < tail; i += blockDim.x) {
+      const int v = (int)queue[i];
+      if (v < G.ns) sum += width_of(((volatile unsigned*)key)[v]);
+    }
+    for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(FULL, sum, o);
+    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = sum;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      long long t = 0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += part[w];
+      out[u] = t;
+    }
+    for (int i = threadIdx.x; i < tail; i += blockDim.x) key[(int)queue[i]] = UNVIS;
+    __syncthreads();
+  }
+  if ((threadIdx.x & 31) == 0 && edges) atomicAdd(stats + ST_EDGES, edges);
+}
+
 template <class K>
 int occupancy(K kernel, int threads, size_t smem) {
   int blocks = 0;
@@ -550,6 +743,10 @@ PathLaunch path_launch_config(const GraphDev& G, int num_sms) {
       c.dyn_smem = gbytes + per * c.warps;
       int blocks = occupancy(k_paths_grouped<true>, c.warps * 32, c.dyn_smem);
       c.grid = num_sms * std::max(1, blocks);
+      // the CTA-cooperative grouped kernel: graph + one key[V] | queue[V] per CTA
+      c.cta_smem = gbytes + ((6 * (size_t)G.V + 15) & ~(size_t)15);
+      const int cb = occupancy(k_paths_grouped_cta, 256, c.cta_smem);
+      c.cta_grid = cb > 0 ? num_sms * cb : 0;
       return c;
     }
   }
@@ -595,6 +792,12 @@ static cudaError_t launch_paths_t(const GraphDev& G, const PathLaunch& c, int nq
   k_pg_count<<<eg, 256, 0, st>>>(G, nq, src, dst, demand, cnt, dmin, bn, hops, path, max_hops, stats);
   k_pg_scan<<<1, 1024, 0, st>>>(V, cnt, start, groups, ctr);
   k_pg_scatter<<<eg, 256, 0, st>>>(G, nq, src, dst, demand, start, fill, order);
+  if (SM && c.cta_grid > 0) {
+    e = cudaFuncSetAttribute(k_paths_grouped_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.cta_smem);
+    if (e != cudaSuccess) return e;
+    k_paths_grouped_cta<<<c.cta_grid, 256, c.cta_smem, st>>>(G, src, demand, dmin, start, groups, order, ctr,
+                                                              deferred, bn, hops, path, max_hops, stats);
+  } else
   k_paths_grouped<SM><<<c.grid, c.warps * 32, c.dyn_smem, st>>>(G, src, demand, dmin, start, groups, order, ctr,
                                                                 deferred, bn, hops, path, max_hops, gs, c.warps,
                                                                 stats);
@@ -618,7 +821,12 @@ cudaError_t launch_logical_bw(const GraphDev& G, const PathLaunch& c, long long*
   if (G.ns <= 0) return cudaSuccess;
   const int grid = std::min(c.grid, (G.ns + c.warps - 1) / c.warps);
   unsigned* gs = c.global_bytes ? gscratch : nullptr;
-  if (c.smem_graph) {
+  if (c.smem_graph && c.cta_grid > 0) {
+    cudaError_t e = cudaFuncSetAttribute(k_logical_bw_cta, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)c.cta_smem);
+    if (e != cudaSuccess) return e;
+    k_logical_bw_cta<<<std::min(c.cta_grid, G.ns), 256, c.cta_smem, st>>>(G, out, stats);
+  } else if (c.smem_graph) {
     cudaError_t e = cudaFuncSetAttribute(k_logical_bw<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)c.dyn_smem);
     if (e != cudaSuccess) return e;
