@@ -443,7 +443,7 @@ def measure_paths(args, ctx, dev, stream, flush, barrier, max_over_ranks, sum_ov
                     "d2h_bytes_per_step": 4 * nq * (mh + 3)},
             "logical_bandwidth": {"value": sum_over_ranks(ns * (ns - 1)) / (ms_lb / 1e3), "unit": "server pairs/s",
                                   "ms_per_step": ms_lb, "edges_scanned_per_source": edges_lb / ns},
-            "kernel": "k_paths (warp per query, level-synchronous BFS, smem atomicMin labels)"}
+            "kernel": "k_paths_grouped_cta (a CTA per destination group: one BFS, smem atomicMin labels; walks per thread)"}
 
 
 # T5: events, average runtime (s), U(ij), U(i) per algorithm on the paper's GPU
