@@ -920,8 +920,9 @@ __device__ void ahp_prefix(Ctx& c, int K, const float2* lv) {
 // (arr[k].x - v) (pass 2, above), or 1 + s * that under the shifted rule.  Terms in FP32
 // with MUFU reciprocals, summed in chunks of 32 (four interleaved accumulators); the
 // chunk sums accumulate in FP64, so the error does not grow with the number of levels.
-template <bool ABOVE>
-__device__ __forceinline__ double rsum_f32(const float2* arr, int k0, int k1, float v, float sc, int rule) {
+template <bool ABOVE, int RULE>  // RULE a template parameter: no per-term selects for the literal rule
+__device__ __forceinline__ double rsum_f32(const float2* arr, int k0, int k1, float v, float sc) {
+  constexpr int rule = RULE;
   double outer = 0.0;
   int k = k0;
   float h0 = 0.f;
@@ -971,9 +972,9 @@ __device__ __forceinline__ double rsum_f32(const float2* arr, int k0, int k1, fl
 // Warp-cooperative version for long level lists (grid passes): lane takes terms
 // k0 + lane + 32 j, FP32 chunks of 32 terms per lane into an FP64 lane sum, then a
 // fixed-order shuffle tree (deterministic).
-template <bool ABOVE>
-__device__ __forceinline__ double rsum_warp(const float2* arr, int k0, int k1, float v, float sc, int rule,
-                                            int lane) {
+template <bool ABOVE, int RULE>
+__device__ __forceinline__ double rsum_warp(const float2* arr, int k0, int k1, float v, float sc, int lane) {
+  constexpr int rule = RULE;
   double outer = 0.0;
   int k = k0 + lane;
   while (k < k1) {
@@ -1029,7 +1030,7 @@ __device__ void ahp_passes_f32(Ctx& c, int kc, int K, int m, float* l2out) {
       const int l = side ? K - 1 - t : t;
       if (side && l == t) break;
       const float2 me = c.lvm[l];
-      const double rec = rsum_f32<false>(c.lvm, 0, l, me.x, sc, rule);
+      const double rec = rule ? rsum_f32<false, 1>(c.lvm, 0, l, me.x, sc) : rsum_f32<false, 0>(c.lvm, 0, l, me.x, sc);
       const double cgt = PAK - c.pa[l + 1];
       const double G = (PBK - c.pb[l + 1]) - cgt * (double)me.x;  // sum_{k>l} m_k (v_k - v_l), exact
       const double col = rule ? cgt + sd * G + (double)me.y + (double)rec
@@ -1044,7 +1045,7 @@ __device__ void ahp_passes_f32(Ctx& c, int kc, int K, int m, float* l2out) {
       const int l = side ? K - 1 - t : t;
       if (side && l == t) break;
       const float2 me = c.lvw[l];
-      const double rec = rsum_f32<true>(c.lvw, l + 1, K, me.x, sc, rule);
+      const double rec = rule ? rsum_f32<true, 1>(c.lvw, l + 1, K, me.x, sc) : rsum_f32<true, 0>(c.lvw, l + 1, K, me.x, sc);
       const double lin = (double)me.x * c.pa[l] - c.pb[l];  // sum_{k<l} w_k (v_l - v_k)
       const double L = rule ? c.pa[l] + sd * lin + (double)me.y + (double)rec
                             : sd * lin + (double)me.y + (double)rec * inv_sd;
@@ -2168,7 +2169,7 @@ __global__ void __launch_bounds__(256) k_ahp_pass(Geo g, Opt o, int q0, int q1, 
 #pragma unroll
           for (int off = 16; off > 0; off >>= 1) rec += __shfl_xor_sync(FULL, rec, off);
         } else {
-          rec = rsum_warp<false>(lvm, 0, l, lvm[l].x, sc, rule, lane);
+          rec = rule ? rsum_warp<false, 1>(lvm, 0, l, lvm[l].x, sc, lane) : rsum_warp<false, 0>(lvm, 0, l, lvm[l].x, sc, lane);
         }
         if (lane == 0) {
           const double cgt = pa[K] - pa[l + 1];
@@ -2190,7 +2191,7 @@ __global__ void __launch_bounds__(256) k_ahp_pass(Geo g, Opt o, int q0, int q1, 
           for (int off = 16; off > 0; off >>= 1) rec += __shfl_xor_sync(FULL, rec, off);
         } else {
           wl = (double)lvw[l].y;
-          rec = rsum_warp<true>(lvw, l + 1, K, lvw[l].x, sc, rule, lane);
+          rec = rule ? rsum_warp<true, 1>(lvw, l + 1, K, lvw[l].x, sc, lane) : rsum_warp<true, 0>(lvw, l + 1, K, lvw[l].x, sc, lane);
         }
         if (lane == 0) {
           const double lin = vl * pa[l] - pb[l];  // sum_{k<l} w_k (v_l - v_k)
