@@ -2536,6 +2536,7 @@ cudaError_t launch_batch(const Geo& g, const Opt& o, const int* d_state, const R
 }
 
 static int single_block_size(const Geo& g) {
+  if (const char* e = getenv("NACS_SEQ_BLOCK")) return atoi(e);  // experiments
   int b = ((g.n / 4 + 31) / 32) * 32;
   if (b < 64) b = 64;
   if (b > 1024) b = 1024;
