@@ -57,6 +57,7 @@ def parse():
     ap.add_argument("--no-variants", action="store_true")
     ap.add_argument("--no-paths", action="store_true")
     ap.add_argument("--no-sim", action="store_true")
+    ap.add_argument("--no-c5", action="store_true")
     return ap.parse_args()
 
 
@@ -292,6 +293,9 @@ def run_ours(args, rank, world, local):
     paths = None if args.no_paths else measure_paths(args, ctx, dev, stream, flush, barrier, max_over_ranks,
                                                      sum_over_ranks, rank, local)
 
+    # C5 (BASELINE configs[4]): k=64, sequential scheduling with the servers sharded over the ranks
+    c5 = None if args.no_c5 else measure_c5(args, rank, world, local, stream, max_over_ranks)
+
     # the E2 campaign through the discrete-event simulator (T5-shaped rows)
     sim = None if (args.no_sim or rank != 0) else measure_sim(ctx)
 
@@ -369,7 +373,7 @@ def run_ours(args, rank, world, local):
                 "kernel_ms": topsis["kernel_ms"], "fp64_decisions": topsis["stats"]["fp64_decisions"],
                 "retries": topsis["stats"]["retries"], "quality": topsis["quality"],
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": args.steps * LAUNCHES["topsis"],
-                "clocks": clocks, "ahp": ahp_obj, "variants": variants, "paths": paths, "simulator": sim,
+                "clocks": clocks, "ahp": ahp_obj, "variants": variants, "paths": paths, "simulator": sim, "c5": c5,
                 "rank_once": None if once is None else {
                     "workload": once["name"].replace("batch", "batch, rank once per request (R25)"),
                     "value": once["value"], "unit": "pods/s", "ms_per_step": once["ms_per_step"],
@@ -380,6 +384,61 @@ def run_ours(args, rank, world, local):
                 "paper_context": "T5 (P:416-426): TOPSIS 3.48-3.84 s, AHP 6.90-9.45 s per 6000-request k=20 campaign "
                                  "on an unnamed CUDA 10.1 GPU (~10-14 M / 4-7 M servers ranked/s derived)"}
         print(json.dumps(line))
+
+
+C5_REQUESTS = {"topsis": 40, "ahp": 12}
+
+
+def measure_c5(args, rank, world, local, stream, max_over_ranks):
+    """C5: fat-tree k=64 (65536 servers), sequential scheduling (live state) of the same requests
+    on every rank, the servers sharded over the `world` ranks (nacs_create_sharded: replicated
+    filter and commit, each rank scores its block, ncclAllGather of (score, index) keys per pod
+    step; AHP sum-allreduces per-level weights and L2).  Strong scaling: the work is fixed, the
+    ranks split it.  At N=1: the unsharded context, plus 8 loopback shards on the one GPU that
+    must give identical placements.  Timed on the device (CUDA events), max over ranks."""
+    import hashlib
+    import torch
+    from paper_1909_07673_b200 import nacs
+    snap = gen.snapshot(64, gen.CONFIG_SEEDS["C5"])
+    res = {}
+    if world > 1:
+        import torch.distributed as dist
+        obj = [nacs.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        modes = [(f"nccl_x{world}", (rank, world, obj[0]))]
+    else:
+        modes = [("unsharded", None), ("loopback_x8", (0, 8, None))]
+    for method, nreq in C5_REQUESTS.items():
+        reqs = gen.requests(nreq, gen.CONFIG_SEEDS["C5"] + 1000)
+        warm = gen.subset(reqs, np.arange(2))
+        for name, shard in modes:
+            ctx = nacs.Context(local, stream, shard=shard)
+            ctx.load_topology(snap)
+            ctx.schedule_request(warm, method, "flat")
+            ctx.load_topology(snap)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            out = ctx.schedule_request(reqs, method, "flat")
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms = max_over_ranks(e0.elapsed_time(e1))
+            st = ctx.last_stats()
+            h = hashlib.sha256(b"".join(np.ascontiguousarray(out[k]).tobytes() for k in sorted(out))).hexdigest()
+            res[f"{method} {name}"] = {"pods_per_s": st["pod_steps"] / (ms / 1e3), "ms": ms,
+                                       "pod_steps": st["pod_steps"], "placements_sha256": h[:16]}
+            ctx.close()
+    same = {m: len({v["placements_sha256"] for k, v in res.items() if k.startswith(m)}) == 1 for m in C5_REQUESTS}
+    if world > 1:  # every rank must hold the same placements (replicated commit)
+        import torch.distributed as dist
+        mine = {k: v["placements_sha256"] for k, v in res.items()}
+        allh = [None] * world
+        dist.all_gather_object(allh, mine)
+        same = {m: all(a == allh[0] for a in allh) for m in C5_REQUESTS}
+    return {"workload": "C5: fat-tree k=64 (65536 servers), sequential Flat scheduling of "
+                        f"{C5_REQUESTS['topsis']} (TOPSIS) / {C5_REQUESTS['ahp']} (AHP) requests, servers sharded "
+                        f"over {world} rank(s)", "scaling": "strong", "modes": res,
+            "identical_placements_across_modes": same}
 
 
 PATH_QUERIES = 1 << 20   # queries per GPU per step (weak scaling)
