@@ -34,14 +34,34 @@ def stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False, out: str = LIB, extra=()) -> str:
+    """Compile the sources in parallel (one nvcc per file, no cross-file device code), then
+    link the shared library."""
     if force or stale():
-        cmd = [NVCC, *FLAGS, *extra, "-I", os.path.join(ROOT, "include"), *NCCL_FLAGS, "-o", out, *SOURCES]
-        p = subprocess.run(cmd, capture_output=True, text=True)
-        if p.returncode != 0:
-            sys.stderr.write(p.stdout + p.stderr)
+        import tempfile
+        from concurrent.futures import ThreadPoolExecutor
+        tmp = tempfile.mkdtemp(prefix="nacs_build_")
+        compile_flags = [f for f in FLAGS if f not in ("-shared", "-cudart", "static")]
+        inc = ["-I", os.path.join(ROOT, "include"), "-I", os.path.join(NCCL, "include")]
+
+        def compile_one(src):
+            obj = os.path.join(tmp, os.path.basename(src) + ".o")
+            return obj, subprocess.run([NVCC, *compile_flags, *extra, *inc, "-c", "-o", obj, src],
+                                       capture_output=True, text=True)
+
+        with ThreadPoolExecutor(len(SOURCES)) as ex:
+            results = list(ex.map(compile_one, SOURCES))
+        log = "".join(p.stdout + p.stderr for _, p in results)
+        if any(p.returncode != 0 for _, p in results):
+            sys.stderr.write(log)
             raise RuntimeError("nvcc failed building libnacs.so")
+        link = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static",
+                "-Xcompiler", "-fPIC", *NCCL_FLAGS, "-o", out, *[o for o, _ in results]]
+        p = subprocess.run(link, capture_output=True, text=True)
+        if p.returncode != 0:
+            sys.stderr.write(log + p.stdout + p.stderr)
+            raise RuntimeError("nvcc failed linking libnacs.so")
         if verbose:
-            sys.stderr.write(p.stderr)
+            sys.stderr.write(log)
     return out
 
 
