@@ -1689,7 +1689,7 @@ __device__ void release_request(Ctx& c, const ReqsDev& R, const OutDev& O, int r
 // attempt.  Per tick: departures (start + duration == t, in acceptance order), arrivals (in
 // `order`, ascending arrival then id), FIFO scan (head-of-line blocking if hol), counters.
 template <int METHOD>
-__global__ void __launch_bounds__(1024) k_simulate(Geo g, Opt o, int* state, ReqsDev R, OutDev O, int2* ulog,
+__global__ void __launch_bounds__(512) k_simulate(Geo g, Opt o, int* state, ReqsDev R, OutDev O, int2* ulog,
                                                    float* ahp_ws, double* w64, unsigned long long* stats, SimDev S,
                                                    int smem_state) {
   extern __shared__ __align__(16) unsigned char dyn[];
@@ -2578,7 +2578,7 @@ cudaError_t launch_simulate(const Geo& g, const Opt& o, int* d_state, const Reqs
                             cudaStream_t st) {
   int ss = 0;
   const size_t smem = seq_smem_bytes(g, &ss);
-  int B = single_block_size(g);
+  const int B = std::min(512, single_block_size(g));  // k_simulate: __launch_bounds__(512)
   switch (o.method) {
     case 0: set_smem<0>(k_simulate<0>, smem); k_simulate<0><<<1, B, smem, st>>>(g, o, d_state, R, O, ulog, ahp_ws, w64, stats, S, ss); break;
     case 1: set_smem<1>(k_simulate<1>, smem); k_simulate<1><<<1, B, smem, st>>>(g, o, d_state, R, O, ulog, ahp_ws, w64, stats, S, ss); break;
