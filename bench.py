@@ -353,6 +353,10 @@ def run_ours(args, rank, world, local):
                "d2h_bytes_per_step": 4 * (R + 3 * Cn + 2 * Vn)}
 
     cpu = None
+    if paths is not None and rank == 0 and world == 1 and not args.no_cpu:
+        paths["cpu_baseline"] = cpu_baseline_paths()
+    if sim is not None and world == 1 and not args.no_cpu:
+        sim["cpu_baseline"] = cpu_baseline_sim()
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline(topsis["snap"], topsis["reqs"], budget_s=15.0)
 
@@ -550,6 +554,38 @@ def measure_sim(ctx):
             "rows": rows,
             "note": "paper_T5 = the paper's numbers on its unnamed CUDA 10.1 GPU with its own unpublished "
                     "workload draw: context, not a like-for-like target"}
+
+
+def cpu_baseline_paths(budget_s=4.0):
+    """The oracle's modified Dijkstra (one O(V^2) label-setting search per query, OpenMP over
+    queries) on a sample of the paths workload."""
+    from oracle import oracle as O
+    cores = len(os.sched_getaffinity(0))
+    g, q = path_workload(0)
+    nq = 256
+    while True:
+        t = time.perf_counter()
+        O.graph_paths(g, q["src"][:nq], q["dst"][:nq], q["demand"][:nq], max_hops=8, nthreads=cores)
+        el = time.perf_counter() - t
+        if el > budget_s / 4 or nq >= 1 << 16:
+            break
+        nq *= 4
+    return {"value": nq / el, "unit": "paths/s", "cores": cores, "kind": "oracle",
+            "sample": f"first {nq} queries of the workload, C++ oracle Dijkstra per query, {el:.1f} s"}
+
+
+def cpu_baseline_sim(n_req=1000):
+    """The oracle's event loop (TOPSIS Flat) on the first n_req requests of the E2 campaign."""
+    from oracle import oracle as O
+    snap = gen.snapshot(20, warm=False)
+    reqs, arrival, duration = gen.sim_workload()
+    sub = gen.subset(reqs, np.arange(n_req))
+    t = time.perf_counter()
+    r = O.simulate(snap, sub, arrival[:n_req], duration[:n_req], "topsis", "flat", max_ticks=5000)
+    el = time.perf_counter() - t
+    return {"value": r["totals"]["attempts"] / el, "unit": "attempts/s", "cores": 1, "kind": "oracle",
+            "sample": f"E2, first {n_req} requests, TOPSIS Flat, sequential C++ oracle, {el:.1f} s "
+                      f"({r['totals']['pod_steps']} pod steps)"}
 
 
 def cpu_baseline(snap, reqs, budget_s=15.0, method="topsis"):
