@@ -1635,15 +1635,15 @@ cudaError_t launch_batch_warp(const Geo& g, const Opt& o, const int* d_state, in
     k_warp_layout<<<1, 1024, lsm, st>>>(g, d_state, lay);
   }
   k_order_lpt<<<1, 1024, 0, st>>>(R, order);
-  static const int group = [] {
-    const char* e = getenv("NACS_WARP_GROUP");
-    int v = e ? atoi(e) : 8;
-    return v < 1 ? 1 : (v > 16 ? 16 : v);
-  }();
-  static const int sync_mask = [] {
-    const char* e = getenv("NACS_WARP_SYNC");
-    return e ? atoi(e) : 3;
-  }();
+  // lockstep group size and the optional barriers before phases B / C (A/B on one box, C4,
+  // NACS_WARP_GROUP / NACS_WARP_SYNC override): per-pod, the whole CTA in lockstep with a
+  // barrier before the commit only, 12.74 ms (groups of 8 with both barriers 13.43 ms, 16 with
+  // none 13.20, 16 with both 13.05); rank-once keeps groups of 8 with both (6.60 vs 6.82 ms)
+  static const char* eg = getenv("NACS_WARP_GROUP");
+  static const char* es = getenv("NACS_WARP_SYNC");
+  int group = eg ? atoi(eg) : (o.rank_once ? 8 : 16);
+  group = group < 1 ? 1 : (group > 16 ? 16 : group);
+  const int sync_mask = es ? atoi(es) : (o.rank_once ? 3 : 2);
   size_t smem = warp_snapshot_bytes(g, u16) + sizeof(WScr) * WWARPS;
   auto go = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
