@@ -609,8 +609,9 @@ nacs_status schedule_sharded(nacs_ctx* ctx, const Opt& o, const nacs::ReqsDev& R
   const size_t b_ws = ahp ? al(nacs::ahp_workspace_bytes(g.n)) : 0, b_lv = ahp ? al(4 * 8 * n2) : 0,
                b_pp = ahp ? al(4 * 8 * (n2 + 2)) : 0, b_lvl = ahp ? al(4 * 4 * (size_t)g.n) : 0,
                b_f = ahp ? al(4 * 4 * n2) : 0, b_d = ahp ? al(4 * 8 * n2) : 0, b_K = ahp ? al(16) : 0;
-  CK(ctx->sh_buf.reserve(b_gs + 2 * b_bm + b_e + b_ctl + b_kx + b_kv + b_ki + b_ws + 2 * b_lv + 2 * b_pp + b_lvl +
-                         2 * b_f + 2 * b_d + b_K));
+  const size_t b_facc = al(11 * 8);
+  CK(ctx->sh_buf.reserve(b_gs + 2 * b_bm + b_e + b_ctl + b_kx + b_kv + b_ki + b_facc + b_ws + 2 * b_lv + 2 * b_pp +
+                         b_lvl + 2 * b_f + 2 * b_d + b_K));
   CK(ctx->sh_ctl.reserve(16));
   CK(ctx->ulog.reserve(nacs::ULOG_CAP));
   CK(ctx->misc.reserve(8));
@@ -624,6 +625,7 @@ nacs_status schedule_sharded(nacs_ctx* ctx, const Opt& o, const nacs::ReqsDev& R
   d.kx = reinterpret_cast<unsigned long long*>(p); p += b_kx;
   d.kxv = reinterpret_cast<double*>(p); p += b_kv;
   d.kxi = reinterpret_cast<int*>(p); p += b_ki;
+  d.facc = reinterpret_cast<unsigned long long*>(p); p += b_facc;
   d.ahp_ws = nullptr;
   d.lvmC = d.lvwC = nullptr;
   d.paC = d.pbC = nullptr;

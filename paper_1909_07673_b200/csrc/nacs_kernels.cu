@@ -424,8 +424,14 @@ __device__ void fabric_tables(Ctx& c) {
 
 // ------------------------------------------------------------- pass A -------
 // a3 + a4: feasibility mask and statistics over F.  Writes maskw, s->nf, mn, mx, sq.
-template <bool WRITE_MASK>
-__device__ void pass_filter(Ctx& c, uint8_t* mask_out, float* scores_out) {
+// GRID: the servers are spread over every CTA of the grid (the sharded engine's k_sh_filter);
+// each CTA reduces in its own shared memory and combines into facc[11] with integer atomics
+// (nf, nact, min/max of CPU, RAM, bandwidth, sums of squares — exact, order-independent);
+// k_sh_prep_b then moves facc into the scratch fields.
+template <bool WRITE_MASK, bool GRID = false>
+__device__ void pass_filter(Ctx& c, uint8_t* mask_out, float* scores_out, unsigned long long* facc = nullptr) {
+  __shared__ int g_red_i[GRID ? MAXW : 1][8];
+  __shared__ unsigned long long g_red_u[GRID ? MAXW : 1][3];
   Scratch* s = c.s;
   const Geo& g = c.g;
   const int n = g.n;
@@ -440,7 +446,9 @@ __device__ void pass_filter(Ctx& c, uint8_t* mask_out, float* scores_out) {
   int nf = 0, nact = 0;
   unsigned mn0 = UINT_MAX, mn1 = UINT_MAX, mn3 = UINT_MAX, mx0 = 0, mx1 = 0, mx3 = 0;
   unsigned long long q0 = 0, q1 = 0, q3 = 0;
-  for (int base = c.warp * 32; base < n; base += c.B) {
+  const int start = GRID ? (blockIdx.x * c.NW + c.warp) * 32 : c.warp * 32;
+  const int stride = GRID ? gridDim.x * c.B : c.B;
+  for (int base = start; base < n; base += stride) {
     int u = base + c.lane;
     bool in = u < n;
     int x0 = 0, x1 = 0, x2 = 0, x3 = 0;
@@ -483,21 +491,23 @@ __device__ void pass_filter(Ctx& c, uint8_t* mask_out, float* scores_out) {
     q1 += __shfl_xor_sync(FULL, q1, o);
     q3 += __shfl_xor_sync(FULL, q3, o);
   }
+  int (*red_i)[8] = GRID ? g_red_i : s->red_i;
+  unsigned long long (*red_u)[3] = GRID ? g_red_u : s->red_u;
   if (c.lane == 0) {
-    int* r = s->red_i[c.warp];
+    int* r = red_i[c.warp];
     r[0] = nf; r[1] = nact; r[2] = (int)mn0; r[3] = (int)mx0; r[4] = (int)mn1; r[5] = (int)mx1;
     r[6] = (int)mn3; r[7] = (int)mx3;
-    s->red_u[c.warp][0] = q0; s->red_u[c.warp][1] = q1; s->red_u[c.warp][2] = q3;
+    red_u[c.warp][0] = q0; red_u[c.warp][1] = q1; red_u[c.warp][2] = q3;
   }
   __syncthreads();
   if (c.warp == 0) {
     bool in = c.lane < c.NW;
-    const int* r = s->red_i[in ? c.lane : 0];
+    const int* r = red_i[in ? c.lane : 0];
     nf = in ? r[0] : 0; nact = in ? r[1] : 0;
     mn0 = in ? (unsigned)r[2] : UINT_MAX; mx0 = in ? (unsigned)r[3] : 0;
     mn1 = in ? (unsigned)r[4] : UINT_MAX; mx1 = in ? (unsigned)r[5] : 0;
     mn3 = in ? (unsigned)r[6] : UINT_MAX; mx3 = in ? (unsigned)r[7] : 0;
-    q0 = in ? s->red_u[c.lane][0] : 0; q1 = in ? s->red_u[c.lane][1] : 0; q3 = in ? s->red_u[c.lane][2] : 0;
+    q0 = in ? red_u[c.lane][0] : 0; q1 = in ? red_u[c.lane][1] : 0; q3 = in ? red_u[c.lane][2] : 0;
     nf = (int)__reduce_add_sync(FULL, (unsigned)nf);
     nact = (int)__reduce_add_sync(FULL, (unsigned)nact);
     mn0 = __reduce_min_sync(FULL, mn0); mx0 = __reduce_max_sync(FULL, mx0);
@@ -508,7 +518,18 @@ __device__ void pass_filter(Ctx& c, uint8_t* mask_out, float* scores_out) {
       q1 += __shfl_xor_sync(FULL, q1, o);
       q3 += __shfl_xor_sync(FULL, q3, o);
     }
-    if (c.lane == 0) {
+    if (GRID) {
+      if (c.lane == 0) {
+        atomicAdd(facc + 0, (unsigned long long)nf);
+        atomicAdd(facc + 1, (unsigned long long)nact);
+        atomicMin(facc + 2, (unsigned long long)mn0); atomicMax(facc + 3, (unsigned long long)mx0);
+        atomicMin(facc + 4, (unsigned long long)mn1); atomicMax(facc + 5, (unsigned long long)mx1);
+        atomicMin(facc + 6, (unsigned long long)mn3); atomicMax(facc + 7, (unsigned long long)mx3);
+        atomicAdd(facc + 8, q0);
+        atomicAdd(facc + 9, q1);
+        atomicAdd(facc + 10, q3);
+      }
+    } else if (c.lane == 0) {
       s->nf = nf;
       s->nact = nact;
       s->mn[0] = (int)mn0; s->mx[0] = (int)mx0;
@@ -1949,6 +1970,30 @@ __global__ void __launch_bounds__(1024) k_sh_begin(Geo g, Opt o, int* state, Req
 }
 
 // pod prologue (new pod) + filter and statistics over all servers (replicated)
+// The pod step's preparation in three launches: prep_a (1 CTA: flows, fabric tables,
+// flow-server feasibility), k_sh_filter (the whole grid: filter and statistics over the
+// 65536 servers of C5), prep_b (1 CTA: rejection, AHP levels and prefix sums).  The filter
+// used to run in the one CTA of prep_a and was the largest item of a C5 pod step.
+template <int METHOD>
+__global__ void __launch_bounds__(1024) k_sh_prep_a(Geo g, Opt o, int* state, ReqsDev R, OutDev O, int r,
+                                                    ShardDev d) {
+  const int phase = d.ctl[0];
+  if (phase != PH_NEWPOD && phase != PH_RETRY) return;
+  Ctx c;
+  sh_ctx(c, g, o, state, d);
+  if (phase == PH_NEWPOD) pod_prologue(c, R, r, d.ctl[1]);
+  if (c.tid < 11) d.facc[c.tid] = (c.tid >= 2 && c.tid <= 7 && !(c.tid & 1)) ? ~0ull : 0ull;
+}
+
+template <int METHOD>
+__global__ void __launch_bounds__(1024) k_sh_filter(Geo g, Opt o, int* state, ShardDev d) {
+  const int phase = d.ctl[0];
+  if (phase != PH_NEWPOD && phase != PH_RETRY) return;
+  Ctx c;
+  sh_ctx(c, g, o, state, d);
+  pass_filter<false, true>(c, nullptr, nullptr, d.facc);
+}
+
 template <int METHOD>
 __global__ void __launch_bounds__(1024) k_sh_prep(Geo g, Opt o, int* state, ReqsDev R, OutDev O, int r,
                                                   ShardDev d) {
@@ -1957,9 +2002,20 @@ __global__ void __launch_bounds__(1024) k_sh_prep(Geo g, Opt o, int* state, Reqs
   Ctx c;
   sh_ctx(c, g, o, state, d);
   Scratch* s = c.s;
-  if (phase == PH_NEWPOD) pod_prologue(c, R, r, d.ctl[1]);
-  pass_filter<false>(c, nullptr, nullptr);
-  if (c.tid == 0) s->c_steps += 1;
+  if (c.tid == 0) {  // the grid filter's statistics (k_sh_filter) into the scratch fields
+    const unsigned long long* f = d.facc;
+    const int nf = (int)f[0], nact = (int)f[1];
+    s->nf = nf;
+    s->nact = nact;
+    s->mn[0] = (int)f[2]; s->mx[0] = (int)f[3];
+    s->mn[1] = (int)f[4]; s->mx[1] = (int)f[5];
+    s->mn[2] = nact == nf ? 1 : 0; s->mx[2] = nact > 0 ? 1 : 0;  // f_u in {0,1}
+    s->mn[3] = (int)f[6]; s->mx[3] = (int)f[7];
+    s->sq[0] = f[8]; s->sq[1] = f[9]; s->sq[2] = (unsigned long long)nact; s->sq[3] = f[10];
+    s->c_feas += (unsigned long long)nf;
+    s->c_steps += 1;
+  }
+  __syncthreads();
   if (s->nf == 0) {
     req_reject(c, R, O, r);
     sh_flush(c, d.stats);
@@ -2330,6 +2386,14 @@ cudaError_t launch_sh_begin(const Geo& g, const Opt& o, int* state, const ReqsDe
 }
 cudaError_t launch_sh_prep(const Geo& g, const Opt& o, int* state, const ReqsDev& R, const OutDev& O, int r,
                            const ShardDev& d, cudaStream_t st) {
+  const int fgrid = (g.n + 1023) / 1024;
+  if (o.method == 1) {
+    k_sh_prep_a<1><<<1, 1024, 0, st>>>(g, o, state, R, O, r, d);
+    k_sh_filter<1><<<fgrid, 1024, 0, st>>>(g, o, state, d);
+  } else {
+    k_sh_prep_a<0><<<1, 1024, 0, st>>>(g, o, state, R, O, r, d);
+    k_sh_filter<0><<<fgrid, 1024, 0, st>>>(g, o, state, d);
+  }
   if (o.method == 1) k_sh_prep<1><<<1, 1024, 0, st>>>(g, o, state, R, O, r, d);
   else k_sh_prep<0><<<1, 1024, 0, st>>>(g, o, state, R, O, r, d);
   return cudaGetLastError();
