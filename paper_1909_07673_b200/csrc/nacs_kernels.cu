@@ -805,6 +805,9 @@ __device__ int presorted_collect(Ctx& c, int ci, bool feasible_only) {
   int s0, s1;
   warp_seg(c, n, s0, s1);
   int cnt = 0;
+  // unrolled: several independent gathers (perm -> value, feasibility, dirty) in flight
+  // per warp when the arrays are in global memory (the sharded engine, 65536 servers)
+#pragma unroll 4
   for (int base = s0; base < s1; base += 32) {
     const int i = base + c.lane;
     const int u = i < s1 ? perm[i] : 0;
@@ -814,6 +817,7 @@ __device__ int presorted_collect(Ctx& c, int ci, bool feasible_only) {
   int mtot;
   int pos = warp_exscan(c, cnt, &mtot);
   if (c.tid == 0) s->m1 = mtot;
+#pragma unroll 4
   for (int base = s0; base < s1; base += 32) {
     const int i = base + c.lane;
     const int u = i < s1 ? perm[i] : 0;
