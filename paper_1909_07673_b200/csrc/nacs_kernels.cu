@@ -2037,6 +2037,16 @@ __global__ void __launch_bounds__(1024) k_sh_prep(Geo g, Opt o, int* state, Reqs
       }
     }
     __syncthreads();
+    // the feasibility and dirty bitmaps into shared memory for the level extraction: the
+    // presorted walk looks both up at random servers (ncu: long_sb 67% on global gathers)
+    extern __shared__ unsigned sh_bits[];
+    for (int w = c.tid; w < c.nW; w += c.B) {
+      sh_bits[w] = c.maskw[w];
+      sh_bits[c.nW + w] = c.dirty[w];
+    }
+    __syncthreads();
+    c.maskw = sh_bits;
+    c.dirty = sh_bits + c.nW;
     const int n2 = next_pow2(g.n);
     for (int k = 0; k < 4; ++k) {
       if (s->ahp_const[k]) {
@@ -2398,8 +2408,9 @@ cudaError_t launch_sh_prep(const Geo& g, const Opt& o, int* state, const ReqsDev
     k_sh_prep_a<0><<<1, 1024, 0, st>>>(g, o, state, R, O, r, d);
     k_sh_filter<0><<<fgrid, 1024, 0, st>>>(g, o, state, d);
   }
+  const size_t bits = 2 * sizeof(unsigned) * (size_t)((g.n + 31) / 32);
   if (o.method == 1) k_sh_prep<1><<<1, 1024, 0, st>>>(g, o, state, R, O, r, d);
-  else k_sh_prep<0><<<1, 1024, 0, st>>>(g, o, state, R, O, r, d);
+  else k_sh_prep<0><<<1, 1024, bits, st>>>(g, o, state, R, O, r, d);
   return cudaGetLastError();
 }
 cudaError_t launch_sh_score(const Geo& g, const Opt& o, int* state, int lo, int hi, int slot, const ShardDev& d,
