@@ -15,6 +15,7 @@
 #include <vector>
 
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>  // header-only: ranges are free unless a profiler is attached
 
 #include "../../include/nacs.h"
 #include "nacs_internal.h"
@@ -119,6 +120,12 @@ struct nacs_ctx {
 };
 
 namespace {
+
+// NVTX range over one API call (tracing): nsys / ncu --nvtx see every call
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 nacs_status fail(nacs_ctx* c, nacs_status s, const std::string& msg) {
   if (c) c->err = msg;
@@ -810,6 +817,7 @@ void nacs_destroy(nacs_ctx* ctx) {
 }
 
 nacs_status nacs_load_topology(nacs_ctx* ctx, const nacs_topology* t) {
+  NvtxRange nvtx_range_("nacs_load_topology");
   if (!ctx) return NACS_EINVAL;
   ctx->err.clear();
   if (!t) return fail(ctx, NACS_EINVAL, "topology: NULL");
@@ -890,16 +898,19 @@ nacs_status nacs_read_topology(nacs_ctx* ctx, int32_t* cpu_res, int32_t* ram_res
 
 nacs_status nacs_rank_ahp(nacs_ctx* ctx, const nacs_options* opt, const nacs_pod_query* q, uint8_t* mask,
                           float* scores, int32_t* best) {
+  NvtxRange nvtx_range_("nacs_rank_ahp");
   return rank_impl(ctx, opt, q, mask, scores, best, 0);
 }
 
 nacs_status nacs_rank_topsis(nacs_ctx* ctx, const nacs_options* opt, const nacs_pod_query* q, uint8_t* mask,
                              float* scores, int32_t* best) {
+  NvtxRange nvtx_range_("nacs_rank_topsis");
   return rank_impl(ctx, opt, q, mask, scores, best, 1);
 }
 
 nacs_status nacs_schedule_batch(nacs_ctx* ctx, const nacs_options* opt, const nacs_requests* batch,
                                 nacs_placements* out) {
+  NvtxRange nvtx_range_("nacs_schedule_batch");
   nacs_status st = begin_call(ctx);
   if (st) return st;
   Opt o;
@@ -988,6 +999,7 @@ nacs_status nacs_schedule_batch(nacs_ctx* ctx, const nacs_options* opt, const na
 
 nacs_status nacs_schedule_request(nacs_ctx* ctx, const nacs_options* opt, const nacs_requests* reqs,
                                   nacs_placements* out) {
+  NvtxRange nvtx_range_("nacs_schedule_request");
   nacs_status st = begin_call(ctx);
   if (st) return st;
   Opt o;
@@ -1059,6 +1071,7 @@ nacs_status nacs_schedule_request(nacs_ctx* ctx, const nacs_options* opt, const 
 // Departures and the discrete-event simulator.
 // ---------------------------------------------------------------------------------------
 nacs_status nacs_release(nacs_ctx* ctx, uint32_t flags, const nacs_requests* reqs, const nacs_placements* pl) {
+  NvtxRange nvtx_range_("nacs_release");
   nacs_status st = begin_call(ctx);
   if (st) return st;
   if (flags & ~(NACS_DEVICE_PTRS | NACS_ASYNC)) return fail(ctx, NACS_EINVAL, "flags: only NACS_DEVICE_PTRS | NACS_ASYNC");
@@ -1109,6 +1122,7 @@ nacs_status nacs_release(nacs_ctx* ctx, uint32_t flags, const nacs_requests* req
 nacs_status nacs_simulate(nacs_ctx* ctx, const nacs_options* opt, const nacs_requests* reqs, const int32_t* arrival,
                           const int32_t* duration, const nacs_sim_config* cfg, nacs_placements* out,
                           nacs_sim_report* rep) {
+  NvtxRange nvtx_range_("nacs_simulate");
   nacs_status st = begin_call(ctx);
   if (st) return st;
   Opt o;
@@ -1222,6 +1236,7 @@ static nacs::GraphDev graph_dev(nacs_ctx* ctx) {
 }
 
 nacs_status nacs_load_graph(nacs_ctx* ctx, const nacs_graph* gr) {
+  NvtxRange nvtx_range_("nacs_load_graph");
   if (!ctx) return NACS_EINVAL;
   ctx->err.clear();
   if (!gr) return fail(ctx, NACS_EINVAL, "graph: NULL");
@@ -1301,6 +1316,7 @@ static nacs_status begin_graph_call(nacs_ctx* ctx, uint32_t flags) {
 
 nacs_status nacs_widest_paths(nacs_ctx* ctx, const nacs_path_query* q, uint32_t flags, int32_t* bottleneck,
                               int32_t* hops, int32_t* path, int32_t max_hops) {
+  NvtxRange nvtx_range_("nacs_widest_paths");
   nacs_status st = begin_graph_call(ctx, flags);
   if (st) return st;
   if (!q || !bottleneck || !hops) return fail(ctx, NACS_EINVAL, "query/bottleneck/hops: NULL");
@@ -1377,6 +1393,7 @@ nacs_status nacs_widest_paths(nacs_ctx* ctx, const nacs_path_query* q, uint32_t 
 }
 
 nacs_status nacs_logical_bandwidth(nacs_ctx* ctx, uint32_t flags, int64_t* out) {
+  NvtxRange nvtx_range_("nacs_logical_bandwidth");
   nacs_status st = begin_graph_call(ctx, flags);
   if (st) return st;
   if (!out) return fail(ctx, NACS_EINVAL, "out: NULL");
