@@ -120,6 +120,7 @@ struct ShardDev {
   double *wq64, *l2q64;        // [4][n2] FP64 re-decision
   int* Kc;                     // [4] levels per criterion (0 = constant criterion)
   unsigned long long* facc;    // [11] the grid filter's statistics (k_sh_filter)
+  int* lvscr;                  // AHP: per-criterion level-extraction scratch, 4 x [5 (n2 + 1)] ints
 };
 
 // Launchers (nacs_kernels.cu).  Each returns the cudaError_t of the launch.

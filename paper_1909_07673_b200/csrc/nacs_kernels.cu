@@ -2037,32 +2037,78 @@ __global__ void __launch_bounds__(1024) k_sh_prep(Geo g, Opt o, int* state, Reqs
       }
     }
     __syncthreads();
-    // the feasibility and dirty bitmaps into shared memory for the level extraction: the
-    // presorted walk looks both up at random servers (ncu: long_sb 67% on global gathers)
-    extern __shared__ unsigned sh_bits[];
-    for (int w = c.tid; w < c.nW; w += c.B) {
-      sh_bits[w] = c.maskw[w];
-      sh_bits[c.nW + w] = c.dirty[w];
-    }
-    __syncthreads();
-    c.maskw = sh_bits;
-    c.dirty = sh_bits + c.nW;
-    const int n2 = next_pow2(g.n);
-    for (int k = 0; k < 4; ++k) {
-      if (s->ahp_const[k]) {
-        if (c.tid == 0) d.Kc[k] = 0;
+  }
+}
+
+// The AHP levels and pass-1 prefix sums of each non-constant criterion, one CTA per criterion
+// (the three numeric criteria are independent; they ran one after another in k_sh_prep's one
+// CTA).  Each CTA works on a shared-memory copy of the scratch block (its merge lists), its
+// own slice of the sorting buffers (d.lvscr) and shared-memory copies of the feasibility and
+// dirty bitmaps (the presorted walk looks both up at random servers).
+__global__ void __launch_bounds__(1024) k_sh_levels(Geo g, Opt o, int* state, ShardDev d) {
+  const int phase = d.ctl[0];
+  if (phase != PH_NEWPOD && phase != PH_RETRY) return;
+  const int k = blockIdx.x;
+  const Scratch* gs = d.gs;
+  if (gs->nf == 0) return;  // rejected in k_sh_prep
+  const int n2 = next_pow2(g.n);
+  if (gs->touch_over) {
+    // the request touched more servers than the merge list holds: the presorted orders are
+    // rebuilt (ahp_levels_of), which writes the shared orders and scratch — one CTA, in turn
+    if (k != 0) return;
+    Ctx c;
+    sh_ctx(c, g, o, state, d);
+    for (int kk = 0; kk < 4; ++kk) {
+      if (c.s->ahp_const[kk]) {
+        if (c.tid == 0) d.Kc[kk] = 0;
         continue;
       }
-      ahp_slice(c, d, k);
-      const int K = ahp_levels_of(c, k);
+      ahp_slice(c, d, kk);
+      const int K = ahp_levels_of(c, kk);
       ahp_prefix(c, K, c.lvm);
-      for (int l = c.tid; l < K; l += c.B) { d.wq[k * n2 + l] = 0.f; d.l2q[k * n2 + l] = 0.f; }
+      for (int l = c.tid; l < K; l += c.B) { d.wq[kk * n2 + l] = 0.f; d.l2q[kk * n2 + l] = 0.f; }
       if (c.tid == 0) {
-        d.Kc[k] = K;
-        s->c_pairs += (unsigned long long)K * (unsigned long long)(K - 1) / 2;
+        d.Kc[kk] = K;
+        c.s->c_pairs += (unsigned long long)K * (unsigned long long)(K - 1) / 2;
       }
       __syncthreads();
     }
+    return;
+  }
+  if (gs->ahp_const[k]) {
+    if (threadIdx.x == 0) d.Kc[k] = 0;
+    return;
+  }
+  __shared__ Scratch ls;
+  extern __shared__ unsigned sh_bits[];
+  {  // the scratch block into shared memory (read-only here except the merge lists)
+    const int* src = reinterpret_cast<const int*>(gs);
+    int* dst = reinterpret_cast<int*>(&ls);
+    for (int i = threadIdx.x; i < (int)(sizeof(Scratch) / 4); i += blockDim.x) dst[i] = src[i];
+  }
+  Ctx c;
+  sh_ctx(c, g, o, state, d);
+  c.s = &ls;
+  for (int w = c.tid; w < c.nW; w += c.B) {
+    sh_bits[w] = c.maskw[w];
+    sh_bits[c.nW + w] = c.dirty[w];
+  }
+  __syncthreads();
+  c.maskw = sh_bits;
+  c.dirty = sh_bits + c.nW;
+  int* sc = d.lvscr + (size_t)k * 5 * (n2 + 1);
+  c.keys = reinterpret_cast<float*>(sc);
+  c.sidx = sc + (n2 + 1);
+  c.keys2 = reinterpret_cast<float*>(sc + 2 * (n2 + 1));
+  c.sidx2 = sc + 3 * (n2 + 1);
+  c.lst = sc + 4 * (n2 + 1);
+  ahp_slice(c, d, k);
+  const int K = ahp_levels_of(c, k);
+  ahp_prefix(c, K, c.lvm);
+  for (int l = c.tid; l < K; l += c.B) { d.wq[k * n2 + l] = 0.f; d.l2q[k * n2 + l] = 0.f; }
+  if (c.tid == 0) {
+    d.Kc[k] = K;
+    atomicAdd(&d.gs->c_pairs, (unsigned long long)K * (unsigned long long)(K - 1) / 2);
   }
 }
 
@@ -2409,8 +2455,12 @@ cudaError_t launch_sh_prep(const Geo& g, const Opt& o, int* state, const ReqsDev
     k_sh_filter<0><<<fgrid, 1024, 0, st>>>(g, o, state, d);
   }
   const size_t bits = 2 * sizeof(unsigned) * (size_t)((g.n + 31) / 32);
-  if (o.method == 1) k_sh_prep<1><<<1, 1024, 0, st>>>(g, o, state, R, O, r, d);
-  else k_sh_prep<0><<<1, 1024, bits, st>>>(g, o, state, R, O, r, d);
+  if (o.method == 1) {
+    k_sh_prep<1><<<1, 1024, 0, st>>>(g, o, state, R, O, r, d);
+  } else {
+    k_sh_prep<0><<<1, 1024, 0, st>>>(g, o, state, R, O, r, d);
+    k_sh_levels<<<4, 1024, bits, st>>>(g, o, state, d);  // one CTA per criterion
+  }
   return cudaGetLastError();
 }
 cudaError_t launch_sh_score(const Geo& g, const Opt& o, int* state, int lo, int hi, int slot, const ShardDev& d,
