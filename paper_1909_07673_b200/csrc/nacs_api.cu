@@ -616,7 +616,7 @@ nacs_status schedule_sharded(nacs_ctx* ctx, const Opt& o, const nacs::ReqsDev& R
   const size_t b_ws = ahp ? al(nacs::ahp_workspace_bytes(g.n)) : 0, b_lv = ahp ? al(4 * 8 * n2) : 0,
                b_pp = ahp ? al(4 * 8 * (n2 + 2)) : 0, b_lvl = ahp ? al(4 * 4 * (size_t)g.n) : 0,
                b_f = ahp ? al(4 * 4 * n2) : 0, b_d = ahp ? al(4 * 8 * n2) : 0, b_K = ahp ? al(16) : 0;
-  const size_t b_facc = al(11 * 8), b_lsc = ahp ? al(4 * 5 * 4 * (n2 + 1)) : 0;
+  const size_t b_facc = al(16 * 8), b_lsc = ahp ? al(4 * 5 * 4 * (n2 + 1)) : 0;
   CK(ctx->sh_buf.reserve(b_gs + 2 * b_bm + b_e + b_ctl + b_kx + b_kv + b_ki + b_facc + b_ws + 2 * b_lv + 2 * b_pp +
                          b_lvl + 2 * b_f + 2 * b_d + b_K + b_lsc));
   CK(ctx->sh_ctl.reserve(16));

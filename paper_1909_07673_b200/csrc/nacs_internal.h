@@ -119,7 +119,7 @@ struct ShardDev {
   float *wq, *l2q;             // [4][n2] pass-1 weights, L2 per level (allreduced)
   double *wq64, *l2q64;        // [4][n2] FP64 re-decision
   int* Kc;                     // [4] levels per criterion (0 = constant criterion)
-  unsigned long long* facc;    // [11] the grid filter's statistics (k_sh_filter)
+  unsigned long long* facc;    // [16]: [0..10] the grid filter's statistics (k_sh_filter), [15] presort flag
   int* lvscr;                  // AHP: per-criterion level-extraction scratch, 4 x [5 (n2 + 1)] ints
 };
 

@@ -1952,9 +1952,14 @@ __global__ void __launch_bounds__(1024) k_sh_begin(Geo g, Opt o, int* state, Req
   Ctx c;
   sh_ctx(c, g, o, state, d);
   Scratch* s = c.s;
+  if (first == 2 && d.facc[15]) {  // AHP: k_sh_presort has just rebuilt the presorted orders
+    for (int w = c.tid; w < c.nW; w += c.B) c.dirty[w] = 0u;
+    if (c.tid == 0) { s->ntouched = 0; s->touch_over = 0; s->presorted = 1; }
+    __syncthreads();
+  }
   if (c.tid == 0) {
     s->c_steps = s->c_retries = s->c_fp64 = s->c_invalid = s->c_feas = s->c_pairs = 0;
-    if (first) { s->presorted = 0; s->touch_over = 0; s->ntouched = 0; }
+    if (first == 1) { s->presorted = 0; s->touch_over = 0; s->ntouched = 0; }
     if (METHOD == 0) {
       double L1[4];
       ahp_l1_dev(o, L1);
@@ -1971,6 +1976,32 @@ __global__ void __launch_bounds__(1024) k_sh_begin(Geo g, Opt o, int* state, Req
     return;
   }
   if (c.tid == 0) { d.ctl[0] = PH_NEWPOD; d.ctl[1] = 0; }
+}
+
+// AHP on the sharded engine: the presorted orders of the three criteria rebuilt in parallel,
+// one CTA per criterion (they were sorted one after another by k_sh_begin's one CTA, ~12 ms
+// at C5), when the request is the call's first or the previous request overflowed the merge
+// list.  The decision is published in facc[15] for k_sh_begin, which resets the flags.
+__global__ void __launch_bounds__(1024) k_sh_presort(Geo g, Opt o, int* state, ShardDev d, int first) {
+  const Scratch* gs = d.gs;
+  const bool need = first || gs->touch_over || !gs->presorted;
+  if (blockIdx.x == 0 && threadIdx.x == 0) d.facc[15] = need ? 1ull : 0ull;
+  if (!need) return;
+  const int ci = blockIdx.x;
+  Ctx c;
+  sh_ctx(c, g, o, state, d);
+  const int n = g.n, P2 = next_pow2(n);
+  int* sc = d.lvscr + (size_t)ci * 5 * (P2 + 1);
+  c.keys = reinterpret_cast<float*>(sc);
+  c.sidx = sc + (P2 + 1);
+  const int* x = c.cr + crit_of(ci) * n;
+  for (int i = c.tid; i < P2; i += c.B) {
+    c.keys[i] = i < n ? (float)x[i] : FLT_MAX;
+    c.sidx[i] = i;
+  }
+  __syncthreads();
+  bitonic(c, P2);
+  for (int i = c.tid; i < n; i += c.B) c.perm[ci * P2 + i] = (unsigned short)c.sidx[i];
 }
 
 // pod prologue (new pod) + filter and statistics over all servers (replicated)
@@ -2440,8 +2471,12 @@ size_t scratch_bytes() { return sizeof(Scratch); }
 
 cudaError_t launch_sh_begin(const Geo& g, const Opt& o, int* state, const ReqsDev& R, const OutDev& O, int r,
                             const ShardDev& d, cudaStream_t st) {
-  if (o.method == 1) k_sh_begin<1><<<1, 1024, 0, st>>>(g, o, state, R, O, r, d, r == 0);
-  else k_sh_begin<0><<<1, 1024, 0, st>>>(g, o, state, R, O, r, d, r == 0);
+  if (o.method == 1) {
+    k_sh_begin<1><<<1, 1024, 0, st>>>(g, o, state, R, O, r, d, r == 0);
+  } else {
+    k_sh_presort<<<3, 1024, 0, st>>>(g, o, state, d, r == 0);
+    k_sh_begin<0><<<1, 1024, 0, st>>>(g, o, state, R, O, r, d, 2);
+  }
   return cudaGetLastError();
 }
 cudaError_t launch_sh_prep(const Geo& g, const Opt& o, int* state, const ReqsDev& R, const OutDev& O, int r,
