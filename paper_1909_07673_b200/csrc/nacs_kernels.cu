@@ -2353,14 +2353,19 @@ __global__ void __launch_bounds__(256) k_ahp_pass(Geo g, Opt o, int q0, int q1, 
 
 // between the passes (1 CTA): (value, weight) levels and their prefix sums
 template <bool FP64>
+// one CTA per criterion (independent): the block scans of ahp_prefix run on a private
+// shared-memory scratch block
 __global__ void __launch_bounds__(1024) k_ahp_mid(Geo g, Opt o, int* state, ShardDev d) {
   if (!sh_live(d, FP64)) return;
+  __shared__ Scratch ls;
   Ctx c;
   sh_ctx(c, g, o, state, d);
+  c.s = &ls;
   const int n2 = next_pow2(g.n);
-  for (int k = 0; k < 4; ++k) {
+  {
+    const int k = blockIdx.x;
     const int K = d.Kc[k];
-    if (K == 0) continue;
+    if (K == 0) return;
     ahp_slice(c, d, k);
     for (int l = c.tid; l < K; l += c.B)
       c.lvw[l] = make_float2(c.lvm[l].x, FP64 ? 0.f : d.wq[k * n2 + l]);
@@ -2456,8 +2461,8 @@ cudaError_t launch_ahp_pass(int pass, bool fp64, const Geo& g, const Opt& o, int
   return cudaGetLastError();
 }
 cudaError_t launch_ahp_mid(bool fp64, const Geo& g, const Opt& o, int* state, const ShardDev& d, cudaStream_t st) {
-  if (fp64) k_ahp_mid<true><<<1, 1024, 0, st>>>(g, o, state, d);
-  else k_ahp_mid<false><<<1, 1024, 0, st>>>(g, o, state, d);
+  if (fp64) k_ahp_mid<true><<<4, 1024, 0, st>>>(g, o, state, d);
+  else k_ahp_mid<false><<<4, 1024, 0, st>>>(g, o, state, d);
   return cudaGetLastError();
 }
 cudaError_t launch_ahp_decide(bool fp64, const Geo& g, const Opt& o, int* state, const ReqsDev& R, const OutDev& O,
