@@ -121,6 +121,8 @@ struct ShardDev {
   int* Kc;                     // [4] levels per criterion (0 = constant criterion)
   unsigned long long* facc;    // [16]: [0..10] the grid filter's statistics (k_sh_filter), [15] presort flag
   int* lvscr;                  // AHP: per-criterion level-extraction scratch, 4 x [5 (n2 + 1)] ints
+  unsigned long long* kpart;   // AHP: per-CTA top-2 keys of k_ahp_pg, [2 * npart]
+  int npart;                   // CTAs of k_ahp_pg
 };
 
 // Launchers (nacs_kernels.cu).  Each returns the cudaError_t of the launch.

@@ -2389,6 +2389,38 @@ __global__ void __launch_bounds__(1024) k_ahp_mid(Geo g, Opt o, int* state, Shar
   }
 }
 
+// PG over F on the whole grid (FP32; one server per thread): each CTA leaves its top-2
+// (score, index) keys in d.kpart for k_ahp_decide.  The top-2 of the union of per-CTA top-2
+// sets is the global top-2, so the decision is the one-CTA kernel's.
+__global__ void __launch_bounds__(1024) k_ahp_pg(Geo g, Opt o, int* state, ShardDev d) {
+  if (!sh_live(d, false)) return;
+  __shared__ Scratch ls;
+  Ctx c;
+  sh_ctx(c, g, o, state, d);
+  const Scratch* gs = d.gs;
+  c.s = &ls;
+  const int n = g.n, n2 = next_pow2(n);
+  const float inv_nf = rcp_approx((float)gs->nf);
+  float L1[4];
+  bool cst[4];
+  for (int k = 0; k < 4; ++k) { L1[k] = gs->L1[k]; cst[k] = gs->ahp_const[k]; }
+  unsigned long long k1 = 0, k2 = 0;
+  for (int u = blockIdx.x * c.B + c.tid; u < n; u += gridDim.x * c.B) {
+    if (!feas_bit(c, u)) continue;
+    float pgv = 0.f;
+    for (int k = 0; k < 4; ++k) {
+      if (cst[k]) pgv += L1[k] * inv_nf;
+      else pgv = fmaf(L1[k], d.l2q[k * n2 + d.lvlC[(size_t)k * n + u]], pgv);
+    }
+    top2_insert(k1, k2, score_key(pgv, u));
+  }
+  block_top2(c, k1, k2);
+  if (c.tid == 0) {
+    d.kpart[2 * blockIdx.x] = ls.key1;
+    d.kpart[2 * blockIdx.x + 1] = ls.key2;
+  }
+}
+
 // decide (1 CTA): PG over F, argmax (top-2 and near-tie test in FP32), commit
 template <bool FP64>
 __global__ void __launch_bounds__(1024) k_ahp_decide(Geo g, Opt o, int* state, ReqsDev R, OutDev O, int r,
@@ -2399,17 +2431,9 @@ __global__ void __launch_bounds__(1024) k_ahp_decide(Geo g, Opt o, int* state, R
   Scratch* s = c.s;
   const int n = g.n, n2 = next_pow2(n), nf = s->nf;
   if (!FP64) {
-    const float inv_nf = rcp_approx((float)nf);
+    // the per-CTA top-2 keys of k_ahp_pg (PG over F on the whole grid), reduced here
     unsigned long long k1 = 0, k2 = 0;
-    for (int u = c.tid; u < n; u += c.B) {
-      if (!feas_bit(c, u)) continue;
-      float pgv = 0.f;
-      for (int k = 0; k < 4; ++k) {
-        if (s->ahp_const[k]) pgv += s->L1[k] * inv_nf;
-        else pgv = fmaf(s->L1[k], d.l2q[k * n2 + d.lvlC[(size_t)k * n + u]], pgv);
-      }
-      top2_insert(k1, k2, score_key(pgv, u));
-    }
+    for (int i = c.tid; i < 2 * d.npart; i += c.B) top2_insert(k1, k2, d.kpart[i]);
     block_top2(c, k1, k2);
     const float drel = ahp_delta_rel(nf);
     if (c.tid == 0) {
@@ -2467,6 +2491,7 @@ cudaError_t launch_ahp_mid(bool fp64, const Geo& g, const Opt& o, int* state, co
 }
 cudaError_t launch_ahp_decide(bool fp64, const Geo& g, const Opt& o, int* state, const ReqsDev& R, const OutDev& O,
                               int r, const ShardDev& d, cudaStream_t st) {
+  if (!fp64) k_ahp_pg<<<d.npart, 1024, 0, st>>>(g, o, state, d);
   if (fp64) k_ahp_decide<true><<<1, 1024, 0, st>>>(g, o, state, R, O, r, d);
   else k_ahp_decide<false><<<1, 1024, 0, st>>>(g, o, state, R, O, r, d);
   return cudaGetLastError();
