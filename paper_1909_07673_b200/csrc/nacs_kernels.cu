@@ -2351,6 +2351,137 @@ __global__ void __launch_bounds__(256) k_ahp_pass(Geo g, Opt o, int q0, int q1, 
   }
 }
 
+// FP32 passes, register-tiled: a warp takes P consecutive levels and walks the union of
+// their term ranges once, each loaded (value, weight) feeding all P levels (the pair-per-warp
+// loop above re-read the level array from L2 once per level: L2-bandwidth bound at C5).
+// Terms sit at absolute positions k = base + lane (base a multiple of 32) in groups of 4
+// sharing one reciprocal; terms outside a level's range enter as weight 0 over 1.  Each lane
+// sums <= 32 terms per level in FP32 before the FP64 accumulation, so the error bound behind
+// ahp_delta_rel (chunks of <= 32 terms, any order) holds unchanged.
+// ABOVE = pass 2 (terms q in (l, K), d = v_q - v_l); else pass 1 (q in [0, l), d = v_l - v_q).
+template <bool ABOVE, int RULE, int P>
+__device__ __forceinline__ void rsum_tile(const float2* arr, int K, int l0, int np, float sc, int lane,
+                                          double (&out)[P]) {
+  float v[P];
+#pragma unroll
+  for (int p = 0; p < P; ++p) { v[p] = arr[l0 + (p < np ? p : 0)].x; out[p] = 0.0; }
+  const int lmax = l0 + np - 1;
+  int kb = ABOVE ? ((l0 + 1) & ~31) : 0;
+  const int kend = ABOVE ? K : lmax;
+  while (kb < kend) {
+    float a[P];
+#pragma unroll
+    for (int p = 0; p < P; ++p) a[p] = 0.f;
+    for (int j = 0; j < 8 && kb < kend; ++j, kb += 128) {
+      const int k = kb + lane;
+      const bool full = ABOVE ? (kb > lmax && kb + 128 <= K) : (kb + 128 <= l0);
+      if (full) {
+        const float2 o0 = arr[k], o1 = arr[k + 32], o2 = arr[k + 64], o3 = arr[k + 96];
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+          float d0 = ABOVE ? o0.x - v[p] : v[p] - o0.x, d1 = ABOVE ? o1.x - v[p] : v[p] - o1.x;
+          float d2 = ABOVE ? o2.x - v[p] : v[p] - o2.x, d3 = ABOVE ? o3.x - v[p] : v[p] - o3.x;
+          if (RULE) {
+            d0 = fmaf(sc, d0, 1.0f);
+            d1 = fmaf(sc, d1, 1.0f);
+            d2 = fmaf(sc, d2, 1.0f);
+            d3 = fmaf(sc, d3, 1.0f);
+          }
+          const float p01 = d0 * d1, p23 = d2 * d3;
+          const float n01 = fmaf(o0.y, d1, o1.y * d0), n23 = fmaf(o2.y, d3, o3.y * d2);
+          a[p] = fmaf(fmaf(n01, p23, n23 * p01), rcp_approx(p01 * p23), a[p]);
+        }
+      } else {
+        float2 o[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) o[i] = k + 32 * i < K ? arr[k + 32 * i] : make_float2(0.f, 0.f);
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+          float d[4], w[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int q = k + 32 * i;
+            const bool in = ABOVE ? (q > l0 + p && q < K) : (q < l0 + p);
+            float di = ABOVE ? o[i].x - v[p] : v[p] - o[i].x;
+            if (RULE) di = fmaf(sc, di, 1.0f);
+            d[i] = in ? di : 1.0f;
+            w[i] = in ? o[i].y : 0.f;
+          }
+          const float p01 = d[0] * d[1], p23 = d[2] * d[3];
+          const float n01 = fmaf(w[0], d[1], w[1] * d[0]), n23 = fmaf(w[2], d[3], w[3] * d[2]);
+          a[p] = fmaf(fmaf(n01, p23, n23 * p01), rcp_approx(p01 * p23), a[p]);
+        }
+      }
+    }
+#pragma unroll
+    for (int p = 0; p < P; ++p) out[p] += (double)a[p];
+  }
+#pragma unroll
+  for (int p = 0; p < P; ++p)
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) out[p] += __shfl_xor_sync(FULL, out[p], off);
+}
+
+constexpr int kAhpTile = 4;
+
+// The rank's pairs (t, K-1-t), t in [a, b), cut into tiles of kAhpTile consecutive t: a warp
+// takes the low levels t.. and the mirrored high levels K-1-t.. of one tile (K-1 terms per
+// pair, as before), skipping the middle level of an odd K on the high side.
+template <int PASS, int RULE>
+__global__ void __launch_bounds__(256, 3) k_ahp_pass_tiled(Geo g, int q0, int q1, int world, ShardDev d) {
+  constexpr int P = kAhpTile;
+  if (!sh_live(d, false)) return;
+  const Scratch* s = d.gs;
+  const int n2 = next_pow2(g.n);
+  const int m = s->nf;
+  const int lane = threadIdx.x & 31;
+  int a[4], b[4], total = 0;
+  for (int k = 0; k < 4; ++k) {
+    const int K = d.Kc[k], half = (K + 1) >> 1;
+    a[k] = (int)((long long)half * q0 / world);
+    b[k] = (int)((long long)half * q1 / world);
+    total += (b[k] - a[k] + P - 1) / P;
+  }
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < total; i += nwarps) {
+    int k = 0, t = i;
+    while (t >= (b[k] - a[k] + P - 1) / P) { t -= (b[k] - a[k] + P - 1) / P; ++k; }
+    const int K = d.Kc[k];
+    const int t0 = a[k] + t * P, nt = min(P, b[k] - t0);
+    const double sd = s->ahp_scaled[k];
+    const float sc = (float)sd;
+    const float2* lvm = d.lvmC + (size_t)k * n2;
+    const float2* lvw = d.lvwC + (size_t)k * n2;
+    const double* pa = d.paC + (size_t)k * (n2 + 2);
+    const double* pb = d.pbC + (size_t)k * (n2 + 2);
+    for (int side = 0; side < 2; ++side) {
+      int l0 = side ? K - (t0 + nt) : t0, np = nt;
+      if (side && l0 == t0 + nt - 1) { ++l0; --np; }  // the middle level, already on the low side
+      if (np <= 0) continue;
+      double rec[P];
+      if (PASS == 1) rsum_tile<false, RULE, P>(lvm, K, l0, np, sc, lane, rec);
+      else rsum_tile<true, RULE, P>(lvw, K, l0, np, sc, lane, rec);
+#pragma unroll
+      for (int p = 0; p < P; ++p) {
+        if (lane != p || p >= np) continue;
+        const int l = l0 + p;
+        if (PASS == 1) {
+          const double vl = lvm[l].x, ml = lvm[l].y;
+          const double cgt = pa[K] - pa[l + 1];
+          const double G = (pb[K] - pb[l + 1]) - cgt * vl;  // sum_{k>l} m_k (v_k - v_l), exact
+          const double col = RULE ? cgt + sd * G + ml + rec[p] : sd * G + ml + rec[p] / sd;
+          d.wq[k * n2 + l] = (float)(ml / col);
+        } else {
+          const double vl = lvw[l].x, wl = (double)lvw[l].y;
+          const double lin = vl * pa[l] - pb[l];  // sum_{k<l} w_k (v_l - v_k)
+          const double L = RULE ? pa[l] + sd * lin + wl + rec[p] : sd * lin + wl + rec[p] / sd;
+          d.l2q[k * n2 + l] = (float)(L / (double)m);
+        }
+      }
+    }
+  }
+}
+
 // between the passes (1 CTA): (value, weight) levels and their prefix sums
 template <bool FP64>
 // one CTA per criterion (independent): the block scans of ahp_prefix run on a private
@@ -2478,10 +2609,16 @@ cudaError_t launch_ahp_pass(int pass, bool fp64, const Geo& g, const Opt& o, int
   int blocks = 0;
   cudaDeviceGetAttribute(&blocks, cudaDevAttrMultiProcessorCount, 0);
   blocks *= 8;
-  if (pass == 1 && !fp64) k_ahp_pass<1, false><<<blocks, 256, 0, st>>>(g, o, q0, q1, world, d);
-  else if (pass == 1) k_ahp_pass<1, true><<<blocks, 256, 0, st>>>(g, o, q0, q1, world, d);
-  else if (!fp64) k_ahp_pass<2, false><<<blocks, 256, 0, st>>>(g, o, q0, q1, world, d);
-  else k_ahp_pass<2, true><<<blocks, 256, 0, st>>>(g, o, q0, q1, world, d);
+  if (!fp64) {
+    if (pass == 1 && o.ahp_rule) k_ahp_pass_tiled<1, 1><<<blocks, 256, 0, st>>>(g, q0, q1, world, d);
+    else if (pass == 1) k_ahp_pass_tiled<1, 0><<<blocks, 256, 0, st>>>(g, q0, q1, world, d);
+    else if (o.ahp_rule) k_ahp_pass_tiled<2, 1><<<blocks, 256, 0, st>>>(g, q0, q1, world, d);
+    else k_ahp_pass_tiled<2, 0><<<blocks, 256, 0, st>>>(g, q0, q1, world, d);
+  } else if (pass == 1) {
+    k_ahp_pass<1, true><<<blocks, 256, 0, st>>>(g, o, q0, q1, world, d);
+  } else {
+    k_ahp_pass<2, true><<<blocks, 256, 0, st>>>(g, o, q0, q1, world, d);
+  }
   return cudaGetLastError();
 }
 cudaError_t launch_ahp_mid(bool fp64, const Geo& g, const Opt& o, int* state, const ShardDev& d, cudaStream_t st) {
