@@ -2422,13 +2422,19 @@ __device__ __forceinline__ void rsum_tile(const float2* arr, int K, int l0, int 
     for (int off = 16; off > 0; off >>= 1) out[p] += __shfl_xor_sync(FULL, out[p], off);
 }
 
-constexpr int kAhpTile = 4;
+#ifndef NACS_AHP_TILE
+#define NACS_AHP_TILE 4
+#endif
+#ifndef NACS_AHP_MINB
+#define NACS_AHP_MINB 3
+#endif
+constexpr int kAhpTile = NACS_AHP_TILE;
 
 // The rank's pairs (t, K-1-t), t in [a, b), cut into tiles of kAhpTile consecutive t: a warp
 // takes the low levels t.. and the mirrored high levels K-1-t.. of one tile (K-1 terms per
 // pair, as before), skipping the middle level of an odd K on the high side.
 template <int PASS, int RULE>
-__global__ void __launch_bounds__(256, 3) k_ahp_pass_tiled(Geo g, int q0, int q1, int world, ShardDev d) {
+__global__ void __launch_bounds__(256, NACS_AHP_MINB) k_ahp_pass_tiled(Geo g, int q0, int q1, int world, ShardDev d) {
   constexpr int P = kAhpTile;
   if (!sh_live(d, false)) return;
   const Scratch* s = d.gs;
