@@ -2426,7 +2426,7 @@ __device__ __forceinline__ void rsum_tile(const float2* arr, int K, int l0, int 
 #define NACS_AHP_TILE 4
 #endif
 #ifndef NACS_AHP_MINB
-#define NACS_AHP_MINB 3
+#define NACS_AHP_MINB 4
 #endif
 constexpr int kAhpTile = NACS_AHP_TILE;
 
@@ -2448,10 +2448,17 @@ __global__ void __launch_bounds__(256, NACS_AHP_MINB) k_ahp_pass_tiled(Geo g, in
     b[k] = (int)((long long)half * q1 / world);
     total += (b[k] - a[k] + P - 1) / P;
   }
+  // criteria in decreasing K (a tile costs ~P (K-1) terms): the longest tiles start first
+  int ord[4] = {0, 1, 2, 3};
+  for (int x = 1; x < 4; ++x)
+    for (int y = x; y > 0 && d.Kc[ord[y]] > d.Kc[ord[y - 1]]; --y) {
+      const int tmp = ord[y]; ord[y] = ord[y - 1]; ord[y - 1] = tmp;
+    }
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
   for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < total; i += nwarps) {
-    int k = 0, t = i;
-    while (t >= (b[k] - a[k] + P - 1) / P) { t -= (b[k] - a[k] + P - 1) / P; ++k; }
+    int j = 0, t = i;
+    while (t >= (b[ord[j]] - a[ord[j]] + P - 1) / P) { t -= (b[ord[j]] - a[ord[j]] + P - 1) / P; ++j; }
+    const int k = ord[j];
     const int K = d.Kc[k];
     const int t0 = a[k] + t * P, nt = min(P, b[k] - t0);
     const double sd = s->ahp_scaled[k];
