@@ -376,7 +376,7 @@ def test_server_sharded_nccl_world1():
         sh.close()
 
 
-@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("world", [2, 3, 4])
 @pytest.mark.parametrize("rule", [0, 1])
 def test_server_sharded_ahp_loopback(world, rule):
     """AHP with the level-pair passes split over G logical ranks (sum-allreduce between
@@ -400,13 +400,16 @@ def test_server_sharded_ahp_loopback(world, rule):
         sh.close()
 
 
-def test_ahp_grid_engine_large_topology(ctx):
-    """k=26 (4394 servers): sequential AHP runs through the grid-wide level passes."""
+@pytest.mark.parametrize("rule", [0, 1])
+def test_ahp_grid_engine_large_topology(ctx, rule):
+    """k=26 (4394 servers): sequential AHP runs through the grid-wide level passes
+    (k_ahp_pass_tiled: thousands of levels per criterion, ragged last tiles, both rules)."""
     snap = gen.snapshot(26, seed=26)
     reqs = gen.requests(3, 27)
     ctx.load_topology(snap)
-    out = ctx.schedule_request(reqs, "ahp", "clustering")
-    assert_schedule_parity(snap, reqs, out, "ahp", "clustering", True, gpu_state=ctx.read_topology())
+    out = ctx.schedule_request(reqs, "ahp", "clustering", ahp_rule=rule)
+    assert_schedule_parity(snap, reqs, out, "ahp", "clustering", True, gpu_state=ctx.read_topology(),
+                           ahp_rule=rule)
 
 
 def test_server_sharded_ahp_nccl_world1():
