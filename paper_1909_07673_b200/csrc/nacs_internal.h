@@ -123,6 +123,7 @@ struct ShardDev {
   int* lvscr;                  // AHP: per-criterion level-extraction scratch, 4 x [5 (n2 + 1)] ints
   unsigned long long* kpart;   // AHP: per-CTA top-2 keys of k_ahp_pg, [2 * npart]
   int npart;                   // CTAs of k_ahp_pg
+  double* midtot;              // AHP: [4][32][2] segment totals of the between-passes scans
 };
 
 // Launchers (nacs_kernels.cu).  Each returns the cudaError_t of the launch.

@@ -2533,6 +2533,83 @@ __global__ void __launch_bounds__(1024) k_ahp_mid(Geo g, Opt o, int* state, Shar
   }
 }
 
+// k_ahp_mid in FP32 as two grid kernels.  ahp_prefix on a 1024-thread CTA cuts K into 32
+// warp segments; these kernels run the same 32 segments, with the same loops, butterflies and
+// shuffle scans (bit-identical prefix sums), as 8 CTAs of 4 warps per criterion instead of 32
+// warps sharing one SM (ncu: the one-CTA version was issue-limited on that SM).
+constexpr int kMidWarps = 32;
+__device__ __forceinline__ void mid_seg(int K, int w, int& s0, int& s1) {
+  const int seg = ((K + kMidWarps - 1) / kMidWarps + 31) & ~31;
+  s0 = min(w * seg, K);
+  s1 = min(s0 + seg, K);
+}
+
+// (value, weight) levels of the segment and its totals
+__global__ void __launch_bounds__(128) k_ahp_mid_a(Geo g, ShardDev d) {
+  if (!sh_live(d, false)) return;
+  const int k = blockIdx.y, K = d.Kc[k];
+  if (K == 0) return;
+  const int w = blockIdx.x * 4 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  const int n2 = next_pow2(g.n);
+  const float2* lvm = d.lvmC + (size_t)k * n2;
+  float2* lvw = d.lvwC + (size_t)k * n2;
+  int s0, s1;
+  mid_seg(K, w, s0, s1);
+  double ta = 0, tb = 0;
+  for (int base = s0; base < s1; base += 32) {
+    const int i = base + lane;
+    if (i < s1) {
+      const float2 e = make_float2(lvm[i].x, d.wq[k * n2 + i]);
+      lvw[i] = e;
+      ta += (double)e.y;
+      tb += (double)e.y * (double)e.x;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) { ta += __shfl_xor_sync(FULL, ta, o); tb += __shfl_xor_sync(FULL, tb, o); }
+  if (lane == 0) {
+    d.midtot[(k * kMidWarps + w) * 2] = ta;
+    d.midtot[(k * kMidWarps + w) * 2 + 1] = tb;
+  }
+}
+
+// exclusive scan of the segment totals (warp_exscan_d2's order), then the segment's prefixes
+__global__ void __launch_bounds__(128) k_ahp_mid_b(Geo g, ShardDev d) {
+  if (!sh_live(d, false)) return;
+  const int k = blockIdx.y, K = d.Kc[k];
+  if (K == 0) return;
+  const int w = blockIdx.x * 4 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  const int n2 = next_pow2(g.n);
+  const float2* lv = d.lvwC + (size_t)k * n2;
+  double* pa = d.paC + (size_t)k * (n2 + 2);
+  double* pb = d.pbC + (size_t)k * (n2 + 2);
+  const double xa = d.midtot[(k * kMidWarps + lane) * 2], xb = d.midtot[(k * kMidWarps + lane) * 2 + 1];
+  double ia = xa, ib = xb;
+  for (int o = 1; o < 32; o <<= 1) {
+    const double ya = __shfl_up_sync(FULL, ia, o), yb = __shfl_up_sync(FULL, ib, o);
+    if (lane >= o) { ia += ya; ib += yb; }
+  }
+  double ra = __shfl_sync(FULL, ia - xa, w), rb = __shfl_sync(FULL, ib - xb, w);
+  const double TA = __shfl_sync(FULL, ia, 31), TB = __shfl_sync(FULL, ib, 31);
+  int s0, s1;
+  mid_seg(K, w, s0, s1);
+  for (int base = s0; base < s1; base += 32) {
+    const int i = base + lane;
+    double a = 0, b = 0;
+    if (i < s1) { const float2 e = lv[i]; a = (double)e.y; b = (double)e.y * (double)e.x; }
+    double ja = a, jb = b;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double ya = __shfl_up_sync(FULL, ja, o), yb = __shfl_up_sync(FULL, jb, o);
+      if (lane >= o) { ja += ya; jb += yb; }
+    }
+    if (i < s1) { pa[i] = ra + (ja - a); pb[i] = rb + (jb - b); }
+    ra += __shfl_sync(FULL, ja, 31);
+    rb += __shfl_sync(FULL, jb, 31);
+  }
+  if (w == 0 && lane == 0) { pa[K] = TA; pb[K] = TB; }
+}
+
 // PG over F on the whole grid (FP32; one server per thread): each CTA leaves its top-2
 // (score, index) keys in d.kpart for k_ahp_decide.  The top-2 of the union of per-CTA top-2
 // sets is the global top-2, so the decision is the one-CTA kernel's.
@@ -2635,8 +2712,12 @@ cudaError_t launch_ahp_pass(int pass, bool fp64, const Geo& g, const Opt& o, int
   return cudaGetLastError();
 }
 cudaError_t launch_ahp_mid(bool fp64, const Geo& g, const Opt& o, int* state, const ShardDev& d, cudaStream_t st) {
-  if (fp64) k_ahp_mid<true><<<4, 1024, 0, st>>>(g, o, state, d);
-  else k_ahp_mid<false><<<4, 1024, 0, st>>>(g, o, state, d);
+  if (fp64) {
+    k_ahp_mid<true><<<4, 1024, 0, st>>>(g, o, state, d);
+  } else {
+    k_ahp_mid_a<<<dim3(kMidWarps / 4, 4), 128, 0, st>>>(g, d);
+    k_ahp_mid_b<<<dim3(kMidWarps / 4, 4), 128, 0, st>>>(g, d);
+  }
   return cudaGetLastError();
 }
 cudaError_t launch_ahp_decide(bool fp64, const Geo& g, const Opt& o, int* state, const ReqsDev& R, const OutDev& O,
