@@ -2426,7 +2426,10 @@ __device__ __forceinline__ void rsum_tile(const float2* arr, int K, int l0, int 
 #define NACS_AHP_TILE 4
 #endif
 #ifndef NACS_AHP_MINB
-#define NACS_AHP_MINB 4
+#define NACS_AHP_MINB 8
+#endif
+#ifndef NACS_AHP_BLOCK
+#define NACS_AHP_BLOCK 128
 #endif
 constexpr int kAhpTile = NACS_AHP_TILE;
 
@@ -2434,7 +2437,7 @@ constexpr int kAhpTile = NACS_AHP_TILE;
 // takes the low levels t.. and the mirrored high levels K-1-t.. of one tile (K-1 terms per
 // pair, as before), skipping the middle level of an odd K on the high side.
 template <int PASS, int RULE>
-__global__ void __launch_bounds__(256, NACS_AHP_MINB) k_ahp_pass_tiled(Geo g, int q0, int q1, int world, ShardDev d) {
+__global__ void __launch_bounds__(NACS_AHP_BLOCK, NACS_AHP_MINB) k_ahp_pass_tiled(Geo g, int q0, int q1, int world, ShardDev d) {
   constexpr int P = kAhpTile;
   if (!sh_live(d, false)) return;
   const Scratch* s = d.gs;
@@ -2700,10 +2703,11 @@ cudaError_t launch_ahp_pass(int pass, bool fp64, const Geo& g, const Opt& o, int
   cudaDeviceGetAttribute(&blocks, cudaDevAttrMultiProcessorCount, 0);
   blocks *= 8;
   if (!fp64) {
-    if (pass == 1 && o.ahp_rule) k_ahp_pass_tiled<1, 1><<<blocks, 256, 0, st>>>(g, q0, q1, world, d);
-    else if (pass == 1) k_ahp_pass_tiled<1, 0><<<blocks, 256, 0, st>>>(g, q0, q1, world, d);
-    else if (o.ahp_rule) k_ahp_pass_tiled<2, 1><<<blocks, 256, 0, st>>>(g, q0, q1, world, d);
-    else k_ahp_pass_tiled<2, 0><<<blocks, 256, 0, st>>>(g, q0, q1, world, d);
+    const int tb = blocks * 256 / NACS_AHP_BLOCK;
+    if (pass == 1 && o.ahp_rule) k_ahp_pass_tiled<1, 1><<<tb, NACS_AHP_BLOCK, 0, st>>>(g, q0, q1, world, d);
+    else if (pass == 1) k_ahp_pass_tiled<1, 0><<<tb, NACS_AHP_BLOCK, 0, st>>>(g, q0, q1, world, d);
+    else if (o.ahp_rule) k_ahp_pass_tiled<2, 1><<<tb, NACS_AHP_BLOCK, 0, st>>>(g, q0, q1, world, d);
+    else k_ahp_pass_tiled<2, 0><<<tb, NACS_AHP_BLOCK, 0, st>>>(g, q0, q1, world, d);
   } else if (pass == 1) {
     k_ahp_pass<1, true><<<blocks, 256, 0, st>>>(g, o, q0, q1, world, d);
   } else {
