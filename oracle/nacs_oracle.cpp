@@ -143,10 +143,14 @@ std::vector<double> ahp_priority(const std::vector<double>& x, int rule) {
     return L;
   }
   auto cell = [&](size_t i, size_t j) { return ahp_cell(9.0 * (x[i] - x[j]) / (hi - lo), rule); };
+  // OpenMP over columns, then over rows (SURVEY §8(c) "OpenMP only across independent
+  // requests or AHP rows"): every sum still runs sequentially in index order.
   std::vector<double> colsum(m, 0.0);
-  for (size_t j = 0; j < m; ++j)
+#pragma omp parallel for schedule(static) if (m >= 2048)
+  for (long j = 0; j < (long)m; ++j)
     for (size_t i = 0; i < m; ++i) colsum[j] += cell(i, j);
-  for (size_t i = 0; i < m; ++i) {
+#pragma omp parallel for schedule(static) if (m >= 2048)
+  for (long i = 0; i < (long)m; ++i) {
     double s = 0.0;
     for (size_t j = 0; j < m; ++j) s += cell(i, j) / colsum[j];
     L[i] = s / (double)m;
@@ -185,9 +189,13 @@ RankOut rank(const DC& dc, const Opts& o, long dem_cpu, long dem_ram,
 
   // a2: widest fabric bottleneck from every edge switch to every flow's server.
   std::vector<std::vector<double>> Fv(flows.size(), std::vector<double>(dc.E, 0.0));
+  // Each table entry is independent: OpenMP over the edge switches (the per-entry
+  // arithmetic is unchanged, so the table is identical at any thread count).
   if (o.path_filter)
-    for (size_t f = 0; f < flows.size(); ++f)
+    for (size_t f = 0; f < flows.size(); ++f) {
+#pragma omp parallel for schedule(static) if (dc.E >= 512)
       for (int e = 0; e < dc.E; ++e) Fv[f][e] = fabric_widest_from_edge(dc, e, flows[f].v);
+    }
 
   // a3: feasibility filter, Eq. 4-7, reading R6.
   for (int u = 0; u < dc.n; ++u) {

@@ -98,6 +98,7 @@ struct nacs_ctx {
   // server sharding (nacs_create_sharded)
   int rank = 0, world = 1;
   bool loopback = false;
+  bool comm_aborted = false;  // an error inside a sharded call aborted the communicator
   ncclComm_t comm = nullptr;
   DevArr<unsigned char> sh_buf;
   PinArr sh_ctl;
@@ -682,16 +683,18 @@ nacs_status schedule_sharded(nacs_ctx* ctx, const Opt& o, const nacs::ReqsDev& R
       if (it > 4L * (g.n + 1) * (nacs::MAXC + 1))
         return fail(ctx, NACS_ECUDA, "sharded engine: pod loop did not finish (phase " + std::to_string(phase) + ")");
       if (ahp) {  // AHP: passes over this process's share of level pairs, sum-allreduce between
+        // (loopback: one launch per logical rank, so the per-rank pair split runs as under NCCL)
         const bool f64 = phase == 3;
-        const int q0 = ctx->loopback ? 0 : ctx->rank, q1 = ctx->loopback ? world : ctx->rank + 1;
         if (!f64) CK(nacs::launch_sh_prep(g, o, ctx->state.p, Rd, Od, r, d, ctx->stream));
-        CK(nacs::launch_ahp_pass(1, f64, g, o, ctx->state.p, q0, q1, world, d, ctx->stream));
+        for (int q = s_lo; q < s_hi; ++q)
+          CK(nacs::launch_ahp_pass(1, f64, g, o, ctx->state.p, q, q + 1, world, d, ctx->num_sms, ctx->stream));
         if (ctx->comm) {
           if (f64) NCK(ncclAllReduce(d.wq64, d.wq64, 4 * n2, ncclFloat64, ncclSum, ctx->comm, ctx->stream));
           else NCK(ncclAllReduce(d.wq, d.wq, 4 * n2, ncclFloat32, ncclSum, ctx->comm, ctx->stream));
         }
         CK(nacs::launch_ahp_mid(f64, g, o, ctx->state.p, d, ctx->stream));
-        CK(nacs::launch_ahp_pass(2, f64, g, o, ctx->state.p, q0, q1, world, d, ctx->stream));
+        for (int q = s_lo; q < s_hi; ++q)
+          CK(nacs::launch_ahp_pass(2, f64, g, o, ctx->state.p, q, q + 1, world, d, ctx->num_sms, ctx->stream));
         if (ctx->comm) {
           if (f64) NCK(ncclAllReduce(d.l2q64, d.l2q64, 4 * n2, ncclFloat64, ncclSum, ctx->comm, ctx->stream));
           else NCK(ncclAllReduce(d.l2q, d.l2q, 4 * n2, ncclFloat32, ncclSum, ctx->comm, ctx->stream));
@@ -710,9 +713,10 @@ nacs_status schedule_sharded(nacs_ctx* ctx, const Opt& o, const nacs::ReqsDev& R
           std::vector<int> ki(world);
           std::vector<double> kv(world);
           std::vector<unsigned long long> kk(2 * world);
-          CK(cudaMemcpy(ki.data(), d.kxi, 4 * world, cudaMemcpyDeviceToHost));
-          CK(cudaMemcpy(kv.data(), d.kxv, 8 * world, cudaMemcpyDeviceToHost));
-          CK(cudaMemcpy(kk.data(), d.kx, 16 * world, cudaMemcpyDeviceToHost));
+          CK(cudaMemcpyAsync(ki.data(), d.kxi, 4 * world, cudaMemcpyDeviceToHost, ctx->stream));
+          CK(cudaMemcpyAsync(kv.data(), d.kxv, 8 * world, cudaMemcpyDeviceToHost, ctx->stream));
+          CK(cudaMemcpyAsync(kk.data(), d.kx, 16 * world, cudaMemcpyDeviceToHost, ctx->stream));
+          CK(cudaStreamSynchronize(ctx->stream));
           for (int q = 0; q < world; ++q)
             fprintf(stderr, "  fp64 slot %d: %d %.17g keys %016llx %016llx\n", q, ki[q], kv[q], kk[2 * q], kk[2 * q + 1]);
         }
@@ -1050,8 +1054,19 @@ nacs_status nacs_schedule_request(nacs_ctx* ctx, const nacs_options* opt, const 
     return fail(ctx, NACS_EINVAL, "options.rank_mode = NACS_RANK_ONCE is not available on server-sharded contexts");
   if (o.method >= NACS_BF && (ctx->world > 1 || ctx->comm))
     return fail(ctx, NACS_EINVAL, "BF / WF are not available on server-sharded contexts");
+  if (ctx->comm_aborted)
+    return fail(ctx, NACS_ENCCL, "the NCCL communicator of this context was aborted after an earlier error");
   if (ctx->world > 1 || ctx->comm || (o.method == NACS_AHP && g.n >= 4096 && !o.rank_once)) {
-    if ((st = schedule_sharded(ctx, o, Rd, Od, R))) return st;
+    if ((st = schedule_sharded(ctx, o, Rd, Od, R))) {
+      // the other ranks may be waiting in this pod step's collective: abort the communicator so
+      // that they fail instead of hanging, and refuse further sharded calls on this context
+      if (ctx->comm) {
+        ncclCommAbort(ctx->comm);
+        ctx->comm = nullptr;
+        ctx->comm_aborted = true;
+      }
+      return st;
+    }
     if (!dev) {
       if ((st = unstage_outputs(ctx, R, C, V, out))) return st;
     }

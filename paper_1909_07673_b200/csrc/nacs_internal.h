@@ -178,7 +178,7 @@ cudaError_t launch_sh_decide64(const Geo& g, const Opt& o, int* state, const Req
 // AHP pod step over the grid and the ranks: passes over this process's share of level
 // pairs (ranks q in [q0, q1) of world), then the 1-CTA middle / decide kernels.
 cudaError_t launch_ahp_pass(int pass, bool fp64, const Geo& g, const Opt& o, int* state, int q0, int q1, int world,
-                            const ShardDev& d, cudaStream_t st);
+                            const ShardDev& d, int num_sms, cudaStream_t st);
 cudaError_t launch_ahp_mid(bool fp64, const Geo& g, const Opt& o, int* state, const ShardDev& d, cudaStream_t st);
 cudaError_t launch_ahp_decide(bool fp64, const Geo& g, const Opt& o, int* state, const ReqsDev& R, const OutDev& O,
                               int r, const ShardDev& d, cudaStream_t st);

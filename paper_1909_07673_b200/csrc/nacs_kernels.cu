@@ -2444,11 +2444,14 @@ __global__ void __launch_bounds__(NACS_AHP_BLOCK, NACS_AHP_MINB) k_ahp_pass_tile
   const int n2 = next_pow2(g.n);
   const int m = s->nf;
   const int lane = threadIdx.x & 31;
+  // ranks split whole tiles: tile starts are multiples of P for every world size, so the
+  // FP32 chunking of each level's terms (rsum_tile, from l0) never depends on the split and
+  // every rank count gives bit-identical weights and L2
   int a[4], b[4], total = 0;
   for (int k = 0; k < 4; ++k) {
-    const int K = d.Kc[k], half = (K + 1) >> 1;
-    a[k] = (int)((long long)half * q0 / world);
-    b[k] = (int)((long long)half * q1 / world);
+    const int K = d.Kc[k], half = (K + 1) >> 1, ntile = (half + P - 1) / P;
+    a[k] = min(half, P * (int)((long long)ntile * q0 / world));
+    b[k] = min(half, P * (int)((long long)ntile * q1 / world));
     total += (b[k] - a[k] + P - 1) / P;
   }
   // criteria in decreasing K (a tile costs ~P (K-1) terms): the longest tiles start first
@@ -2697,11 +2700,9 @@ __global__ void __launch_bounds__(1024) k_ahp_decide(Geo g, Opt o, int* state, R
 }
 
 cudaError_t launch_ahp_pass(int pass, bool fp64, const Geo& g, const Opt& o, int* state, int q0, int q1, int world,
-                            const ShardDev& d, cudaStream_t st) {
+                            const ShardDev& d, int num_sms, cudaStream_t st) {
   (void)state;
-  int blocks = 0;
-  cudaDeviceGetAttribute(&blocks, cudaDevAttrMultiProcessorCount, 0);
-  blocks *= 8;
+  const int blocks = num_sms * 8;
   if (!fp64) {
     const int tb = blocks * 256 / NACS_AHP_BLOCK;
     if (pass == 1 && o.ahp_rule) k_ahp_pass_tiled<1, 1><<<tb, NACS_AHP_BLOCK, 0, st>>>(g, q0, q1, world, d);

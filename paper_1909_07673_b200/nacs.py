@@ -259,6 +259,21 @@ class Context:
         return dict(mask=mask, scores=scores, best=int(best[0]))
 
     # ------------------------------------------------------------ schedule ---
+    def _check_tensor(self, key, a, min_numel=None, exact_numel=None):
+        """A torch tensor handed to the library by pointer must be int32, contiguous and on
+        this context's device, and hold at least the elements the kernels will touch."""
+        import torch
+        if a.dtype != torch.int32:
+            raise ValueError(f"{key}: dtype {a.dtype}, expected torch.int32")
+        if not a.is_contiguous():
+            raise ValueError(f"{key}: not contiguous")
+        if a.device.type != "cuda" or a.device.index != self.device:
+            raise ValueError(f"{key}: on {a.device}, expected cuda:{self.device}")
+        if exact_numel is not None and a.numel() != exact_numel:
+            raise ValueError(f"{key}: {a.numel()} elements, expected {exact_numel}")
+        if min_numel is not None and a.numel() < min_numel:
+            raise ValueError(f"{key}: {a.numel()} elements, at least {min_numel} needed")
+
     def _requests(self, reqs: dict):
         arrs = []
         dev = None
@@ -272,13 +287,62 @@ class Context:
                 arrs.append(_i32(a))
         if dev == "mixed":
             raise ValueError("request arrays must be all host or all device")
-        r = Requests(int(reqs["n_requests"]), *[_ptr(a) for a in arrs])
+        R = int(reqs["n_requests"])
+        if R < 0:
+            raise ValueError("n_requests < 0")
+        by_key = dict(zip(REQ_KEYS, arrs))
+        if dev:
+            import torch
+            for key, a in by_key.items():  # dtype and layout of every array before devices and sizes
+                if a.dtype != torch.int32:
+                    raise ValueError(f"{key}: dtype {a.dtype}, expected torch.int32")
+                if not a.is_contiguous():
+                    raise ValueError(f"{key}: not contiguous")
+            # container_off[R] / vlink_off[R] live on the device: the per-container and per-vlink
+            # arrays must agree in length with each other (their common length bounds the offsets)
+            for key in ("container_off", "vlink_off"):
+                self._check_tensor(key, by_key[key], exact_numel=R + 1)
+            for group in (("cpu_min", "cpu_max", "ram_min", "ram_max", "pod_of"), ("vl_src", "vl_dst", "bw_min", "bw_max")):
+                for key in group:
+                    self._check_tensor(key, by_key[key], exact_numel=by_key[group[0]].numel())
+            sizes = dict(R=R, C=by_key["cpu_min"].numel(), V=by_key["vl_src"].numel())
+        else:
+            for key in ("container_off", "vlink_off"):
+                if by_key[key].size != R + 1:
+                    raise ValueError(f"{key}: {by_key[key].size} elements, expected n_requests + 1 = {R + 1}")
+            Cn, Vn = int(by_key["container_off"][-1]), int(by_key["vlink_off"][-1])
+            for key, need in (("cpu_min", Cn), ("cpu_max", Cn), ("ram_min", Cn), ("ram_max", Cn), ("pod_of", Cn),
+                              ("vl_src", Vn), ("vl_dst", Vn), ("bw_min", Vn), ("bw_max", Vn)):
+                if by_key[key].size < need:
+                    raise ValueError(f"{key}: {by_key[key].size} elements, at least {need} needed")
+            sizes = dict(R=R, C=Cn, V=Vn)
+        self._req_sizes = sizes
+        r = Requests(R, *[_ptr(a) for a in arrs])
         return r, arrs, bool(dev)
+
+    def _check_out(self, out: dict, device: bool):
+        """Caller-supplied output arrays: int32, contiguous, on the right side, large enough."""
+        s = self._req_sizes
+        need = dict(status=s["R"], server_of_container=s["C"], cpu_alloc=s["C"], ram_alloc=s["C"], bw_alloc=s["V"],
+                    path_of_vlink=s["V"])
+        for key in OUT_KEYS:
+            a = out[key]
+            if device:
+                if not _is_torch(a):
+                    raise ValueError(f"out[{key}]: device requests need torch CUDA outputs")
+                self._check_tensor(f"out[{key}]", a, min_numel=need[key])
+            else:
+                if _is_torch(a) or not isinstance(a, np.ndarray):
+                    raise ValueError(f"out[{key}]: host requests need numpy outputs")
+                if a.dtype != np.int32 or not a.flags.c_contiguous or not a.flags.writeable:
+                    raise ValueError(f"out[{key}]: must be a writeable C-contiguous int32 array")
+                if a.size < need[key]:
+                    raise ValueError(f"out[{key}]: {a.size} elements, at least {need[key]} needed")
 
     def _alloc_out(self, reqs: dict, device: bool):
         R = int(reqs["n_requests"])
-        Cn = int(reqs["container_off"][-1])
-        Vn = int(reqs["vlink_off"][-1])
+        Cn = int(reqs["container_off"][-1]) if len(reqs["container_off"]) else 0
+        Vn = int(reqs["vlink_off"][-1]) if len(reqs["vlink_off"]) else 0
         sizes = dict(status=R, server_of_container=Cn, cpu_alloc=Cn, ram_alloc=Cn, bw_alloc=Vn, path_of_vlink=Vn)
         if device:
             import torch
@@ -295,6 +359,8 @@ class Context:
         sizes = None
         if out is None:
             out, sizes = self._alloc_out(reqs, dev)
+        else:
+            self._check_out(out, dev)
         p = Placements(*[_ptr(out[k]) for k in OUT_KEYS])
         self._check(fn(self._h, C.byref(o), C.byref(r), C.byref(p)))
         del keep
@@ -316,9 +382,11 @@ class Context:
         r, keep, dev = self._requests(reqs)
         if dev:
             flags |= NACS_DEVICE_PTRS
+            self._check_out(placements, True)
             outs = [placements[k] for k in OUT_KEYS]
         else:
             outs = [_i32(placements[k]) for k in OUT_KEYS]
+            self._check_out(dict(zip(OUT_KEYS, outs)), False)
         p = Placements(*[_ptr(a) for a in outs])
         self._check(self._lib.nacs_release(self._h, flags, C.byref(r), C.byref(p)))
         del keep
@@ -365,6 +433,11 @@ class Context:
         if not dev:
             src, dst, demand = _i32(src), _i32(dst), _i32(demand)
         nq = int(src.numel() if dev else src.size)
+        if dev:
+            for key, a in (("src", src), ("dst", dst), ("demand", demand)):
+                self._check_tensor(key, a, exact_numel=nq)
+        elif dst.size != nq or demand.size != nq:
+            raise ValueError("src, dst and demand must have the same length")
         if max_hops is None:
             max_hops = 16
         if out is None:
@@ -375,6 +448,15 @@ class Context:
                 mk = lambda *shape: np.zeros(shape, np.int32)
             out = (mk(max(nq, 1)), mk(max(nq, 1)), mk(max(nq, 1), max_hops + 1) if with_path else None)
         bn, hops, path = out
+        for key, a, need in (("bottleneck", bn, nq), ("hops", hops, nq),
+                             ("path", path, nq * (max_hops + 1))):
+            if a is None:
+                continue
+            if dev:
+                self._check_tensor(key, a, min_numel=need)
+            elif (not isinstance(a, np.ndarray) or a.dtype != np.int32 or not a.flags.c_contiguous
+                  or a.size < need):
+                raise ValueError(f"{key}: must be a C-contiguous int32 array of at least {need} elements")
         q = PathQuery(nq, _ptr(src), _ptr(dst), _ptr(demand))
         if dev:
             flags |= NACS_DEVICE_PTRS
@@ -387,7 +469,13 @@ class Context:
         if out is None:
             out = np.zeros(self.graph_ns, np.int64)
         if _is_torch(out):
+            import torch
+            if out.dtype != torch.int64 or not out.is_contiguous() or out.numel() < self.graph_ns or \
+                    out.device != torch.device("cuda", self.device):
+                raise ValueError(f"out: a contiguous int64 cuda:{self.device} tensor of >= {self.graph_ns} elements")
             flags |= NACS_DEVICE_PTRS
+        elif out.dtype != np.int64 or not out.flags.c_contiguous or out.size < self.graph_ns:
+            raise ValueError(f"out: a C-contiguous int64 array of >= {self.graph_ns} elements")
         self._check(self._lib.nacs_logical_bandwidth(self._h, flags, _ptr(out)))
         return out
 

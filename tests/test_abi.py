@@ -81,3 +81,44 @@ def test_product_does_not_import_oracle():
             if f.endswith((".py", ".cu", ".h", ".cuh", ".cpp")):
                 src = open(os.path.join(dirpath, f)).read()
                 assert "oracle" not in re.sub(r"(#|//).*", "", src), f
+
+
+def _bare_ctx():
+    """A Context object without a device handle: only the binding's argument checks run."""
+    c = nacs.Context.__new__(nacs.Context)
+    c.device = 0
+    c._h = None
+    return c
+
+
+def test_binding_rejects_bad_arrays():
+    """tensors passed by pointer are checked for dtype, layout, device and size
+    before any library call (an int64 tensor read as int32 would be garbage)."""
+    import numpy as np
+    import torch
+    from inputs import gen
+    c = _bare_ctx()
+    reqs = gen.requests(3, 5)
+    t = {k: (torch.from_numpy(v) if isinstance(v, np.ndarray) else v) for k, v in reqs.items()}
+    with pytest.raises(ValueError, match="expected cuda:0"):
+        c._requests(t)  # CPU tensors
+    t64 = dict(t, cpu_min=t["cpu_min"].to(torch.int64))
+    with pytest.raises(ValueError, match="dtype"):
+        c._requests(t64)
+    strided = dict(t, cpu_min=torch.from_numpy(np.repeat(reqs["cpu_min"], 2))[::2])
+    with pytest.raises(ValueError, match="contiguous"):
+        c._requests(strided)
+    short = dict(reqs, cpu_min=reqs["cpu_min"][:-1])
+    with pytest.raises(ValueError, match="cpu_min"):
+        c._requests(short)
+    with pytest.raises(ValueError, match="container_off"):
+        c._requests(dict(reqs, container_off=reqs["container_off"][:-1]))
+    c._requests(reqs)
+    out = c._alloc_out(reqs, False)[0]
+    c._check_out(out, False)
+    with pytest.raises(ValueError, match="at least"):
+        c._check_out(dict(out, bw_alloc=out["bw_alloc"][:-1]), False)
+    with pytest.raises(ValueError, match="int32"):
+        c._check_out(dict(out, status=out["status"].astype(np.int64)), False)
+    with pytest.raises(ValueError, match="numpy"):
+        c._check_out(dict(out, status=torch.from_numpy(out["status"])), False)

@@ -1,0 +1,230 @@
+"""GPU parity, round 2: the hand-worked commit cases (R17/R18/R19), the paper-literal flags
+(path_filter = 0, R6; l1_mode = 1, R10), nacs_rank_* at k = 32 and 64, and configuration
+C5 (fat-tree k = 64, 65536 servers) against the oracle (needs a B200)."""
+import numpy as np
+import pytest
+
+from inputs import gen
+from oracle import oracle as O
+from tests import commit_cases as CC
+from tests.ahp_closed_form import ahp_levels_l2
+from tests.parity import SCORE_RTOL, assert_rank_parity, assert_schedule_parity, to_np
+
+pytestmark = pytest.mark.gpu
+SCHEMAS = ("flat", "clustering", "network")
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    from paper_1909_07673_b200 import nacs
+    c = nacs.Context(0)
+    yield c
+    c.close()
+
+
+def random_flows(rng, n, nflow, dmax=60):
+    vs = rng.choice(n, size=min(nflow, n), replace=False)
+    return [(int(v), int(rng.integers(1, dmax))) for v in vs]
+
+
+# ----------------------------------------------- R17 / R18 / R19 by hand -----
+@pytest.mark.parametrize("case", sorted(CC.CASES))
+@pytest.mark.parametrize("method", ["ahp", "topsis"])
+def test_commit_cases_sequential(ctx, case, method):
+    snap, req, expect = CC.CASES[case]()
+    ctx.load_topology(snap)
+    out = to_np(ctx.schedule_request(req, method, "flat"))
+    st = ctx.read_topology()
+    CC.check(expect, out, st, ctx.last_stats()["retries"], f"{case} {method}")
+    assert_schedule_parity(snap, req, out, method, "flat", True, gpu_state=st)
+
+
+@pytest.mark.parametrize("case", sorted(CC.CASES))
+@pytest.mark.parametrize("method", ["ahp", "topsis"])
+def test_commit_cases_batch(ctx, case, method):
+    """Batch mode: the TOPSIS warp fast path (k_batch_warp) and the CTA kernel (AHP)."""
+    snap, req, expect = CC.CASES[case]()
+    ctx.load_topology(snap)
+    out = to_np(ctx.schedule_batch(req, method, "flat"))
+    CC.check(expect, out, None, ctx.last_stats()["retries"], f"{case} {method}")
+
+
+@pytest.mark.parametrize("case", sorted(CC.CASES))
+@pytest.mark.parametrize("world", [1, 3])
+def test_commit_cases_server_sharded(case, world):
+    """The server-sharded engine (loopback shards) on the same hand-worked cases."""
+    from paper_1909_07673_b200 import nacs
+    snap, req, expect = CC.CASES[case]()
+    sh = nacs.Context(0, shard=(0, world, None))
+    try:
+        for method in ("topsis", "ahp"):
+            sh.load_topology(snap)
+            out = to_np(sh.schedule_request(req, method, "flat"))
+            CC.check(expect, out, sh.read_topology(), sh.last_stats()["retries"], f"{case} {method} x{world}")
+    finally:
+        sh.close()
+
+
+# ----------------------------------------------------- paper-literal flags -----
+@pytest.mark.parametrize("k", [4, 8, 16])
+@pytest.mark.parametrize("method", ["topsis", "ahp"])
+def test_rank_flags_parity(ctx, k, method):
+    """R6 flag path_filter = 0 (select on CPU/RAM only, route after: P:382-383) and R10 flag
+    l1_mode = 1 (L1 = W): masks, scores and argmax against the oracle."""
+    rng = np.random.default_rng(500 + k)
+    n = k ** 3 // 4
+    for trial in range(4):
+        snap = gen.snapshot(k, seed=600 + trial, quantised=trial == 3)
+        if trial % 2:
+            snap["link_res"] = rng.integers(0, 120, size=len(snap["link_res"])).astype(np.int32)
+        ctx.load_topology(snap)
+        flows = random_flows(rng, n, int(rng.integers(1, 4)))
+        dc, dr = int(rng.integers(100, 8000)), int(rng.integers(128, 30000))
+        for schema in SCHEMAS:
+            kws = [dict(path_filter=0)]
+            if method == "ahp":
+                kws += [dict(l1_mode=1), dict(l1_mode=1, ahp_rule=1), dict(path_filter=0, l1_mode=1)]
+            for kw in kws:
+                g = ctx.rank(method, schema, dc, dr, flows, **kw)
+                o = O.rank(snap, method, schema, dc, dr, flows, **kw)
+                assert_rank_parity(g, o, (k, trial, schema, kw))
+
+
+@pytest.mark.parametrize("method", ["topsis", "ahp"])
+def test_schedule_path_filter_0(ctx, method):
+    """Select-then-route (R6 flag): a congested fabric makes routing fail after selection,
+    which excludes the server and redoes the pod step (R18) — sequential and batch."""
+    tight = gen.snapshot(8, seed=77)
+    tight["link_res"] = np.random.default_rng(1).integers(0, 90, size=len(tight["link_res"])).astype(np.int32)
+    reqs = gen.requests(200, 78, bw_max_hi=60)
+    for schema in ("flat", "network"):
+        ctx.load_topology(tight)
+        out = ctx.schedule_request(reqs, method, schema, path_filter=0)
+        cnt = assert_schedule_parity(tight, reqs, out, method, schema, True, gpu_state=ctx.read_topology(),
+                                     path_filter=0)
+        assert cnt["retries"] == ctx.last_stats()["retries"] and cnt["retries"] > 0
+        ctx.load_topology(tight)
+        out = ctx.schedule_batch(reqs, method, schema, path_filter=0)
+        assert_schedule_parity(tight, reqs, out, method, schema, False, path_filter=0)
+    snap, c2 = gen.config("C2")
+    ctx.load_topology(snap)
+    out = ctx.schedule_batch(c2, method, "clustering", path_filter=0)
+    assert_schedule_parity(snap, c2, out, method, "clustering", False, path_filter=0)
+
+
+@pytest.mark.parametrize("rule", [0, 1])
+def test_schedule_l1_weights(ctx, rule):
+    """AHP with L1 = W (R10 flag), both pairwise rules, sequential and batch (C2)."""
+    snap, reqs = gen.config("C2")
+    for schema in SCHEMAS:
+        ctx.load_topology(snap)
+        out = ctx.schedule_request(reqs, "ahp", schema, l1_mode=1, ahp_rule=rule)
+        assert_schedule_parity(snap, reqs, out, "ahp", schema, True, gpu_state=ctx.read_topology(), l1_mode=1,
+                               ahp_rule=rule)
+        ctx.load_topology(snap)
+        out = ctx.schedule_batch(reqs, "ahp", schema, l1_mode=1, ahp_rule=rule)
+        assert_schedule_parity(snap, reqs, out, "ahp", schema, False, l1_mode=1, ahp_rule=rule)
+
+
+def test_flags_on_server_sharded_engine():
+    """path_filter = 0 and l1_mode = 1 through the server-sharded engine (loopback x2)."""
+    from paper_1909_07673_b200 import nacs
+    snap, reqs = gen.config("C2")
+    sub = gen.subset(reqs, np.arange(40))
+    sh = nacs.Context(0, shard=(0, 2, None))
+    try:
+        for method, kw in (("topsis", dict(path_filter=0)), ("ahp", dict(path_filter=0)),
+                           ("ahp", dict(l1_mode=1))):
+            sh.load_topology(snap)
+            out = sh.schedule_request(sub, method, "network", **kw)
+            assert_schedule_parity(snap, sub, out, method, "network", True, gpu_state=sh.read_topology(), **kw)
+    finally:
+        sh.close()
+
+
+# ---------------------------------------------------- rank at k = 32, 64 -----
+@pytest.mark.parametrize("k", [32, 64])
+@pytest.mark.parametrize("method", ["topsis", "ahp"])
+def test_rank_parity_large(ctx, k, method):
+    """nacs_rank_* on the C4 / C5 snapshots.  At k = 64 AHP takes CPU/RAM demands that leave
+    |F| ~ 2.7e4 (the oracle's explicit pairwise cells are O(|F|^2))."""
+    rng = np.random.default_rng(70 + k)
+    n = k ** 3 // 4
+    snap = gen.snapshot(k, gen.CONFIG_SEEDS["C4" if k == 32 else "C5"])
+    ctx.load_topology(snap)
+    cases = [(1500, 3000, random_flows(rng, n, 3)), (800, 1000, [])]
+    if method == "ahp" and k == 64:
+        cases = [(21000, 200000, random_flows(rng, n, 2))]
+    for dc, dr, flows in cases:
+        for schema in (SCHEMAS if k == 32 else ("network",)):
+            g = ctx.rank(method, schema, dc, dr, flows)
+            o = O.rank(snap, method, schema, dc, dr, flows)
+            assert_rank_parity(g, o, (k, schema, dc))
+
+
+def test_rank_ahp_k64_quantised_closed_form(ctx):
+    """AHP at full C5 scale (65536 feasible servers) against the K-level closed form of
+    SURVEY §8(c) "AHP" (tests/ahp_closed_form.py): quantised residuals have a few dozen
+    CPU/RAM levels, the 0/1 flag two, the access links ~950."""
+    snap = gen.snapshot(64, gen.CONFIG_SEEDS["C5"], quantised=True)
+    ctx.load_topology(snap)
+    for schema, L1 in (("flat", (0.25, 0.25, 0.25, 0.25)),):
+        for rule in (0, 1):
+            g = ctx.rank("ahp", schema, 1, 1, ahp_rule=rule)
+            assert g["mask"].all()
+            crit = [snap["cpu_res"], snap["ram_res"], snap["active"], snap["link_res"][: 65536]]
+            pg = sum(w * ahp_levels_l2(np.asarray(x, np.int64), rule) for w, x in zip(L1, crit))
+            assert abs(pg.sum() - 1.0) < 1e-12
+            err = np.abs(g["scores"].astype(np.float64) - pg) / pg
+            assert err.max() <= SCORE_RTOL, err.max()
+            top = pg.max()
+            tie = pg >= top - 1e-9 * top
+            assert tie[g["best"]]
+
+
+# --------------------------------------------------------------------- C5 -----
+def _run_modes(snap, reqs, method, modes):
+    """Schedule on each context mode; require identical placements and final states across
+    modes; return the first mode's output and state."""
+    from paper_1909_07673_b200 import nacs
+    res = []
+    for shard in modes:
+        c = nacs.Context(0, shard=None if shard is None else (0, shard, None))
+        try:
+            c.load_topology(snap)
+            out = to_np(c.schedule_request(reqs, method, "flat"))
+            res.append((out, c.read_topology(), c.last_stats()))
+        finally:
+            c.close()
+    for out, st, _ in res[1:]:
+        for key in out:
+            assert np.array_equal(out[key], res[0][0][key]), key
+        for key in st:
+            assert np.array_equal(st[key], res[0][1][key]), key
+    return res[0]
+
+
+def test_c5_topsis_sequential_vs_oracle():
+    """BASELINE configs[4]: k = 64, sequential TOPSIS Flat over the bench's 40 C5 requests —
+    unsharded (k_sequential on the global state) and as 8 loopback server shards —
+    identical placements and final state, equal to the oracle's."""
+    snap = gen.snapshot(64, gen.CONFIG_SEEDS["C5"])
+    reqs = gen.requests(40, gen.CONFIG_SEEDS["C5"] + 1000)
+    out, st, stats = _run_modes(snap, reqs, "topsis", [None, 8])
+    cnt = assert_schedule_parity(snap, reqs, out, "topsis", "flat", True, gpu_state=st)
+    assert stats["pod_steps"] == cnt["pod_steps"]
+
+
+def test_c5_ahp_sequential_vs_oracle():
+    """C5 AHP: the first pod steps of the bench's request stream (the first request of fewest pods
+    with vlinks: 4), unsharded and over 3 loopback shards (uneven level-pair splits); the
+    oracle's explicit O(|F|^2) cells with |F| ~ 6e4 take ~20 s per pod step on 16 cores."""
+    snap = gen.snapshot(64, gen.CONFIG_SEEDS["C5"])
+    reqs = gen.requests(40, gen.CONFIG_SEEDS["C5"] + 1000)
+    co, vo = reqs["container_off"], reqs["vlink_off"]
+    pods = [int(reqs["pod_of"][co[r]:co[r + 1]].max()) + 1 for r in range(40)]
+    r = min((i for i in range(40) if vo[i + 1] > vo[i]), key=lambda i: (pods[i], i))  # request 1: 4 pods
+    one = gen.subset(reqs, [r])
+    out, st, stats = _run_modes(snap, one, "ahp", [None, 3])
+    cnt = assert_schedule_parity(snap, one, out, "ahp", "flat", True, gpu_state=st)
+    assert cnt["pod_steps"] == pods[r] == stats["pod_steps"]
