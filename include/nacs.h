@@ -157,7 +157,8 @@ typedef struct {
   int64_t fp64_decisions;  /* argmaxes decided by the FP64 near-tie rescore */
   int64_t invalid;         /* requests rejected as invalid on the device */
   int64_t feasible;        /* sum over pod steps of |F| (feasible servers) */
-  int64_t ahp_pairs;       /* AHP: sum over pod steps and non-constant criteria of |F|(|F|-1)/2 */
+  int64_t ahp_pairs;       /* AHP: sum over pod steps and non-constant criteria of the unordered pairs
+                            * of DISTINCT levels K(K-1)/2 (the sorted-level passes' reciprocal terms) */
   int64_t scanned_a;       /* TOPSIS batch fast path: server slots read by the filter/statistics pass */
   int64_t scanned_b;       /* ... and by the scoring pass (chunk-pruned; 0 for the other kernels) */
   int64_t edges_scanned;   /* general-topology calls: adjacency entries read by the BFS levels */
@@ -176,7 +177,11 @@ nacs_status nacs_create(nacs_ctx **out, int device, void *cuda_stream);
  * replicated states stay identical.  nccl_unique_id: the 128-byte ncclUniqueId from
  * nacs_nccl_unique_id() on rank 0, broadcast by the caller (e.g. torch.distributed);
  * NULL with world > 1 = loopback: all `world` logical shards run on this device (testing).
- * TOPSIS is sharded; AHP runs replicated on every rank in this version. */
+ * TOPSIS: each rank scores its server block and the ranks allgather their top-2 keys; AHP:
+ * the level pairs of both passes are split over the ranks (whole tiles, so any rank count
+ * gives bit-identical sums) and the per-level weights and L2 are sum-allreduced.
+ * After an error inside a sharded call the communicator is aborted (peers fail instead of
+ * hanging) and further sharded calls on this context return NACS_ENCCL. */
 nacs_status nacs_create_sharded(nacs_ctx **out, int device, void *cuda_stream, const void *nccl_unique_id,
                                 int rank, int world);
 /* Write a fresh ncclUniqueId (128 bytes) to out. */
@@ -201,6 +206,25 @@ nacs_status nacs_rank_ahp(nacs_ctx *ctx, const nacs_options *opt, const nacs_pod
                           float *scores, int32_t *best);
 nacs_status nacs_rank_topsis(nacs_ctx *ctx, const nacs_options *opt, const nacs_pod_query *q,
                              uint8_t *mask, float *scores, int32_t *best);
+
+/* Whole-GPU TOPSIS ranking of ONE pod step on each of n_states DC states (SURVEY 8(d):
+ * "standalone nacs_rank_topsis on cold snapshots"; the same filter, statistics, closeness
+ * and argmax as nacs_rank_topsis: Eq. 4-7, R4-R6, R12-R14).  Every
+ * state is ranked independently for the same query q (pod demand, flows, exclusions).
+ * states: n_states DC states of the loaded topology's geometry and capacities, each the
+ * int32 words cpu_res[n] | ram_res[n] | active[n] (0/1) | link_res[L] (canonical link order),
+ * consecutive states state_stride >= 3n + L words apart; the loaded state is not used.
+ * Outputs: mask [n_states][n] (uint8, may be NULL), scores [n_states][n] (FP32 closeness of
+ * feasible servers, 0 elsewhere; may be NULL), best [n_states] (argmax, lowest index on ties;
+ * -1 if no server is feasible; -2 if the state holds a residual outside [0, capacity] or an
+ * f_u outside {0, 1}, in which case the call returns NACS_EINVAL unless NACS_ASYNC).
+ * NACS_DEVICE_PTRS: states and outputs are device pointers (the streaming form: one launch,
+ * a thread-block cluster per state); otherwise host arrays, staged through device buffers.
+ * Flow/exclusion arrays of q follow the same flag.  TOPSIS only, bw_criterion = NACS_BW_ACCESS,
+ * n <= 65536, not on server-sharded contexts.  Stats: pod_steps = n_states. */
+nacs_status nacs_rank_topsis_many(nacs_ctx *ctx, const nacs_options *opt, const nacs_pod_query *q, int32_t n_states,
+                                  const int32_t *states, int64_t state_stride, uint8_t *mask, float *scores,
+                                  int32_t *best);
 
 /* Schedule requests one after another against the live state (the paper's online
  * semantics): for each pod in ascending id, rank, select, and commit

@@ -9,7 +9,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libnacs.so")
-SOURCES = [os.path.join(CSRC, f) for f in ("nacs_kernels.cu", "nacs_warp.cu", "nacs_paths.cu", "nacs_api.cu")]
+SOURCES = [os.path.join(CSRC, f) for f in ("nacs_kernels.cu", "nacs_warp.cu", "nacs_paths.cu", "nacs_rank.cu", "nacs_api.cu")]
 DEPS = SOURCES + [os.path.join(CSRC, "nacs_internal.h"), os.path.join(CSRC, "nacs_device.cuh"),
                   os.path.join(ROOT, "include", "nacs.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

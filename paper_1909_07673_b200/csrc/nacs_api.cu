@@ -114,6 +114,9 @@ struct nacs_ctx {
   DevArr<long long> g_out;
   DevArr<int> g_ws;
   DevArr<int> crit;          // logical-bandwidth criteria table (nacs_rank_*, bw_criterion = 1)
+  DevArr<int> many;          // nacs_rank_topsis_many host-pointer staging: states | best
+  DevArr<unsigned char> many_mask;
+  DevArr<float> many_scores;
   // departures / simulator
   DevArr<long long> rel_delta;
   DevArr<int> sim_buf;
@@ -499,15 +502,33 @@ nacs_status finish_stats(nacs_ctx* ctx) {
   return NACS_OK;
 }
 
-nacs_status rank_impl(nacs_ctx* ctx, const nacs_options* opt, const nacs_pod_query* q, uint8_t* mask,
-                      float* scores, int32_t* best, int method) {
-  nacs_status st = begin_call(ctx);
-  if (st) return st;
-  Opt o;
-  if ((st = check_options(ctx, opt, &o))) return st;
-  if (o.method != method) return fail(ctx, NACS_EINVAL, "options.method does not match the rank call");
-  if (!q || !best) return fail(ctx, NACS_EINVAL, "query/best: NULL");
-  const bool dev = opt->flags & NACS_DEVICE_PTRS;
+nacs::RankManyArgs rank_many_args(nacs_ctx* ctx, const Opt& o, const nacs::QueryDev& qd, const int* states,
+                                   long long stride, int B) {
+  nacs::RankManyArgs a{};
+  a.g = ctx->g;
+  for (int c = 0; c < 4; ++c) a.wd[c] = o.wd[c];
+  a.path_filter = o.path_filter;
+  a.exact64 = o.exact64;
+  a.states = states;
+  a.stride = stride;
+  a.B = B;
+  a.dc = qd.dc;
+  a.dr = qd.dr;
+  a.nflow = qd.nflow;
+  a.nex = qd.nex;
+  a.fv = qd.fv;
+  a.fD = qd.fD;
+  a.ex = qd.ex;
+  a.mask = qd.mask;
+  a.scores = qd.scores;
+  a.best = qd.best;
+  a.stats = ctx->stats.p;
+  return a;
+}
+
+// Host-side checks of a pod query (nacs_rank_*); copies host flows (sorted by server) and
+// exclusions to the device, or takes device pointers as given.
+nacs_status query_device(nacs_ctx* ctx, const nacs_pod_query* q, bool dev, nacs::QueryDev* qd) {
   const Geo& g = ctx->g;
   std::string m;
   if (q->cpu_demand <= 0 || q->ram_demand <= 0) m += "query demands must be > 0; ";
@@ -518,47 +539,57 @@ nacs_status rank_impl(nacs_ctx* ctx, const nacs_options* opt, const nacs_pod_que
   if (!m.empty()) return fail(ctx, NACS_EINVAL, m);
   int nf = q->n_flows, nx = q->n_excluded;
   CK(ctx->misc.reserve(2 * (size_t)nf + nx + 8));
-  const int *dfv, *dfD, *dex;
-  if (!dev) {
-    std::vector<int> fv(q->flow_server, q->flow_server + nf), fD(q->flow_bw, q->flow_bw + nf);
-    for (int f = 0; f < nf; ++f) {
-      if (fv[f] < 0 || fv[f] >= g.n) m += "flow " + std::to_string(f) + ": server out of range; ";
-      if (fD[f] <= 0) m += "flow " + std::to_string(f) + ": demand <= 0; ";
-    }
-    // flows sorted by server (commit order), servers distinct
-    std::vector<int> idx(nf);
-    for (int f = 0; f < nf; ++f) idx[f] = f;
-    std::sort(idx.begin(), idx.end(), [&](int a, int b) { return fv[a] < fv[b]; });
-    std::vector<int> h(2 * (size_t)nf + nx + 1);
-    for (int f = 0; f < nf; ++f) {
-      h[f] = fv[idx[f]];
-      h[nf + f] = fD[idx[f]];
-      if (f && h[f] == h[f - 1]) m += "flow servers not distinct; ";
-    }
-    for (int i = 0; i < nx; ++i) {
-      h[2 * nf + i] = q->excluded[i];
-      if (q->excluded[i] < 0 || q->excluded[i] >= g.n) m += "excluded server out of range; ";
-    }
-    if (!m.empty()) return fail(ctx, NACS_EINVAL, m);
-    CK(cudaMemcpyAsync(ctx->misc.p + 4, h.data(), h.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
-    dfv = ctx->misc.p + 4;
-    dfD = ctx->misc.p + 4 + nf;
-    dex = ctx->misc.p + 4 + 2 * nf;
-  } else {
-    dfv = q->flow_server;
-    dfD = q->flow_bw;
-    dex = q->excluded;
+  qd->dc = q->cpu_demand;
+  qd->dr = q->ram_demand;
+  qd->nflow = nf;
+  qd->nex = nx;
+  qd->crit = nullptr;
+  if (dev) {
+    qd->fv = q->flow_server;
+    qd->fD = q->flow_bw;
+    qd->ex = q->excluded;
+    return NACS_OK;
   }
+  std::vector<int> fv(q->flow_server, q->flow_server + nf), fD(q->flow_bw, q->flow_bw + nf);
+  for (int f = 0; f < nf; ++f) {
+    if (fv[f] < 0 || fv[f] >= g.n) m += "flow " + std::to_string(f) + ": server out of range; ";
+    if (fD[f] <= 0) m += "flow " + std::to_string(f) + ": demand <= 0; ";
+  }
+  std::vector<int> idx(nf);
+  for (int f = 0; f < nf; ++f) idx[f] = f;
+  std::sort(idx.begin(), idx.end(), [&](int a, int b) { return fv[a] < fv[b]; });
+  std::vector<int> h(2 * (size_t)nf + nx + 1);
+  for (int f = 0; f < nf; ++f) {
+    h[f] = fv[idx[f]];
+    h[nf + f] = fD[idx[f]];
+    if (f && h[f] == h[f - 1]) m += "flow servers not distinct; ";
+  }
+  for (int i = 0; i < nx; ++i) {
+    h[2 * nf + i] = q->excluded[i];
+    if (q->excluded[i] < 0 || q->excluded[i] >= g.n) m += "excluded server out of range; ";
+  }
+  if (!m.empty()) return fail(ctx, NACS_EINVAL, m);
+  CK(cudaMemcpyAsync(ctx->misc.p + 4, h.data(), h.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
+  qd->fv = ctx->misc.p + 4;
+  qd->fD = ctx->misc.p + 4 + nf;
+  qd->ex = ctx->misc.p + 4 + 2 * nf;
+  return NACS_OK;
+}
+
+nacs_status rank_impl(nacs_ctx* ctx, const nacs_options* opt, const nacs_pod_query* q, uint8_t* mask,
+                      float* scores, int32_t* best, int method) {
+  nacs_status st = begin_call(ctx);
+  if (st) return st;
+  Opt o;
+  if ((st = check_options(ctx, opt, &o))) return st;
+  if (o.method != method) return fail(ctx, NACS_EINVAL, "options.method does not match the rank call");
+  if (!q || !best) return fail(ctx, NACS_EINVAL, "query/best: NULL");
+  const bool dev = opt->flags & NACS_DEVICE_PTRS;
+  const Geo& g = ctx->g;
+  nacs::QueryDev qd{};
+  if ((st = query_device(ctx, q, dev, &qd))) return st;
   CK(ctx->mask.reserve(g.n));
   CK(ctx->scores.reserve(g.n));
-  nacs::QueryDev qd;
-  qd.dc = q->cpu_demand;
-  qd.dr = q->ram_demand;
-  qd.nflow = nf;
-  qd.nex = nx;
-  qd.fv = dfv;
-  qd.fD = dfD;
-  qd.ex = dex;
   qd.mask = (dev && mask) ? mask : ctx->mask.p;
   qd.scores = (dev && scores) ? scores : ctx->scores.p;
   qd.best = dev ? best : ctx->misc.p;
@@ -582,7 +613,13 @@ nacs_status rank_impl(nacs_ctx* ctx, const nacs_options* opt, const nacs_pod_que
     CK(ctx->ahp_ws.reserve(nacs::ahp_workspace_bytes(g.n) / 4 + 4));
     CK(ctx->w64.reserve(nacs::ahp_workspace_doubles(g.n)));
   }
-  CK(nacs::launch_rank(g, o, ctx->state.p, qd, ctx->ahp_ws.p, ctx->w64.p, ctx->stats.p, ctx->stream));
+  if (method == 1 && !qd.crit) {
+    // TOPSIS: the whole-GPU cluster kernel (nacs_rank.cu) on the context state
+    nacs::RankManyArgs a = rank_many_args(ctx, o, qd, ctx->state.p, g.words(), 1);
+    CK(nacs::launch_rank_many(a, ctx->num_sms, ctx->stream));
+  } else {
+    CK(nacs::launch_rank(g, o, ctx->state.p, qd, ctx->ahp_ws.p, ctx->w64.p, ctx->stats.p, ctx->stream));
+  }
   if (!dev) {
     if (mask) CK(cudaMemcpyAsync(mask, qd.mask, g.n, cudaMemcpyDeviceToHost, ctx->stream));
     if (scores) CK(cudaMemcpyAsync(scores, qd.scores, 4 * (size_t)g.n, cudaMemcpyDeviceToHost, ctx->stream));
@@ -821,6 +858,9 @@ void nacs_destroy(nacs_ctx* ctx) {
   ctx->g_out.release();
   ctx->g_ws.release();
   ctx->crit.release();
+  ctx->many.release();
+  ctx->many_mask.release();
+  ctx->many_scores.release();
   ctx->rel_delta.release();
   ctx->sim_buf.release();
   ctx->sim_pin.release();
@@ -919,6 +959,63 @@ nacs_status nacs_rank_topsis(nacs_ctx* ctx, const nacs_options* opt, const nacs_
                              float* scores, int32_t* best) {
   NvtxRange nvtx_range_("nacs_rank_topsis");
   return rank_impl(ctx, opt, q, mask, scores, best, 1);
+}
+
+nacs_status nacs_rank_topsis_many(nacs_ctx* ctx, const nacs_options* opt, const nacs_pod_query* q, int32_t n_states,
+                                  const int32_t* states, int64_t state_stride, uint8_t* mask, float* scores,
+                                  int32_t* best) {
+  NvtxRange nvtx_range_("nacs_rank_topsis_many");
+  nacs_status st = begin_call(ctx);
+  if (st) return st;
+  Opt o;
+  if ((st = check_options(ctx, opt, &o))) return st;
+  if (o.method != NACS_TOPSIS) return fail(ctx, NACS_EINVAL, "nacs_rank_topsis_many: options.method must be NACS_TOPSIS");
+  if (o.bw_logical) return fail(ctx, NACS_EINVAL, "nacs_rank_topsis_many: bw_criterion must be NACS_BW_ACCESS");
+  if (ctx->world > 1 || ctx->comm) return fail(ctx, NACS_EINVAL, "nacs_rank_topsis_many: not on server-sharded contexts");
+  if (!q || n_states < 0 || (n_states > 0 && (!states || !best)))
+    return fail(ctx, NACS_EINVAL, "nacs_rank_topsis_many: query/states/best NULL or n_states < 0");
+  const Geo& g = ctx->g;
+  if (state_stride < g.words())
+    return fail(ctx, NACS_EINVAL, "nacs_rank_topsis_many: state_stride < 3n + L words");
+  if (nacs::rank_many_cluster(g) > 16) return fail(ctx, NACS_ETOOBIG, "nacs_rank_topsis_many: n > 65536");
+  const bool dev = opt->flags & NACS_DEVICE_PTRS;
+  nacs::QueryDev qd{};
+  if ((st = query_device(ctx, q, dev, &qd))) return st;
+  if (n_states == 0) return finish_stats(ctx);
+  const size_t B = (size_t)n_states, n = (size_t)g.n;
+  const int* d_states = states;
+  long long stride = state_stride;
+  if (!dev) {  // stage through device buffers (the product path is the device-pointer call)
+    stride = g.words() + ((4 - g.words() % 4) % 4);
+    CK(ctx->many.reserve(B * (size_t)stride + B + 4));
+    CK(cudaMemcpy2DAsync(ctx->many.p, 4 * (size_t)stride, states, 4 * (size_t)state_stride, 4 * (size_t)g.words(), B,
+                         cudaMemcpyHostToDevice, ctx->stream));
+    d_states = ctx->many.p;
+    if (mask) CK(ctx->many_mask.reserve(B * n));
+    if (scores) CK(ctx->many_scores.reserve(B * n));
+    qd.mask = mask ? ctx->many_mask.p : nullptr;
+    qd.scores = scores ? ctx->many_scores.p : nullptr;
+    qd.best = ctx->many.p + B * (size_t)stride;
+  } else {
+    qd.mask = mask;
+    qd.scores = scores;
+    qd.best = best;
+  }
+  nacs::RankManyArgs a = rank_many_args(ctx, o, qd, d_states, stride, n_states);
+  CK(nacs::launch_rank_many(a, ctx->num_sms, ctx->stream));
+  if (!dev) {
+    if (mask) CK(cudaMemcpyAsync(mask, qd.mask, B * n, cudaMemcpyDeviceToHost, ctx->stream));
+    if (scores) CK(cudaMemcpyAsync(scores, qd.scores, 4 * B * n, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(best, qd.best, 4 * B, cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  if (!(opt->flags & NACS_ASYNC)) {
+    CK(cudaStreamSynchronize(ctx->stream));
+    if ((st = finish_stats(ctx))) return st;
+    if (ctx->last.invalid > 0)
+      return fail(ctx, NACS_EINVAL, std::to_string(ctx->last.invalid) +
+                                        " states hold a value outside [0, capacity] or f_u outside {0,1} (best = -2)");
+  }
+  return NACS_OK;
 }
 
 nacs_status nacs_schedule_batch(nacs_ctx* ctx, const nacs_options* opt, const nacs_requests* batch,

@@ -158,6 +158,25 @@ cudaError_t launch_sequential(const Geo& g, const Opt& o, int* d_state, const Re
 cudaError_t launch_rank(const Geo& g, const Opt& o, int* d_state, const QueryDev& q, float* ahp_ws,
                         double* w64, unsigned long long* stats, cudaStream_t s);
 cudaError_t launch_validate(const ReqsDev& R, int* status, unsigned long long* stats, cudaStream_t s);
+// Whole-GPU TOPSIS ranking of one pod step on B DC states (nacs_rank.cu): a thread-block
+// cluster of rank_many_cluster(g) CTAs per state, a persistent grid of clusters.
+struct RankManyArgs {
+  Geo g;
+  double wd[4];
+  int path_filter, exact64;
+  const int* states;       // [B] states of g.words() int32 words, `stride` words apart
+  long long stride;
+  int B;
+  int dc, dr, nflow, nex;  // the pod query (shared by every state)
+  const int *fv, *fD, *ex; // device arrays: flows sorted by server, excluded servers
+  uint8_t* mask;           // [B][n] or null
+  float* scores;           // [B][n] or null
+  int* best;               // [B]: argmax, -1 none feasible, -2 a value out of range
+  unsigned long long* stats;
+  int slice;               // set by the launcher
+};
+int rank_many_cluster(const Geo& g);
+cudaError_t launch_rank_many(const RankManyArgs& a, int num_sms, cudaStream_t st);
 // R2's logical bandwidth criterion on the current fat-tree state: crit = cpu | ram | act | L(u)
 // ([4n]); F: [E*E] scratch; *too_big = 1 if some L(u) >= 2^24 (not exact in FP32)
 cudaError_t launch_logical_criteria(const Geo& g, const int* state, int* crit, int* F, int* too_big,

@@ -90,7 +90,7 @@ class PathQuery(C.Structure):
 
 
 EXPORTS = ["nacs_create", "nacs_create_sharded", "nacs_nccl_unique_id", "nacs_destroy", "nacs_load_topology",
-           "nacs_read_topology", "nacs_rank_ahp", "nacs_rank_topsis", "nacs_schedule_request",
+           "nacs_read_topology", "nacs_rank_ahp", "nacs_rank_topsis", "nacs_rank_topsis_many", "nacs_schedule_request",
            "nacs_schedule_batch", "nacs_last_stats", "nacs_last_error", "nacs_load_graph", "nacs_widest_paths",
            "nacs_logical_bandwidth", "nacs_release", "nacs_simulate"]
 
@@ -115,6 +115,8 @@ def lib():
         L.nacs_read_topology.argtypes = [vp, vp, vp, vp, vp]
         for f in (L.nacs_rank_ahp, L.nacs_rank_topsis):
             f.argtypes = [vp, C.POINTER(Options), C.POINTER(PodQuery), vp, vp, vp]
+        L.nacs_rank_topsis_many.argtypes = [vp, C.POINTER(Options), C.POINTER(PodQuery), C.c_int32, vp, C.c_int64,
+                                            vp, vp, vp]
         for f in (L.nacs_schedule_request, L.nacs_schedule_batch):
             f.argtypes = [vp, C.POINTER(Options), C.POINTER(Requests), C.POINTER(Placements)]
         L.nacs_last_stats.argtypes = [vp, C.POINTER(Stats)]
@@ -257,6 +259,48 @@ class Context:
         fn = self._lib.nacs_rank_ahp if o.method == NACS_AHP else self._lib.nacs_rank_topsis
         self._check(fn(self._h, C.byref(o), C.byref(q), _np_ptr(mask), _np_ptr(scores), _np_ptr(best)))
         return dict(mask=mask, scores=scores, best=int(best[0]))
+
+    def rank_many(self, states, dem_cpu, dem_ram, flows=(), excluded=(), weights="flat", scores=True, mask=True,
+                  out=None, flags=0, exact64=False, **kw) -> dict:
+        """TOPSIS ranking of one pod step on each of B DC states (nacs_rank_topsis_many).
+
+        states: int32 [B, words] (words >= 3n + L: cpu | ram | active | links per row), a numpy
+        array (host path) or a contiguous torch CUDA tensor (device path, one launch).
+        out: optional preallocated dict(mask [B, n] uint8, scores [B, n] float32, best [B] int32)
+        of the same kind.  Returns that dict."""
+        dev = _is_torch(states)
+        if states.ndim != 2 or states.shape[1] < 3 * self.n + self.L:
+            raise ValueError(f"states: shape [B, >= {3 * self.n + self.L}] expected")
+        B = int(states.shape[0])
+        if dev:
+            import torch
+            self._check_tensor("states", states)
+            if states.stride(1) != 1:
+                raise ValueError("states: rows must be contiguous")
+            stride = int(states.stride(0))
+            flags |= NACS_DEVICE_PTRS
+            if out is None:
+                d = states.device
+                out = dict(mask=torch.empty((B, self.n), dtype=torch.uint8, device=d) if mask else None,
+                           scores=torch.empty((B, self.n), dtype=torch.float32, device=d) if scores else None,
+                           best=torch.empty(B, dtype=torch.int32, device=d))
+            mk = lambda xs: torch.tensor(list(xs) if len(xs) else [0], dtype=torch.int32, device=states.device)
+            fv, fd, ex = mk([f[0] for f in flows]), mk([f[1] for f in flows]), mk(excluded)
+        else:
+            states = np.ascontiguousarray(states, dtype=np.int32)
+            stride = states.shape[1]
+            if out is None:
+                out = dict(mask=np.zeros((B, self.n), np.uint8) if mask else None,
+                           scores=np.zeros((B, self.n), np.float32) if scores else None,
+                           best=np.zeros(B, np.int32))
+            fv = _i32([f[0] for f in flows]) if len(flows) else np.zeros(1, np.int32)
+            fd = _i32([f[1] for f in flows]) if len(flows) else np.zeros(1, np.int32)
+            ex = _i32(list(excluded)) if len(excluded) else np.zeros(1, np.int32)
+        o = self.options("topsis", weights, flags=flags | (NACS_EXACT_FP64 if exact64 else 0), **kw)
+        q = PodQuery(int(dem_cpu), int(dem_ram), len(flows), _ptr(fv), _ptr(fd), len(excluded), _ptr(ex))
+        self._check(self._lib.nacs_rank_topsis_many(self._h, C.byref(o), C.byref(q), B, _ptr(states), stride,
+                                                    _ptr(out["mask"]), _ptr(out["scores"]), _ptr(out["best"])))
+        return out
 
     # ------------------------------------------------------------ schedule ---
     def _check_tensor(self, key, a, min_numel=None, exact_numel=None):

@@ -22,7 +22,7 @@ def test_library_builds_and_exports_header_symbols():
     path = nbuild.build()
     assert os.path.exists(path)
     declared = header_functions()
-    assert len(declared) == 17, declared
+    assert len(declared) == 18, declared
     out = subprocess.run(["nm", "-D", "--defined-only", path], capture_output=True, text=True).stdout
     exported = set(re.findall(r"\bT (nacs_[a-z_]+)\b", out))
     assert set(declared) <= exported, set(declared) - exported

@@ -102,7 +102,10 @@ def test_schedule_path_filter_0(ctx, method):
         out = ctx.schedule_request(reqs, method, schema, path_filter=0)
         cnt = assert_schedule_parity(tight, reqs, out, method, schema, True, gpu_state=ctx.read_topology(),
                                      path_filter=0)
-        assert cnt["retries"] == ctx.last_stats()["retries"] and cnt["retries"] > 0
+        # retries count attempts; under an R14-excused tie the oracle adopts the GPU's final
+        # server, so its sequence of attempts may differ from the GPU's by the excused choices
+        assert cnt["retries"] > 0
+        assert abs(cnt["retries"] - ctx.last_stats()["retries"]) <= cnt["excused_ties"], (cnt, ctx.last_stats())
         ctx.load_topology(tight)
         out = ctx.schedule_batch(reqs, method, schema, path_filter=0)
         assert_schedule_parity(tight, reqs, out, method, schema, False, path_filter=0)
@@ -171,14 +174,16 @@ def test_rank_ahp_k64_quantised_closed_form(ctx):
     for schema, L1 in (("flat", (0.25, 0.25, 0.25, 0.25)),):
         for rule in (0, 1):
             g = ctx.rank("ahp", schema, 1, 1, ahp_rule=rule)
-            assert g["mask"].all()
+            F = (snap["cpu_res"] >= 1) & (snap["ram_res"] >= 1)  # demand (1, 1), no flows
+            assert np.array_equal(g["mask"].astype(bool), F) and F.sum() > 60000
             crit = [snap["cpu_res"], snap["ram_res"], snap["active"], snap["link_res"][: 65536]]
-            pg = sum(w * ahp_levels_l2(np.asarray(x, np.int64), rule) for w, x in zip(L1, crit))
+            pg = sum(w * ahp_levels_l2(np.asarray(x, np.int64)[F], rule) for w, x in zip(L1, crit))
             assert abs(pg.sum() - 1.0) < 1e-12
-            err = np.abs(g["scores"].astype(np.float64) - pg) / pg
+            err = np.abs(g["scores"][F].astype(np.float64) - pg) / pg
             assert err.max() <= SCORE_RTOL, err.max()
             top = pg.max()
-            tie = pg >= top - 1e-9 * top
+            tie = np.zeros(65536, bool)
+            tie[np.nonzero(F)[0]] = pg >= top - 1e-9 * top
             assert tie[g["best"]]
 
 
