@@ -890,7 +890,7 @@ nacs_status nacs_load_topology(nacs_ctx* ctx, const nacs_topology* t) {
   g.cpu_cap = t->cpu_cap;
   g.ram_cap = t->ram_cap;
   g.link_cap = t->link_cap;
-  g.magic_h = (unsigned)((((unsigned long long)1 << 32) + g.h - 1) / g.h);
+  g.magic_h = g.h == 1 ? 0u : (unsigned)((((unsigned long long)1 << 32) + g.h - 1) / g.h);  // div_h
   std::vector<int> h((size_t)g.words());
   int n = g.n;
   int bad_cpu = 0, bad_ram = 0, bad_act = 0, bad_link = 0;

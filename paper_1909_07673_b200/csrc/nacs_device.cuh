@@ -28,7 +28,9 @@ __device__ __forceinline__ float rsqrt_approx(float x) {
 __device__ __forceinline__ float scaled_diff(float s, float s2p23, int d) {
   return fmaf(s, __int_as_float(0x4B000000 | d), -s2p23);
 }
-__device__ __forceinline__ unsigned div_h(unsigned x, unsigned magic) { return __umulhi(x, magic); }
+// x / h for x < 2^24 with magic = ceil(2^32 / h); h = 1 (k = 2) has no 32-bit magic and is
+// stored as magic = 0
+__device__ __forceinline__ unsigned div_h(unsigned x, unsigned magic) { return magic ? __umulhi(x, magic) : x; }
 
 // FP32 error-bound constants.  u = 2^-24.
 // TOPSIS: |r32 - r| <= 20u; ambiguous top-2 gap <= 2^-17 (> 4 x 40u).

@@ -21,7 +21,7 @@ constexpr int ULOG_CAP = 3 * MAXC + 6 * MAXV + 2 * MAXC + 6 * MAXV + 64;
 struct Geo {
   int k, h, n, E, L;
   int cpu_cap, ram_cap, link_cap;
-  unsigned magic_h;  // ceil(2^32 / h): x / h == __umulhi(x, magic_h) for x < 2^24
+  unsigned magic_h;  // ceil(2^32 / h): x / h == __umulhi(x, magic_h) for x < 2^24; 0 for h = 1 (div_h)
   __host__ __device__ int words() const { return 3 * n + L; }
 };
 

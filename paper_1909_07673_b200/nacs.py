@@ -284,7 +284,7 @@ class Context:
                 out = dict(mask=torch.empty((B, self.n), dtype=torch.uint8, device=d) if mask else None,
                            scores=torch.empty((B, self.n), dtype=torch.float32, device=d) if scores else None,
                            best=torch.empty(B, dtype=torch.int32, device=d))
-            mk = lambda xs: torch.tensor(list(xs) if len(xs) else [0], dtype=torch.int32, device=states.device)
+            mk = lambda xs: torch.tensor(list(xs), dtype=torch.int32, device=states.device) if len(xs) else None
             fv, fd, ex = mk([f[0] for f in flows]), mk([f[1] for f in flows]), mk(excluded)
         else:
             states = np.ascontiguousarray(states, dtype=np.int32)

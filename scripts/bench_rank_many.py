@@ -29,7 +29,8 @@ def main():
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     ctx = nacs.Context(0, stream)
-    for k, B in ((32, 4096), (64, 512), (16, 16384)):
+    for variant, k, B in [(v, k, B) for v in ("occ", "stream", "many") for k, B in ((32, 4096), (64, 512), (16, 16384))]:
+        os.environ["NACS_RANK_KERNEL"] = variant
         snap = gen.snapshot(k, 4)
         ctx.load_topology(snap)
         n = k ** 3 // 4
@@ -48,7 +49,7 @@ def main():
         torch.cuda.synchronize()
         ms = ev[0].elapsed_time(ev[1]) / reps
         byts = B * n * (16 + 4)
-        print(f"k={k} B={B} n={n}: {ms:.3f} ms/call, {B * n / ms / 1e6:.3e} servers/s, "
+        print(f"{variant} k={k} B={B} n={n}: {ms:.3f} ms/call, {B * n / ms * 1e3:.3e} servers/s, "
               f"{byts / ms / 1e6:.1f} GB/s algorithmic (16 B read + 4 B score per server)")
         torch.cuda.synchronize()
         ctx.rank_many(st[:8], 1500, 3000)
