@@ -631,6 +631,29 @@ __global__ void __launch_bounds__(RM_T, 1) k_rank_many(RankManyArgs a) {
   cl.sync();  // no CTA may leave while another still reads its shared memory
 }
 
+// Reduce 32 lanes' WStats (exact integers, any order); the result is valid in every lane.
+__device__ __forceinline__ void ws_warp_reduce(WStats& x) {
+  x.nf = (int)__reduce_add_sync(NACS_FULL, (unsigned)x.nf);
+  x.nact = (int)__reduce_add_sync(NACS_FULL, (unsigned)x.nact);
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    x.mn[c] = __reduce_min_sync(NACS_FULL, x.mn[c]);
+    x.mx[c] = __reduce_max_sync(NACS_FULL, x.mx[c]);
+    x.q[c] = warp_sum_u64(x.q[c]);
+  }
+#pragma unroll
+  for (int c = 0; c < 4; ++c) x.vmax[c] = __reduce_max_sync(NACS_FULL, x.vmax[c]);
+}
+__device__ __forceinline__ WStats ws_identity() {
+  WStats x;
+  x.nf = 0; x.nact = 0;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) { x.mn[c] = UINT_MAX; x.mx[c] = 0; x.q[c] = 0; }
+#pragma unroll
+  for (int c = 0; c < 4; ++c) x.vmax[c] = 0;
+  return x;
+}
+
 // =====================================================================================
 // Occupancy-2 streaming kernel (16-byte aligned states, no flows/exclusions: the cold
 // snapshot stream of §8(d)).  256 threads x 16 servers per CTA (slice of 4096), TWO CTAs of
@@ -705,13 +728,7 @@ __device__ __forceinline__ RoKey rokey_merge(RoKey a, RoKey b) {
   return r;
 }
 
-__device__ __forceinline__ void ws_reset(WStats& w) {
-  w.nf = 0; w.nact = 0;
-#pragma unroll
-  for (int c = 0; c < 3; ++c) { w.mn[c] = UINT_MAX; w.mx[c] = 0; w.q[c] = 0; }
-#pragma unroll
-  for (int c = 0; c < 4; ++c) w.vmax[c] = 0;
-}
+__device__ __forceinline__ void ws_reset(WStats& w) { w = ws_identity(); }
 
 __device__ void ro_params(const RankManyArgs& a, const RmThread& t, RoShared& sm, cg::cluster_group& cl, int p) {
   WStats x = t.lane < t.C ? *cl.map_shared_rank(&sm.cs[p], t.lane) : ws_identity();
