@@ -56,8 +56,10 @@ def parse():
     ap.add_argument("--no-once", action="store_true")
     ap.add_argument("--no-variants", action="store_true")
     ap.add_argument("--no-paths", action="store_true")
-    ap.add_argument("--no-sim", action="store_true")
+    ap.add_argument("--sim", action="store_true", help="also run the E2 simulator campaign (context only)")
     ap.add_argument("--no-c5", action="store_true")
+    ap.add_argument("--no-matrix", action="store_true")
+    ap.add_argument("--no-cold", action="store_true")
     return ap.parse_args()
 
 
@@ -147,16 +149,17 @@ class ClockSampler:
                 "source": "nvml" if self._nvml is not None else "nvidia-smi"}
 
 
-def workload(rank: int, method: str):
-    """Snapshot and this rank's request shard (weak scaling: 100k C4 requests per rank)."""
-    if method == "topsis":
-        snap = gen.snapshot(32, gen.CONFIG_SEEDS["C4"])
-        reqs = gen.requests(gen.CONFIG_REQUESTS["C4"], gen.CONFIG_SEEDS["C4"] + 1000 + 7919 * rank)
-        name = "C4: fat-tree k=32 (8192 servers), 100k requests/GPU of 4-20 containers, TOPSIS Flat, batch"
-    else:
-        snap = gen.snapshot(16, gen.CONFIG_SEEDS["C3"])
-        reqs = gen.requests(gen.CONFIG_REQUESTS["C3"], gen.CONFIG_SEEDS["C3"] + 1000 + 7919 * rank)
-        name = "C3: fat-tree k=16 (1024 servers), 10k requests/GPU, AHP Flat, batch"
+CFG_K = {"C2": 8, "C3": 16, "C4": 32}
+
+
+def workload(rank: int, cfg: str, n_req: int | None = None):
+    """Snapshot and this rank's request shard of a batch config (weak scaling: the config's
+    request count per rank, or its first n_req requests)."""
+    k = CFG_K[cfg]
+    snap = gen.snapshot(k, gen.CONFIG_SEEDS[cfg])
+    R = gen.CONFIG_REQUESTS[cfg] if n_req is None else n_req
+    reqs = gen.requests(R, gen.CONFIG_SEEDS[cfg] + 1000 + 7919 * rank)
+    name = f"{cfg}: fat-tree k={k} ({k ** 3 // 4} servers), {R} requests/GPU of 4-20 containers, batch"
     return snap, reqs, name
 
 
@@ -179,6 +182,54 @@ def quality(reqs: dict, out: dict) -> dict:
     np.maximum.at(pods, req_of_c, reqs["pod_of"].astype(np.int64) + 1)
     return {"acceptance": float(acc_r.mean()) if R else None, "accepted_pods": int(pods[acc_r].sum()),
             "U_i": float(ui.mean()) if ui.size else None, "U_ij": float(uij.mean()) if uij.size else None}
+
+
+def alu_peak_tops(mhz: float) -> float:
+    """FP32/INT issue roof: 148 SMs x 4 schedulers x 32 lanes per clock (T thread-instr/s)."""
+    return 148 * 128 * mhz * 1e6 / 1e12
+
+
+# ncu issue-slot utilisation of the TOPSIS batch kernel in the bench launch configuration
+# (profiles/r01_summary.md: k_batch_warp, C4, 100k requests)
+TOPSIS_NCU_ISSUE = 0.411
+
+
+def topsis_roofline(st: dict, kernel_ms: float, mhz: float, pk_kind: str) -> dict:
+    """Method-equivalent ALU throughput of the TOPSIS batch kernels: SURVEY 8(d)'s algorithmic op
+    count (3 per server ranked + 45 per feasible server) per second against the issue roof.  The
+    kernel reads only `slots_read_frac` of the slots a two-pass scan reads (whole-tile statistics,
+    pruned scoring), so this is a method-equivalent rate; `ncu_issue_slots` is how busy the
+    SMs actually were (ncu, profiles/r01_summary.md)."""
+    ops = TOPSIS_OPS_ALL * st["servers_ranked"] + TOPSIS_OPS_FEAS * st["feasible"]
+    achieved = ops / (kernel_ms / 1e3) / 1e12
+    peak = alu_peak_tops(mhz)
+    traffic = None
+    if os.path.exists(TRAFFIC):
+        traffic = json.load(open(TRAFFIC)).get("k_batch_warp", {}).get("dram_bytes_per_launch")
+    read_frac = (st["scanned_a"] + st["scanned_b"]) / max(1, 2 * st["servers_ranked"])
+    return {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Top/s", "frac": achieved / peak,
+            "traffic": traffic, "kernel": "k_batch_warp<TOPSIS> (whole call)",
+            "ops": "method-algorithmic: 3 per server ranked + 45 per feasible server (SURVEY 8(d))",
+            "slots_read_frac": read_frac, "ncu_issue_slots": TOPSIS_NCU_ISSUE,
+            "peak_source": f"148 SMs x 128 lanes x {mhz:.0f} MHz (sm_max_mhz, {pk_kind})"}
+
+
+# Thread-instructions per EXECUTED AHP term: the sorted-level passes evaluate each unordered pair
+# of distinct levels once per pass, 4 terms sharing one MUFU.RCP in ~15 instructions (DESIGN §5)
+AHP_INSTR_PER_TERM = 15 / 4
+
+
+def ahp_roofline(st: dict, kernel_ms: float, mhz: float) -> dict:
+    """AHP against the issue-slot bound of what the kernel executes: 2 passes x the unordered
+    pairs of distinct levels per non-constant criterion (nacs_stats.ahp_pairs) x ~15/4
+    instructions per term, over the 148 x 128 lane-issue roof."""
+    terms = 2 * st["ahp_pairs"]
+    achieved = terms * AHP_INSTR_PER_TERM / (kernel_ms / 1e3) / 1e12
+    peak = alu_peak_tops(mhz)
+    return {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "T instr/s", "frac": achieved / peak,
+            "terms_per_step": terms, "kernel": "k_batch<AHP> (sorted-level passes)",
+            "ops": "2 passes x level pairs x 15/4 instructions per term (4-term groups, one MUFU.RCP each)",
+            "peak_source": f"148 SMs x 128 lanes x {mhz:.0f} MHz"}
 
 
 def run_ours(args, rank, world, local):
@@ -218,16 +269,16 @@ def run_ours(args, rank, world, local):
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
         return float(t.item())
 
-    def measure(method, **kw):
-        snap, reqs, name = workload(rank, method)
+    def measure(method, schema="flat", cfg="C4", n_req=None, **kw):
+        snap, reqs, name = workload(rank, cfg, n_req)
+        name = name.replace("batch", f"{method.upper()} {schema.capitalize()}, batch")
         ctx.load_topology(snap)
         d = {k: (torch.from_numpy(v).to(dev) if isinstance(v, np.ndarray) else v) for k, v in reqs.items()}
         out = ctx._alloc_out(reqs, True)[0]
         for _ in range(args.warmup):  # warm-up includes the flush (its first launch loads torch's module)
             flush.zero_()
-            ctx.schedule_batch(d, method, "flat", out=out, flags=nacs.NACS_ASYNC, **kw)
+            ctx.schedule_batch(d, method, schema, out=out, flags=nacs.NACS_ASYNC, **kw)
         torch.cuda.synchronize(dev)
-        st0 = ctx.last_stats()
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
         sampler = ClockSampler(local)
         barrier()
@@ -238,7 +289,7 @@ def run_ours(args, rank, world, local):
             for i in range(args.steps):
                 flush.zero_()
                 ev[i][0].record(stream)
-                ctx.schedule_batch(d, method, "flat", out=out, flags=nacs.NACS_ASYNC, **kw)
+                ctx.schedule_batch(d, method, schema, out=out, flags=nacs.NACS_ASYNC, **kw)
                 ev[i][1].record(stream)
             t1.record(stream)
             torch.cuda.synchronize(dev)
@@ -257,8 +308,10 @@ def run_ours(args, rank, world, local):
                    clocks=sampler.summary(), snap=snap, reqs=reqs, out=out, d=d)
         return res
 
-    topsis = measure("topsis")
-    ahp = None if args.no_ahp else measure("ahp")
+    topsis = measure("topsis", "flat", "C4")
+    ahp = None if args.no_ahp else measure("ahp", "flat", "C3")
+    # AHP and TOPSIS x {Flat, Clustering, Network} (T4 P:315-331) at C3 and C4
+    matrix = None if args.no_matrix else measure_matrix(args, measure, topsis, ahp, pk)
     # rank once per request, pods walk the first pod step's order
     once = None if args.no_once else measure("topsis", rank_once=True)
     # the paper-literal variant flags as benchmarked modes
@@ -270,7 +323,7 @@ def run_ours(args, rank, world, local):
                                ("ahp_l1_weights (R10 flag)", "ahp", {"l1_mode": 1})):
             if meth == "ahp" and args.no_ahp:
                 continue
-            v = measure(meth, **kw)
+            v = measure(meth, "flat", "C4" if meth == "topsis" else "C3", **kw)
             variants[name] = {"workload": v["name"], "value": v["value"], "unit": "pods/s",
                               "ms_per_step": v["ms_per_step"]}
         # R2's alternative (bw_criterion = logical): one pod step through nacs_rank_topsis on the
@@ -296,42 +349,27 @@ def run_ours(args, rank, world, local):
     # C5 (BASELINE configs[4]): k=64, sequential scheduling with the servers sharded over the ranks
     c5 = None if args.no_c5 else measure_c5(args, rank, world, local, stream, max_over_ranks)
 
-    # the E2 campaign through the discrete-event simulator (T5-shaped rows)
-    sim = None if (args.no_sim or rank != 0) else measure_sim(ctx)
+    # C2 sequential (live state, commits) for both methods
+    c2 = None if args.no_matrix else measure_c2(args, ctx, stream, max_over_ranks)
+    # standalone nacs_rank_topsis on cold snapshots against HBM
+    cold = None if args.no_cold else measure_cold(args, ctx, dev, stream, flush, barrier, max_over_ranks,
+                                                  sum_over_ranks, pk, pk_kind)
+    # the E2 campaign through the discrete-event simulator (T5-shaped rows):
+    # context only (the paper's T5 numbers are not a target), so only with --sim
+    sim = measure_sim(ctx) if (args.sim and rank == 0) else None
 
-    # roofline of the dominant kernel (k_batch<TOPSIS>): issue-bound ALU
+    # roofline of the dominant kernel (k_batch_warp<TOPSIS>): issue-bound ALU
     clocks = topsis["clocks"]
     mhz = float(pk.get("sm_max_mhz", 1965.0))
-    alu_peak = 148 * 128 * mhz * 1e6 / 1e12  # Top/s: 4 schedulers x 32 lanes per SM per clock
-    st = topsis["stats"]
-    ops = TOPSIS_OPS_ALL * st["servers_ranked"] + TOPSIS_OPS_FEAS * st["feasible"]
-    achieved = ops / (topsis["kernel_ms"] / 1e3) / 1e12
-    traffic = None
-    if os.path.exists(TRAFFIC):
-        traffic = json.load(open(TRAFFIC)).get("k_batch_warp", {}).get("dram_bytes_per_launch")
-    # the kernel reads only part of the slots (whole-chunk statistics, pruned scoring):
-    # the fraction of the 2 x servers_ranked slot reads a full two-pass scan would make
-    read_frac = (st["scanned_a"] + st["scanned_b"]) / max(1, 2 * st["servers_ranked"])
-    roofline = {"bound": "alu", "achieved": achieved, "peak": alu_peak, "unit": "Top/s",
-                "frac": achieved / alu_peak, "traffic": traffic, "kernel": "k_batch_warp<TOPSIS> (whole call)",
-                "ops": "method-algorithmic: 3 per server ranked + 45 per feasible server (SURVEY 8(d))",
-                "slots_read_frac": read_frac,
-                "peak_source": f"148 SMs x 128 lanes x {mhz:.0f} MHz (sm_max_mhz, {pk_kind})"}
+    roofline = topsis_roofline(topsis["stats"], topsis["kernel_ms"], mhz, pk_kind)
 
     ahp_obj = None
     if ahp is not None:
         sa = ahp["stats"]
-        rcp = 2 * sa["ahp_pairs"]  # two passes; pairs = sum over non-constant criteria of nf(nf-1)/2
-        mufu_peak = 16 * 148 * mhz * 1e6 / 1e12
-        ach = rcp / (ahp["kernel_ms"] / 1e3) / 1e12
         ahp_obj = {"workload": ahp["name"], "value": ahp["value"], "unit": "pods/s",
                    "servers_ranked_per_s": ahp["servers_ranked_per_s"], "ms_per_step": ahp["ms_per_step"],
                    "pod_steps_per_step": ahp["pod_steps_per_step"], "fp64_decisions": sa["fp64_decisions"],
-                   "quality": ahp["quality"],
-                   "roofline": {"bound": "mufu", "achieved": ach, "peak": mufu_peak, "unit": "T rcp/s",
-                                "frac": ach / mufu_peak, "kernel": "k_batch<AHP>",
-                                "peak_source": f"16 MUFU.RCP/clk/SM (measured 15.9: scripts/micro/mufu_rcp.cu, "
-                                               f"profiles/r01_micro_mufu_rcp.txt) x 148 x {mhz:.0f} MHz"}}
+                   "quality": ahp["quality"], "roofline": ahp_roofline(sa, ahp["kernel_ms"], mhz)}
 
     # e2e: the public API with host buffers (staging copies inside the timed region)
     e2e = None
@@ -371,13 +409,16 @@ def run_ours(args, rank, world, local):
                 "vs_baseline": None, "dtype": "f32", "data": "synthetic",
                 "config": {"workload": topsis["name"], "k": 32, "servers": topsis["n"],
                            "requests_per_gpu": gen.CONFIG_REQUESTS["C4"], "method": "topsis", "schema": "flat",
-                           "parallelism": f"request-sharded x{world}", "l2": "flushed between steps (256 MB write)"},
+                           "parallelism": f"dp{world}: each rank schedules its own seeded 100k-request shard "
+                                          "(requests independent, R21; no data-path collective)",
+                           "l2": "flushed between steps (256 MB write)"},
                 "servers_ranked_per_s": topsis["servers_ranked_per_s"],
                 "pod_steps_per_step": topsis["pod_steps_per_step"],
                 "kernel_ms": topsis["kernel_ms"], "fp64_decisions": topsis["stats"]["fp64_decisions"],
                 "retries": topsis["stats"]["retries"], "quality": topsis["quality"],
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": args.steps * LAUNCHES["topsis"],
-                "clocks": clocks, "ahp": ahp_obj, "variants": variants, "paths": paths, "simulator": sim, "c5": c5,
+                "clocks": clocks, "ahp": ahp_obj, "matrix": matrix, "c2_sequential": c2, "rank_cold": cold,
+                "variants": variants, "paths": paths, "simulator": sim, "c5": c5,
                 "rank_once": None if once is None else {
                     "workload": once["name"].replace("batch", "batch, rank once per request (R25)"),
                     "value": once["value"], "unit": "pods/s", "ms_per_step": once["ms_per_step"],
@@ -388,6 +429,134 @@ def run_ours(args, rank, world, local):
                 "paper_context": "T5 (P:416-426): TOPSIS 3.48-3.84 s, AHP 6.90-9.45 s per 6000-request k=20 campaign "
                                  "on an unnamed CUDA 10.1 GPU (~10-14 M / 4-7 M servers ranked/s derived)"}
         print(json.dumps(line))
+
+
+AHP_C4_REQUESTS = 1000   # C4 AHP cell: the first 1000 requests per GPU (O(K^2) levels per pod step)
+
+
+def measure_matrix(args, measure, topsis, ahp, pk):
+    """AHP and TOPSIS x the three schemas of T4 at C3 and C4, batch mode,
+    each cell device-timed like the headline (L2 flushed between steps)."""
+    from paper_1909_07673_b200 import nacs
+    mhz = float(pk.get("sm_max_mhz", 1965.0))
+    cells = {}
+    for cfg in ("C3", "C4"):
+        for method in ("topsis", "ahp"):
+            for schema in ("flat", "clustering", "network"):
+                key = f"{cfg} {method} {schema}"
+                if (cfg, method, schema) == ("C4", "topsis", "flat"):
+                    r = topsis
+                elif (cfg, method, schema) == ("C3", "ahp", "flat") and ahp is not None:
+                    r = ahp
+                else:
+                    try:
+                        r = measure(method, schema, cfg, AHP_C4_REQUESTS if (cfg, method) == ("C4", "ahp") else None)
+                    except nacs.NacsError as e:
+                        cells[key] = {"unavailable": str(e)}
+                        continue
+                st = r["stats"]
+                rl = topsis_roofline(st, r["kernel_ms"], mhz, "") if method == "topsis" else \
+                    ahp_roofline(st, r["kernel_ms"], mhz)
+                cells[key] = {"workload": r["name"], "value": r["value"], "unit": "pods/s",
+                              "servers_ranked_per_s": r["servers_ranked_per_s"], "ms_per_step": r["ms_per_step"],
+                              "pod_steps_per_step": r["pod_steps_per_step"], "fp64_decisions": st["fp64_decisions"],
+                              "quality": r["quality"],
+                              "roofline": {k: rl[k] for k in ("bound", "achieved", "peak", "unit", "frac")}}
+    return cells
+
+
+def measure_c2(args, ctx, stream, max_over_ranks):
+    """fat-tree k=8, 100 requests scheduled sequentially on the live state
+    (commits), TOPSIS and AHP Flat; device arrays, the state reloaded before each rep."""
+    import torch
+    from paper_1909_07673_b200 import nacs
+    snap, reqs = gen.config("C2")
+    dev = torch.device("cuda", ctx.device)
+    d = {k: (torch.from_numpy(v).to(dev) if isinstance(v, np.ndarray) else v) for k, v in reqs.items()}
+    res = {}
+    for method in ("topsis", "ahp"):
+        out = ctx._alloc_out(reqs, True)[0]
+        times = []
+        for rep in range(args.warmup + args.steps):
+            ctx.load_topology(snap)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            ctx.schedule_request(d, method, "flat", out=out, flags=nacs.NACS_ASYNC)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            if rep >= args.warmup:
+                times.append(e0.elapsed_time(e1))
+        ms = max_over_ranks(statistics.median(times))
+        st = ctx.last_stats()
+        res[method] = {"value": st["pod_steps"] / (ms / 1e3), "unit": "pods/s", "ms_per_step": ms,
+                       "pod_steps_per_step": st["pod_steps"], "servers_ranked_per_s": st["servers_ranked"] / (ms / 1e3),
+                       "quality": quality(reqs, out)}
+    return {"workload": "C2: fat-tree k=8 (128 servers), 100 requests, sequential Flat scheduling (live state)",
+            "modes": res}
+
+
+def cold_states(snap: dict, B: int, seed: int = 1):
+    """B distinct DC states (device-generated, seeded): the snapshot's links, residual CPU / RAM /
+    access link and f_u drawn uniformly over their ranges (inputs/gen.py's magnitudes)."""
+    import torch
+    k = snap["k"]
+    n = k ** 3 // 4
+    row = np.concatenate([snap["cpu_res"], snap["ram_res"], snap["active"].astype(np.int32), snap["link_res"]])
+    st = torch.from_numpy(np.tile(row.astype(np.int32), (B, 1))).cuda()
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    st[:, :n] = torch.randint(0, snap["cpu_cap"] + 1, (B, n), device="cuda", generator=g, dtype=torch.int32)
+    st[:, n:2 * n] = torch.randint(0, snap["ram_cap"] + 1, (B, n), device="cuda", generator=g, dtype=torch.int32)
+    st[:, 2 * n:3 * n] = torch.randint(0, 2, (B, n), device="cuda", generator=g, dtype=torch.int32)
+    st[:, 3 * n:4 * n] = torch.randint(50, snap["link_cap"] + 1, (B, n), device="cuda", generator=g, dtype=torch.int32)
+    return st
+
+
+COLD = (("C4 geometry", 32, 4096), ("C5 geometry", 64, 512))
+
+
+def measure_cold(args, ctx, dev, stream, flush, barrier, max_over_ranks, sum_over_ranks, pk, pk_kind):
+    """standalone TOPSIS ranking on COLD snapshots against HBM: one
+    nacs_rank_topsis_many call ranks one pod step (the request's first: demand, no flows) on each
+    of B distinct device-resident DC states (B x 16 n bytes >> the 126 MB L2, so every step
+    streams from HBM; no flush needed).  Algorithmic bytes per server: 16 read (cpu, ram, f_u,
+    access link) + 4 written (the FP32 score)."""
+    import torch
+    from paper_1909_07673_b200 import nacs
+    res = {}
+    for name, k, B in COLD:
+        snap = gen.snapshot(k, gen.CONFIG_SEEDS["C4" if k == 32 else "C5"])
+        ctx.load_topology(snap)
+        n = k ** 3 // 4
+        st = cold_states(snap, B, seed=11 + ctx.device)
+        out = dict(mask=None, scores=torch.empty((B, n), dtype=torch.float32, device=dev),
+                   best=torch.empty(B, dtype=torch.int32, device=dev))
+        for _ in range(args.warmup):
+            ctx.rank_many(st, 1500, 3000, out=out, mask=False, flags=nacs.NACS_ASYNC)
+        torch.cuda.synchronize(dev)
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        barrier()
+        for i in range(args.steps):
+            ev[i][0].record(stream)
+            ctx.rank_many(st, 1500, 3000, out=out, mask=False, flags=nacs.NACS_ASYNC)
+            ev[i][1].record(stream)
+        torch.cuda.synchronize(dev)
+        barrier()
+        ms = max_over_ranks(sum(a.elapsed_time(b) for a, b in ev) / args.steps)
+        stats = ctx.last_stats()
+        byts = B * n * (16 + 4)
+        ach = byts / (ms / 1e3) / 1e9
+        peak = float(pk.get("hbm_gbs", 6650.0))
+        res[name] = {"workload": f"fat-tree k={k} ({n} servers): {B} distinct states per GPU, one pod step each "
+                                 f"(demand 1500 mc / 3000 MiB, no flows), TOPSIS Flat",
+                     "value": sum_over_ranks(B * n) / (ms / 1e3), "unit": "servers ranked/s",
+                     "states_per_s": sum_over_ranks(B) / (ms / 1e3), "ms_per_step": ms,
+                     "fp64_decisions": stats["fp64_decisions"], "gpu_launches": 1,
+                     "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                                  "traffic": None, "kernel": "k_rank_occ (nacs_rank.cu)",
+                                  "bytes": "16 B read + 4 B score written per server",
+                                  "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({pk_kind})"}}
+    return res
 
 
 C5_REQUESTS = {"topsis": 40, "ahp": 12}
@@ -409,7 +578,8 @@ def measure_c5(args, rank, world, local, stream, max_over_ranks):
         import torch.distributed as dist
         obj = [nacs.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
-        modes = [(f"nccl_x{world}", (rank, world, obj[0]))]
+        # the unsharded run on every rank is the reference the NCCL shards must reproduce
+        modes = [("unsharded", None), (f"nccl_x{world}", (rank, world, obj[0]))]
     else:
         modes = [("unsharded", None), ("loopback_x8", (0, 8, None))]
     for method, nreq in C5_REQUESTS.items():
@@ -429,16 +599,20 @@ def measure_c5(args, rank, world, local, stream, max_over_ranks):
             ms = max_over_ranks(e0.elapsed_time(e1))
             st = ctx.last_stats()
             h = hashlib.sha256(b"".join(np.ascontiguousarray(out[k]).tobytes() for k in sorted(out))).hexdigest()
+            mhz = float(peaks()[0].get("sm_max_mhz", 1965.0))
+            rl = topsis_roofline(st, ms, mhz, "") if method == "topsis" else ahp_roofline(st, ms, mhz)
             res[f"{method} {name}"] = {"pods_per_s": st["pod_steps"] / (ms / 1e3), "ms": ms,
-                                       "pod_steps": st["pod_steps"], "placements_sha256": h[:16]}
+                                       "us_per_pod_step": ms * 1e3 / max(1, st["pod_steps"]),
+                                       "pod_steps": st["pod_steps"], "placements_sha256": h[:16],
+                                       "roofline": {k: rl[k] for k in ("bound", "achieved", "peak", "unit", "frac")}}
             ctx.close()
     same = {m: len({v["placements_sha256"] for k, v in res.items() if k.startswith(m)}) == 1 for m in C5_REQUESTS}
-    if world > 1:  # every rank must hold the same placements (replicated commit)
+    if world > 1:  # every rank holds the same placements (replicated commit), equal to unsharded
         import torch.distributed as dist
         mine = {k: v["placements_sha256"] for k, v in res.items()}
         allh = [None] * world
         dist.all_gather_object(allh, mine)
-        same = {m: all(a == allh[0] for a in allh) for m in C5_REQUESTS}
+        same = {m: same[m] and all(a == allh[0] for a in allh) for m in C5_REQUESTS}
     return {"workload": "C5: fat-tree k=64 (65536 servers), sequential Flat scheduling of "
                         f"{C5_REQUESTS['topsis']} (TOPSIS) / {C5_REQUESTS['ahp']} (AHP) requests, servers sharded "
                         f"over {world} rank(s)", "scaling": "strong", "modes": res,
@@ -634,9 +808,27 @@ def run_reference(args, rank, world):
                       "e2e": {"value": value, "unit": "pods/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
 
 
+def self_launch(args) -> int:
+    """--gpus N > 1 without a torchrun environment: launch N ranks (one process per GPU) with
+    torchrun on 127.0.0.1 and pass the JSON line through."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")  # the communicator lines name the N ranks
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.run(cmd, env=env).returncode
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args))
     rank, world, local = dist_env()
+    if "WORLD_SIZE" in os.environ and world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
