@@ -23,11 +23,20 @@ SCHEMAS = {"flat": (0.25, 0.25, 0.25, 0.25),
            "network": (0.17, 0.17, 0.16, 0.5)}
 
 
+# NACS_ORACLE_SANITIZE=1: an AddressSanitizer + UndefinedBehaviorSanitizer build of the same
+# source (SURVEY §4 layer 6), loaded instead; the process must preload libasan
+# (tests/test_oracle_sanitized.py runs the pins that way).
+SANITIZE = os.environ.get("NACS_ORACLE_SANITIZE") == "1"
+SAN_LIB = os.path.join(HERE, "liboracle_san.so")
+
+
 def build(force: bool = False) -> str:
-    if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < os.path.getmtime(SRC):
-        subprocess.check_call(["g++", "-O2", "-std=c++17", "-fopenmp", "-shared", "-fPIC",
-                               "-o", LIB, SRC])
-    return LIB
+    out, extra = (SAN_LIB, ["-g", "-fsanitize=address,undefined", "-fno-sanitize-recover=undefined",
+                            "-fno-omit-frame-pointer"]) if SANITIZE else (LIB, [])
+    if force or not os.path.exists(out) or os.path.getmtime(out) < os.path.getmtime(SRC):
+        subprocess.check_call(["g++", "-O2", "-std=c++17", "-fopenmp", "-shared", "-fPIC", *extra,
+                               "-o", out, SRC])
+    return out
 
 
 _lib = None
