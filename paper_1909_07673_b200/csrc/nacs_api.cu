@@ -86,6 +86,7 @@ struct nacs_ctx {
   DevArr<int> deferred;      // requests k_batch_warp hands to k_batch
   DevArr<double> w64;
   DevArr<float> ahp_ws;
+  DevArr<unsigned char> ahp_glob;  // AHP batch workspace in global memory (k_batch, large n)
   DevArr<int> misc;          // next-request counter, query arrays, best
   DevArr<unsigned char> mask;
   DevArr<float> scores;
@@ -842,6 +843,7 @@ void nacs_destroy(nacs_ctx* ctx) {
   ctx->deferred.release();
   ctx->w64.release();
   ctx->ahp_ws.release();
+  ctx->ahp_glob.release();
   ctx->misc.release();
   ctx->mask.release();
   ctx->scores.release();
@@ -1066,6 +1068,12 @@ nacs_status nacs_schedule_batch(nacs_ctx* ctx, const nacs_options* opt, const na
   if (grid > R) grid = R;
   CK(ctx->ulog.reserve((size_t)grid * nacs::ULOG_CAP));
   if (o.method == 0 || o.rank_once) CK(ctx->w64.reserve((size_t)grid * nacs::ahp_workspace_doubles(g.n)));
+  unsigned char* ahp_g = nullptr;
+  if (nacs::batch_ahp_global(g, o.method)) {
+    const size_t per = (nacs::ahp_workspace_bytes(g.n) + 15) & ~(size_t)15;
+    CK(ctx->ahp_glob.reserve((size_t)grid * per));
+    ahp_g = ctx->ahp_glob.p;
+  }
   CK(ctx->misc.reserve(8));
   CK(cudaMemsetAsync(ctx->misc.p, 0, 4 * sizeof(int), ctx->stream));
   const int warps = o.method == NACS_TOPSIS && !ctx->cta_only ? nacs::warp_kernel_warps(g) : 0;
@@ -1077,10 +1085,10 @@ nacs_status nacs_schedule_batch(nacs_ctx* ctx, const nacs_options* opt, const na
     CK(ctx->deferred.reserve(2 * (size_t)R));
     CK(nacs::launch_batch_warp(g, o, ctx->state.p, ctx->wlay.p, Rd, Od, ctx->wlog.p, ctx->misc.p, ctx->deferred.p + R,
                                ctx->deferred.p, ctx->misc.p + 2, ctx->stats.p, wgrid, warps, ctx->stream));
-    CK(nacs::launch_batch(g, o, ctx->state.p, Rd, Od, ctx->ulog.p, ctx->w64.p, ctx->misc.p + 1, ctx->stats.p,
+    CK(nacs::launch_batch(g, o, ctx->state.p, Rd, Od, ctx->ulog.p, ctx->w64.p, ahp_g, ctx->misc.p + 1, ctx->stats.p,
                           grid, ctx->stream, ctx->deferred.p, ctx->misc.p + 2));
   } else {
-    CK(nacs::launch_batch(g, o, ctx->state.p, Rd, Od, ctx->ulog.p, ctx->w64.p, ctx->misc.p, ctx->stats.p, grid,
+    CK(nacs::launch_batch(g, o, ctx->state.p, Rd, Od, ctx->ulog.p, ctx->w64.p, ahp_g, ctx->misc.p, ctx->stats.p, grid,
                           ctx->stream));
   }
   if (!dev) {

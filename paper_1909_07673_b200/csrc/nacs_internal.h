@@ -138,12 +138,15 @@ size_t ahp_workspace_bytes(int n);
 size_t ahp_workspace_doubles(int n);
 // dynamic shared memory of the batch kernel, 0 if it does not fit
 size_t batch_smem_bytes(const Geo& g, int method);
+// AHP batch with the sorted-level workspace in global memory (per CTA: ahp_workspace_bytes(n),
+// 16-byte aligned) because it does not fit in shared memory beside the snapshot
+bool batch_ahp_global(const Geo& g, int method);
 int batch_block_size(const Geo& g, int method);
 cudaError_t batch_occupancy(const Geo& g, int method, int* blocks_per_sm);
 
 cudaError_t launch_batch(const Geo& g, const Opt& o, const int* d_state, const ReqsDev& R, const OutDev& O,
-                         int2* ulog, double* w64, int* next, unsigned long long* stats, int grid,
-                         cudaStream_t s, const int* idx = nullptr, const int* n_idx = nullptr);
+                         int2* ulog, double* w64, unsigned char* ahp_g, int* next, unsigned long long* stats,
+                         int grid, cudaStream_t s, const int* idx = nullptr, const int* n_idx = nullptr);
 // warp-per-request TOPSIS batch kernel (nacs_warp.cu): warps per CTA (0 = does not fit)
 int warp_kernel_warps(const Geo& g);
 size_t warp_ulog_entries(int grid, int warps);

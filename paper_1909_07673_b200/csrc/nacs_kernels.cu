@@ -1556,7 +1556,7 @@ __device__ void flush_stats(Ctx& c, unsigned long long* stats) {
 
 template <int METHOD>
 __global__ void __launch_bounds__(1024) k_batch(Geo g, Opt o, const int* __restrict__ snap, ReqsDev R,
-                                                OutDev O, int2* ulog, double* w64, int* next,
+                                                OutDev O, int2* ulog, double* w64, unsigned char* ahp_g, int* next,
                                                 unsigned long long* stats, const int* idx, const int* n_idx) {
   extern __shared__ __align__(16) unsigned char dyn[];
   __shared__ Scratch s;
@@ -1579,7 +1579,7 @@ __global__ void __launch_bounds__(1024) k_batch(Geo g, Opt o, const int* __restr
   c.edgebad = reinterpret_cast<unsigned*>(dyn + off);
   off = align16(off + sizeof(unsigned) * nEW);
   c.nfcap = n;
-  if (METHOD == 0) ahp_carve(c, dyn + off, n);
+  if (METHOD == 0) ahp_carve(c, ahp_g ? ahp_g + (size_t)blockIdx.x * align16(ahp_bytes(n)) : dyn + off, n);
   if (w64) c.w64 = w64 + (size_t)blockIdx.x * ahp_w64_doubles(n);  // AHP FP64; R25 scores
   c.snap = snap;
   c.ulog = ulog + (size_t)blockIdx.x * ULOG_CAP;
@@ -2916,9 +2916,21 @@ static size_t bitmap_bytes(const Geo& g) {
   return align16(4 * (size_t)nW) * 3 + align16(4 * (size_t)nEW);
 }
 
+// AHP whose sorted-level workspace (ahp_bytes, ~68 B per server) does not fit beside the
+// snapshot (k = 32: 196 KB + 561 KB) keeps only the snapshot and bitmaps in shared memory and
+// carves the workspace from a per-CTA block of global memory (L1/L2-resident).
+bool batch_ahp_global(const Geo& g, int method) {
+  if (method != 0) return false;
+  int dev = 0, optin = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  const size_t b = align16(sizeof(int) * (size_t)g.words()) + bitmap_bytes(g) + sizeof(Scratch) + 64;
+  return b + ahp_bytes(g.n) > (size_t)optin && b <= (size_t)optin;
+}
+
 size_t batch_smem_bytes(const Geo& g, int method) {
   size_t b = align16(sizeof(int) * (size_t)g.words()) + bitmap_bytes(g);
-  if (method == 0) b += ahp_bytes(g.n);
+  if (method == 0 && !batch_ahp_global(g, method)) b += ahp_bytes(g.n);
   int dev = 0, optin = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
@@ -2946,21 +2958,22 @@ cudaError_t batch_occupancy(const Geo& g, int method, int* blocks_per_sm) {
 
 template <int M>
 static void launch_batch_t(const Geo& g, const Opt& o, const int* d_state, const ReqsDev& R, const OutDev& O,
-                           int2* ulog, double* w64, int* next, unsigned long long* stats, int grid, cudaStream_t st,
-                           const int* idx, const int* n_idx) {
+                           int2* ulog, double* w64, unsigned char* ahp_g, int* next, unsigned long long* stats,
+                           int grid, cudaStream_t st, const int* idx, const int* n_idx) {
   size_t smem = batch_smem_bytes(g, M);
   cudaFuncSetAttribute(k_batch<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_batch<M><<<grid, batch_block_size(g, M), smem, st>>>(g, o, d_state, R, O, ulog, w64, next, stats, idx, n_idx);
+  k_batch<M><<<grid, batch_block_size(g, M), smem, st>>>(g, o, d_state, R, O, ulog, w64, ahp_g, next, stats, idx,
+                                                         n_idx);
 }
 
 cudaError_t launch_batch(const Geo& g, const Opt& o, const int* d_state, const ReqsDev& R, const OutDev& O,
-                         int2* ulog, double* w64, int* next, unsigned long long* stats, int grid,
-                         cudaStream_t st, const int* idx, const int* n_idx) {
+                         int2* ulog, double* w64, unsigned char* ahp_g, int* next, unsigned long long* stats,
+                         int grid, cudaStream_t st, const int* idx, const int* n_idx) {
   switch (o.method) {
-    case 0: launch_batch_t<0>(g, o, d_state, R, O, ulog, w64, next, stats, grid, st, idx, n_idx); break;
-    case 1: launch_batch_t<1>(g, o, d_state, R, O, ulog, w64, next, stats, grid, st, idx, n_idx); break;
-    case 2: launch_batch_t<2>(g, o, d_state, R, O, ulog, w64, next, stats, grid, st, idx, n_idx); break;
-    default: launch_batch_t<3>(g, o, d_state, R, O, ulog, w64, next, stats, grid, st, idx, n_idx); break;
+    case 0: launch_batch_t<0>(g, o, d_state, R, O, ulog, w64, ahp_g, next, stats, grid, st, idx, n_idx); break;
+    case 1: launch_batch_t<1>(g, o, d_state, R, O, ulog, w64, nullptr, next, stats, grid, st, idx, n_idx); break;
+    case 2: launch_batch_t<2>(g, o, d_state, R, O, ulog, w64, nullptr, next, stats, grid, st, idx, n_idx); break;
+    default: launch_batch_t<3>(g, o, d_state, R, O, ulog, w64, nullptr, next, stats, grid, st, idx, n_idx); break;
   }
   return cudaGetLastError();
 }

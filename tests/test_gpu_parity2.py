@@ -233,3 +233,19 @@ def test_c5_ahp_sequential_vs_oracle():
     out, st, stats = _run_modes(snap, one, "ahp", [None, 3])
     cnt = assert_schedule_parity(snap, one, out, "ahp", "flat", True, gpu_state=st)
     assert cnt["pod_steps"] == pods[r] == stats["pod_steps"]
+
+
+# ------------------------------------------------------------------ C4 AHP -----
+def test_c4_ahp_batch_subsample(ctx):
+    """BASELINE configs[3] with AHP (SURVEY §8(c) "C4: a seeded subsample of 20-50 requests"):
+    the batch kernel with its sorted-level workspace in global memory (k = 32 does not fit in
+    shared memory beside the snapshot); requests are independent under R21, so per-request
+    parity on a subsample is exact."""
+    snap, reqs = gen.config("C4")
+    idx = np.arange(0, reqs["n_requests"], 4000)  # 25 requests spread over the stream
+    sub = gen.subset(reqs, idx)
+    ctx.load_topology(snap)
+    for schema, rule in (("flat", 0), ("network", 1)):
+        out = ctx.schedule_batch(sub, "ahp", schema, ahp_rule=rule)
+        cnt = assert_schedule_parity(snap, sub, out, "ahp", schema, False, ahp_rule=rule)
+        assert ctx.last_stats()["pod_steps"] == cnt["pod_steps"]
