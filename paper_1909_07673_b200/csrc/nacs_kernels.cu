@@ -1554,7 +1554,7 @@ __device__ void flush_stats(Ctx& c, unsigned long long* stats) {
 // dynamic shared memory layout of k_batch:
 //   state words (6n ints) | maskw[nW] | special[nW] | edgebad[nEW] | AHP arrays
 
-template <int METHOD>
+template <int METHOD, bool AHPG = false>
 __global__ void __launch_bounds__(1024) k_batch(Geo g, Opt o, const int* __restrict__ snap, ReqsDev R,
                                                 OutDev O, int2* ulog, double* w64, unsigned char* ahp_g, int* next,
                                                 unsigned long long* stats, const int* idx, const int* n_idx) {
@@ -1579,7 +1579,8 @@ __global__ void __launch_bounds__(1024) k_batch(Geo g, Opt o, const int* __restr
   c.edgebad = reinterpret_cast<unsigned*>(dyn + off);
   off = align16(off + sizeof(unsigned) * nEW);
   c.nfcap = n;
-  if (METHOD == 0) ahp_carve(c, ahp_g ? ahp_g + (size_t)blockIdx.x * align16(ahp_bytes(n)) : dyn + off, n);
+  // (separate instantiations keep the shared-memory layout's pointers provably shared)
+  if (METHOD == 0) ahp_carve(c, AHPG ? ahp_g + (size_t)blockIdx.x * align16(ahp_bytes(n)) : dyn + off, n);
   if (w64) c.w64 = w64 + (size_t)blockIdx.x * ahp_w64_doubles(n);  // AHP FP64; R25 scores
   c.snap = snap;
   c.ulog = ulog + (size_t)blockIdx.x * ULOG_CAP;
@@ -2961,6 +2962,12 @@ static void launch_batch_t(const Geo& g, const Opt& o, const int* d_state, const
                            int2* ulog, double* w64, unsigned char* ahp_g, int* next, unsigned long long* stats,
                            int grid, cudaStream_t st, const int* idx, const int* n_idx) {
   size_t smem = batch_smem_bytes(g, M);
+  if (M == 0 && ahp_g) {
+    cudaFuncSetAttribute(k_batch<M, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_batch<M, true><<<grid, batch_block_size(g, M), smem, st>>>(g, o, d_state, R, O, ulog, w64, ahp_g, next, stats,
+                                                                 idx, n_idx);
+    return;
+  }
   cudaFuncSetAttribute(k_batch<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k_batch<M><<<grid, batch_block_size(g, M), smem, st>>>(g, o, d_state, R, O, ulog, w64, ahp_g, next, stats, idx,
                                                          n_idx);
