@@ -56,6 +56,9 @@ struct Scratch {
   int fv[MAXF], fD[MAXF], fok[MAXF], fpath[MAXF], fexcl[MAXF];
   unsigned pm[MAXK];
   int fail, log_n, log_mark;
+  // a lower bound of every fabric (edge-agg, agg-core) residual of the state (0 = unknown):
+  // a flow with D <= minfab passes every edge switch, so its fabric tables are skipped (exact)
+  int minfab, minfab0;
   // statistics over the feasible set F
   int nf, nact, mn[4], mx[4];
   unsigned long long sq[4];
@@ -132,6 +135,7 @@ __device__ __forceinline__ void st_set(Ctx& c, int off, int val) {
   c.ulog[s->log_n] = make_int2(off, c.st[off]);
   s->log_n += 1;
   c.st[off] = val;
+  if (off >= 4 * c.g.n && val < s->minfab) s->minfab = val;  // commits only lower the bound
   if (c.dirty && off < 4 * c.g.n) {  // AHP: the server leaves its presorted position
     const int u = off % c.g.n;
     if (!((c.dirty[u >> 5] >> (u & 31)) & 1u)) {
@@ -393,6 +397,7 @@ __device__ void fabric_tables(Ctx& c) {
   const int* AC = EA + g.E * h;
   for (int f = 0; f < s->nflow; ++f) {
     int v = s->fv[f], D = s->fD[f];
+    if (D <= s->minfab) continue;  // every fabric link carries D: no edge switch fails this flow
     int ev = (int)div_h(v, g.magic_h), pv = (int)div_h(ev, g.magic_h);
     for (int p = c.tid; p < g.k; p += c.B) s->pm[p] = 0u;
     if (c.tid == 0) s->vm = 0;
@@ -1528,6 +1533,7 @@ __device__ void init_ctx(Ctx& c, const Geo& g, const Opt& o, Scratch* s) {
   c.dirty = nullptr;
   if (c.tid == 0) {
     s->c_steps = s->c_retries = s->c_fp64 = s->c_invalid = s->c_feas = s->c_pairs = 0;
+    s->minfab = s->minfab0 = 0;
     s->presorted = 0;
     s->touch_over = 0;
     s->ntouched = 0;
@@ -1549,6 +1555,22 @@ __device__ void flush_stats(Ctx& c, unsigned long long* stats) {
     if (s->c_feas) atomicAdd(&stats[ST_FEAS], s->c_feas);
     if (s->c_pairs) atomicAdd(&stats[ST_PAIRS], s->c_pairs);
   }
+}
+
+// s->minfab = the smallest fabric residual of the state (block reduction).  All threads.
+__device__ void init_minfab(Ctx& c) {
+  const int n = c.g.n, L = c.g.L;
+  int m = INT_MAX;
+  for (int i = 4 * n + c.tid; i < 3 * n + L; i += c.B) m = min(m, c.st[i]);
+  m = (int)__reduce_min_sync(FULL, (unsigned)m);  // residuals are >= 0
+  if (c.lane == 0) c.s->red_i[c.warp][0] = m;
+  __syncthreads();
+  if (c.tid == 0) {
+    int b = INT_MAX;
+    for (int w = 0; w < c.NW; ++w) b = min(b, c.s->red_i[w][0]);
+    c.s->minfab = c.s->minfab0 = b == INT_MAX ? 0 : b;
+  }
+  __syncthreads();
 }
 
 // dynamic shared memory layout of k_batch:
@@ -1614,6 +1636,7 @@ __global__ void __launch_bounds__(1024) k_batch(Geo g, Opt o, const int* __restr
   for (int w = c.tid; w < nW; w += c.B) { c.maskw[w] = 0u; c.special[w] = 0u; }
   for (int w = c.tid; w < nEW; w += c.B) c.edgebad[w] = 0u;
   __syncthreads();
+  init_minfab(c);
   if (METHOD == 0) ahp_presort(c);  // the snapshot's order serves every request
 
   for (;;) {
@@ -1624,6 +1647,7 @@ __global__ void __launch_bounds__(1024) k_batch(Geo g, Opt o, const int* __restr
     if (r >= n_req) break;
     if (idx) r = idx[r];
     run_request<METHOD>(c, R, O, r, false);
+    if (c.tid == 0) s.minfab = s.minfab0;  // the request's overlay is undone: the snapshot again
   }
   flush_stats(c, stats);
 }
@@ -1672,6 +1696,7 @@ __global__ void __launch_bounds__(1024) k_sequential(Geo g, Opt o, int* state, R
   for (int w = c.tid; w < c.nW; w += c.B) { c.maskw[w] = 0u; c.special[w] = 0u; }
   for (int w = c.tid; w < c.nEW; w += c.B) c.edgebad[w] = 0u;
   __syncthreads();
+  init_minfab(c);
   for (int r = 0; r < R.n; ++r) run_request<METHOD>(c, R, O, r, true);
   if (smem_state) store_state_smem(c, sst, state);
   flush_stats(c, stats);
@@ -1747,6 +1772,7 @@ __global__ void __launch_bounds__(512) k_simulate(Geo g, Opt o, int* state, Reqs
   for (int i = c.tid; i < S.max_ticks; i += c.B) S.head[i] = -1;
   if (c.tid == 0) { qn = 0; next = 0; done = 0; n_att = 0; n_acc = 0; }
   __syncthreads();
+  init_minfab(c);  // departures raise residuals: the bound stays a lower bound
   int* qa = S.qbuf;
   int* qb = S.qtmp;
   int t = 0;
@@ -1953,6 +1979,7 @@ __global__ void __launch_bounds__(1024) k_sh_begin(Geo g, Opt o, int* state, Req
   Ctx c;
   sh_ctx(c, g, o, state, d);
   Scratch* s = c.s;
+  if (r == 0) init_minfab(c);  // the call's first request: the bound of the live state
   if (first == 2 && d.facc[15]) {  // AHP: k_sh_presort has just rebuilt the presorted orders
     for (int w = c.tid; w < c.nW; w += c.B) c.dirty[w] = 0u;
     if (c.tid == 0) { s->ntouched = 0; s->touch_over = 0; s->presorted = 1; }
