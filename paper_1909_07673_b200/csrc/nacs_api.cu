@@ -87,6 +87,7 @@ struct nacs_ctx {
   DevArr<double> w64;
   DevArr<float> ahp_ws;
   DevArr<unsigned char> ahp_glob;  // AHP batch workspace in global memory (k_batch, large n)
+  DevArr<unsigned long long> seqc; // k_seq_cluster exchange: statistics, keys, FP64 candidates
   DevArr<int> misc;          // next-request counter, query arrays, best
   DevArr<unsigned char> mask;
   DevArr<float> scores;
@@ -844,6 +845,7 @@ void nacs_destroy(nacs_ctx* ctx) {
   ctx->w64.release();
   ctx->ahp_ws.release();
   ctx->ahp_glob.release();
+  ctx->seqc.release();
   ctx->misc.release();
   ctx->mask.release();
   ctx->scores.release();
@@ -1182,6 +1184,20 @@ nacs_status nacs_schedule_request(nacs_ctx* ctx, const nacs_options* opt, const 
     return NACS_OK;
   }
   CK(ctx->ulog.reserve(nacs::ULOG_CAP));
+  const int seqc = o.method == NACS_TOPSIS && !o.rank_once ? nacs::seq_cluster_size(g) : 0;
+  if (seqc > 0) {  // TOPSIS on a large DC: the whole request stream on one thread-block cluster
+    CK(ctx->seqc.reserve(96));
+    CK(nacs::launch_seq_cluster(g, o, ctx->state.p, Rd, Od, ctx->ulog.p, ctx->stats.p, ctx->seqc.p, seqc,
+                                ctx->stream));
+    if (!dev) {
+      if ((st = unstage_outputs(ctx, R, C, V, out))) return st;
+    }
+    if (!async) {
+      CK(cudaStreamSynchronize(ctx->stream));
+      if ((st = finish_stats(ctx))) return st;
+    }
+    return NACS_OK;
+  }
   if (o.method == 0) CK(ctx->ahp_ws.reserve(nacs::ahp_workspace_bytes(g.n) / 4 + 4));
   if (o.method == 0 || o.rank_once) CK(ctx->w64.reserve(nacs::ahp_workspace_doubles(g.n)));
   CK(nacs::launch_sequential(g, o, ctx->state.p, Rd, Od, ctx->ulog.p, ctx->ahp_ws.p, ctx->w64.p, ctx->stats.p,

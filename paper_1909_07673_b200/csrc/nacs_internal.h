@@ -158,6 +158,11 @@ cudaError_t launch_batch_warp(const Geo& g, const Opt& o, const int* d_state, in
 cudaError_t launch_sequential(const Geo& g, const Opt& o, int* d_state, const ReqsDev& R, const OutDev& O,
                               int2* ulog, float* ahp_ws, double* w64, unsigned long long* stats,
                               cudaStream_t s);
+// sequential TOPSIS on one thread-block cluster of C CTAs (large n; 0 = not used)
+int seq_cluster_size(const Geo& g);
+cudaError_t launch_seq_cluster(const Geo& g, const Opt& o, int* d_state, const ReqsDev& R, const OutDev& O,
+                               int2* ulog, unsigned long long* stats, unsigned long long* work, int C,
+                               cudaStream_t st);
 cudaError_t launch_rank(const Geo& g, const Opt& o, int* d_state, const QueryDev& q, float* ahp_ws,
                         double* w64, unsigned long long* stats, cudaStream_t s);
 cudaError_t launch_validate(const ReqsDev& R, int* status, unsigned long long* stats, cudaStream_t s);

@@ -19,6 +19,8 @@
 // 2^23 magic-number trick (no I2F on the hot loop).  TOPSIS norms are exact integer sums
 // of squares (64-bit).  Scores are FP32; an argmax whose top-2 FP32 gap is inside the
 // derived FP32 error bound is re-decided in FP64 over the near-max candidates (R14).
+#include <cooperative_groups.h>
+
 #include <cfloat>
 #include <cstdlib>
 #include <climits>
@@ -1702,6 +1704,163 @@ __global__ void __launch_bounds__(1024) k_sequential(Geo g, Opt o, int* state, R
   flush_stats(c, stats);
 }
 
+// ------------------------------------------- sequential engine on a cluster ---
+// nacs_schedule_request for TOPSIS on a large DC (the paper's online semantics, P:206, P:391,
+// on C5's 65536 servers): ONE thread-block cluster of C CTAs runs the whole request stream in
+// one launch, no host round trip.  Every CTA keeps its own scratch (request decode, pods,
+// flows, fabric tables, flow-server feasibility: identical, deterministic copies) and filters
+// and scores its grid-stride share of the servers on the live state in global memory (L2);
+// the exact integer statistics meet in global accumulators (atomics, double-buffered per
+// attempt), the top-2 keys (and FP64 near-tie candidates) in one slot per CTA.  The leader
+// (rank 0) alone commits (a8, R16-R18), tops up (R19), rejects (R20) and writes outputs; the
+// others read its verdict (R18 failure) and fabric bound over DSMEM after the barrier and
+// replicate the exclusion.  Three cluster barriers per pod step.
+namespace cgx = cooperative_groups;
+
+__device__ __forceinline__ void facc_reset(unsigned long long* f, int tid) {
+  if (tid < 11) f[tid] = (tid >= 2 && tid <= 7 && !(tid & 1)) ? ~0ull : 0ull;
+}
+
+__global__ void __launch_bounds__(1024) k_seq_cluster(Geo g, Opt o, int* state, ReqsDev R, OutDev O, int2* ulog,
+                                                      unsigned long long* stats, unsigned long long* facc,
+                                                      unsigned long long* kx, double* kxv, int* kxi) {
+  extern __shared__ __align__(16) unsigned char dyn[];
+  __shared__ Scratch s;
+  cgx::cluster_group cl = cgx::this_cluster();
+  const int C = (int)cl.num_blocks(), q = (int)cl.block_rank();
+  const bool lead = q == 0;
+  Ctx c;
+  init_ctx(c, g, o, &s);
+  size_t off = 0;
+  c.maskw = reinterpret_cast<unsigned*>(dyn + off);
+  off = align16(off + sizeof(unsigned) * c.nW);
+  c.special = reinterpret_cast<unsigned*>(dyn + off);
+  off = align16(off + sizeof(unsigned) * c.nW);
+  c.f0w = reinterpret_cast<unsigned*>(dyn + off);
+  off = align16(off + sizeof(unsigned) * c.nW);
+  c.edgebad = reinterpret_cast<unsigned*>(dyn + off);
+  c.st = state;
+  c.cr = state;
+  c.snap = state;
+  c.ulog = ulog;
+  c.nfcap = g.n;
+  c.w64 = nullptr;
+  const int n = g.n;
+  for (int w = c.tid; w < c.nW; w += c.B) { c.maskw[w] = 0u; c.special[w] = 0u; }
+  for (int w = c.tid; w < c.nEW; w += c.B) c.edgebad[w] = 0u;
+  if (lead) { facc_reset(facc, c.tid); facc_reset(facc + 16, c.tid); }
+  __syncthreads();
+  init_minfab(c);  // every CTA reads the same state: the same bound
+  cl.sync();
+  int t = 0;  // attempt counter (the same in every CTA)
+  for (int r = 0; r < R.n; ++r) {
+    req_begin<1>(c, R, r, true);
+    if (!s.req_ok) {
+      if (lead) write_rejected(c, R, O, r, -1);
+      continue;
+    }
+    bool rejected = false;
+    for (int p = 0; p < s.P && !rejected; ++p) {
+      pod_prologue(c, R, r, p);
+      for (;;) {
+        unsigned long long* fa = facc + 16 * (t & 1);
+        pass_filter<false, true>(c, nullptr, nullptr, fa);  // a3 + a4 on this CTA's grid-stride share
+        cl.sync();  // (1) the exact statistics of every CTA are in fa
+        if (c.tid == 0) {
+          const int nf = (int)fa[0], nact = (int)fa[1];
+          s.nf = nf;
+          s.nact = nact;
+          s.mn[0] = (int)fa[2]; s.mx[0] = (int)fa[3];
+          s.mn[1] = (int)fa[4]; s.mx[1] = (int)fa[5];
+          s.mn[2] = nact == nf ? 1 : 0; s.mx[2] = nact > 0 ? 1 : 0;  // f_u in {0,1}
+          s.mn[3] = (int)fa[6]; s.mx[3] = (int)fa[7];
+          s.sq[0] = fa[8]; s.sq[1] = fa[9]; s.sq[2] = (unsigned long long)nact; s.sq[3] = fa[10];
+          if (lead) { s.c_steps += 1; s.c_feas += (unsigned long long)nf; }
+        }
+        if (lead) facc_reset(facc + 16 * ((t + 1) & 1), c.tid);  // read by everyone at the last attempt
+        __syncthreads();
+        ++t;
+        if (s.nf == 0) {  // F empty: reject the request atomically (R20)
+          if (lead) req_reject(c, R, O, r);
+          rejected = true;
+          break;
+        }
+        // a5T: closeness of this CTA's feasible servers, top-2 keys into its slot
+        TopsisP tp;
+        for (int k = 0; k < 4; ++k) { tp.mx[k] = s.mx[k]; tp.mn[k] = s.mn[k]; }
+        topsis_params(tp, o.wd, s.sq);
+        {
+          unsigned long long k1 = 0, k2 = 0;
+          for (int base = (blockIdx.x * c.NW + c.warp) * 32; base < n; base += gridDim.x * c.B) {
+            if (!((c.maskw[base >> 5] >> c.lane) & 1u)) continue;
+            const int u = base + c.lane;
+            const float rr = topsis32(tp, c.st[u], c.st[n + u], c.st[2 * n + u], c.st[3 * n + u]);
+            top2_insert(k1, k2, score_key(rr, u));
+          }
+          block_top2(c, k1, k2);
+          if (c.tid == 0) { kx[2 * q] = s.key1; kx[2 * q + 1] = s.key2; }
+        }
+        cl.sync();  // (2) every CTA's keys
+        if (c.tid == 0) {  // a7: argmax, lowest index on ties (R14); FP64 near-tie re-decision
+          unsigned long long k1 = 0, k2 = 0;
+          for (int i = 0; i < C; ++i) top2_merge(k1, k2, kx[2 * i], kx[2 * i + 1]);
+          const float s1 = __uint_as_float((unsigned)(k1 >> 32)), s2 = __uint_as_float((unsigned)(k2 >> 32));
+          s.best = (int)(0xFFFFFFFFu - (unsigned)(k1 & 0xFFFFFFFFull));
+          s.amb = o.exact64 || (k2 != 0ull && s1 - s2 <= kTopsisDelta);
+          s.thr = o.exact64 ? -1.0f : s1 - 2.0f * kTopsisDelta;
+        }
+        __syncthreads();
+        if (s.amb) {
+          double bv = -DBL_MAX;
+          int bj = -1;
+          for (int base = (blockIdx.x * c.NW + c.warp) * 32; base < n; base += gridDim.x * c.B) {
+            if (!((c.maskw[base >> 5] >> c.lane) & 1u)) continue;
+            const int u = base + c.lane;
+            const int x0 = c.st[u], x1 = c.st[n + u], x2 = c.st[2 * n + u], x3 = c.st[3 * n + u];
+            if (topsis32(tp, x0, x1, x2, x3) < s.thr) continue;
+            const double rr = topsis64(tp, x0, x1, x2, x3);
+            if (rr > bv || (rr == bv && u < bj)) { bv = rr; bj = u; }
+          }
+          block_argmax64(c, bv, bj);
+          if (c.tid == 0) { kxv[q] = s.bestv; kxi[q] = s.best; }
+          cl.sync();  // (2') every CTA's FP64 candidate
+          if (c.tid == 0) {
+            double v = -DBL_MAX;
+            int j = -1;
+            for (int i = 0; i < C; ++i)
+              if (kxi[i] >= 0 && (j < 0 || kxv[i] > v || (kxv[i] == v && kxi[i] < j))) { v = kxv[i]; j = kxi[i]; }
+            s.best = j;
+            if (lead) s.c_fp64 += 1;
+          }
+          __syncthreads();
+        }
+        if (lead && c.warp == 0) commit(c, R, r, p);  // a8 on the live state (R16-R18)
+        cl.sync();  // (3) the commit (or its undo) is visible; the leader's verdict over DSMEM
+        if (c.tid == 0 && !lead) {
+          const Scratch* ls = cl.map_shared_rank(&s, 0);
+          const int u = s.best;
+          s.fail = ls->fail;
+          s.minfab = ls->minfab;
+          if (s.fail) {  // R18: the same exclusion as the leader's
+            for (int i = 0; i < s.nflow; ++i) if (s.fv[i] == u) s.fexcl[i] = 1;
+            c.special[u >> 5] |= 1u << (u & 31);
+          } else {
+            s.pod_srv[p] = u;
+          }
+        }
+        __syncthreads();
+        if (!s.fail) break;
+      }
+    }
+    if (!rejected && lead) req_finish(c, R, O, r, true);  // a9: top-up (R19), outputs
+    cl.sync();  // (4) the request's top-up / rollback is visible before the next one reads the state
+    if (c.tid == 0 && !lead) s.minfab = cl.map_shared_rank(&s, 0)->minfab;
+    __syncthreads();
+  }
+  if (lead) flush_stats(c, stats);
+  cl.sync();  // no CTA leaves while another may still read its shared memory
+}
+
 // ------------------------------------------------------- simulator kernel ---
 // Departure of accepted request r on the live state (thread 0): the exact inverse of its
 // commit and top-up; f_u of its servers re-derived (R22).  st_set keeps the AHP presorted
@@ -3048,6 +3207,43 @@ cudaError_t launch_sequential(const Geo& g, const Opt& o, int* d_state, const Re
     default: set_smem<3>(k_sequential<3>, smem); k_sequential<3><<<1, B, smem, st>>>(g, o, d_state, R, O, ulog, ahp_ws, w64, stats, ss); break;
   }
   return cudaGetLastError();
+}
+
+int seq_cluster_size(const Geo& g) {
+  if (const char* e = getenv("NACS_SEQC")) return atoi(e);  // experiments (0 = off)
+  if (g.n < 16384) return 0;  // below: the one-CTA engine keeps the live state in shared memory
+  return g.n >= 65536 ? 16 : 8;
+}
+
+cudaError_t launch_seq_cluster(const Geo& g, const Opt& o, int* d_state, const ReqsDev& R, const OutDev& O,
+                               int2* ulog, unsigned long long* stats, unsigned long long* work, int C,
+                               cudaStream_t st) {
+  // work: facc [2][16] | kx [2][16] | kxv [16] | kxi [16] (unsigned long long words)
+  unsigned long long* facc = work;
+  unsigned long long* kx = work + 32;
+  double* kxv = reinterpret_cast<double*>(work + 64);
+  int* kxi = reinterpret_cast<int*>(work + 80);
+  const size_t nW = (size_t)(g.n + 31) / 32, nEW = (size_t)(g.E + 31) / 32;
+  const size_t smem = 3 * align16(4 * nW) + align16(4 * nEW);
+  cudaError_t e;
+  if (C > 8 && (e = cudaFuncSetAttribute(k_seq_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) !=
+                   cudaSuccess)
+    return e;
+  if ((e = cudaFuncSetAttribute(k_seq_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
+    return e;
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3(C, 1, 1);
+  cfg.blockDim = dim3(1024, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_seq_cluster, g, o, d_state, R, O, ulog, stats, facc, kx, kxv, kxi);
 }
 
 cudaError_t launch_simulate(const Geo& g, const Opt& o, int* d_state, const ReqsDev& R, const OutDev& O,

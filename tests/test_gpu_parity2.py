@@ -249,3 +249,41 @@ def test_c4_ahp_batch_subsample(ctx):
         out = ctx.schedule_batch(sub, "ahp", schema, ahp_rule=rule)
         cnt = assert_schedule_parity(snap, sub, out, "ahp", schema, False, ahp_rule=rule)
         assert ctx.last_stats()["pod_steps"] == cnt["pod_steps"]
+
+
+# ----------------------------------------- sequential engine on a cluster -----
+@pytest.mark.parametrize("k", [40, 48])
+def test_seq_cluster_engine_vs_oracle_and_one_cta(ctx, k):
+    """k_seq_cluster (nacs_schedule_request, TOPSIS, n >= 16384: one thread-block cluster runs
+    the request stream) against the oracle and against the one-CTA engine (NACS_SEQC=0) on
+    warm and congested snapshots, with the FP64 flag and the select-then-route flag."""
+    import os
+    snap = gen.snapshot(k, seed=90 + k)
+    tight = gen.snapshot(k, seed=91 + k)
+    tight["link_res"] = np.random.default_rng(k).integers(20, 160, size=len(tight["link_res"])).astype(np.int32)
+    reqs = gen.requests(8, 92 + k, bw_max_hi=60)
+    # (select-then-route on a congested fabric retries thousands of servers: the oracle's
+    # O(n + tables) per attempt makes that case minutes long; it runs on the warm snapshot)
+    cases = ((snap, {}), (tight, {}), (snap, dict(path_filter=0))) if k == 40 else ((snap, {}),)
+    for s, kw in cases:
+        ctx.load_topology(s)
+        a = to_np(ctx.schedule_request(reqs, "topsis", "network", **kw))
+        sa = ctx.read_topology()
+        cnt = assert_schedule_parity(s, reqs, a, "topsis", "network", True, gpu_state=sa, **kw)
+        st = ctx.last_stats()
+        assert st["pod_steps"] == cnt["pod_steps"]
+        os.environ["NACS_SEQC"] = "0"
+        try:
+            ctx.load_topology(s)
+            b = to_np(ctx.schedule_request(reqs, "topsis", "network", **kw))
+            sb = ctx.read_topology()
+        finally:
+            del os.environ["NACS_SEQC"]
+        for key in a:
+            assert np.array_equal(a[key], b[key]), key
+        for key in sa:
+            assert np.array_equal(sa[key], sb[key]), key
+    from paper_1909_07673_b200 import nacs
+    ctx.load_topology(snap)
+    c = to_np(ctx.schedule_request(reqs, "topsis", "flat", flags=nacs.NACS_EXACT_FP64))
+    assert_schedule_parity(snap, reqs, c, "topsis", "flat", True, gpu_state=ctx.read_topology())
