@@ -1222,6 +1222,48 @@ __device__ void select_ahp(Ctx& c, float* scores_out) {
 // ------------------------------------------------------------- request ------
 // Build the flows of pod p (R17): every vlink between p and a placed pod q on server v
 // adds bw^min to D_v; flows sorted by ascending v.  Thread 0.
+// build_flows with the vlinks' global loads spread over a warp (lane e reads vlink e's
+// endpoints and demand; lane 0 merges them in vlink order, as build_flows).  Warp 0.
+__device__ void build_flows_warp(Ctx& c, const ReqsDev& R, int r, int p) {
+  Scratch* s = c.s;
+  const int v0 = R.voff[r];
+  int nflow = 0, sumD = 0;
+  for (int e0 = 0; e0 < s->nV; e0 += 32) {
+    const int e = e0 + c.lane;
+    int v = -1, D = 0;
+    if (e < s->nV) {
+      const int a = s->cpod[R.src[v0 + e]], b = s->cpod[R.dst[v0 + e]];
+      int other = -1;
+      if (a == p && b != p && s->pod_srv[b] >= 0) other = b;
+      else if (b == p && a != p && s->pod_srv[a] >= 0) other = a;
+      if (other >= 0) { v = s->pod_srv[other]; D = R.bw_min[v0 + e]; }
+    }
+    unsigned has = __ballot_sync(FULL, v >= 0);
+    while (has) {
+      const int l = __ffs(has) - 1;
+      has &= has - 1;
+      const int vv = __shfl_sync(FULL, v, l), DD = __shfl_sync(FULL, D, l);
+      if (c.lane == 0) {
+        int i = 0;
+        while (i < nflow && s->fv[i] < vv) ++i;
+        if (i < nflow && s->fv[i] == vv) {
+          s->fD[i] += DD;
+        } else {
+          for (int t = nflow; t > i; --t) { s->fv[t] = s->fv[t - 1]; s->fD[t] = s->fD[t - 1]; }
+          s->fv[i] = vv;
+          s->fD[i] = DD;
+          ++nflow;
+        }
+        sumD += DD;
+      }
+    }
+  }
+  if (c.lane == 0) {
+    s->nflow = nflow;
+    s->sumD = sumD;
+  }
+}
+
 __device__ void build_flows(Ctx& c, const ReqsDev& R, int r, int p) {
   Scratch* s = c.s;
   int v0 = R.voff[r];
@@ -1343,6 +1385,117 @@ __device__ void commit(Ctx& c, const ReqsDev& R, int r, int p) {
   }
 }
 
+// Widest ECMP path from u to v (R16) over the WHOLE CTA: one candidate (a, or (a, b)) per
+// thread, a block-wide max of (bottleneck << 32 | ~candidate) keeps the lowest candidate on
+// ties, as widest_path_warp.  Returns (path id, fabric bottleneck) in every thread.
+__device__ int2 widest_path_cta(Ctx& c, int u, int v) {
+  const Geo& g = c.g;
+  const int h = g.h;
+  const int eu = (int)div_h(u, g.magic_h), ev = (int)div_h(v, g.magic_h);
+  if (eu == ev) return make_int2(0, INT_MAX);
+  const int pu = (int)div_h(eu, g.magic_h), pv = (int)div_h(ev, g.magic_h);
+  const int* EA = c.st + 4 * g.n;
+  const int* AC = EA + g.E * h;
+  const int nc = pu == pv ? h : h * h;
+  unsigned long long key = 0;
+  for (int t = c.tid; t < nc; t += c.B) {
+    int x;
+    if (pu == pv) {
+      x = min(EA[eu * h + t], EA[ev * h + t]);
+    } else {
+      const int a = (int)div_h(t, g.magic_h), b = t - a * h;
+      x = min(min(EA[eu * h + a], EA[ev * h + a]), min(AC[(pu * h + a) * h + b], AC[(pv * h + a) * h + b]));
+    }
+    const unsigned long long k = ((unsigned long long)(unsigned)x << 32) | (0xFFFFFFFFu - (unsigned)t);
+    key = k > key ? k : key;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long b = __shfl_xor_sync(FULL, key, o);
+    key = b > key ? b : key;
+  }
+  Scratch* s = c.s;
+  __syncthreads();
+  if (c.lane == 0) s->red_k[c.warp][0] = key;
+  __syncthreads();
+  if (c.warp == 0) {
+    key = c.lane < c.NW ? s->red_k[c.lane][0] : 0ull;
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long b = __shfl_xor_sync(FULL, key, o);
+      key = b > key ? b : key;
+    }
+    if (c.lane == 0) s->key1 = key;
+  }
+  __syncthreads();
+  key = s->key1;
+  const int bt = (int)(0xFFFFFFFFu - (unsigned)(key & 0xFFFFFFFFull));
+  return make_int2(pu == pv ? 1 + bt : 1 + h + bt, (int)(key >> 32));
+}
+
+// commit (a8) with the widest paths searched by the whole CTA (k_seq_cluster's leader: the
+// other CTAs wait at the next barrier, so the search latency is on the critical path).  Same
+// state changes, undo log, R18 handling and outputs as commit().  All threads.
+__device__ void commit_cta(Ctx& c, const ReqsDev& R, int r, int p) {
+  Scratch* s = c.s;
+  const Geo& g = c.g;
+  const int n = g.n;
+  const int u = s->best;
+  if (c.tid == 0) {
+    s->log_mark = s->log_n;
+    st_set(c, u, c.st[u] - s->dc);
+    st_set(c, n + u, c.st[n + u] - s->dr);
+    st_set(c, 2 * n + u, 1);
+    s->fail = 0;
+  }
+  __syncthreads();
+  for (int f = 0; f < s->nflow; ++f) {
+    const int v = s->fv[f], D = s->fD[f];
+    if (v == u) {
+      if (c.tid == 0) s->fpath[f] = -1;
+      continue;
+    }
+    const int2 wp = widest_path_cta(c, u, v);  // ends with __syncthreads: earlier deductions seen
+    if (c.tid == 0) {
+      const int bott = min(min(c.st[3 * n + u], c.st[3 * n + v]), wp.y);
+      if (bott < D) {
+        s->fail = 1;
+      } else {
+        st_set(c, 3 * n + u, c.st[3 * n + u] - D);
+        st_set(c, 3 * n + v, c.st[3 * n + v] - D);
+        int off[4];
+        const int m = path_links(g, u, v, wp.x, off);
+        for (int t = 0; t < m; ++t) st_set(c, off[t], c.st[off[t]] - D);
+        s->fpath[f] = wp.x;
+      }
+    }
+    __syncthreads();
+    if (s->fail) break;
+  }
+  if (c.tid == 0) {
+    if (s->fail) {  // R18: undo this pod's commit, exclude u, redo the pod step
+      undo_to(c, s->log_mark);
+      int f = -1;
+      for (int i = 0; i < s->nflow; ++i) if (s->fv[i] == u) f = i;
+      if (f >= 0) s->fexcl[f] = 1;
+      c.special[u >> 5] |= 1u << (u & 31);
+      s->c_retries += 1;
+    } else {
+      s->pod_srv[p] = u;
+      const int v0 = R.voff[r];
+      for (int e = 0; e < s->nV; ++e) {
+        const int a = s->cpod[R.src[v0 + e]], b = s->cpod[R.dst[v0 + e]];
+        int other = -1;
+        if (a == p && b != p && b < p) other = b;
+        else if (b == p && a != p && a < p) other = a;
+        if (other < 0) continue;
+        const int v = s->pod_srv[other];
+        int fp = -1;
+        for (int i = 0; i < s->nflow; ++i) if (s->fv[i] == v) fp = s->fpath[i];
+        s->vpath[e] = fp;
+      }
+    }
+  }
+}
+
 // Outputs of a non-accepted request (status 0 or -1).  All threads.
 __device__ void write_rejected(Ctx& c, const ReqsDev& R, const OutDev& O, int r, int status) {
   int c0 = R.coff[r], nC = R.coff[r + 1] - c0;
@@ -1406,8 +1559,8 @@ __device__ void pod_prologue(Ctx& c, const ReqsDev& R, int r, int p) {
     s->p = p;
     s->dc = s->pod_cpu[p];
     s->dr = s->pod_ram[p];
-    build_flows(c, R, r, p);
   }
+  if (c.warp == 0) build_flows_warp(c, R, r, p);
   clear_bitmaps(c);
   __syncthreads();
   if (c.o.path_filter && s->nflow > 0) fabric_tables(c);
@@ -1766,16 +1919,22 @@ __global__ void __launch_bounds__(1024) k_seq_cluster(Geo g, Opt o, int* state, 
         unsigned long long* fa = facc + 16 * (t & 1);
         pass_filter<false, true>(c, nullptr, nullptr, fa);  // a3 + a4 on this CTA's grid-stride share
         cl.sync();  // (1) the exact statistics of every CTA are in fa
-        if (c.tid == 0) {
-          const int nf = (int)fa[0], nact = (int)fa[1];
-          s.nf = nf;
-          s.nact = nact;
-          s.mn[0] = (int)fa[2]; s.mx[0] = (int)fa[3];
-          s.mn[1] = (int)fa[4]; s.mx[1] = (int)fa[5];
-          s.mn[2] = nact == nf ? 1 : 0; s.mx[2] = nact > 0 ? 1 : 0;  // f_u in {0,1}
-          s.mn[3] = (int)fa[6]; s.mx[3] = (int)fa[7];
-          s.sq[0] = fa[8]; s.sq[1] = fa[9]; s.sq[2] = (unsigned long long)nact; s.sq[3] = fa[10];
-          if (lead) { s.c_steps += 1; s.c_feas += (unsigned long long)nf; }
+        if (c.warp == 0) {  // the 11 accumulators in one parallel load
+          const unsigned long long fv = c.lane < 11 ? fa[c.lane] : 0ull;
+          unsigned long long f[11];
+#pragma unroll
+          for (int i = 0; i < 11; ++i) f[i] = __shfl_sync(FULL, fv, i);
+          if (c.lane == 0) {
+            const int nf = (int)f[0], nact = (int)f[1];
+            s.nf = nf;
+            s.nact = nact;
+            s.mn[0] = (int)f[2]; s.mx[0] = (int)f[3];
+            s.mn[1] = (int)f[4]; s.mx[1] = (int)f[5];
+            s.mn[2] = nact == nf ? 1 : 0; s.mx[2] = nact > 0 ? 1 : 0;  // f_u in {0,1}
+            s.mn[3] = (int)f[6]; s.mx[3] = (int)f[7];
+            s.sq[0] = f[8]; s.sq[1] = f[9]; s.sq[2] = (unsigned long long)nact; s.sq[3] = f[10];
+            if (lead) { s.c_steps += 1; s.c_feas += (unsigned long long)nf; }
+          }
         }
         if (lead) facc_reset(facc + 16 * ((t + 1) & 1), c.tid);  // read by everyone at the last attempt
         __syncthreads();
@@ -1785,10 +1944,15 @@ __global__ void __launch_bounds__(1024) k_seq_cluster(Geo g, Opt o, int* state, 
           rejected = true;
           break;
         }
-        // a5T: closeness of this CTA's feasible servers, top-2 keys into its slot
-        TopsisP tp;
-        for (int k = 0; k < 4; ++k) { tp.mx[k] = s.mx[k]; tp.mn[k] = s.mn[k]; }
-        topsis_params(tp, o.wd, s.sq);
+        // a5T: closeness of this CTA's feasible servers, top-2 keys into its slot (the
+        // parameters computed once per CTA)
+        __shared__ TopsisP tps;
+        if (c.tid == 0) {
+          for (int k = 0; k < 4; ++k) { tps.mx[k] = s.mx[k]; tps.mn[k] = s.mn[k]; }
+          topsis_params(tps, o.wd, s.sq);
+        }
+        __syncthreads();
+        const TopsisP tp = tps;
         {
           unsigned long long k1 = 0, k2 = 0;
           for (int base = (blockIdx.x * c.NW + c.warp) * 32; base < n; base += gridDim.x * c.B) {
@@ -1801,13 +1965,15 @@ __global__ void __launch_bounds__(1024) k_seq_cluster(Geo g, Opt o, int* state, 
           if (c.tid == 0) { kx[2 * q] = s.key1; kx[2 * q + 1] = s.key2; }
         }
         cl.sync();  // (2) every CTA's keys
-        if (c.tid == 0) {  // a7: argmax, lowest index on ties (R14); FP64 near-tie re-decision
-          unsigned long long k1 = 0, k2 = 0;
-          for (int i = 0; i < C; ++i) top2_merge(k1, k2, kx[2 * i], kx[2 * i + 1]);
-          const float s1 = __uint_as_float((unsigned)(k1 >> 32)), s2 = __uint_as_float((unsigned)(k2 >> 32));
-          s.best = (int)(0xFFFFFFFFu - (unsigned)(k1 & 0xFFFFFFFFull));
-          s.amb = o.exact64 || (k2 != 0ull && s1 - s2 <= kTopsisDelta);
-          s.thr = o.exact64 ? -1.0f : s1 - 2.0f * kTopsisDelta;
+        if (c.warp == 0) {  // a7: argmax, lowest index on ties (R14); FP64 near-tie re-decision
+          unsigned long long k1 = c.lane < C ? kx[2 * c.lane] : 0ull, k2 = c.lane < C ? kx[2 * c.lane + 1] : 0ull;
+          warp_top2(k1, k2);  // order-free merge: every lane holds the cluster's top-2
+          if (c.lane == 0) {
+            const float s1 = __uint_as_float((unsigned)(k1 >> 32)), s2 = __uint_as_float((unsigned)(k2 >> 32));
+            s.best = (int)(0xFFFFFFFFu - (unsigned)(k1 & 0xFFFFFFFFull));
+            s.amb = o.exact64 || (k2 != 0ull && s1 - s2 <= kTopsisDelta);
+            s.thr = o.exact64 ? -1.0f : s1 - 2.0f * kTopsisDelta;
+          }
         }
         __syncthreads();
         if (s.amb) {
@@ -1834,7 +2000,7 @@ __global__ void __launch_bounds__(1024) k_seq_cluster(Geo g, Opt o, int* state, 
           }
           __syncthreads();
         }
-        if (lead && c.warp == 0) commit(c, R, r, p);  // a8 on the live state (R16-R18)
+        if (lead) commit_cta(c, R, r, p);  // a8 on the live state (R16-R18)
         cl.sync();  // (3) the commit (or its undo) is visible; the leader's verdict over DSMEM
         if (c.tid == 0 && !lead) {
           const Scratch* ls = cl.map_shared_rank(&s, 0);
