@@ -515,6 +515,13 @@ def cold_states(snap: dict, B: int, seed: int = 1):
 COLD = (("C4 geometry", 32, 4096), ("C5 geometry", 64, 512))
 
 
+def cold_traffic(k: int, B: int):
+    """DRAM bytes per launch of k_rank_occ from the committed ncu capture (k = 32, B = 4096)."""
+    if (k, B) != (32, 4096) or not os.path.exists(TRAFFIC):
+        return None
+    return json.load(open(TRAFFIC)).get("k_rank_occ", {}).get("dram_bytes_per_launch")
+
+
 def measure_cold(args, ctx, dev, stream, flush, barrier, max_over_ranks, sum_over_ranks, pk, pk_kind):
     """standalone TOPSIS ranking on COLD snapshots against HBM: one
     nacs_rank_topsis_many call ranks one pod step (the request's first: demand, no flows) on each
@@ -553,7 +560,7 @@ def measure_cold(args, ctx, dev, stream, flush, barrier, max_over_ranks, sum_ove
                      "states_per_s": sum_over_ranks(B) / (ms / 1e3), "ms_per_step": ms,
                      "fp64_decisions": stats["fp64_decisions"], "gpu_launches": 1,
                      "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
-                                  "traffic": None, "kernel": "k_rank_occ (nacs_rank.cu)",
+                                  "traffic": cold_traffic(k, B), "kernel": "k_rank_occ (nacs_rank.cu)",
                                   "bytes": "16 B read + 4 B score written per server",
                                   "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({pk_kind})"}}
     return res

@@ -1906,15 +1906,62 @@ __global__ void __launch_bounds__(1024) k_seq_cluster(Geo g, Opt o, int* state, 
   init_minfab(c);  // every CTA reads the same state: the same bound
   cl.sync();
   int t = 0;  // attempt counter (the same in every CTA)
-  for (int r = 0; r < R.n; ++r) {
-    req_begin<1>(c, R, r, true);
+  // the current request's arrays in shared memory (one parallel copy per request: the
+  // thread-0 loops of decode, flows, commit and top-up then read on-chip), presented to the
+  // device functions as a one-request batch (r = 0) with offset output pointers
+  __shared__ int rq[5 * MAXC + 4 * MAXV];
+  __shared__ int roff[4];
+  for (int rg = 0; rg < R.n; ++rg) {
+    const int c0 = R.coff[rg], nC = R.coff[rg + 1] - c0, v0 = R.voff[rg], nV = R.voff[rg + 1] - v0;
+    const bool local = nC >= 0 && nC <= MAXC && nV >= 0 && nV <= MAXV;
+    ReqsDev RL = R;
+    OutDev OL = O;
+    int r = rg;
+    if (local) {
+      for (int i = c.tid; i < nC; i += c.B) {
+        rq[i] = R.cpu_min[c0 + i];
+        rq[MAXC + i] = R.cpu_max[c0 + i];
+        rq[2 * MAXC + i] = R.ram_min[c0 + i];
+        rq[3 * MAXC + i] = R.ram_max[c0 + i];
+        rq[4 * MAXC + i] = R.pod_of[c0 + i];
+      }
+      for (int e = c.tid; e < nV; e += c.B) {
+        rq[5 * MAXC + e] = R.src[v0 + e];
+        rq[5 * MAXC + MAXV + e] = R.dst[v0 + e];
+        rq[5 * MAXC + 2 * MAXV + e] = R.bw_min[v0 + e];
+        rq[5 * MAXC + 3 * MAXV + e] = R.bw_max[v0 + e];
+      }
+      if (c.tid == 0) { roff[0] = 0; roff[1] = nC; roff[2] = 0; roff[3] = nV; }
+      RL.n = 1;
+      RL.coff = roff;
+      RL.voff = roff + 2;
+      RL.cpu_min = rq;
+      RL.cpu_max = rq + MAXC;
+      RL.ram_min = rq + 2 * MAXC;
+      RL.ram_max = rq + 3 * MAXC;
+      RL.pod_of = rq + 4 * MAXC;
+      RL.src = rq + 5 * MAXC;
+      RL.dst = rq + 5 * MAXC + MAXV;
+      RL.bw_min = rq + 5 * MAXC + 2 * MAXV;
+      RL.bw_max = rq + 5 * MAXC + 3 * MAXV;
+      OL.status = O.status + rg;
+      OL.server = O.server + c0;
+      OL.cpu_a = O.cpu_a + c0;
+      OL.ram_a = O.ram_a + c0;
+      OL.bw_a = O.bw_a + v0;
+      OL.path = O.path + v0;
+      r = 0;
+      __syncthreads();
+    }
+    req_begin<1>(c, RL, r, true);
     if (!s.req_ok) {
-      if (lead) write_rejected(c, R, O, r, -1);
+      if (lead) write_rejected(c, RL, OL, r, -1);
+      __syncthreads();  // the shared request copy is rewritten by the next request
       continue;
     }
     bool rejected = false;
     for (int p = 0; p < s.P && !rejected; ++p) {
-      pod_prologue(c, R, r, p);
+      pod_prologue(c, RL, r, p);
       for (;;) {
         unsigned long long* fa = facc + 16 * (t & 1);
         pass_filter<false, true>(c, nullptr, nullptr, fa);  // a3 + a4 on this CTA's grid-stride share
@@ -1940,7 +1987,7 @@ __global__ void __launch_bounds__(1024) k_seq_cluster(Geo g, Opt o, int* state, 
         __syncthreads();
         ++t;
         if (s.nf == 0) {  // F empty: reject the request atomically (R20)
-          if (lead) req_reject(c, R, O, r);
+          if (lead) req_reject(c, RL, OL, r);
           rejected = true;
           break;
         }
@@ -2000,7 +2047,7 @@ __global__ void __launch_bounds__(1024) k_seq_cluster(Geo g, Opt o, int* state, 
           }
           __syncthreads();
         }
-        if (lead) commit_cta(c, R, r, p);  // a8 on the live state (R16-R18)
+        if (lead) commit_cta(c, RL, r, p);  // a8 on the live state (R16-R18)
         cl.sync();  // (3) the commit (or its undo) is visible; the leader's verdict over DSMEM
         if (c.tid == 0 && !lead) {
           const Scratch* ls = cl.map_shared_rank(&s, 0);
@@ -2018,7 +2065,7 @@ __global__ void __launch_bounds__(1024) k_seq_cluster(Geo g, Opt o, int* state, 
         if (!s.fail) break;
       }
     }
-    if (!rejected && lead) req_finish(c, R, O, r, true);  // a9: top-up (R19), outputs
+    if (!rejected && lead) req_finish(c, RL, OL, r, true);  // a9: top-up (R19), outputs
     cl.sync();  // (4) the request's top-up / rollback is visible before the next one reads the state
     if (c.tid == 0 && !lead) s.minfab = cl.map_shared_rank(&s, 0)->minfab;
     __syncthreads();
