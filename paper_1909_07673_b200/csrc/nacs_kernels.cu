@@ -22,6 +22,7 @@
 #include <cooperative_groups.h>
 
 #include <cfloat>
+#include <cstdio>
 #include <cstdlib>
 #include <climits>
 #include <cstdint>
@@ -147,6 +148,15 @@ __device__ __forceinline__ void st_set(Ctx& c, int off, int val) {
       s->ntouched += 1;
     }
   }
+}
+// st_set with the word's current value already known (no reload: on global state a reload
+// after the previous store costs a full L2 round trip in the thread-0 commit chain)
+__device__ __forceinline__ void st_set_v(Ctx& c, int off, int old, int val) {
+  Scratch* s = c.s;
+  c.ulog[s->log_n] = make_int2(off, old);
+  s->log_n += 1;
+  c.st[off] = val;
+  if (off >= 4 * c.g.n && val < s->minfab) s->minfab = val;
 }
 __device__ __forceinline__ void undo_to(Ctx& c, int mark) {
   Scratch* s = c.s;
@@ -435,58 +445,15 @@ __device__ void fabric_tables(Ctx& c) {
 // each CTA reduces in its own shared memory and combines into facc[11] with integer atomics
 // (nf, nact, min/max of CPU, RAM, bandwidth, sums of squares — exact, order-independent);
 // k_sh_prep_b then moves facc into the scratch fields.
-template <bool WRITE_MASK, bool GRID = false>
-__device__ void pass_filter(Ctx& c, uint8_t* mask_out, float* scores_out, unsigned long long* facc = nullptr) {
+// a4's reductions of pass_filter: per-thread statistics -> the CTA's (scratch) or, with GRID,
+// the grid's (exact integer atomics into facc).  All threads.
+template <bool GRID>
+__device__ void filter_reduce(Ctx& c, int nf, int nact, unsigned mn0, unsigned mx0, unsigned mn1, unsigned mx1,
+                              unsigned mn3, unsigned mx3, unsigned long long q0, unsigned long long q1,
+                              unsigned long long q3, unsigned long long* facc) {
   __shared__ int g_red_i[GRID ? MAXW : 1][8];
   __shared__ unsigned long long g_red_u[GRID ? MAXW : 1][3];
   Scratch* s = c.s;
-  const Geo& g = c.g;
-  const int n = g.n;
-  const int* cpu = c.st;
-  const int* ram = c.st + n;
-  const int* act = c.st + 2 * n;
-  const int* acc = c.st + 3 * n;     // access-link residuals: the filter (Eq. 5-7)
-  const int* bwc = c.cr + 3 * n;     // the Bandwidth criterion (R2, or its logical reading)
-  const int dc = s->dc, dr = s->dr, sumD = s->sumD;
-  const bool net = c.o.path_filter && s->nflow > 0;
-  const bool G = s->G != 0;
-  int nf = 0, nact = 0;
-  unsigned mn0 = UINT_MAX, mn1 = UINT_MAX, mn3 = UINT_MAX, mx0 = 0, mx1 = 0, mx3 = 0;
-  unsigned long long q0 = 0, q1 = 0, q3 = 0;
-  const int start = GRID ? (blockIdx.x * c.NW + c.warp) * 32 : c.warp * 32;
-  const int stride = GRID ? gridDim.x * c.B : c.B;
-  for (int base = start; base < n; base += stride) {
-    int u = base + c.lane;
-    bool in = u < n;
-    int x0 = 0, x1 = 0, x2 = 0, x3 = 0;
-    if (in) { x0 = cpu[u]; x1 = ram[u]; x2 = act[u]; x3 = bwc[u]; }
-    bool ok = in && x0 >= dc && x1 >= dr;
-    if (net) {
-      unsigned e = div_h((unsigned)u, g.magic_h);
-      ok = ok && G && acc[u] >= sumD && !((c.edgebad[e >> 5] >> (e & 31)) & 1u);
-    }
-    unsigned sp = c.special[base >> 5];
-    if ((sp >> c.lane) & 1u) {
-      // a flow server (its own flow needs no network) or an excluded server (R18)
-      int f = -1;
-      for (int i = 0; i < s->nflow; ++i) if (s->fv[i] == u) f = i;
-      if (f < 0 || s->fexcl[f]) ok = false;
-      else ok = x0 >= dc && x1 >= dr && (!c.o.path_filter || s->fok[f]);
-    }
-    unsigned bal = __ballot_sync(FULL, ok);
-    if (c.lane == 0) c.maskw[base >> 5] = bal;
-    if (WRITE_MASK && in) { mask_out[u] = ok ? 1 : 0; scores_out[u] = 0.0f; }
-    if (ok) {
-      nf += 1;
-      nact += x2;
-      mn0 = min(mn0, (unsigned)x0); mx0 = max(mx0, (unsigned)x0);
-      mn1 = min(mn1, (unsigned)x1); mx1 = max(mx1, (unsigned)x1);
-      mn3 = min(mn3, (unsigned)x3); mx3 = max(mx3, (unsigned)x3);
-      q0 += (unsigned long long)((unsigned)x0) * (unsigned)x0;
-      q1 += (unsigned long long)((unsigned)x1) * (unsigned)x1;
-      q3 += (unsigned long long)((unsigned)x3) * (unsigned)x3;
-    }
-  }
   // warp reductions (redux.sync for 32-bit, shuffles for 64-bit sums)
   nf = (int)__reduce_add_sync(FULL, (unsigned)nf);
   nact = (int)__reduce_add_sync(FULL, (unsigned)nact);
@@ -548,6 +515,59 @@ __device__ void pass_filter(Ctx& c, uint8_t* mask_out, float* scores_out, unsign
     }
   }
   __syncthreads();
+}
+
+template <bool WRITE_MASK, bool GRID = false>
+__device__ void pass_filter(Ctx& c, uint8_t* mask_out, float* scores_out, unsigned long long* facc = nullptr) {
+  Scratch* s = c.s;
+  const Geo& g = c.g;
+  const int n = g.n;
+  const int* cpu = c.st;
+  const int* ram = c.st + n;
+  const int* act = c.st + 2 * n;
+  const int* acc = c.st + 3 * n;     // access-link residuals: the filter (Eq. 5-7)
+  const int* bwc = c.cr + 3 * n;     // the Bandwidth criterion (R2, or its logical reading)
+  const int dc = s->dc, dr = s->dr, sumD = s->sumD;
+  const bool net = c.o.path_filter && s->nflow > 0;
+  const bool G = s->G != 0;
+  int nf = 0, nact = 0;
+  unsigned mn0 = UINT_MAX, mn1 = UINT_MAX, mn3 = UINT_MAX, mx0 = 0, mx1 = 0, mx3 = 0;
+  unsigned long long q0 = 0, q1 = 0, q3 = 0;
+  const int start = GRID ? (blockIdx.x * c.NW + c.warp) * 32 : c.warp * 32;
+  const int stride = GRID ? gridDim.x * c.B : c.B;
+  for (int base = start; base < n; base += stride) {
+    int u = base + c.lane;
+    bool in = u < n;
+    int x0 = 0, x1 = 0, x2 = 0, x3 = 0;
+    if (in) { x0 = cpu[u]; x1 = ram[u]; x2 = act[u]; x3 = bwc[u]; }
+    bool ok = in && x0 >= dc && x1 >= dr;
+    if (net) {
+      unsigned e = div_h((unsigned)u, g.magic_h);
+      ok = ok && G && acc[u] >= sumD && !((c.edgebad[e >> 5] >> (e & 31)) & 1u);
+    }
+    unsigned sp = c.special[base >> 5];
+    if ((sp >> c.lane) & 1u) {
+      // a flow server (its own flow needs no network) or an excluded server (R18)
+      int f = -1;
+      for (int i = 0; i < s->nflow; ++i) if (s->fv[i] == u) f = i;
+      if (f < 0 || s->fexcl[f]) ok = false;
+      else ok = x0 >= dc && x1 >= dr && (!c.o.path_filter || s->fok[f]);
+    }
+    unsigned bal = __ballot_sync(FULL, ok);
+    if (c.lane == 0) c.maskw[base >> 5] = bal;
+    if (WRITE_MASK && in) { mask_out[u] = ok ? 1 : 0; scores_out[u] = 0.0f; }
+    if (ok) {
+      nf += 1;
+      nact += x2;
+      mn0 = min(mn0, (unsigned)x0); mx0 = max(mx0, (unsigned)x0);
+      mn1 = min(mn1, (unsigned)x1); mx1 = max(mx1, (unsigned)x1);
+      mn3 = min(mn3, (unsigned)x3); mx3 = max(mx3, (unsigned)x3);
+      q0 += (unsigned long long)((unsigned)x0) * (unsigned)x0;
+      q1 += (unsigned long long)((unsigned)x1) * (unsigned)x1;
+      q3 += (unsigned long long)((unsigned)x3) * (unsigned)x3;
+    }
+  }
+  filter_reduce<GRID>(c, nf, nact, mn0, mx0, mn1, mx1, mn3, mx3, q0, q1, q3, facc);
 }
 
 // ------------------------------------------------------------ TOPSIS --------
@@ -1439,12 +1459,16 @@ __device__ void commit_cta(Ctx& c, const ReqsDev& R, int r, int p) {
   const Geo& g = c.g;
   const int n = g.n;
   const int u = s->best;
-  if (c.tid == 0) {
-    s->log_mark = s->log_n;
-    st_set(c, u, c.st[u] - s->dc);
-    st_set(c, n + u, c.st[n + u] - s->dr);
-    st_set(c, 2 * n + u, 1);
-    s->fail = 0;
+  if (c.warp == 0) {  // the server's three words read in parallel, applied by lane 0 (no AHP dirty list here)
+    const int w = c.lane == 0 ? c.st[u] : c.lane == 1 ? c.st[n + u] : c.lane == 2 ? c.st[2 * n + u] : 0;
+    const int x0 = __shfl_sync(FULL, w, 0), x1 = __shfl_sync(FULL, w, 1), x2 = __shfl_sync(FULL, w, 2);
+    if (c.lane == 0) {
+      s->log_mark = s->log_n;
+      st_set_v(c, u, x0, x0 - s->dc);
+      st_set_v(c, n + u, x1, x1 - s->dr);
+      st_set_v(c, 2 * n + u, x2, 1);
+      s->fail = 0;
+    }
   }
   __syncthreads();
   for (int f = 0; f < s->nflow; ++f) {
@@ -1454,17 +1478,23 @@ __device__ void commit_cta(Ctx& c, const ReqsDev& R, int r, int p) {
       continue;
     }
     const int2 wp = widest_path_cta(c, u, v);  // ends with __syncthreads: earlier deductions seen
-    if (c.tid == 0) {
-      const int bott = min(min(c.st[3 * n + u], c.st[3 * n + v]), wp.y);
-      if (bott < D) {
-        s->fail = 1;
-      } else {
-        st_set(c, 3 * n + u, c.st[3 * n + u] - D);
-        st_set(c, 3 * n + v, c.st[3 * n + v] - D);
-        int off[4];
-        const int m = path_links(g, u, v, wp.x, off);
-        for (int t = 0; t < m; ++t) st_set(c, off[t], c.st[off[t]] - D);
-        s->fpath[f] = wp.x;
+    if (c.warp == 0) {  // the path's words (2 access + up to 4 fabric) read by lanes 0..5 at once
+      int off[6];
+      off[0] = 3 * n + u;
+      off[1] = 3 * n + v;
+      const int m = path_links(g, u, v, wp.x, off + 2);
+      const int val = c.lane < 2 + m ? c.st[off[c.lane < 6 ? c.lane : 0]] : 0;
+      int x[6];
+#pragma unroll
+      for (int i = 0; i < 6; ++i) x[i] = __shfl_sync(FULL, val, i);
+      if (c.lane == 0) {
+        const int bott = min(min(x[0], x[1]), wp.y);
+        if (bott < D) {
+          s->fail = 1;
+        } else {
+          for (int i = 0; i < 2 + m; ++i) st_set_v(c, off[i], x[i], x[i] - D);
+          s->fpath[f] = wp.x;
+        }
       }
     }
     __syncthreads();
@@ -1874,6 +1904,81 @@ __device__ __forceinline__ void facc_reset(unsigned long long* f, int tid) {
   if (tid < 11) f[tid] = (tid >= 2 && tid <= 7 && !(tid & 1)) ? ~0ull : 0ull;
 }
 
+// k_seq_cluster's a3 + a4: pass_filter's test on this CTA's grid-stride share of at most
+// SQ_J servers per thread, with every row of the share loaded up front (one L2 round trip
+// instead of one per stride) and kept in registers for the scoring pass.
+constexpr int SQ_J = 4;
+__device__ __forceinline__ void seqc_filter(Ctx& c, unsigned long long* facc, int (&x)[SQ_J][4], unsigned& okb) {
+  Scratch* s = c.s;
+  const Geo& g = c.g;
+  const int n = g.n;
+  const int dc = s->dc, dr = s->dr, sumD = s->sumD;
+  const bool net = c.o.path_filter && s->nflow > 0;
+  const bool G = s->G != 0;
+  const int start = (blockIdx.x * c.NW + c.warp) * 32, stride = gridDim.x * c.B;
+#pragma unroll
+  for (int j = 0; j < SQ_J; ++j) {
+    const int u = start + j * stride + c.lane;
+    const bool in = u < n;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) x[j][q] = in ? c.st[q * n + u] : 0;
+  }
+  int nf = 0, nact = 0;
+  unsigned mn0 = UINT_MAX, mn1 = UINT_MAX, mn3 = UINT_MAX, mx0 = 0, mx1 = 0, mx3 = 0;
+  unsigned long long q0 = 0, q1 = 0, q3 = 0;
+  okb = 0;
+#pragma unroll
+  for (int j = 0; j < SQ_J; ++j) {
+    const int base = start + j * stride;
+    if (base >= n) break;  // warp-uniform
+    const int u = base + c.lane;
+    const bool in = u < n;
+    const int x0 = x[j][0], x1 = x[j][1], x2 = x[j][2], x3 = x[j][3];
+    bool ok = in && x0 >= dc && x1 >= dr;
+    if (net) {
+      const unsigned e = div_h((unsigned)u, g.magic_h);
+      ok = ok && G && x3 >= sumD && !((c.edgebad[e >> 5] >> (e & 31)) & 1u);
+    }
+    const unsigned sp = c.special[base >> 5];
+    if ((sp >> c.lane) & 1u) {  // a flow server (its own flow needs no network) or an excluded one (R18)
+      int f = -1;
+      for (int i = 0; i < s->nflow; ++i) if (s->fv[i] == u) f = i;
+      if (f < 0 || s->fexcl[f]) ok = false;
+      else ok = x0 >= dc && x1 >= dr && (!c.o.path_filter || s->fok[f]);
+    }
+    const unsigned bal = __ballot_sync(FULL, ok);
+    if (c.lane == 0) c.maskw[base >> 5] = bal;
+    okb |= (ok ? 1u : 0u) << j;
+    if (ok) {
+      nf += 1;
+      nact += x2;
+      mn0 = min(mn0, (unsigned)x0); mx0 = max(mx0, (unsigned)x0);
+      mn1 = min(mn1, (unsigned)x1); mx1 = max(mx1, (unsigned)x1);
+      mn3 = min(mn3, (unsigned)x3); mx3 = max(mx3, (unsigned)x3);
+      q0 += (unsigned long long)((unsigned)x0) * (unsigned)x0;
+      q1 += (unsigned long long)((unsigned)x1) * (unsigned)x1;
+      q3 += (unsigned long long)((unsigned)x3) * (unsigned)x3;
+    }
+  }
+  filter_reduce<true>(c, nf, nact, mn0, mx0, mn1, mx1, mn3, mx3, q0, q1, q3, facc);
+}
+
+#ifdef NACS_SEQC_PROF  // experiment builds: per-phase time of the leader CTA (device printf at the end)
+#define SEQC_T(i)                                                                  \
+  do {                                                                             \
+    if (lead && c.tid == 0) {                                                      \
+      unsigned long long now_;                                                     \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now_));                     \
+      prof_[i] += now_ - prof_last_;                                               \
+      prof_last_ = now_;                                                           \
+    }                                                                              \
+  } while (0)
+#else
+#define SEQC_T(i) \
+  do {            \
+  } while (0)
+#endif
+
 __global__ void __launch_bounds__(1024) k_seq_cluster(Geo g, Opt o, int* state, ReqsDev R, OutDev O, int2* ulog,
                                                       unsigned long long* stats, unsigned long long* facc,
                                                       unsigned long long* kx, double* kxv, int* kxi) {
@@ -1906,6 +2011,10 @@ __global__ void __launch_bounds__(1024) k_seq_cluster(Geo g, Opt o, int* state, 
   init_minfab(c);  // every CTA reads the same state: the same bound
   cl.sync();
   int t = 0;  // attempt counter (the same in every CTA)
+#ifdef NACS_SEQC_PROF
+  unsigned long long prof_[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0}, prof_last_ = 0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(prof_last_));
+#endif
   // the current request's arrays in shared memory (one parallel copy per request: the
   // thread-0 loops of decode, flows, commit and top-up then read on-chip), presented to the
   // device functions as a one-request batch (r = 0) with offset output pointers
@@ -1953,7 +2062,9 @@ __global__ void __launch_bounds__(1024) k_seq_cluster(Geo g, Opt o, int* state, 
       r = 0;
       __syncthreads();
     }
+    SEQC_T(0);
     req_begin<1>(c, RL, r, true);
+    SEQC_T(1);
     if (!s.req_ok) {
       if (lead) write_rejected(c, RL, OL, r, -1);
       __syncthreads();  // the shared request copy is rewritten by the next request
@@ -1962,10 +2073,15 @@ __global__ void __launch_bounds__(1024) k_seq_cluster(Geo g, Opt o, int* state, 
     bool rejected = false;
     for (int p = 0; p < s.P && !rejected; ++p) {
       pod_prologue(c, RL, r, p);
+      SEQC_T(2);
       for (;;) {
         unsigned long long* fa = facc + 16 * (t & 1);
-        pass_filter<false, true>(c, nullptr, nullptr, fa);  // a3 + a4 on this CTA's grid-stride share
+        int xr[SQ_J][4];
+        unsigned okb;
+        seqc_filter(c, fa, xr, okb);  // a3 + a4 on this CTA's grid-stride share (rows kept in registers)
+        SEQC_T(3);
         cl.sync();  // (1) the exact statistics of every CTA are in fa
+        SEQC_T(4);
         if (c.warp == 0) {  // the 11 accumulators in one parallel load
           const unsigned long long fv = c.lane < 11 ? fa[c.lane] : 0ull;
           unsigned long long f[11];
@@ -2002,16 +2118,19 @@ __global__ void __launch_bounds__(1024) k_seq_cluster(Geo g, Opt o, int* state, 
         const TopsisP tp = tps;
         {
           unsigned long long k1 = 0, k2 = 0;
-          for (int base = (blockIdx.x * c.NW + c.warp) * 32; base < n; base += gridDim.x * c.B) {
-            if (!((c.maskw[base >> 5] >> c.lane) & 1u)) continue;
-            const int u = base + c.lane;
-            const float rr = topsis32(tp, c.st[u], c.st[n + u], c.st[2 * n + u], c.st[3 * n + u]);
+#pragma unroll
+          for (int j = 0; j < SQ_J; ++j) {
+            if (!((okb >> j) & 1u)) continue;
+            const int u = (blockIdx.x * c.NW + c.warp) * 32 + j * gridDim.x * c.B + c.lane;
+            const float rr = topsis32(tp, xr[j][0], xr[j][1], xr[j][2], xr[j][3]);
             top2_insert(k1, k2, score_key(rr, u));
           }
           block_top2(c, k1, k2);
           if (c.tid == 0) { kx[2 * q] = s.key1; kx[2 * q + 1] = s.key2; }
         }
+        SEQC_T(5);
         cl.sync();  // (2) every CTA's keys
+        SEQC_T(6);
         if (c.warp == 0) {  // a7: argmax, lowest index on ties (R14); FP64 near-tie re-decision
           unsigned long long k1 = c.lane < C ? kx[2 * c.lane] : 0ull, k2 = c.lane < C ? kx[2 * c.lane + 1] : 0ull;
           warp_top2(k1, k2);  // order-free merge: every lane holds the cluster's top-2
@@ -2026,10 +2145,11 @@ __global__ void __launch_bounds__(1024) k_seq_cluster(Geo g, Opt o, int* state, 
         if (s.amb) {
           double bv = -DBL_MAX;
           int bj = -1;
-          for (int base = (blockIdx.x * c.NW + c.warp) * 32; base < n; base += gridDim.x * c.B) {
-            if (!((c.maskw[base >> 5] >> c.lane) & 1u)) continue;
-            const int u = base + c.lane;
-            const int x0 = c.st[u], x1 = c.st[n + u], x2 = c.st[2 * n + u], x3 = c.st[3 * n + u];
+#pragma unroll
+          for (int j = 0; j < SQ_J; ++j) {
+            if (!((okb >> j) & 1u)) continue;
+            const int u = (blockIdx.x * c.NW + c.warp) * 32 + j * gridDim.x * c.B + c.lane;
+            const int x0 = xr[j][0], x1 = xr[j][1], x2 = xr[j][2], x3 = xr[j][3];
             if (topsis32(tp, x0, x1, x2, x3) < s.thr) continue;
             const double rr = topsis64(tp, x0, x1, x2, x3);
             if (rr > bv || (rr == bv && u < bj)) { bv = rr; bj = u; }
@@ -2047,8 +2167,11 @@ __global__ void __launch_bounds__(1024) k_seq_cluster(Geo g, Opt o, int* state, 
           }
           __syncthreads();
         }
+        SEQC_T(7);
         if (lead) commit_cta(c, RL, r, p);  // a8 on the live state (R16-R18)
+        SEQC_T(8);
         cl.sync();  // (3) the commit (or its undo) is visible; the leader's verdict over DSMEM
+        SEQC_T(4);
         if (c.tid == 0 && !lead) {
           const Scratch* ls = cl.map_shared_rank(&s, 0);
           const int u = s.best;
@@ -2065,12 +2188,20 @@ __global__ void __launch_bounds__(1024) k_seq_cluster(Geo g, Opt o, int* state, 
         if (!s.fail) break;
       }
     }
+    SEQC_T(9);
     if (!rejected && lead) req_finish(c, RL, OL, r, true);  // a9: top-up (R19), outputs
+    SEQC_T(9);
     cl.sync();  // (4) the request's top-up / rollback is visible before the next one reads the state
+    SEQC_T(4);
     if (c.tid == 0 && !lead) s.minfab = cl.map_shared_rank(&s, 0)->minfab;
     __syncthreads();
   }
   if (lead) flush_stats(c, stats);
+#ifdef NACS_SEQC_PROF
+  if (lead && c.tid == 0)
+    printf("seqc ns: copy+begin %llu %llu prologue %llu filter %llu barriers %llu score %llu merge %llu commit %llu finish %llu\n",
+           prof_[0], prof_[1], prof_[2], prof_[3], prof_[4], prof_[5], prof_[6] + prof_[7], prof_[8], prof_[9]);
+#endif
   cl.sync();  // no CTA leaves while another may still read its shared memory
 }
 
@@ -3423,9 +3554,12 @@ cudaError_t launch_sequential(const Geo& g, const Opt& o, int* d_state, const Re
 }
 
 int seq_cluster_size(const Geo& g) {
-  if (const char* e = getenv("NACS_SEQC")) return atoi(e);  // experiments (0 = off)
-  if (g.n < 16384) return 0;  // below: the one-CTA engine keeps the live state in shared memory
-  return g.n >= 65536 ? 16 : 8;
+  if (const char* e = getenv("NACS_SEQC")) {  // experiments (0 = off)
+    const int C = atoi(e);
+    return C > 0 && C <= 16 && (long long)C * 1024 * SQ_J >= g.n ? C : 0;
+  }
+  if (g.n < 16384 || g.n > 65536) return 0;  // below: the one-CTA engine keeps the state in shared memory
+  return g.n > 32768 ? 16 : 8;  // at most SQ_J = 4 servers per thread (1024 threads per CTA)
 }
 
 cudaError_t launch_seq_cluster(const Geo& g, const Opt& o, int* d_state, const ReqsDev& R, const OutDev& O,
