@@ -111,6 +111,24 @@ __device__ __forceinline__ double topsis64(const TopsisP& t, int x0, int x1, int
   return (ep + em) > 0 ? em / (ep + em) : 0.0;
 }
 
+// TOPSIS parameters from the per-criterion scales sd_c = w_c / ||x_c|| (mx, mn already set).
+__device__ __forceinline__ void topsis_params_sd(TopsisP& t, const double sdv[4]) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const double sd = sdv[c];
+    t.sd[c] = sd;
+    t.sf[c] = (float)sd;
+    t.s2p23[c] = (float)sd * 8388608.0f;
+    t.mxb[c] = 0x4B000000 + t.mx[c];
+    t.mnb[c] = 0x4B000000 - t.mn[c];
+  }
+  const float q2 = __fmul_rn(t.sf[2], t.sf[2]);
+  t.p2sq[0] = t.mx[2] - 0 ? q2 : 0.f;
+  t.p2sq[1] = t.mx[2] - 1 ? q2 : 0.f;
+  t.m2sq[0] = 0 - t.mn[2] ? q2 : 0.f;
+  t.m2sq[1] = 1 - t.mn[2] ? q2 : 0.f;
+}
+
 // Statistics -> TOPSIS parameters (R12): ||x_c|| = sqrt(sum over F of x_c^2), exact sums.
 __device__ __forceinline__ void topsis_params(TopsisP& t, const double w[4], const unsigned long long sq[4]) {
 #pragma unroll

@@ -2110,9 +2110,17 @@ __global__ void __launch_bounds__(1024) k_seq_cluster(Geo g, Opt o, int* state, 
         // a5T: closeness of this CTA's feasible servers, top-2 keys into its slot (the
         // parameters computed once per CTA)
         __shared__ TopsisP tps;
-        if (c.tid == 0) {
-          for (int k = 0; k < 4; ++k) { tps.mx[k] = s.mx[k]; tps.mn[k] = s.mn[k]; }
-          topsis_params(tps, o.wd, s.sq);
+        if (c.warp == 0) {  // lane k < 4: criterion k's FP64 norm and scale in parallel (R12)
+          const int k = c.lane & 3;
+          const double N = sqrt((double)s.sq[k]);
+          const double sdk = N > 0 ? o.wd[k] / N : 0.0;
+          double sd[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) sd[q] = __shfl_sync(FULL, sdk, q);
+          if (c.lane == 0) {
+            for (int q = 0; q < 4; ++q) { tps.mx[q] = s.mx[q]; tps.mn[q] = s.mn[q]; }
+            topsis_params_sd(tps, sd);
+          }
         }
         __syncthreads();
         const TopsisP tp = tps;
