@@ -662,8 +662,8 @@ __device__ __forceinline__ WStats ws_identity() {
 // TMA is issued at once (async proxy: the cluster barrier does not wait for it), so the load
 // of state b + #clusters overlaps the whole ranking of state b.
 // =====================================================================================
-constexpr int RO_T = 256, RO_NW = RO_T / 32, RO_V = 16, RO_NJ = RO_V / 4;
-static_assert(RO_T * RO_V == RM_S, "one slice per CTA");
+constexpr int RO_V = 16, RO_NJ = RO_V / 4;  // servers per thread; the CTA has T threads (128 or 256)
+constexpr int RO_MAXW = 8;
 
 struct RoKey {  // top-2 entry: b = FP32 closeness bits + 1 (0 = none), i = its server, b2 = runner-up bits + 1
   unsigned b1;
@@ -672,13 +672,13 @@ struct RoKey {  // top-2 entry: b = FP32 closeness bits + 1 (0 = none), i = its 
 };
 struct RoShared {
   WStats cs[2];                 // the CTA's statistics of a state (shared-memory atomics of its warps)
-  RoKey ks[2][RO_NW];           // per-warp top-2 entries
+  RoKey ks[2][RO_MAXW];         // per-warp top-2 entries
   TopsisP tp[2];
   int NF[2], BAD[2], state[2];
   double argv;
   int argj, best, amb;
-  double rd[RO_NW];
-  int rj[RO_NW];
+  double rd[RO_MAXW];
+  int rj[RO_MAXW];
   unsigned long long cnt[4];
   __align__(8) unsigned long long full;
 };
@@ -768,10 +768,11 @@ __device__ void ro_params(const RankManyArgs& a, const RmThread& t, RoShared& sm
 }
 
 // top-2 of slot q's state from the C x 8 warp entries; ambiguity (gap <= 2^-17)
+template <int NW>
 __device__ void ro_keys(const RankManyArgs& a, const RmThread& t, RoShared& sm, cg::cluster_group& cl, int q) {
   RoKey e;
   e.b1 = 0; e.i1 = 0x7FFFFFFF; e.b2 = 0;
-  for (int j = t.lane; j < t.C * RO_NW; j += 32) e = rokey_merge(e, *cl.map_shared_rank(&sm.ks[q][j % RO_NW], j / RO_NW));
+  for (int j = t.lane; j < t.C * NW; j += 32) e = rokey_merge(e, *cl.map_shared_rank(&sm.ks[q][j % NW], j / NW));
   e = rokey_warp(e);
   if (t.lane == 0) {
     const float s1 = __uint_as_float(e.b1 - 1u), s2 = __uint_as_float(e.b2 - 1u);
@@ -784,7 +785,9 @@ __device__ void ro_keys(const RankManyArgs& a, const RmThread& t, RoShared& sm, 
 
 // Finish slot q's state after ro_keys: FP64 re-decision when ambiguous (the state's slice is
 // read again; two more cluster barriers; every CTA takes the branch), then rank 0 writes.
+template <int T>
 __device__ void ro_finish(const RankManyArgs& a, const RmThread& t, RoShared& sm, cg::cluster_group& cl, int q) {
+  constexpr int NW = T / 32;
   const bool amb = sm.amb;
   const int b = sm.state[q];
   if (amb) {
@@ -794,7 +797,7 @@ __device__ void ro_finish(const RankManyArgs& a, const RmThread& t, RoShared& sm
     const int* st = a.states + (long long)b * a.stride;
     double bv = -DBL_MAX;
     int bj = -1;
-    for (int u = t.lo + t.tid; u < t.hi; u += RO_T) {
+    for (int u = t.lo + t.tid; u < t.hi; u += T) {
       const int x0 = st[u], x1 = st[n + u], x2 = st[2 * n + u], x3 = st[3 * n + u];
       if (!(x0 >= a.dc && x1 >= a.dr)) continue;
       if (topsis32f(tp, x0, x1, x2, x3) < thr) continue;
@@ -806,8 +809,8 @@ __device__ void ro_finish(const RankManyArgs& a, const RmThread& t, RoShared& sm
     if (t.lane == 0) { sm.rd[t.warp] = bv; sm.rj[t.warp] = bj; }
     __syncthreads();
     if (t.warp == 0) {
-      bv = t.lane < RO_NW ? sm.rd[t.lane] : -DBL_MAX;
-      bj = t.lane < RO_NW ? sm.rj[t.lane] : -1;
+      bv = t.lane < NW ? sm.rd[t.lane] : -DBL_MAX;
+      bj = t.lane < NW ? sm.rj[t.lane] : -1;
       warp_argmax64(bv, bj);
       if (t.lane == 0) { sm.argv = bv; sm.argj = bj; }
     }
@@ -843,7 +846,9 @@ __device__ __forceinline__ void ro_store_scores(const float* src, float* dst, un
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
 
-__global__ void __launch_bounds__(RO_T, 2) k_rank_occ(RankManyArgs a) {
+template <int T>
+__global__ void __launch_bounds__(T, 512 / T) k_rank_occ(RankManyArgs a) {
+  constexpr int RO_T = T;
   extern __shared__ __align__(128) int stage[];  // [4][slice] rows | [2][slice] scores
   __shared__ RoShared sm;
   cg::cluster_group cl = cg::this_cluster();
@@ -959,10 +964,10 @@ __global__ void __launch_bounds__(RO_T, 2) k_rank_occ(RankManyArgs a) {
     }
     cl.sync();  // this state's statistics and the previous state's keys are visible over DSMEM
     if (t.warp == 0) ro_params(a, t, sm, cl, p);
-    if (t.warp == 1 && i > 0) ro_keys(a, t, sm, cl, p ^ 1);
+    if (t.warp == 1 && i > 0) ro_keys<T / 32>(a, t, sm, cl, p ^ 1);
     __syncthreads();
     if (t.tid == 0) ws_reset(sm.cs[p ^ 1]);  // every CTA has read the previous state's slot
-    if (i > 0) ro_finish(a, t, sm, cl, p ^ 1);
+    if (i > 0) ro_finish<T>(a, t, sm, cl, p ^ 1);
     // ----------------------------------------------- a5T: closeness, top-2 keys --
     TopsisP tp;
 #pragma unroll
@@ -1007,9 +1012,9 @@ __global__ void __launch_bounds__(RO_T, 2) k_rank_occ(RankManyArgs a) {
   cl.sync();  // the last state's keys are visible
   if (i > 0) {
     const int q = (i - 1) & 1;
-    if (t.warp == 0) ro_keys(a, t, sm, cl, q);
+    if (t.warp == 0) ro_keys<T / 32>(a, t, sm, cl, q);
     __syncthreads();
-    ro_finish(a, t, sm, cl, q);
+    ro_finish<T>(a, t, sm, cl, q);
     if (t.tid == 0 && have && a.scores) {
       ro_store_scores(scbuf + q * S, a.scores + (long long)prev_b * n + t.lo, 4u * (unsigned)(t.hi - t.lo));
       asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
@@ -1029,24 +1034,31 @@ int rank_many_cluster(const Geo& g) { return (g.n + RM_S - 1) / RM_S; }
 
 cudaError_t launch_rank_many(const RankManyArgs& a0, int num_sms, cudaStream_t st) {
   RankManyArgs a = a0;
-  const int C = rank_many_cluster(a.g);
-  if (C > 16) return cudaErrorInvalidValue;
+  if (rank_many_cluster(a.g) > 16) return cudaErrorInvalidValue;
   const bool v4 = (a.g.n % 4 == 0) && (a.stride % 4 == 0) && ((uintptr_t)a.states % 16 == 0);
+  const bool flows = a.nflow > 0 || a.nex > 0;
+  const char* kenv = getenv("NACS_RANK_KERNEL");  // experiment knob: "many" | "occ256"
+  const bool occ = v4 && !flows && !(kenv && !strcmp(kenv, "many"));
+  // k_rank_occ: 128-thread CTAs (4 per SM) when one CTA holds the whole state (n <= 2048: no
+  // cluster barrier at all), else 256 (4096-server slices, 2 per SM: at k=32, 4 CTAs of 2048
+  // measured 3.47 TB/s against 4.20); k_rank_many: 512 threads, 4096-server slices
+  const bool occ128 = occ && a.g.n <= 2048 && !(kenv && !strcmp(kenv, "occ256"));
+  const int T = occ ? (occ128 ? 128 : 256) : RM_T;
+  const int per_cta = occ ? T * RO_V : RM_S;
+  const int C = (a.g.n + per_cta - 1) / per_cta;
   const int VW = v4 ? 4 : 2;
-  // slices of <= RM_S servers, a multiple of VW so that vector accesses stay aligned
+  // slices of <= per_cta servers, a multiple of VW so that vector accesses stay aligned
   int S = (a.g.n + C - 1) / C;
   S = (S + VW - 1) / VW * VW;
   a.slice = S;
-  const bool flows = a.nflow > 0 || a.nex > 0;
-  const char* kenv = getenv("NACS_RANK_KERNEL");  // experiment knob: "many" forces the general kernel
-  const bool occ = v4 && !flows && !(kenv && !strcmp(kenv, "many"));
-  void (*kern)(RankManyArgs) = occ ? k_rank_occ
+  void (*kern)(RankManyArgs) = occ ? (occ128 ? k_rank_occ<128> : k_rank_occ<256>)
                                : v4 ? (flows ? k_rank_many<4, true, true> : k_rank_many<4, true, false>)
                                     : (flows ? k_rank_many<2, false, true> : k_rank_many<2, false, false>);
-  const size_t dyn = v4 ? 2 * 4 * sizeof(int) * (size_t)S : 0;
-  const int kid = occ ? 2 : flows;
-  static int max_clusters[2][3][17] = {};
-  static bool dyn_set[3] = {};
+  // dynamic shared memory: occ = the row stage + 2 score rows (6 S int32); many = 2 row stages
+  const size_t dyn = occ ? 6 * sizeof(int) * (size_t)S : v4 ? 2 * 4 * sizeof(int) * (size_t)S : 0;
+  const int kid = occ ? (occ128 ? 3 : 2) : flows;
+  static int max_clusters[2][4][17] = {};
+  static bool dyn_set[4] = {};
   int& mc = max_clusters[v4][kid][C];
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr[1];
@@ -1054,16 +1066,15 @@ cudaError_t launch_rank_many(const RankManyArgs& a0, int num_sms, cudaStream_t s
   attr[0].val.clusterDim.x = C;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
-  cfg.blockDim = dim3(occ ? RO_T : RM_T, 1, 1);
-  cfg.dynamicSmemBytes = occ ? 6 * sizeof(int) * (size_t)S : dyn;  // occ: rows + 2 score buffers
+  cfg.blockDim = dim3(T, 1, 1);
+  cfg.dynamicSmemBytes = dyn;
   cfg.stream = st;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   cudaError_t e;
-  if (v4 && !dyn_set[kid]) {  // the largest stage (2 x 4 x RM_S int32 = 128 KB); one CTA per SM either way
-    if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (occ ? 6 : 8) * 4 * RM_S)) !=
-        cudaSuccess)
-      return e;
+  if (v4 && !dyn_set[kid]) {  // the variant's largest dynamic shared memory
+    const int maxdyn = occ ? 6 * 4 * T * RO_V : 8 * 4 * RM_S;
+    if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, maxdyn)) != cudaSuccess) return e;
     dyn_set[kid] = true;
   }
   if (mc == 0) {

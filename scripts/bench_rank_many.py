@@ -29,7 +29,7 @@ def main():
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     ctx = nacs.Context(0, stream)
-    for variant, k, B in [(v, k, B) for v in ("occ", "stream", "many") for k, B in ((32, 4096), (64, 512), (16, 16384))]:
+    for variant, k, B in [(v, k, B) for v in ("occ", "occ256", "many") for k, B in ((32, 4096), (64, 512), (16, 16384))]:
         os.environ["NACS_RANK_KERNEL"] = variant
         snap = gen.snapshot(k, 4)
         ctx.load_topology(snap)
