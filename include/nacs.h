@@ -201,7 +201,8 @@ nacs_status nacs_read_topology(nacs_ctx *ctx, int32_t *cpu_res, int32_t *ram_res
  * TOPSIS (R12-R13) scores over the feasible set, then the argmax with the
  * lowest server index on ties (R14).  mask[n] (uint8, may be NULL): 1 = feasible.
  * scores[n] (float, may be NULL): the FP32 score of feasible servers, 0 elsewhere.
- * best: the chosen server, -1 if none is feasible. */
+ * best: the chosen server, -1 if none is feasible.  Device pointers (NACS_DEVICE_PTRS):
+ * scores 16-byte aligned, mask 4-byte aligned (else NACS_EINVAL). */
 nacs_status nacs_rank_ahp(nacs_ctx *ctx, const nacs_options *opt, const nacs_pod_query *q, uint8_t *mask,
                           float *scores, int32_t *best);
 nacs_status nacs_rank_topsis(nacs_ctx *ctx, const nacs_options *opt, const nacs_pod_query *q,
@@ -219,7 +220,8 @@ nacs_status nacs_rank_topsis(nacs_ctx *ctx, const nacs_options *opt, const nacs_
  * -1 if no server is feasible; -2 if the state holds a residual outside [0, capacity] or an
  * f_u outside {0, 1}, in which case the call returns NACS_EINVAL unless NACS_ASYNC).
  * NACS_DEVICE_PTRS: states and outputs are device pointers (the streaming form: one launch,
- * a thread-block cluster per state); otherwise host arrays, staged through device buffers.
+ * a thread-block cluster per state) — states and scores 16-byte aligned, mask and best 4-byte
+ * aligned (else NACS_EINVAL); otherwise host arrays, staged through device buffers.
  * Flow/exclusion arrays of q follow the same flag.  TOPSIS only, bw_criterion = NACS_BW_ACCESS,
  * n <= 65536, not on server-sharded contexts.  Stats: pod_steps = n_states. */
 nacs_status nacs_rank_topsis_many(nacs_ctx *ctx, const nacs_options *opt, const nacs_pod_query *q, int32_t n_states,

@@ -592,6 +592,8 @@ nacs_status rank_impl(nacs_ctx* ctx, const nacs_options* opt, const nacs_pod_que
   if ((st = query_device(ctx, q, dev, &qd))) return st;
   CK(ctx->mask.reserve(g.n));
   CK(ctx->scores.reserve(g.n));
+  if (dev && (((uintptr_t)scores % 16) || ((uintptr_t)mask % 4)))
+    return fail(ctx, NACS_EINVAL, "device scores must be 16-byte aligned and mask 4-byte aligned");
   qd.mask = (dev && mask) ? mask : ctx->mask.p;
   qd.scores = (dev && scores) ? scores : ctx->scores.p;
   qd.best = dev ? best : ctx->misc.p;
@@ -1001,6 +1003,9 @@ nacs_status nacs_rank_topsis_many(nacs_ctx* ctx, const nacs_options* opt, const 
     qd.scores = scores ? ctx->many_scores.p : nullptr;
     qd.best = ctx->many.p + B * (size_t)stride;
   } else {
+    if (((uintptr_t)scores % 16) || ((uintptr_t)mask % 4) || ((uintptr_t)states % 16) || ((uintptr_t)best % 4))
+      return fail(ctx, NACS_EINVAL,
+                  "nacs_rank_topsis_many: device arrays must be aligned (states, scores 16 B; mask, best 4 B)");
     qd.mask = mask;
     qd.scores = scores;
     qd.best = best;

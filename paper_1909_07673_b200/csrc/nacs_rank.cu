@@ -1038,7 +1038,8 @@ cudaError_t launch_rank_many(const RankManyArgs& a0, int num_sms, cudaStream_t s
   const bool v4 = (a.g.n % 4 == 0) && (a.stride % 4 == 0) && ((uintptr_t)a.states % 16 == 0);
   const bool flows = a.nflow > 0 || a.nex > 0;
   const char* kenv = getenv("NACS_RANK_KERNEL");  // experiment knob: "many" | "occ256"
-  const bool occ = v4 && !flows && !(kenv && !strcmp(kenv, "many"));
+  // (k_rank_occ stores the scores with TMA bulk copies: 16-byte aligned rows)
+  const bool occ = v4 && !flows && ((uintptr_t)a.scores % 16 == 0) && !(kenv && !strcmp(kenv, "many"));
   // k_rank_occ: 128-thread CTAs (4 per SM) when one CTA holds the whole state (n <= 2048: no
   // cluster barrier at all), else 256 (4096-server slices, 2 per SM: at k=32, 4 CTAs of 2048
   // measured 3.47 TB/s against 4.20); k_rank_many: 512 threads, 4096-server slices

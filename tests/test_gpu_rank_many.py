@@ -78,6 +78,31 @@ def test_rank_many_device_pointers_and_path_filter(ctx):
             assert_rank_parity(dict(mask=host["mask"][b], scores=host["scores"][b], best=int(host["best"][b])), o)
 
 
+def test_rank_many_unaligned_device_outputs(ctx):
+    """Device outputs the vector / TMA stores cannot take (scores not 16-byte aligned, mask not
+    4-byte aligned) are rejected with NACS_EINVAL before any launch; the context stays usable."""
+    import torch
+    from paper_1909_07673_b200 import nacs
+    ss = snaps(16, 3, 12)
+    ctx.load_topology(ss[0])
+    states = torch.from_numpy(np.stack([state_words(s) for s in ss])).cuda()
+    n = 1024
+    best = torch.zeros(3, dtype=torch.int32, device="cuda")
+    sc = torch.zeros(3 * n + 1, dtype=torch.float32, device="cuda")[1:].view(3, n)
+    mk = torch.zeros(3 * n + 3, dtype=torch.uint8, device="cuda")[3:].view(3, n)
+    ok_sc = torch.zeros((3, n), dtype=torch.float32, device="cuda")
+    ok_mk = torch.zeros((3, n), dtype=torch.uint8, device="cuda")
+    for m, s_ in ((ok_mk, sc), (mk, ok_sc)):
+        with pytest.raises(nacs.NacsError) as e:
+            ctx.rank_many(states, 700, 900, out=dict(mask=m, scores=s_, best=best))
+        assert e.value.status == nacs.NACS_EINVAL
+    out = ctx.rank_many(states, 700, 900, out=dict(mask=ok_mk, scores=ok_sc, best=best))
+    for b, s in enumerate(ss):
+        o = O.rank(s, "topsis", "flat", 700, 900)
+        assert_rank_parity(dict(mask=out["mask"][b].cpu().numpy(), scores=out["scores"][b].cpu().numpy(),
+                                best=int(out["best"][b])), o, b)
+
+
 def test_rank_many_equals_single_rank_and_exact64(ctx):
     """One state through rank_many equals nacs_rank_topsis on the loaded state (both run the
     cluster kernel) and the FP64 re-decision flag picks the same server."""
@@ -124,8 +149,8 @@ def test_rank_many_edge_cases(ctx):
 
 
 def test_rank_many_cold_stream_sampled(ctx):
-    """The bench's cold-snapshot configuration (k = 32, 512 distinct device-generated states,
-    4 GB of state rows): sampled states against the oracle."""
+    """The bench's cold-snapshot configuration (k = 32, distinct device-generated states; 512
+    here, 100 MB of state rows): sampled states against the oracle."""
     import torch
     from paper_1909_07673_b200 import nacs
     snap = gen.snapshot(32, gen.CONFIG_SEEDS["C4"])
