@@ -221,7 +221,8 @@ nacs_status nacs_rank_topsis(nacs_ctx *ctx, const nacs_options *opt, const nacs_
  * f_u outside {0, 1}, in which case the call returns NACS_EINVAL unless NACS_ASYNC).
  * NACS_DEVICE_PTRS: states and outputs are device pointers (the streaming form: one launch,
  * a thread-block cluster per state) — states and scores 16-byte aligned, mask and best 4-byte
- * aligned (else NACS_EINVAL); otherwise host arrays, staged through device buffers.
+ * aligned, state_stride even (a multiple of 4 takes the TMA path) — else NACS_EINVAL;
+ * otherwise host arrays, staged through device buffers.
  * Flow/exclusion arrays of q follow the same flag.  TOPSIS only, bw_criterion = NACS_BW_ACCESS,
  * n <= 65536, not on server-sharded contexts.  Stats: pod_steps = n_states. */
 nacs_status nacs_rank_topsis_many(nacs_ctx *ctx, const nacs_options *opt, const nacs_pod_query *q, int32_t n_states,

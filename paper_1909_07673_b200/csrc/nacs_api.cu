@@ -1003,9 +1003,11 @@ nacs_status nacs_rank_topsis_many(nacs_ctx* ctx, const nacs_options* opt, const 
     qd.scores = scores ? ctx->many_scores.p : nullptr;
     qd.best = ctx->many.p + B * (size_t)stride;
   } else {
-    if (((uintptr_t)scores % 16) || ((uintptr_t)mask % 4) || ((uintptr_t)states % 16) || ((uintptr_t)best % 4))
+    if (((uintptr_t)scores % 16) || ((uintptr_t)mask % 4) || ((uintptr_t)states % 16) || ((uintptr_t)best % 4) ||
+        (state_stride % 2))
       return fail(ctx, NACS_EINVAL,
-                  "nacs_rank_topsis_many: device arrays must be aligned (states, scores 16 B; mask, best 4 B)");
+                  "nacs_rank_topsis_many: device arrays must be aligned (states, scores 16 B; mask, best 4 B; "
+                  "an even state_stride)");
     qd.mask = mask;
     qd.scores = scores;
     qd.best = best;
