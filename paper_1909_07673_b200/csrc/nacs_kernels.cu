@@ -157,6 +157,15 @@ __device__ __forceinline__ void st_set_v(Ctx& c, int off, int old, int val) {
   s->log_n += 1;
   c.st[off] = val;
   if (off >= 4 * c.g.n && val < s->minfab) s->minfab = val;
+  if (c.dirty && off < 4 * c.g.n) {  // AHP: the server leaves its presorted position (as st_set)
+    const int u = off % c.g.n;
+    if (!((c.dirty[u >> 5] >> (u & 31)) & 1u)) {
+      c.dirty[u >> 5] |= 1u << (u & 31);
+      if (s->ntouched < 2 * MAXC) s->touched[s->ntouched] = u;
+      else s->touch_over = 1;
+      s->ntouched += 1;
+    }
+  }
 }
 __device__ __forceinline__ void undo_to(Ctx& c, int mark) {
   Scratch* s = c.s;
@@ -2715,7 +2724,7 @@ template <int METHOD>
 __device__ void sh_commit_advance(Ctx& c, const ReqsDev& R, const OutDev& O, int r, const ShardDev& d) {
   Scratch* s = c.s;
   const int p = d.ctl[1];
-  if (c.warp == 0) commit(c, R, r, p);
+  commit_cta(c, R, r, p);  // the widest paths over the whole CTA, the words read in parallel
   __syncthreads();
   if (c.tid == 0) { d.ctl[2] = s->best; d.ctl[3] = s->fail; }
   if (s->fail) {
