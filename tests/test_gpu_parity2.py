@@ -287,3 +287,36 @@ def test_seq_cluster_engine_vs_oracle_and_one_cta(ctx, k):
     ctx.load_topology(snap)
     c = to_np(ctx.schedule_request(reqs, "topsis", "flat", flags=nacs.NACS_EXACT_FP64))
     assert_schedule_parity(snap, reqs, c, "topsis", "flat", True, gpu_state=ctx.read_topology())
+
+
+# ------------------------------------------------------ randomized sweeps -----
+def test_seq_cluster_random_sweep(ctx):
+    """The cluster engine equals the one-CTA engine (NACS_SEQC=0) on random DCs at every even
+    k from 40 to 64 (n = 16000 .. 65536, clusters of 8 and 16, ragged last shares), warm /
+    quantised / congested fabrics, random schemas and flags."""
+    import os
+    rng = np.random.default_rng(2024)
+    for k in range(40, 66, 4):
+        for trial in range(2):
+            snap = gen.snapshot(k, seed=1000 + 10 * k + trial, quantised=trial == 1)
+            if rng.random() < 0.5:
+                snap["link_res"] = rng.integers(10, 200, size=len(snap["link_res"])).astype(np.int32)
+            reqs = gen.requests(6, 2000 + k + trial, bw_max_hi=80)
+            schema = ("flat", "clustering", "network")[int(rng.integers(3))]
+            kw = dict(path_filter=int(rng.integers(2))) if rng.random() < 0.3 else {}
+            res = []
+            for seqc in (None, "0"):
+                if seqc is not None:
+                    os.environ["NACS_SEQC"] = seqc
+                try:
+                    ctx.load_topology(snap)
+                    out = to_np(ctx.schedule_request(reqs, "topsis", schema, **kw))
+                    res.append((out, ctx.read_topology(), ctx.last_stats()["pod_steps"]))
+                finally:
+                    os.environ.pop("NACS_SEQC", None)
+            (a, sa, pa), (b, sb, pb) = res
+            for key in a:
+                assert np.array_equal(a[key], b[key]), (k, trial, key)
+            for key in sa:
+                assert np.array_equal(sa[key], sb[key]), (k, trial, key)
+            assert pa == pb

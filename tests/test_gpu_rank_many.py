@@ -173,3 +173,29 @@ def test_rank_many_cold_stream_sampled(ctx):
         o = O.rank(s, "topsis", "flat", 1500, 3000)
         assert_rank_parity(dict(mask=out["mask"][b].cpu().numpy(), scores=out["scores"][b].cpu().numpy(),
                                 best=int(best[b])), o, b)
+
+
+def test_rank_many_random_sweep(ctx):
+    """Random geometries (every even k from 2 to 30 and a few large ones), demands, flows and
+    exclusions: every state against the oracle."""
+    rng = np.random.default_rng(77)
+    for k in list(range(2, 32, 2)) + [36, 48]:
+        n = k ** 3 // 4
+        B = 3
+        ss = [gen.snapshot(k, seed=int(rng.integers(1 << 30)), quantised=bool(rng.integers(2))) for _ in range(B)]
+        for s in ss:
+            if rng.random() < 0.5:
+                s["link_res"] = rng.integers(0, 200, size=len(s["link_res"])).astype(np.int32)
+        ctx.load_topology(ss[0])
+        states = np.stack([state_words(s) for s in ss])
+        nfl = int(rng.integers(0, min(4, n) + 1))
+        flows = [(int(v), int(rng.integers(1, 80))) for v in rng.choice(n, size=nfl, replace=False)]
+        nex = int(rng.integers(0, min(3, n) + 1))
+        ex = [int(x) for x in rng.choice(n, size=nex, replace=False)]
+        dc, dr = int(rng.integers(1, 20000)), int(rng.integers(1, 200000))
+        schema = ("flat", "clustering", "network")[int(rng.integers(3))]
+        got = ctx.rank_many(states, dc, dr, flows=flows, excluded=ex, weights=schema)
+        for b, s in enumerate(ss):
+            o = O.rank(s, "topsis", schema, dc, dr, flows, ex)
+            assert_rank_parity(dict(mask=got["mask"][b], scores=got["scores"][b], best=int(got["best"][b])), o,
+                               (k, b, len(flows), len(ex)))
