@@ -128,16 +128,58 @@ struct Ctx {
   double* w64;         // FP64 re-decision: [n2] per-level weights + [nfcap] priorities (global)
   int nfcap;
   int2* ulog;          // undo log (global)
+  int* const* mirr = nullptr;  // k_seq_cluster: every CTA's shared-memory copy of its share of the
+                              // per-server rows (cluster addresses), kept current by st_set
   int tid, B, NW, lane, warp;
   int nW, nEW;
 };
 
+#ifdef NACS_SEQC_PROF  // experiment builds: per-phase time of the leader CTA (device printf at the end)
+__shared__ unsigned long long seqc_prof_[24], seqc_last_;
+#define SEQC_T(i)                                                                  \
+  do {                                                                             \
+    if (blockIdx.x == 0 && threadIdx.x == 0) {                                     \
+      unsigned long long now_;                                                     \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now_));                     \
+      seqc_prof_[i] += now_ - seqc_last_;                                          \
+      seqc_last_ = now_;                                                           \
+    }                                                                              \
+  } while (0)
+#else
+#define SEQC_T(i) \
+  do {            \
+  } while (0)
+#endif
+
 // ------------------------------------------------------- undo log (1 thread) --
+// k_seq_cluster's row copies: server u of criterion row q lives in CTA (u / 1024) mod C at
+// q * SQC_M + (u / (SQC_T C)) * SQC_T + u mod SQC_T (its grid-stride share, see seqc_filter)
+#ifndef NACS_SEQC_T
+#define NACS_SEQC_T 512
+#endif
+constexpr int SQC_T = NACS_SEQC_T;  // threads per CTA (a power of two)
+constexpr int SQC_M = 4096;         // servers per CTA: C = 16 covers k = 64
+constexpr int SQ_J = SQC_M / SQC_T; // servers per thread, kept in registers over a pod step
+// (C, the cluster size, is a power of two: seq_cluster_size)
+__device__ __forceinline__ int* mirror_ptr(const Ctx& c, int off) {
+  const int n = c.g.n;
+  const int q = (off >= n) + (off >= 2 * n) + (off >= 3 * n);
+  const int u = off - q * n;
+  const int C = (int)gridDim.x;
+  return c.mirr[(u / SQC_T) & (C - 1)] + q * SQC_M + ((u >> (__ffs(C * SQC_T) - 1)) * SQC_T) + (u & (SQC_T - 1));
+}
+__device__ __forceinline__ void mirror_put(const Ctx& c, int off, int val) { *mirror_ptr(c, off) = val; }
+// A state word for the thread-0 chains: a per-server row word from the cluster copy (a
+// distributed-shared-memory round trip instead of an L2 one), else the global state.
+__device__ __forceinline__ int st_get(const Ctx& c, int off) {
+  return c.mirr && off < 4 * c.g.n ? *mirror_ptr(c, off) : c.st[off];
+}
 __device__ __forceinline__ void st_set(Ctx& c, int off, int val) {
   Scratch* s = c.s;
-  c.ulog[s->log_n] = make_int2(off, c.st[off]);
+  c.ulog[s->log_n] = make_int2(off, st_get(c, off));
   s->log_n += 1;
   c.st[off] = val;
+  if (c.mirr && off < 4 * c.g.n) mirror_put(c, off, val);
   if (off >= 4 * c.g.n && val < s->minfab) s->minfab = val;  // commits only lower the bound
   if (c.dirty && off < 4 * c.g.n) {  // AHP: the server leaves its presorted position
     const int u = off % c.g.n;
@@ -156,6 +198,7 @@ __device__ __forceinline__ void st_set_v(Ctx& c, int off, int old, int val) {
   c.ulog[s->log_n] = make_int2(off, old);
   s->log_n += 1;
   c.st[off] = val;
+  if (c.mirr && off < 4 * c.g.n) mirror_put(c, off, val);
   if (off >= 4 * c.g.n && val < s->minfab) s->minfab = val;
   if (c.dirty && off < 4 * c.g.n) {  // AHP: the server leaves its presorted position (as st_set)
     const int u = off % c.g.n;
@@ -172,6 +215,7 @@ __device__ __forceinline__ void undo_to(Ctx& c, int mark) {
   for (int i = s->log_n - 1; i >= mark; --i) {
     int2 e = c.ulog[i];
     c.st[e.x] = e.y;
+    if (c.mirr && e.x < 4 * c.g.n) mirror_put(c, e.x, e.y);
   }
   s->log_n = mark;
 }
@@ -1325,6 +1369,28 @@ __device__ void build_flows(Ctx& c, const ReqsDev& R, int r, int p) {
 __device__ void flow_server_ok(Ctx& c) {
   Scratch* s = c.s;
   const int* acc = c.st + 3 * c.g.n;
+  if (c.B >= MAXF) {  // one flow per thread: every access word loaded once, at the same time
+    const int f = c.tid, nflow = s->nflow;
+    int u = 0, au = 0, bad = 0;
+    if (f < nflow) {
+      u = s->fv[f];
+      au = acc[u];
+      bad = au < s->fD[f];
+    }
+    // flow f's server is feasible iff its access link carries the other flows and every other
+    // flow's peer carries its own flow: no bad peer other than possibly f itself
+    const int nbad = __syncthreads_count(bad);
+    if (f < nflow) {
+      bool ok = au >= s->sumD - s->fD[f] && (nbad == 0 || (nbad == 1 && bad));
+      const unsigned e = div_h((unsigned)u, c.g.magic_h);
+      if ((c.edgebad[e >> 5] >> (e & 31)) & 1u) ok = false;
+      s->fok[f] = ok;
+      s->fexcl[f] = 0;
+      atomicOr(&c.special[u >> 5], 1u << (u & 31));
+    }
+    if (c.tid == 0) s->G = nbad == 0;
+    return;
+  }
   for (int f = c.tid; f < s->nflow; f += c.B) {
     int u = s->fv[f];
     bool ok = acc[u] >= s->sumD - s->fD[f];
@@ -1469,7 +1535,7 @@ __device__ void commit_cta(Ctx& c, const ReqsDev& R, int r, int p) {
   const int n = g.n;
   const int u = s->best;
   if (c.warp == 0) {  // the server's three words read in parallel, applied by lane 0 (no AHP dirty list here)
-    const int w = c.lane == 0 ? c.st[u] : c.lane == 1 ? c.st[n + u] : c.lane == 2 ? c.st[2 * n + u] : 0;
+    const int w = c.lane < 3 ? st_get(c, c.lane * n + u) : 0;
     const int x0 = __shfl_sync(FULL, w, 0), x1 = __shfl_sync(FULL, w, 1), x2 = __shfl_sync(FULL, w, 2);
     if (c.lane == 0) {
       s->log_mark = s->log_n;
@@ -1480,6 +1546,7 @@ __device__ void commit_cta(Ctx& c, const ReqsDev& R, int r, int p) {
     }
   }
   __syncthreads();
+  SEQC_T(15);
   for (int f = 0; f < s->nflow; ++f) {
     const int v = s->fv[f], D = s->fD[f];
     if (v == u) {
@@ -1487,12 +1554,13 @@ __device__ void commit_cta(Ctx& c, const ReqsDev& R, int r, int p) {
       continue;
     }
     const int2 wp = widest_path_cta(c, u, v);  // ends with __syncthreads: earlier deductions seen
+    SEQC_T(16);
     if (c.warp == 0) {  // the path's words (2 access + up to 4 fabric) read by lanes 0..5 at once
       int off[6];
       off[0] = 3 * n + u;
       off[1] = 3 * n + v;
       const int m = path_links(g, u, v, wp.x, off + 2);
-      const int val = c.lane < 2 + m ? c.st[off[c.lane < 6 ? c.lane : 0]] : 0;
+      const int val = c.lane < 2 + m ? st_get(c, off[c.lane < 6 ? c.lane : 0]) : 0;
       int x[6];
 #pragma unroll
       for (int i = 0; i < 6; ++i) x[i] = __shfl_sync(FULL, val, i);
@@ -1507,6 +1575,7 @@ __device__ void commit_cta(Ctx& c, const ReqsDev& R, int r, int p) {
       }
     }
     __syncthreads();
+    SEQC_T(17);
     if (s->fail) break;
   }
   if (c.tid == 0) {
@@ -1519,18 +1588,20 @@ __device__ void commit_cta(Ctx& c, const ReqsDev& R, int r, int p) {
       s->c_retries += 1;
     } else {
       s->pod_srv[p] = u;
-      const int v0 = R.voff[r];
-      for (int e = 0; e < s->nV; ++e) {
-        const int a = s->cpod[R.src[v0 + e]], b = s->cpod[R.dst[v0 + e]];
-        int other = -1;
-        if (a == p && b != p && b < p) other = b;
-        else if (b == p && a != p && a < p) other = a;
-        if (other < 0) continue;
-        const int v = s->pod_srv[other];
-        int fp = -1;
-        for (int i = 0; i < s->nflow; ++i) if (s->fv[i] == v) fp = s->fpath[i];
-        s->vpath[e] = fp;
-      }
+    }
+  }
+  if (!s->fail && c.warp == 0) {  // each vlink of pod p to an earlier pod takes its flow's path (lanes)
+    const int v0 = R.voff[r];
+    for (int e = c.lane; e < s->nV; e += 32) {
+      const int a = s->cpod[R.src[v0 + e]], b = s->cpod[R.dst[v0 + e]];
+      int other = -1;
+      if (a == p && b != p && b < p) other = b;
+      else if (b == p && a != p && a < p) other = a;
+      if (other < 0) continue;
+      const int v = s->pod_srv[other];
+      int fp = -1;
+      for (int i = 0; i < s->nflow; ++i) if (s->fv[i] == v) fp = s->fpath[i];
+      s->vpath[e] = fp;
     }
   }
 }
@@ -1602,7 +1673,9 @@ __device__ void pod_prologue(Ctx& c, const ReqsDev& R, int r, int p) {
   if (c.warp == 0) build_flows_warp(c, R, r, p);
   clear_bitmaps(c);
   __syncthreads();
+  SEQC_T(18);
   if (c.o.path_filter && s->nflow > 0) fabric_tables(c);
+  SEQC_T(19);
   flow_server_ok(c);
   __syncthreads();
 }
@@ -1625,10 +1698,11 @@ __device__ void req_finish(Ctx& c, const ReqsDev& R, const OutDev& O, int r, boo
     for (int i = 0; i < s->nC; ++i) {
       int u = s->pod_srv[s->cpod[i]];
       int cmin = R.cpu_min[c0 + i], rmin = R.ram_min[c0 + i];
-      int ec = min(R.cpu_max[c0 + i] - cmin, c.st[u]);
-      int er = min(R.ram_max[c0 + i] - rmin, c.st[n + u]);
-      if (ec) st_set(c, u, c.st[u] - ec);
-      if (er) st_set(c, n + u, c.st[n + u] - er);
+      const int xc = st_get(c, u), xr = st_get(c, n + u);  // two independent loads
+      int ec = min(R.cpu_max[c0 + i] - cmin, xc);
+      int er = min(R.ram_max[c0 + i] - rmin, xr);
+      if (ec) st_set_v(c, u, xc, xc - ec);
+      if (er) st_set_v(c, n + u, xr, xr - er);
       O.server[c0 + i] = u;
       O.cpu_a[c0 + i] = cmin + ec;
       O.ram_a[c0 + i] = rmin + er;
@@ -1642,15 +1716,19 @@ __device__ void req_finish(Ctx& c, const ReqsDev& R, const OutDev& O, int r, boo
         continue;
       }
       int pid = s->vpath[e];
-      int off[4];
-      int m = path_links(g, us, ud, pid, off);
-      int resid = min(c.st[3 * n + us], c.st[3 * n + ud]);
-      for (int t = 0; t < m; ++t) resid = min(resid, c.st[off[t]]);
+      int off[6];
+      off[0] = 3 * n + us;
+      off[1] = 3 * n + ud;
+      const int m = 2 + path_links(g, us, ud, pid, off + 2);
+      int x[6];  // the path's words, loaded together (distinct links: no reload after a store)
+#pragma unroll
+      for (int t = 0; t < 6; ++t) x[t] = t < m ? st_get(c, off[t]) : INT_MAX;
+      int resid = x[0];
+#pragma unroll
+      for (int t = 1; t < 6; ++t) resid = min(resid, x[t]);
       int extra = min(bmax - bmin, resid);
       if (extra) {
-        st_set(c, 3 * n + us, c.st[3 * n + us] - extra);
-        st_set(c, 3 * n + ud, c.st[3 * n + ud] - extra);
-        for (int t = 0; t < m; ++t) st_set(c, off[t], c.st[off[t]] - extra);
+        for (int t = 0; t < m; ++t) st_set_v(c, off[t], x[t], x[t] - extra);
       }
       O.bw_a[v0 + e] = bmin + extra;
       O.path[v0 + e] = pid;
@@ -1725,6 +1803,7 @@ __device__ void init_ctx(Ctx& c, const Geo& g, const Opt& o, Scratch* s) {
   c.nW = (g.n + 31) >> 5;
   c.nEW = (g.E + 31) >> 5;
   c.dirty = nullptr;
+  c.mirr = nullptr;
   if (c.tid == 0) {
     s->c_steps = s->c_retries = s->c_fp64 = s->c_invalid = s->c_feas = s->c_pairs = 0;
     s->minfab = s->minfab0 = 0;
@@ -1913,11 +1992,12 @@ __device__ __forceinline__ void facc_reset(unsigned long long* f, int tid) {
   if (tid < 11) f[tid] = (tid >= 2 && tid <= 7 && !(tid & 1)) ? ~0ull : 0ull;
 }
 
+
 // k_seq_cluster's a3 + a4: pass_filter's test on this CTA's grid-stride share of at most
-// SQ_J servers per thread, with every row of the share loaded up front (one L2 round trip
-// instead of one per stride) and kept in registers for the scoring pass.
-constexpr int SQ_J = 4;
-__device__ __forceinline__ void seqc_filter(Ctx& c, unsigned long long* facc, int (&x)[SQ_J][4], unsigned& okb) {
+// SQ_J servers per thread, read from the CTA's shared-memory copy of the rows (mir; the
+// cluster lives in one GPC, whose L2 port made the 1 MB global read of every pod step the
+// largest phase) and kept in registers for the scoring pass.
+__device__ __forceinline__ void seqc_filter(Ctx& c, const int* mir, unsigned long long* facc, unsigned& okb) {
   Scratch* s = c.s;
   const Geo& g = c.g;
   const int n = g.n;
@@ -1925,12 +2005,13 @@ __device__ __forceinline__ void seqc_filter(Ctx& c, unsigned long long* facc, in
   const bool net = c.o.path_filter && s->nflow > 0;
   const bool G = s->G != 0;
   const int start = (blockIdx.x * c.NW + c.warp) * 32, stride = gridDim.x * c.B;
+  int x[SQ_J][4];
 #pragma unroll
   for (int j = 0; j < SQ_J; ++j) {
     const int u = start + j * stride + c.lane;
     const bool in = u < n;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) x[j][q] = in ? c.st[q * n + u] : 0;
+    for (int q = 0; q < 4; ++q) x[j][q] = in ? mir[q * SQC_M + j * SQC_T + c.tid] : 0;
   }
   int nf = 0, nact = 0;
   unsigned mn0 = UINT_MAX, mn1 = UINT_MAX, mn3 = UINT_MAX, mx0 = 0, mx1 = 0, mx3 = 0;
@@ -1969,26 +2050,11 @@ __device__ __forceinline__ void seqc_filter(Ctx& c, unsigned long long* facc, in
       q3 += (unsigned long long)((unsigned)x3) * (unsigned)x3;
     }
   }
+  SEQC_T(10);
   filter_reduce<true>(c, nf, nact, mn0, mx0, mn1, mx1, mn3, mx3, q0, q1, q3, facc);
 }
 
-#ifdef NACS_SEQC_PROF  // experiment builds: per-phase time of the leader CTA (device printf at the end)
-#define SEQC_T(i)                                                                  \
-  do {                                                                             \
-    if (lead && c.tid == 0) {                                                      \
-      unsigned long long now_;                                                     \
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now_));                     \
-      prof_[i] += now_ - prof_last_;                                               \
-      prof_last_ = now_;                                                           \
-    }                                                                              \
-  } while (0)
-#else
-#define SEQC_T(i) \
-  do {            \
-  } while (0)
-#endif
-
-__global__ void __launch_bounds__(1024) k_seq_cluster(Geo g, Opt o, int* state, ReqsDev R, OutDev O, int2* ulog,
+__global__ void __launch_bounds__(SQC_T, 1) k_seq_cluster(Geo g, Opt o, int* state, ReqsDev R, OutDev O, int2* ulog,
                                                       unsigned long long* stats, unsigned long long* facc,
                                                       unsigned long long* kx, double* kxv, int* kxi) {
   extern __shared__ __align__(16) unsigned char dyn[];
@@ -2006,6 +2072,11 @@ __global__ void __launch_bounds__(1024) k_seq_cluster(Geo g, Opt o, int* state, 
   c.f0w = reinterpret_cast<unsigned*>(dyn + off);
   off = align16(off + sizeof(unsigned) * c.nW);
   c.edgebad = reinterpret_cast<unsigned*>(dyn + off);
+  off = align16(off + sizeof(unsigned) * c.nEW);
+  int* mir = reinterpret_cast<int*>(dyn + off);  // [4][SQC_M] this CTA's rows
+  __shared__ int* mirr[16];
+  if (c.tid < C) mirr[c.tid] = cl.map_shared_rank(mir, c.tid);
+  c.mirr = mirr;
   c.st = state;
   c.cr = state;
   c.snap = state;
@@ -2013,6 +2084,12 @@ __global__ void __launch_bounds__(1024) k_seq_cluster(Geo g, Opt o, int* state, 
   c.nfcap = g.n;
   c.w64 = nullptr;
   const int n = g.n;
+#pragma unroll
+  for (int j = 0; j < SQ_J; ++j) {
+    const int u = blockIdx.x * SQC_T + j * C * SQC_T + c.tid;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) mir[q * SQC_M + j * SQC_T + c.tid] = u < n ? state[q * n + u] : 0;
+  }
   for (int w = c.tid; w < c.nW; w += c.B) { c.maskw[w] = 0u; c.special[w] = 0u; }
   for (int w = c.tid; w < c.nEW; w += c.B) c.edgebad[w] = 0u;
   if (lead) { facc_reset(facc, c.tid); facc_reset(facc + 16, c.tid); }
@@ -2021,8 +2098,8 @@ __global__ void __launch_bounds__(1024) k_seq_cluster(Geo g, Opt o, int* state, 
   cl.sync();
   int t = 0;  // attempt counter (the same in every CTA)
 #ifdef NACS_SEQC_PROF
-  unsigned long long prof_[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0}, prof_last_ = 0;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(prof_last_));
+  if (c.tid < 24) seqc_prof_[c.tid] = 0;
+  if (c.tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(seqc_last_));
 #endif
   // the current request's arrays in shared memory (one parallel copy per request: the
   // thread-0 loops of decode, flows, commit and top-up then read on-chip), presented to the
@@ -2085,9 +2162,8 @@ __global__ void __launch_bounds__(1024) k_seq_cluster(Geo g, Opt o, int* state, 
       SEQC_T(2);
       for (;;) {
         unsigned long long* fa = facc + 16 * (t & 1);
-        int xr[SQ_J][4];
         unsigned okb;
-        seqc_filter(c, fa, xr, okb);  // a3 + a4 on this CTA's grid-stride share (rows kept in registers)
+        seqc_filter(c, mir, fa, okb);  // a3 + a4 on this CTA's grid-stride share (rows kept in registers)
         SEQC_T(3);
         cl.sync();  // (1) the exact statistics of every CTA are in fa
         SEQC_T(4);
@@ -2110,6 +2186,7 @@ __global__ void __launch_bounds__(1024) k_seq_cluster(Geo g, Opt o, int* state, 
         }
         if (lead) facc_reset(facc + 16 * ((t + 1) & 1), c.tid);  // read by everyone at the last attempt
         __syncthreads();
+        SEQC_T(12);
         ++t;
         if (s.nf == 0) {  // F empty: reject the request atomically (R20)
           if (lead) req_reject(c, RL, OL, r);
@@ -2132,16 +2209,28 @@ __global__ void __launch_bounds__(1024) k_seq_cluster(Geo g, Opt o, int* state, 
           }
         }
         __syncthreads();
+        SEQC_T(13);
         const TopsisP tp = tps;
         {
-          unsigned long long k1 = 0, k2 = 0;
+          // the thread's top-2 in FP32 (rows re-read from the CTA's copy: no registers held
+          // across the barrier): servers ascend with j, so a strict > keeps the lowest index
+          // first and an equal score lands in s2 (a tie, decided in FP64 below)
+          float s1 = -1.0f, s2 = -1.0f;
+          int j1 = 0;
 #pragma unroll
           for (int j = 0; j < SQ_J; ++j) {
             if (!((okb >> j) & 1u)) continue;
-            const int u = (blockIdx.x * c.NW + c.warp) * 32 + j * gridDim.x * c.B + c.lane;
-            const float rr = topsis32(tp, xr[j][0], xr[j][1], xr[j][2], xr[j][3]);
-            top2_insert(k1, k2, score_key(rr, u));
+            const int* m = mir + j * SQC_T + c.tid;
+            const float rr = topsis32(tp, m[0], m[SQC_M], m[2 * SQC_M], m[3 * SQC_M]);
+            if (rr > s1) { s2 = s1; s1 = rr; j1 = j; }
+            else if (rr > s2) s2 = rr;
           }
+          // as keys: (score, ~index) for the best; the second's index never matters, only
+          // that it ranks below any best of the same score and is nonzero (0 = none)
+          const int u1 = (blockIdx.x * c.NW + c.warp) * 32 + j1 * gridDim.x * c.B + c.lane;
+          const unsigned long long k1 = s1 >= 0.f ? score_key(s1, u1) : 0ull;
+          const unsigned long long k2 = s2 >= 0.f ? ((unsigned long long)__float_as_uint(s2) << 32) | 1ull : 0ull;
+          SEQC_T(14);
           block_top2(c, k1, k2);
           if (c.tid == 0) { kx[2 * q] = s.key1; kx[2 * q + 1] = s.key2; }
         }
@@ -2166,7 +2255,8 @@ __global__ void __launch_bounds__(1024) k_seq_cluster(Geo g, Opt o, int* state, 
           for (int j = 0; j < SQ_J; ++j) {
             if (!((okb >> j) & 1u)) continue;
             const int u = (blockIdx.x * c.NW + c.warp) * 32 + j * gridDim.x * c.B + c.lane;
-            const int x0 = xr[j][0], x1 = xr[j][1], x2 = xr[j][2], x3 = xr[j][3];
+            const int* m = mir + j * SQC_T + c.tid;
+            const int x0 = m[0], x1 = m[SQC_M], x2 = m[2 * SQC_M], x3 = m[3 * SQC_M];
             if (topsis32(tp, x0, x1, x2, x3) < s.thr) continue;
             const double rr = topsis64(tp, x0, x1, x2, x3);
             if (rr > bv || (rr == bv && u < bj)) { bv = rr; bj = u; }
@@ -2216,8 +2306,12 @@ __global__ void __launch_bounds__(1024) k_seq_cluster(Geo g, Opt o, int* state, 
   if (lead) flush_stats(c, stats);
 #ifdef NACS_SEQC_PROF
   if (lead && c.tid == 0)
-    printf("seqc ns: copy+begin %llu %llu prologue %llu filter %llu barriers %llu score %llu merge %llu commit %llu finish %llu\n",
-           prof_[0], prof_[1], prof_[2], prof_[3], prof_[4], prof_[5], prof_[6] + prof_[7], prof_[8], prof_[9]);
+    printf("commit ns: server %llu widest %llu path %llu vpath %llu | prologue: flows+clear %llu fabric %llu fok %llu\n",
+           seqc_prof_[15], seqc_prof_[16], seqc_prof_[17], seqc_prof_[8], seqc_prof_[18], seqc_prof_[19], seqc_prof_[2]);
+    printf("seqc ns: copy %llu begin %llu prologue %llu filter[loop %llu reduce %llu] barriers %llu "
+           "score[stats %llu params %llu loop %llu top2 %llu] merge %llu commit %llu finish %llu\n",
+           seqc_prof_[0], seqc_prof_[1], seqc_prof_[2], seqc_prof_[10], seqc_prof_[3], seqc_prof_[4], seqc_prof_[12],
+           seqc_prof_[13], seqc_prof_[14], seqc_prof_[5], seqc_prof_[6] + seqc_prof_[7], seqc_prof_[8], seqc_prof_[9]);
 #endif
   cl.sync();  // no CTA leaves while another may still read its shared memory
 }
@@ -3572,11 +3666,11 @@ cudaError_t launch_sequential(const Geo& g, const Opt& o, int* d_state, const Re
 
 int seq_cluster_size(const Geo& g) {
   if (const char* e = getenv("NACS_SEQC")) {  // experiments (0 = off)
-    const int C = atoi(e);
-    return C > 0 && C <= 16 && (long long)C * 1024 * SQ_J >= g.n ? C : 0;
+    const int C = atoi(e);  // a power of two (mirror_ptr)
+    return C > 0 && C <= 16 && !(C & (C - 1)) && (long long)C * SQC_M >= g.n ? C : 0;
   }
   if (g.n < 16384 || g.n > 65536) return 0;  // below: the one-CTA engine keeps the state in shared memory
-  return g.n > 32768 ? 16 : 8;  // at most SQ_J = 4 servers per thread (1024 threads per CTA)
+  return g.n > 32768 ? 16 : 8;  // at most SQC_M servers per CTA
 }
 
 cudaError_t launch_seq_cluster(const Geo& g, const Opt& o, int* d_state, const ReqsDev& R, const OutDev& O,
@@ -3588,7 +3682,7 @@ cudaError_t launch_seq_cluster(const Geo& g, const Opt& o, int* d_state, const R
   double* kxv = reinterpret_cast<double*>(work + 64);
   int* kxi = reinterpret_cast<int*>(work + 80);
   const size_t nW = (size_t)(g.n + 31) / 32, nEW = (size_t)(g.E + 31) / 32;
-  const size_t smem = 3 * align16(4 * nW) + align16(4 * nEW);
+  const size_t smem = 3 * align16(4 * nW) + align16(4 * nEW) + sizeof(int) * 4 * SQC_M;
   cudaError_t e;
   if (C > 8 && (e = cudaFuncSetAttribute(k_seq_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) !=
                    cudaSuccess)
@@ -3602,7 +3696,7 @@ cudaError_t launch_seq_cluster(const Geo& g, const Opt& o, int* d_state, const R
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.gridDim = dim3(C, 1, 1);
-  cfg.blockDim = dim3(1024, 1, 1);
+  cfg.blockDim = dim3(SQC_T, 1, 1);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cfg.attrs = attr;

@@ -1,6 +1,6 @@
 """Per-source-line instruction and stall-sample shares of an ncu report (hot lines first).
 
-usage: python scripts/ncu_lines.py report.ncu-rep [n_lines]
+usage: python scripts/ncu_lines.py report.ncu-rep [n_lines] [inst]   (inst: sort by executed instructions)
 """
 import csv
 import io
@@ -25,5 +25,6 @@ for r in csv.reader(io.StringIO(txt)):
             out.append((ex, sm, f"{cur}:{r[0]}", r[1][:100]))
 tot = sum(o[0] for o in out) or 1
 ts = sum(o[1] for o in out) or 1
-for ex, sm, loc, src in sorted(out, key=lambda o: -o[1])[:nl]:
+key = 0 if len(sys.argv) > 3 and sys.argv[3] == "inst" else 1
+for ex, sm, loc, src in sorted(out, key=lambda o: -o[key])[:nl]:
     print(f"{ex / tot * 100:5.1f}% inst {sm / ts * 100:5.1f}% samples  {loc:22s} {src}")
