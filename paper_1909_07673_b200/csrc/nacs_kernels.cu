@@ -110,6 +110,9 @@ struct Ctx {
   unsigned* f0w;       // [nW] R25: the feasible set of the request's first pod step
   unsigned* special;   // [nW] flow servers and excluded servers of the pod step
   unsigned* edgebad;   // [nEW] edge switches some flow cannot reach with its demand
+  unsigned* spok = nullptr;  // k_seq_cluster: [nW] the special servers' own verdict (a flow
+                             // server not excluded and, with path_filter, fok), so the filter
+                             // needs no per-server flow search
   // AHP workspace (ahp_carve): presorted orders, sorted levels, prefix sums
   unsigned short* perm;  // [3][n2] servers in ascending CPU, RAM, access-bandwidth order
   unsigned* dirty;       // [nW] servers whose criteria the current request has changed
@@ -136,11 +139,21 @@ struct Ctx {
 
 #ifdef NACS_SEQC_PROF  // experiment builds: per-phase time of the leader CTA (device printf at the end)
 __shared__ unsigned long long seqc_prof_[24], seqc_last_;
+#ifdef NACS_SEQC_CYCLES  // SM cycles instead of nanoseconds
+#define SEQC_CLOCK() ((unsigned long long)clock64())
+#else
+__device__ __forceinline__ unsigned long long seqc_gt() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define SEQC_CLOCK() seqc_gt()
+#endif
 #define SEQC_T(i)                                                                  \
   do {                                                                             \
     if (blockIdx.x == 0 && threadIdx.x == 0) {                                     \
       unsigned long long now_;                                                     \
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now_));                     \
+      now_ = SEQC_CLOCK();                                                         \
       seqc_prof_[i] += now_ - seqc_last_;                                          \
       seqc_last_ = now_;                                                           \
     }                                                                              \
@@ -1387,6 +1400,7 @@ __device__ void flow_server_ok(Ctx& c) {
       s->fok[f] = ok;
       s->fexcl[f] = 0;
       atomicOr(&c.special[u >> 5], 1u << (u & 31));
+      if (c.spok && (ok || !c.o.path_filter)) atomicOr(&c.spok[u >> 5], 1u << (u & 31));
     }
     if (c.tid == 0) s->G = nbad == 0;
     return;
@@ -1401,6 +1415,7 @@ __device__ void flow_server_ok(Ctx& c) {
     s->fok[f] = ok;
     s->fexcl[f] = 0;
     atomicOr(&c.special[u >> 5], 1u << (u & 31));
+    if (c.spok && (ok || !c.o.path_filter)) atomicOr(&c.spok[u >> 5], 1u << (u & 31));
   }
   if (c.tid == 0) {
     int G = 1;
@@ -1412,6 +1427,8 @@ __device__ void flow_server_ok(Ctx& c) {
 
 __device__ void clear_bitmaps(Ctx& c) {
   for (int w = c.tid; w < c.nW; w += c.B) c.special[w] = 0u;
+  if (c.spok)
+    for (int w = c.tid; w < c.nW; w += c.B) c.spok[w] = 0u;
   for (int w = c.tid; w < c.nEW; w += c.B) c.edgebad[w] = 0u;
 }
 
@@ -1585,6 +1602,7 @@ __device__ void commit_cta(Ctx& c, const ReqsDev& R, int r, int p) {
       for (int i = 0; i < s->nflow; ++i) if (s->fv[i] == u) f = i;
       if (f >= 0) s->fexcl[f] = 1;
       c.special[u >> 5] |= 1u << (u & 31);
+      if (c.spok) c.spok[u >> 5] &= ~(1u << (u & 31));
       s->c_retries += 1;
     } else {
       s->pod_srv[p] = u;
@@ -1998,6 +2016,7 @@ __device__ __forceinline__ void facc_reset(unsigned long long* f, int tid) {
 // cluster lives in one GPC, whose L2 port made the 1 MB global read of every pod step the
 // largest phase) and kept in registers for the scoring pass.
 __device__ __forceinline__ void seqc_filter(Ctx& c, const int* mir, unsigned long long* facc, unsigned& okb) {
+  SEQC_T(21);
   Scratch* s = c.s;
   const Geo& g = c.g;
   const int n = g.n;
@@ -2013,6 +2032,10 @@ __device__ __forceinline__ void seqc_filter(Ctx& c, const int* mir, unsigned lon
 #pragma unroll
     for (int q = 0; q < 4; ++q) x[j][q] = in ? mir[q * SQC_M + j * SQC_T + c.tid] : 0;
   }
+#ifdef NACS_SEQC_PROF
+  asm volatile("" ::"r"(x[0][0]), "r"(x[SQ_J - 1][3]));
+#endif
+  SEQC_T(20);
   int nf = 0, nact = 0;
   unsigned mn0 = UINT_MAX, mn1 = UINT_MAX, mn3 = UINT_MAX, mx0 = 0, mx1 = 0, mx3 = 0;
   unsigned long long q0 = 0, q1 = 0, q3 = 0;
@@ -2024,18 +2047,16 @@ __device__ __forceinline__ void seqc_filter(Ctx& c, const int* mir, unsigned lon
     const int u = base + c.lane;
     const bool in = u < n;
     const int x0 = x[j][0], x1 = x[j][1], x2 = x[j][2], x3 = x[j][3];
-    bool ok = in && x0 >= dc && x1 >= dr;
+    const bool okr = in && x0 >= dc && x1 >= dr;
+    bool ok = okr;
     if (net) {
       const unsigned e = div_h((unsigned)u, g.magic_h);
       ok = ok && G && x3 >= sumD && !((c.edgebad[e >> 5] >> (e & 31)) & 1u);
     }
-    const unsigned sp = c.special[base >> 5];
-    if ((sp >> c.lane) & 1u) {  // a flow server (its own flow needs no network) or an excluded one (R18)
-      int f = -1;
-      for (int i = 0; i < s->nflow; ++i) if (s->fv[i] == u) f = i;
-      if (f < 0 || s->fexcl[f]) ok = false;
-      else ok = x0 >= dc && x1 >= dr && (!c.o.path_filter || s->fok[f]);
-    }
+    // a flow server (its own flow needs no network) or an excluded one (R18): the verdict
+    // flow_server_ok and the exclusions keep in spok
+    const unsigned sp = c.special[base >> 5], so = c.spok[base >> 5];
+    if ((sp >> c.lane) & 1u) ok = okr && ((so >> c.lane) & 1u);
     const unsigned bal = __ballot_sync(FULL, ok);
     if (c.lane == 0) c.maskw[base >> 5] = bal;
     okb |= (ok ? 1u : 0u) << j;
@@ -2073,6 +2094,8 @@ __global__ void __launch_bounds__(SQC_T, 1) k_seq_cluster(Geo g, Opt o, int* sta
   off = align16(off + sizeof(unsigned) * c.nW);
   c.edgebad = reinterpret_cast<unsigned*>(dyn + off);
   off = align16(off + sizeof(unsigned) * c.nEW);
+  c.spok = reinterpret_cast<unsigned*>(dyn + off);
+  off = align16(off + sizeof(unsigned) * c.nW);
   int* mir = reinterpret_cast<int*>(dyn + off);  // [4][SQC_M] this CTA's rows
   __shared__ int* mirr[16];
   if (c.tid < C) mirr[c.tid] = cl.map_shared_rank(mir, c.tid);
@@ -2090,7 +2113,7 @@ __global__ void __launch_bounds__(SQC_T, 1) k_seq_cluster(Geo g, Opt o, int* sta
 #pragma unroll
     for (int q = 0; q < 4; ++q) mir[q * SQC_M + j * SQC_T + c.tid] = u < n ? state[q * n + u] : 0;
   }
-  for (int w = c.tid; w < c.nW; w += c.B) { c.maskw[w] = 0u; c.special[w] = 0u; }
+  for (int w = c.tid; w < c.nW; w += c.B) { c.maskw[w] = 0u; c.special[w] = 0u; c.spok[w] = 0u; }
   for (int w = c.tid; w < c.nEW; w += c.B) c.edgebad[w] = 0u;
   if (lead) { facc_reset(facc, c.tid); facc_reset(facc + 16, c.tid); }
   __syncthreads();
@@ -2099,7 +2122,7 @@ __global__ void __launch_bounds__(SQC_T, 1) k_seq_cluster(Geo g, Opt o, int* sta
   int t = 0;  // attempt counter (the same in every CTA)
 #ifdef NACS_SEQC_PROF
   if (c.tid < 24) seqc_prof_[c.tid] = 0;
-  if (c.tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(seqc_last_));
+  if (c.tid == 0) seqc_last_ = SEQC_CLOCK();
 #endif
   // the current request's arrays in shared memory (one parallel copy per request: the
   // thread-0 loops of decode, flows, commit and top-up then read on-chip), presented to the
@@ -2287,6 +2310,7 @@ __global__ void __launch_bounds__(SQC_T, 1) k_seq_cluster(Geo g, Opt o, int* sta
           if (s.fail) {  // R18: the same exclusion as the leader's
             for (int i = 0; i < s.nflow; ++i) if (s.fv[i] == u) s.fexcl[i] = 1;
             c.special[u >> 5] |= 1u << (u & 31);
+            c.spok[u >> 5] &= ~(1u << (u & 31));
           } else {
             s.pod_srv[p] = u;
           }
@@ -2305,13 +2329,15 @@ __global__ void __launch_bounds__(SQC_T, 1) k_seq_cluster(Geo g, Opt o, int* sta
   }
   if (lead) flush_stats(c, stats);
 #ifdef NACS_SEQC_PROF
-  if (lead && c.tid == 0)
+  if (lead && c.tid == 0) {
+    printf("filter: pre %llu loads %llu\n", seqc_prof_[21], seqc_prof_[20]);
     printf("commit ns: server %llu widest %llu path %llu vpath %llu | prologue: flows+clear %llu fabric %llu fok %llu\n",
            seqc_prof_[15], seqc_prof_[16], seqc_prof_[17], seqc_prof_[8], seqc_prof_[18], seqc_prof_[19], seqc_prof_[2]);
     printf("seqc ns: copy %llu begin %llu prologue %llu filter[loop %llu reduce %llu] barriers %llu "
            "score[stats %llu params %llu loop %llu top2 %llu] merge %llu commit %llu finish %llu\n",
            seqc_prof_[0], seqc_prof_[1], seqc_prof_[2], seqc_prof_[10], seqc_prof_[3], seqc_prof_[4], seqc_prof_[12],
            seqc_prof_[13], seqc_prof_[14], seqc_prof_[5], seqc_prof_[6] + seqc_prof_[7], seqc_prof_[8], seqc_prof_[9]);
+  }
 #endif
   cl.sync();  // no CTA leaves while another may still read its shared memory
 }
@@ -3682,7 +3708,7 @@ cudaError_t launch_seq_cluster(const Geo& g, const Opt& o, int* d_state, const R
   double* kxv = reinterpret_cast<double*>(work + 64);
   int* kxi = reinterpret_cast<int*>(work + 80);
   const size_t nW = (size_t)(g.n + 31) / 32, nEW = (size_t)(g.E + 31) / 32;
-  const size_t smem = 3 * align16(4 * nW) + align16(4 * nEW) + sizeof(int) * 4 * SQC_M;
+  const size_t smem = 4 * align16(4 * nW) + align16(4 * nEW) + sizeof(int) * 4 * SQC_M;
   cudaError_t e;
   if (C > 8 && (e = cudaFuncSetAttribute(k_seq_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) !=
                    cudaSuccess)
