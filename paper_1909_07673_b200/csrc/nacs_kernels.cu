@@ -2040,23 +2040,28 @@ __device__ __forceinline__ void seqc_filter(Ctx& c, const int* mir, unsigned lon
   unsigned mn0 = UINT_MAX, mn1 = UINT_MAX, mn3 = UINT_MAX, mx0 = 0, mx1 = 0, mx3 = 0;
   unsigned long long q0 = 0, q1 = 0, q3 = 0;
   okb = 0;
+  // the bitmap words of every share first (independent loads), then branch-free tests
+  unsigned eb[SQ_J], sp[SQ_J], so[SQ_J];
+#pragma unroll
+  for (int j = 0; j < SQ_J; ++j) {
+    const int base = start + j * stride;
+    const int w = base < n ? base >> 5 : 0;
+    const unsigned e = div_h((unsigned)min(base + c.lane, n - 1), g.magic_h);
+    eb[j] = net ? c.edgebad[e >> 5] >> (e & 31) : 0u;
+    sp[j] = c.special[w] >> c.lane;
+    so[j] = c.spok[w] >> c.lane;
+  }
 #pragma unroll
   for (int j = 0; j < SQ_J; ++j) {
     const int base = start + j * stride;
     if (base >= n) break;  // warp-uniform
-    const int u = base + c.lane;
-    const bool in = u < n;
+    const bool in = base + c.lane < n;
     const int x0 = x[j][0], x1 = x[j][1], x2 = x[j][2], x3 = x[j][3];
-    const bool okr = in && x0 >= dc && x1 >= dr;
-    bool ok = okr;
-    if (net) {
-      const unsigned e = div_h((unsigned)u, g.magic_h);
-      ok = ok && G && x3 >= sumD && !((c.edgebad[e >> 5] >> (e & 31)) & 1u);
-    }
+    const bool okr = in & (x0 >= dc) & (x1 >= dr);
     // a flow server (its own flow needs no network) or an excluded one (R18): the verdict
     // flow_server_ok and the exclusions keep in spok
-    const unsigned sp = c.special[base >> 5], so = c.spok[base >> 5];
-    if ((sp >> c.lane) & 1u) ok = okr && ((so >> c.lane) & 1u);
+    const bool ok = (sp[j] & 1u) ? okr & ((so[j] & 1u) != 0u)
+                                 : okr & (!net | (G & (x3 >= sumD) & !(eb[j] & 1u)));
     const unsigned bal = __ballot_sync(FULL, ok);
     if (c.lane == 0) c.maskw[base >> 5] = bal;
     okb |= (ok ? 1u : 0u) << j;
