@@ -89,6 +89,12 @@ struct Scratch {
   double scand_total[2];
   int scan_total;
   int lvK, m1, nd, ntouched, touch_over, presorted;
+  // cluster-wide scans (k_sh_levels): this CTA's totals, read by the others over DSMEM
+  // (double-buffered by call parity), and the scan's result
+  int cl_pub[2];
+  double cl_pubd[2][2];
+  int cl_base, cl_total;
+  double cl_based[2], cl_totald[2];
   int touched[2 * MAXC];   // servers with changed criteria in the current request (AHP)
   float dval[2 * MAXC];    // dirty feasible values / servers of a pod step, sorted
   int dsrv[2 * MAXC];
@@ -2816,6 +2822,303 @@ __global__ void __launch_bounds__(1024) k_sh_levels(Geo g, Opt o, int* state, Sh
   }
 }
 
+// ---- the same level extraction on a cluster of CL CTAs per criterion (k_sh_levels_cl) ----
+// Every loop of presorted_collect / ahp_levels_sorted / ahp_prefix runs over the cluster's
+// warps (global warp segments); the scans between warps become a CTA scan plus a scan over
+// the CTAs' totals read over DSMEM; the work arrays (keys, levels, prefix sums) are the
+// criterion's global slices as before.  The thread-0 merge list of touched servers is
+// replicated in every CTA (each reads the same global values).  Same results as the one-CTA
+// kernel: the same sorted order, levels and (exact, integer-valued) FP64 prefix sums.
+struct ClSeg {
+  int r, C;  // this CTA's rank in the cluster, cluster size
+  int par;   // scan call parity
+};
+__device__ __forceinline__ void cl_seg(const Ctx& c, const ClSeg& q, int N, int& s0, int& s1) {
+  const int GW = q.C * c.NW;
+  const int seg = ((N + GW - 1) / GW + 31) & ~31;
+  s0 = min((q.r * c.NW + c.warp) * seg, N);
+  s1 = min(s0 + seg, N);
+}
+// exclusive scan over all warps of the cluster of one int per warp; *total = the sum
+__device__ int cl_exscan(Ctx& c, ClSeg& q, cgx::cluster_group& cl, int x, int* total) {
+  Scratch* s = c.s;
+  int cta_total;
+  const int r = warp_exscan(c, x, &cta_total);
+  const int par = q.par;
+  q.par ^= 1;
+  if (c.tid == 0) s->cl_pub[par] = cta_total;
+  cl.sync();
+  if (c.warp == 0) {
+    const int v = c.lane < q.C ? *cl.map_shared_rank(&s->cl_pub[par], c.lane) : 0;
+    int iv = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(FULL, iv, o);
+      if (c.lane >= o) iv += y;
+    }
+    const int base = __shfl_sync(FULL, iv - v, q.r), tot = __shfl_sync(FULL, iv, 31);
+    if (c.lane == 0) { s->cl_base = base; s->cl_total = tot; }
+  }
+  __syncthreads();
+  *total = s->cl_total;
+  const int b = s->cl_base;
+  __syncthreads();
+  return r + b;
+}
+__device__ void cl_exscan_d2(Ctx& c, ClSeg& q, cgx::cluster_group& cl, double& a, double& b, double* ta, double* tb) {
+  Scratch* s = c.s;
+  double A, B;
+  warp_exscan_d2(c, a, b, &A, &B);
+  const int par = q.par;
+  q.par ^= 1;
+  if (c.tid == 0) { s->cl_pubd[par][0] = A; s->cl_pubd[par][1] = B; }
+  cl.sync();
+  if (c.warp == 0) {
+    double va = 0.0, vb = 0.0;
+    if (c.lane < q.C) {
+      const double* rp = cl.map_shared_rank(&s->cl_pubd[par][0], c.lane);
+      va = rp[0];
+      vb = rp[1];
+    }
+    double ia = va, ib = vb;
+    for (int o = 1; o < 32; o <<= 1) {
+      const double ya = __shfl_up_sync(FULL, ia, o), yb = __shfl_up_sync(FULL, ib, o);
+      if (c.lane >= o) { ia += ya; ib += yb; }
+    }
+    const double ba = __shfl_sync(FULL, ia - va, q.r), bb = __shfl_sync(FULL, ib - vb, q.r);
+    const double sa = __shfl_sync(FULL, ia, 31), sb = __shfl_sync(FULL, ib, 31);
+    if (c.lane == 0) { s->cl_based[0] = ba; s->cl_based[1] = bb; s->cl_totald[0] = sa; s->cl_totald[1] = sb; }
+  }
+  __syncthreads();
+  a += s->cl_based[0];
+  b += s->cl_based[1];
+  *ta = s->cl_totald[0];
+  *tb = s->cl_totald[1];
+  __syncthreads();
+}
+
+// presorted_collect(c, ci, true) over the cluster
+__device__ int cl_collect(Ctx& c, ClSeg& q, cgx::cluster_group& cl, int ci) {
+  Scratch* s = c.s;
+  const int n = c.g.n, P2 = next_pow2(n);
+  const int* x = c.cr + crit_of(ci) * n;
+  const unsigned short* perm = c.perm + ci * P2;
+  int s0, s1;
+  cl_seg(c, q, n, s0, s1);
+  int cnt = 0;
+#pragma unroll 4
+  for (int base = s0; base < s1; base += 32) {
+    const int i = base + c.lane;
+    const int u = i < s1 ? perm[i] : 0;
+    const bool k = i < s1 && feas_bit(c, u) && !((c.dirty[u >> 5] >> (u & 31)) & 1u);
+    cnt += __popc(__ballot_sync(FULL, k));
+  }
+  int mtot;
+  int pos = cl_exscan(c, q, cl, cnt, &mtot);
+#pragma unroll 4
+  for (int base = s0; base < s1; base += 32) {
+    const int i = base + c.lane;
+    const int u = i < s1 ? perm[i] : 0;
+    const bool k = i < s1 && feas_bit(c, u) && !((c.dirty[u >> 5] >> (u & 31)) & 1u);
+    const unsigned bal = __ballot_sync(FULL, k);
+    if (k) {
+      const int qq = pos + __popc(bal & ((1u << c.lane) - 1u));
+      c.keys2[qq] = (float)x[u];
+      c.sidx2[qq] = u;
+    }
+    pos += __popc(bal);
+  }
+  if (c.tid == 0) {  // touched feasible servers, insertion-sorted by current value (every CTA)
+    int d = 0;
+    const int nt = min(s->ntouched, 2 * MAXC);
+    for (int t = 0; t < nt; ++t) {
+      const int u = s->touched[t];
+      if (!feas_bit(c, u)) continue;
+      const float v = (float)x[u];
+      int j = d;
+      while (j > 0 && s->dval[j - 1] > v) { s->dval[j] = s->dval[j - 1]; s->dsrv[j] = s->dsrv[j - 1]; --j; }
+      s->dval[j] = v;
+      s->dsrv[j] = u;
+      ++d;
+    }
+    s->nd = d;
+  }
+  cl.sync();  // keys2 / sidx2 complete; nd in every CTA
+  const int m1 = mtot, d = s->nd;
+  const int gt = q.r * c.B + c.tid, gB = q.C * c.B;
+  for (int i = gt; i < m1; i += gB) {
+    const float v = c.keys2[i];
+    int lo = 0, hi = d;
+    while (lo < hi) { int mid = (lo + hi) >> 1; if (s->dval[mid] < v) lo = mid + 1; else hi = mid; }
+    c.keys[i + lo] = v;
+    c.sidx[i + lo] = c.sidx2[i];
+  }
+  for (int j = gt; j < d; j += gB) {
+    const float v = s->dval[j];
+    int lo = 0, hi = m1;
+    while (lo < hi) { int mid = (lo + hi) >> 1; if (c.keys2[mid] <= v) lo = mid + 1; else hi = mid; }
+    c.keys[j + lo] = v;
+    c.sidx[j + lo] = s->dsrv[j];
+  }
+  cl.sync();
+  return m1 + d;
+}
+
+// ahp_levels_sorted over the cluster
+__device__ int cl_levels_sorted(Ctx& c, ClSeg& q, cgx::cluster_group& cl, int m) {
+  int s0, s1;
+  cl_seg(c, q, m, s0, s1);
+  int cnt = 0;
+#pragma unroll 4
+  for (int base = s0; base < s1; base += 32) {
+    const int i = base + c.lane;
+    const bool f = i < s1 && (i == 0 || c.keys[i] != c.keys[i - 1]);
+    cnt += __popc(__ballot_sync(FULL, f));
+  }
+  int K;
+  int l0 = cl_exscan(c, q, cl, cnt, &K);
+#pragma unroll 2
+  for (int base = s0; base < s1; base += 32) {
+    const int i = base + c.lane;
+    const bool in = i < s1;
+    const bool f = in && (i == 0 || c.keys[i] != c.keys[i - 1]);
+    const unsigned bal = __ballot_sync(FULL, f);
+    const int qq = l0 + __popc(bal & (0xffffffffu >> (31 - c.lane))) - 1;
+    if (f) {
+      c.lvm[qq].x = c.keys[i];
+      c.lst[qq] = i;
+    }
+    if (in) c.lvl[c.sidx[i]] = qq;
+    l0 += __popc(bal);
+  }
+  cl.sync();
+  const int gt = q.r * c.B + c.tid, gB = q.C * c.B;
+  for (int l = gt; l < K; l += gB) c.lvm[l].y = (float)((l + 1 < K ? c.lst[l + 1] : m) - c.lst[l]);
+  cl.sync();
+  return K;
+}
+
+// ahp_levels_active over the cluster
+__device__ int cl_levels_active(Ctx& c, ClSeg& q, cgx::cluster_group& cl) {
+  Scratch* s = c.s;
+  const int n = c.g.n;
+  const int nf = s->nf, nact = s->nact;
+  const int K = (nact > 0) + (nact < nf);
+  const int gt = q.r * c.B + c.tid, gB = q.C * c.B;
+  for (int u = gt; u < n; u += gB)
+    if (feas_bit(c, u)) c.lvl[u] = c.st[2 * n + u] ? (nact < nf ? 1 : 0) : 0;
+  if (q.r == 0 && c.tid == 0) {
+    int l = 0;
+    if (nact < nf) c.lvm[l++] = make_float2(0.0f, (float)(nf - nact));
+    if (nact > 0) c.lvm[l++] = make_float2(1.0f, (float)nact);
+  }
+  cl.sync();
+  return K;
+}
+
+// ahp_prefix over the cluster
+__device__ void cl_prefix(Ctx& c, ClSeg& q, cgx::cluster_group& cl, int K, const float2* lv) {
+  int s0, s1;
+  cl_seg(c, q, K, s0, s1);
+  double ta = 0, tb = 0;
+  for (int base = s0; base < s1; base += 32) {
+    const int i = base + c.lane;
+    if (i < s1) { const float2 e = lv[i]; ta += (double)e.y; tb += (double)e.y * (double)e.x; }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) { ta += __shfl_xor_sync(FULL, ta, o); tb += __shfl_xor_sync(FULL, tb, o); }
+  double TA, TB;
+  cl_exscan_d2(c, q, cl, ta, tb, &TA, &TB);
+  double ra = ta, rb = tb;
+  for (int base = s0; base < s1; base += 32) {
+    const int i = base + c.lane;
+    double a = 0, b = 0;
+    if (i < s1) { const float2 e = lv[i]; a = (double)e.y; b = (double)e.y * (double)e.x; }
+    double ia = a, ib = b;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double ya = __shfl_up_sync(FULL, ia, o), yb = __shfl_up_sync(FULL, ib, o);
+      if (c.lane >= o) { ia += ya; ib += yb; }
+    }
+    if (i < s1) { c.pa[i] = ra + (ia - a); c.pb[i] = rb + (ib - b); }
+    ra += __shfl_sync(FULL, ia, 31);
+    rb += __shfl_sync(FULL, ib, 31);
+  }
+  if (q.r == 0 && c.tid == 0) { c.pa[K] = TA; c.pb[K] = TB; }
+}
+
+// k_sh_levels on a cluster per criterion: grid = 4 clusters of C CTAs (criterion = cluster id)
+__global__ void __launch_bounds__(1024) k_sh_levels_cl(Geo g, Opt o, int* state, ShardDev d) {
+  const int phase = d.ctl[0];
+  if (phase != PH_NEWPOD && phase != PH_RETRY) return;
+  cgx::cluster_group cl = cgx::this_cluster();
+  ClSeg q;
+  q.r = (int)cl.block_rank();
+  q.C = (int)cl.num_blocks();
+  q.par = 0;
+  const int k = blockIdx.x / q.C;
+  const Scratch* gs = d.gs;
+  if (gs->nf == 0) return;  // rejected in k_sh_prep (the same in every CTA)
+  const int n2 = next_pow2(g.n);
+  if (gs->touch_over) {  // the presorted orders are rebuilt: k_sh_levels' one-CTA path, CTA 0
+    if (blockIdx.x != 0) return;
+    Ctx c;
+    sh_ctx(c, g, o, state, d);
+    for (int kk = 0; kk < 4; ++kk) {
+      if (c.s->ahp_const[kk]) {
+        if (c.tid == 0) d.Kc[kk] = 0;
+        continue;
+      }
+      ahp_slice(c, d, kk);
+      const int K = ahp_levels_of(c, kk);
+      ahp_prefix(c, K, c.lvm);
+      for (int l = c.tid; l < K; l += c.B) { d.wq[kk * n2 + l] = 0.f; d.l2q[kk * n2 + l] = 0.f; }
+      if (c.tid == 0) {
+        d.Kc[kk] = K;
+        c.s->c_pairs += (unsigned long long)K * (unsigned long long)(K - 1) / 2;
+      }
+      __syncthreads();
+    }
+    return;
+  }
+  if (gs->ahp_const[k]) {
+    if (q.r == 0 && threadIdx.x == 0) d.Kc[k] = 0;
+    return;
+  }
+  __shared__ Scratch ls;
+  extern __shared__ unsigned sh_bits[];
+  {
+    const int* src = reinterpret_cast<const int*>(gs);
+    int* dst = reinterpret_cast<int*>(&ls);
+    for (int i = threadIdx.x; i < (int)(sizeof(Scratch) / 4); i += blockDim.x) dst[i] = src[i];
+  }
+  Ctx c;
+  sh_ctx(c, g, o, state, d);
+  c.s = &ls;
+  for (int w = c.tid; w < c.nW; w += c.B) {
+    sh_bits[w] = c.maskw[w];
+    sh_bits[c.nW + w] = c.dirty[w];
+  }
+  __syncthreads();
+  c.maskw = sh_bits;
+  c.dirty = sh_bits + c.nW;
+  int* sc = d.lvscr + (size_t)k * 5 * (n2 + 1);
+  c.keys = reinterpret_cast<float*>(sc);
+  c.sidx = sc + (n2 + 1);
+  c.keys2 = reinterpret_cast<float*>(sc + 2 * (n2 + 1));
+  c.sidx2 = sc + 3 * (n2 + 1);
+  c.lst = sc + 4 * (n2 + 1);
+  ahp_slice(c, d, k);
+  const int K = k == 2 ? cl_levels_active(c, q, cl) : cl_levels_sorted(c, q, cl, cl_collect(c, q, cl, k == 3 ? 2 : k));
+  cl_prefix(c, q, cl, K, c.lvm);
+  const int gt = q.r * c.B + c.tid, gB = q.C * c.B;
+  for (int l = gt; l < K; l += gB) { d.wq[k * n2 + l] = 0.f; d.l2q[k * n2 + l] = 0.f; }
+  if (q.r == 0 && c.tid == 0) {
+    d.Kc[k] = K;
+    atomicAdd(&d.gs->c_pairs, (unsigned long long)K * (unsigned long long)(K - 1) / 2);
+  }
+  cl.sync();  // no CTA leaves while another may still read its shared memory
+}
+
 // TOPSIS: closeness of this rank's servers [lo, hi); top-2 keys into slot
 __global__ void __launch_bounds__(1024) k_sh_score(Geo g, Opt o, int* state, int lo, int hi, int slot,
                                                    ShardDev d) {
@@ -3408,6 +3711,13 @@ cudaError_t launch_ahp_decide(bool fp64, const Geo& g, const Opt& o, int* state,
 
 size_t scratch_bytes() { return sizeof(Scratch); }
 
+// CTAs per criterion of the sharded engine's AHP level extraction (1: k_sh_levels, one CTA)
+static int sh_levels_cluster() {
+  int C = 8;
+  if (const char* e = getenv("NACS_LEVELS_CLUSTER")) C = atoi(e);  // experiments: 1, 2, 4, 8, 16
+  return C < 1 || C > 16 ? 8 : C;
+}
+
 cudaError_t launch_sh_begin(const Geo& g, const Opt& o, int* state, const ReqsDev& R, const OutDev& O, int r,
                             const ShardDev& d, cudaStream_t st) {
   if (o.method == 1) {
@@ -3433,7 +3743,29 @@ cudaError_t launch_sh_prep(const Geo& g, const Opt& o, int* state, const ReqsDev
     k_sh_prep<1><<<1, 1024, 0, st>>>(g, o, state, R, O, r, d);
   } else {
     k_sh_prep<0><<<1, 1024, 0, st>>>(g, o, state, R, O, r, d);
-    k_sh_levels<<<4, 1024, bits, st>>>(g, o, state, d);  // one CTA per criterion
+    const int CL = sh_levels_cluster();
+    if (CL <= 1) {
+      k_sh_levels<<<4, 1024, bits, st>>>(g, o, state, d);  // one CTA per criterion
+    } else {  // a cluster of CL CTAs per criterion
+      if (CL > 8) {
+        cudaError_t e = cudaFuncSetAttribute(k_sh_levels_cl, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (e != cudaSuccess) return e;
+      }
+      cudaLaunchConfig_t cfg = {};
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = CL;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.gridDim = dim3(4 * CL, 1, 1);
+      cfg.blockDim = dim3(1024, 1, 1);
+      cfg.dynamicSmemBytes = bits;
+      cfg.stream = st;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      cudaError_t e = cudaLaunchKernelEx(&cfg, k_sh_levels_cl, g, o, state, d);
+      if (e != cudaSuccess) return e;
+    }
   }
   return cudaGetLastError();
 }

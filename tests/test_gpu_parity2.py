@@ -320,3 +320,31 @@ def test_seq_cluster_random_sweep(ctx):
             for key in sa:
                 assert np.array_equal(sa[key], sb[key]), (k, trial, key)
             assert pa == pb
+
+
+@pytest.mark.parametrize("k,nreq", [(32, 6), (64, 2)])
+def test_ahp_levels_cluster_equals_one_cta(k, nreq):
+    """The grid engine's AHP level extraction on a cluster of CTAs per criterion
+    (k_sh_levels_cl, NACS_LEVELS_CLUSTER = 4, 8, 16) equals the one-CTA kernel (= 1): same
+    placements, final state and pair counts (the levels and their exact prefix sums)."""
+    import os
+    from paper_1909_07673_b200 import nacs
+    snap = gen.snapshot(k, seed=77 + k, quantised=k == 64)
+    reqs = gen.requests(nreq, 300 + k)
+    res = []
+    for cl in ("1", "4", "8", "16"):
+        os.environ["NACS_LEVELS_CLUSTER"] = cl
+        c = nacs.Context(0)
+        try:
+            c.load_topology(snap)
+            out = to_np(c.schedule_request(reqs, "ahp", "network"))
+            res.append((out, c.read_topology(), c.last_stats()))
+        finally:
+            c.close()
+            os.environ.pop("NACS_LEVELS_CLUSTER", None)
+    for out, st, stats in res[1:]:
+        for key in out:
+            assert np.array_equal(out[key], res[0][0][key]), key
+        for key in st:
+            assert np.array_equal(st[key], res[0][1][key]), key
+        assert stats["ahp_pairs"] == res[0][2]["ahp_pairs"] and stats["pod_steps"] == res[0][2]["pod_steps"]
