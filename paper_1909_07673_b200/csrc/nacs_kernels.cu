@@ -2631,7 +2631,7 @@ __global__ void __launch_bounds__(1024) k_sh_begin(Geo g, Opt o, int* state, Req
   sh_ctx(c, g, o, state, d);
   Scratch* s = c.s;
   if (r == 0) init_minfab(c);  // the call's first request: the bound of the live state
-  if (first == 2 && d.facc[15]) {  // AHP: k_sh_presort has just rebuilt the presorted orders
+  if (first == 2 && d.facc[15]) {  // AHP: k_presort_runs / _merge have just rebuilt the presorted orders
     for (int w = c.tid; w < c.nW; w += c.B) c.dirty[w] = 0u;
     if (c.tid == 0) { s->ntouched = 0; s->touch_over = 0; s->presorted = 1; }
     __syncthreads();
@@ -2657,30 +2657,75 @@ __global__ void __launch_bounds__(1024) k_sh_begin(Geo g, Opt o, int* state, Req
   if (c.tid == 0) { d.ctl[0] = PH_NEWPOD; d.ctl[1] = 0; }
 }
 
-// AHP on the sharded engine: the presorted orders of the three criteria rebuilt in parallel,
-// one CTA per criterion (they were sorted one after another by k_sh_begin's one CTA, ~12 ms
-// at C5), when the request is the call's first or the previous request overflowed the merge
-// list.  The decision is published in facc[15] for k_sh_begin, which resets the flags.
-__global__ void __launch_bounds__(1024) k_sh_presort(Geo g, Opt o, int* state, ShardDev d, int first) {
+// AHP on the sharded engine: the presorted orders of the three criteria, rebuilt when the
+// request is the call's first or the previous request overflowed the merge list (the
+// decision is published in facc[15] for k_sh_begin, which resets the flags), from sorted
+// runs: k_presort_runs sorts runs of SQP_RUN keys
+// (value << 32 | server: unique, so every order is total) in shared memory, one CTA per run
+// and criterion; k_presort_merge puts each key at its final position — its position in its
+// run plus the count of smaller keys in every other run (binary searches).  (A bitonic sort
+// over global memory by one CTA per criterion took 5 ms at C5.)
+constexpr int SQP_RUN = 8192;  // keys per run (64 KB of shared memory)
+__device__ __forceinline__ unsigned long long* presort_runs(const ShardDev& d, int ci, int P2) {
+  const size_t off = ((size_t)ci * 5 * (P2 + 1) + 1) & ~(size_t)1;  // 8-byte aligned in the slice
+  return reinterpret_cast<unsigned long long*>(d.lvscr + off);
+}
+__device__ __forceinline__ bool presort_needed(const ShardDev& d, int first) {
   const Scratch* gs = d.gs;
-  const bool need = first || gs->touch_over || !gs->presorted;
+  return first || gs->touch_over || !gs->presorted;
+}
+__global__ void __launch_bounds__(1024) k_presort_runs(Geo g, int* state, ShardDev d, int first) {
+  const bool need = presort_needed(d, first);
   if (blockIdx.x == 0 && threadIdx.x == 0) d.facc[15] = need ? 1ull : 0ull;
   if (!need) return;
-  const int ci = blockIdx.x;
-  Ctx c;
-  sh_ctx(c, g, o, state, d);
-  const int n = g.n, P2 = next_pow2(n);
-  int* sc = d.lvscr + (size_t)ci * 5 * (P2 + 1);
-  c.keys = reinterpret_cast<float*>(sc);
-  c.sidx = sc + (P2 + 1);
-  const int* x = c.cr + crit_of(ci) * n;
-  for (int i = c.tid; i < P2; i += c.B) {
-    c.keys[i] = i < n ? (float)x[i] : FLT_MAX;
-    c.sidx[i] = i;
+  extern __shared__ unsigned long long sk[];
+  const int n = g.n, P2 = next_pow2(n), S = min(P2, SQP_RUN), R = P2 / S;
+  const int ci = blockIdx.x / R, run = blockIdx.x % R;
+  const int* x = state + crit_of(ci) * n;
+  for (int i = threadIdx.x; i < S; i += blockDim.x) {
+    const int u = run * S + i;
+    sk[i] = u < n ? ((unsigned long long)(unsigned)x[u] << 32) | (unsigned)u : ~0ull;
   }
   __syncthreads();
-  bitonic(c, P2);
-  for (int i = c.tid; i < n; i += c.B) c.perm[ci * P2 + i] = (unsigned short)c.sidx[i];
+  for (int k = 2; k <= S; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < S; i += blockDim.x) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const unsigned long long a = sk[i], b = sk[ixj];
+          if ((a > b) == ((i & k) == 0)) { sk[i] = b; sk[ixj] = a; }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  unsigned long long* out = presort_runs(d, ci, P2) + (size_t)run * S;
+  for (int i = threadIdx.x; i < S; i += blockDim.x) out[i] = sk[i];
+}
+__global__ void __launch_bounds__(256) k_presort_merge(Geo g, ShardDev d, int first) {
+  if (!presort_needed(d, first)) return;
+  const int n = g.n, P2 = next_pow2(n), S = min(P2, SQP_RUN), R = P2 / S;
+  unsigned short* perm = reinterpret_cast<unsigned short*>(d.ahp_ws);  // ahp_carve: perm first
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < 3 * P2; t += gridDim.x * blockDim.x) {
+    const int ci = t / P2, i = t - ci * P2, run = i / S;
+    const unsigned long long* runs = presort_runs(d, ci, P2);
+    const unsigned long long key = runs[i];
+    const int u = (int)(unsigned)(key & 0xffffffffull);
+    if (key == ~0ull || u >= n) continue;
+    int pos = i - run * S;
+    for (int r2 = 0; r2 < R; ++r2) {
+      if (r2 == run) continue;
+      const unsigned long long* a = runs + (size_t)r2 * S;
+      int lo = 0, hi = S;  // keys of run r2 below key
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (a[mid] < key) lo = mid + 1;
+        else hi = mid;
+      }
+      pos += lo;
+    }
+    perm[ci * P2 + pos] = (unsigned short)u;
+  }
 }
 
 // pod prologue (new pod) + filter and statistics over all servers (replicated)
@@ -3723,7 +3768,12 @@ cudaError_t launch_sh_begin(const Geo& g, const Opt& o, int* state, const ReqsDe
   if (o.method == 1) {
     k_sh_begin<1><<<1, 1024, 0, st>>>(g, o, state, R, O, r, d, r == 0);
   } else {
-    k_sh_presort<<<3, 1024, 0, st>>>(g, o, state, d, r == 0);
+    const int P2 = next_pow2(g.n), S = P2 < SQP_RUN ? P2 : SQP_RUN;
+    const size_t sm = sizeof(unsigned long long) * (size_t)S;
+    cudaError_t e = cudaFuncSetAttribute(k_presort_runs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    k_presort_runs<<<3 * (P2 / S), 1024, sm, st>>>(g, state, d, r == 0);
+    k_presort_merge<<<(3 * P2 + 255) / 256, 256, 0, st>>>(g, d, r == 0);
     k_sh_begin<0><<<1, 1024, 0, st>>>(g, o, state, R, O, r, d, 2);
   }
   return cudaGetLastError();
