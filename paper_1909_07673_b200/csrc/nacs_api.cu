@@ -707,6 +707,7 @@ nacs_status schedule_sharded(nacs_ctx* ctx, const Opt& o, const nacs::ReqsDev& R
   d.ulog = ctx->ulog.p;
   d.stats = ctx->stats.p;
   CK(cudaMemsetAsync(d.maskw, 0, 2 * b_bm + b_e, ctx->stream));
+  CK(cudaMemsetAsync(d.facc, 0, b_facc, ctx->stream));  // [14]: no presorted-order update pending
   int* ctl = reinterpret_cast<int*>(ctx->sh_ctl.p);
   // this process's shards: all of them in loopback, its own rank otherwise
   const int s_lo = ctx->loopback ? 0 : ctx->rank, s_hi = ctx->loopback ? world : ctx->rank + 1;

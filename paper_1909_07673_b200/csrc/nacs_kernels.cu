@@ -2941,7 +2941,8 @@ __device__ void cl_exscan_d2(Ctx& c, ClSeg& q, cgx::cluster_group& cl, double& a
   __syncthreads();
 }
 
-// presorted_collect(c, ci, true) over the cluster
+// presorted_collect(c, ci, FEAS) over the cluster
+template <bool FEAS>
 __device__ int cl_collect(Ctx& c, ClSeg& q, cgx::cluster_group& cl, int ci) {
   Scratch* s = c.s;
   const int n = c.g.n, P2 = next_pow2(n);
@@ -2954,7 +2955,7 @@ __device__ int cl_collect(Ctx& c, ClSeg& q, cgx::cluster_group& cl, int ci) {
   for (int base = s0; base < s1; base += 32) {
     const int i = base + c.lane;
     const int u = i < s1 ? perm[i] : 0;
-    const bool k = i < s1 && feas_bit(c, u) && !((c.dirty[u >> 5] >> (u & 31)) & 1u);
+    const bool k = i < s1 && (!FEAS || feas_bit(c, u)) && !((c.dirty[u >> 5] >> (u & 31)) & 1u);
     cnt += __popc(__ballot_sync(FULL, k));
   }
   int mtot;
@@ -2963,7 +2964,7 @@ __device__ int cl_collect(Ctx& c, ClSeg& q, cgx::cluster_group& cl, int ci) {
   for (int base = s0; base < s1; base += 32) {
     const int i = base + c.lane;
     const int u = i < s1 ? perm[i] : 0;
-    const bool k = i < s1 && feas_bit(c, u) && !((c.dirty[u >> 5] >> (u & 31)) & 1u);
+    const bool k = i < s1 && (!FEAS || feas_bit(c, u)) && !((c.dirty[u >> 5] >> (u & 31)) & 1u);
     const unsigned bal = __ballot_sync(FULL, k);
     if (k) {
       const int qq = pos + __popc(bal & ((1u << c.lane) - 1u));
@@ -2972,12 +2973,12 @@ __device__ int cl_collect(Ctx& c, ClSeg& q, cgx::cluster_group& cl, int ci) {
     }
     pos += __popc(bal);
   }
-  if (c.tid == 0) {  // touched feasible servers, insertion-sorted by current value (every CTA)
+  if (c.tid == 0) {  // touched (feasible) servers, insertion-sorted by current value (every CTA)
     int d = 0;
     const int nt = min(s->ntouched, 2 * MAXC);
     for (int t = 0; t < nt; ++t) {
       const int u = s->touched[t];
-      if (!feas_bit(c, u)) continue;
+      if (FEAS && !feas_bit(c, u)) continue;
       const float v = (float)x[u];
       int j = d;
       while (j > 0 && s->dval[j - 1] > v) { s->dval[j] = s->dval[j - 1]; s->dsrv[j] = s->dsrv[j - 1]; --j; }
@@ -3153,7 +3154,7 @@ __global__ void __launch_bounds__(1024) k_sh_levels_cl(Geo g, Opt o, int* state,
   c.sidx2 = sc + 3 * (n2 + 1);
   c.lst = sc + 4 * (n2 + 1);
   ahp_slice(c, d, k);
-  const int K = k == 2 ? cl_levels_active(c, q, cl) : cl_levels_sorted(c, q, cl, cl_collect(c, q, cl, k == 3 ? 2 : k));
+  const int K = k == 2 ? cl_levels_active(c, q, cl) : cl_levels_sorted(c, q, cl, cl_collect<true>(c, q, cl, k == 3 ? 2 : k));
   cl_prefix(c, q, cl, K, c.lvm);
   const int gt = q.r * c.B + c.tid, gB = q.C * c.B;
   for (int l = gt; l < K; l += gB) { d.wq[k * n2 + l] = 0.f; d.l2q[k * n2 + l] = 0.f; }
@@ -3162,6 +3163,57 @@ __global__ void __launch_bounds__(1024) k_sh_levels_cl(Geo g, Opt o, int* state,
     atomicAdd(&d.gs->c_pairs, (unsigned long long)K * (unsigned long long)(K - 1) / 2);
   }
   cl.sync();  // no CTA leaves while another may still read its shared memory
+}
+
+// After an accepted request on the grid engine (facc[14], set by sh_commit_advance): the
+// touched servers re-merged into the three presorted orders (ahp_presort_update), one
+// cluster per order; k_presort_update_fin then forgets the touched servers.
+__global__ void __launch_bounds__(1024) k_presort_update_cl(Geo g, Opt o, int* state, ShardDev d) {
+  if (!d.facc[14]) return;
+  cgx::cluster_group cl = cgx::this_cluster();
+  ClSeg q;
+  q.r = (int)cl.block_rank();
+  q.C = (int)cl.num_blocks();
+  q.par = 0;
+  const int ci = blockIdx.x / q.C;
+  const int n2 = next_pow2(g.n);
+  __shared__ Scratch ls;
+  extern __shared__ unsigned sh_bits[];
+  {
+    const int* src = reinterpret_cast<const int*>(d.gs);
+    int* dst = reinterpret_cast<int*>(&ls);
+    for (int i = threadIdx.x; i < (int)(sizeof(Scratch) / 4); i += blockDim.x) dst[i] = src[i];
+  }
+  Ctx c;
+  sh_ctx(c, g, o, state, d);
+  c.s = &ls;
+  for (int w = c.tid; w < c.nW; w += c.B) sh_bits[w] = c.dirty[w];
+  __syncthreads();
+  unsigned short* perm = c.perm;
+  c.dirty = sh_bits;
+  int* sc = d.lvscr + (size_t)ci * 5 * (n2 + 1);
+  c.keys = reinterpret_cast<float*>(sc);
+  c.sidx = sc + (n2 + 1);
+  c.keys2 = reinterpret_cast<float*>(sc + 2 * (n2 + 1));
+  c.sidx2 = sc + 3 * (n2 + 1);
+  const int m = cl_collect<false>(c, q, cl, ci);  // ends with a cluster barrier: sidx complete
+  for (int i = q.r * c.B + c.tid; i < m; i += q.C * c.B) perm[ci * n2 + i] = (unsigned short)c.sidx[i];
+  cl.sync();  // no CTA leaves while another may still read its shared memory
+}
+__global__ void __launch_bounds__(256) k_presort_update_fin(Geo g, ShardDev d) {
+  if (!d.facc[14]) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {  // ahp_clear_dirty on the global scratch
+    Scratch* s = d.gs;
+    unsigned* dirty = reinterpret_cast<unsigned*>(d.ahp_ws + align16(6 * (size_t)next_pow2(g.n)));  // ahp_carve
+    const int nt = min(s->ntouched, 2 * MAXC);
+    for (int i = 0; i < nt; ++i) {
+      const int u = s->touched[i];
+      dirty[u >> 5] &= ~(1u << (u & 31));
+    }
+    s->ntouched = 0;
+    d.facc[14] = 0ull;
+  }
 }
 
 // TOPSIS: closeness of this rank's servers [lo, hi); top-2 keys into slot
@@ -3206,7 +3258,13 @@ __device__ void sh_commit_advance(Ctx& c, const ReqsDev& R, const OutDev& O, int
   }
   if (p + 1 == s->P) {
     req_finish(c, R, O, r, true);
-    if (METHOD == 0) ahp_presort_update(c);
+    if (METHOD == 0) {  // the presorted orders: k_presort_update_cl (after this kernel) on clusters
+      __syncthreads();
+      if (c.tid == 0) {
+        if (s->touch_over) s->presorted = 0;  // more than the merge list holds: sort again next request
+        else d.facc[14] = 1ull;
+      }
+    }
     sh_flush(c, d.stats);
     if (c.tid == 0) d.ctl[0] = PH_DONE;
   } else if (c.tid == 0) {
@@ -3720,6 +3778,13 @@ __global__ void __launch_bounds__(1024) k_ahp_decide(Geo g, Opt o, int* state, R
   sh_commit_advance<0>(c, R, O, r, d);
 }
 
+// CTAs per criterion of the sharded engine's AHP level extraction (1: k_sh_levels, one CTA)
+static int sh_levels_cluster() {
+  int C = 8;
+  if (const char* e = getenv("NACS_LEVELS_CLUSTER")) C = atoi(e);  // experiments: 1, 2, 4, 8, 16
+  return C < 1 || C > 16 ? 8 : C;
+}
+
 cudaError_t launch_ahp_pass(int pass, bool fp64, const Geo& g, const Opt& o, int* state, int q0, int q1, int world,
                             const ShardDev& d, int num_sms, cudaStream_t st) {
   (void)state;
@@ -3751,17 +3816,33 @@ cudaError_t launch_ahp_decide(bool fp64, const Geo& g, const Opt& o, int* state,
   if (!fp64) k_ahp_pg<<<d.npart, 1024, 0, st>>>(g, o, state, d);
   if (fp64) k_ahp_decide<true><<<1, 1024, 0, st>>>(g, o, state, R, O, r, d);
   else k_ahp_decide<false><<<1, 1024, 0, st>>>(g, o, state, R, O, r, d);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  // the request's last pod step: the presorted orders re-merged on clusters (no-ops otherwise)
+  const int CL = sh_levels_cluster();
+  if (CL > 8 && (e = cudaFuncSetAttribute(k_presort_update_cl, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) !=
+                    cudaSuccess)
+    return e;
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CL;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3(3 * CL, 1, 1);
+  cfg.blockDim = dim3(1024, 1, 1);
+  cfg.dynamicSmemBytes = sizeof(unsigned) * (size_t)((g.n + 31) / 32);
+  cfg.stream = st;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  if ((e = cudaLaunchKernelEx(&cfg, k_presort_update_cl, g, o, state, d)) != cudaSuccess) return e;
+  k_presort_update_fin<<<1, 256, 0, st>>>(g, d);
   return cudaGetLastError();
 }
 
 size_t scratch_bytes() { return sizeof(Scratch); }
 
-// CTAs per criterion of the sharded engine's AHP level extraction (1: k_sh_levels, one CTA)
-static int sh_levels_cluster() {
-  int C = 8;
-  if (const char* e = getenv("NACS_LEVELS_CLUSTER")) C = atoi(e);  // experiments: 1, 2, 4, 8, 16
-  return C < 1 || C > 16 ? 8 : C;
-}
+
 
 cudaError_t launch_sh_begin(const Geo& g, const Opt& o, int* state, const ReqsDev& R, const OutDev& O, int r,
                             const ShardDev& d, cudaStream_t st) {
