@@ -660,7 +660,7 @@ nacs_status schedule_sharded(nacs_ctx* ctx, const Opt& o, const nacs::ReqsDev& R
                b_f = ahp ? al(4 * 4 * n2) : 0, b_d = ahp ? al(4 * 8 * n2) : 0, b_K = ahp ? al(16) : 0;
   const int npart = std::max(1, std::min(256, (g.n + 1023) / 1024));
   const size_t b_facc = al(16 * 8), b_lsc = ahp ? al(4 * 5 * 4 * (n2 + 1)) : 0,
-               b_kp = ahp ? al(2 * 8 * (size_t)npart) : 0, b_mt = ahp ? al(4 * 32 * 2 * 8) : 0;
+               b_kp = ahp ? al(2 * 8 * (size_t)npart) : 0, b_mt = ahp ? al(4 * nacs::AHP_MID_WARPS * 2 * 8) : 0;
   CK(ctx->sh_buf.reserve(b_gs + 2 * b_bm + b_e + b_ctl + b_kx + b_kv + b_ki + b_facc + b_ws + 2 * b_lv + 2 * b_pp +
                          b_lvl + 2 * b_f + 2 * b_d + b_K + b_lsc + b_kp + b_mt));
   CK(ctx->sh_ctl.reserve(16));

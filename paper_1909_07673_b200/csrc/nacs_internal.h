@@ -102,6 +102,9 @@ __host__ __device__ inline int validate_request(int nC, int nV, const int* cpu_m
 
 // Device pointers of the server-sharded engine (nacs_kernels.cu, k_sh_*).
 struct Scratch;
+// warps per criterion of the grid engine's between-passes kernels (k_ahp_mid_a / _b)
+constexpr int AHP_MID_WARPS = 128;
+
 struct ShardDev {
   Scratch* gs;                 // per-request scratch (global memory)
   unsigned *maskw, *special, *edgebad;
@@ -123,7 +126,7 @@ struct ShardDev {
   int* lvscr;                  // AHP: per-criterion level-extraction scratch, 4 x [5 (n2 + 1)] ints
   unsigned long long* kpart;   // AHP: per-CTA top-2 keys of k_ahp_pg, [2 * npart]
   int npart;                   // CTAs of k_ahp_pg
-  double* midtot;              // AHP: [4][32][2] segment totals of the between-passes scans
+  double* midtot;              // AHP: [4][AHP_MID_WARPS][2] segment totals of the between-passes scans
 };
 
 // Launchers (nacs_kernels.cu).  Each returns the cudaError_t of the launch.

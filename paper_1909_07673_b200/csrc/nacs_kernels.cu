@@ -3622,7 +3622,8 @@ __global__ void __launch_bounds__(1024) k_ahp_mid(Geo g, Opt o, int* state, Shar
 // warp segments; these kernels run the same 32 segments, with the same loops, butterflies and
 // shuffle scans (bit-identical prefix sums), as 8 CTAs of 4 warps per criterion instead of 32
 // warps sharing one SM (ncu: the one-CTA version was issue-limited on that SM).
-constexpr int kMidWarps = 32;
+constexpr int kMidWarps = AHP_MID_WARPS;  // a multiple of 32
+constexpr int kMidPer = kMidWarps / 32;     // segment totals per lane in k_ahp_mid_b's scan
 __device__ __forceinline__ void mid_seg(int K, int w, int& s0, int& s1) {
   const int seg = ((K + kMidWarps - 1) / kMidWarps + 31) & ~31;
   s0 = min(w * seg, K);
@@ -3668,13 +3669,28 @@ __global__ void __launch_bounds__(128) k_ahp_mid_b(Geo g, ShardDev d) {
   const float2* lv = d.lvwC + (size_t)k * n2;
   double* pa = d.paC + (size_t)k * (n2 + 2);
   double* pb = d.pbC + (size_t)k * (n2 + 2);
-  const double xa = d.midtot[(k * kMidWarps + lane) * 2], xb = d.midtot[(k * kMidWarps + lane) * 2 + 1];
+  // lane L holds segments L*kMidPer ..: their exclusive prefixes within the lane, then a
+  // warp scan of the lane sums
+  double pa_l[kMidPer], pb_l[kMidPer], xa = 0.0, xb = 0.0;
+#pragma unroll
+  for (int j = 0; j < kMidPer; ++j) {
+    pa_l[j] = xa;
+    pb_l[j] = xb;
+    xa += d.midtot[(k * kMidWarps + lane * kMidPer + j) * 2];
+    xb += d.midtot[(k * kMidWarps + lane * kMidPer + j) * 2 + 1];
+  }
   double ia = xa, ib = xb;
   for (int o = 1; o < 32; o <<= 1) {
     const double ya = __shfl_up_sync(FULL, ia, o), yb = __shfl_up_sync(FULL, ib, o);
     if (lane >= o) { ia += ya; ib += yb; }
   }
-  double ra = __shfl_sync(FULL, ia - xa, w), rb = __shfl_sync(FULL, ib - xb, w);
+  double qa = pa_l[0], qb = pb_l[0];
+#pragma unroll
+  for (int j = 1; j < kMidPer; ++j)
+    if (j == w % kMidPer) { qa = pa_l[j]; qb = pb_l[j]; }
+  // segment w's exclusive prefix: its lane's exclusive prefix plus its offset in the lane
+  double ra = __shfl_sync(FULL, ia - xa, w / kMidPer) + __shfl_sync(FULL, qa, w / kMidPer);
+  double rb = __shfl_sync(FULL, ib - xb, w / kMidPer) + __shfl_sync(FULL, qb, w / kMidPer);
   const double TA = __shfl_sync(FULL, ia, 31), TB = __shfl_sync(FULL, ib, 31);
   int s0, s1;
   mid_seg(K, w, s0, s1);
@@ -3780,9 +3796,10 @@ __global__ void __launch_bounds__(1024) k_ahp_decide(Geo g, Opt o, int* state, R
 
 // CTAs per criterion of the sharded engine's AHP level extraction (1: k_sh_levels, one CTA)
 static int sh_levels_cluster() {
-  int C = 8;
+  // A/B at C5 (scripts/ab_c5_ahp.py, 12 requests): 1 -> 645, 4 -> 518, 8 -> 492, 16 -> 479 us per pod step
+  int C = 16;
   if (const char* e = getenv("NACS_LEVELS_CLUSTER")) C = atoi(e);  // experiments: 1, 2, 4, 8, 16
-  return C < 1 || C > 16 ? 8 : C;
+  return C < 1 || C > 16 ? 16 : C;
 }
 
 cudaError_t launch_ahp_pass(int pass, bool fp64, const Geo& g, const Opt& o, int* state, int q0, int q1, int world,
