@@ -3540,7 +3540,25 @@ __global__ void __launch_bounds__(NACS_AHP_BLOCK, NACS_AHP_MINB) k_ahp_pass_tile
       const int tmp = ord[y]; ord[y] = ord[y - 1]; ord[y - 1] = tmp;
     }
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
+#ifndef NACS_AHP_STATIC
+  // tiles handed out in order (largest K first) from a counter: the warps that drew short
+  // tiles take more, so the SMs run dry together; the last warp out resets the counters for
+  // the next launch (facc[12] tiles, facc[13] warps done)
+  unsigned long long* ctr = d.facc + 12;
+  for (;;) {
+    int i = 0;
+    if (lane == 0) i = (int)atomicAdd(ctr, 1ull);
+    i = __shfl_sync(FULL, i, 0);
+    if (i >= total) {
+      if (lane == 0 && atomicAdd(ctr + 1, 1ull) == (unsigned long long)(nwarps - 1)) {
+        ctr[0] = 0ull;
+        ctr[1] = 0ull;
+      }
+      break;
+    }
+#else
   for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < total; i += nwarps) {
+#endif
     int j = 0, t = i;
     while (t >= (b[ord[j]] - a[ord[j]] + P - 1) / P) { t -= (b[ord[j]] - a[ord[j]] + P - 1) / P; ++j; }
     const int k = ord[j];
