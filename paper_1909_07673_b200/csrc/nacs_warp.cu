@@ -35,6 +35,10 @@ constexpr int WDW = 40;   // dirty-row bitmap words: fabric rows E + k*h = k^2 <
 constexpr int WEW = 20;   // edge bitmap words: E = k^2/2 <= 640
 constexpr int WCH = 96;   // chunks of 128 slots: n <= 12288
 constexpr int WWARPS = 16; // warps per CTA (static per-warp scratch)
+#ifndef NACS_WARP_THREADS  // threads of k_batch_warp (<= 32 WWARPS); the register budget is 64K / this
+#define NACS_WARP_THREADS 512
+#endif
+static_assert(NACS_WARP_THREADS % 32 == 0 && NACS_WARP_THREADS <= 32 * WWARPS, "k_batch_warp threads");
 }  // namespace
 
 struct __align__(16) WScr {
@@ -1191,7 +1195,7 @@ __device__ __forceinline__ bool group_sync_and(int id, int nt, bool p) {
 // on its own request, so that all warps run the same loop at the same time (one copy of
 // the hot code in the instruction caches); within a phase no warp waits for another.
 template <typename LT, bool RO>  // RO: R25 rank-once instantiation
-__global__ void __launch_bounds__(512, 1) k_batch_warp(Geo g, Opt o, const int* __restrict__ state,
+__global__ void __launch_bounds__(NACS_WARP_THREADS, 1) k_batch_warp(Geo g, Opt o, const int* __restrict__ state,
                                                        const int* __restrict__ lay, ReqsDev R, OutDev O,
                                                        int4* ulog_all, int* next, const int* order, int* deferred,
                                                        int* n_deferred, unsigned long long* stats, int group,
@@ -1614,7 +1618,7 @@ int warp_kernel_warps(const Geo& g) {
   const size_t stat = sizeof(WScr) * WWARPS + 64;
   if (warp_snapshot_bytes(g, u16) + stat > (size_t)optin || ((g.n + 127) >> 7) > WCH) return 0;
   if (g.E > 32 * WEW || g.E + g.k * g.h > 32 * WDW || g.k > 64) return 0;
-  return WWARPS;
+  return NACS_WARP_THREADS / 32;
 }
 
 size_t warp_ulog_entries(int grid, int warps) { return (size_t)grid * warps * WLOG; }
