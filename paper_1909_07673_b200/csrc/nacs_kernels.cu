@@ -29,6 +29,24 @@
 
 #include "nacs_device.cuh"
 
+// Debug builds (-DNACS_CHECKS): bounds checks of the cluster engines' index arithmetic trap
+// with a message (python paper_1909_07673_b200/build.py exp_checks.so -DNACS_CHECKS, then
+// NACS_LIB=... on the GPU tests).
+#ifdef NACS_CHECKS
+#define NACS_DCHECK(cond)                                                                   \
+  do {                                                                                     \
+    if (!(cond)) {                                                                         \
+      printf("NACS_CHECK failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__, __LINE__, \
+             (int)blockIdx.x, (int)threadIdx.x);                                           \
+      __trap();                                                                            \
+    }                                                                                      \
+  } while (0)
+#else
+#define NACS_DCHECK(cond) \
+  do {                    \
+  } while (0)
+#endif
+
 namespace nacs {
 
 #define FULL 0xffffffffu
@@ -185,6 +203,7 @@ __device__ __forceinline__ int* mirror_ptr(const Ctx& c, int off) {
   const int q = (off >= n) + (off >= 2 * n) + (off >= 3 * n);
   const int u = off - q * n;
   const int C = (int)gridDim.x;
+  NACS_DCHECK(off >= 0 && q < 4 && u >= 0 && u < n && (C & (C - 1)) == 0 && (u >> (__ffs(C * SQC_T) - 1)) < SQ_J);
   return c.mirr[(u / SQC_T) & (C - 1)] + q * SQC_M + ((u >> (__ffs(C * SQC_T) - 1)) * SQC_T) + (u & (SQC_T - 1));
 }
 __device__ __forceinline__ void mirror_put(const Ctx& c, int off, int val) { *mirror_ptr(c, off) = val; }
@@ -2108,6 +2127,7 @@ __global__ void __launch_bounds__(SQC_T, 1) k_seq_cluster(Geo g, Opt o, int* sta
   c.spok = reinterpret_cast<unsigned*>(dyn + off);
   off = align16(off + sizeof(unsigned) * c.nW);
   int* mir = reinterpret_cast<int*>(dyn + off);  // [4][SQC_M] this CTA's rows
+  NACS_DCHECK(C * SQC_M >= g.n && (int)blockDim.x == SQC_T);
   __shared__ int* mirr[16];
   if (c.tid < C) mirr[c.tid] = cl.map_shared_rank(mir, c.tid);
   c.mirr = mirr;
@@ -2724,6 +2744,7 @@ __global__ void __launch_bounds__(256) k_presort_merge(Geo g, ShardDev d, int fi
       }
       pos += lo;
     }
+    NACS_DCHECK(pos >= 0 && pos < n);
     perm[ci * P2 + pos] = (unsigned short)u;
   }
 }
@@ -2968,6 +2989,7 @@ __device__ int cl_collect(Ctx& c, ClSeg& q, cgx::cluster_group& cl, int ci) {
     const unsigned bal = __ballot_sync(FULL, k);
     if (k) {
       const int qq = pos + __popc(bal & ((1u << c.lane) - 1u));
+      NACS_DCHECK(qq >= 0 && qq < n);
       c.keys2[qq] = (float)x[u];
       c.sidx2[qq] = u;
     }
@@ -2995,6 +3017,7 @@ __device__ int cl_collect(Ctx& c, ClSeg& q, cgx::cluster_group& cl, int ci) {
     const float v = c.keys2[i];
     int lo = 0, hi = d;
     while (lo < hi) { int mid = (lo + hi) >> 1; if (s->dval[mid] < v) lo = mid + 1; else hi = mid; }
+    NACS_DCHECK(i + lo < n);
     c.keys[i + lo] = v;
     c.sidx[i + lo] = c.sidx2[i];
   }
@@ -3029,6 +3052,7 @@ __device__ int cl_levels_sorted(Ctx& c, ClSeg& q, cgx::cluster_group& cl, int m)
     const bool f = in && (i == 0 || c.keys[i] != c.keys[i - 1]);
     const unsigned bal = __ballot_sync(FULL, f);
     const int qq = l0 + __popc(bal & (0xffffffffu >> (31 - c.lane))) - 1;
+    NACS_DCHECK(!in || (qq >= 0 && qq < m && c.sidx[i] >= 0 && c.sidx[i] < c.g.n));
     if (f) {
       c.lvm[qq].x = c.keys[i];
       c.lst[qq] = i;
