@@ -3475,6 +3475,34 @@ __device__ __forceinline__ void rsum_tile(const float2* arr, int K, int l0, int 
     float a[P];
 #pragma unroll
     for (int p = 0; p < P; ++p) a[p] = 0.f;
+    // a block of 8 chunks all inside every level's range: the same terms in the same order
+    // without the per-chunk range tests (they were ~20% of the executed instructions)
+    const bool block_full = ABOVE ? (kb > lmax && kb + 1024 <= K) : (kb + 1024 <= l0);
+    if (block_full) {
+      const float2* ap = arr + kb + lane;
+#pragma unroll
+      for (int j = 0; j < 8; ++j, ap += 128) {
+        const float2 o0 = ap[0], o1 = ap[32], o2 = ap[64], o3 = ap[96];
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+          float d0 = ABOVE ? o0.x - v[p] : v[p] - o0.x, d1 = ABOVE ? o1.x - v[p] : v[p] - o1.x;
+          float d2 = ABOVE ? o2.x - v[p] : v[p] - o2.x, d3 = ABOVE ? o3.x - v[p] : v[p] - o3.x;
+          if (RULE) {
+            d0 = fmaf(sc, d0, 1.0f);
+            d1 = fmaf(sc, d1, 1.0f);
+            d2 = fmaf(sc, d2, 1.0f);
+            d3 = fmaf(sc, d3, 1.0f);
+          }
+          const float p01 = d0 * d1, p23 = d2 * d3;
+          const float n01 = fmaf(o0.y, d1, o1.y * d0), n23 = fmaf(o2.y, d3, o3.y * d2);
+          a[p] = fmaf(fmaf(n01, p23, n23 * p01), rcp_approx(p01 * p23), a[p]);
+        }
+      }
+      kb += 1024;
+#pragma unroll
+      for (int p = 0; p < P; ++p) out[p] += (double)a[p];
+      continue;
+    }
     for (int j = 0; j < 8 && kb < kend; ++j, kb += 128) {
       const int k = kb + lane;
       const bool full = ABOVE ? (kb > lmax && kb + 128 <= K) : (kb + 128 <= l0);

@@ -18,10 +18,14 @@ for it in range(3):
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    ctx.schedule_request(reqs, "ahp", "flat")
+    out = ctx.schedule_request(reqs, "ahp", "flat")
     e1.record()
     torch.cuda.synchronize()
     ts.append(e0.elapsed_time(e1))
 st = ctx.last_stats()
+import hashlib  # noqa: E402
+import numpy as np  # noqa: E402
+hsh = hashlib.sha256(b"".join(np.ascontiguousarray(np.asarray(out[k].cpu() if hasattr(out[k], "cpu") else out[k])).tobytes()
+                              for k in sorted(out))).hexdigest()[:16]
 print(f"LEVELS_CLUSTER={os.environ.get('NACS_LEVELS_CLUSTER', 'default')} ms={min(ts):.2f} "
-      f"us/pod_step={1e3 * min(ts) / st['pod_steps']:.1f} pods/s={st['pod_steps'] / min(ts) * 1e3:.0f}")
+      f"us/pod_step={1e3 * min(ts) / st['pod_steps']:.1f} pods/s={st['pod_steps'] / min(ts) * 1e3:.0f} placements {hsh}")
