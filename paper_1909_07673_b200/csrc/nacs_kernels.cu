@@ -3578,19 +3578,29 @@ __global__ void __launch_bounds__(NACS_AHP_BLOCK, NACS_AHP_MINB) k_ahp_pass_tile
   // ranks split whole tiles: tile starts are multiples of P for every world size, so the
   // FP32 chunking of each level's terms (rsum_tile, from l0) never depends on the split and
   // every rank count gives bit-identical weights and L2
-  int a[4], b[4], total = 0;
-  for (int k = 0; k < 4; ++k) {
-    const int K = d.Kc[k], half = (K + 1) >> 1, ntile = (half + P - 1) / P;
-    a[k] = min(half, P * (int)((long long)ntile * q0 / world));
-    b[k] = min(half, P * (int)((long long)ntile * q1 / world));
-    total += (b[k] - a[k] + P - 1) / P;
-  }
-  // criteria in decreasing K (a tile costs ~P (K-1) terms): the longest tiles start first
-  int ord[4] = {0, 1, 2, 3};
-  for (int x = 1; x < 4; ++x)
-    for (int y = x; y > 0 && d.Kc[ord[y]] > d.Kc[ord[y - 1]]; --y) {
-      const int tmp = ord[y]; ord[y] = ord[y - 1]; ord[y - 1] = tmp;
+  // the split and the criteria order once per CTA (thread 0: 64-bit divisions), then shared
+  __shared__ int s_ab[2][4], s_ord[4], s_total;
+  if (threadIdx.x == 0) {
+    int total = 0;
+    for (int k = 0; k < 4; ++k) {
+      const int K = d.Kc[k], half = (K + 1) >> 1, ntile = (half + P - 1) / P;
+      s_ab[0][k] = min(half, P * (int)((long long)ntile * q0 / world));
+      s_ab[1][k] = min(half, P * (int)((long long)ntile * q1 / world));
+      total += (s_ab[1][k] - s_ab[0][k] + P - 1) / P;
     }
+    // criteria in decreasing K (a tile costs ~P (K-1) terms): the longest tiles start first
+    int ord[4] = {0, 1, 2, 3};
+    for (int x = 1; x < 4; ++x)
+      for (int y = x; y > 0 && d.Kc[ord[y]] > d.Kc[ord[y - 1]]; --y) {
+        const int tmp = ord[y]; ord[y] = ord[y - 1]; ord[y - 1] = tmp;
+      }
+    for (int k = 0; k < 4; ++k) s_ord[k] = ord[k];
+    s_total = total;
+  }
+  __syncthreads();
+  int a[4], b[4], ord[4];
+  for (int k = 0; k < 4; ++k) { a[k] = s_ab[0][k]; b[k] = s_ab[1][k]; ord[k] = s_ord[k]; }
+  const int total = s_total;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
 #ifndef NACS_AHP_STATIC
   // tiles handed out in order (largest K first) from a counter: the warps that drew short

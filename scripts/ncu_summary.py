@@ -33,6 +33,8 @@ iw, ie = h.index('Warp Stall Sampling (All Samples)'), h.index('Instructions Exe
 stalls = [c for c in h if c.startswith('stall_') and 'Not Issued' not in c]
 data = []
 for row in rows[2:]:
+    if row and row[0] == "Kernel Name":  # a report with several kernels: the first one
+        break
     if len(row) < len(h):
         continue
     data.append((row[isrc].strip(), float(row[iw] or 0), float(row[ie] or 0),
