@@ -3556,8 +3556,8 @@ __device__ __forceinline__ void rsum_tile(const float2* arr, int K, int l0, int 
 #ifndef NACS_AHP_TILE
 #define NACS_AHP_TILE 4
 #endif
-#ifndef NACS_AHP_MINB
-#define NACS_AHP_MINB 8
+#ifndef NACS_AHP_MINB  // CTAs per SM (the register budget): A/B at C5 (scripts/ab_c5_ahp.py,
+#define NACS_AHP_MINB 5  // 128-thread CTAs): 4 -> 393.5, 5 -> 390.5, 6 -> 402, 7 -> 401, 8 -> 406 us per pod step
 #endif
 #ifndef NACS_AHP_BLOCK
 #define NACS_AHP_BLOCK 128
@@ -3887,7 +3887,10 @@ cudaError_t launch_ahp_pass(int pass, bool fp64, const Geo& g, const Opt& o, int
   (void)state;
   const int blocks = num_sms * 8;
   if (!fp64) {
-    const int tb = blocks * 256 / NACS_AHP_BLOCK;
+    // one resident wave of CTAs, the tiles from the counter (A/B: 387.3 vs 390.6 us per C5
+    // pod step with 2368 CTAs)
+    const int tb = num_sms * NACS_AHP_MINB;
+    (void)blocks;
     if (pass == 1 && o.ahp_rule) k_ahp_pass_tiled<1, 1><<<tb, NACS_AHP_BLOCK, 0, st>>>(g, q0, q1, world, d);
     else if (pass == 1) k_ahp_pass_tiled<1, 0><<<tb, NACS_AHP_BLOCK, 0, st>>>(g, q0, q1, world, d);
     else if (o.ahp_rule) k_ahp_pass_tiled<2, 1><<<tb, NACS_AHP_BLOCK, 0, st>>>(g, q0, q1, world, d);
