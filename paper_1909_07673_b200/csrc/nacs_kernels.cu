@@ -2995,20 +2995,38 @@ __device__ int cl_collect(Ctx& c, ClSeg& q, cgx::cluster_group& cl, int ci) {
     }
     pos += __popc(bal);
   }
-  if (c.tid == 0) {  // touched (feasible) servers, insertion-sorted by current value (every CTA)
-    int d = 0;
+  if (c.warp == 0) {  // touched (feasible) servers sorted by current value, ties in touch order
+    // (the insertion sort of presorted_collect): warp 0 loads them at once, keeps the feasible
+    // ones in order, and places each at its rank (every CTA)
+    __shared__ float tv[2 * MAXC];
+    __shared__ int tu[2 * MAXC];
     const int nt = min(s->ntouched, 2 * MAXC);
-    for (int t = 0; t < nt; ++t) {
-      const int u = s->touched[t];
-      if (FEAS && !feas_bit(c, u)) continue;
-      const float v = (float)x[u];
-      int j = d;
-      while (j > 0 && s->dval[j - 1] > v) { s->dval[j] = s->dval[j - 1]; s->dsrv[j] = s->dsrv[j - 1]; --j; }
-      s->dval[j] = v;
-      s->dsrv[j] = u;
-      ++d;
+    int d = 0;
+    for (int t0 = 0; t0 < nt; t0 += 32) {
+      const int t = t0 + c.lane;
+      const int u = t < nt ? s->touched[t] : 0;
+      const bool keep = t < nt && (!FEAS || feas_bit(c, u));
+      const float v = keep ? (float)x[u] : 0.f;
+      const unsigned bal = __ballot_sync(FULL, keep);
+      if (keep) {
+        const int at = d + __popc(bal & ((1u << c.lane) - 1u));
+        tv[at] = v;
+        tu[at] = u;
+      }
+      d += __popc(bal);
     }
-    s->nd = d;
+    __syncwarp();
+    for (int t = c.lane; t < d; t += 32) {
+      const float v = tv[t];
+      int r = 0;
+      for (int j = 0; j < d; ++j) {
+        const float w = tv[j];
+        r += (w < v) || (w == v && j < t);
+      }
+      s->dval[r] = v;
+      s->dsrv[r] = tu[t];
+    }
+    if (c.lane == 0) s->nd = d;
   }
   cl.sync();  // keys2 / sidx2 complete; nd in every CTA
   const int m1 = mtot, d = s->nd;
