@@ -3809,6 +3809,68 @@ __global__ void __launch_bounds__(128) k_ahp_mid_b(Geo g, ShardDev d) {
   if (w == 0 && lane == 0) { pa[K] = TA; pb[K] = TB; }
 }
 
+// k_ahp_mid_a + _b in one launch: a thread-block cluster per criterion (criterion = cluster
+// id), the segment totals scanned over DSMEM (cl_exscan_d2) instead of through global memory
+// between two kernels.  Same (value, weight) levels; the FP64 prefix sums in another order
+// (segments of the cluster's warps).
+__global__ void __launch_bounds__(1024) k_ahp_mid_cl(Geo g, ShardDev d) {
+  if (!sh_live(d, false)) return;
+  cgx::cluster_group cl = cgx::this_cluster();
+  ClSeg q;
+  q.r = (int)cl.block_rank();
+  q.C = (int)cl.num_blocks();
+  q.par = 0;
+  const int k = blockIdx.x / q.C, K = d.Kc[k];
+  if (K == 0) return;  // the same in every CTA of the cluster
+  __shared__ Scratch ls;
+  Ctx c;
+  c.s = &ls;
+  c.tid = threadIdx.x;
+  c.B = blockDim.x;
+  c.NW = blockDim.x >> 5;
+  c.lane = threadIdx.x & 31;
+  c.warp = threadIdx.x >> 5;
+  const int n2 = next_pow2(g.n);
+  const float2* lvm = d.lvmC + (size_t)k * n2;
+  float2* lvw = d.lvwC + (size_t)k * n2;
+  const float* wq = d.wq + (size_t)k * n2;
+  double* pa = d.paC + (size_t)k * (n2 + 2);
+  double* pb = d.pbC + (size_t)k * (n2 + 2);
+  int s0, s1;
+  cl_seg(c, q, K, s0, s1);
+  double ta = 0, tb = 0;
+  for (int base = s0; base < s1; base += 32) {
+    const int i = base + c.lane;
+    if (i < s1) {
+      const float2 e = make_float2(lvm[i].x, wq[i]);
+      lvw[i] = e;
+      ta += (double)e.y;
+      tb += (double)e.y * (double)e.x;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) { ta += __shfl_xor_sync(FULL, ta, o); tb += __shfl_xor_sync(FULL, tb, o); }
+  double TA, TB;
+  cl_exscan_d2(c, q, cl, ta, tb, &TA, &TB);  // ta, tb: this segment's exclusive prefix
+  double ra = ta, rb = tb;
+  for (int base = s0; base < s1; base += 32) {
+    const int i = base + c.lane;
+    double a = 0, b = 0;
+    if (i < s1) { const float2 e = lvw[i]; a = (double)e.y; b = (double)e.y * (double)e.x; }
+    double ja = a, jb = b;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double ya = __shfl_up_sync(FULL, ja, o), yb = __shfl_up_sync(FULL, jb, o);
+      if (c.lane >= o) { ja += ya; jb += yb; }
+    }
+    if (i < s1) { pa[i] = ra + (ja - a); pb[i] = rb + (jb - b); }
+    ra += __shfl_sync(FULL, ja, 31);
+    rb += __shfl_sync(FULL, jb, 31);
+  }
+  if (q.r == 0 && c.tid == 0) { pa[K] = TA; pb[K] = TB; }
+  cl.sync();  // no CTA leaves while another may still read its shared memory
+}
+
 // PG over F on the whole grid (FP32; one server per thread): each CTA leaves its top-2
 // (score, index) keys in d.kpart for k_ahp_decide.  The top-2 of the union of per-CTA top-2
 // sets is the global top-2, so the decision is the one-CTA kernel's.
@@ -3900,6 +3962,14 @@ static int sh_levels_cluster() {
   return C < 1 || C > 16 ? 16 : C;
 }
 
+// CTAs per criterion of the between-passes kernel (1: k_ahp_mid_a / _b over 128 warps)
+// (A/B at C5, 3 runs each: 1 -> 386.6, 16 -> 382.7 us per pod step, identical placements)
+static int mid_cluster() {
+  int C = 16;
+  if (const char* e = getenv("NACS_MID_CLUSTER")) C = atoi(e);  // experiments: 1, 2, 4, 8, 16
+  return C < 1 || C > 16 ? 16 : C;
+}
+
 cudaError_t launch_ahp_pass(int pass, bool fp64, const Geo& g, const Opt& o, int* state, int q0, int q1, int world,
                             const ShardDev& d, int num_sms, cudaStream_t st) {
   (void)state;
@@ -3924,8 +3994,29 @@ cudaError_t launch_ahp_mid(bool fp64, const Geo& g, const Opt& o, int* state, co
   if (fp64) {
     k_ahp_mid<true><<<4, 1024, 0, st>>>(g, o, state, d);
   } else {
-    k_ahp_mid_a<<<dim3(kMidWarps / 4, 4), 128, 0, st>>>(g, d);
-    k_ahp_mid_b<<<dim3(kMidWarps / 4, 4), 128, 0, st>>>(g, d);
+    const int CL = mid_cluster();
+    if (CL <= 1) {
+      k_ahp_mid_a<<<dim3(kMidWarps / 4, 4), 128, 0, st>>>(g, d);
+      k_ahp_mid_b<<<dim3(kMidWarps / 4, 4), 128, 0, st>>>(g, d);
+    } else {
+      cudaError_t e;
+      if (CL > 8 && (e = cudaFuncSetAttribute(k_ahp_mid_cl, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) !=
+                        cudaSuccess)
+        return e;
+      cudaLaunchConfig_t cfg = {};
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = CL;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.gridDim = dim3(4 * CL, 1, 1);
+      cfg.blockDim = dim3(1024, 1, 1);
+      cfg.dynamicSmemBytes = 0;
+      cfg.stream = st;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      if ((e = cudaLaunchKernelEx(&cfg, k_ahp_mid_cl, g, d)) != cudaSuccess) return e;
+    }
   }
   return cudaGetLastError();
 }
