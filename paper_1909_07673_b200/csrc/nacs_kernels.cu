@@ -2774,6 +2774,32 @@ __global__ void __launch_bounds__(1024) k_sh_filter(Geo g, Opt o, int* state, Sh
   pass_filter<false, true>(c, nullptr, nullptr, d.facc);
 }
 
+// The grid filter's statistics (k_sh_filter, in facc) into the scratch fields, and for AHP
+// each criterion's scale 9 / (max - min) (one thread).  count: the call's counters too.
+__device__ void sh_prep_fields(Scratch* s, const unsigned long long* f, bool ahp, bool count) {
+  const int nf = (int)f[0], nact = (int)f[1];
+  s->nf = nf;
+  s->nact = nact;
+  s->mn[0] = (int)f[2]; s->mx[0] = (int)f[3];
+  s->mn[1] = (int)f[4]; s->mx[1] = (int)f[5];
+  s->mn[2] = nact == nf ? 1 : 0; s->mx[2] = nact > 0 ? 1 : 0;  // f_u in {0,1}
+  s->mn[3] = (int)f[6]; s->mx[3] = (int)f[7];
+  s->sq[0] = f[8]; s->sq[1] = f[9]; s->sq[2] = (unsigned long long)nact; s->sq[3] = f[10];
+  if (count) {
+    s->c_feas += (unsigned long long)nf;
+    s->c_steps += 1;
+  }
+  if (ahp && nf > 0) {  // levels and pass-1 prefix sums of every non-constant criterion
+    for (int k = 0; k < 4; ++k) {
+      const int lo = s->mn[k], hi = s->mx[k];
+      s->ahp_const[k] = hi == lo;
+      const double sc = hi > lo ? 9.0 / (double)(hi - lo) : 0.0;
+      s->ahp_scaled[k] = sc;
+      s->ahp_scale[k] = (float)sc;
+    }
+  }
+}
+
 template <int METHOD>
 __global__ void __launch_bounds__(1024) k_sh_prep(Geo g, Opt o, int* state, ReqsDev R, OutDev O, int r,
                                                   ShardDev d) {
@@ -2782,37 +2808,13 @@ __global__ void __launch_bounds__(1024) k_sh_prep(Geo g, Opt o, int* state, Reqs
   Ctx c;
   sh_ctx(c, g, o, state, d);
   Scratch* s = c.s;
-  if (c.tid == 0) {  // the grid filter's statistics (k_sh_filter) into the scratch fields
-    const unsigned long long* f = d.facc;
-    const int nf = (int)f[0], nact = (int)f[1];
-    s->nf = nf;
-    s->nact = nact;
-    s->mn[0] = (int)f[2]; s->mx[0] = (int)f[3];
-    s->mn[1] = (int)f[4]; s->mx[1] = (int)f[5];
-    s->mn[2] = nact == nf ? 1 : 0; s->mx[2] = nact > 0 ? 1 : 0;  // f_u in {0,1}
-    s->mn[3] = (int)f[6]; s->mx[3] = (int)f[7];
-    s->sq[0] = f[8]; s->sq[1] = f[9]; s->sq[2] = (unsigned long long)nact; s->sq[3] = f[10];
-    s->c_feas += (unsigned long long)nf;
-    s->c_steps += 1;
-  }
+  if (c.tid == 0) sh_prep_fields(s, d.facc, METHOD == 0, true);
   __syncthreads();
   if (s->nf == 0) {
     req_reject(c, R, O, r);
     sh_flush(c, d.stats);
     if (c.tid == 0) d.ctl[0] = PH_DONE;
     return;
-  }
-  if (METHOD == 0) {  // levels and pass-1 prefix sums of every non-constant criterion
-    if (c.tid == 0) {
-      for (int k = 0; k < 4; ++k) {
-        const int lo = s->mn[k], hi = s->mx[k];
-        s->ahp_const[k] = hi == lo;
-        const double sc = hi > lo ? 9.0 / (double)(hi - lo) : 0.0;
-        s->ahp_scaled[k] = sc;
-        s->ahp_scale[k] = (float)sc;
-      }
-    }
-    __syncthreads();
   }
 }
 
@@ -3135,7 +3137,8 @@ __device__ void cl_prefix(Ctx& c, ClSeg& q, cgx::cluster_group& cl, int K, const
 }
 
 // k_sh_levels on a cluster per criterion: grid = 4 clusters of C CTAs (criterion = cluster id)
-__global__ void __launch_bounds__(1024) k_sh_levels_cl(Geo g, Opt o, int* state, ShardDev d) {
+__global__ void __launch_bounds__(1024) k_sh_levels_cl(Geo g, Opt o, int* state, ReqsDev R, OutDev O, int r,
+                                                      ShardDev d) {
   const int phase = d.ctl[0];
   if (phase != PH_NEWPOD && phase != PH_RETRY) return;
   cgx::cluster_group cl = cgx::this_cluster();
@@ -3144,8 +3147,21 @@ __global__ void __launch_bounds__(1024) k_sh_levels_cl(Geo g, Opt o, int* state,
   q.C = (int)cl.num_blocks();
   q.par = 0;
   const int k = blockIdx.x / q.C;
-  const Scratch* gs = d.gs;
-  if (gs->nf == 0) return;  // rejected in k_sh_prep (the same in every CTA)
+  Scratch* gs = d.gs;
+  const int nf = (int)d.facc[0];
+  if (blockIdx.x == 0) {  // k_sh_prep's work in CTA 0: the scratch fields, an empty F rejected (R20)
+    Ctx c0;
+    sh_ctx(c0, g, o, state, d);
+    if (threadIdx.x == 0) sh_prep_fields(gs, d.facc, true, true);
+    __syncthreads();
+    if (nf == 0) {
+      req_reject(c0, R, O, r);
+      sh_flush(c0, d.stats);
+      if (threadIdx.x == 0) d.ctl[0] = PH_DONE;
+      return;
+    }
+  }
+  if (nf == 0) return;  // the same in every CTA
   const int n2 = next_pow2(g.n);
   if (gs->touch_over) {  // the presorted orders are rebuilt: k_sh_levels' one-CTA path, CTA 0
     if (blockIdx.x != 0) return;
@@ -3168,16 +3184,20 @@ __global__ void __launch_bounds__(1024) k_sh_levels_cl(Geo g, Opt o, int* state,
     }
     return;
   }
-  if (gs->ahp_const[k]) {
-    if (q.r == 0 && threadIdx.x == 0) d.Kc[k] = 0;
-    return;
-  }
   __shared__ Scratch ls;
   extern __shared__ unsigned sh_bits[];
-  {
+  {  // (CTA 0 may be writing the statistics fields of gs: every CTA sets its own from facc)
     const int* src = reinterpret_cast<const int*>(gs);
     int* dst = reinterpret_cast<int*>(&ls);
     for (int i = threadIdx.x; i < (int)(sizeof(Scratch) / 4); i += blockDim.x) dst[i] = src[i];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) sh_prep_fields(&ls, d.facc, true, false);
+  __syncthreads();
+  if (ls.ahp_const[k]) {
+    if (q.r == 0 && threadIdx.x == 0) d.Kc[k] = 0;
+    cl.sync();  // (a cluster's CTAs leave together: the others may still be in their scans)
+    return;
   }
   Ctx c;
   sh_ctx(c, g, o, state, d);
@@ -4082,9 +4102,9 @@ cudaError_t launch_sh_prep(const Geo& g, const Opt& o, int* state, const ReqsDev
   if (o.method == 1) {
     k_sh_prep<1><<<1, 1024, 0, st>>>(g, o, state, R, O, r, d);
   } else {
-    k_sh_prep<0><<<1, 1024, 0, st>>>(g, o, state, R, O, r, d);
     const int CL = sh_levels_cluster();
     if (CL <= 1) {
+      k_sh_prep<0><<<1, 1024, 0, st>>>(g, o, state, R, O, r, d);
       k_sh_levels<<<4, 1024, bits, st>>>(g, o, state, d);  // one CTA per criterion
     } else {  // a cluster of CL CTAs per criterion
       if (CL > 8) {
@@ -4103,7 +4123,8 @@ cudaError_t launch_sh_prep(const Geo& g, const Opt& o, int* state, const ReqsDev
       cfg.stream = st;
       cfg.attrs = at;
       cfg.numAttrs = 1;
-      cudaError_t e = cudaLaunchKernelEx(&cfg, k_sh_levels_cl, g, o, state, d);
+      // (k_sh_prep's work runs in the cluster kernel's CTA 0)
+      cudaError_t e = cudaLaunchKernelEx(&cfg, k_sh_levels_cl, g, o, state, R, O, r, d);
       if (e != cudaSuccess) return e;
     }
   }
