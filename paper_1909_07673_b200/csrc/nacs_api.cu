@@ -721,7 +721,10 @@ nacs_status schedule_sharded(nacs_ctx* ctx, const Opt& o, const nacs::ReqsDev& R
       const int phase = ctl[0];
       if (dbg) fprintf(stderr, "[shard] r=%d it=%ld phase=%d pod=%d best=%d fail=%d\n", r, it, phase, ctl[1], ctl[2],
                        ctl[3]);
-      if (phase == 0) break;  // PH_DONE
+      if (phase == 0) {  // PH_DONE (AHP: an accepted request's touched servers into the presorted orders)
+        if (ahp) CK(nacs::launch_presort_update(g, o, ctx->state.p, d, ctx->stream));
+        break;
+      }
       if (it > 4L * (g.n + 1) * (nacs::MAXC + 1))
         return fail(ctx, NACS_ECUDA, "sharded engine: pod loop did not finish (phase " + std::to_string(phase) + ")");
       if (ahp) {  // AHP: passes over this process's share of level pairs, sum-allreduce between

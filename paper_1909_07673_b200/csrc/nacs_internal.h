@@ -212,6 +212,7 @@ cudaError_t launch_ahp_pass(int pass, bool fp64, const Geo& g, const Opt& o, int
 cudaError_t launch_ahp_mid(bool fp64, const Geo& g, const Opt& o, int* state, const ShardDev& d, cudaStream_t st);
 cudaError_t launch_ahp_decide(bool fp64, const Geo& g, const Opt& o, int* state, const ReqsDev& R, const OutDev& O,
                               int r, const ShardDev& d, cudaStream_t st);
+cudaError_t launch_presort_update(const Geo& g, const Opt& o, int* state, const ShardDev& d, cudaStream_t st);
 
 // departures (nacs_release, nacs_simulate): idx = null releases every request of R with
 // status 1, else the requests idx[0 .. n_idx); delta: g.words() int64 scratch; bad: 1 int

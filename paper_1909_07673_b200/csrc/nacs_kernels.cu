@@ -4045,9 +4045,12 @@ cudaError_t launch_ahp_decide(bool fp64, const Geo& g, const Opt& o, int* state,
   if (!fp64) k_ahp_pg<<<d.npart, 1024, 0, st>>>(g, o, state, d);
   if (fp64) k_ahp_decide<true><<<1, 1024, 0, st>>>(g, o, state, R, O, r, d);
   else k_ahp_decide<false><<<1, 1024, 0, st>>>(g, o, state, R, O, r, d);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
-  // the request's last pod step: the presorted orders re-merged on clusters (no-ops otherwise)
+  return cudaGetLastError();
+}
+// After a request's last pod step (the host saw PH_DONE): the presorted orders re-merged on
+// clusters (no-ops unless facc[14] was set by an accepted request's commit)
+cudaError_t launch_presort_update(const Geo& g, const Opt& o, int* state, const ShardDev& d, cudaStream_t st) {
+  cudaError_t e;
   const int CL = sh_levels_cluster();
   if (CL > 8 && (e = cudaFuncSetAttribute(k_presort_update_cl, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) !=
                     cudaSuccess)
