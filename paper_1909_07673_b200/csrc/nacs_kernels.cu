@@ -3894,7 +3894,11 @@ __global__ void __launch_bounds__(1024) k_ahp_mid_cl(Geo g, ShardDev d) {
 // PG over F on the whole grid (FP32; one server per thread): each CTA leaves its top-2
 // (score, index) keys in d.kpart for k_ahp_decide.  The top-2 of the union of per-CTA top-2
 // sets is the global top-2, so the decision is the one-CTA kernel's.
-__global__ void __launch_bounds__(1024) k_ahp_pg(Geo g, Opt o, int* state, ShardDev d) {
+template <bool FP64>
+__device__ void ahp_decide_cta(const Geo& g, const Opt& o, int* state, const ReqsDev& R, const OutDev& O, int r,
+                               const ShardDev& d);
+__global__ void __launch_bounds__(1024) k_ahp_pg(Geo g, Opt o, int* state, ReqsDev R, OutDev O, int r,
+                                                 ShardDev d) {
   if (!sh_live(d, false)) return;
   __shared__ Scratch ls;
   Ctx c;
@@ -3917,17 +3921,25 @@ __global__ void __launch_bounds__(1024) k_ahp_pg(Geo g, Opt o, int* state, Shard
     top2_insert(k1, k2, score_key(pgv, u));
   }
   block_top2(c, k1, k2);
+  // the last CTA to finish takes the decision (k_ahp_decide's FP32 path) in the same launch
+  __shared__ bool last;
   if (c.tid == 0) {
     d.kpart[2 * blockIdx.x] = ls.key1;
     d.kpart[2 * blockIdx.x + 1] = ls.key2;
+    __threadfence();
+    last = atomicAdd(d.facc + 11, 1ull) == (unsigned long long)(gridDim.x - 1);
   }
+  __syncthreads();
+  if (!last) return;
+  if (c.tid == 0) d.facc[11] = 0ull;  // for the next pod step
+  __threadfence();
+  ahp_decide_cta<false>(g, o, state, R, O, r, d);
 }
 
 // decide (1 CTA): PG over F, argmax (top-2 and near-tie test in FP32), commit
 template <bool FP64>
-__global__ void __launch_bounds__(1024) k_ahp_decide(Geo g, Opt o, int* state, ReqsDev R, OutDev O, int r,
-                                                     ShardDev d) {
-  if (!sh_live(d, FP64)) return;
+__device__ void ahp_decide_cta(const Geo& g, const Opt& o, int* state, const ReqsDev& R, const OutDev& O, int r,
+                               const ShardDev& d) {
   Ctx c;
   sh_ctx(c, g, o, state, d);
   Scratch* s = c.s;
@@ -3935,7 +3947,7 @@ __global__ void __launch_bounds__(1024) k_ahp_decide(Geo g, Opt o, int* state, R
   if (!FP64) {
     // the per-CTA top-2 keys of k_ahp_pg (PG over F on the whole grid), reduced here
     unsigned long long k1 = 0, k2 = 0;
-    for (int i = c.tid; i < 2 * d.npart; i += c.B) top2_insert(k1, k2, d.kpart[i]);
+    for (int i = c.tid; i < 2 * d.npart; i += c.B) top2_insert(k1, k2, __ldcg(d.kpart + i));
     block_top2(c, k1, k2);
     const float drel = ahp_delta_rel(nf);
     if (c.tid == 0) {
@@ -3972,6 +3984,12 @@ __global__ void __launch_bounds__(1024) k_ahp_decide(Geo g, Opt o, int* state, R
     if (c.tid == 0) s->c_fp64 += 1;
   }
   sh_commit_advance<0>(c, R, O, r, d);
+}
+template <bool FP64>
+__global__ void __launch_bounds__(1024) k_ahp_decide(Geo g, Opt o, int* state, ReqsDev R, OutDev O, int r,
+                                                     ShardDev d) {
+  if (!sh_live(d, FP64)) return;
+  ahp_decide_cta<FP64>(g, o, state, R, O, r, d);
 }
 
 // CTAs per criterion of the sharded engine's AHP level extraction (1: k_sh_levels, one CTA)
@@ -4042,9 +4060,9 @@ cudaError_t launch_ahp_mid(bool fp64, const Geo& g, const Opt& o, int* state, co
 }
 cudaError_t launch_ahp_decide(bool fp64, const Geo& g, const Opt& o, int* state, const ReqsDev& R, const OutDev& O,
                               int r, const ShardDev& d, cudaStream_t st) {
-  if (!fp64) k_ahp_pg<<<d.npart, 1024, 0, st>>>(g, o, state, d);
-  if (fp64) k_ahp_decide<true><<<1, 1024, 0, st>>>(g, o, state, R, O, r, d);
-  else k_ahp_decide<false><<<1, 1024, 0, st>>>(g, o, state, R, O, r, d);
+  // FP32: PG over the grid, the last CTA decides (and commits); FP64: one CTA
+  if (!fp64) k_ahp_pg<<<d.npart, 1024, 0, st>>>(g, o, state, R, O, r, d);
+  else k_ahp_decide<true><<<1, 1024, 0, st>>>(g, o, state, R, O, r, d);
   return cudaGetLastError();
 }
 // After a request's last pod step (the host saw PH_DONE): the presorted orders re-merged on
