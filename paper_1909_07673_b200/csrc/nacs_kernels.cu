@@ -1713,7 +1713,9 @@ __device__ void pod_prologue(Ctx& c, const ReqsDev& R, int r, int p) {
     s->dc = s->pod_cpu[p];
     s->dr = s->pod_ram[p];
   }
+  SEQC_T(23);
   if (c.warp == 0) build_flows_warp(c, R, r, p);
+  SEQC_T(22);
   clear_bitmaps(c);
   __syncthreads();
   SEQC_T(18);
@@ -2361,7 +2363,8 @@ __global__ void __launch_bounds__(SQC_T, 1) k_seq_cluster(Geo g, Opt o, int* sta
   if (lead) flush_stats(c, stats);
 #ifdef NACS_SEQC_PROF
   if (lead && c.tid == 0) {
-    printf("filter: pre %llu loads %llu\n", seqc_prof_[21], seqc_prof_[20]);
+    printf("filter: pre %llu loads %llu | prologue: head %llu flows %llu\n", seqc_prof_[21], seqc_prof_[20],
+           seqc_prof_[23], seqc_prof_[22]);
     printf("commit ns: server %llu widest %llu path %llu vpath %llu | prologue: flows+clear %llu fabric %llu fok %llu\n",
            seqc_prof_[15], seqc_prof_[16], seqc_prof_[17], seqc_prof_[8], seqc_prof_[18], seqc_prof_[19], seqc_prof_[2]);
     printf("seqc ns: copy %llu begin %llu prologue %llu filter[loop %llu reduce %llu] barriers %llu "
