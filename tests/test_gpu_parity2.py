@@ -348,3 +348,30 @@ def test_ahp_levels_cluster_equals_one_cta(k, nreq):
         for key in st:
             assert np.array_equal(st[key], res[0][1][key]), key
         assert stats["ahp_pairs"] == res[0][2]["ahp_pairs"] and stats["pod_steps"] == res[0][2]["pod_steps"]
+
+
+@pytest.mark.parametrize("rule", [0, 1])
+def test_ahp_mid_cluster_equals_split_kernels(rule):
+    """The between-passes scans as one cluster launch (k_ahp_mid_cl, NACS_MID_CLUSTER = 16)
+    and as the two 128-warp kernels (= 1) sum the FP64 prefixes in different orders; the
+    decisions are the same (an FP32 decision inside the error bound is the exact one, and a
+    near tie is re-decided by the unchanged FP64 passes): same placements and final state."""
+    import os
+    from paper_1909_07673_b200 import nacs
+    snap = gen.snapshot(32, seed=5150 + rule, quantised=rule == 1)
+    reqs = gen.requests(6, 808 + rule)
+    res = []
+    for cl in ("1", "16"):
+        os.environ["NACS_MID_CLUSTER"] = cl
+        c = nacs.Context(0)
+        try:
+            c.load_topology(snap)
+            out = to_np(c.schedule_request(reqs, "ahp", "clustering", ahp_rule=rule))
+            res.append((out, c.read_topology()))
+        finally:
+            c.close()
+            os.environ.pop("NACS_MID_CLUSTER", None)
+    for key in res[0][0]:
+        assert np.array_equal(res[0][0][key], res[1][0][key]), key
+    for key in res[0][1]:
+        assert np.array_equal(res[0][1][key], res[1][1][key]), key
