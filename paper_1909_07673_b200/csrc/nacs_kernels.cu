@@ -2271,21 +2271,29 @@ __global__ void __launch_bounds__(SQC_T, 1) k_seq_cluster(Geo g, Opt o, int* sta
           // the thread's top-2 in FP32 (rows re-read from the CTA's copy: no registers held
           // across the barrier): servers ascend with j, so a strict > keeps the lowest index
           // first and an equal score lands in s2 (a tie, decided in FP64 below)
-          float s1 = -1.0f, s2 = -1.0f;
-          int j1 = 0;
+          // argmax of the closeness = argmin of q = Ed+^2 / Ed-^2 (topsis_q32: one reciprocal
+          // instead of two square roots and a division; the warp kernel's decision rule)
+          const float INF = __int_as_float(0x7f800000);
+          float q1 = INF, q2 = INF;
+          int j1 = -1;
 #pragma unroll
           for (int j = 0; j < SQ_J; ++j) {
             if (!((okb >> j) & 1u)) continue;
             const int* m = mir + j * SQC_T + c.tid;
-            const float rr = topsis32(tp, m[0], m[SQC_M], m[2 * SQC_M], m[3 * SQC_M]);
-            if (rr > s1) { s2 = s1; s1 = rr; j1 = j; }
-            else if (rr > s2) s2 = rr;
+            const float qv = topsis_q32(tp, m[0], m[SQC_M], m[2 * SQC_M], m[3 * SQC_M]);
+            if (j1 < 0 || qv < q1) { q2 = j1 < 0 ? q2 : q1; q1 = qv; j1 = j; }
+            else if (qv < q2) q2 = qv;
           }
-          // as keys: (score, ~index) for the best; the second's index never matters, only
-          // that it ranks below any best of the same score and is nonzero (0 = none)
-          const int u1 = (blockIdx.x * c.NW + c.warp) * 32 + j1 * gridDim.x * c.B + c.lane;
-          const unsigned long long k1 = s1 >= 0.f ? score_key(s1, u1) : 0ull;
-          const unsigned long long k2 = s2 >= 0.f ? ((unsigned long long)__float_as_uint(s2) << 32) | 1ull : 0ull;
+          // as keys for a max-merge: (0x7F800001 - bits(q), ~index) for the best (smaller q,
+          // then the lower index, ranks higher; q = +inf still > 0); the second's index never
+          // matters, only that it ranks below any best of the same q and is nonzero (0 = none)
+          const int u1 = (blockIdx.x * c.NW + c.warp) * 32 + max(j1, 0) * gridDim.x * c.B + c.lane;
+          const bool has2 = __popc(okb) >= 2;
+          const unsigned long long k1 =
+              j1 >= 0 ? ((unsigned long long)(0x7F800001u - __float_as_uint(q1)) << 32) | (0xFFFFFFFFu - (unsigned)u1)
+                      : 0ull;
+          const unsigned long long k2 =
+              has2 ? ((unsigned long long)(0x7F800001u - __float_as_uint(q2)) << 32) | 1ull : 0ull;
           SEQC_T(14);
           block_top2(c, k1, k2);
           if (c.tid == 0) { kx[2 * q] = s.key1; kx[2 * q + 1] = s.key2; }
@@ -2296,11 +2304,12 @@ __global__ void __launch_bounds__(SQC_T, 1) k_seq_cluster(Geo g, Opt o, int* sta
         if (c.warp == 0) {  // a7: argmax, lowest index on ties (R14); FP64 near-tie re-decision
           unsigned long long k1 = c.lane < C ? kx[2 * c.lane] : 0ull, k2 = c.lane < C ? kx[2 * c.lane + 1] : 0ull;
           warp_top2(k1, k2);  // order-free merge: every lane holds the cluster's top-2
-          if (c.lane == 0) {
-            const float s1 = __uint_as_float((unsigned)(k1 >> 32)), s2 = __uint_as_float((unsigned)(k2 >> 32));
+          if (c.lane == 0) {  // R14: near tie (relative q window, as the warp kernel) -> FP64
+            const unsigned m1 = 0x7F800001u - (unsigned)(k1 >> 32), m2 = 0x7F800001u - (unsigned)(k2 >> 32);
+            const float q1 = __uint_as_float(m1), q2 = __uint_as_float(m2);
             s.best = (int)(0xFFFFFFFFu - (unsigned)(k1 & 0xFFFFFFFFull));
-            s.amb = o.exact64 || (k2 != 0ull && s1 - s2 <= kTopsisDelta);
-            s.thr = o.exact64 ? -1.0f : s1 - 2.0f * kTopsisDelta;
+            s.amb = o.exact64 || (k2 != 0ull && (m2 == m1 || q2 - q1 <= kTopsisDeltaQ * q1));
+            s.thr = o.exact64 ? __int_as_float(0x7f800000) : q1 * (1.0f + 2.0f * kTopsisDeltaQ);
           }
         }
         __syncthreads();
@@ -2313,7 +2322,7 @@ __global__ void __launch_bounds__(SQC_T, 1) k_seq_cluster(Geo g, Opt o, int* sta
             const int u = (blockIdx.x * c.NW + c.warp) * 32 + j * gridDim.x * c.B + c.lane;
             const int* m = mir + j * SQC_T + c.tid;
             const int x0 = m[0], x1 = m[SQC_M], x2 = m[2 * SQC_M], x3 = m[3 * SQC_M];
-            if (topsis32(tp, x0, x1, x2, x3) < s.thr) continue;
+            if (topsis_q32(tp, x0, x1, x2, x3) > s.thr) continue;
             const double rr = topsis64(tp, x0, x1, x2, x3);
             if (rr > bv || (rr == bv && u < bj)) { bv = rr; bj = u; }
           }
