@@ -2050,7 +2050,7 @@ __device__ __forceinline__ void seqc_filter(Ctx& c, const int* mir, unsigned lon
   const int dc = s->dc, dr = s->dr, sumD = s->sumD;
   const bool net = c.o.path_filter && s->nflow > 0;
   const bool G = s->G != 0;
-  const int start = (blockIdx.x * c.NW + c.warp) * 32, stride = gridDim.x * c.B;
+  const int start = (blockIdx.x * (SQC_T >> 5) + c.warp) * 32, stride = gridDim.x * SQC_T;
   int x[SQ_J][4];
 #pragma unroll
   for (int j = 0; j < SQ_J; ++j) {
@@ -2117,6 +2117,8 @@ __global__ void __launch_bounds__(SQC_T, 1) k_seq_cluster(Geo g, Opt o, int* sta
   const bool lead = q == 0;
   Ctx c;
   init_ctx(c, g, o, &s);
+  c.B = SQC_T;  // compile-time block shape: the compiler folds it instead of re-deriving it
+  c.NW = SQC_T >> 5;
   size_t off = 0;
   c.maskw = reinterpret_cast<unsigned*>(dyn + off);
   off = align16(off + sizeof(unsigned) * c.nW);
@@ -2287,7 +2289,7 @@ __global__ void __launch_bounds__(SQC_T, 1) k_seq_cluster(Geo g, Opt o, int* sta
           // as keys for a max-merge: (0x7F800001 - bits(q), ~index) for the best (smaller q,
           // then the lower index, ranks higher; q = +inf still > 0); the second's index never
           // matters, only that it ranks below any best of the same q and is nonzero (0 = none)
-          const int u1 = (blockIdx.x * c.NW + c.warp) * 32 + max(j1, 0) * gridDim.x * c.B + c.lane;
+          const int u1 = blockIdx.x * SQC_T + c.tid + max(j1, 0) * gridDim.x * SQC_T;
           const bool has2 = __popc(okb) >= 2;
           const unsigned long long k1 =
               j1 >= 0 ? ((unsigned long long)(0x7F800001u - __float_as_uint(q1)) << 32) | (0xFFFFFFFFu - (unsigned)u1)
@@ -2319,7 +2321,7 @@ __global__ void __launch_bounds__(SQC_T, 1) k_seq_cluster(Geo g, Opt o, int* sta
 #pragma unroll
           for (int j = 0; j < SQ_J; ++j) {
             if (!((okb >> j) & 1u)) continue;
-            const int u = (blockIdx.x * c.NW + c.warp) * 32 + j * gridDim.x * c.B + c.lane;
+            const int u = blockIdx.x * SQC_T + c.tid + j * gridDim.x * SQC_T;
             const int* m = mir + j * SQC_T + c.tid;
             const int x0 = m[0], x1 = m[SQC_M], x2 = m[2 * SQC_M], x3 = m[3 * SQC_M];
             if (topsis_q32(tp, x0, x1, x2, x3) > s.thr) continue;
