@@ -36,9 +36,10 @@ from inputs import gen  # noqa: E402
 # Algorithmic operation counts.
 TOPSIS_OPS_ALL = 3       # per server ranked: the CPU/RAM/access-bandwidth compares of the filter
 TOPSIS_OPS_FEAS = 45     # per feasible server: stats (14) + closeness (30) + argmax (1)
-# kernels launched per nacs_schedule_batch call: TOPSIS = k_pod_max + k_warp_layout + k_order_lpt +
-# k_batch_warp + k_batch (deferred requests; exits at once when none); AHP = k_batch
-LAUNCHES = {"topsis": 5, "ahp": 1}
+# kernels launched per nacs_schedule_batch call: TOPSIS = k_pod_max + k_layout_order (the chunk
+# layout and the largest-first order, one CTA each) + k_batch_warp + k_batch (deferred requests;
+# exits at once when none); AHP = k_batch
+LAUNCHES = {"topsis": 4, "ahp": 1}
 # DRAM bytes per launch of k_batch_warp from the committed `ncu --set full` capture
 TRAFFIC = os.path.join(ROOT, "profiles", "ncu_traffic.json")
 AHP_RCP_PER_PAIR = 1     # per unordered pair per non-constant criterion per pass: one reciprocal

@@ -1405,7 +1405,7 @@ __global__ void __launch_bounds__(NACS_WARP_THREADS, 1) k_batch_warp(Geo g, Opt 
 // count, so that the last requests handed out are the shortest and the warps of a CTA
 // run out of work together.  One CTA; the order within a size class is arbitrary (the
 // requests are independent, R21, so results do not depend on it).
-__global__ void __launch_bounds__(1024) k_order_lpt(ReqsDev R, int* order) {
+__device__ void order_lpt(const ReqsDev& R, int* order) {
   __shared__ int hist[MAXC + 2];
   __shared__ int base[MAXC + 2];
   for (int i = threadIdx.x; i < MAXC + 2; i += blockDim.x) hist[i] = 0;
@@ -1479,7 +1479,7 @@ __device__ __forceinline__ unsigned quant10(int v, int vmax) {
 }
 
 // One CTA: sort the servers by layout key, write the criteria tiles, inv and the chunk table.
-__global__ void __launch_bounds__(1024) k_warp_layout(Geo g, const int* __restrict__ state, int* lay) {
+__device__ void warp_layout(const Geo& g, const int* __restrict__ state, int* lay) {
   extern __shared__ unsigned long long key[];
   __shared__ int smax[3];
   const int n = g.n, npad = (n + 127) & ~127, nch = npad >> 7;
@@ -1623,6 +1623,14 @@ int warp_kernel_warps(const Geo& g) {
 
 size_t warp_ulog_entries(int grid, int warps) { return (size_t)grid * warps * WLOG; }
 
+// The chunk layout (CTA 0) and the largest-first request order (CTA 1) are independent:
+// one launch of two CTAs runs them side by side (they were two one-CTA launches in a row).
+__global__ void __launch_bounds__(1024) k_layout_order(Geo g, const int* __restrict__ state, int* lay, ReqsDev R,
+                                                       int* order) {
+  if (blockIdx.x == 0) warp_layout(g, state, lay);
+  else order_lpt(R, order);
+}
+
 cudaError_t launch_batch_warp(const Geo& g, const Opt& o, const int* d_state, int* lay, const ReqsDev& R,
                               const OutDev& O, int4* ulog, int* next, int* order, int* deferred, int* n_deferred,
                               unsigned long long* stats, int grid, int warps, cudaStream_t st) {
@@ -1635,10 +1643,9 @@ cudaError_t launch_batch_warp(const Geo& g, const Opt& o, const int* d_state, in
     int P2 = 1;
     while (P2 < npad) P2 <<= 1;
     const size_t lsm = sizeof(unsigned long long) * (size_t)P2;
-    cudaFuncSetAttribute(k_warp_layout, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsm);
-    k_warp_layout<<<1, 1024, lsm, st>>>(g, d_state, lay);
+    cudaFuncSetAttribute(k_layout_order, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsm);
+    k_layout_order<<<2, 1024, lsm, st>>>(g, d_state, lay, R, order);
   }
-  k_order_lpt<<<1, 1024, 0, st>>>(R, order);
   // lockstep group size and the optional barriers before phases B / C (A/B on one box, C4,
   // NACS_WARP_GROUP / NACS_WARP_SYNC override): per-pod, the whole CTA in lockstep with a
   // barrier before the commit only, 12.74 ms (groups of 8 with both barriers 13.43 ms, 16 with
